@@ -1,0 +1,406 @@
+"""CPU oracle for the AMS-sort hot path — TEST INFRASTRUCTURE ONLY.
+
+This module restates the reference algorithm (`mlpsort.ams.ams_sort` with
+``scheme="simple"``) with numpy arrays so the GPU path can be checked at
+sizes the pure-Python reference cannot reach.  It is the *checker*: only
+``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
+``--impl reference`` legs may import it.  The product path
+(`paper_1410_6754_b200`) never imports, links or executes anything here.
+
+Parity pin: every function cites the reference file:line it restates, and
+``tests/test_oracle.py`` checks this oracle against golden fixtures produced
+by running the real reference (``oracle/make_goldens.py`` →
+``tests/golden/*.json``).  Parity is therefore pinned against the reference
+itself, not only against this restatement.
+
+Element identity: the reference orders ``Element(key, origin_pe,
+origin_pos)`` lexicographically (core.py:19-43).  Inside one PE group the
+reference's concatenation keeps equal keys in origin order, so
+``(key, position-in-group-buffer)`` is the same strict total order; the
+oracle carries positions implicitly as array indices.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import math
+import random
+from dataclasses import dataclass, field
+
+import numpy as np
+
+U64 = np.uint64
+
+
+# --------------------------------------------------------------------------
+# Seeded streams  (core.py:46-71)
+
+def stream_seed_int(master_seed: int, stream_id: str) -> int:
+    """``int.from_bytes(SeedSpec(master, stream)._digest(), "big")``
+    (core.py:62-67): blake2b-128 of ``f"{master}\\x1f{stream}\\x1f"``."""
+    text = f"{master_seed}\x1f{stream_id}\x1f"
+    return int.from_bytes(
+        hashlib.blake2b(text.encode(), digest_size=16).digest(), "big")
+
+
+def sample_indices(master_seed: int, stream_id: str, n: int, take: int) -> list[int]:
+    """``sorted(Random(seed).sample(range(n), take))`` (ams.py:171-173)."""
+    rng = random.Random(stream_seed_int(master_seed, stream_id))
+    return sorted(rng.sample(range(n), take))
+
+
+# --------------------------------------------------------------------------
+# Consecutive-bucket grouping  (ams.py:78-154)
+
+@dataclass(frozen=True)
+class Plan:
+    boundaries: tuple
+    loads: tuple
+    max_load: int
+
+
+def _scan(sizes, r, limit):
+    """Greedy packing under ``limit`` (ams.py:78-109)."""
+    overflow = None
+    boundaries = [0]
+    loads = []
+    cur = 0
+    for i, size in enumerate(sizes):
+        if size > limit:
+            return None, overflow
+        if cur + size > limit:
+            if overflow is None or cur + size < overflow:
+                overflow = cur + size
+            boundaries.append(i)
+            loads.append(cur)
+            cur = size
+        else:
+            cur += size
+    boundaries.append(len(sizes))
+    loads.append(cur)
+    if len(loads) > r:
+        return None, overflow
+    while len(loads) < r:
+        boundaries.append(len(sizes))
+        loads.append(0)
+    return Plan(tuple(boundaries), tuple(loads), max(loads)), overflow
+
+
+def group_plan(sizes, r: int) -> Plan:
+    """Binary search over the scan with overflow tightening
+    (ams.py:119-154)."""
+    sizes = [int(s) for s in sizes]
+    total = sum(sizes)
+    lo = max(max(sizes), -(-total // r))
+    b_est = max(1, len(sizes) // r)
+    hi = max(lo, math.ceil(total / r * (1.0 + 4.0 / b_est)))
+    plan, overflow = _scan(sizes, r, hi)
+    if plan is None:
+        lo = max(lo, overflow if overflow is not None else hi + 1)
+        hi = total
+        plan, _ = _scan(sizes, r, hi)
+    hi = plan.max_load
+    best = plan
+    while lo < hi:
+        mid = (lo + hi) // 2
+        plan, overflow = _scan(sizes, r, mid)
+        if plan is not None:
+            hi = plan.max_load
+            best = plan
+        else:
+            lo = overflow if overflow is not None else mid + 1
+    return best
+
+
+# --------------------------------------------------------------------------
+# One level of one group  (ams.py:214-268 + delivery.py:151-180)
+
+@dataclass
+class LevelInfo:
+    """What the oracle records about one group at one level (for parity)."""
+
+    level: int                 # 0-based lv as in ams.py:285
+    group_lo: int              # first PE of the group
+    n_g: int
+    bucket_count: int
+    sample_size: int
+    splitter_keys: np.ndarray  # (br-1,) uint64
+    splitter_pos: np.ndarray   # (br-1,) int64, position in group buffer
+    hist: np.ndarray           # (P, br) per-member bucket histogram
+    plan: Plan
+    new_sizes: list            # sizes of the next-level member arrays
+    stats: dict = field(default_factory=dict)
+
+
+def classify(keys: np.ndarray, pos: np.ndarray, s_keys: np.ndarray,
+             s_pos: np.ndarray) -> np.ndarray:
+    """Bucket = number of splitters strictly below ``(key, pos)``
+    (ams.py:201-211, bisect_left at 210)."""
+    if len(s_keys) == 0:
+        return np.zeros(len(keys), dtype=np.int64)
+    b = np.searchsorted(s_keys, keys, side="left").astype(np.int64)
+    hi = np.searchsorted(s_keys, keys, side="right")
+    tie = np.nonzero(hi > b)[0]
+    if len(tie):
+        # Equal-key splitter runs: add the run members with a smaller
+        # position (splitters are sorted by (key, pos)).
+        for k in np.unique(keys[tie]):
+            sel = tie[keys[tie] == k]
+            lo_i = np.searchsorted(s_keys, k, side="left")
+            hi_i = np.searchsorted(s_keys, k, side="right")
+            b[sel] += np.searchsorted(s_pos[lo_i:hi_i], pos[sel], side="left")
+    return b
+
+
+def select_splitters(sample_keys, sample_pos, br):
+    """Splitters = sorted sample at ranks ``(i*S)//br`` (ams.py:178-198;
+    fastsort.py:57-130 ranks the same set)."""
+    S = len(sample_keys)
+    if br <= 1:
+        return np.zeros(0, dtype=U64), np.zeros(0, dtype=np.int64)
+    order = np.lexsort((sample_pos, sample_keys))
+    ranks = sorted({(i * S) // br for i in range(1, br)})
+    idx = order[np.asarray(ranks, dtype=np.int64)]
+    return sample_keys[idx], sample_pos[idx]
+
+
+def _exchange_stats(piece_sizes: np.ndarray, sub_sizes: int, members: list):
+    """Data-exchange shape of ``deliver_simple`` (delivery.py:151-180,
+    _slice_range 83-106) as ``Network.exchange`` counts it
+    (simnet.py:294-335): self messages and empty payloads are free."""
+    P, r = piece_sizes.shape
+    sub = P // r
+    sw = np.zeros(P, np.int64); rw = np.zeros(P, np.int64)
+    sm = np.zeros(P, np.int64); rm = np.zeros(P, np.int64)
+    for g in range(r):
+        col = piece_sizes[:, g]
+        m = int(col.sum())
+        starts = np.concatenate([[0], np.cumsum(col)[:-1]])
+        for j in range(P):
+            size = int(col[j]); start = int(starts[j])
+            if size == 0 or m == 0:
+                continue
+            for t in range(sub):
+                lo = (m * t) // sub; hi = (m * (t + 1)) // sub
+                take = min(start + size, hi) - max(start, lo)
+                if take <= 0:
+                    continue
+                dest = g * sub + t
+                if dest != j:
+                    sw[j] += take; rw[dest] += take; sm[j] += 1; rm[dest] += 1
+    hs, hr = int(sw.max(initial=0)), int(rw.max(initial=0))
+    ms, mr = int(sm.max(initial=0)), int(rm.max(initial=0))
+    return {"max_words": max(hs, hr), "max_msgs": max(ms, mr),
+            "max_sent_msgs": ms, "max_recv_msgs": mr}
+
+
+def ams_level(buf: np.ndarray, sizes: list, r: int, b: int, a: float,
+              master_seed: int, stream: str, level: int, group_lo: int,
+              vals: np.ndarray | None = None, with_stats: bool = False):
+    """One level on one group whose member arrays are consecutive in
+    ``buf`` (ams.py:214-268).  Returns the new group buffer (the stable
+    ``(g, j, b)`` order of SURVEY §8 layout contract), new member sizes and
+    a LevelInfo."""
+    P = len(sizes)
+    n_g = int(sum(sizes))
+    offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    br = min(b * r, n_g + 1)                                   # ams.py:224
+    target = min(n_g, max(br - 1, math.ceil(a * br)))          # ams.py:225
+    base, extra = divmod(target, P)                            # ams.py:166
+    s_idx = []
+    for i in range(P):                                         # ams.py:168-174
+        quota = base + (1 if i < extra else 0)
+        take = min(quota, sizes[i])
+        pe = group_lo + i
+        sid = f"{stream}/L{level}-g{group_lo}/sample/pe{pe}"
+        idx = sample_indices(master_seed, sid, sizes[i], take)
+        s_idx.extend(int(offs[i]) + t for t in idx)
+    s_pos = np.asarray(s_idx, dtype=np.int64)
+    drawn = len(s_pos)
+    br = min(br, drawn + 1)                                    # ams.py:228
+    sk, sp = select_splitters(buf[s_pos], s_pos, br)
+    pos = np.arange(n_g, dtype=np.int64)
+    bucket = classify(buf, pos, sk, sp)
+    member = np.repeat(np.arange(P, dtype=np.int64), sizes)
+    hist = np.zeros((P, br), dtype=np.int64)
+    np.add.at(hist, (member, bucket), 1)
+    plan = group_plan(hist.sum(axis=0), r)                     # ams.py:236-238
+    bnd = np.asarray(plan.boundaries, dtype=np.int64)
+    gid = np.searchsorted(bnd, bucket, side="right") - 1
+    # Empty trailing groups share boundary == br; buckets never reach br.
+    comp = (gid * P + member) * br + bucket
+    order = np.argsort(comp, kind="stable")                    # F10 layout
+    out = buf[order]
+    out_vals = vals[order] if vals is not None else None
+    sub = P // r
+    new_sizes = []
+    for g in range(r):                                         # delivery.py:78-80
+        m = int(plan.loads[g])
+        for t in range(sub):
+            new_sizes.append((m * (t + 1)) // sub - (m * t) // sub)
+    info = LevelInfo(level, group_lo, n_g, br, drawn, sk, sp, hist, plan,
+                     new_sizes)
+    if with_stats:
+        pieces = np.zeros((P, r), np.int64)
+        for g in range(r):
+            pieces[:, g] = hist[:, bnd[g]:bnd[g + 1]].sum(axis=1)
+        info.stats = _exchange_stats(pieces, sub, list(range(P)))
+    return out, out_vals, new_sizes, info
+
+
+@dataclass
+class SortResult:
+    keys: np.ndarray
+    vals: np.ndarray | None
+    pe_sizes: list
+    levels: list          # list[list[LevelInfo]] per level, per group
+    reports: list         # reference-shaped level reports (ams.py:296-308)
+
+
+def default_oversampling(n: int) -> float:
+    """ams.py:278-280."""
+    return 1.6 * math.log10(max(n, 10))
+
+
+def ams_sort(keys: np.ndarray, pe_sizes: list, group_counts: tuple,
+             oversampling: float | None = None, overpartition: int = 16,
+             imbalance: float = 0.2, master_seed: int = 0,
+             stream: str = "root", vals: np.ndarray | None = None,
+             with_stats: bool = True) -> SortResult:
+    """Restatement of ``ams_sort`` with ``scheme="simple"`` (ams.py:271-313).
+    ``keys`` is the PE-major concatenation of the per-PE inputs (uint64)."""
+    keys = np.ascontiguousarray(keys, dtype=U64)
+    p = len(pe_sizes)
+    if math.prod(group_counts) != p:                           # ams.py:61-65
+        raise ValueError(f"group counts {group_counts} do not telescope {p} PEs")
+    n = int(sum(pe_sizes))
+    a = oversampling if oversampling is not None else default_oversampling(n)
+    k = len(group_counts)
+    eps_l = (1.0 + imbalance) ** (1.0 / k) - 1.0               # ams.py:58-59
+    buf = keys.copy()
+    vbuf = None if vals is None else np.asarray(vals).copy()
+    sizes = [int(s) for s in pe_sizes]
+    groups = [(0, p)]                                          # (lo, count)
+    all_levels = []
+    reports = []
+    for lv, r in enumerate(group_counts):
+        offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+        new_buf = np.empty_like(buf)
+        new_vbuf = None if vbuf is None else np.empty_like(vbuf)
+        new_sizes = list(sizes)
+        infos = []
+        next_groups = []
+        for lo, cnt in groups:
+            gs, ge = int(offs[lo]), int(offs[lo + cnt])
+            out, out_v, ns, info = ams_level(
+                buf[gs:ge], sizes[lo:lo + cnt], r, overpartition, a,
+                master_seed, stream, lv, lo,
+                None if vbuf is None else vbuf[gs:ge], with_stats)
+            new_buf[gs:ge] = out
+            if new_vbuf is not None:
+                new_vbuf[gs:ge] = out_v
+            new_sizes[lo:lo + cnt] = ns
+            budget = math.ceil((1.0 + eps_l) * info.n_g / r)   # ams.py:258
+            info.stats["over_budget"] = info.plan.max_load > budget
+            infos.append(info)
+            step = cnt // r
+            next_groups.extend((lo + i * step, step) for i in range(r))
+        buf, vbuf, sizes, groups = new_buf, new_vbuf, new_sizes, next_groups
+        all_levels.append(infos)
+        rep = {"level": lv + 1, "r": r, "max_load": max(sizes),
+               "min_load": min(sizes),
+               "sample_size": max(i.sample_size for i in infos),
+               "plan_load": max(i.plan.max_load for i in infos),
+               "over_budget": sum(bool(i.stats.get("over_budget")) for i in infos)}
+        if with_stats:
+            for key in ("max_words", "max_msgs", "max_sent_msgs", "max_recv_msgs"):
+                rep[key] = max(i.stats[key] for i in infos)
+        reports.append(rep)
+    # Final local sort, stable by key (ams.py:310-312; F6).
+    offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    for pe in range(p):
+        s, e = int(offs[pe]), int(offs[pe + 1])
+        order = np.argsort(buf[s:e], kind="stable")
+        buf[s:e] = buf[s:e][order]
+        if vbuf is not None:
+            vbuf[s:e] = vbuf[s:e][order]
+    return SortResult(buf, vbuf, sizes, all_levels, reports)
+
+
+# --------------------------------------------------------------------------
+# Inputs  (bench.py:153-177 for the reference generators)
+
+def reference_uniform_input(p: int, n_per_pe: int, seed: int, rep: int = 0) -> np.ndarray:
+    """The reference's ``generate_input(dist="uniform")`` keys
+    (bench.py:159-164): PE stream ``input/rep{rep}/pe{pe}``,
+    ``getrandbits(64)`` per key."""
+    out = np.empty(p * n_per_pe, dtype=U64)
+    for pe in range(p):
+        rng = random.Random(stream_seed_int(seed, f"input/rep{rep}/pe{pe}"))
+        # getrandbits(64 * n) packs n draws little-endian, identical to n
+        # successive getrandbits(64) calls.
+        big = rng.getrandbits(64 * n_per_pe) if n_per_pe else 0
+        out[pe * n_per_pe:(pe + 1) * n_per_pe] = np.frombuffer(
+            big.to_bytes(8 * n_per_pe, "little"), dtype="<u8")
+    return out
+
+
+_ZIPF_UNIVERSE = 100_000                                       # bench.py:137
+_zipf_cache: dict = {}
+
+
+def _zipf_cdf(theta: float) -> list:
+    """bench.py:141-150 (same float accumulation order)."""
+    cdf = _zipf_cache.get(theta)
+    if cdf is None:
+        acc = 0.0
+        cdf = []
+        for k in range(1, _ZIPF_UNIVERSE + 1):
+            acc += k ** -theta
+            cdf.append(acc)
+        _zipf_cache[theta] = cdf
+    return cdf
+
+
+def reference_input(dist: str, p: int, n_per_pe: int, seed: int, rep: int = 0) -> np.ndarray:
+    """All of ``generate_input``'s distributions (bench.py:153-177) as one
+    PE-major uint64 array (origin tag of index i = (i // n_per_pe,
+    i % n_per_pe))."""
+    from bisect import bisect_left
+    n = p * n_per_pe
+    if dist == "uniform":
+        return reference_uniform_input(p, n_per_pe, seed, rep)
+    if dist == "sorted":
+        return np.arange(n, dtype=U64)
+    if dist == "reverse":
+        return (n - 1 - np.arange(n, dtype=np.int64)).astype(U64)
+    if dist == "equal":
+        return np.full(n, 42, dtype=U64)
+    if dist.startswith("zipf:"):
+        theta = float(dist.split(":", 1)[1])
+        cdf = _zipf_cdf(theta)
+        total = cdf[-1]
+        out = np.empty(n, dtype=U64)
+        for pe in range(p):
+            rng = random.Random(stream_seed_int(seed, f"input/rep{rep}/pe{pe}"))
+            out[pe * n_per_pe:(pe + 1) * n_per_pe] = [
+                bisect_left(cdf, rng.random() * total) for _ in range(n_per_pe)]
+        return out
+    raise ValueError(f"unknown input distribution {dist!r}")
+
+
+def zipf_keys(n: int, seed: int, s: float = 1.1, universe: int = 1024) -> np.ndarray:
+    """Config 4(a): Zipf(s) ranks 1..universe by inverse CDF."""
+    rng = np.random.default_rng(seed)
+    w = np.arange(1, universe + 1, dtype=np.float64) ** -s
+    cdf = np.cumsum(w)
+    cdf /= cdf[-1]
+    u = rng.random(n)
+    return (np.searchsorted(cdf, u, side="left") + 1).astype(U64)
+
+
+def f64_to_ordered_u64(x: np.ndarray) -> np.ndarray:
+    """Order-preserving float64 → uint64 map (sign-flip transform)."""
+    b = np.ascontiguousarray(x, dtype=np.float64).view(U64)
+    neg = (b >> U64(63)).astype(bool)
+    return np.where(neg, ~b, b | U64(1 << 63))
