@@ -1,0 +1,166 @@
+/*
+ * ams_b200.h — C ABI of the B200-native AMS-sort hot path.
+ *
+ * The reference (`mlpsort`, pure Python) exposes this path only as the
+ * Python function
+ *     ams_sort(net, data, params, scheme, seed) -> (dict[pe] -> list, reports)
+ * (/root/reference/pkg/src/mlpsort/ams.py:271-313).  There is no native
+ * FFI in the reference; this header is the boundary a binding would load
+ * (ctypes stub in INTEGRATION.md, used by paper_1410_6754_b200/_lib.py).
+ * Plain C types only: device buffers are `void*` / `uint64_t*` device
+ * pointers, small per-level metadata are host arrays.
+ *
+ * Every function returns AMS_OK (0) or an error code; ams_last_error()
+ * returns the thread-local message.  Error classes follow the reference:
+ * AMS_EINVAL maps to Python ValueError (ams.py:45-52, 61-65, 164-165,
+ * 186-187, 206-207), AMS_ECUDA / AMS_EINTERNAL to RuntimeError
+ * (fastsort.py:128-129, delivery.py:104-105, simnet.py:190-191).
+ * Nothing here prints or exits.
+ */
+#ifndef AMS_B200_H
+#define AMS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AMS_OK 0
+#define AMS_EINVAL 1
+#define AMS_ECUDA 2
+#define AMS_ENOMEM 3
+#define AMS_EINTERNAL 4
+
+/* Key encodings: kernels compare keys as uint64 after an order-preserving
+ * map (uint64: identity, int64: sign flip, float64: sign-flip transform).
+ * The reference's keys are Python ints from getrandbits(64)
+ * (bench.py:159-164) — AMS_KEY_U64. */
+#define AMS_KEY_U64 0
+#define AMS_KEY_I64 1
+#define AMS_KEY_F64 2
+
+/* Kernel tile (elements per CTA tile in the level kernels) and the
+ * largest bucket the CTA-local final sort handles in shared memory. */
+#define AMS_TILE 4096
+#define AMS_SMEM_SORT_CAP 8192
+#define AMS_MAX_BUCKETS 4096
+
+const char* ams_last_error(void);
+int ams_version(void);
+
+/* ------------------------------------------------------------------ */
+/* Host helpers (no GPU needed).                                       */
+
+/* SeedSpec(master_seed, stream_id).rng() seeding (core.py:62-67): the
+ * 32-bit words CPython's random_seed() feeds init_by_array, least
+ * significant first; *out_nwords = number of words used (1..4). */
+int ams_stream_seed(int64_t master_seed, const char* stream_id, uint32_t out_words[4],
+                    int* out_nwords);
+/* hashlib.blake2b(msg, digest_size=16).digest() (core.py:64). */
+int ams_blake2b_128(const uint8_t* msg, uint64_t len, uint8_t out[16]);
+/* sorted(random.Random(seed).sample(range(n), k)) (ams.py:171-173). */
+int ams_sample_indices(const uint32_t* seed_words, int nwords, uint64_t n, uint64_t k,
+                       uint64_t* out);
+/* `count` successive Random(seed).getrandbits(k), 1 <= k <= 64. */
+int ams_mt_getrandbits(const uint32_t* seed_words, int nwords, int k, uint64_t count,
+                       uint64_t* out);
+/* draw_sample (ams.py:157-175) for all groups of one level; see seeds.cpp. */
+int ams_draw_sample_positions(int64_t master_seed, const char* stream, int level,
+                              int ngroups, const int32_t* group_first, const int32_t* group_npe,
+                              const uint64_t* targets, const uint64_t* sizes,
+                              const uint64_t* offs, uint64_t capacity, uint64_t* out_idx,
+                              uint64_t* out_gpos, uint64_t* out_group_count);
+/* scan_groups (ams.py:112-116): AMS_OK if feasible, 1 if not. */
+int ams_scan_groups(const uint64_t* sizes, int nb, int r, uint64_t limit,
+                    uint64_t* out_boundaries, uint64_t* out_loads, uint64_t* out_max_load);
+/* optimal_group_plan (ams.py:119-154). */
+int ams_group_plan(const uint64_t* sizes, int nb, int r, uint64_t* out_boundaries,
+                   uint64_t* out_loads, uint64_t* out_max_load);
+/* Host half of ams_level for all groups of a level (ams.py:231-258 +
+ * delivery.py:78-180): plans, next-level member sizes, exchange stats. */
+int ams_plan_level(int ngroups, const int32_t* group_npe, const int32_t* group_nb, int r,
+                   const uint32_t* seg_hist, int nb_stride, uint64_t* out_boundaries,
+                   uint64_t* out_loads, uint64_t* out_max_load, uint64_t* out_new_sizes,
+                   uint64_t* out_stats);
+
+/* ------------------------------------------------------------------ */
+/* Device context: one per GPU (one process per GPU).                  */
+
+typedef struct ams_ctx ams_ctx_t;
+
+/* `stream` is a cudaStream_t (NULL = the legacy default stream). */
+int ams_ctx_create(int device, void* stream, ams_ctx_t** out);
+int ams_ctx_destroy(ams_ctx_t* ctx);
+int ams_ctx_set_stream(ams_ctx_t* ctx, void* stream);
+/* Number of this library's kernels launched so far on the context. */
+uint64_t ams_ctx_launches(const ams_ctx_t* ctx);
+int ams_ctx_sync(ams_ctx_t* ctx);
+
+/* K1 — sample gather (draw_sample, ams.py:157-175, data side):
+ *   d_out_keys[i] = ordered(src[h_idx[i]]), d_out_pos[i] = h_gpos[i]. */
+int ams_level_sample(ams_ctx_t* ctx, const void* src, int key_kind, uint64_t count,
+                     const uint64_t* h_idx, const uint64_t* h_gpos, uint64_t* d_out_keys,
+                     uint32_t* d_out_pos);
+
+/* K2 — splitter selection (select_splitters ams.py:178-198 via the
+ * fast work-inefficient rank sort fastsort.py:57-130): per group g the
+ * sample [h_soff[g], h_soff[g+1]) is ranked by counting under
+ * (key, pos); splitter i = element of rank (i*S)//nb.  Builds the
+ * classifier (sorted splitters + key-range LUT) of each group in the
+ * context. */
+int ams_level_splitters(ams_ctx_t* ctx, int ngroups, const uint64_t* d_sample_keys,
+                        const uint32_t* d_sample_pos, const uint64_t* h_soff,
+                        const int32_t* h_nb);
+/* Copy group g's splitters to host (parity checks / reports). */
+int ams_read_splitters(ams_ctx_t* ctx, int group, uint64_t* keys, uint32_t* pos, int* nspl);
+
+/* K3 — classify + per-tile / per-segment histograms (partition_buckets,
+ * ams.py:201-211; histogram allreduce input ams.py:236-237).
+ * Segment s = one PE: [h_seg_off[s], +h_seg_len[s]) of `src`, member of
+ * group h_seg_group[s] (groups are contiguous runs of segments); element
+ * position for tie-breaking = buffer index + h_group_posbase[g].  Blocks
+ * until the per-segment histogram is in h_seg_hist_out ([nseg][nb_stride]).
+ * track_minmax: record global min/max key (for the final sort's ranges). */
+int ams_level_classify(ams_ctx_t* ctx, const void* src, int key_kind, int nseg,
+                       const uint64_t* h_seg_off, const uint64_t* h_seg_len,
+                       const int32_t* h_seg_group, int ngroups, const int64_t* h_group_posbase,
+                       int nb_stride, int track_minmax, uint32_t* h_seg_hist_out);
+
+/* K4+K6 — stable scatter into (group, source segment, bucket) order
+ * (the simple delivery layout: pieces ams.py:240-248, deliver_simple
+ * delivery.py:151-180, exchange order simnet.py:324-325, receive concat
+ * ams.py:252-256).  Uses the segments of the last ams_level_classify.
+ * h_boundaries: [ngroups][r+1] plan boundaries; group g's output begins
+ * at dst + h_group_dst_start[g].  vals may be NULL (keys only). */
+int ams_level_scatter(ams_ctx_t* ctx, const void* src, const void* src_vals, int key_kind,
+                      void* dst, void* dst_vals, int r, const uint64_t* h_boundaries,
+                      const uint64_t* h_group_dst_start);
+
+/* Global min/max key seen by a track_minmax classify (ordered encoding);
+ * the multi-rank driver all-reduces them and writes them back before the
+ * final sort so every rank's key ranges are true bounds. */
+int ams_get_minmax(ams_ctx_t* ctx, uint64_t out[2]);
+int ams_set_minmax(ams_ctx_t* ctx, const uint64_t in[2]);
+
+/* K7-K9 — final local sort (ams.py:310-312), stable by key.  Segment s
+ * of `src` (transformed keys) is final PE s; its key range comes from the
+ * last level's classifier h_seg_cls[s] and its bucket range
+ * [h_seg_b0[s], h_seg_b1[s]) of h_seg_nb[s] buckets.  Large segments are
+ * digit-partitioned into `tmp` and every cell sorted in shared memory
+ * into `out` (keys mapped back to `key_kind`).  `src` is clobbered. */
+int ams_final_sort(ams_ctx_t* ctx, void* src, void* src_vals, void* tmp, void* tmp_vals,
+                   void* out, void* out_vals, int key_kind, int nseg, const uint64_t* h_seg_off,
+                   const uint64_t* h_seg_len, const int32_t* h_seg_cls, const uint64_t* h_seg_b0,
+                   const uint64_t* h_seg_b1, const int32_t* h_seg_nb);
+
+/* Plain copy with key mapping (used for the p == 1 / k == 0 edge and the
+ * host-buffer end-to-end path). */
+int ams_map_keys(ams_ctx_t* ctx, const void* src, void* dst, uint64_t n, int from_kind,
+                 int to_kind);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* AMS_B200_H */

@@ -1,0 +1,277 @@
+"""ctypes binding of ``libams_b200.so`` (the C ABI in include/ams_b200.h).
+
+The library is the only compute path: there is no CPU fallback.  If it is
+missing, importing this module raises — build it with
+``python -m paper_1410_6754_b200.build`` (``__graft_entry__.build()``).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from .build import LIB
+
+AMS_OK, AMS_EINVAL, AMS_ECUDA, AMS_ENOMEM, AMS_EINTERNAL = 0, 1, 2, 3, 4
+KEY_U64, KEY_I64, KEY_F64 = 0, 1, 2
+TILE = 4096
+SMEM_SORT_CAP = 8192
+MAX_BUCKETS = 4096
+
+_P = C.c_void_p
+_I = C.c_int
+_I64 = C.c_int64
+_U64 = C.c_uint64
+
+# name -> (restype, argtypes); every array argument is passed as a pointer.
+_SIGNATURES = {
+    "ams_last_error": (C.c_char_p, []),
+    "ams_version": (_I, []),
+    "ams_stream_seed": (_I, [_I64, C.c_char_p, _P, _P]),
+    "ams_blake2b_128": (_I, [_P, _U64, _P]),
+    "ams_sample_indices": (_I, [_P, _I, _U64, _U64, _P]),
+    "ams_mt_getrandbits": (_I, [_P, _I, _I, _U64, _P]),
+    "ams_draw_sample_positions": (_I, [_I64, C.c_char_p, _I, _I, _P, _P, _P, _P, _P, _U64,
+                                       _P, _P, _P]),
+    "ams_scan_groups": (_I, [_P, _I, _I, _U64, _P, _P, _P]),
+    "ams_group_plan": (_I, [_P, _I, _I, _P, _P, _P]),
+    "ams_plan_level": (_I, [_I, _P, _P, _I, _P, _I, _P, _P, _P, _P, _P]),
+    "ams_ctx_create": (_I, [_I, _P, C.POINTER(_P)]),
+    "ams_ctx_destroy": (_I, [_P]),
+    "ams_ctx_set_stream": (_I, [_P, _P]),
+    "ams_ctx_launches": (_U64, [_P]),
+    "ams_ctx_sync": (_I, [_P]),
+    "ams_level_sample": (_I, [_P, _P, _I, _U64, _P, _P, _P, _P]),
+    "ams_level_splitters": (_I, [_P, _I, _P, _P, _P, _P]),
+    "ams_read_splitters": (_I, [_P, _I, _P, _P, C.POINTER(_I)]),
+    "ams_level_classify": (_I, [_P, _P, _I, _I, _P, _P, _P, _I, _P, _I, _I, _P]),
+    "ams_level_scatter": (_I, [_P, _P, _P, _I, _P, _P, _I, _P, _P]),
+    "ams_get_minmax": (_I, [_P, _P]),
+    "ams_set_minmax": (_I, [_P, _P]),
+    "ams_final_sort": (_I, [_P, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P, _P, _P, _P, _P]),
+    "ams_map_keys": (_I, [_P, _P, _P, _U64, _I, _I]),
+}
+
+EXPORTED = tuple(_SIGNATURES)
+
+
+def _load():
+    if not os.path.exists(LIB):
+        raise ImportError(
+            f"{LIB} is missing: build it with `python -m paper_1410_6754_b200.build` "
+            "(there is no CPU fallback for the AMS-sort hot path)")
+    lib = C.CDLL(LIB)
+    for name, (res, args) in _SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+lib = _load()
+
+
+class AmsError(RuntimeError):
+    pass
+
+
+def check(rc: int) -> int:
+    if rc == AMS_OK:
+        return rc
+    msg = lib.ams_last_error().decode(errors="replace")
+    if rc == AMS_EINVAL:
+        raise ValueError(msg)
+    raise AmsError(f"libams_b200 error {rc}: {msg}")
+
+
+def ptr(a) -> int | None:
+    """Address of a numpy array or torch tensor (None for None)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data
+    return a.data_ptr()
+
+
+def u64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.uint64)
+
+
+def i64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.int64)
+
+
+def i32(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.int32)
+
+
+# ---------------------------------------------------------------- host helpers
+
+def stream_seed_words(master_seed: int, stream_id: str) -> np.ndarray:
+    words = np.zeros(4, dtype=np.uint32)
+    n = C.c_int(0)
+    check(lib.ams_stream_seed(int(master_seed), stream_id.encode(), words.ctypes.data,
+                              C.addressof(n)))
+    return words[: n.value].copy()
+
+
+def blake2b_128(msg: bytes) -> bytes:
+    buf = np.frombuffer(msg, dtype=np.uint8) if msg else np.zeros(1, np.uint8)
+    out = np.zeros(16, dtype=np.uint8)
+    check(lib.ams_blake2b_128(buf.ctypes.data, len(msg), out.ctypes.data))
+    return out.tobytes()
+
+
+def sample_indices(seed_words: np.ndarray, n: int, k: int) -> np.ndarray:
+    w = np.ascontiguousarray(seed_words, dtype=np.uint32)
+    out = np.zeros(max(k, 1), dtype=np.uint64)
+    check(lib.ams_sample_indices(w.ctypes.data, len(w), n, k, out.ctypes.data))
+    return out[:k]
+
+
+def getrandbits(seed_words: np.ndarray, k: int, count: int) -> np.ndarray:
+    w = np.ascontiguousarray(seed_words, dtype=np.uint32)
+    out = np.zeros(max(count, 1), dtype=np.uint64)
+    check(lib.ams_mt_getrandbits(w.ctypes.data, len(w), k, count, out.ctypes.data))
+    return out[:count]
+
+
+def draw_sample_positions(master_seed, stream, level, group_first, group_npe, targets, sizes,
+                          offs):
+    gf, gn = i32(group_first), i32(group_npe)
+    tg, sz, of = u64(targets), u64(sizes), u64(offs)
+    cap = int(tg.sum())
+    idx = np.zeros(max(cap, 1), np.uint64)
+    gpos = np.zeros(max(cap, 1), np.uint64)
+    cnt = np.zeros(len(gf), np.uint64)
+    check(lib.ams_draw_sample_positions(int(master_seed), stream.encode(), level, len(gf),
+                                        gf.ctypes.data, gn.ctypes.data, tg.ctypes.data,
+                                        sz.ctypes.data, of.ctypes.data, cap, idx.ctypes.data,
+                                        gpos.ctypes.data, cnt.ctypes.data))
+    total = int(cnt.sum())
+    return idx[:total], gpos[:total], cnt
+
+
+def scan_groups(sizes, r: int, limit: int):
+    s = u64(sizes)
+    bnd = np.zeros(r + 1, np.uint64)
+    loads = np.zeros(r, np.uint64)
+    mx = np.zeros(1, np.uint64)
+    rc = lib.ams_scan_groups(s.ctypes.data, len(s), r, limit, bnd.ctypes.data, loads.ctypes.data,
+                             mx.ctypes.data)
+    if rc == 1:
+        return None
+    check(rc)
+    return tuple(int(x) for x in bnd), tuple(int(x) for x in loads), int(mx[0])
+
+
+def group_plan(sizes, r: int):
+    s = u64(sizes)
+    bnd = np.zeros(r + 1, np.uint64)
+    loads = np.zeros(r, np.uint64)
+    mx = np.zeros(1, np.uint64)
+    check(lib.ams_group_plan(s.ctypes.data, len(s), r, bnd.ctypes.data, loads.ctypes.data,
+                             mx.ctypes.data))
+    return tuple(int(x) for x in bnd), tuple(int(x) for x in loads), int(mx[0])
+
+
+def plan_level(group_npe, group_nb, r: int, seg_hist: np.ndarray, with_stats: bool = True):
+    gn, gb = i32(group_npe), i32(group_nb)
+    G = len(gn)
+    hist = np.ascontiguousarray(seg_hist, dtype=np.uint32)
+    nb_stride = hist.shape[1]
+    bnd = np.zeros((G, r + 1), np.uint64)
+    loads = np.zeros((G, r), np.uint64)
+    mx = np.zeros(G, np.uint64)
+    new_sizes = np.zeros(int(gn.sum()), np.uint64)
+    stats = np.zeros((G, 4), np.uint64) if with_stats else None
+    check(lib.ams_plan_level(G, gn.ctypes.data, gb.ctypes.data, r, hist.ctypes.data, nb_stride,
+                             bnd.ctypes.data, loads.ctypes.data, mx.ctypes.data,
+                             new_sizes.ctypes.data, ptr(stats)))
+    return bnd, loads, mx, new_sizes, stats
+
+
+# ---------------------------------------------------------------- device context
+
+class Context:
+    """One ``ams_ctx_t`` bound to a CUDA device and stream."""
+
+    def __init__(self, device: int, stream: int | None = None):
+        h = C.c_void_p()
+        check(lib.ams_ctx_create(int(device), stream, C.byref(h)))
+        self.h = h
+        self.device = int(device)
+
+    def close(self):
+        if self.h:
+            lib.ams_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):  # pragma: no cover - best effort
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_stream(self, stream: int | None):
+        check(lib.ams_ctx_set_stream(self.h, stream))
+
+    @property
+    def launches(self) -> int:
+        return int(lib.ams_ctx_launches(self.h))
+
+    def sync(self):
+        check(lib.ams_ctx_sync(self.h))
+
+    def level_sample(self, src, kind, idx, gpos, out_keys, out_pos):
+        idx, gpos = u64(idx), u64(gpos)
+        check(lib.ams_level_sample(self.h, ptr(src), kind, len(idx), idx.ctypes.data,
+                                   gpos.ctypes.data, ptr(out_keys), ptr(out_pos)))
+
+    def level_splitters(self, sample_keys, sample_pos, soff, nb):
+        soff, nb = u64(soff), i32(nb)
+        check(lib.ams_level_splitters(self.h, len(nb), ptr(sample_keys), ptr(sample_pos),
+                                      soff.ctypes.data, nb.ctypes.data))
+
+    def read_splitters(self, group: int):
+        keys = np.zeros(MAX_BUCKETS, np.uint64)
+        pos = np.zeros(MAX_BUCKETS, np.uint32)
+        n = C.c_int(0)
+        check(lib.ams_read_splitters(self.h, group, keys.ctypes.data, pos.ctypes.data, C.byref(n)))
+        return keys[: n.value].copy(), pos[: n.value].copy()
+
+    def level_classify(self, src, kind, seg_off, seg_len, seg_group, group_posbase, nb_stride,
+                       track_minmax):
+        so, sl, sg, pb = u64(seg_off), u64(seg_len), i32(seg_group), i64(group_posbase)
+        out = np.zeros((len(so), nb_stride), np.uint32)
+        check(lib.ams_level_classify(self.h, ptr(src), kind, len(so), so.ctypes.data,
+                                     sl.ctypes.data, sg.ctypes.data, len(pb), pb.ctypes.data,
+                                     nb_stride, int(bool(track_minmax)), out.ctypes.data))
+        return out
+
+    def level_scatter(self, src, src_vals, kind, dst, dst_vals, r, boundaries, group_dst_start):
+        b, d = u64(boundaries), u64(group_dst_start)
+        check(lib.ams_level_scatter(self.h, ptr(src), ptr(src_vals), kind, ptr(dst), ptr(dst_vals),
+                                    r, b.ctypes.data, d.ctypes.data))
+
+    def get_minmax(self):
+        out = np.zeros(2, np.uint64)
+        check(lib.ams_get_minmax(self.h, out.ctypes.data))
+        return int(out[0]), int(out[1])
+
+    def set_minmax(self, lo: int, hi: int):
+        a = np.array([lo, hi], np.uint64)
+        check(lib.ams_set_minmax(self.h, a.ctypes.data))
+
+    def final_sort(self, src, src_vals, tmp, tmp_vals, out, out_vals, key_kind, seg_off, seg_len,
+                   seg_cls, seg_b0, seg_b1, seg_nb):
+        so, sl, sc = u64(seg_off), u64(seg_len), i32(seg_cls)
+        b0, b1, nb = u64(seg_b0), u64(seg_b1), i32(seg_nb)
+        check(lib.ams_final_sort(self.h, ptr(src), ptr(src_vals), ptr(tmp), ptr(tmp_vals), ptr(out),
+                                 ptr(out_vals), key_kind, len(so), so.ctypes.data, sl.ctypes.data,
+                                 sc.ctypes.data, b0.ctypes.data, b1.ctypes.data, nb.ctypes.data))
+
+    def map_keys(self, src, dst, n, from_kind, to_kind):
+        check(lib.ams_map_keys(self.h, ptr(src), ptr(dst), n, from_kind, to_kind))

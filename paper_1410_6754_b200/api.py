@@ -1,0 +1,132 @@
+"""Public entry points.
+
+* :func:`ams_sort` — drop-in for the reference's
+  ``mlpsort.ams.ams_sort(net, data, params, scheme, seed)``
+  (ams.py:271-313): same arguments, same return structure
+  ``(dict[pe] -> sorted list of Elements, level_reports)``.
+* :func:`ams_sort_tensors` — the same sort over a device tensor of keys
+  (optionally with 8-byte payloads), no Python objects per element.
+* :func:`ams_sort_host` — host (numpy) buffers in, host buffers out; the
+  end-to-end path (H2D, sort, D2H) a user without device buffers calls.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from .engine import AmsSorter, SortOutput
+from .params import Element, as_params
+
+_SORTERS: dict = {}
+
+SUPPORTED_SCHEMES = ("simple",)
+
+
+def get_sorter(device=None) -> AmsSorter:
+    idx = torch.cuda.current_device() if device is None else (
+        device.index if isinstance(device, torch.device) else int(device))
+    s = _SORTERS.get(idx)
+    if s is None:
+        s = _SORTERS[idx] = AmsSorter(idx)
+    return s
+
+
+def _check_scheme(scheme: str):
+    if scheme not in SUPPORTED_SCHEMES:
+        raise ValueError(
+            f"delivery scheme {scheme!r} is not implemented on the B200 path; "
+            f"supported: {SUPPORTED_SCHEMES} (the reference's 'simple' layout, delivery.py:151-180)")
+
+
+def ams_sort_tensors(keys: torch.Tensor, pe_sizes, params, seed, vals: torch.Tensor | None = None,
+                     scheme: str = "simple", key_kind=None, out=None, out_vals=None,
+                     record_splitters: bool = False) -> SortOutput:
+    """Sort device keys laid out PE-major (``pe_sizes``); returns a
+    :class:`~paper_1410_6754_b200.engine.SortOutput`."""
+    _check_scheme(scheme)
+    return get_sorter(keys.device).sort(keys, pe_sizes, params, seed, vals=vals, out=out,
+                                        out_vals=out_vals, key_kind=key_kind,
+                                        record_splitters=record_splitters)
+
+
+def ams_sort_host(keys: np.ndarray, pe_sizes, params, seed, vals: np.ndarray | None = None,
+                  device=None, key_kind=None):
+    """Host buffers in and out: pinned H2D copy, device sort, D2H copy.
+    Returns (sorted keys ndarray, sorted vals ndarray or None, pe_sizes,
+    reports)."""
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else int(device))
+    kt = torch.from_numpy(np.ascontiguousarray(keys))
+    d_keys = kt.pin_memory().to(dev, non_blocking=True)
+    d_vals = None
+    if vals is not None:
+        d_vals = torch.from_numpy(np.ascontiguousarray(vals)).pin_memory().to(dev, non_blocking=True)
+    res = ams_sort_tensors(d_keys, pe_sizes, params, seed, vals=d_vals, key_kind=key_kind)
+    out_k = res.keys.cpu().numpy()
+    out_v = res.vals.cpu().numpy() if res.vals is not None else None
+    return out_k, out_v, res.pe_sizes, res.reports
+
+
+def _flatten(data, p):
+    keys, tags = [], []
+    sizes = np.zeros(p, dtype=np.uint64)
+    flat = []
+    for pe in range(p):
+        seq = data[pe]
+        sizes[pe] = len(seq)
+        flat.extend(seq)
+    return flat, sizes
+
+
+def ams_sort(net, data, params, scheme: str, seed):
+    """Drop-in for ``mlpsort.ams.ams_sort`` (ams.py:271-313).
+
+    ``net`` only needs ``.p`` (the reference's ``Network``); the simulated
+    ledger is not charged (cost accounting is not part of the B200 path).
+    Elements keep their identity: the returned lists hold the caller's own
+    Element objects.  Requires origin tags that increase along the PE-major
+    concatenation (as ``generate_input`` produces, bench.py:176), which makes
+    the reference's (key, origin_pe, origin_pos) order equal to the
+    (key, position) order the device uses.
+    """
+    _check_scheme(scheme)
+    params = as_params(params)
+    p = int(net.p)
+    params.validate_for(p)
+    flat, sizes = _flatten(data, p)
+    n = len(flat)
+    if n:
+        tags = np.array([(e.origin_pe, e.origin_pos) for e in flat], dtype=np.int64)
+        if n > 1:
+            d0 = np.diff(tags[:, 0])
+            d1 = np.diff(tags[:, 1])
+            if np.any((d0 < 0) | ((d0 == 0) & (d1 <= 0))):
+                raise ValueError("element origin tags must increase along the PE-major input "
+                                 "order for the B200 path (tie-break by position)")
+        ks = [int(e.key) for e in flat]
+        lo, hi = min(ks), max(ks)
+        if lo < 0:
+            if lo < -(1 << 63) or hi >= (1 << 63):
+                raise ValueError("keys must fit in 64 bits")
+            keys = np.array(ks, dtype=np.int64)
+            kind = "i64"
+        else:
+            if hi >= (1 << 64):
+                raise ValueError("keys must fit in 64 bits")
+            keys = np.array(ks, dtype=np.uint64)
+            kind = "u64"
+    else:
+        keys = np.zeros(0, dtype=np.uint64)
+        kind = "u64"
+    dev = torch.device("cuda", torch.cuda.current_device())
+    d_keys = torch.from_numpy(keys.view(np.int64)).to(dev)
+    d_vals = torch.arange(n, dtype=torch.int64, device=dev)
+    res = ams_sort_tensors(d_keys, sizes, params, seed, vals=d_vals, key_kind=kind)
+    order = res.vals.cpu().numpy()
+    out, start = {}, 0
+    for pe in range(p):
+        cnt = int(res.pe_sizes[pe])
+        out[pe] = [flat[i] for i in order[start:start + cnt]]
+        start += cnt
+    return out, res.reports

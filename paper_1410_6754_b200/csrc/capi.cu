@@ -1,0 +1,615 @@
+// C ABI of the AMS-sort hot path: device context, metadata staging and the
+// level / final-sort entry points declared in include/ams_b200.h.
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "ams_host.h"
+#include "launch.h"
+
+namespace ams {
+
+static thread_local std::string g_last_error;
+
+int set_error(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+namespace {
+
+#define AMS_CK(call)                                                                   \
+  do {                                                                                 \
+    cudaError_t _e = (call);                                                           \
+    if (_e != cudaSuccess)                                                             \
+      return set_error(AMS_ECUDA, std::string(#call) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap) return cudaSuccess;
+    if (p) {
+      cudaError_t e = cudaFree(p);
+      if (e != cudaSuccess) return e;
+      p = nullptr;
+      cap = 0;
+    }
+    size_t want = std::max<size_t>(bytes, 256);
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+  template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+struct HostBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap) return cudaSuccess;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = std::max<size_t>(bytes, 4096);
+    cudaError_t e = cudaMallocHost(&p, want);
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+  }
+  template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+// Packs small host arrays, uploads them with one async copy from pinned
+// memory, and keeps the device copy until the next upload on this stage.
+struct Stage {
+  std::vector<uint8_t> pack;
+  HostBuf h;
+  DevBuf d;
+  cudaEvent_t ev = nullptr;
+  bool pending = false;
+
+  void reset() { pack.clear(); }
+  template <class T>
+  size_t put(const T* src, size_t n) {
+    size_t off = (pack.size() + 15) & ~(size_t)15;
+    pack.resize(off + sizeof(T) * n);
+    if (n) std::memcpy(pack.data() + off, src, sizeof(T) * n);
+    return off;
+  }
+  template <class T>
+  size_t put(const std::vector<T>& v) { return put(v.data(), v.size()); }
+  cudaError_t upload(cudaStream_t st) {
+    cudaError_t e;
+    if (!ev) {
+      e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+      if (e != cudaSuccess) return e;
+    }
+    if (pending) {
+      e = cudaEventSynchronize(ev);
+      if (e != cudaSuccess) return e;
+      pending = false;
+    }
+    const size_t bytes = std::max<size_t>(pack.size(), 16);
+    if ((e = h.ensure(bytes)) != cudaSuccess) return e;
+    if ((e = d.ensure(bytes)) != cudaSuccess) return e;
+    std::memcpy(h.p, pack.data(), pack.size());
+    if ((e = cudaMemcpyAsync(d.p, h.p, pack.size(), cudaMemcpyHostToDevice, st)) != cudaSuccess)
+      return e;
+    if ((e = cudaEventRecord(ev, st)) != cudaSuccess) return e;
+    pending = true;
+    return cudaSuccess;
+  }
+  template <class T> const T* dev(size_t off) const {
+    return reinterpret_cast<const T*>(static_cast<const uint8_t*>(d.p) + off);
+  }
+  void release() {
+    h.release();
+    d.release();
+    if (ev) cudaEventDestroy(ev);
+    ev = nullptr;
+  }
+};
+
+int ceil_log2_u64(uint64_t x) { return x <= 1 ? 0 : 64 - __builtin_clzll(x - 1); }
+
+}  // namespace
+}  // namespace ams
+
+using namespace ams;
+
+struct ams_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  uint64_t launches = 0;
+  Stage st_sample, st_split, st_level, st_scatter, st_final;
+  // splitters / classifiers of the current level
+  DevBuf blobs, sorted_keys, sorted_pos, sample_idx;
+  std::vector<int32_t> group_nb;
+  int nspl_cap = 0, cells_cap = 0;
+  // level state (classify -> scatter)
+  int nseg = 0, ngroups = 0, nb_stride = 0;
+  uint64_t ntiles = 0, nchunks = 0;
+  std::vector<int32_t> group_first, group_nseg;
+  SegMeta meta{};
+  DevBuf tile_hist, chunk_tot, seg_hist, cell_base, pieces, minmax;
+  HostBuf h_hist;
+  // final sort
+  DevBuf dcls, ovf, ovf_count;
+  HostBuf h_small;
+};
+
+namespace {
+
+// Tile / chunk prefix arrays of a segment list.
+void tile_layout(const uint64_t* len, int nseg, std::vector<uint64_t>& tile_prefix,
+                 std::vector<uint64_t>& chunk_prefix) {
+  tile_prefix.assign(nseg + 1, 0);
+  chunk_prefix.assign(nseg + 1, 0);
+  for (int s = 0; s < nseg; ++s) {
+    const uint64_t tiles = (len[s] + kTile - 1) / kTile;
+    tile_prefix[s + 1] = tile_prefix[s] + tiles;
+    chunk_prefix[s + 1] = chunk_prefix[s] + (tiles + kChunkTiles - 1) / kChunkTiles;
+  }
+}
+
+// Upload a segment table; returns the device-side SegMeta.
+cudaError_t upload_segments(Stage& st, cudaStream_t stream, const uint64_t* off,
+                            const uint64_t* len, const int32_t* cls, int nseg,
+                            const int64_t* posbase, int ncls, SegMeta* m, uint64_t* ntiles,
+                            uint64_t* nchunks) {
+  std::vector<uint64_t> tp, cp;
+  tile_layout(len, nseg, tp, cp);
+  st.reset();
+  const size_t o_off = st.put(off, nseg), o_len = st.put(len, nseg), o_cls = st.put(cls, nseg);
+  const size_t o_tp = st.put(tp), o_cp = st.put(cp);
+  const size_t o_pb = posbase ? st.put(posbase, ncls) : 0;
+  cudaError_t e = st.upload(stream);
+  if (e != cudaSuccess) return e;
+  m->off = st.dev<uint64_t>(o_off);
+  m->len = st.dev<uint64_t>(o_len);
+  m->cls = st.dev<int32_t>(o_cls);
+  m->tile_prefix = st.dev<uint64_t>(o_tp);
+  m->chunk_prefix = st.dev<uint64_t>(o_cp);
+  m->posbase = posbase ? st.dev<int64_t>(o_pb) : nullptr;
+  m->nseg = nseg;
+  *ntiles = tp[nseg];
+  *nchunks = cp[nseg];
+  return cudaSuccess;
+}
+
+// hist -> chunk scan for a segment table whose classifiers are ready.
+int run_histogram(ams_ctx* c, const void* src, int kind, bool digit, const SegMeta& m,
+                  uint64_t ntiles, uint64_t nchunks, int nb_stride, const DigitCls* dcls,
+                  unsigned long long* minmax) {
+  AMS_CK(c->tile_hist.ensure(sizeof(uint32_t) * std::max<uint64_t>(ntiles, 1) * nb_stride));
+  AMS_CK(c->chunk_tot.ensure(sizeof(uint32_t) * std::max<uint64_t>(nchunks, 1) * nb_stride));
+  AMS_CK(c->seg_hist.ensure(sizeof(uint32_t) * (size_t)std::max(m.nseg, 1) * nb_stride));
+  AMS_CK(cudaMemsetAsync(c->seg_hist.p, 0, sizeof(uint32_t) * (size_t)m.nseg * nb_stride, c->stream));
+  AMS_CK(launch_hist(c->stream, src, kind, digit, m, nchunks, c->blobs.as<uint8_t>(), dcls,
+                     c->nspl_cap, c->cells_cap, nb_stride, c->tile_hist.as<uint32_t>(),
+                     c->chunk_tot.as<uint32_t>(), c->seg_hist.as<uint32_t>(), minmax));
+  AMS_CK(launch_chunk_scan(c->stream, c->chunk_tot.as<uint32_t>(), m, nb_stride));
+  c->launches += 2 + (nchunks ? 0 : 0);
+  return AMS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ams_last_error(void) { return g_last_error.c_str(); }
+int ams_version(void) { return 1; }
+
+int ams_ctx_create(int device, void* stream, ams_ctx_t** out) {
+  if (!out) return set_error(AMS_EINVAL, "null output pointer");
+  int ndev = 0;
+  AMS_CK(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev)
+    return set_error(AMS_EINVAL, "device " + std::to_string(device) + " out of range");
+  AMS_CK(cudaSetDevice(device));
+  ams_ctx* c = new ams_ctx();
+  c->device = device;
+  c->stream = static_cast<cudaStream_t>(stream);
+  *out = c;
+  return AMS_OK;
+}
+
+int ams_ctx_destroy(ams_ctx_t* c) {
+  if (!c) return AMS_OK;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (Stage* s : {&c->st_sample, &c->st_split, &c->st_level, &c->st_scatter, &c->st_final})
+    s->release();
+  for (DevBuf* b : {&c->blobs, &c->sorted_keys, &c->sorted_pos, &c->sample_idx, &c->tile_hist,
+                    &c->chunk_tot, &c->seg_hist, &c->cell_base, &c->pieces, &c->minmax, &c->dcls,
+                    &c->ovf, &c->ovf_count})
+    b->release();
+  c->h_hist.release();
+  c->h_small.release();
+  delete c;
+  return AMS_OK;
+}
+
+int ams_ctx_set_stream(ams_ctx_t* c, void* stream) {
+  if (!c) return set_error(AMS_EINVAL, "null context");
+  c->stream = static_cast<cudaStream_t>(stream);
+  return AMS_OK;
+}
+
+uint64_t ams_ctx_launches(const ams_ctx_t* c) { return c ? c->launches : 0; }
+
+int ams_ctx_sync(ams_ctx_t* c) {
+  if (!c) return set_error(AMS_EINVAL, "null context");
+  AMS_CK(cudaSetDevice(c->device));
+  AMS_CK(cudaStreamSynchronize(c->stream));
+  return AMS_OK;
+}
+
+int ams_level_sample(ams_ctx_t* c, const void* src, int key_kind, uint64_t count,
+                     const uint64_t* h_idx, const uint64_t* h_gpos, uint64_t* d_out_keys,
+                     uint32_t* d_out_pos) {
+  if (!c) return set_error(AMS_EINVAL, "null context");
+  if (count == 0) return AMS_OK;
+  if (!src || !h_idx || !h_gpos || !d_out_keys || !d_out_pos)
+    return set_error(AMS_EINVAL, "null argument");
+  AMS_CK(cudaSetDevice(c->device));
+  Stage& st = c->st_sample;
+  st.reset();
+  const size_t oi = st.put(h_idx, count), og = st.put(h_gpos, count);
+  AMS_CK(st.upload(c->stream));
+  AMS_CK(launch_gather_sample(c->stream, src, key_kind, st.dev<uint64_t>(oi), st.dev<uint64_t>(og),
+                              count, d_out_keys, d_out_pos));
+  c->launches += 1;
+  return AMS_OK;
+}
+
+int ams_level_splitters(ams_ctx_t* c, int ngroups, const uint64_t* d_sample_keys,
+                        const uint32_t* d_sample_pos, const uint64_t* h_soff, const int32_t* h_nb) {
+  if (!c) return set_error(AMS_EINVAL, "null context");
+  if (ngroups < 1 || !h_soff || !h_nb) return set_error(AMS_EINVAL, "bad group list");
+  AMS_CK(cudaSetDevice(c->device));
+  uint64_t max_s = 0;
+  int max_nb = 1, cells_cap = 1;
+  for (int g = 0; g < ngroups; ++g) {
+    const uint64_t S = h_soff[g + 1] - h_soff[g];
+    const int nb = h_nb[g];
+    if (h_soff[g + 1] < h_soff[g]) return set_error(AMS_EINVAL, "sample offsets not ascending");
+    if (nb < 1 || nb > AMS_MAX_BUCKETS)
+      return set_error(AMS_EINVAL, "bucket count " + std::to_string(nb) + " outside 1.." +
+                                       std::to_string(AMS_MAX_BUCKETS));
+    if (S < (uint64_t)(nb - 1))  // ams.py:186-187
+      return set_error(AMS_EINVAL, "sample of " + std::to_string(S) + " too small for " +
+                                       std::to_string(nb) + " buckets");
+    max_s = std::max(max_s, S);
+    max_nb = std::max(max_nb, nb);
+    if (nb > 1) cells_cap = std::max(cells_cap, 1 << lut_bits_for(nb - 1));
+  }
+  const uint64_t total = h_soff[ngroups];
+  if (total > 0 && (!d_sample_keys || !d_sample_pos)) return set_error(AMS_EINVAL, "null sample");
+  Stage& st = c->st_split;
+  st.reset();
+  const size_t os = st.put(h_soff, ngroups + 1), on = st.put(h_nb, ngroups);
+  AMS_CK(st.upload(c->stream));
+  AMS_CK(c->blobs.ensure(kBlobStride * (size_t)ngroups));
+  AMS_CK(c->sorted_keys.ensure(sizeof(uint64_t) * std::max<uint64_t>(total, 1)));
+  AMS_CK(c->sorted_pos.ensure(sizeof(uint32_t) * std::max<uint64_t>(total, 1)));
+  AMS_CK(launch_sample_rank(c->stream, ngroups, max_s, d_sample_keys, d_sample_pos,
+                            st.dev<uint64_t>(os), c->sorted_keys.as<uint64_t>(),
+                            c->sorted_pos.as<uint32_t>()));
+  AMS_CK(launch_build_cls(c->stream, ngroups, c->sorted_keys.as<uint64_t>(),
+                          c->sorted_pos.as<uint32_t>(), st.dev<uint64_t>(os), st.dev<int32_t>(on),
+                          c->blobs.as<uint8_t>()));
+  c->launches += (max_s ? 1 : 0) + 1;
+  c->group_nb.assign(h_nb, h_nb + ngroups);
+  c->ngroups = ngroups;
+  c->nspl_cap = max_nb - 1;
+  c->cells_cap = cells_cap;
+  return AMS_OK;
+}
+
+int ams_read_splitters(ams_ctx_t* c, int group, uint64_t* keys, uint32_t* pos, int* nspl) {
+  if (!c) return set_error(AMS_EINVAL, "null context");
+  if (group < 0 || group >= c->ngroups) return set_error(AMS_EINVAL, "group out of range");
+  AMS_CK(cudaSetDevice(c->device));
+  ClsHeader h;
+  const uint8_t* blob = c->blobs.as<uint8_t>() + (size_t)group * kBlobStride;
+  AMS_CK(cudaMemcpyAsync(&h, blob, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+  AMS_CK(cudaStreamSynchronize(c->stream));
+  if (nspl) *nspl = (int)h.nspl;
+  if (h.nspl) {
+    if (keys) AMS_CK(cudaMemcpy(keys, blob + kBlobKeys, 8 * (size_t)h.nspl, cudaMemcpyDeviceToHost));
+    if (pos) AMS_CK(cudaMemcpy(pos, blob + kBlobPos, 4 * (size_t)h.nspl, cudaMemcpyDeviceToHost));
+  }
+  return AMS_OK;
+}
+
+int ams_level_classify(ams_ctx_t* c, const void* src, int key_kind, int nseg,
+                       const uint64_t* h_seg_off, const uint64_t* h_seg_len,
+                       const int32_t* h_seg_group, int ngroups, const int64_t* h_group_posbase,
+                       int nb_stride, int track_minmax, uint32_t* h_seg_hist_out) {
+  if (!c) return set_error(AMS_EINVAL, "null context");
+  if (nseg < 1 || !h_seg_off || !h_seg_len || !h_seg_group || !h_group_posbase)
+    return set_error(AMS_EINVAL, "bad segment list");
+  if (ngroups != c->ngroups)
+    return set_error(AMS_EINVAL, "group count differs from the last ams_level_splitters call");
+  int max_nb = 1;
+  for (int g = 0; g < ngroups; ++g) max_nb = std::max(max_nb, c->group_nb[g]);
+  if (nb_stride < max_nb) return set_error(AMS_EINVAL, "nb_stride smaller than the bucket count");
+  AMS_CK(cudaSetDevice(c->device));
+  // Groups are contiguous runs of segments.
+  c->group_first.assign(ngroups, -1);
+  c->group_nseg.assign(ngroups, 0);
+  for (int s = 0; s < nseg; ++s) {
+    const int g = h_seg_group[s];
+    if (g < 0 || g >= ngroups) return set_error(AMS_EINVAL, "segment group out of range");
+    if (s > 0 && g < h_seg_group[s - 1]) return set_error(AMS_EINVAL, "segments not group-major");
+    if (c->group_first[g] < 0) c->group_first[g] = s;
+    c->group_nseg[g] += 1;
+  }
+  for (int g = 0; g < ngroups; ++g) {
+    if (c->group_nseg[g] == 0) return set_error(AMS_EINVAL, "group without segments");
+    uint64_t n_g = 0;
+    for (int j = 0; j < c->group_nseg[g]; ++j) n_g += h_seg_len[c->group_first[g] + j];
+    if (n_g >= 0xFFFFFFFFull) return set_error(AMS_EINVAL, "group too large for 32-bit positions");
+  }
+  AMS_CK(upload_segments(c->st_level, c->stream, h_seg_off, h_seg_len, h_seg_group, nseg,
+                         h_group_posbase, ngroups, &c->meta, &c->ntiles, &c->nchunks));
+  c->nseg = nseg;
+  c->nb_stride = nb_stride;
+  unsigned long long* mm = nullptr;
+  if (track_minmax) {
+    AMS_CK(c->minmax.ensure(16));
+    const unsigned long long init[2] = {~0ULL, 0ULL};
+    AMS_CK(c->h_small.ensure(64));
+    AMS_CK(cudaStreamSynchronize(c->stream));
+    std::memcpy(c->h_small.p, init, sizeof init);
+    AMS_CK(cudaMemcpyAsync(c->minmax.p, c->h_small.p, sizeof init, cudaMemcpyHostToDevice, c->stream));
+    mm = c->minmax.as<unsigned long long>();
+  }
+  int rc = run_histogram(c, src, key_kind, false, c->meta, c->ntiles, c->nchunks, nb_stride,
+                         nullptr, mm);
+  if (rc) return rc;
+  const size_t hb = sizeof(uint32_t) * (size_t)nseg * nb_stride;
+  AMS_CK(c->h_hist.ensure(hb));
+  AMS_CK(cudaMemcpyAsync(c->h_hist.p, c->seg_hist.p, hb, cudaMemcpyDeviceToHost, c->stream));
+  AMS_CK(cudaStreamSynchronize(c->stream));
+  if (h_seg_hist_out) std::memcpy(h_seg_hist_out, c->h_hist.p, hb);
+  return AMS_OK;
+}
+
+int ams_level_scatter(ams_ctx_t* c, const void* src, const void* src_vals, int key_kind,
+                      void* dst, void* dst_vals, int r, const uint64_t* h_boundaries,
+                      const uint64_t* h_group_dst_start) {
+  if (!c) return set_error(AMS_EINVAL, "null context");
+  if (c->nseg == 0) return set_error(AMS_EINVAL, "ams_level_classify must run first");
+  if (r < 1 || !h_boundaries || !h_group_dst_start) return set_error(AMS_EINVAL, "bad plan");
+  if ((src_vals == nullptr) != (dst_vals == nullptr))
+    return set_error(AMS_EINVAL, "values must be given for both source and destination");
+  AMS_CK(cudaSetDevice(c->device));
+  const int G = c->ngroups;
+  for (int g = 0; g < G; ++g) {
+    const uint64_t* b = h_boundaries + (size_t)g * (r + 1);
+    if (b[0] != 0 || b[r] != (uint64_t)c->group_nb[g])
+      return set_error(AMS_EINVAL, "plan boundaries do not cover the buckets");
+    for (int i = 0; i < r; ++i)
+      if (b[i + 1] < b[i]) return set_error(AMS_EINVAL, "plan boundaries not ascending");
+  }
+  Stage& st = c->st_scatter;
+  st.reset();
+  const size_t of = st.put(c->group_first), on = st.put(c->group_nseg);
+  const size_t ob = st.put(h_boundaries, (size_t)G * (r + 1));
+  const size_t od = st.put(h_group_dst_start, G);
+  AMS_CK(st.upload(c->stream));
+  GroupMeta gm;
+  gm.first = st.dev<int32_t>(of);
+  gm.nseg = st.dev<int32_t>(on);
+  gm.bnd = st.dev<uint64_t>(ob);
+  gm.dst_start = st.dev<uint64_t>(od);
+  AMS_CK(c->pieces.ensure(sizeof(uint64_t) * (size_t)c->nseg * r));
+  AMS_CK(c->cell_base.ensure(sizeof(uint64_t) * (size_t)c->nseg * c->nb_stride));
+  AMS_CK(launch_cell_base(c->stream, c->seg_hist.as<uint32_t>(), c->nb_stride, gm, G, r,
+                          c->pieces.as<uint64_t>(), c->cell_base.as<uint64_t>()));
+  AMS_CK(launch_scatter(c->stream, src, src_vals, key_kind, false, dst, dst_vals, c->meta,
+                        c->ntiles, c->blobs.as<uint8_t>(), nullptr, c->nspl_cap, c->cells_cap,
+                        c->nb_stride, c->tile_hist.as<uint32_t>(), c->chunk_tot.as<uint32_t>(),
+                        c->cell_base.as<uint64_t>()));
+  c->launches += 2;
+  return AMS_OK;
+}
+
+int ams_get_minmax(ams_ctx_t* c, uint64_t out[2]) {
+  if (!c || !out) return set_error(AMS_EINVAL, "null argument");
+  if (!c->minmax.p) return set_error(AMS_EINVAL, "no min/max recorded");
+  AMS_CK(cudaSetDevice(c->device));
+  AMS_CK(cudaMemcpyAsync(c->h_small.p, c->minmax.p, 16, cudaMemcpyDeviceToHost, c->stream));
+  AMS_CK(cudaStreamSynchronize(c->stream));
+  std::memcpy(out, c->h_small.p, 16);
+  return AMS_OK;
+}
+
+int ams_set_minmax(ams_ctx_t* c, const uint64_t in[2]) {
+  if (!c || !in) return set_error(AMS_EINVAL, "null argument");
+  AMS_CK(cudaSetDevice(c->device));
+  AMS_CK(c->minmax.ensure(16));
+  AMS_CK(c->h_small.ensure(64));
+  AMS_CK(cudaStreamSynchronize(c->stream));
+  std::memcpy(c->h_small.p, in, 16);
+  AMS_CK(cudaMemcpyAsync(c->minmax.p, c->h_small.p, 16, cudaMemcpyHostToDevice, c->stream));
+  return AMS_OK;
+}
+
+int ams_final_sort(ams_ctx_t* c, void* src, void* src_vals, void* tmp, void* tmp_vals, void* out,
+                   void* out_vals, int key_kind, int nseg, const uint64_t* h_seg_off,
+                   const uint64_t* h_seg_len, const int32_t* h_seg_cls, const uint64_t* h_seg_b0,
+                   const uint64_t* h_seg_b1, const int32_t* h_seg_nb) {
+  if (!c) return set_error(AMS_EINVAL, "null context");
+  if (nseg < 0 || (nseg > 0 && (!h_seg_off || !h_seg_len))) return set_error(AMS_EINVAL, "bad segments");
+  const bool vals = src_vals != nullptr;
+  if (vals && (!tmp_vals || !out_vals)) return set_error(AMS_EINVAL, "missing value buffers");
+  AMS_CK(cudaSetDevice(c->device));
+  constexpr uint64_t kTargetCell = 4096;
+  std::vector<uint64_t> s_off, s_len, b_off, b_len, b_b0, b_b1;
+  std::vector<int32_t> b_cls, b_nb;
+  uint64_t total = 0, max_big = 0;
+  for (int s = 0; s < nseg; ++s) {
+    total += h_seg_len[s];
+    if (h_seg_len[s] == 0) continue;
+    if (h_seg_len[s] <= (uint64_t)AMS_SMEM_SORT_CAP) {
+      s_off.push_back(h_seg_off[s]);
+      s_len.push_back(h_seg_len[s]);
+    } else {
+      if (!h_seg_cls || !h_seg_b0 || !h_seg_b1 || !h_seg_nb)
+        return set_error(AMS_EINVAL, "large segments need their bucket ranges");
+      if (h_seg_cls[s] < 0 || h_seg_cls[s] >= c->ngroups)
+        return set_error(AMS_EINVAL, "segment classifier out of range");
+      if (!c->minmax.p) return set_error(AMS_EINVAL, "no key range recorded (track_minmax)");
+      b_off.push_back(h_seg_off[s]);
+      b_len.push_back(h_seg_len[s]);
+      b_cls.push_back(h_seg_cls[s]);
+      b_b0.push_back(h_seg_b0[s]);
+      b_b1.push_back(h_seg_b1[s]);
+      b_nb.push_back(h_seg_nb[s]);
+      max_big = std::max(max_big, h_seg_len[s]);
+    }
+  }
+  const uint64_t ovf_cap = total / (AMS_SMEM_SORT_CAP + 1) + 16;
+  AMS_CK(c->ovf.ensure(sizeof(OverflowRec) * ovf_cap));
+  AMS_CK(c->ovf_count.ensure(sizeof(unsigned int)));
+  AMS_CK(cudaMemsetAsync(c->ovf_count.p, 0, sizeof(unsigned int), c->stream));
+  Stage& st = c->st_final;
+  // 1. Segments that fit in shared memory: sort straight into `out`.
+  if (!s_off.empty()) {
+    st.reset();
+    const size_t oo = st.put(s_off), ol = st.put(s_len);
+    AMS_CK(st.upload(c->stream));
+    CellSource cs{};
+    cs.mode = 1;
+    cs.seg_off = st.dev<uint64_t>(oo);
+    cs.seg_len = st.dev<uint64_t>(ol);
+    AMS_CK(launch_smem_sort(c->stream, src, src_vals, out, out_vals, key_kind, cs, s_off.size(),
+                            c->ovf.as<OverflowRec>(), c->ovf_count.as<unsigned int>()));
+    c->launches += 1;
+  }
+  // 2. Large segments: digit partition src -> tmp, then per-cell sorts.
+  void* cur = src;
+  void* cur_v = src_vals;
+  void* oth = tmp;
+  void* oth_v = tmp_vals;
+  std::vector<DigitCls> host_dcls;
+  bool first_round = true;
+  while (!b_off.empty()) {
+    const int nb_seg = (int)b_off.size();
+    const int nbits = std::min(11, std::max(1, ceil_log2_u64((max_big + kTargetCell - 1) / kTargetCell)));
+    const int nbs = 1 << nbits;
+    std::vector<int32_t> idx(nb_seg);
+    for (int i = 0; i < nb_seg; ++i) idx[i] = i;
+    SegMeta m;
+    uint64_t ntiles, nchunks;
+    AMS_CK(c->dcls.ensure(sizeof(DigitCls) * (size_t)nb_seg));
+    if (first_round) {
+      Stage& sf = c->st_split;  // free after the level: reuse for the range table
+      sf.reset();
+      const size_t oc = sf.put(b_cls), o0 = sf.put(b_b0), o1 = sf.put(b_b1), on = sf.put(b_nb);
+      AMS_CK(sf.upload(c->stream));
+      FinalRangeMeta fm;
+      fm.cls = sf.dev<int32_t>(oc);
+      fm.b0 = sf.dev<uint64_t>(o0);
+      fm.b1 = sf.dev<uint64_t>(o1);
+      fm.nb = sf.dev<int32_t>(on);
+      fm.nseg = nb_seg;
+      fm.nbits = nbits;
+      AMS_CK(launch_final_ranges(c->stream, fm, c->blobs.as<uint8_t>(),
+                                 c->minmax.as<unsigned long long>(), c->dcls.as<DigitCls>()));
+      c->launches += 1;
+    } else {
+      host_dcls.resize(nb_seg);
+      for (int i = 0; i < nb_seg; ++i) {
+        DigitCls d;
+        d.lo = b_b0[i];
+        d.hi = b_b1[i];
+        const int bl = bit_length64(d.hi - d.lo);
+        d.shift = bl > nbits ? (uint32_t)(bl - nbits) : 0u;
+        d.nb = (uint32_t)nbs;
+        host_dcls[i] = d;
+      }
+      AMS_CK(c->h_small.ensure(sizeof(DigitCls) * (size_t)nb_seg + 64));
+      AMS_CK(cudaStreamSynchronize(c->stream));
+      std::memcpy(c->h_small.p, host_dcls.data(), sizeof(DigitCls) * (size_t)nb_seg);
+      AMS_CK(cudaMemcpyAsync(c->dcls.p, c->h_small.p, sizeof(DigitCls) * (size_t)nb_seg,
+                             cudaMemcpyHostToDevice, c->stream));
+    }
+    AMS_CK(upload_segments(st, c->stream, b_off.data(), b_len.data(), idx.data(), nb_seg, nullptr,
+                           0, &m, &ntiles, &nchunks));
+    int rc = run_histogram(c, cur, AMS_KEY_U64, true, m, ntiles, nchunks, nbs,
+                           c->dcls.as<DigitCls>(), nullptr);
+    if (rc) return rc;
+    AMS_CK(c->cell_base.ensure(sizeof(uint64_t) * (size_t)nb_seg * nbs));
+    AMS_CK(launch_digit_base(c->stream, c->seg_hist.as<uint32_t>(), nbs, m,
+                             c->cell_base.as<uint64_t>()));
+    AMS_CK(launch_scatter(c->stream, cur, cur_v, AMS_KEY_U64, true, oth, oth_v, m, ntiles,
+                          c->blobs.as<uint8_t>(), c->dcls.as<DigitCls>(), 0, 0, nbs,
+                          c->tile_hist.as<uint32_t>(), c->chunk_tot.as<uint32_t>(),
+                          c->cell_base.as<uint64_t>()));
+    AMS_CK(cudaMemsetAsync(c->ovf_count.p, 0, sizeof(unsigned int), c->stream));
+    CellSource cs{};
+    cs.mode = 0;
+    cs.nbits = nbits;
+    cs.cell_base = c->cell_base.as<uint64_t>();
+    cs.cell_cnt = c->seg_hist.as<uint32_t>();
+    cs.dcls = c->dcls.as<DigitCls>();
+    AMS_CK(launch_smem_sort(c->stream, oth, oth_v, out, out_vals, key_kind, cs,
+                            (uint64_t)nb_seg * nbs, c->ovf.as<OverflowRec>(),
+                            c->ovf_count.as<unsigned int>()));
+    c->launches += 3;
+    // Cells that still exceed shared memory go round again.
+    unsigned int novf = 0;
+    AMS_CK(c->h_small.ensure(64));
+    AMS_CK(cudaMemcpyAsync(c->h_small.p, c->ovf_count.p, sizeof novf, cudaMemcpyDeviceToHost, c->stream));
+    AMS_CK(cudaStreamSynchronize(c->stream));
+    std::memcpy(&novf, c->h_small.p, sizeof novf);
+    b_off.clear(); b_len.clear(); b_b0.clear(); b_b1.clear();
+    max_big = 0;
+    if (novf) {
+      std::vector<OverflowRec> recs(novf);
+      AMS_CK(cudaMemcpy(recs.data(), c->ovf.p, sizeof(OverflowRec) * novf, cudaMemcpyDeviceToHost));
+      std::sort(recs.begin(), recs.end(),
+                [](const OverflowRec& a, const OverflowRec& b) { return a.off < b.off; });
+      for (const OverflowRec& r : recs) {
+        b_off.push_back(r.off);
+        b_len.push_back(r.count);
+        b_b0.push_back(r.lo);  // exact min/max of the cell
+        b_b1.push_back(r.hi);
+        max_big = std::max(max_big, r.count);
+      }
+    }
+    first_round = false;
+    std::swap(cur, oth);
+    std::swap(cur_v, oth_v);
+  }
+  return AMS_OK;
+}
+
+int ams_map_keys(ams_ctx_t* c, const void* src, void* dst, uint64_t n, int from_kind, int to_kind) {
+  if (!c) return set_error(AMS_EINVAL, "null context");
+  AMS_CK(cudaSetDevice(c->device));
+  AMS_CK(launch_map_keys(c->stream, src, dst, n, from_kind, to_kind));
+  c->launches += n ? 1 : 0;
+  return AMS_OK;
+}
+
+}  // extern "C"

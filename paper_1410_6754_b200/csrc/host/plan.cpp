@@ -1,0 +1,209 @@
+// Consecutive-bucket grouping and the per-level delivery bookkeeping,
+// restated natively.
+//
+// Reference: _scan / scan_groups / optimal_group_plan (ams.py:78-154) and
+// the simple delivery's quota slots (delivery.py:78-106, 138-180) with the
+// exchange shape Network.exchange records (simnet.py:294-335).
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../ams_host.h"
+
+namespace ams {
+namespace {
+
+struct Plan {
+  std::vector<uint64_t> boundaries, loads;
+  uint64_t max_load = 0;
+};
+
+// _scan (ams.py:78-109): returns feasibility; `overflow` = smallest
+// load+bucket that failed to fit (UINT64_MAX when none).
+bool scan(const uint64_t* sizes, int nb, int r, uint64_t limit, Plan* plan, uint64_t* overflow) {
+  uint64_t ovf = UINT64_MAX;
+  plan->boundaries.assign(1, 0);
+  plan->loads.clear();
+  uint64_t cur = 0;
+  for (int i = 0; i < nb; ++i) {
+    const uint64_t size = sizes[i];
+    if (size > limit) { *overflow = ovf; return false; }
+    if (cur + size > limit) {
+      if (cur + size < ovf) ovf = cur + size;
+      plan->boundaries.push_back((uint64_t)i);
+      plan->loads.push_back(cur);
+      cur = size;
+    } else {
+      cur += size;
+    }
+  }
+  plan->boundaries.push_back((uint64_t)nb);
+  plan->loads.push_back(cur);
+  *overflow = ovf;
+  if ((int)plan->loads.size() > r) return false;
+  while ((int)plan->loads.size() < r) {
+    plan->boundaries.push_back((uint64_t)nb);
+    plan->loads.push_back(0);
+  }
+  plan->max_load = *std::max_element(plan->loads.begin(), plan->loads.end());
+  return true;
+}
+
+// optimal_group_plan (ams.py:119-154), including the float window bound.
+void optimal_plan(const uint64_t* sizes, int nb, int r, Plan* best) {
+  uint64_t total = 0, mx = 0;
+  for (int i = 0; i < nb; ++i) { total += sizes[i]; mx = std::max(mx, sizes[i]); }
+  uint64_t lo = std::max(mx, (total + r - 1) / (uint64_t)r);
+  const int b_est = std::max(1, nb / r);
+  const double est = (double)total / (double)r * (1.0 + 4.0 / (double)b_est);
+  uint64_t hi = std::max(lo, (uint64_t)std::ceil(est));
+  Plan plan;
+  uint64_t overflow;
+  bool ok = scan(sizes, nb, r, hi, &plan, &overflow);
+  if (!ok) {
+    lo = std::max(lo, overflow != UINT64_MAX ? overflow : hi + 1);
+    hi = total;
+    scan(sizes, nb, r, hi, &plan, &overflow);  // one group of everything fits
+  }
+  hi = plan.max_load;
+  *best = plan;
+  while (lo < hi) {
+    const uint64_t mid = lo + (hi - lo) / 2;
+    ok = scan(sizes, nb, r, mid, &plan, &overflow);
+    if (ok) {
+      hi = plan.max_load;
+      *best = plan;
+    } else {
+      lo = overflow != UINT64_MAX ? overflow : mid + 1;
+    }
+  }
+}
+
+// Exchange shape of deliver_simple for one group (see oracle
+// _exchange_stats): pieces[j][g], P members, r subgroups of P/r.
+void exchange_stats(const std::vector<uint64_t>& pieces, int P, int r, uint64_t out[4]) {
+  const int sub = P / r;
+  std::vector<uint64_t> sw(P, 0), rw(P, 0), sm(P, 0), rm(P, 0);
+  for (int g = 0; g < r; ++g) {
+    uint64_t m = 0;
+    for (int j = 0; j < P; ++j) m += pieces[(size_t)j * r + g];
+    uint64_t start = 0;
+    for (int j = 0; j < P; ++j) {
+      const uint64_t size = pieces[(size_t)j * r + g];
+      if (size == 0 || m == 0) { start += size; continue; }
+      // First owner of element number `start` (delivery.py:94).
+      int t = (int)(((unsigned __int128)(start + 1) * sub + m - 1) / m) - 1;
+      uint64_t covered = 0;
+      while (covered < size && t < sub) {
+        const uint64_t slot_hi = (uint64_t)(((unsigned __int128)m * (t + 1)) / sub);
+        const int64_t take = (int64_t)std::min(start + size, slot_hi) - (int64_t)(start + covered);
+        if (take > 0) {
+          const int dest = g * sub + t;
+          if (dest != j) { sw[j] += take; rw[dest] += take; sm[j] += 1; rm[dest] += 1; }
+          covered += (uint64_t)take;
+        }
+        ++t;
+      }
+      start += size;
+    }
+  }
+  uint64_t hs = 0, hr = 0, ms = 0, mr = 0;
+  for (int j = 0; j < P; ++j) {
+    hs = std::max(hs, sw[j]); hr = std::max(hr, rw[j]);
+    ms = std::max(ms, sm[j]); mr = std::max(mr, rm[j]);
+  }
+  out[0] = std::max(hs, hr);
+  out[1] = std::max(ms, mr);
+  out[2] = ms;
+  out[3] = mr;
+}
+
+}  // namespace
+}  // namespace ams
+
+using namespace ams;
+
+extern "C" {
+
+int ams_scan_groups(const uint64_t* sizes, int nb, int r, uint64_t limit,
+                    uint64_t* out_boundaries, uint64_t* out_loads, uint64_t* out_max_load) {
+  if (nb < 1 || r < 1) return set_error(AMS_EINVAL, "bad histogram / group count");
+  Plan plan;
+  uint64_t ovf;
+  if (!scan(sizes, nb, r, limit, &plan, &ovf)) return 1;  // infeasible (not an error)
+  std::copy(plan.boundaries.begin(), plan.boundaries.end(), out_boundaries);
+  std::copy(plan.loads.begin(), plan.loads.end(), out_loads);
+  *out_max_load = plan.max_load;
+  return AMS_OK;
+}
+
+int ams_group_plan(const uint64_t* sizes, int nb, int r, uint64_t* out_boundaries,
+                   uint64_t* out_loads, uint64_t* out_max_load) {
+  if (r < 1) return set_error(AMS_EINVAL, "need at least one group");
+  if (nb < 1) return set_error(AMS_EINVAL, "histogram has no buckets");
+  Plan plan;
+  optimal_plan(sizes, nb, r, &plan);
+  std::copy(plan.boundaries.begin(), plan.boundaries.end(), out_boundaries);
+  std::copy(plan.loads.begin(), plan.loads.end(), out_loads);
+  *out_max_load = plan.max_load;
+  return AMS_OK;
+}
+
+// The host half of one level (ams.py:231-256) for every group, given the
+// per-member bucket histograms.
+//   seg_hist: [sum(group_npe)][nb_stride] u32, members group-major.
+//   Per group g (npe P, nb buckets, r groups): boundaries (r+1), loads (r),
+//   max_load; per member the next-level size (quota slots of the subgroup,
+//   delivery.py:78-80); 4 exchange stats (max_words, max_msgs,
+//   max_sent_msgs, max_recv_msgs).
+int ams_plan_level(int ngroups, const int32_t* group_npe, const int32_t* group_nb, int r,
+                   const uint32_t* seg_hist, int nb_stride, uint64_t* out_boundaries,
+                   uint64_t* out_loads, uint64_t* out_max_load, uint64_t* out_new_sizes,
+                   uint64_t* out_stats) {
+  if (r < 1) return set_error(AMS_EINVAL, "need at least one group");
+  size_t seg0 = 0;
+  std::vector<uint64_t> h, pieces;
+  for (int g = 0; g < ngroups; ++g) {
+    const int P = group_npe[g], nb = group_nb[g];
+    if (P % r != 0) {
+      return set_error(AMS_EINVAL, std::to_string(P) + " PEs cannot form " +
+                                       std::to_string(r) + " groups");
+    }
+    if (nb < 1 || nb > nb_stride) return set_error(AMS_EINVAL, "bad bucket count");
+    h.assign(nb, 0);
+    for (int j = 0; j < P; ++j)
+      for (int b = 0; b < nb; ++b) h[b] += seg_hist[(seg0 + j) * nb_stride + b];
+    Plan plan;
+    optimal_plan(h.data(), nb, r, &plan);
+    std::copy(plan.boundaries.begin(), plan.boundaries.end(), out_boundaries + (size_t)g * (r + 1));
+    std::copy(plan.loads.begin(), plan.loads.end(), out_loads + (size_t)g * r);
+    out_max_load[g] = plan.max_load;
+    const int sub = P / r;
+    for (int gg = 0; gg < r; ++gg) {
+      const uint64_t m = plan.loads[gg];
+      for (int t = 0; t < sub; ++t) {
+        const uint64_t a = (uint64_t)(((unsigned __int128)m * t) / sub);
+        const uint64_t b = (uint64_t)(((unsigned __int128)m * (t + 1)) / sub);
+        out_new_sizes[seg0 + (size_t)gg * sub + t] = b - a;
+      }
+    }
+    if (out_stats) {
+      pieces.assign((size_t)P * r, 0);
+      for (int j = 0; j < P; ++j)
+        for (int gg = 0; gg < r; ++gg) {
+          uint64_t s = 0;
+          for (uint64_t b = plan.boundaries[gg]; b < plan.boundaries[gg + 1]; ++b)
+            s += seg_hist[(seg0 + j) * nb_stride + b];
+          pieces[(size_t)j * r + gg] = s;
+        }
+      exchange_stats(pieces, P, r, out_stats + (size_t)g * 4);
+    }
+    seg0 += P;
+  }
+  return AMS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,794 @@
+// sm_100a kernels of the AMS-sort hot path.
+//
+//   K1 k_gather_sample   sample elements at host-drawn positions
+//                        (draw_sample, ams.py:157-175)
+//   K2 k_sample_rank     work-inefficient rank-by-counting of the group
+//      k_build_cls       sample, splitters at ranks (i*S)//nb, key LUT
+//                        (select_splitters ams.py:178-198, fastsort.py:57-130)
+//   K3 k_hist            classification + tile/chunk/segment histograms
+//                        (partition_buckets ams.py:201-211, allreduce 236-237)
+//   K4 k_chunk_scan,     offsets of every (group, source PE, bucket) cell
+//      k_cell_base,      (deliver_simple prefix sums delivery.py:138-180)
+//      k_digit_base
+//   K6 k_scatter         stable bucket-contiguous scatter (pieces ams.py:
+//                        240-248, exchange order simnet.py:324-325)
+//   K7 k_final_ranges    key range of every final PE
+//   K9 k_smem_sort       CTA-local stable sort in shared memory (sorted(),
+//                        ams.py:310-312)
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "ams_device.cuh"
+#include "launch.h"
+
+namespace ams {
+
+namespace {
+
+__device__ __forceinline__ int upper_bound_u64(const uint64_t* a, int n, uint64_t x) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (a[mid] <= x) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+constexpr uint32_t kInvalid = 0xFFFFFFFFu;
+
+// -------------------------------------------------------------------- K1
+template <int KIND>
+__global__ void k_gather_sample(const uint64_t* __restrict__ src, const uint64_t* __restrict__ idx,
+                                const uint64_t* __restrict__ gpos, uint64_t n,
+                                uint64_t* __restrict__ out_keys, uint32_t* __restrict__ out_pos) {
+  const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  out_keys[i] = to_ordered<KIND>(src[idx[i]]);
+  out_pos[i] = (uint32_t)gpos[i];
+}
+
+// -------------------------------------------------------------------- K2
+// rank_i = #{j : (k_j, p_j) < (k_i, p_i)} over the group's sample; every
+// warp walks the sample 32 elements at a time and broadcasts them with
+// __shfl_sync (the all-gather + rank-by-counting of fastsort.py:57-108).
+__global__ void __launch_bounds__(256) k_sample_rank(const uint64_t* __restrict__ keys,
+                                                     const uint32_t* __restrict__ pos,
+                                                     const uint64_t* __restrict__ soff,
+                                                     uint64_t* __restrict__ sorted_keys,
+                                                     uint32_t* __restrict__ sorted_pos) {
+  const int g = blockIdx.y;
+  const uint64_t s0 = soff[g], S = soff[g + 1] - s0;
+  const uint64_t first = (uint64_t)blockIdx.x * blockDim.x;
+  if (first >= S) return;
+  const uint64_t i = first + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const bool mine = i < S;
+  const uint64_t ki = mine ? keys[s0 + i] : ~0ULL;
+  const uint32_t pi = mine ? pos[s0 + i] : 0xFFFFFFFFu;
+  uint32_t cnt = 0;
+  for (uint64_t c = 0; c < S; c += 32) {
+    const bool ok = c + lane < S;
+    const uint64_t kl = ok ? keys[s0 + c + lane] : ~0ULL;
+    const uint32_t pl = ok ? pos[s0 + c + lane] : 0xFFFFFFFFu;
+#pragma unroll 8
+    for (int t = 0; t < 32; ++t) {
+      const uint64_t kj = __shfl_sync(0xffffffffu, kl, t);
+      const uint32_t pj = __shfl_sync(0xffffffffu, pl, t);
+      cnt += (kj < ki) | ((kj == ki) & (pj < pi));
+    }
+  }
+  if (mine) {
+    sorted_keys[s0 + cnt] = ki;
+    sorted_pos[s0 + cnt] = pi;
+  }
+}
+
+__device__ __forceinline__ uint32_t lower_bound_smem(const uint64_t* a, uint32_t n, uint64_t x) {
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    uint32_t mid = (lo + hi) >> 1;
+    if (a[mid] < x) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// One CTA per group: splitter i (0-based) = sorted sample at rank
+// ((i+1)*S)//nb (ams.py:190), then the cell LUT.
+__global__ void __launch_bounds__(1024) k_build_cls(const uint64_t* __restrict__ sorted_keys,
+                                                    const uint32_t* __restrict__ sorted_pos,
+                                                    const uint64_t* __restrict__ soff,
+                                                    const int32_t* __restrict__ nbs,
+                                                    uint8_t* __restrict__ blobs) {
+  __shared__ uint64_t sk[kMaxSpl];
+  const int g = blockIdx.x;
+  const uint64_t s0 = soff[g], S = soff[g + 1] - s0;
+  const uint32_t nb = (uint32_t)nbs[g], nspl = nb - 1;
+  uint8_t* blob = blobs + (size_t)g * kBlobStride;
+  ClsHeader* h = reinterpret_cast<ClsHeader*>(blob);
+  uint64_t* bk = reinterpret_cast<uint64_t*>(blob + kBlobKeys);
+  uint32_t* bp = reinterpret_cast<uint32_t*>(blob + kBlobPos);
+  uint16_t* lut = reinterpret_cast<uint16_t*>(blob + kBlobLut);
+  for (uint32_t i = threadIdx.x; i < nspl; i += blockDim.x) {
+    const uint64_t r = ((uint64_t)(i + 1) * S) / nb;
+    const uint64_t k = sorted_keys[s0 + r];
+    sk[i] = k;
+    bk[i] = k;
+    bp[i] = sorted_pos[s0 + r];
+  }
+  __syncthreads();
+  if (nspl == 0) {
+    if (threadIdx.x == 0) { h->lo = 0; h->hi = 0; h->nspl = 0; h->shift = 0; h->ncells = 0; h->pad = 0; }
+    return;
+  }
+  const uint64_t lo = sk[0], hi = sk[nspl - 1];
+  const int bits = lut_bits_for((int)nspl);
+  const int bl = bit_length64(hi - lo);
+  const uint32_t shift = bl > bits ? (uint32_t)(bl - bits) : 0u;
+  const uint32_t ncells = (uint32_t)((hi - lo) >> shift) + 1;
+  for (uint32_t c = threadIdx.x; c < ncells; c += blockDim.x)
+    lut[c] = (uint16_t)lower_bound_smem(sk, nspl, lo + ((uint64_t)c << shift));
+  if (threadIdx.x == 0) {
+    lut[ncells] = (uint16_t)nspl;
+    h->lo = lo; h->hi = hi; h->nspl = nspl; h->shift = shift; h->ncells = ncells; h->pad = 0;
+  }
+}
+
+// -------------------------------------------------------------------- K3
+// One CTA per chunk (<= kChunkTiles tiles of one segment).  Per tile:
+// classify every key, warp-aggregated shared histogram; tile_hist row =
+// exclusive prefix inside the chunk; chunk_tot = chunk histogram;
+// seg_hist += chunk histogram.
+template <int KIND, bool DIGIT>
+__global__ void __launch_bounds__(kThreads) k_hist(const uint64_t* __restrict__ src, SegMeta m,
+                                                   const uint8_t* __restrict__ blobs,
+                                                   const DigitCls* __restrict__ dcls, int nspl_cap,
+                                                   int nb_stride, uint32_t* __restrict__ tile_hist,
+                                                   uint32_t* __restrict__ chunk_tot,
+                                                   uint32_t* __restrict__ seg_hist,
+                                                   unsigned long long* __restrict__ minmax) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ int s_seg;
+  __shared__ unsigned long long s_min[kWarps], s_max[kWarps];
+  const uint64_t c = blockIdx.x;
+  if (threadIdx.x == 0) s_seg = upper_bound_u64(m.chunk_prefix, m.nseg + 1, c) - 1;
+  __syncthreads();
+  const int s = s_seg;
+  const uint64_t seg_off = m.off[s], seg_len = m.len[s];
+  const uint64_t tile0 = (c - m.chunk_prefix[s]) * kChunkTiles;
+  const uint64_t seg_tiles = m.tile_prefix[s + 1] - m.tile_prefix[s];
+  const int ntiles = (int)min((uint64_t)kChunkTiles, seg_tiles - tile0);
+  uint32_t* hist = reinterpret_cast<uint32_t*>(smem);
+  uint32_t* run = hist + nb_stride;
+  uint8_t* clsmem = smem + (size_t)8 * nb_stride;
+  const int cls = m.cls[s];
+  TreeView tv;
+  DigitView dv;
+  int64_t posbase = 0;
+  if constexpr (DIGIT) {
+    dv.c = dcls[cls];
+  } else {
+    tv = load_tree(blobs + (size_t)cls * kBlobStride, clsmem, nspl_cap);
+    posbase = m.posbase[cls];
+  }
+  for (int b = threadIdx.x; b < nb_stride; b += kThreads) run[b] = 0;
+  const int lane = threadIdx.x & 31;
+  unsigned long long mn = ~0ULL, mx = 0;
+  for (int it = 0; it < ntiles; ++it) {
+    for (int b = threadIdx.x; b < nb_stride; b += kThreads) hist[b] = 0;
+    __syncthreads();
+    const uint64_t tl = tile0 + it;
+    const uint64_t tstart = tl * kTile;
+    const uint32_t tcount = (uint32_t)min((uint64_t)kTile, seg_len - tstart);
+    const uint64_t base = seg_off + tstart;
+    uint64_t keys[kItems];
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+      const uint32_t e = i * kThreads + threadIdx.x;
+      keys[i] = e < tcount ? to_ordered<KIND>(ldg_stream(src + base + e)) : 0;
+    }
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+      const uint32_t e = i * kThreads + threadIdx.x;
+      uint32_t b = kInvalid;
+      if (e < tcount) {
+        if constexpr (DIGIT) b = dv.classify(keys[i], 0);
+        else b = tv.classify(keys[i], (uint32_t)((int64_t)(base + e) + posbase));
+        if (minmax) { mn = min(mn, (unsigned long long)keys[i]); mx = max(mx, (unsigned long long)keys[i]); }
+      }
+      const uint32_t peers = __match_any_sync(0xffffffffu, b);
+      if (b != kInvalid && lane == __ffs(peers) - 1) atomicAdd(&hist[b], (uint32_t)__popc(peers));
+    }
+    __syncthreads();
+    const uint64_t tg = m.tile_prefix[s] + tl;
+    for (int b = threadIdx.x; b < nb_stride; b += kThreads) {
+      const uint32_t hv = hist[b];
+      tile_hist[tg * nb_stride + b] = run[b];
+      run[b] += hv;
+    }
+    __syncthreads();
+  }
+  for (int b = threadIdx.x; b < nb_stride; b += kThreads) {
+    const uint32_t v = run[b];
+    chunk_tot[c * nb_stride + b] = v;
+    if (v) atomicAdd(&seg_hist[(uint64_t)s * nb_stride + b], v);
+  }
+  if (minmax) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if (lane == 0) { s_min[threadIdx.x >> 5] = mn; s_max[threadIdx.x >> 5] = mx; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < kWarps; ++w) { mn = min(mn, s_min[w]); mx = max(mx, s_max[w]); }
+      atomicMin(&minmax[0], mn);
+      atomicMax(&minmax[1], mx);
+    }
+  }
+}
+
+// -------------------------------------------------------------------- K4
+// Exclusive scan of the chunk histograms along each segment's chunks.
+__global__ void k_chunk_scan(uint32_t* __restrict__ chunk_tot, SegMeta m, int nb_stride) {
+  const int s = blockIdx.x;
+  const uint64_t c0 = m.chunk_prefix[s], c1 = m.chunk_prefix[s + 1];
+  for (int b = threadIdx.x; b < nb_stride; b += blockDim.x) {
+    uint32_t run = 0;
+    uint64_t c = c0;
+    for (; c + 8 <= c1; c += 8) {
+      uint32_t v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = chunk_tot[(c + u) * nb_stride + b];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) { chunk_tot[(c + u) * nb_stride + b] = run; run += v[u]; }
+    }
+    for (; c < c1; ++c) {
+      const uint32_t v = chunk_tot[c * nb_stride + b];
+      chunk_tot[c * nb_stride + b] = run;
+      run += v;
+    }
+  }
+}
+
+// Output offset of every (source segment j, bucket b) cell of a group in
+// the simple-delivery order (g(b), j, b) (SURVEY §8 layout contract step 5).
+__global__ void __launch_bounds__(256) k_cell_base(const uint32_t* __restrict__ seg_hist, int nb_stride,
+                                                   GroupMeta gm, int r, uint64_t* __restrict__ pieces,
+                                                   uint64_t* __restrict__ cell_base) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint64_t* mtot = reinterpret_cast<uint64_t*>(smem);  // r entries
+  const int g = blockIdx.x;
+  const int first = gm.first[g], P = gm.nseg[g];
+  const uint64_t* bnd = gm.bnd + (size_t)g * (r + 1);
+  for (int idx = threadIdx.x; idx < P * r; idx += blockDim.x) {
+    const int j = idx / r, gg = idx % r;
+    const uint32_t* hrow = seg_hist + (uint64_t)(first + j) * nb_stride;
+    uint64_t sum = 0;
+    for (uint64_t b = bnd[gg]; b < bnd[gg + 1]; ++b) sum += hrow[b];
+    pieces[(uint64_t)(first + j) * r + gg] = sum;
+  }
+  __syncthreads();
+  for (int gg = threadIdx.x; gg < r; gg += blockDim.x) {
+    uint64_t run = 0;
+    for (int j = 0; j < P; ++j) {
+      uint64_t* p = pieces + (uint64_t)(first + j) * r + gg;
+      const uint64_t v = *p;
+      *p = run;
+      run += v;
+    }
+    mtot[gg] = run;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t acc = 0;
+    for (int gg = 0; gg < r; ++gg) { const uint64_t t = mtot[gg]; mtot[gg] = acc; acc += t; }
+  }
+  __syncthreads();
+  const uint64_t start = gm.dst_start[g];
+  for (int idx = threadIdx.x; idx < P * r; idx += blockDim.x) {
+    const int j = idx / r, gg = idx % r;
+    const uint32_t* hrow = seg_hist + (uint64_t)(first + j) * nb_stride;
+    uint64_t* crow = cell_base + (uint64_t)(first + j) * nb_stride;
+    uint64_t base = start + mtot[gg] + pieces[(uint64_t)(first + j) * r + gg];
+    for (uint64_t b = bnd[gg]; b < bnd[gg + 1]; ++b) { crow[b] = base; base += hrow[b]; }
+  }
+}
+
+// Digit partition: cell (s, d) starts at off[s] + sum of earlier digits.
+__global__ void k_digit_base(const uint32_t* __restrict__ seg_hist, int nb_stride, SegMeta m,
+                             uint64_t* __restrict__ cell_base) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= m.nseg) return;
+  uint64_t base = m.off[s];
+  for (int d = 0; d < nb_stride; ++d) {
+    cell_base[(uint64_t)s * nb_stride + d] = base;
+    base += seg_hist[(uint64_t)s * nb_stride + d];
+  }
+}
+
+// -------------------------------------------------------------------- K6
+// Stable scatter of one tile: warp-level ranks (match_any), per-warp
+// bucket counters, bucket-major reorder in shared memory, then coalesced
+// runs to dst.  Order inside a bucket = input order, so the output is the
+// stable (cell, position) order the reference's concatenations produce.
+template <int KIND, bool DIGIT, bool VALS>
+__global__ void __launch_bounds__(kThreads) k_scatter(const uint64_t* __restrict__ src,
+                                                      const uint64_t* __restrict__ src_vals,
+                                                      uint64_t* __restrict__ dst,
+                                                      uint64_t* __restrict__ dst_vals, SegMeta m,
+                                                      const uint8_t* __restrict__ blobs,
+                                                      const DigitCls* __restrict__ dcls,
+                                                      int nspl_cap, int nb_stride,
+                                                      const uint32_t* __restrict__ tile_hist,
+                                                      const uint32_t* __restrict__ chunk_tot,
+                                                      const uint64_t* __restrict__ cell_base) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ int s_seg;
+  __shared__ uint32_t s_scan[kWarps + 1];
+  // layout
+  uint64_t* keys_s = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* vals_s = keys_s + kTile;
+  int64_t* delta = reinterpret_cast<int64_t*>(smem + (VALS ? 16 : 8) * (size_t)kTile);
+  uint32_t* wh = reinterpret_cast<uint32_t*>(delta + nb_stride);
+  uint32_t* btot = wh + (size_t)kWarps * nb_stride;
+  uint16_t* bkt_s = reinterpret_cast<uint16_t*>(btot + nb_stride);
+  uint8_t* clsmem = reinterpret_cast<uint8_t*>(bkt_s + kTile);
+
+  const uint64_t t = blockIdx.x;
+  if (threadIdx.x == 0) s_seg = upper_bound_u64(m.tile_prefix, m.nseg + 1, t) - 1;
+  for (int i = threadIdx.x; i < kWarps * nb_stride; i += kThreads) wh[i] = 0;
+  __syncthreads();
+  const int s = s_seg;
+  const uint64_t tl = t - m.tile_prefix[s];
+  const uint64_t chunk = m.chunk_prefix[s] + tl / kChunkTiles;
+  const uint64_t tstart = tl * kTile;
+  const uint32_t tcount = (uint32_t)min((uint64_t)kTile, m.len[s] - tstart);
+  const uint64_t base = m.off[s] + tstart;
+  const int cls = m.cls[s];
+  TreeView tv;
+  DigitView dv;
+  int64_t posbase = 0;
+  if constexpr (DIGIT) {
+    dv.c = dcls[cls];
+  } else {
+    tv = load_tree(blobs + (size_t)cls * kBlobStride, clsmem, nspl_cap);
+    posbase = m.posbase[cls];
+    __syncthreads();
+  }
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t lt = lanemask_lt();
+  uint64_t keys[kItems];
+  uint64_t vals[VALS ? kItems : 1];
+  uint32_t pk[kItems];
+#pragma unroll
+  for (int i = 0; i < kItems; ++i) {
+    const uint32_t e = w * (kItems * 32) + i * 32 + lane;
+    keys[i] = e < tcount ? to_ordered<KIND>(ldg_stream(src + base + e)) : 0;
+    if constexpr (VALS) vals[i] = e < tcount ? ldg_stream(src_vals + base + e) : 0;
+  }
+  uint32_t* whw = wh + (size_t)w * nb_stride;
+#pragma unroll
+  for (int i = 0; i < kItems; ++i) {
+    const uint32_t e = w * (kItems * 32) + i * 32 + lane;
+    uint32_t b = kInvalid;
+    if (e < tcount) {
+      if constexpr (DIGIT) b = dv.classify(keys[i], 0);
+      else b = tv.classify(keys[i], (uint32_t)((int64_t)(base + e) + posbase));
+    }
+    const uint32_t peers = __match_any_sync(0xffffffffu, b);
+    uint32_t cnt = 0;
+    if (b != kInvalid) {
+      cnt = whw[b];
+      pk[i] = (b << 16) | (cnt + __popc(peers & lt));
+    } else {
+      pk[i] = kInvalid;
+    }
+    __syncwarp();
+    if (b != kInvalid && lane == __ffs(peers) - 1) whw[b] = cnt + __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < nb_stride; b += kThreads) {
+    uint32_t acc = 0;
+#pragma unroll
+    for (int ww = 0; ww < kWarps; ++ww) {
+      const uint32_t v = wh[(size_t)ww * nb_stride + b];
+      wh[(size_t)ww * nb_stride + b] = acc;
+      acc += v;
+    }
+    btot[b] = acc;
+  }
+  __syncthreads();
+  block_excl_scan<kThreads>(btot, nb_stride, s_scan);
+  const uint32_t* th = tile_hist + t * nb_stride;
+  const uint32_t* ct = chunk_tot + chunk * nb_stride;
+  const uint64_t* cb = cell_base + (uint64_t)s * nb_stride;
+  for (int b = threadIdx.x; b < nb_stride; b += kThreads)
+    delta[b] = (int64_t)(cb[b] + ct[b] + th[b]) - (int64_t)btot[b];
+#pragma unroll
+  for (int i = 0; i < kItems; ++i) {
+    if (pk[i] != kInvalid) {
+      const uint32_t b = pk[i] >> 16;
+      const uint32_t slot = btot[b] + whw[b] + (pk[i] & 0xFFFFu);
+      keys_s[slot] = keys[i];
+      bkt_s[slot] = (uint16_t)b;
+      if constexpr (VALS) vals_s[slot] = vals[i];
+    }
+  }
+  __syncthreads();
+  for (uint32_t j = threadIdx.x; j < tcount; j += kThreads) {
+    const int64_t d = delta[bkt_s[j]] + (int64_t)j;
+    dst[d] = keys_s[j];
+    if constexpr (VALS) dst_vals[d] = vals_s[j];
+  }
+}
+
+// -------------------------------------------------------------------- K7
+__global__ void k_final_ranges(FinalRangeMeta fm, const uint8_t* __restrict__ blobs,
+                               const unsigned long long* __restrict__ minmax,
+                               DigitCls* __restrict__ out) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= fm.nseg) return;
+  const uint8_t* blob = blobs + (size_t)fm.cls[s] * kBlobStride;
+  const uint64_t* bk = reinterpret_cast<const uint64_t*>(blob + kBlobKeys);
+  const uint64_t b0 = fm.b0[s], b1 = fm.b1[s];
+  const uint64_t nb = (uint64_t)fm.nb[s];
+  uint64_t lo = b0 == 0 ? (uint64_t)minmax[0] : bk[b0 - 1];
+  uint64_t hi = b1 >= nb ? (uint64_t)minmax[1] : bk[b1 - 1];
+  if (hi < lo) hi = lo;
+  const int bl = bit_length64(hi - lo);
+  const int nbits = fm.nbits;
+  DigitCls d;
+  d.lo = lo;
+  d.hi = hi;
+  d.shift = bl > nbits ? (uint32_t)(bl - nbits) : 0u;
+  d.nb = 1u << nbits;
+  out[s] = d;
+}
+
+// -------------------------------------------------------------------- K9
+constexpr int kSortThreads = 512;
+constexpr int kSortWarps = kSortThreads / 32;
+constexpr int kSortCap = AMS_SMEM_SORT_CAP;
+constexpr int kSortItems = kSortCap / kSortThreads;  // per-warp iterations
+constexpr int kRadix = 256;
+
+__device__ __forceinline__ void block_minmax(uint64_t& mn, uint64_t& mx, uint64_t* s2) {
+  // s2: 2*kSortWarps scratch
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    mn = min(mn, (uint64_t)__shfl_xor_sync(0xffffffffu, mn, o));
+    mx = max(mx, (uint64_t)__shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) { s2[w] = mn; s2[kSortWarps + w] = mx; }
+  __syncthreads();
+  mn = s2[0]; mx = s2[kSortWarps];
+  for (int i = 1; i < kSortWarps; ++i) { mn = min(mn, s2[i]); mx = max(mx, s2[kSortWarps + i]); }
+  __syncthreads();
+}
+
+// One CTA per cell.  Cells larger than the shared-memory capacity are
+// copied when they hold one key value, otherwise recorded for another
+// partition round.  The sort is an LSD radix sort over the bits that vary
+// inside the cell (key - min), 8 bits per pass, each pass a stable
+// counting sort with match_any warp ranks — stable end to end.
+template <int KIND_OUT, bool VALS>
+__global__ void __launch_bounds__(kSortThreads, 1)
+    k_smem_sort(const uint64_t* __restrict__ src, const uint64_t* __restrict__ src_vals,
+                uint64_t* __restrict__ out, uint64_t* __restrict__ out_vals, CellSource cs,
+                OverflowRec* __restrict__ ovf, unsigned int* __restrict__ ovf_count) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ uint64_t s_mm[2 * kSortWarps];
+  __shared__ uint32_t s_scan[kSortWarps + 1];
+  uint64_t* kA = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* kB = kA + kSortCap;
+  uint16_t* iA = reinterpret_cast<uint16_t*>(kB + kSortCap);
+  uint16_t* iB = iA + kSortCap;
+  uint32_t* wh = reinterpret_cast<uint32_t*>(iB + kSortCap);  // [kSortWarps][kRadix]
+  uint32_t* btot = wh + kSortWarps * kRadix;
+
+  const uint64_t cid = blockIdx.x;
+  uint64_t off, count;
+  bool constant = false;
+  if (cs.mode == 0) {
+    off = cs.cell_base[cid];
+    count = cs.cell_cnt[cid];
+    constant = cs.dcls[cid >> cs.nbits].shift == 0;
+  } else {
+    off = cs.seg_off[cid];
+    count = cs.seg_len[cid];
+  }
+  if (count == 0) return;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (count > (uint64_t)kSortCap) {
+    uint64_t mn = ~0ULL, mx = 0;
+    for (uint64_t i = threadIdx.x; i < count; i += kSortThreads) {
+      const uint64_t k = src[off + i];
+      mn = min(mn, k); mx = max(mx, k);
+    }
+    block_minmax(mn, mx, s_mm);
+    (void)constant;
+    if (mn == mx) {
+      const uint64_t ko = from_ordered<KIND_OUT>(mn);
+      for (uint64_t i = threadIdx.x; i < count; i += kSortThreads) {
+        out[off + i] = ko;
+        if constexpr (VALS) out_vals[off + i] = src_vals[off + i];
+      }
+    } else if (threadIdx.x == 0) {
+      const unsigned int slot = atomicAdd(ovf_count, 1u);
+      OverflowRec r; r.off = off; r.count = count; r.lo = mn; r.hi = mx;
+      ovf[slot] = r;
+    }
+    return;
+  }
+  const uint32_t n = (uint32_t)count;
+  uint64_t mn = ~0ULL, mx = 0;
+  for (uint32_t i = threadIdx.x; i < n; i += kSortThreads) {
+    const uint64_t k = src[off + i];
+    kA[i] = k;
+    iA[i] = (uint16_t)i;
+    mn = min(mn, k); mx = max(mx, k);
+  }
+  block_minmax(mn, mx, s_mm);
+  if (mn != mx) {
+    const int bits = bit_length64(mx - mn);
+    const int passes = (bits + 7) / 8;
+    const uint32_t chunk = ((n + kSortWarps - 1) / kSortWarps + 31) & ~31u;
+    const uint32_t lt = lanemask_lt();
+    uint32_t* whw = wh + w * kRadix;
+    for (int p = 0; p < passes; ++p) {
+      const int sh = 8 * p;
+      for (int i = threadIdx.x; i < kSortWarps * kRadix; i += kSortThreads) wh[i] = 0;
+      __syncthreads();
+      uint32_t pk[kSortItems];
+#pragma unroll
+      for (int it = 0; it < kSortItems; ++it) {
+        const uint32_t e = w * chunk + it * 32 + lane;
+        const bool valid = (it * 32 < (int)chunk) && e < n;
+        const uint32_t d = valid ? (uint32_t)(((kA[e] - mn) >> sh) & 255) : kInvalid;
+        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        uint32_t cnt = 0;
+        if (valid) { cnt = whw[d]; pk[it] = (d << 16) | (cnt + __popc(peers & lt)); }
+        else pk[it] = kInvalid;
+        __syncwarp();
+        if (valid && lane == __ffs(peers) - 1) whw[d] = cnt + __popc(peers);
+        __syncwarp();
+      }
+      __syncthreads();
+      for (int d = threadIdx.x; d < kRadix; d += kSortThreads) {
+        uint32_t acc = 0;
+#pragma unroll
+        for (int ww = 0; ww < kSortWarps; ++ww) {
+          const uint32_t v = wh[ww * kRadix + d];
+          wh[ww * kRadix + d] = acc;
+          acc += v;
+        }
+        btot[d] = acc;
+      }
+      __syncthreads();
+      block_excl_scan<kSortThreads>(btot, kRadix, s_scan);
+#pragma unroll
+      for (int it = 0; it < kSortItems; ++it) {
+        if (pk[it] != kInvalid) {
+          const uint32_t e = w * chunk + it * 32 + lane;
+          const uint32_t d = pk[it] >> 16;
+          const uint32_t slot = btot[d] + whw[d] + (pk[it] & 0xFFFFu);
+          kB[slot] = kA[e];
+          iB[slot] = iA[e];
+        }
+      }
+      __syncthreads();
+      uint64_t* tk = kA; kA = kB; kB = tk;
+      uint16_t* ti = iA; iA = iB; iB = ti;
+    }
+  }
+  for (uint32_t i = threadIdx.x; i < n; i += kSortThreads) {
+    out[off + i] = from_ordered<KIND_OUT>(kA[i]);
+    if constexpr (VALS) out_vals[off + i] = src_vals[off + iA[i]];
+  }
+}
+
+template <int FROM, int TO>
+__global__ void k_map_keys(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst, uint64_t n) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    dst[i] = from_ordered<TO>(to_ordered<FROM>(src[i]));
+}
+
+}  // namespace
+
+// ======================================================================
+// Launchers
+// ======================================================================
+
+#define AMS_KIND_DISPATCH(kind, K, ...)          \
+  switch (kind) {                                \
+    case AMS_KEY_I64: { constexpr int K = AMS_KEY_I64; __VA_ARGS__; } break; \
+    case AMS_KEY_F64: { constexpr int K = AMS_KEY_F64; __VA_ARGS__; } break; \
+    default: { constexpr int K = AMS_KEY_U64; __VA_ARGS__; } break;          \
+  }
+
+cudaError_t launch_gather_sample(cudaStream_t st, const void* src, int kind, const uint64_t* idx,
+                                 const uint64_t* gpos, uint64_t n, uint64_t* out_keys,
+                                 uint32_t* out_pos) {
+  if (n == 0) return cudaSuccess;
+  const unsigned blocks = (unsigned)((n + 255) / 256);
+  AMS_KIND_DISPATCH(kind, K, k_gather_sample<K><<<blocks, 256, 0, st>>>(
+      static_cast<const uint64_t*>(src), idx, gpos, n, out_keys, out_pos));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sample_rank(cudaStream_t st, int ngroups, uint64_t max_s, const uint64_t* keys,
+                               const uint32_t* pos, const uint64_t* soff, uint64_t* sorted_keys,
+                               uint32_t* sorted_pos) {
+  if (ngroups == 0 || max_s == 0) return cudaSuccess;
+  dim3 grid((unsigned)((max_s + 255) / 256), (unsigned)ngroups);
+  k_sample_rank<<<grid, 256, 0, st>>>(keys, pos, soff, sorted_keys, sorted_pos);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_build_cls(cudaStream_t st, int ngroups, const uint64_t* sorted_keys,
+                             const uint32_t* sorted_pos, const uint64_t* soff, const int32_t* nbs,
+                             uint8_t* blobs) {
+  if (ngroups == 0) return cudaSuccess;
+  k_build_cls<<<ngroups, 1024, 0, st>>>(sorted_keys, sorted_pos, soff, nbs, blobs);
+  return cudaGetLastError();
+}
+
+size_t hist_smem_bytes(int nb_stride, int nspl_cap, int cells_cap, bool digit) {
+  return (size_t)8 * nb_stride + (digit ? 0 : tree_smem_bytes(nspl_cap, cells_cap));
+}
+
+cudaError_t launch_hist(cudaStream_t st, const void* src, int kind, bool digit, const SegMeta& m,
+                        uint64_t nchunks, const uint8_t* blobs, const DigitCls* dcls, int nspl_cap,
+                        int cells_cap, int nb_stride, uint32_t* tile_hist, uint32_t* chunk_tot,
+                        uint32_t* seg_hist, unsigned long long* minmax) {
+  if (nchunks == 0) return cudaSuccess;
+  const size_t smem = hist_smem_bytes(nb_stride, nspl_cap, cells_cap, digit);
+  const uint64_t* s = static_cast<const uint64_t*>(src);
+  cudaError_t e = cudaSuccess;
+  if (digit) {
+    auto fn = k_hist<AMS_KEY_U64, true>;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    fn<<<(unsigned)nchunks, kThreads, smem, st>>>(s, m, blobs, dcls, nspl_cap, nb_stride,
+                                                   tile_hist, chunk_tot, seg_hist, minmax);
+  } else {
+    AMS_KIND_DISPATCH(kind, K, {
+      auto fn = k_hist<K, false>;
+      e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      fn<<<(unsigned)nchunks, kThreads, smem, st>>>(s, m, blobs, dcls, nspl_cap, nb_stride,
+                                                     tile_hist, chunk_tot, seg_hist, minmax);
+    });
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_chunk_scan(cudaStream_t st, uint32_t* chunk_tot, const SegMeta& m, int nb_stride) {
+  if (m.nseg == 0) return cudaSuccess;
+  const int threads = nb_stride < 1024 ? ((nb_stride + 31) / 32) * 32 : 1024;
+  k_chunk_scan<<<m.nseg, threads, 0, st>>>(chunk_tot, m, nb_stride);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cell_base(cudaStream_t st, const uint32_t* seg_hist, int nb_stride,
+                             const GroupMeta& gm, int ngroups, int r, uint64_t* pieces,
+                             uint64_t* cell_base) {
+  if (ngroups == 0) return cudaSuccess;
+  const size_t smem = sizeof(uint64_t) * (size_t)r;
+  k_cell_base<<<ngroups, 256, smem, st>>>(seg_hist, nb_stride, gm, r, pieces, cell_base);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_digit_base(cudaStream_t st, const uint32_t* seg_hist, int nb_stride,
+                              const SegMeta& m, uint64_t* cell_base) {
+  if (m.nseg == 0) return cudaSuccess;
+  k_digit_base<<<(m.nseg + 127) / 128, 128, 0, st>>>(seg_hist, nb_stride, m, cell_base);
+  return cudaGetLastError();
+}
+
+size_t scatter_smem_bytes(int nb_stride, int nspl_cap, int cells_cap, bool digit, bool vals) {
+  size_t b = (vals ? 16 : 8) * (size_t)kTile;       // keys (+vals)
+  b += 8 * (size_t)nb_stride;                       // delta
+  b += 4 * (size_t)kWarps * nb_stride;              // warp histograms
+  b += 4 * (size_t)nb_stride;                       // bucket totals
+  b += 2 * (size_t)kTile;                           // bucket ids
+  b = (b + 15) & ~(size_t)15;
+  if (!digit) b += tree_smem_bytes(nspl_cap, cells_cap);
+  return b;
+}
+
+cudaError_t launch_scatter(cudaStream_t st, const void* src, const void* src_vals, int kind,
+                           bool digit, void* dst, void* dst_vals, const SegMeta& m, uint64_t ntiles,
+                           const uint8_t* blobs, const DigitCls* dcls, int nspl_cap, int cells_cap,
+                           int nb_stride, const uint32_t* tile_hist, const uint32_t* chunk_tot,
+                           const uint64_t* cell_base) {
+  if (ntiles == 0) return cudaSuccess;
+  const bool vals = src_vals != nullptr;
+  const size_t smem = scatter_smem_bytes(nb_stride, nspl_cap, cells_cap, digit, vals);
+  const uint64_t* s = static_cast<const uint64_t*>(src);
+  const uint64_t* sv = static_cast<const uint64_t*>(src_vals);
+  uint64_t* d = static_cast<uint64_t*>(dst);
+  uint64_t* dv = static_cast<uint64_t*>(dst_vals);
+  cudaError_t e = cudaSuccess;
+#define AMS_SCATTER_GO(K, DG, V)                                                              \
+  {                                                                                           \
+    auto fn = k_scatter<K, DG, V>;                                                            \
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
+    if (e != cudaSuccess) return e;                                                           \
+    fn<<<(unsigned)ntiles, kThreads, smem, st>>>(s, sv, d, dv, m, blobs, dcls, nspl_cap,      \
+                                                  nb_stride, tile_hist, chunk_tot, cell_base); \
+  }
+  if (digit) {
+    if (vals) AMS_SCATTER_GO(AMS_KEY_U64, true, true) else AMS_SCATTER_GO(AMS_KEY_U64, true, false)
+  } else if (vals) {
+    AMS_KIND_DISPATCH(kind, K, AMS_SCATTER_GO(K, false, true))
+  } else {
+    AMS_KIND_DISPATCH(kind, K, AMS_SCATTER_GO(K, false, false))
+  }
+#undef AMS_SCATTER_GO
+  return cudaGetLastError();
+}
+
+cudaError_t launch_final_ranges(cudaStream_t st, const FinalRangeMeta& fm, const uint8_t* blobs,
+                                const unsigned long long* minmax, DigitCls* out) {
+  if (fm.nseg == 0) return cudaSuccess;
+  k_final_ranges<<<(fm.nseg + 127) / 128, 128, 0, st>>>(fm, blobs, minmax, out);
+  return cudaGetLastError();
+}
+
+size_t smem_sort_bytes() {
+  return (size_t)kSortCap * (8 + 8 + 2 + 2) + (size_t)4 * kSortWarps * kRadix + 4 * kRadix;
+}
+
+cudaError_t launch_smem_sort(cudaStream_t st, const void* src, const void* src_vals, void* out,
+                             void* out_vals, int kind_out, const CellSource& cs, uint64_t ncells,
+                             OverflowRec* ovf, unsigned int* ovf_count) {
+  if (ncells == 0) return cudaSuccess;
+  const size_t smem = smem_sort_bytes();
+  const uint64_t* s = static_cast<const uint64_t*>(src);
+  const uint64_t* sv = static_cast<const uint64_t*>(src_vals);
+  uint64_t* o = static_cast<uint64_t*>(out);
+  uint64_t* ov = static_cast<uint64_t*>(out_vals);
+  cudaError_t e = cudaSuccess;
+#define AMS_SORT_GO(K, V)                                                                 \
+  {                                                                                       \
+    auto fn = k_smem_sort<K, V>;                                                          \
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    if (e != cudaSuccess) return e;                                                       \
+    fn<<<(unsigned)ncells, kSortThreads, smem, st>>>(s, sv, o, ov, cs, ovf, ovf_count);    \
+  }
+  if (sv) {
+    AMS_KIND_DISPATCH(kind_out, K, AMS_SORT_GO(K, true))
+  } else {
+    AMS_KIND_DISPATCH(kind_out, K, AMS_SORT_GO(K, false))
+  }
+#undef AMS_SORT_GO
+  return cudaGetLastError();
+}
+
+cudaError_t launch_map_keys(cudaStream_t st, const void* src, void* dst, uint64_t n, int from,
+                            int to) {
+  if (n == 0) return cudaSuccess;
+  const uint64_t* s = static_cast<const uint64_t*>(src);
+  uint64_t* d = static_cast<uint64_t*>(dst);
+  const unsigned blocks = (unsigned)std::min<uint64_t>((n + 255) / 256, 148 * 16);
+#define AMS_MAP_GO(F)                                                              \
+  switch (to) {                                                                    \
+    case AMS_KEY_I64: k_map_keys<F, AMS_KEY_I64><<<blocks, 256, 0, st>>>(s, d, n); break; \
+    case AMS_KEY_F64: k_map_keys<F, AMS_KEY_F64><<<blocks, 256, 0, st>>>(s, d, n); break; \
+    default: k_map_keys<F, AMS_KEY_U64><<<blocks, 256, 0, st>>>(s, d, n); break;          \
+  }
+  switch (from) {
+    case AMS_KEY_I64: AMS_MAP_GO(AMS_KEY_I64) break;
+    case AMS_KEY_F64: AMS_MAP_GO(AMS_KEY_F64) break;
+    default: AMS_MAP_GO(AMS_KEY_U64) break;
+  }
+#undef AMS_MAP_GO
+  return cudaGetLastError();
+}
+
+}  // namespace ams

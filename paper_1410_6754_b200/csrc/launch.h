@@ -1,0 +1,86 @@
+// Host-callable kernel launchers (kernels.cu) and the small device-side
+// metadata structs they take by value.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "ams_device.cuh"
+
+namespace ams {
+
+// Segments (PEs) of one launch; arrays are device pointers.
+struct SegMeta {
+  const uint64_t* off;           // [nseg] start index in the source buffer
+  const uint64_t* len;           // [nseg]
+  const int32_t* cls;            // [nseg] classifier index
+  const uint64_t* tile_prefix;   // [nseg+1] first global tile of each segment
+  const uint64_t* chunk_prefix;  // [nseg+1] first global chunk of each segment
+  const int64_t* posbase;        // [ncls] tie-break position = index + posbase
+  int nseg;
+};
+
+// Groups of one level (contiguous runs of segments).
+struct GroupMeta {
+  const int32_t* first;       // [ngroups] first segment
+  const int32_t* nseg;        // [ngroups] member count
+  const uint64_t* bnd;        // [ngroups][r+1] plan boundaries
+  const uint64_t* dst_start;  // [ngroups] output start of the group
+};
+
+struct FinalRangeMeta {
+  const int32_t* cls;
+  const uint64_t* b0;
+  const uint64_t* b1;
+  const int32_t* nb;
+  int nseg;
+  int nbits;
+};
+
+// Work list of the shared-memory sort: mode 0 = cells of a digit
+// partition (cell id = seg << nbits | digit), mode 1 = explicit segments.
+struct CellSource {
+  int mode;
+  int nbits;
+  const uint64_t* cell_base;
+  const uint32_t* cell_cnt;
+  const DigitCls* dcls;
+  const uint64_t* seg_off;
+  const uint64_t* seg_len;
+};
+
+cudaError_t launch_gather_sample(cudaStream_t st, const void* src, int kind, const uint64_t* idx,
+                                 const uint64_t* gpos, uint64_t n, uint64_t* out_keys,
+                                 uint32_t* out_pos);
+cudaError_t launch_sample_rank(cudaStream_t st, int ngroups, uint64_t max_s, const uint64_t* keys,
+                               const uint32_t* pos, const uint64_t* soff, uint64_t* sorted_keys,
+                               uint32_t* sorted_pos);
+cudaError_t launch_build_cls(cudaStream_t st, int ngroups, const uint64_t* sorted_keys,
+                             const uint32_t* sorted_pos, const uint64_t* soff, const int32_t* nbs,
+                             uint8_t* blobs);
+size_t hist_smem_bytes(int nb_stride, int nspl_cap, int cells_cap, bool digit);
+cudaError_t launch_hist(cudaStream_t st, const void* src, int kind, bool digit, const SegMeta& m,
+                        uint64_t nchunks, const uint8_t* blobs, const DigitCls* dcls, int nspl_cap,
+                        int cells_cap, int nb_stride, uint32_t* tile_hist, uint32_t* chunk_tot,
+                        uint32_t* seg_hist, unsigned long long* minmax);
+cudaError_t launch_chunk_scan(cudaStream_t st, uint32_t* chunk_tot, const SegMeta& m, int nb_stride);
+cudaError_t launch_cell_base(cudaStream_t st, const uint32_t* seg_hist, int nb_stride,
+                             const GroupMeta& gm, int ngroups, int r, uint64_t* pieces,
+                             uint64_t* cell_base);
+cudaError_t launch_digit_base(cudaStream_t st, const uint32_t* seg_hist, int nb_stride,
+                              const SegMeta& m, uint64_t* cell_base);
+size_t scatter_smem_bytes(int nb_stride, int nspl_cap, int cells_cap, bool digit, bool vals);
+cudaError_t launch_scatter(cudaStream_t st, const void* src, const void* src_vals, int kind,
+                           bool digit, void* dst, void* dst_vals, const SegMeta& m, uint64_t ntiles,
+                           const uint8_t* blobs, const DigitCls* dcls, int nspl_cap, int cells_cap,
+                           int nb_stride, const uint32_t* tile_hist, const uint32_t* chunk_tot,
+                           const uint64_t* cell_base);
+cudaError_t launch_final_ranges(cudaStream_t st, const FinalRangeMeta& fm, const uint8_t* blobs,
+                                const unsigned long long* minmax, DigitCls* out);
+size_t smem_sort_bytes();
+cudaError_t launch_smem_sort(cudaStream_t st, const void* src, const void* src_vals, void* out,
+                             void* out_vals, int kind_out, const CellSource& cs, uint64_t ncells,
+                             OverflowRec* ovf, unsigned int* ovf_count);
+cudaError_t launch_map_keys(cudaStream_t st, const void* src, void* dst, uint64_t n, int from,
+                            int to);
+
+}  // namespace ams

@@ -1,0 +1,220 @@
+"""Level orchestration of AMS-sort on one B200 (host side, Python).
+
+One call of :meth:`AmsSorter.sort` runs the reference's ``ams_sort``
+(ams.py:271-313) with ``scheme="simple"`` over device-resident keys:
+
+    for each level lv, r in group_counts:                       ams.py:285
+        sample positions (C++ restatement of SeedSpec + random.sample)
+        K1 gather + K2 rank-by-counting splitters            ams.py:223-229
+        K3 classify + histograms  -> host (the level's one sync)  231-237
+        plan (C++ optimal_group_plan) + next member sizes        238, 78-80
+        K4 offsets + K6 stable scatter into (g, j, b) order      240-256
+    K7-K9 final per-PE stable sort                               310-312
+
+Positions are implicit (index in the group buffer): the tie-broken order
+(key, origin_pe, origin_pos) equals (key, position) inside every group
+(SURVEY F6), so no origin tags are stored on the device.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from .params import AmsParams, as_params, as_seed
+
+_KIND_OF_DTYPE = {torch.uint64: L.KEY_U64, torch.int64: L.KEY_I64, torch.float64: L.KEY_F64}
+_KIND_NAMES = {"u64": L.KEY_U64, "uint64": L.KEY_U64, "i64": L.KEY_I64, "int64": L.KEY_I64,
+               "f64": L.KEY_F64, "float64": L.KEY_F64}
+
+
+def key_kind_of(t: torch.Tensor, key_kind=None) -> int:
+    if key_kind is not None:
+        return _KIND_NAMES[key_kind] if isinstance(key_kind, str) else int(key_kind)
+    if t.dtype not in _KIND_OF_DTYPE:
+        raise ValueError(f"keys must be uint64, int64 or float64, got {t.dtype}")
+    return _KIND_OF_DTYPE[t.dtype]
+
+
+@dataclass
+class LevelRecord:
+    """Host-side facts of one level (all groups), for reports and parity."""
+
+    level: int
+    r: int
+    group_first: np.ndarray
+    group_npe: np.ndarray
+    sizes_before: np.ndarray
+    sample_size: np.ndarray       # per group: drawn
+    bucket_count: np.ndarray      # per group: br after shrinking (ams.py:228)
+    seg_hist: np.ndarray          # (P_total, nb_stride)
+    boundaries: np.ndarray        # (G, r+1)
+    loads: np.ndarray             # (G, r)
+    max_load: np.ndarray          # (G,)
+    load_budget: np.ndarray       # (G,)
+    new_sizes: np.ndarray         # (P_total,)
+    stats: np.ndarray | None      # (G, 4) exchange stats
+    splitters: list = field(default_factory=list)  # per group (keys, pos) if recorded
+
+    def report(self) -> dict:
+        """The per-level dict ams_sort returns (ams.py:296-308)."""
+        rep = {
+            "level": self.level + 1,
+            "r": self.r,
+            "max_load": int(self.new_sizes.max()),
+            "min_load": int(self.new_sizes.min()),
+            "sample_size": int(self.sample_size.max()),
+            "plan_load": int(self.max_load.max()),
+            "over_budget": int((self.max_load > self.load_budget).sum()),
+        }
+        if self.stats is not None:
+            for i, k in enumerate(("max_words", "max_msgs", "max_sent_msgs", "max_recv_msgs")):
+                rep[k] = int(self.stats[:, i].max())
+        return rep
+
+
+@dataclass
+class SortOutput:
+    keys: torch.Tensor
+    vals: torch.Tensor | None
+    pe_sizes: np.ndarray
+    levels: list
+    launches: int
+
+    @property
+    def reports(self) -> list:
+        return [lv.report() for lv in self.levels]
+
+
+def level_targets(n_g: np.ndarray, r: int, b: int, a: float):
+    """br and sample target per group (ams.py:224-225)."""
+    br = np.minimum(b * r, n_g + 1).astype(np.int64)
+    target = np.array([min(int(n), max(int(x) - 1, math.ceil(a * int(x))))
+                       for n, x in zip(n_g, br)], dtype=np.int64)
+    return br, target
+
+
+def load_budget(n_g: np.ndarray, r: int, eps_level: float) -> np.ndarray:
+    """ams.py:258."""
+    return np.array([math.ceil((1.0 + eps_level) * int(n) / r) for n in n_g], dtype=np.int64)
+
+
+class AmsSorter:
+    """Device-resident AMS-sort on one GPU (one process per GPU)."""
+
+    def __init__(self, device: int | torch.device | None = None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("AmsSorter needs a CUDA device (B200, sm_100a); there is no CPU path")
+        dev = torch.device("cuda", torch.cuda.current_device() if device is None else
+                           (device.index if isinstance(device, torch.device) else int(device)))
+        self.device = dev
+        self.ctx = L.Context(dev.index)
+        self._work: dict = {}
+
+    def close(self):
+        self.ctx.close()
+
+    # -- workspace ----------------------------------------------------------
+    def workspace(self, n: int, with_vals: bool):
+        key = (n, with_vals)
+        if key not in self._work:
+            self._work.clear()
+            mk = lambda: torch.empty(max(n, 1), dtype=torch.int64, device=self.device)
+            self._work[key] = ([mk(), mk()], [mk(), mk()] if with_vals else [None, None])
+        return self._work[key]
+
+    # -- main entry ---------------------------------------------------------
+    def sort(self, keys: torch.Tensor, pe_sizes, params: AmsParams, seed, vals=None, out=None,
+             out_vals=None, key_kind=None, record_splitters: bool = False,
+             with_stats: bool = True) -> SortOutput:
+        """Sort ``keys`` (1-D, PE-major: PE i owns the next ``pe_sizes[i]``
+        keys) exactly as ams_sort(scheme="simple") orders them; returns the
+        sorted keys (concatenation of per-PE outputs), per-PE sizes and
+        per-level records."""
+        params = as_params(params)
+        master, stream_id = as_seed(seed)
+        if keys.dim() != 1 or not keys.is_cuda:
+            raise ValueError("keys must be a 1-D CUDA tensor")
+        kind = key_kind_of(keys, key_kind)
+        sizes = np.asarray(pe_sizes, dtype=np.uint64)
+        p = len(sizes)
+        params.validate_for(p)                                       # ams.py:276
+        n = int(sizes.sum())
+        if n != keys.numel():
+            raise ValueError(f"pe_sizes sum to {n}, keys has {keys.numel()} elements")
+        if vals is not None and (vals.numel() != n or vals.element_size() != 8 or not vals.is_cuda):
+            raise ValueError("vals must be a CUDA tensor of n 8-byte values")
+        keys = keys.contiguous()
+        if vals is not None:
+            vals = vals.contiguous()
+        if out is None:
+            out = torch.empty_like(keys)
+        if vals is not None and out_vals is None:
+            out_vals = torch.empty_like(vals)
+        stream = torch.cuda.current_stream(self.device)
+        self.ctx.set_stream(stream.cuda_stream)
+        launches0 = self.ctx.launches
+        a = params.oversampling_for(n)                               # ams.py:278-280
+        eps_l = params.per_level_imbalance()
+        b = params.overpartition
+        work, work_v = self.workspace(n, vals is not None)
+        src, src_v, src_kind = keys, vals, kind
+        gf = np.zeros(1, np.int32)
+        gn = np.array([p], np.int32)
+        levels = []
+        for lv, r in enumerate(params.group_counts):
+            offs = np.zeros(p + 1, np.uint64)
+            np.cumsum(sizes, out=offs[1:])
+            G = len(gf)
+            n_g = np.add.reduceat(sizes, gf) if p else np.zeros(G, np.uint64)
+            br, target = level_targets(n_g, r, b, a)
+            idx, gpos, drawn = L.draw_sample_positions(master, stream_id, lv, gf, gn, target,
+                                                       sizes, offs[:-1])
+            nb = np.minimum(br, drawn.astype(np.int64) + 1)             # ams.py:228
+            if nb.max() > L.MAX_BUCKETS:
+                raise ValueError(f"{int(nb.max())} buckets exceed the supported {L.MAX_BUCKETS}")
+            soff = np.zeros(G + 1, np.uint64)
+            np.cumsum(drawn, out=soff[1:])
+            S = int(soff[-1])
+            s_keys = torch.empty(max(S, 1), dtype=torch.int64, device=self.device)
+            s_pos = torch.empty(max(S, 1), dtype=torch.int32, device=self.device)
+            self.ctx.level_sample(src, src_kind, idx, gpos, s_keys, s_pos)
+            self.ctx.level_splitters(s_keys, s_pos, soff, nb)
+            seg_group = np.repeat(np.arange(G, dtype=np.int32), gn)
+            posbase = -offs[gf].astype(np.int64)
+            nb_stride = int(nb.max())
+            hist = self.ctx.level_classify(src, src_kind, offs[:-1], sizes, seg_group, posbase,
+                                           nb_stride, track_minmax=(lv == 0))
+            bnd, loads, mx, new_sizes, stats = L.plan_level(gn, nb, r, hist, with_stats)
+            dst, dst_v = work[lv % 2], work_v[lv % 2]
+            self.ctx.level_scatter(src, src_v, src_kind, dst, dst_v, r, bnd, offs[gf])
+            rec = LevelRecord(lv, r, gf.copy(), gn.copy(), sizes.copy(), drawn, nb, hist, bnd,
+                              loads, mx, load_budget(n_g, r, eps_l), new_sizes, stats)
+            if record_splitters:
+                rec.splitters = [self.ctx.read_splitters(g) for g in range(G)]
+            levels.append(rec)
+            src, src_v, src_kind = dst, dst_v, L.KEY_U64
+            sizes = new_sizes
+            step = gn // r
+            gf = (gf[:, None] + np.arange(r, dtype=np.int32)[None, :] * step[:, None]).reshape(-1)
+            gf = gf.astype(np.int32)
+            gn = np.repeat(step, r).astype(np.int32)
+        # Final local sort (ams.py:310-312).  Final PE t of last-level group g
+        # holds buckets [B_t, B_{t+1}) of g.
+        last = levels[-1]
+        k = len(params.group_counts)
+        offs = np.zeros(p + 1, np.uint64)
+        np.cumsum(sizes, out=offs[1:])
+        pe_group = np.repeat(np.arange(len(last.group_first), dtype=np.int32), last.group_npe)
+        t_local = np.arange(p) - last.group_first[pe_group]
+        b0 = last.boundaries[pe_group, t_local]
+        b1 = last.boundaries[pe_group, t_local + 1]
+        seg_nb = last.bucket_count[pe_group]
+        tmp, tmp_v = work[k % 2], work_v[k % 2]
+        self.ctx.final_sort(src, src_v, tmp, tmp_v, out, out_vals, kind, offs[:-1], sizes,
+                            pe_group, b0, b1, seg_nb)
+        return SortOutput(out, out_vals, sizes, levels, self.ctx.launches - launches0)
