@@ -1,0 +1,361 @@
+"""Benchmark of the B200 AMS-sort hot path (driver contract: one JSON line).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload cfg2|cfg1|cfg3|cfg4a|cfg4b|cfg4c|cfg4d]
+
+Metric (BASELINE.json): 64-bit keys sorted per second; `value` is the
+whole-job rate with keys resident in HBM, `e2e` the same sort through the
+host-buffer API (pinned H2D + sort + D2H each step).  A step = one full
+ams_sort of the workload (every level, the final local sort, and the one
+host sync per level the seeded sample streams need).
+
+--impl reference times the reference algorithm's CPU implementation — the
+numpy oracle port (the reference itself is pure Python and is not present on
+the GPU box) — on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "64-bit keys sorted/sec"
+UNIT = "keys/s"
+
+WORKLOADS = {
+    "cfg1": dict(desc="CPU-reference workload: n=2^20 uint64 (reference generate_input seed 0), "
+                      "p=16, (16,), a=16, eps=0.1",
+                 log2n=20, p=16, groups=(16,), a=16.0, eps=0.1, seed=0, gen="reference", dtype="u64"),
+    "cfg2": dict(desc="Single B200: n=2^28 uint64 uniform (default_rng(1)), p=64 PEs, (8,8), eps=0.1",
+                 log2n=28, p=64, groups=(8, 8), a=None, eps=0.1, seed=1, gen="uniform", dtype="u64"),
+    "cfg3": dict(desc="n=2^30 float64 uniform [0,1) (default_rng(2)), p=256, (8,32), eps=0.1",
+                 log2n=30, p=256, groups=(8, 32), a=None, eps=0.1, seed=2, gen="float01", dtype="f64"),
+    "cfg4a": dict(desc="n=2^30 uint64 Zipf(1.1) over 2^10 values, p=256, (8,32)", log2n=30, p=256,
+                  groups=(8, 32), a=None, eps=0.1, seed=4, gen="zipf", dtype="u64"),
+    "cfg4b": dict(desc="n=2^30 uint64 sorted, p=256, (8,32)", log2n=30, p=256, groups=(8, 32),
+                  a=None, eps=0.1, seed=4, gen="sorted", dtype="u64"),
+    "cfg4c": dict(desc="n=2^30 uint64 reverse sorted, p=256, (8,32)", log2n=30, p=256,
+                  groups=(8, 32), a=None, eps=0.1, seed=4, gen="reverse", dtype="u64"),
+    "cfg4d": dict(desc="n=2^30 uint64 all equal (42), p=256, (8,32)", log2n=30, p=256,
+                  groups=(8, 32), a=None, eps=0.1, seed=4, gen="equal", dtype="u64"),
+}
+
+
+def gen_keys(w: dict, log2n: int) -> np.ndarray:
+    from oracle import ams_oracle as O  # input generators only (not the measured path)
+    n = 1 << log2n
+    g = w["gen"]
+    if g == "reference":
+        return O.reference_uniform_input(w["p"], n // w["p"], w["seed"])
+    if g == "uniform":
+        return np.random.default_rng(w["seed"]).integers(0, 2**64, n, dtype=np.uint64)
+    if g == "float01":
+        return np.random.default_rng(w["seed"]).random(n)
+    if g == "zipf":
+        return O.zipf_keys(n, w["seed"])
+    if g == "sorted":
+        return np.arange(n, dtype=np.uint64)
+    if g == "reverse":
+        return (n - 1 - np.arange(n, dtype=np.int64)).astype(np.uint64)
+    if g == "equal":
+        return np.full(n, 42, dtype=np.uint64)
+    raise ValueError(g)
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ------------------------------------------------------------------ clocks
+_REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+            0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+            0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+            0x100: "display_clock_setting"}
+
+
+class ClockSampler:
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], None, set()
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 3:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+                mask = int(parts[2], 16)
+            except ValueError:
+                continue
+            for bit, name in _REASONS.items():
+                if mask & bit and name != "gpu_idle":
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ CPU arms
+def cpu_port_rate(w: dict, budget_s: float = 20.0):
+    """The oracle port (numpy restatement of the reference algorithm) on a
+    bounded sample of the workload: same p, group counts, a-rule, b, eps;
+    n scaled down.  Returns (keys/s, sample description)."""
+    from oracle import ams_oracle as O
+    log2n = min(w["log2n"], 22)
+    keys = gen_keys(dict(w, gen="uniform" if w["gen"] == "reference" else w["gen"]), log2n)
+    if w["dtype"] == "f64":
+        keys = O.f64_to_ordered_u64(keys)
+    n = len(keys)
+    p = w["p"]
+    sizes = [n // p] * p
+    reps, t_tot = 0, 0.0
+    while True:
+        t0 = time.perf_counter()
+        res = O.ams_sort(keys, sizes, w["groups"], w["a"], 16, w["eps"], w["seed"], "algo/rep0",
+                         with_stats=False)
+        t_tot += time.perf_counter() - t0
+        reps += 1
+        if t_tot > budget_s / 2 or reps >= 3:
+            break
+    assert np.array_equal(res.keys, np.sort(keys))
+    sample = (f"numpy oracle port of ams_sort(scheme=simple), n=2^{log2n} (reduced from "
+              f"2^{w['log2n']}), p={p}, groups={w['groups']}, {reps} rep(s), 1 thread")
+    return n * reps / t_tot, sample
+
+
+def reference_arm(args, w):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    rate, sample = cpu_port_rate(w)
+    line = {
+        "metric": METRIC, "value": rate, "unit": UNIT, "impl": "reference",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": None, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": w["dtype"], "data": "synthetic",
+        "config": {"workload": args.workload, "desc": w["desc"], "groups": list(w["groups"]),
+                   "p": w["p"]},
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": 1, "kind": "port",
+                         "sample": sample, "host_cpus": os.cpu_count()},
+        "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ GPU arm
+def verify_device(torch, out, keys_dev, pe_sizes, eps, p, kind):
+    """Cheap full-size checks: non-decreasing, same multiset checksum, size
+    bound.  (Bit-exact parity vs numpy.sort is in tests/test_gpu_parity.py.)"""
+    flip = torch.tensor(-(2**63), dtype=torch.int64, device=out.device)
+    o = out.view(torch.int64)
+    if kind == "f64":
+        # ordered encoding of float64 bits
+        neg = o < 0
+        o = torch.where(neg, ~o, o ^ flip)
+    o = o ^ flip  # unsigned order -> signed order
+    ok_sorted = bool((o[1:] >= o[:-1]).all().item())
+    ok_sum = int(out.view(torch.int64).sum().item()) == int(keys_dev.view(torch.int64).sum().item())
+    n = out.numel()
+    ok_bound = int(max(pe_sizes)) <= (1 + eps) * n / p
+    return ok_sorted and ok_sum, ok_bound
+
+
+def ours_arm(args, w):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        raise SystemExit("multi-GPU bench: see DESIGN.md (round 1 measures N=1)")
+    torch.cuda.set_device(local)
+    from paper_1410_6754_b200 import AmsParams, SeedSpec
+    from paper_1410_6754_b200.api import get_sorter
+
+    log2n = w["log2n"]
+    n = 1 << log2n
+    p = w["p"]
+    keys_h = gen_keys(w, log2n)
+    kt_host = torch.from_numpy(keys_h.view(np.int64) if keys_h.dtype == np.uint64 else keys_h)
+    keys_dev = kt_host.to("cuda")
+    kind = w["dtype"]
+    params = AmsParams(tuple(w["groups"]), w["a"], 16, w["eps"])
+    seed = SeedSpec(w["seed"], "algo/rep0")
+    sizes = [n // p] * p
+    sorter = get_sorter(local)
+    ctx = sorter.ctx
+    out = torch.empty_like(keys_dev)
+
+    def step():
+        return sorter.sort(keys_dev, sizes, params, seed, out=out, key_kind=kind, with_stats=False)
+
+    for _ in range(max(args.warmup, 0)):
+        res = step()
+    torch.cuda.synchronize()
+    ctx.set_timing(True)
+    ctx.reset_stats()
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = ctx.launches
+    stream = torch.cuda.current_stream()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        res = step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    elapsed_ms = ev0.elapsed_time(ev1)
+    launches = ctx.launches - launches0
+    stats = ctx.kernel_stats()
+    ctx.set_timing(False)
+    fstats = ctx.final_sort_stats()
+    ms_per_step = elapsed_ms / args.steps
+    value = n / (ms_per_step / 1e3)
+    ok_sorted, ok_bound = verify_device(torch, out, keys_dev, res.pe_sizes, w["eps"], p, kind)
+
+    peak, peak_src = measured_peak()
+    # dominant kernel = largest share of device time in the timed region
+    dom = max(stats.items(), key=lambda kv: kv[1][0])
+    dname, (dms, dbytes, dlaunch) = dom
+    achieved = dbytes / (dms / 1e3) / 1e9 if dms > 0 else 0.0
+    total_kernel_ms = sum(v[0] for v in stats.values())
+    k = len(w["groups"])
+    b_hbm = 2 * 8 * n * (k + 1)
+    t_roof_ms = b_hbm / (peak * 1e9) * 1e3
+    roofline = {
+        "bound": "hbm", "kernel": dname, "achieved": achieved, "peak": peak, "unit": "GB/s",
+        "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+        "bytes_per_launch": dbytes / max(dlaunch, 1), "avg_launch_ms": dms / max(dlaunch, 1),
+        "share_of_step": dms / max(total_kernel_ms, 1e-9),
+        "step": {"algorithmic_bytes": b_hbm, "t_roof_ms": t_roof_ms,
+                 "frac": t_roof_ms / ms_per_step,
+                 "t_roof_ms_8TBps": b_hbm / 8.0e12 * 1e3},
+    }
+    kernels = {name: {"ms_per_step": v[0] / args.steps, "GBps": (v[1] / (v[0] / 1e3) / 1e9) if v[0] else None,
+                      "launches_per_step": v[2] / args.steps}
+               for name, v in stats.items() if v[2]}
+
+    # --- end to end through the host-buffer path (pinned H2D + sort + D2H)
+    e2e = None
+    if not args.no_e2e:
+        h_in = kt_host.pin_memory()
+        h_out = torch.empty_like(h_in).pin_memory()
+        d_in = torch.empty_like(keys_dev)
+
+        def e2e_step():
+            d_in.view(torch.int64).copy_(h_in.view(torch.int64), non_blocking=True)
+            r = sorter.sort(d_in, sizes, params, seed, out=out, key_kind=kind, with_stats=False)
+            h_out.view(torch.int64).copy_(out.view(torch.int64), non_blocking=True)
+            return r
+
+        e2e_step()
+        torch.cuda.synchronize()
+        ke = max(1, min(args.steps, 5))
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        e0.record()
+        for _ in range(ke):
+            e2e_step()
+        e1.record()
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        ok_e2e = bool(np.array_equal(h_out.numpy().view(np.uint64)[:1024],
+                                     out.view(torch.int64)[:1024].cpu().numpy().view(np.uint64)))
+        e2e = {"value": n * ke / wall, "unit": UNIT, "h2d_bytes_per_step": 8 * n,
+               "d2h_bytes_per_step": 8 * n, "ms_per_step": wall * 1e3 / ke,
+               "device_ms_per_step": e0.elapsed_time(e1) / ke, "verified": ok_e2e}
+
+    cpu = None
+    if not args.no_cpu_baseline and rank == 0:
+        rate, sample = cpu_port_rate(w)
+        cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample,
+               "host_cpus": os.cpu_count()}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": kind, "data": "synthetic",
+        "config": {"workload": args.workload, "desc": w["desc"], "n": n, "p": p,
+                   "groups": list(w["groups"]), "eps": w["eps"], "a": w["a"], "b": 16,
+                   "scheme": "simple", "sample_mode": "parity (reference seeded streams)",
+                   "l2": "inputs (8 B x n) larger than the 126 MB L2 between steps",
+                   "parallelism": f"{p} PEs on {world} GPU(s)"},
+        "verified": {"sorted_and_checksum": ok_sorted, "pe_size_bound": ok_bound},
+        "gpu_launches": launches, "launches_per_step": launches / args.steps,
+        "roofline": roofline, "kernels": kernels, "final_sort_cells": fstats, "clocks": clk,
+        "e2e": e2e, "cpu_baseline": cpu,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default=None, choices=sorted(WORKLOADS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.workload is None:
+        args.workload = "cfg2" if int(os.environ.get("WORLD_SIZE", args.gpus)) == 1 else "cfg3"
+    w = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        return reference_arm(args, w)
+    return ours_arm(args, w)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -97,6 +97,28 @@ int ams_ctx_set_stream(ams_ctx_t* ctx, void* stream);
 uint64_t ams_ctx_launches(const ams_ctx_t* ctx);
 int ams_ctx_sync(ams_ctx_t* ctx);
 
+/* Optional per-kernel-category timing: when enabled every launch is
+ * bracketed by CUDA events on the context's stream; stats give the summed
+ * device milliseconds, algorithmic bytes (keys/values read + written) and
+ * launch counts per category. */
+#define AMS_KCAT_SAMPLE 0
+#define AMS_KCAT_RANK 1
+#define AMS_KCAT_CLS 2
+#define AMS_KCAT_HIST 3
+#define AMS_KCAT_CHUNKSCAN 4
+#define AMS_KCAT_CELLBASE 5
+#define AMS_KCAT_SCATTER 6
+#define AMS_KCAT_RANGES 7
+#define AMS_KCAT_FHIST 8
+#define AMS_KCAT_FSCATTER 9
+#define AMS_KCAT_SMEMSORT 10
+#define AMS_KCAT_MAP 11
+#define AMS_KCAT_SCATTER_U 12
+#define AMS_NUM_KCAT 13
+int ams_ctx_set_timing(ams_ctx_t* ctx, int enable);
+int ams_ctx_kernel_stats(ams_ctx_t* ctx, double* ms, double* bytes, uint64_t* launches, int ncat);
+int ams_ctx_reset_stats(ams_ctx_t* ctx);
+
 /* K1 — sample gather (draw_sample, ams.py:157-175, data side):
  *   d_out_keys[i] = ordered(src[h_idx[i]]), d_out_pos[i] = h_gpos[i]. */
 int ams_level_sample(ams_ctx_t* ctx, const void* src, int key_kind, uint64_t count,
@@ -132,10 +154,16 @@ int ams_level_classify(ams_ctx_t* ctx, const void* src, int key_kind, int nseg,
  * delivery.py:151-180, exchange order simnet.py:324-325, receive concat
  * ams.py:252-256).  Uses the segments of the last ams_level_classify.
  * h_boundaries: [ngroups][r+1] plan boundaries; group g's output begins
- * at dst + h_group_dst_start[g].  vals may be NULL (keys only). */
+ * at dst + h_group_dst_start[g].  vals may be NULL (keys only).
+ * stable = 0 allows any order inside one tile's bucket run: valid only for
+ * the last level without values, where only PE membership matters (F7).
+ * Also derives the key bounds of the ngroups*r child groups; children
+ * [child_first, child_first + child_count) are this GPU's groups at the
+ * next level (all of them on a single GPU). */
 int ams_level_scatter(ams_ctx_t* ctx, const void* src, const void* src_vals, int key_kind,
                       void* dst, void* dst_vals, int r, const uint64_t* h_boundaries,
-                      const uint64_t* h_group_dst_start);
+                      const uint64_t* h_group_dst_start, int stable, int child_first,
+                      int child_count);
 
 /* Global min/max key seen by a track_minmax classify (ordered encoding);
  * the multi-rank driver all-reduces them and writes them back before the
@@ -144,15 +172,17 @@ int ams_get_minmax(ams_ctx_t* ctx, uint64_t out[2]);
 int ams_set_minmax(ams_ctx_t* ctx, const uint64_t in[2]);
 
 /* K7-K9 — final local sort (ams.py:310-312), stable by key.  Segment s
- * of `src` (transformed keys) is final PE s; its key range comes from the
- * last level's classifier h_seg_cls[s] and its bucket range
- * [h_seg_b0[s], h_seg_b1[s]) of h_seg_nb[s] buckets.  Large segments are
- * digit-partitioned into `tmp` and every cell sorted in shared memory
- * into `out` (keys mapped back to `key_kind`).  `src` is clobbered. */
+ * of `src` (ordered keys) is final PE s = child s of the last
+ * ams_level_scatter (its key bounds come from there).  Large segments are
+ * digit-partitioned into `tmp` and every cell sorted in shared memory into
+ * `out` (keys mapped back to `key_kind`).  `src` is clobbered. */
 int ams_final_sort(ams_ctx_t* ctx, void* src, void* src_vals, void* tmp, void* tmp_vals,
                    void* out, void* out_vals, int key_kind, int nseg, const uint64_t* h_seg_off,
-                   const uint64_t* h_seg_len, const int32_t* h_seg_cls, const uint64_t* h_seg_b0,
-                   const uint64_t* h_seg_b1, const int32_t* h_seg_nb);
+                   const uint64_t* h_seg_len);
+
+/* Cells of the final sort that needed another partition round / the LSD
+ * fallback, summed since the context was created: out = {overflow, fallback}. */
+int ams_final_sort_stats(ams_ctx_t* ctx, uint64_t out[2]);
 
 /* Plain copy with key mapping (used for the p == 1 / k == 0 edge and the
  * host-buffer end-to-end path). */

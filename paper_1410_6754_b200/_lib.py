@@ -19,6 +19,9 @@ KEY_U64, KEY_I64, KEY_F64 = 0, 1, 2
 TILE = 4096
 SMEM_SORT_CAP = 8192
 MAX_BUCKETS = 4096
+KCAT_NAMES = ("sample_gather", "sample_rank", "build_classifier", "level_hist", "chunk_scan",
+              "cell_base", "level_scatter", "final_ranges", "final_hist", "final_scatter",
+              "smem_sort", "map_keys", "level_scatter_unstable")
 
 _P = C.c_void_p
 _I = C.c_int
@@ -43,14 +46,18 @@ _SIGNATURES = {
     "ams_ctx_set_stream": (_I, [_P, _P]),
     "ams_ctx_launches": (_U64, [_P]),
     "ams_ctx_sync": (_I, [_P]),
+    "ams_ctx_set_timing": (_I, [_P, _I]),
+    "ams_ctx_kernel_stats": (_I, [_P, _P, _P, _P, _I]),
+    "ams_ctx_reset_stats": (_I, [_P]),
     "ams_level_sample": (_I, [_P, _P, _I, _U64, _P, _P, _P, _P]),
     "ams_level_splitters": (_I, [_P, _I, _P, _P, _P, _P]),
     "ams_read_splitters": (_I, [_P, _I, _P, _P, C.POINTER(_I)]),
     "ams_level_classify": (_I, [_P, _P, _I, _I, _P, _P, _P, _I, _P, _I, _I, _P]),
-    "ams_level_scatter": (_I, [_P, _P, _P, _I, _P, _P, _I, _P, _P]),
+    "ams_level_scatter": (_I, [_P, _P, _P, _I, _P, _P, _I, _P, _P, _I, _I, _I]),
+    "ams_final_sort_stats": (_I, [_P, _P]),
     "ams_get_minmax": (_I, [_P, _P]),
     "ams_set_minmax": (_I, [_P, _P]),
-    "ams_final_sort": (_I, [_P, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P, _P, _P, _P, _P]),
+    "ams_final_sort": (_I, [_P, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P]),
     "ams_map_keys": (_I, [_P, _P, _P, _U64, _I, _I]),
 }
 
@@ -225,6 +232,21 @@ class Context:
     def sync(self):
         check(lib.ams_ctx_sync(self.h))
 
+    def set_timing(self, enable: bool):
+        check(lib.ams_ctx_set_timing(self.h, int(bool(enable))))
+
+    def reset_stats(self):
+        check(lib.ams_ctx_reset_stats(self.h))
+
+    def kernel_stats(self) -> dict:
+        """{category: (device ms, algorithmic bytes, launches)} since reset."""
+        n = len(KCAT_NAMES)
+        ms = np.zeros(n, np.float64)
+        by = np.zeros(n, np.float64)
+        la = np.zeros(n, np.uint64)
+        check(lib.ams_ctx_kernel_stats(self.h, ms.ctypes.data, by.ctypes.data, la.ctypes.data, n))
+        return {name: (float(ms[i]), float(by[i]), int(la[i])) for i, name in enumerate(KCAT_NAMES)}
+
     def level_sample(self, src, kind, idx, gpos, out_keys, out_pos):
         idx, gpos = u64(idx), u64(gpos)
         check(lib.ams_level_sample(self.h, ptr(src), kind, len(idx), idx.ctypes.data,
@@ -251,10 +273,19 @@ class Context:
                                      nb_stride, int(bool(track_minmax)), out.ctypes.data))
         return out
 
-    def level_scatter(self, src, src_vals, kind, dst, dst_vals, r, boundaries, group_dst_start):
+    def level_scatter(self, src, src_vals, kind, dst, dst_vals, r, boundaries, group_dst_start,
+                      stable=True, child_first=0, child_count=None):
         b, d = u64(boundaries), u64(group_dst_start)
+        if child_count is None:
+            child_count = len(d) * r
         check(lib.ams_level_scatter(self.h, ptr(src), ptr(src_vals), kind, ptr(dst), ptr(dst_vals),
-                                    r, b.ctypes.data, d.ctypes.data))
+                                    r, b.ctypes.data, d.ctypes.data, int(bool(stable)),
+                                    int(child_first), int(child_count)))
+
+    def final_sort_stats(self):
+        out = np.zeros(2, np.uint64)
+        check(lib.ams_final_sort_stats(self.h, out.ctypes.data))
+        return {"overflow_cells": int(out[0]), "fallback_cells": int(out[1])}
 
     def get_minmax(self):
         out = np.zeros(2, np.uint64)
@@ -265,13 +296,10 @@ class Context:
         a = np.array([lo, hi], np.uint64)
         check(lib.ams_set_minmax(self.h, a.ctypes.data))
 
-    def final_sort(self, src, src_vals, tmp, tmp_vals, out, out_vals, key_kind, seg_off, seg_len,
-                   seg_cls, seg_b0, seg_b1, seg_nb):
-        so, sl, sc = u64(seg_off), u64(seg_len), i32(seg_cls)
-        b0, b1, nb = u64(seg_b0), u64(seg_b1), i32(seg_nb)
+    def final_sort(self, src, src_vals, tmp, tmp_vals, out, out_vals, key_kind, seg_off, seg_len):
+        so, sl = u64(seg_off), u64(seg_len)
         check(lib.ams_final_sort(self.h, ptr(src), ptr(src_vals), ptr(tmp), ptr(tmp_vals), ptr(out),
-                                 ptr(out_vals), key_kind, len(so), so.ctypes.data, sl.ctypes.data,
-                                 sc.ctypes.data, b0.ctypes.data, b1.ctypes.data, nb.ctypes.data))
+                                 ptr(out_vals), key_kind, len(so), so.ctypes.data, sl.ctypes.data))
 
     def map_keys(self, src, dst, n, from_kind, to_kind):
         check(lib.ams_map_keys(self.h, ptr(src), ptr(dst), n, from_kind, to_kind))

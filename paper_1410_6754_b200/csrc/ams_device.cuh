@@ -14,7 +14,8 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kItems = AMS_TILE / kThreads;  // 16
 constexpr int kTile = AMS_TILE;              // 4096
-constexpr int kChunkTiles = 8;
+constexpr int kChunkTiles = 16;
+constexpr int kChunk = kTile * kChunkTiles;  // keys per histogram / scatter CTA
 static_assert(kItems * kThreads == kTile, "tile geometry");
 
 // Tree classifier blob (one per group) in global memory.

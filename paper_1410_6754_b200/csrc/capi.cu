@@ -143,68 +143,127 @@ struct ams_ctx {
   int nspl_cap = 0, cells_cap = 0;
   // level state (classify -> scatter)
   int nseg = 0, ngroups = 0, nb_stride = 0;
-  uint64_t ntiles = 0, nchunks = 0;
+  uint64_t nchunks = 0, level_elems = 0;
   std::vector<int32_t> group_first, group_nseg;
   SegMeta meta{};
-  DevBuf tile_hist, chunk_tot, seg_hist, cell_base, pieces, minmax;
+  DevBuf chunk_tot, seg_hist, cell_base, pieces, minmax;
+  // key bounds [lo, hi] of the current level's groups (ping-pong)
+  DevBuf bounds[2];
+  int bcur = 0;
   HostBuf h_hist;
   // final sort
-  DevBuf dcls, ovf, ovf_count;
+  DevBuf dcls, ovf, ovf_count, fb, fb_count;
   HostBuf h_small;
+  uint64_t overflow_cells = 0, fallback_cells = 0;
+  // optional per-category kernel timing (CUDA events on the launching stream)
+  bool timing = false;
+  struct Timed { int cat; cudaEvent_t a, b; double bytes; };
+  std::vector<Timed> pending;
+  std::vector<cudaEvent_t> free_events;
+  double cat_ms[AMS_NUM_KCAT] = {};
+  double cat_bytes[AMS_NUM_KCAT] = {};
+  uint64_t cat_launches[AMS_NUM_KCAT] = {};
 };
 
 namespace {
 
-// Tile / chunk prefix arrays of a segment list.
-void tile_layout(const uint64_t* len, int nseg, std::vector<uint64_t>& tile_prefix,
-                 std::vector<uint64_t>& chunk_prefix) {
-  tile_prefix.assign(nseg + 1, 0);
-  chunk_prefix.assign(nseg + 1, 0);
-  for (int s = 0; s < nseg; ++s) {
-    const uint64_t tiles = (len[s] + kTile - 1) / kTile;
-    tile_prefix[s + 1] = tile_prefix[s] + tiles;
-    chunk_prefix[s + 1] = chunk_prefix[s] + (tiles + kChunkTiles - 1) / kChunkTiles;
+cudaEvent_t take_event(ams_ctx* c) {
+  if (!c->free_events.empty()) {
+    cudaEvent_t e = c->free_events.back();
+    c->free_events.pop_back();
+    return e;
   }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// Brackets one launch with events when timing is on; `bytes` is the
+// launch's algorithmic traffic (what bench.py divides by the time).
+struct KTimer {
+  ams_ctx* c;
+  int cat;
+  double bytes;
+  cudaEvent_t a = nullptr;
+  KTimer(ams_ctx* c_, int cat_, double bytes_) : c(c_), cat(cat_), bytes(bytes_) {
+    if (c->timing) {
+      a = take_event(c);
+      cudaEventRecord(a, c->stream);
+    }
+  }
+  ~KTimer() {
+    c->cat_launches[cat] += 1;
+    if (a) {
+      cudaEvent_t b = take_event(c);
+      cudaEventRecord(b, c->stream);
+      c->pending.push_back({cat, a, b, bytes});
+    } else {
+      c->cat_bytes[cat] += bytes;
+    }
+  }
+};
+
+void resolve_timing(ams_ctx* c) {
+  for (auto& t : c->pending) {
+    float ms = 0.f;
+    cudaEventSynchronize(t.b);
+    cudaEventElapsedTime(&ms, t.a, t.b);
+    c->cat_ms[t.cat] += ms;
+    c->cat_bytes[t.cat] += t.bytes;
+    c->free_events.push_back(t.a);
+    c->free_events.push_back(t.b);
+  }
+  c->pending.clear();
+}
+
+// Chunk prefix of a segment list (a chunk = kChunk keys of one segment,
+// one CTA of the histogram and scatter kernels).
+void chunk_layout(const uint64_t* len, int nseg, std::vector<uint64_t>& chunk_prefix) {
+  chunk_prefix.assign(nseg + 1, 0);
+  for (int s = 0; s < nseg; ++s)
+    chunk_prefix[s + 1] = chunk_prefix[s] + (len[s] + kChunk - 1) / kChunk;
 }
 
 // Upload a segment table; returns the device-side SegMeta.
 cudaError_t upload_segments(Stage& st, cudaStream_t stream, const uint64_t* off,
                             const uint64_t* len, const int32_t* cls, int nseg,
-                            const int64_t* posbase, int ncls, SegMeta* m, uint64_t* ntiles,
-                            uint64_t* nchunks) {
-  std::vector<uint64_t> tp, cp;
-  tile_layout(len, nseg, tp, cp);
+                            const int64_t* posbase, int ncls, SegMeta* m, uint64_t* nchunks) {
+  std::vector<uint64_t> cp;
+  chunk_layout(len, nseg, cp);
   st.reset();
   const size_t o_off = st.put(off, nseg), o_len = st.put(len, nseg), o_cls = st.put(cls, nseg);
-  const size_t o_tp = st.put(tp), o_cp = st.put(cp);
+  const size_t o_cp = st.put(cp);
   const size_t o_pb = posbase ? st.put(posbase, ncls) : 0;
   cudaError_t e = st.upload(stream);
   if (e != cudaSuccess) return e;
   m->off = st.dev<uint64_t>(o_off);
   m->len = st.dev<uint64_t>(o_len);
   m->cls = st.dev<int32_t>(o_cls);
-  m->tile_prefix = st.dev<uint64_t>(o_tp);
   m->chunk_prefix = st.dev<uint64_t>(o_cp);
   m->posbase = posbase ? st.dev<int64_t>(o_pb) : nullptr;
   m->nseg = nseg;
-  *ntiles = tp[nseg];
   *nchunks = cp[nseg];
   return cudaSuccess;
 }
 
 // hist -> chunk scan for a segment table whose classifiers are ready.
 int run_histogram(ams_ctx* c, const void* src, int kind, bool digit, const SegMeta& m,
-                  uint64_t ntiles, uint64_t nchunks, int nb_stride, const DigitCls* dcls,
-                  unsigned long long* minmax) {
-  AMS_CK(c->tile_hist.ensure(sizeof(uint32_t) * std::max<uint64_t>(ntiles, 1) * nb_stride));
+                  uint64_t nchunks, int nb_stride, const DigitCls* dcls,
+                  unsigned long long* minmax, uint64_t nelems) {
   AMS_CK(c->chunk_tot.ensure(sizeof(uint32_t) * std::max<uint64_t>(nchunks, 1) * nb_stride));
   AMS_CK(c->seg_hist.ensure(sizeof(uint32_t) * (size_t)std::max(m.nseg, 1) * nb_stride));
   AMS_CK(cudaMemsetAsync(c->seg_hist.p, 0, sizeof(uint32_t) * (size_t)m.nseg * nb_stride, c->stream));
-  AMS_CK(launch_hist(c->stream, src, kind, digit, m, nchunks, c->blobs.as<uint8_t>(), dcls,
-                     c->nspl_cap, c->cells_cap, nb_stride, c->tile_hist.as<uint32_t>(),
-                     c->chunk_tot.as<uint32_t>(), c->seg_hist.as<uint32_t>(), minmax));
-  AMS_CK(launch_chunk_scan(c->stream, c->chunk_tot.as<uint32_t>(), m, nb_stride));
-  c->launches += 2 + (nchunks ? 0 : 0);
+  {
+    KTimer kt(c, digit ? AMS_KCAT_FHIST : AMS_KCAT_HIST, 8.0 * nelems);
+    AMS_CK(launch_hist(c->stream, src, kind, digit, m, nchunks, c->blobs.as<uint8_t>(), dcls,
+                       c->nspl_cap, c->cells_cap, nb_stride, c->chunk_tot.as<uint32_t>(),
+                       c->seg_hist.as<uint32_t>(), minmax));
+  }
+  {
+    KTimer kt(c, AMS_KCAT_CHUNKSCAN, 8.0 * nchunks * nb_stride);
+    AMS_CK(launch_chunk_scan(c->stream, c->chunk_tot.as<uint32_t>(), m, nb_stride));
+  }
+  c->launches += 2;
   return AMS_OK;
 }
 
@@ -233,11 +292,13 @@ int ams_ctx_destroy(ams_ctx_t* c) {
   if (!c) return AMS_OK;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
+  resolve_timing(c);
+  for (cudaEvent_t e : c->free_events) cudaEventDestroy(e);
   for (Stage* s : {&c->st_sample, &c->st_split, &c->st_level, &c->st_scatter, &c->st_final})
     s->release();
-  for (DevBuf* b : {&c->blobs, &c->sorted_keys, &c->sorted_pos, &c->sample_idx, &c->tile_hist,
+  for (DevBuf* b : {&c->blobs, &c->sorted_keys, &c->sorted_pos, &c->sample_idx, &c->bounds[0], &c->bounds[1],
                     &c->chunk_tot, &c->seg_hist, &c->cell_base, &c->pieces, &c->minmax, &c->dcls,
-                    &c->ovf, &c->ovf_count})
+                    &c->ovf, &c->ovf_count, &c->fb, &c->fb_count})
     b->release();
   c->h_hist.release();
   c->h_small.release();
@@ -252,6 +313,32 @@ int ams_ctx_set_stream(ams_ctx_t* c, void* stream) {
 }
 
 uint64_t ams_ctx_launches(const ams_ctx_t* c) { return c ? c->launches : 0; }
+
+int ams_ctx_set_timing(ams_ctx_t* c, int enable) {
+  if (!c) return set_error(AMS_EINVAL, "null context");
+  c->timing = enable != 0;
+  return AMS_OK;
+}
+
+int ams_ctx_kernel_stats(ams_ctx_t* c, double* ms, double* bytes, uint64_t* launches, int ncat) {
+  if (!c) return set_error(AMS_EINVAL, "null context");
+  AMS_CK(cudaSetDevice(c->device));
+  resolve_timing(c);
+  for (int i = 0; i < ncat && i < AMS_NUM_KCAT; ++i) {
+    if (ms) ms[i] = c->cat_ms[i];
+    if (bytes) bytes[i] = c->cat_bytes[i];
+    if (launches) launches[i] = c->cat_launches[i];
+  }
+  return AMS_OK;
+}
+
+int ams_ctx_reset_stats(ams_ctx_t* c) {
+  if (!c) return set_error(AMS_EINVAL, "null context");
+  AMS_CK(cudaSetDevice(c->device));
+  resolve_timing(c);
+  for (int i = 0; i < AMS_NUM_KCAT; ++i) { c->cat_ms[i] = 0; c->cat_bytes[i] = 0; c->cat_launches[i] = 0; }
+  return AMS_OK;
+}
 
 int ams_ctx_sync(ams_ctx_t* c) {
   if (!c) return set_error(AMS_EINVAL, "null context");
@@ -272,8 +359,11 @@ int ams_level_sample(ams_ctx_t* c, const void* src, int key_kind, uint64_t count
   st.reset();
   const size_t oi = st.put(h_idx, count), og = st.put(h_gpos, count);
   AMS_CK(st.upload(c->stream));
-  AMS_CK(launch_gather_sample(c->stream, src, key_kind, st.dev<uint64_t>(oi), st.dev<uint64_t>(og),
-                              count, d_out_keys, d_out_pos));
+  {
+    KTimer kt(c, AMS_KCAT_SAMPLE, 12.0 * count);
+    AMS_CK(launch_gather_sample(c->stream, src, key_kind, st.dev<uint64_t>(oi),
+                                st.dev<uint64_t>(og), count, d_out_keys, d_out_pos));
+  }
   c->launches += 1;
   return AMS_OK;
 }
@@ -308,12 +398,18 @@ int ams_level_splitters(ams_ctx_t* c, int ngroups, const uint64_t* d_sample_keys
   AMS_CK(c->blobs.ensure(kBlobStride * (size_t)ngroups));
   AMS_CK(c->sorted_keys.ensure(sizeof(uint64_t) * std::max<uint64_t>(total, 1)));
   AMS_CK(c->sorted_pos.ensure(sizeof(uint32_t) * std::max<uint64_t>(total, 1)));
-  AMS_CK(launch_sample_rank(c->stream, ngroups, max_s, d_sample_keys, d_sample_pos,
-                            st.dev<uint64_t>(os), c->sorted_keys.as<uint64_t>(),
-                            c->sorted_pos.as<uint32_t>()));
-  AMS_CK(launch_build_cls(c->stream, ngroups, c->sorted_keys.as<uint64_t>(),
-                          c->sorted_pos.as<uint32_t>(), st.dev<uint64_t>(os), st.dev<int32_t>(on),
-                          c->blobs.as<uint8_t>()));
+  {
+    KTimer kt(c, AMS_KCAT_RANK, 24.0 * total);
+    AMS_CK(launch_sample_rank(c->stream, ngroups, max_s, d_sample_keys, d_sample_pos,
+                              st.dev<uint64_t>(os), c->sorted_keys.as<uint64_t>(),
+                              c->sorted_pos.as<uint32_t>()));
+  }
+  {
+    KTimer kt(c, AMS_KCAT_CLS, 12.0 * total);
+    AMS_CK(launch_build_cls(c->stream, ngroups, c->sorted_keys.as<uint64_t>(),
+                            c->sorted_pos.as<uint32_t>(), st.dev<uint64_t>(os),
+                            st.dev<int32_t>(on), c->blobs.as<uint8_t>()));
+  }
   c->launches += (max_s ? 1 : 0) + 1;
   c->group_nb.assign(h_nb, h_nb + ngroups);
   c->ngroups = ngroups;
@@ -368,7 +464,7 @@ int ams_level_classify(ams_ctx_t* c, const void* src, int key_kind, int nseg,
     if (n_g >= 0xFFFFFFFFull) return set_error(AMS_EINVAL, "group too large for 32-bit positions");
   }
   AMS_CK(upload_segments(c->st_level, c->stream, h_seg_off, h_seg_len, h_seg_group, nseg,
-                         h_group_posbase, ngroups, &c->meta, &c->ntiles, &c->nchunks));
+                         h_group_posbase, ngroups, &c->meta, &c->nchunks));
   c->nseg = nseg;
   c->nb_stride = nb_stride;
   unsigned long long* mm = nullptr;
@@ -381,9 +477,21 @@ int ams_level_classify(ams_ctx_t* c, const void* src, int key_kind, int nseg,
     AMS_CK(cudaMemcpyAsync(c->minmax.p, c->h_small.p, sizeof init, cudaMemcpyHostToDevice, c->stream));
     mm = c->minmax.as<unsigned long long>();
   }
-  int rc = run_histogram(c, src, key_kind, false, c->meta, c->ntiles, c->nchunks, nb_stride,
-                         nullptr, mm);
+  uint64_t nel = 0;
+  for (int s = 0; s < nseg; ++s) nel += h_seg_len[s];
+  c->level_elems = nel;
+  int rc = run_histogram(c, src, key_kind, false, c->meta, c->nchunks, nb_stride, nullptr, mm,
+                         nel);
   if (rc) return rc;
+  if (track_minmax) {
+    // The whole input is one group at the first level: its bounds are the
+    // global key range.
+    AMS_CK(c->bounds[0].ensure(16 * (size_t)ngroups));
+    AMS_CK(cudaMemcpyAsync(c->bounds[0].p, c->minmax.p, 16, cudaMemcpyDeviceToDevice, c->stream));
+    c->bcur = 0;
+  } else if (!c->bounds[c->bcur].p || c->bounds[c->bcur].cap < 16 * (size_t)ngroups) {
+    return set_error(AMS_EINVAL, "no key bounds for these groups (first level needs track_minmax)");
+  }
   const size_t hb = sizeof(uint32_t) * (size_t)nseg * nb_stride;
   AMS_CK(c->h_hist.ensure(hb));
   AMS_CK(cudaMemcpyAsync(c->h_hist.p, c->seg_hist.p, hb, cudaMemcpyDeviceToHost, c->stream));
@@ -394,14 +502,17 @@ int ams_level_classify(ams_ctx_t* c, const void* src, int key_kind, int nseg,
 
 int ams_level_scatter(ams_ctx_t* c, const void* src, const void* src_vals, int key_kind,
                       void* dst, void* dst_vals, int r, const uint64_t* h_boundaries,
-                      const uint64_t* h_group_dst_start) {
+                      const uint64_t* h_group_dst_start, int stable, int child_first,
+                      int child_count) {
   if (!c) return set_error(AMS_EINVAL, "null context");
   if (c->nseg == 0) return set_error(AMS_EINVAL, "ams_level_classify must run first");
   if (r < 1 || !h_boundaries || !h_group_dst_start) return set_error(AMS_EINVAL, "bad plan");
   if ((src_vals == nullptr) != (dst_vals == nullptr))
     return set_error(AMS_EINVAL, "values must be given for both source and destination");
-  AMS_CK(cudaSetDevice(c->device));
   const int G = c->ngroups;
+  if (child_first < 0 || child_count < 0 || child_first + child_count > G * r)
+    return set_error(AMS_EINVAL, "child group range outside the level's children");
+  AMS_CK(cudaSetDevice(c->device));
   for (int g = 0; g < G; ++g) {
     const uint64_t* b = h_boundaries + (size_t)g * (r + 1);
     if (b[0] != 0 || b[r] != (uint64_t)c->group_nb[g])
@@ -422,13 +533,32 @@ int ams_level_scatter(ams_ctx_t* c, const void* src, const void* src_vals, int k
   gm.dst_start = st.dev<uint64_t>(od);
   AMS_CK(c->pieces.ensure(sizeof(uint64_t) * (size_t)c->nseg * r));
   AMS_CK(c->cell_base.ensure(sizeof(uint64_t) * (size_t)c->nseg * c->nb_stride));
-  AMS_CK(launch_cell_base(c->stream, c->seg_hist.as<uint32_t>(), c->nb_stride, gm, G, r,
-                          c->pieces.as<uint64_t>(), c->cell_base.as<uint64_t>()));
-  AMS_CK(launch_scatter(c->stream, src, src_vals, key_kind, false, dst, dst_vals, c->meta,
-                        c->ntiles, c->blobs.as<uint8_t>(), nullptr, c->nspl_cap, c->cells_cap,
-                        c->nb_stride, c->tile_hist.as<uint32_t>(), c->chunk_tot.as<uint32_t>(),
-                        c->cell_base.as<uint64_t>()));
-  c->launches += 2;
+  {
+    KTimer kt(c, AMS_KCAT_CELLBASE, 12.0 * c->nseg * c->nb_stride);
+    AMS_CK(launch_cell_base(c->stream, c->seg_hist.as<uint32_t>(), c->nb_stride, gm, G, r,
+                            c->pieces.as<uint64_t>(), c->cell_base.as<uint64_t>()));
+  }
+  {
+    KTimer kt(c, stable ? AMS_KCAT_SCATTER : AMS_KCAT_SCATTER_U,
+              (src_vals ? 32.0 : 16.0) * c->level_elems);
+    AMS_CK(launch_scatter(c->stream, src, src_vals, key_kind, false, stable != 0, dst, dst_vals,
+                          c->meta, c->nchunks, c->blobs.as<uint8_t>(), nullptr, c->nspl_cap,
+                          c->cells_cap, c->nb_stride, c->chunk_tot.as<uint32_t>(),
+                          c->cell_base.as<uint64_t>()));
+  }
+  // Key bounds of the next level's groups (this rank's children).
+  const int nxt = 1 - c->bcur;
+  AMS_CK(c->bounds[nxt].ensure(16 * (size_t)std::max(G * r, 1)));
+  {
+    KTimer kt(c, AMS_KCAT_RANGES, 0.0);
+    AMS_CK(launch_child_bounds(c->stream, c->blobs.as<uint8_t>(), gm, G, r,
+                               c->bounds[c->bcur].as<uint64_t>(), c->bounds[nxt].as<uint64_t>()));
+  }
+  if (child_first > 0 && child_count > 0)
+    AMS_CK(cudaMemcpyAsync(c->bounds[nxt].p, c->bounds[nxt].as<uint64_t>() + 2 * child_first,
+                           16 * (size_t)child_count, cudaMemcpyDeviceToDevice, c->stream));
+  c->bcur = nxt;
+  c->launches += 3;
   return AMS_OK;
 }
 
@@ -450,67 +580,99 @@ int ams_set_minmax(ams_ctx_t* c, const uint64_t in[2]) {
   AMS_CK(cudaStreamSynchronize(c->stream));
   std::memcpy(c->h_small.p, in, 16);
   AMS_CK(cudaMemcpyAsync(c->minmax.p, c->h_small.p, 16, cudaMemcpyHostToDevice, c->stream));
+  AMS_CK(c->bounds[c->bcur].ensure(16));
+  AMS_CK(cudaMemcpyAsync(c->bounds[c->bcur].p, c->minmax.p, 16, cudaMemcpyDeviceToDevice, c->stream));
   return AMS_OK;
 }
 
+namespace {
+
+// Counting sort of a cell list into `out`, then the LSD fallback for the
+// cells whose keys cluster.  Syncs once to learn the fallback count.
+int sort_cells(ams_ctx* c, const void* src, const void* src_vals, void* out, void* out_vals,
+               int key_kind, const CellSource& cs, uint64_t ncells, uint64_t nelems) {
+  const bool vals = src_vals != nullptr;
+  AMS_CK(cudaMemsetAsync(c->fb_count.p, 0, sizeof(unsigned int), c->stream));
+  {
+    KTimer kt(c, AMS_KCAT_SMEMSORT, (vals ? 32.0 : 16.0) * nelems);
+    AMS_CK(launch_smem_sort(c->stream, src, src_vals, out, out_vals, key_kind, cs, ncells,
+                            c->ovf.as<OverflowRec>(), c->ovf_count.as<unsigned int>(),
+                            c->fb.as<OverflowRec>(), c->fb_count.as<unsigned int>()));
+  }
+  c->launches += 1;
+  unsigned int nfb = 0;
+  AMS_CK(cudaMemcpyAsync(c->h_small.p, c->fb_count.p, sizeof nfb, cudaMemcpyDeviceToHost, c->stream));
+  AMS_CK(cudaStreamSynchronize(c->stream));
+  std::memcpy(&nfb, c->h_small.p, sizeof nfb);
+  c->fallback_cells += nfb;
+  if (nfb) {
+    CellSource fc{};
+    fc.mode = 2;
+    fc.recs = c->fb.as<OverflowRec>();
+    KTimer kt(c, AMS_KCAT_SMEMSORT, 0.0);
+    AMS_CK(launch_smem_sort_lsd(c->stream, src, src_vals, out, out_vals, key_kind, fc, nfb));
+    c->launches += 1;
+  }
+  return AMS_OK;
+}
+
+}  // namespace
+
 int ams_final_sort(ams_ctx_t* c, void* src, void* src_vals, void* tmp, void* tmp_vals, void* out,
                    void* out_vals, int key_kind, int nseg, const uint64_t* h_seg_off,
-                   const uint64_t* h_seg_len, const int32_t* h_seg_cls, const uint64_t* h_seg_b0,
-                   const uint64_t* h_seg_b1, const int32_t* h_seg_nb) {
+                   const uint64_t* h_seg_len) {
   if (!c) return set_error(AMS_EINVAL, "null context");
   if (nseg < 0 || (nseg > 0 && (!h_seg_off || !h_seg_len))) return set_error(AMS_EINVAL, "bad segments");
   const bool vals = src_vals != nullptr;
   if (vals && (!tmp_vals || !out_vals)) return set_error(AMS_EINVAL, "missing value buffers");
   AMS_CK(cudaSetDevice(c->device));
   constexpr uint64_t kTargetCell = 4096;
-  std::vector<uint64_t> s_off, s_len, b_off, b_len, b_b0, b_b1;
-  std::vector<int32_t> b_cls, b_nb;
-  uint64_t total = 0, max_big = 0;
+  std::vector<uint64_t> s_off, s_len, b_off, b_len, b_lo, b_hi;
+  std::vector<int32_t> b_seg;
+  uint64_t total = 0, max_big = 0, small_n = 0;
   for (int s = 0; s < nseg; ++s) {
     total += h_seg_len[s];
     if (h_seg_len[s] == 0) continue;
     if (h_seg_len[s] <= (uint64_t)AMS_SMEM_SORT_CAP) {
       s_off.push_back(h_seg_off[s]);
       s_len.push_back(h_seg_len[s]);
+      small_n += h_seg_len[s];
     } else {
-      if (!h_seg_cls || !h_seg_b0 || !h_seg_b1 || !h_seg_nb)
-        return set_error(AMS_EINVAL, "large segments need their bucket ranges");
-      if (h_seg_cls[s] < 0 || h_seg_cls[s] >= c->ngroups)
-        return set_error(AMS_EINVAL, "segment classifier out of range");
-      if (!c->minmax.p) return set_error(AMS_EINVAL, "no key range recorded (track_minmax)");
       b_off.push_back(h_seg_off[s]);
       b_len.push_back(h_seg_len[s]);
-      b_cls.push_back(h_seg_cls[s]);
-      b_b0.push_back(h_seg_b0[s]);
-      b_b1.push_back(h_seg_b1[s]);
-      b_nb.push_back(h_seg_nb[s]);
+      b_seg.push_back(s);
       max_big = std::max(max_big, h_seg_len[s]);
     }
   }
-  const uint64_t ovf_cap = total / (AMS_SMEM_SORT_CAP + 1) + 16;
-  AMS_CK(c->ovf.ensure(sizeof(OverflowRec) * ovf_cap));
+  if (!b_off.empty() && c->bounds[c->bcur].cap < 16 * (size_t)nseg)
+    return set_error(AMS_EINVAL, "final segments need the key bounds of the last level");
+  const uint64_t rec_cap = total / (AMS_SMEM_SORT_CAP / 2) + 64;
+  AMS_CK(c->ovf.ensure(sizeof(OverflowRec) * rec_cap));
+  AMS_CK(c->fb.ensure(sizeof(OverflowRec) * rec_cap));
   AMS_CK(c->ovf_count.ensure(sizeof(unsigned int)));
+  AMS_CK(c->fb_count.ensure(sizeof(unsigned int)));
+  AMS_CK(c->h_small.ensure(4096));
   AMS_CK(cudaMemsetAsync(c->ovf_count.p, 0, sizeof(unsigned int), c->stream));
   Stage& st = c->st_final;
   // 1. Segments that fit in shared memory: sort straight into `out`.
   if (!s_off.empty()) {
-    st.reset();
-    const size_t oo = st.put(s_off), ol = st.put(s_len);
-    AMS_CK(st.upload(c->stream));
+    Stage& ss = c->st_sample;  // free after the levels
+    ss.reset();
+    const size_t oo = ss.put(s_off), ol = ss.put(s_len);
+    AMS_CK(ss.upload(c->stream));
     CellSource cs{};
     cs.mode = 1;
-    cs.seg_off = st.dev<uint64_t>(oo);
-    cs.seg_len = st.dev<uint64_t>(ol);
-    AMS_CK(launch_smem_sort(c->stream, src, src_vals, out, out_vals, key_kind, cs, s_off.size(),
-                            c->ovf.as<OverflowRec>(), c->ovf_count.as<unsigned int>()));
-    c->launches += 1;
+    cs.seg_off = ss.dev<uint64_t>(oo);
+    cs.seg_len = ss.dev<uint64_t>(ol);
+    int rc = sort_cells(c, src, src_vals, out, out_vals, key_kind, cs, s_off.size(), small_n);
+    if (rc) return rc;
   }
-  // 2. Large segments: digit partition src -> tmp, then per-cell sorts.
+  // 2. Large segments: digit partition src -> tmp, then per-cell sorts;
+  //    cells still above shared memory go round again (tmp -> src -> ...).
   void* cur = src;
   void* cur_v = src_vals;
   void* oth = tmp;
   void* oth_v = tmp_vals;
-  std::vector<DigitCls> host_dcls;
   bool first_round = true;
   while (!b_off.empty()) {
     const int nb_seg = (int)b_off.size();
@@ -519,52 +681,53 @@ int ams_final_sort(ams_ctx_t* c, void* src, void* src_vals, void* tmp, void* tmp
     std::vector<int32_t> idx(nb_seg);
     for (int i = 0; i < nb_seg; ++i) idx[i] = i;
     SegMeta m;
-    uint64_t ntiles, nchunks;
+    uint64_t nchunks;
     AMS_CK(c->dcls.ensure(sizeof(DigitCls) * (size_t)nb_seg));
+    AMS_CK(c->pieces.ensure(16 * (size_t)nb_seg));
+    Stage& sf = c->st_split;  // free after the levels: reuse for the range table
+    sf.reset();
+    size_t ob;
     if (first_round) {
-      Stage& sf = c->st_split;  // free after the level: reuse for the range table
-      sf.reset();
-      const size_t oc = sf.put(b_cls), o0 = sf.put(b_b0), o1 = sf.put(b_b1), on = sf.put(b_nb);
-      AMS_CK(sf.upload(c->stream));
-      FinalRangeMeta fm;
-      fm.cls = sf.dev<int32_t>(oc);
-      fm.b0 = sf.dev<uint64_t>(o0);
-      fm.b1 = sf.dev<uint64_t>(o1);
-      fm.nb = sf.dev<int32_t>(on);
-      fm.nseg = nb_seg;
-      fm.nbits = nbits;
-      AMS_CK(launch_final_ranges(c->stream, fm, c->blobs.as<uint8_t>(),
-                                 c->minmax.as<unsigned long long>(), c->dcls.as<DigitCls>()));
-      c->launches += 1;
+      // Bounds of the final segments that need a partition (segment order).
+      ob = sf.put(b_seg);
     } else {
-      host_dcls.resize(nb_seg);
-      for (int i = 0; i < nb_seg; ++i) {
-        DigitCls d;
-        d.lo = b_b0[i];
-        d.hi = b_b1[i];
-        const int bl = bit_length64(d.hi - d.lo);
-        d.shift = bl > nbits ? (uint32_t)(bl - nbits) : 0u;
-        d.nb = (uint32_t)nbs;
-        host_dcls[i] = d;
-      }
-      AMS_CK(c->h_small.ensure(sizeof(DigitCls) * (size_t)nb_seg + 64));
-      AMS_CK(cudaStreamSynchronize(c->stream));
-      std::memcpy(c->h_small.p, host_dcls.data(), sizeof(DigitCls) * (size_t)nb_seg);
-      AMS_CK(cudaMemcpyAsync(c->dcls.p, c->h_small.p, sizeof(DigitCls) * (size_t)nb_seg,
-                             cudaMemcpyHostToDevice, c->stream));
+      std::vector<uint64_t> lohi(2 * (size_t)nb_seg);
+      for (int i = 0; i < nb_seg; ++i) { lohi[2 * i] = b_lo[i]; lohi[2 * i + 1] = b_hi[i]; }
+      ob = sf.put(lohi);
+    }
+    AMS_CK(sf.upload(c->stream));
+    const uint64_t* bounds;
+    if (first_round) {
+      AMS_CK(launch_gather_bounds(c->stream, c->bounds[c->bcur].as<uint64_t>(),
+                                  sf.dev<int32_t>(ob), nb_seg, c->pieces.as<uint64_t>()));
+      bounds = c->pieces.as<uint64_t>();
+    } else {
+      bounds = sf.dev<uint64_t>(ob);
+    }
+    {
+      KTimer kt(c, AMS_KCAT_RANGES, 0.0);
+      AMS_CK(launch_final_ranges(c->stream, bounds, nb_seg, nbits, c->dcls.as<DigitCls>()));
     }
     AMS_CK(upload_segments(st, c->stream, b_off.data(), b_len.data(), idx.data(), nb_seg, nullptr,
-                           0, &m, &ntiles, &nchunks));
-    int rc = run_histogram(c, cur, AMS_KEY_U64, true, m, ntiles, nchunks, nbs,
-                           c->dcls.as<DigitCls>(), nullptr);
+                           0, &m, &nchunks));
+    uint64_t nel = 0;
+    for (uint64_t v : b_len) nel += v;
+    int rc = run_histogram(c, cur, AMS_KEY_U64, true, m, nchunks, nbs, c->dcls.as<DigitCls>(),
+                           nullptr, nel);
     if (rc) return rc;
     AMS_CK(c->cell_base.ensure(sizeof(uint64_t) * (size_t)nb_seg * nbs));
-    AMS_CK(launch_digit_base(c->stream, c->seg_hist.as<uint32_t>(), nbs, m,
-                             c->cell_base.as<uint64_t>()));
-    AMS_CK(launch_scatter(c->stream, cur, cur_v, AMS_KEY_U64, true, oth, oth_v, m, ntiles,
-                          c->blobs.as<uint8_t>(), c->dcls.as<DigitCls>(), 0, 0, nbs,
-                          c->tile_hist.as<uint32_t>(), c->chunk_tot.as<uint32_t>(),
-                          c->cell_base.as<uint64_t>()));
+    {
+      KTimer kt(c, AMS_KCAT_CELLBASE, 12.0 * nb_seg * nbs);
+      AMS_CK(launch_digit_base(c->stream, c->seg_hist.as<uint32_t>(), nbs, m,
+                               c->cell_base.as<uint64_t>()));
+    }
+    {
+      KTimer kt(c, AMS_KCAT_FSCATTER, (vals ? 32.0 : 16.0) * nel);
+      AMS_CK(launch_scatter(c->stream, cur, cur_v, AMS_KEY_U64, true, /*stable=*/vals, oth, oth_v,
+                            m, nchunks, c->blobs.as<uint8_t>(), c->dcls.as<DigitCls>(), 0, 0, nbs,
+                            c->chunk_tot.as<uint32_t>(), c->cell_base.as<uint64_t>()));
+    }
+    c->launches += 5;
     AMS_CK(cudaMemsetAsync(c->ovf_count.p, 0, sizeof(unsigned int), c->stream));
     CellSource cs{};
     cs.mode = 0;
@@ -572,18 +735,14 @@ int ams_final_sort(ams_ctx_t* c, void* src, void* src_vals, void* tmp, void* tmp
     cs.cell_base = c->cell_base.as<uint64_t>();
     cs.cell_cnt = c->seg_hist.as<uint32_t>();
     cs.dcls = c->dcls.as<DigitCls>();
-    AMS_CK(launch_smem_sort(c->stream, oth, oth_v, out, out_vals, key_kind, cs,
-                            (uint64_t)nb_seg * nbs, c->ovf.as<OverflowRec>(),
-                            c->ovf_count.as<unsigned int>()));
-    c->launches += 3;
-    // Cells that still exceed shared memory go round again.
+    rc = sort_cells(c, oth, oth_v, out, out_vals, key_kind, cs, (uint64_t)nb_seg * nbs, nel);
+    if (rc) return rc;
+    // Cells that still exceed shared memory go round again (sort_cells synced).
     unsigned int novf = 0;
-    AMS_CK(c->h_small.ensure(64));
-    AMS_CK(cudaMemcpyAsync(c->h_small.p, c->ovf_count.p, sizeof novf, cudaMemcpyDeviceToHost, c->stream));
-    AMS_CK(cudaStreamSynchronize(c->stream));
-    std::memcpy(&novf, c->h_small.p, sizeof novf);
-    b_off.clear(); b_len.clear(); b_b0.clear(); b_b1.clear();
+    AMS_CK(cudaMemcpy(&novf, c->ovf_count.p, sizeof novf, cudaMemcpyDeviceToHost));
+    b_off.clear(); b_len.clear(); b_lo.clear(); b_hi.clear();
     max_big = 0;
+    c->overflow_cells += novf;
     if (novf) {
       std::vector<OverflowRec> recs(novf);
       AMS_CK(cudaMemcpy(recs.data(), c->ovf.p, sizeof(OverflowRec) * novf, cudaMemcpyDeviceToHost));
@@ -592,8 +751,8 @@ int ams_final_sort(ams_ctx_t* c, void* src, void* src_vals, void* tmp, void* tmp
       for (const OverflowRec& r : recs) {
         b_off.push_back(r.off);
         b_len.push_back(r.count);
-        b_b0.push_back(r.lo);  // exact min/max of the cell
-        b_b1.push_back(r.hi);
+        b_lo.push_back(r.lo);  // exact min/max of the cell
+        b_hi.push_back(r.hi);
         max_big = std::max(max_big, r.count);
       }
     }
@@ -604,9 +763,17 @@ int ams_final_sort(ams_ctx_t* c, void* src, void* src_vals, void* tmp, void* tmp
   return AMS_OK;
 }
 
+int ams_final_sort_stats(ams_ctx_t* c, uint64_t out[2]) {
+  if (!c || !out) return set_error(AMS_EINVAL, "null argument");
+  out[0] = c->overflow_cells;
+  out[1] = c->fallback_cells;
+  return AMS_OK;
+}
+
 int ams_map_keys(ams_ctx_t* c, const void* src, void* dst, uint64_t n, int from_kind, int to_kind) {
   if (!c) return set_error(AMS_EINVAL, "null context");
   AMS_CK(cudaSetDevice(c->device));
+  KTimer kt(c, AMS_KCAT_MAP, 16.0 * n);
   AMS_CK(launch_map_keys(c->stream, src, dst, n, from_kind, to_kind));
   c->launches += n ? 1 : 0;
   return AMS_OK;

@@ -5,11 +5,11 @@
 //   K2 k_sample_rank     work-inefficient rank-by-counting of the group
 //      k_build_cls       sample, splitters at ranks (i*S)//nb, key LUT
 //                        (select_splitters ams.py:178-198, fastsort.py:57-130)
-//   K3 k_hist            classification + tile/chunk/segment histograms
+//   K3 k_hist            classification + chunk/segment histograms
 //                        (partition_buckets ams.py:201-211, allreduce 236-237)
 //   K4 k_chunk_scan,     offsets of every (group, source PE, bucket) cell
 //      k_cell_base,      (deliver_simple prefix sums delivery.py:138-180)
-//      k_digit_base
+//      k_digit_base, k_child_bounds (key range of every next-level group)
 //   K6 k_scatter         stable bucket-contiguous scatter (pieces ams.py:
 //                        240-248, exchange order simnet.py:324-325)
 //   K7 k_final_ranges    key range of every final PE
@@ -134,32 +134,31 @@ __global__ void __launch_bounds__(1024) k_build_cls(const uint64_t* __restrict__
 }
 
 // -------------------------------------------------------------------- K3
-// One CTA per chunk (<= kChunkTiles tiles of one segment).  Per tile:
-// classify every key, warp-aggregated shared histogram; tile_hist row =
-// exclusive prefix inside the chunk; chunk_tot = chunk histogram;
-// seg_hist += chunk histogram.
+// One CTA per chunk (<= kChunkTiles tiles of one segment): classify every
+// key, count buckets in shared memory with run-aggregated atomics (a run of
+// same-bucket items of one thread costs one atomic — sorted and
+// duplicate-heavy inputs stay cheap), then write the chunk histogram and
+// add it to the segment histogram.
 template <int KIND, bool DIGIT>
 __global__ void __launch_bounds__(kThreads) k_hist(const uint64_t* __restrict__ src, SegMeta m,
                                                    const uint8_t* __restrict__ blobs,
                                                    const DigitCls* __restrict__ dcls, int nspl_cap,
-                                                   int nb_stride, uint32_t* __restrict__ tile_hist,
-                                                   uint32_t* __restrict__ chunk_tot,
+                                                   int nb_stride, uint32_t* __restrict__ chunk_tot,
                                                    uint32_t* __restrict__ seg_hist,
                                                    unsigned long long* __restrict__ minmax) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ int s_seg;
   __shared__ unsigned long long s_min[kWarps], s_max[kWarps];
   const uint64_t c = blockIdx.x;
+  uint32_t* hist = reinterpret_cast<uint32_t*>(smem);
+  uint8_t* clsmem = smem + (((size_t)4 * nb_stride + 15) & ~(size_t)15);
   if (threadIdx.x == 0) s_seg = upper_bound_u64(m.chunk_prefix, m.nseg + 1, c) - 1;
+  for (int b = threadIdx.x; b < nb_stride; b += kThreads) hist[b] = 0;
   __syncthreads();
   const int s = s_seg;
   const uint64_t seg_off = m.off[s], seg_len = m.len[s];
-  const uint64_t tile0 = (c - m.chunk_prefix[s]) * kChunkTiles;
-  const uint64_t seg_tiles = m.tile_prefix[s + 1] - m.tile_prefix[s];
-  const int ntiles = (int)min((uint64_t)kChunkTiles, seg_tiles - tile0);
-  uint32_t* hist = reinterpret_cast<uint32_t*>(smem);
-  uint32_t* run = hist + nb_stride;
-  uint8_t* clsmem = smem + (size_t)8 * nb_stride;
+  const uint64_t first = (c - m.chunk_prefix[s]) * (uint64_t)kChunk;
+  const uint64_t last = min(first + (uint64_t)kChunk, seg_len);
   const int cls = m.cls[s];
   TreeView tv;
   DigitView dv;
@@ -169,46 +168,41 @@ __global__ void __launch_bounds__(kThreads) k_hist(const uint64_t* __restrict__ 
   } else {
     tv = load_tree(blobs + (size_t)cls * kBlobStride, clsmem, nspl_cap);
     posbase = m.posbase[cls];
+    __syncthreads();
   }
-  for (int b = threadIdx.x; b < nb_stride; b += kThreads) run[b] = 0;
   const int lane = threadIdx.x & 31;
   unsigned long long mn = ~0ULL, mx = 0;
-  for (int it = 0; it < ntiles; ++it) {
-    for (int b = threadIdx.x; b < nb_stride; b += kThreads) hist[b] = 0;
-    __syncthreads();
-    const uint64_t tl = tile0 + it;
-    const uint64_t tstart = tl * kTile;
-    const uint32_t tcount = (uint32_t)min((uint64_t)kTile, seg_len - tstart);
-    const uint64_t base = seg_off + tstart;
+  for (uint64_t t0 = first; t0 < last; t0 += kTile) {
+    const uint32_t tcount = (uint32_t)min((uint64_t)kTile, last - t0);
+    const uint64_t base = seg_off + t0;
     uint64_t keys[kItems];
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
       const uint32_t e = i * kThreads + threadIdx.x;
       keys[i] = e < tcount ? to_ordered<KIND>(ldg_stream(src + base + e)) : 0;
     }
+    uint32_t cur = kInvalid, cnt = 0;
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
       const uint32_t e = i * kThreads + threadIdx.x;
-      uint32_t b = kInvalid;
       if (e < tcount) {
+        uint32_t b;
         if constexpr (DIGIT) b = dv.classify(keys[i], 0);
         else b = tv.classify(keys[i], (uint32_t)((int64_t)(base + e) + posbase));
         if (minmax) { mn = min(mn, (unsigned long long)keys[i]); mx = max(mx, (unsigned long long)keys[i]); }
+        if (b != cur) {
+          if (cnt) atomicAdd(&hist[cur], cnt);
+          cur = b;
+          cnt = 0;
+        }
+        ++cnt;
       }
-      const uint32_t peers = __match_any_sync(0xffffffffu, b);
-      if (b != kInvalid && lane == __ffs(peers) - 1) atomicAdd(&hist[b], (uint32_t)__popc(peers));
     }
-    __syncthreads();
-    const uint64_t tg = m.tile_prefix[s] + tl;
-    for (int b = threadIdx.x; b < nb_stride; b += kThreads) {
-      const uint32_t hv = hist[b];
-      tile_hist[tg * nb_stride + b] = run[b];
-      run[b] += hv;
-    }
-    __syncthreads();
+    if (cnt) atomicAdd(&hist[cur], cnt);
   }
+  __syncthreads();
   for (int b = threadIdx.x; b < nb_stride; b += kThreads) {
-    const uint32_t v = run[b];
+    const uint32_t v = hist[b];
     chunk_tot[c * nb_stride + b] = v;
     if (v) atomicAdd(&seg_hist[(uint64_t)s * nb_stride + b], v);
   }
@@ -307,12 +301,81 @@ __global__ void k_digit_base(const uint32_t* __restrict__ seg_hist, int nb_strid
   }
 }
 
+// Key bounds of every child group: child t of group g holds buckets
+// [B_t, B_{t+1}) of g, so its keys lie between splitter B_t - 1 and
+// splitter B_{t+1} - 1 (the parent's bounds at the open ends).
+__global__ void k_child_bounds(const uint8_t* __restrict__ blobs, GroupMeta gm, int ngroups, int r,
+                               const uint64_t* __restrict__ parent, uint64_t* __restrict__ child) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= ngroups * r) return;
+  const int g = idx / r, t = idx % r;
+  const uint8_t* blob = blobs + (size_t)g * kBlobStride;
+  const ClsHeader* h = reinterpret_cast<const ClsHeader*>(blob);
+  const uint64_t* bk = reinterpret_cast<const uint64_t*>(blob + kBlobKeys);
+  const uint64_t nb = (uint64_t)h->nspl + 1;
+  const uint64_t* bnd = gm.bnd + (size_t)g * (r + 1);
+  const uint64_t b0 = bnd[t], b1 = bnd[t + 1];
+  uint64_t lo = parent[2 * g], hi = parent[2 * g + 1];
+  if (b0 > 0) lo = max(lo, bk[b0 - 1]);
+  if (b1 < nb) hi = min(hi, bk[b1 - 1]);
+  if (hi < lo) hi = lo;  // empty child
+  child[2 * idx] = lo;
+  child[2 * idx + 1] = hi;
+}
+
 // -------------------------------------------------------------------- K6
-// Stable scatter of one tile: warp-level ranks (match_any), per-warp
-// bucket counters, bucket-major reorder in shared memory, then coalesced
-// runs to dst.  Order inside a bucket = input order, so the output is the
-// stable (cell, position) order the reference's concatenations produce.
-template <int KIND, bool DIGIT, bool VALS>
+// Ranking modes of the scatter.
+constexpr int kRankWarp = 0;     // stable, one bucket-counter array per warp
+constexpr int kRankSerial = 1;   // stable, one shared array, warps take turns
+constexpr int kRankAtomic = 2;   // unstable (keys only, order inside a run is free)
+
+// Stable rank of this lane's item among the warp's items in the same bucket:
+// a 32-lane bitonic sort of (bucket << 5 | lane) with shuffles (15 steps;
+// __match_any_sync costs ~57 SM-cycles per warp on B200, this ~20), group
+// heads by ballot, the head bumps the per-warp counter, and the rank goes
+// back to the item's lane through `xch`.
+__device__ __forceinline__ uint32_t warp_stable_rank(uint32_t b, int lane, uint32_t* whw,
+                                                     uint32_t* xch) {
+  constexpr uint32_t kNone = 0x7FFFFFFu;
+  uint32_t v = ((b == kInvalid ? kNone : b) << 5) | (uint32_t)lane;
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const uint32_t o = __shfl_xor_sync(0xffffffffu, v, j);
+      const bool up = (lane & k) == 0;
+      const bool lower = (lane & j) == 0;
+      v = (lower == up) ? min(v, o) : max(v, o);
+    }
+  }
+  const uint32_t sb = v >> 5, src = v & 31u;
+  const uint32_t prev = __shfl_up_sync(0xffffffffu, sb, 1);
+  const bool head = lane == 0 || prev != sb;
+  const uint32_t heads = __ballot_sync(0xffffffffu, head);
+  const uint32_t upto = 0xFFFFFFFFu >> (31 - lane);
+  const int start = 31 - __clz(heads & upto);
+  const uint32_t after = heads & ~upto;
+  const int next = after ? __ffs(after) - 1 : 32;
+  uint32_t old = 0;
+  if (head && sb != kNone) {
+    old = whw[sb];
+    whw[sb] = old + (uint32_t)(next - start);
+  }
+  old = __shfl_sync(0xffffffffu, old, start);
+  xch[src] = old + (uint32_t)(lane - start);
+  __syncwarp();
+  const uint32_t r = xch[lane];
+  __syncwarp();
+  return r;
+}
+
+// One CTA per chunk (the histogram kernel's chunks): the running output
+// offset of every bucket starts at cell base + the chunk's exclusive prefix;
+// each tile is classified, ranked, reordered bucket-major in shared memory
+// and written as coalesced runs, then the running offsets advance.  With a
+// stable mode the order inside a bucket is the input order — the stable
+// (cell, position) order the reference's concatenations produce.
+template <int KIND, bool DIGIT, bool VALS, int MODE>
 __global__ void __launch_bounds__(kThreads) k_scatter(const uint64_t* __restrict__ src,
                                                       const uint64_t* __restrict__ src_vals,
                                                       uint64_t* __restrict__ dst,
@@ -320,32 +383,37 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const uint64_t* __restrict
                                                       const uint8_t* __restrict__ blobs,
                                                       const DigitCls* __restrict__ dcls,
                                                       int nspl_cap, int nb_stride,
-                                                      const uint32_t* __restrict__ tile_hist,
                                                       const uint32_t* __restrict__ chunk_tot,
                                                       const uint64_t* __restrict__ cell_base) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ int s_seg;
   __shared__ uint32_t s_scan[kWarps + 1];
-  // layout
+  __shared__ uint32_t s_xch[kWarps][32];
+  constexpr int kHists = MODE == kRankWarp ? kWarps : 1;
   uint64_t* keys_s = reinterpret_cast<uint64_t*>(smem);
   uint64_t* vals_s = keys_s + kTile;
-  int64_t* delta = reinterpret_cast<int64_t*>(smem + (VALS ? 16 : 8) * (size_t)kTile);
+  int64_t* run = reinterpret_cast<int64_t*>(smem + (VALS ? 16 : 8) * (size_t)kTile);
+  int64_t* delta = run + nb_stride;
   uint32_t* wh = reinterpret_cast<uint32_t*>(delta + nb_stride);
-  uint32_t* btot = wh + (size_t)kWarps * nb_stride;
-  uint16_t* bkt_s = reinterpret_cast<uint16_t*>(btot + nb_stride);
-  uint8_t* clsmem = reinterpret_cast<uint8_t*>(bkt_s + kTile);
+  uint32_t* btot = wh + (size_t)kHists * nb_stride;
+  uint32_t* tcnt = btot + nb_stride;
+  uint16_t* bkt_s = reinterpret_cast<uint16_t*>(tcnt + nb_stride);
+  uint8_t* clsmem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(bkt_s + kTile) + 15) & ~static_cast<uintptr_t>(15));
 
-  const uint64_t t = blockIdx.x;
-  if (threadIdx.x == 0) s_seg = upper_bound_u64(m.tile_prefix, m.nseg + 1, t) - 1;
-  for (int i = threadIdx.x; i < kWarps * nb_stride; i += kThreads) wh[i] = 0;
+  const uint64_t c = blockIdx.x;
+  if (threadIdx.x == 0) s_seg = upper_bound_u64(m.chunk_prefix, m.nseg + 1, c) - 1;
   __syncthreads();
   const int s = s_seg;
-  const uint64_t tl = t - m.tile_prefix[s];
-  const uint64_t chunk = m.chunk_prefix[s] + tl / kChunkTiles;
-  const uint64_t tstart = tl * kTile;
-  const uint32_t tcount = (uint32_t)min((uint64_t)kTile, m.len[s] - tstart);
-  const uint64_t base = m.off[s] + tstart;
+  const uint64_t seg_off = m.off[s];
+  const uint64_t first = (c - m.chunk_prefix[s]) * (uint64_t)kChunk;
+  const uint64_t last = min(first + (uint64_t)kChunk, m.len[s]);
   const int cls = m.cls[s];
+  {
+    const uint32_t* ct = chunk_tot + c * nb_stride;
+    const uint64_t* cb = cell_base + (uint64_t)s * nb_stride;
+    for (int b = threadIdx.x; b < nb_stride; b += kThreads) run[b] = (int64_t)(cb[b] + ct[b]);
+  }
   TreeView tv;
   DigitView dv;
   int64_t posbase = 0;
@@ -354,91 +422,101 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const uint64_t* __restrict
   } else {
     tv = load_tree(blobs + (size_t)cls * kBlobStride, clsmem, nspl_cap);
     posbase = m.posbase[cls];
-    __syncthreads();
   }
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t lt = lanemask_lt();
-  uint64_t keys[kItems];
-  uint64_t vals[VALS ? kItems : 1];
-  uint32_t pk[kItems];
+  uint32_t* whw = wh + (MODE == kRankWarp ? (size_t)w * nb_stride : 0);
+  for (uint64_t t0 = first; t0 < last; t0 += kTile) {
+    const uint32_t tcount = (uint32_t)min((uint64_t)kTile, last - t0);
+    const uint64_t base = seg_off + t0;
+    for (int i = threadIdx.x; i < kHists * nb_stride; i += kThreads) wh[i] = 0;
+    uint64_t keys[kItems];
+    uint64_t vals[VALS ? kItems : 1];
+    uint32_t pk[kItems];
 #pragma unroll
-  for (int i = 0; i < kItems; ++i) {
-    const uint32_t e = w * (kItems * 32) + i * 32 + lane;
-    keys[i] = e < tcount ? to_ordered<KIND>(ldg_stream(src + base + e)) : 0;
-    if constexpr (VALS) vals[i] = e < tcount ? ldg_stream(src_vals + base + e) : 0;
-  }
-  uint32_t* whw = wh + (size_t)w * nb_stride;
+    for (int i = 0; i < kItems; ++i) {
+      const uint32_t e = w * (kItems * 32) + i * 32 + lane;
+      keys[i] = e < tcount ? to_ordered<KIND>(ldg_stream(src + base + e)) : 0;
+      if constexpr (VALS) vals[i] = e < tcount ? ldg_stream(src_vals + base + e) : 0;
+    }
+    __syncthreads();  // counters zeroed, tree loaded, previous tile written out
 #pragma unroll
-  for (int i = 0; i < kItems; ++i) {
-    const uint32_t e = w * (kItems * 32) + i * 32 + lane;
-    uint32_t b = kInvalid;
-    if (e < tcount) {
-      if constexpr (DIGIT) b = dv.classify(keys[i], 0);
-      else b = tv.classify(keys[i], (uint32_t)((int64_t)(base + e) + posbase));
+    for (int i = 0; i < kItems; ++i) {
+      const uint32_t e = w * (kItems * 32) + i * 32 + lane;
+      uint32_t b = kInvalid;
+      if (e < tcount) {
+        if constexpr (DIGIT) b = dv.classify(keys[i], 0);
+        else b = tv.classify(keys[i], (uint32_t)((int64_t)(base + e) + posbase));
+      }
+      pk[i] = b;
+      if constexpr (MODE == kRankAtomic) {
+        if (b != kInvalid) pk[i] = (b << 16) | atomicAdd(&whw[b], 1u);
+      }
     }
-    const uint32_t peers = __match_any_sync(0xffffffffu, b);
-    uint32_t cnt = 0;
-    if (b != kInvalid) {
-      cnt = whw[b];
-      pk[i] = (b << 16) | (cnt + __popc(peers & lt));
-    } else {
-      pk[i] = kInvalid;
-    }
-    __syncwarp();
-    if (b != kInvalid && lane == __ffs(peers) - 1) whw[b] = cnt + __popc(peers);
-    __syncwarp();
-  }
-  __syncthreads();
-  for (int b = threadIdx.x; b < nb_stride; b += kThreads) {
-    uint32_t acc = 0;
+    if constexpr (MODE != kRankAtomic) {
+      for (int turn = 0; turn < (MODE == kRankSerial ? kWarps : 1); ++turn) {
+        if (MODE == kRankWarp || w == turn) {
 #pragma unroll
-    for (int ww = 0; ww < kWarps; ++ww) {
-      const uint32_t v = wh[(size_t)ww * nb_stride + b];
-      wh[(size_t)ww * nb_stride + b] = acc;
-      acc += v;
+          for (int i = 0; i < kItems; ++i) {
+            const uint32_t b = pk[i];
+            const uint32_t r = warp_stable_rank(b, lane, whw, s_xch[w]);
+            if (b != kInvalid) pk[i] = (b << 16) | r;
+          }
+        }
+        if (MODE == kRankSerial) __syncthreads();
+      }
     }
-    btot[b] = acc;
-  }
-  __syncthreads();
-  block_excl_scan<kThreads>(btot, nb_stride, s_scan);
-  const uint32_t* th = tile_hist + t * nb_stride;
-  const uint32_t* ct = chunk_tot + chunk * nb_stride;
-  const uint64_t* cb = cell_base + (uint64_t)s * nb_stride;
-  for (int b = threadIdx.x; b < nb_stride; b += kThreads)
-    delta[b] = (int64_t)(cb[b] + ct[b] + th[b]) - (int64_t)btot[b];
+    __syncthreads();
+    for (int b = threadIdx.x; b < nb_stride; b += kThreads) {
+      uint32_t acc = 0;
 #pragma unroll
-  for (int i = 0; i < kItems; ++i) {
-    if (pk[i] != kInvalid) {
-      const uint32_t b = pk[i] >> 16;
-      const uint32_t slot = btot[b] + whw[b] + (pk[i] & 0xFFFFu);
-      keys_s[slot] = keys[i];
-      bkt_s[slot] = (uint16_t)b;
-      if constexpr (VALS) vals_s[slot] = vals[i];
+      for (int ww = 0; ww < kHists; ++ww) {
+        const uint32_t v = wh[(size_t)ww * nb_stride + b];
+        wh[(size_t)ww * nb_stride + b] = acc;
+        acc += v;
+      }
+      btot[b] = acc;
+      tcnt[b] = acc;
     }
-  }
-  __syncthreads();
-  for (uint32_t j = threadIdx.x; j < tcount; j += kThreads) {
-    const int64_t d = delta[bkt_s[j]] + (int64_t)j;
-    dst[d] = keys_s[j];
-    if constexpr (VALS) dst_vals[d] = vals_s[j];
+    __syncthreads();
+    block_excl_scan<kThreads>(btot, nb_stride, s_scan);
+    for (int b = threadIdx.x; b < nb_stride; b += kThreads) {
+      delta[b] = run[b] - (int64_t)btot[b];
+      run[b] += tcnt[b];
+    }
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+      if (pk[i] != kInvalid) {
+        const uint32_t b = pk[i] >> 16;
+        const uint32_t slot = btot[b] + whw[b] + (pk[i] & 0xFFFFu);
+        keys_s[slot] = keys[i];
+        bkt_s[slot] = (uint16_t)b;
+        if constexpr (VALS) vals_s[slot] = vals[i];
+      }
+    }
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < tcount; j += kThreads) {
+      const int64_t d = delta[bkt_s[j]] + (int64_t)j;
+      dst[d] = keys_s[j];
+      if constexpr (VALS) dst_vals[d] = vals_s[j];
+    }
   }
 }
 
 // -------------------------------------------------------------------- K7
-__global__ void k_final_ranges(FinalRangeMeta fm, const uint8_t* __restrict__ blobs,
-                               const unsigned long long* __restrict__ minmax,
+__global__ void k_gather_bounds(const uint64_t* __restrict__ bounds, const int32_t* __restrict__ sel,
+                                int n, uint64_t* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  out[2 * i] = bounds[2 * sel[i]];
+  out[2 * i + 1] = bounds[2 * sel[i] + 1];
+}
+
+__global__ void k_final_ranges(const uint64_t* __restrict__ bounds, int nseg, int nbits,
                                DigitCls* __restrict__ out) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= fm.nseg) return;
-  const uint8_t* blob = blobs + (size_t)fm.cls[s] * kBlobStride;
-  const uint64_t* bk = reinterpret_cast<const uint64_t*>(blob + kBlobKeys);
-  const uint64_t b0 = fm.b0[s], b1 = fm.b1[s];
-  const uint64_t nb = (uint64_t)fm.nb[s];
-  uint64_t lo = b0 == 0 ? (uint64_t)minmax[0] : bk[b0 - 1];
-  uint64_t hi = b1 >= nb ? (uint64_t)minmax[1] : bk[b1 - 1];
-  if (hi < lo) hi = lo;
+  if (s >= nseg) return;
+  const uint64_t lo = bounds[2 * s], hi = bounds[2 * s + 1];
   const int bl = bit_length64(hi - lo);
-  const int nbits = fm.nbits;
   DigitCls d;
   d.lo = lo;
   d.hi = hi;
@@ -469,16 +547,56 @@ __device__ __forceinline__ void block_minmax(uint64_t& mn, uint64_t& mx, uint64_
   __syncthreads();
 }
 
-// One CTA per cell.  Cells larger than the shared-memory capacity are
-// copied when they hold one key value, otherwise recorded for another
-// partition round.  The sort is an LSD radix sort over the bits that vary
-// inside the cell (key - min), 8 bits per pass, each pass a stable
-// counting sort with match_any warp ranks — stable end to end.
+__device__ __forceinline__ void cell_of(const CellSource& cs, uint64_t cid, uint64_t& off,
+                                        uint64_t& count) {
+  if (cs.mode == 0) {
+    off = cs.cell_base[cid];
+    count = cs.cell_cnt[cid];
+  } else if (cs.mode == 1) {
+    off = cs.seg_off[cid];
+    count = cs.seg_len[cid];
+  } else {
+    off = cs.recs[cid].off;
+    count = cs.recs[cid].count;
+  }
+}
+
+// Cells too big for shared memory: copy when they hold one key value,
+// otherwise record them (with their exact key range) for another
+// partition round.  Returns true when the cell was handled here.
+template <int KIND_OUT, bool VALS>
+__device__ bool big_cell(const uint64_t* __restrict__ src, const uint64_t* __restrict__ src_vals,
+                         uint64_t* __restrict__ out, uint64_t* __restrict__ out_vals, uint64_t off,
+                         uint64_t count, OverflowRec* ovf, unsigned int* ovf_count, uint64_t* s_mm) {
+  if (count <= (uint64_t)kSortCap) return false;
+  uint64_t mn = ~0ULL, mx = 0;
+  for (uint64_t i = threadIdx.x; i < count; i += blockDim.x) {
+    const uint64_t k = src[off + i];
+    mn = min(mn, k); mx = max(mx, k);
+  }
+  block_minmax(mn, mx, s_mm);
+  if (mn == mx) {
+    const uint64_t ko = from_ordered<KIND_OUT>(mn);
+    for (uint64_t i = threadIdx.x; i < count; i += blockDim.x) {
+      out[off + i] = ko;
+      if constexpr (VALS) out_vals[off + i] = src_vals[off + i];
+    }
+  } else if (threadIdx.x == 0) {
+    const unsigned int slot = atomicAdd(ovf_count, 1u);
+    OverflowRec r; r.off = off; r.count = count; r.lo = mn; r.hi = mx;
+    ovf[slot] = r;
+  }
+  return true;
+}
+
+// Fallback for cells whose keys cluster (a sub-bucket of the counting sort
+// got too big): LSD radix sort over the bits that vary inside the cell
+// (key - min), 8 bits per pass, each pass a stable counting sort with
+// warp ranks — stable end to end.
 template <int KIND_OUT, bool VALS>
 __global__ void __launch_bounds__(kSortThreads, 1)
-    k_smem_sort(const uint64_t* __restrict__ src, const uint64_t* __restrict__ src_vals,
-                uint64_t* __restrict__ out, uint64_t* __restrict__ out_vals, CellSource cs,
-                OverflowRec* __restrict__ ovf, unsigned int* __restrict__ ovf_count) {
+    k_smem_sort_lsd(const uint64_t* __restrict__ src, const uint64_t* __restrict__ src_vals,
+                    uint64_t* __restrict__ out, uint64_t* __restrict__ out_vals, CellSource cs) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ uint64_t s_mm[2 * kSortWarps];
   __shared__ uint32_t s_scan[kSortWarps + 1];
@@ -488,41 +606,12 @@ __global__ void __launch_bounds__(kSortThreads, 1)
   uint16_t* iB = iA + kSortCap;
   uint32_t* wh = reinterpret_cast<uint32_t*>(iB + kSortCap);  // [kSortWarps][kRadix]
   uint32_t* btot = wh + kSortWarps * kRadix;
+  __shared__ uint32_t s_xch[kSortWarps][32];
 
-  const uint64_t cid = blockIdx.x;
   uint64_t off, count;
-  bool constant = false;
-  if (cs.mode == 0) {
-    off = cs.cell_base[cid];
-    count = cs.cell_cnt[cid];
-    constant = cs.dcls[cid >> cs.nbits].shift == 0;
-  } else {
-    off = cs.seg_off[cid];
-    count = cs.seg_len[cid];
-  }
-  if (count == 0) return;
+  cell_of(cs, blockIdx.x, off, count);
+  if (count == 0 || count > (uint64_t)kSortCap) return;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (count > (uint64_t)kSortCap) {
-    uint64_t mn = ~0ULL, mx = 0;
-    for (uint64_t i = threadIdx.x; i < count; i += kSortThreads) {
-      const uint64_t k = src[off + i];
-      mn = min(mn, k); mx = max(mx, k);
-    }
-    block_minmax(mn, mx, s_mm);
-    (void)constant;
-    if (mn == mx) {
-      const uint64_t ko = from_ordered<KIND_OUT>(mn);
-      for (uint64_t i = threadIdx.x; i < count; i += kSortThreads) {
-        out[off + i] = ko;
-        if constexpr (VALS) out_vals[off + i] = src_vals[off + i];
-      }
-    } else if (threadIdx.x == 0) {
-      const unsigned int slot = atomicAdd(ovf_count, 1u);
-      OverflowRec r; r.off = off; r.count = count; r.lo = mn; r.hi = mx;
-      ovf[slot] = r;
-    }
-    return;
-  }
   const uint32_t n = (uint32_t)count;
   uint64_t mn = ~0ULL, mx = 0;
   for (uint32_t i = threadIdx.x; i < n; i += kSortThreads) {
@@ -536,7 +625,6 @@ __global__ void __launch_bounds__(kSortThreads, 1)
     const int bits = bit_length64(mx - mn);
     const int passes = (bits + 7) / 8;
     const uint32_t chunk = ((n + kSortWarps - 1) / kSortWarps + 31) & ~31u;
-    const uint32_t lt = lanemask_lt();
     uint32_t* whw = wh + w * kRadix;
     for (int p = 0; p < passes; ++p) {
       const int sh = 8 * p;
@@ -548,13 +636,8 @@ __global__ void __launch_bounds__(kSortThreads, 1)
         const uint32_t e = w * chunk + it * 32 + lane;
         const bool valid = (it * 32 < (int)chunk) && e < n;
         const uint32_t d = valid ? (uint32_t)(((kA[e] - mn) >> sh) & 255) : kInvalid;
-        const uint32_t peers = __match_any_sync(0xffffffffu, d);
-        uint32_t cnt = 0;
-        if (valid) { cnt = whw[d]; pk[it] = (d << 16) | (cnt + __popc(peers & lt)); }
-        else pk[it] = kInvalid;
-        __syncwarp();
-        if (valid && lane == __ffs(peers) - 1) whw[d] = cnt + __popc(peers);
-        __syncwarp();
+        const uint32_t r = warp_stable_rank(d, lane, whw, s_xch[w]);
+        pk[it] = valid ? ((d << 16) | r) : kInvalid;
       }
       __syncthreads();
       for (int d = threadIdx.x; d < kRadix; d += kSortThreads) {
@@ -587,6 +670,119 @@ __global__ void __launch_bounds__(kSortThreads, 1)
   for (uint32_t i = threadIdx.x; i < n; i += kSortThreads) {
     out[off + i] = from_ordered<KIND_OUT>(kA[i]);
     if constexpr (VALS) out_vals[off + i] = src_vals[off + iA[i]];
+  }
+}
+
+// One CTA per cell (<= kSortCap keys): counting sort of the keys into
+// ~n/2 sub-buckets by their top varying bits (shared atomics), then an
+// insertion sort of every sub-bucket (ties by input index when values
+// ride along, so the result is stable).  Cells whose keys cluster (a
+// sub-bucket above kInsertMax) go to the LSD fallback list.
+constexpr int kSubBits = 12;
+constexpr int kInsertMax = 32;
+
+template <int KIND_OUT, bool VALS>
+__global__ void __launch_bounds__(kSortThreads)
+    k_smem_sort(const uint64_t* __restrict__ src, const uint64_t* __restrict__ src_vals,
+                uint64_t* __restrict__ out, uint64_t* __restrict__ out_vals, CellSource cs,
+                OverflowRec* __restrict__ ovf, unsigned int* __restrict__ ovf_count,
+                OverflowRec* __restrict__ fb, unsigned int* __restrict__ fb_count) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ uint64_t s_mm[2 * kSortWarps];
+  __shared__ uint32_t s_scan[kSortWarps + 1];
+  __shared__ uint32_t s_max[kSortWarps];
+  uint64_t* kB = reinterpret_cast<uint64_t*>(smem);
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(kB + kSortCap);   // [1 << kSubBits]
+  uint16_t* iB = reinterpret_cast<uint16_t*>(cnt + (1 << kSubBits));
+
+  uint64_t off, count;
+  cell_of(cs, blockIdx.x, off, count);
+  if (count == 0) return;
+  if (big_cell<KIND_OUT, VALS>(src, src_vals, out, out_vals, off, count, ovf, ovf_count, s_mm))
+    return;
+  const uint32_t n = (uint32_t)count;
+  uint64_t kr[kSortItems];
+  uint64_t mn = ~0ULL, mx = 0;
+#pragma unroll
+  for (int it = 0; it < kSortItems; ++it) {
+    const uint32_t i = it * kSortThreads + threadIdx.x;
+    kr[it] = i < n ? ldg_stream(src + off + i) : 0;
+    if (i < n) { mn = min(mn, kr[it]); mx = max(mx, kr[it]); }
+  }
+  block_minmax(mn, mx, s_mm);
+  if (mn == mx) {
+    const uint64_t ko = from_ordered<KIND_OUT>(mn);
+    for (uint32_t i = threadIdx.x; i < n; i += kSortThreads) {
+      out[off + i] = ko;
+      if constexpr (VALS) out_vals[off + i] = src_vals[off + i];
+    }
+    return;
+  }
+  int lg = bit_length64((uint64_t)n - 1) - 1;   // ~n/2 sub-buckets
+  lg = lg < 1 ? 1 : (lg > kSubBits ? kSubBits : lg);
+  const int bl = bit_length64(mx - mn);
+  const int sh = bl > lg ? bl - lg : 0;
+  const uint32_t nsub = (uint32_t)((mx - mn) >> sh) + 1;
+  for (uint32_t j = threadIdx.x; j < nsub; j += kSortThreads) cnt[j] = 0;
+  __syncthreads();
+#pragma unroll
+  for (int it = 0; it < kSortItems; ++it) {
+    const uint32_t i = it * kSortThreads + threadIdx.x;
+    if (i < n) atomicAdd(&cnt[(uint32_t)((kr[it] - mn) >> sh)], 1u);
+  }
+  __syncthreads();
+  uint32_t big = 0;
+  for (uint32_t j = threadIdx.x; j < nsub; j += kSortThreads) big = max(big, cnt[j]);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) big = max(big, __shfl_xor_sync(0xffffffffu, big, o));
+  if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = big;
+  block_excl_scan<kSortThreads>(cnt, (int)nsub, s_scan);
+  big = 0;
+  for (int w = 0; w < kSortWarps; ++w) big = max(big, s_max[w]);
+  // Exact-key sub-buckets (sh == 0) hold one key each: fine without values.
+  if (big > (uint32_t)kInsertMax && (VALS || sh != 0)) {
+    if (threadIdx.x == 0) {
+      const unsigned int slot = atomicAdd(fb_count, 1u);
+      OverflowRec r; r.off = off; r.count = count; r.lo = mn; r.hi = mx;
+      fb[slot] = r;
+    }
+    return;
+  }
+#pragma unroll
+  for (int it = 0; it < kSortItems; ++it) {
+    const uint32_t i = it * kSortThreads + threadIdx.x;
+    if (i < n) {
+      const uint32_t slot = atomicAdd(&cnt[(uint32_t)((kr[it] - mn) >> sh)], 1u);
+      kB[slot] = kr[it];
+      if constexpr (VALS) iB[slot] = (uint16_t)i;
+    }
+  }
+  __syncthreads();
+  // cnt[j] is now the end of sub-bucket j.
+  for (uint32_t j = threadIdx.x; j < nsub; j += kSortThreads) {
+    const uint32_t b0 = j ? cnt[j - 1] : 0, b1 = cnt[j];
+    for (uint32_t a = b0 + 1; a < b1; ++a) {
+      const uint64_t k = kB[a];
+      uint16_t ix = 0;
+      if constexpr (VALS) ix = iB[a];
+      uint32_t c = a;
+      while (c > b0) {
+        const uint64_t pkey = kB[c - 1];
+        bool gt = pkey > k;
+        if constexpr (VALS) gt = gt || (pkey == k && iB[c - 1] > ix);
+        if (!gt) break;
+        kB[c] = pkey;
+        if constexpr (VALS) iB[c] = iB[c - 1];
+        --c;
+      }
+      kB[c] = k;
+      if constexpr (VALS) iB[c] = ix;
+    }
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < n; i += kSortThreads) {
+    out[off + i] = from_ordered<KIND_OUT>(kB[i]);
+    if constexpr (VALS) out_vals[off + i] = src_vals[off + iB[i]];
   }
 }
 
@@ -638,13 +834,14 @@ cudaError_t launch_build_cls(cudaStream_t st, int ngroups, const uint64_t* sorte
 }
 
 size_t hist_smem_bytes(int nb_stride, int nspl_cap, int cells_cap, bool digit) {
-  return (size_t)8 * nb_stride + (digit ? 0 : tree_smem_bytes(nspl_cap, cells_cap));
+  return (((size_t)4 * nb_stride + 15) & ~(size_t)15) +
+         (digit ? 0 : tree_smem_bytes(nspl_cap, cells_cap));
 }
 
 cudaError_t launch_hist(cudaStream_t st, const void* src, int kind, bool digit, const SegMeta& m,
                         uint64_t nchunks, const uint8_t* blobs, const DigitCls* dcls, int nspl_cap,
-                        int cells_cap, int nb_stride, uint32_t* tile_hist, uint32_t* chunk_tot,
-                        uint32_t* seg_hist, unsigned long long* minmax) {
+                        int cells_cap, int nb_stride, uint32_t* chunk_tot, uint32_t* seg_hist,
+                        unsigned long long* minmax) {
   if (nchunks == 0) return cudaSuccess;
   const size_t smem = hist_smem_bytes(nb_stride, nspl_cap, cells_cap, digit);
   const uint64_t* s = static_cast<const uint64_t*>(src);
@@ -654,14 +851,14 @@ cudaError_t launch_hist(cudaStream_t st, const void* src, int kind, bool digit, 
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     fn<<<(unsigned)nchunks, kThreads, smem, st>>>(s, m, blobs, dcls, nspl_cap, nb_stride,
-                                                   tile_hist, chunk_tot, seg_hist, minmax);
+                                                   chunk_tot, seg_hist, minmax);
   } else {
     AMS_KIND_DISPATCH(kind, K, {
       auto fn = k_hist<K, false>;
       e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
       fn<<<(unsigned)nchunks, kThreads, smem, st>>>(s, m, blobs, dcls, nspl_cap, nb_stride,
-                                                     tile_hist, chunk_tot, seg_hist, minmax);
+                                                     chunk_tot, seg_hist, minmax);
     });
   }
   return cudaGetLastError();
@@ -690,25 +887,43 @@ cudaError_t launch_digit_base(cudaStream_t st, const uint32_t* seg_hist, int nb_
   return cudaGetLastError();
 }
 
-size_t scatter_smem_bytes(int nb_stride, int nspl_cap, int cells_cap, bool digit, bool vals) {
-  size_t b = (vals ? 16 : 8) * (size_t)kTile;       // keys (+vals)
-  b += 8 * (size_t)nb_stride;                       // delta
-  b += 4 * (size_t)kWarps * nb_stride;              // warp histograms
-  b += 4 * (size_t)nb_stride;                       // bucket totals
-  b += 2 * (size_t)kTile;                           // bucket ids
+cudaError_t launch_child_bounds(cudaStream_t st, const uint8_t* blobs, const GroupMeta& gm,
+                                int ngroups, int r, const uint64_t* parent, uint64_t* child) {
+  const int n = ngroups * r;
+  if (n == 0) return cudaSuccess;
+  k_child_bounds<<<(n + 127) / 128, 128, 0, st>>>(blobs, gm, ngroups, r, parent, child);
+  return cudaGetLastError();
+}
+
+constexpr int kSerialAbove = 1024;  // buckets beyond which warps share one counter array
+
+int scatter_mode(int nb_stride, bool stable) {
+  if (!stable) return kRankAtomic;
+  return nb_stride > kSerialAbove ? kRankSerial : kRankWarp;
+}
+
+size_t scatter_smem_bytes(int nb_stride, int nspl_cap, int cells_cap, bool digit, bool vals,
+                          bool stable) {
+  const int mode = scatter_mode(nb_stride, stable);
+  size_t b = (vals ? 16 : 8) * (size_t)kTile;                         // keys (+vals)
+  b += 16 * (size_t)nb_stride;                                        // run + delta
+  b += 4 * (size_t)(mode == kRankWarp ? kWarps : 1) * nb_stride;      // bucket counters
+  b += 8 * (size_t)nb_stride;                                         // totals + tile counts
+  b += 2 * (size_t)kTile;                                             // bucket ids
   b = (b + 15) & ~(size_t)15;
-  if (!digit) b += tree_smem_bytes(nspl_cap, cells_cap);
+  if (!digit) b += tree_smem_bytes(nspl_cap, cells_cap) + 16;
   return b;
 }
 
 cudaError_t launch_scatter(cudaStream_t st, const void* src, const void* src_vals, int kind,
-                           bool digit, void* dst, void* dst_vals, const SegMeta& m, uint64_t ntiles,
-                           const uint8_t* blobs, const DigitCls* dcls, int nspl_cap, int cells_cap,
-                           int nb_stride, const uint32_t* tile_hist, const uint32_t* chunk_tot,
+                           bool digit, bool stable, void* dst, void* dst_vals, const SegMeta& m,
+                           uint64_t nchunks, const uint8_t* blobs, const DigitCls* dcls,
+                           int nspl_cap, int cells_cap, int nb_stride, const uint32_t* chunk_tot,
                            const uint64_t* cell_base) {
-  if (ntiles == 0) return cudaSuccess;
+  if (nchunks == 0) return cudaSuccess;
   const bool vals = src_vals != nullptr;
-  const size_t smem = scatter_smem_bytes(nb_stride, nspl_cap, cells_cap, digit, vals);
+  const int mode = scatter_mode(nb_stride, stable);
+  const size_t smem = scatter_smem_bytes(nb_stride, nspl_cap, cells_cap, digit, vals, stable);
   const uint64_t* s = static_cast<const uint64_t*>(src);
   const uint64_t* sv = static_cast<const uint64_t*>(src_vals);
   uint64_t* d = static_cast<uint64_t*>(dst);
@@ -716,11 +931,13 @@ cudaError_t launch_scatter(cudaStream_t st, const void* src, const void* src_val
   cudaError_t e = cudaSuccess;
 #define AMS_SCATTER_GO(K, DG, V)                                                              \
   {                                                                                           \
-    auto fn = k_scatter<K, DG, V>;                                                            \
+    auto fn = mode == kRankWarp ? k_scatter<K, DG, V, kRankWarp>                              \
+              : mode == kRankSerial ? k_scatter<K, DG, V, kRankSerial>                        \
+                                    : k_scatter<K, DG, V, kRankAtomic>;                       \
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
     if (e != cudaSuccess) return e;                                                           \
-    fn<<<(unsigned)ntiles, kThreads, smem, st>>>(s, sv, d, dv, m, blobs, dcls, nspl_cap,      \
-                                                  nb_stride, tile_hist, chunk_tot, cell_base); \
+    fn<<<(unsigned)nchunks, kThreads, smem, st>>>(s, sv, d, dv, m, blobs, dcls, nspl_cap,     \
+                                                   nb_stride, chunk_tot, cell_base);          \
   }
   if (digit) {
     if (vals) AMS_SCATTER_GO(AMS_KEY_U64, true, true) else AMS_SCATTER_GO(AMS_KEY_U64, true, false)
@@ -733,20 +950,32 @@ cudaError_t launch_scatter(cudaStream_t st, const void* src, const void* src_val
   return cudaGetLastError();
 }
 
-cudaError_t launch_final_ranges(cudaStream_t st, const FinalRangeMeta& fm, const uint8_t* blobs,
-                                const unsigned long long* minmax, DigitCls* out) {
-  if (fm.nseg == 0) return cudaSuccess;
-  k_final_ranges<<<(fm.nseg + 127) / 128, 128, 0, st>>>(fm, blobs, minmax, out);
+cudaError_t launch_gather_bounds(cudaStream_t st, const uint64_t* bounds, const int32_t* sel, int n,
+                                 uint64_t* out) {
+  if (n == 0) return cudaSuccess;
+  k_gather_bounds<<<(n + 127) / 128, 128, 0, st>>>(bounds, sel, n, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_final_ranges(cudaStream_t st, const uint64_t* bounds, int nseg, int nbits,
+                                DigitCls* out) {
+  if (nseg == 0) return cudaSuccess;
+  k_final_ranges<<<(nseg + 127) / 128, 128, 0, st>>>(bounds, nseg, nbits, out);
   return cudaGetLastError();
 }
 
 size_t smem_sort_bytes() {
+  return (size_t)kSortCap * 8 + ((size_t)4 << kSubBits) + (size_t)kSortCap * 2;
+}
+
+size_t smem_sort_lsd_bytes() {
   return (size_t)kSortCap * (8 + 8 + 2 + 2) + (size_t)4 * kSortWarps * kRadix + 4 * kRadix;
 }
 
 cudaError_t launch_smem_sort(cudaStream_t st, const void* src, const void* src_vals, void* out,
                              void* out_vals, int kind_out, const CellSource& cs, uint64_t ncells,
-                             OverflowRec* ovf, unsigned int* ovf_count) {
+                             OverflowRec* ovf, unsigned int* ovf_count, OverflowRec* fb,
+                             unsigned int* fb_count) {
   if (ncells == 0) return cudaSuccess;
   const size_t smem = smem_sort_bytes();
   const uint64_t* s = static_cast<const uint64_t*>(src);
@@ -754,12 +983,39 @@ cudaError_t launch_smem_sort(cudaStream_t st, const void* src, const void* src_v
   uint64_t* o = static_cast<uint64_t*>(out);
   uint64_t* ov = static_cast<uint64_t*>(out_vals);
   cudaError_t e = cudaSuccess;
+#define AMS_SORT_GO(K, V)                                                                   \
+  {                                                                                         \
+    auto fn = k_smem_sort<K, V>;                                                            \
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);   \
+    if (e != cudaSuccess) return e;                                                         \
+    fn<<<(unsigned)ncells, kSortThreads, smem, st>>>(s, sv, o, ov, cs, ovf, ovf_count, fb,   \
+                                                     fb_count);                             \
+  }
+  if (sv) {
+    AMS_KIND_DISPATCH(kind_out, K, AMS_SORT_GO(K, true))
+  } else {
+    AMS_KIND_DISPATCH(kind_out, K, AMS_SORT_GO(K, false))
+  }
+#undef AMS_SORT_GO
+  return cudaGetLastError();
+}
+
+cudaError_t launch_smem_sort_lsd(cudaStream_t st, const void* src, const void* src_vals, void* out,
+                                 void* out_vals, int kind_out, const CellSource& cs,
+                                 uint64_t ncells) {
+  if (ncells == 0) return cudaSuccess;
+  const size_t smem = smem_sort_lsd_bytes();
+  const uint64_t* s = static_cast<const uint64_t*>(src);
+  const uint64_t* sv = static_cast<const uint64_t*>(src_vals);
+  uint64_t* o = static_cast<uint64_t*>(out);
+  uint64_t* ov = static_cast<uint64_t*>(out_vals);
+  cudaError_t e = cudaSuccess;
 #define AMS_SORT_GO(K, V)                                                                 \
   {                                                                                       \
-    auto fn = k_smem_sort<K, V>;                                                          \
+    auto fn = k_smem_sort_lsd<K, V>;                                                      \
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
     if (e != cudaSuccess) return e;                                                       \
-    fn<<<(unsigned)ncells, kSortThreads, smem, st>>>(s, sv, o, ov, cs, ovf, ovf_count);    \
+    fn<<<(unsigned)ncells, kSortThreads, smem, st>>>(s, sv, o, ov, cs);                   \
   }
   if (sv) {
     AMS_KIND_DISPATCH(kind_out, K, AMS_SORT_GO(K, true))

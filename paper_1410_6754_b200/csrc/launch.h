@@ -13,7 +13,6 @@ struct SegMeta {
   const uint64_t* off;           // [nseg] start index in the source buffer
   const uint64_t* len;           // [nseg]
   const int32_t* cls;            // [nseg] classifier index
-  const uint64_t* tile_prefix;   // [nseg+1] first global tile of each segment
   const uint64_t* chunk_prefix;  // [nseg+1] first global chunk of each segment
   const int64_t* posbase;        // [ncls] tie-break position = index + posbase
   int nseg;
@@ -27,17 +26,9 @@ struct GroupMeta {
   const uint64_t* dst_start;  // [ngroups] output start of the group
 };
 
-struct FinalRangeMeta {
-  const int32_t* cls;
-  const uint64_t* b0;
-  const uint64_t* b1;
-  const int32_t* nb;
-  int nseg;
-  int nbits;
-};
-
 // Work list of the shared-memory sort: mode 0 = cells of a digit
-// partition (cell id = seg << nbits | digit), mode 1 = explicit segments.
+// partition (cell id = seg << nbits | digit), mode 1 = explicit segments,
+// mode 2 = records (fallback list on the device).
 struct CellSource {
   int mode;
   int nbits;
@@ -46,6 +37,7 @@ struct CellSource {
   const DigitCls* dcls;
   const uint64_t* seg_off;
   const uint64_t* seg_len;
+  const OverflowRec* recs;
 };
 
 cudaError_t launch_gather_sample(cudaStream_t st, const void* src, int kind, const uint64_t* idx,
@@ -60,26 +52,40 @@ cudaError_t launch_build_cls(cudaStream_t st, int ngroups, const uint64_t* sorte
 size_t hist_smem_bytes(int nb_stride, int nspl_cap, int cells_cap, bool digit);
 cudaError_t launch_hist(cudaStream_t st, const void* src, int kind, bool digit, const SegMeta& m,
                         uint64_t nchunks, const uint8_t* blobs, const DigitCls* dcls, int nspl_cap,
-                        int cells_cap, int nb_stride, uint32_t* tile_hist, uint32_t* chunk_tot,
-                        uint32_t* seg_hist, unsigned long long* minmax);
+                        int cells_cap, int nb_stride, uint32_t* chunk_tot, uint32_t* seg_hist,
+                        unsigned long long* minmax);
 cudaError_t launch_chunk_scan(cudaStream_t st, uint32_t* chunk_tot, const SegMeta& m, int nb_stride);
 cudaError_t launch_cell_base(cudaStream_t st, const uint32_t* seg_hist, int nb_stride,
                              const GroupMeta& gm, int ngroups, int r, uint64_t* pieces,
                              uint64_t* cell_base);
 cudaError_t launch_digit_base(cudaStream_t st, const uint32_t* seg_hist, int nb_stride,
                               const SegMeta& m, uint64_t* cell_base);
-size_t scatter_smem_bytes(int nb_stride, int nspl_cap, int cells_cap, bool digit, bool vals);
+size_t scatter_smem_bytes(int nb_stride, int nspl_cap, int cells_cap, bool digit, bool vals,
+                          bool stable);
+// stable=false lets items of one tile land in any order inside their
+// bucket run (keys-only last level / final partition: only membership matters).
 cudaError_t launch_scatter(cudaStream_t st, const void* src, const void* src_vals, int kind,
-                           bool digit, void* dst, void* dst_vals, const SegMeta& m, uint64_t ntiles,
-                           const uint8_t* blobs, const DigitCls* dcls, int nspl_cap, int cells_cap,
-                           int nb_stride, const uint32_t* tile_hist, const uint32_t* chunk_tot,
+                           bool digit, bool stable, void* dst, void* dst_vals, const SegMeta& m,
+                           uint64_t nchunks, const uint8_t* blobs, const DigitCls* dcls,
+                           int nspl_cap, int cells_cap, int nb_stride, const uint32_t* chunk_tot,
                            const uint64_t* cell_base);
-cudaError_t launch_final_ranges(cudaStream_t st, const FinalRangeMeta& fm, const uint8_t* blobs,
-                                const unsigned long long* minmax, DigitCls* out);
-size_t smem_sort_bytes();
+// Child-group key bounds [2*(g*r+t)] from parent bounds [2*g] and the plan.
+cudaError_t launch_child_bounds(cudaStream_t st, const uint8_t* blobs, const GroupMeta& gm,
+                                int ngroups, int r, const uint64_t* parent, uint64_t* child);
+cudaError_t launch_gather_bounds(cudaStream_t st, const uint64_t* bounds, const int32_t* sel, int n,
+                                 uint64_t* out);
+cudaError_t launch_final_ranges(cudaStream_t st, const uint64_t* bounds, int nseg, int nbits,
+                                DigitCls* out);
+// Counting + insertion sort of every cell; cells above the shared-memory
+// capacity go to `ovf` (or are copied when constant), clustered cells to `fb`.
 cudaError_t launch_smem_sort(cudaStream_t st, const void* src, const void* src_vals, void* out,
                              void* out_vals, int kind_out, const CellSource& cs, uint64_t ncells,
-                             OverflowRec* ovf, unsigned int* ovf_count);
+                             OverflowRec* ovf, unsigned int* ovf_count, OverflowRec* fb,
+                             unsigned int* fb_count);
+// LSD radix fallback for the `fb` records.
+cudaError_t launch_smem_sort_lsd(cudaStream_t st, const void* src, const void* src_vals, void* out,
+                                 void* out_vals, int kind_out, const CellSource& cs,
+                                 uint64_t ncells);
 cudaError_t launch_map_keys(cudaStream_t st, const void* src, void* dst, uint64_t n, int from,
                             int to);
 

@@ -155,6 +155,15 @@ class AmsSorter:
             out = torch.empty_like(keys)
         if vals is not None and out_vals is None:
             out_vals = torch.empty_like(vals)
+        ret_out, ret_vals = out, out_vals
+        if n == 0:
+            # Empty tensors have no storage; every segment is empty, so the
+            # kernels never touch these one-element stand-ins.
+            keys = torch.zeros(1, dtype=keys.dtype, device=keys.device)
+            out = torch.zeros_like(keys)
+            if vals is not None:
+                vals = torch.zeros(1, dtype=vals.dtype, device=vals.device)
+                out_vals = torch.zeros_like(vals)
         stream = torch.cuda.current_stream(self.device)
         self.ctx.set_stream(stream.cuda_stream)
         launches0 = self.ctx.launches
@@ -191,7 +200,11 @@ class AmsSorter:
                                            nb_stride, track_minmax=(lv == 0))
             bnd, loads, mx, new_sizes, stats = L.plan_level(gn, nb, r, hist, with_stats)
             dst, dst_v = work[lv % 2], work_v[lv % 2]
-            self.ctx.level_scatter(src, src_v, src_kind, dst, dst_v, r, bnd, offs[gf])
+            # Only PE membership matters at the last level (F7): keys-only
+            # runs may drop in-tile order there.
+            last_level = lv == len(params.group_counts) - 1
+            self.ctx.level_scatter(src, src_v, src_kind, dst, dst_v, r, bnd, offs[gf],
+                                   stable=not (last_level and vals is None))
             rec = LevelRecord(lv, r, gf.copy(), gn.copy(), sizes.copy(), drawn, nb, hist, bnd,
                               loads, mx, load_budget(n_g, r, eps_l), new_sizes, stats)
             if record_splitters:
@@ -203,18 +216,11 @@ class AmsSorter:
             gf = (gf[:, None] + np.arange(r, dtype=np.int32)[None, :] * step[:, None]).reshape(-1)
             gf = gf.astype(np.int32)
             gn = np.repeat(step, r).astype(np.int32)
-        # Final local sort (ams.py:310-312).  Final PE t of last-level group g
-        # holds buckets [B_t, B_{t+1}) of g.
-        last = levels[-1]
+        # Final local sort (ams.py:310-312): final PE s = child s of the
+        # last level; its key bounds were derived by the last scatter.
         k = len(params.group_counts)
         offs = np.zeros(p + 1, np.uint64)
         np.cumsum(sizes, out=offs[1:])
-        pe_group = np.repeat(np.arange(len(last.group_first), dtype=np.int32), last.group_npe)
-        t_local = np.arange(p) - last.group_first[pe_group]
-        b0 = last.boundaries[pe_group, t_local]
-        b1 = last.boundaries[pe_group, t_local + 1]
-        seg_nb = last.bucket_count[pe_group]
         tmp, tmp_v = work[k % 2], work_v[k % 2]
-        self.ctx.final_sort(src, src_v, tmp, tmp_v, out, out_vals, kind, offs[:-1], sizes,
-                            pe_group, b0, b1, seg_nb)
-        return SortOutput(out, out_vals, sizes, levels, self.ctx.launches - launches0)
+        self.ctx.final_sort(src, src_v, tmp, tmp_v, out, out_vals, kind, offs[:-1], sizes)
+        return SortOutput(ret_out, ret_vals, sizes, levels, self.ctx.launches - launches0)

@@ -1,0 +1,212 @@
+"""GPU parity: the CUDA path (through libams_b200.so) against the reference's
+golden fixtures and the CPU oracle.
+
+Bar: output bit-exact with the reference and numpy.sort;
+per-level splitters, histograms, plans and member sizes identical to the
+reference when the sample streams are the same; per-PE sizes within
+(1+eps)·n/p where the reference met its budget; stable payload order.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import ams_oracle as O
+from tests import golden_util as G
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def api():
+    from paper_1410_6754_b200 import api as A
+    return A
+
+
+def dev_u64(a: np.ndarray) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.uint64).view(np.int64)).cuda()
+
+
+def host_u64(t: torch.Tensor) -> np.ndarray:
+    return t.cpu().numpy().view(np.uint64)
+
+
+def run_gpu(api, keys, sizes, groups, a, b, eps, master, stream, vals=True, record=True):
+    from paper_1410_6754_b200 import AmsParams, SeedSpec
+    d_keys = dev_u64(keys)
+    d_vals = torch.arange(len(keys), dtype=torch.int64, device="cuda") if vals else None
+    res = api.ams_sort_tensors(d_keys, sizes, AmsParams(tuple(groups), a, b, eps),
+                               SeedSpec(master, stream), vals=d_vals, key_kind="u64",
+                               record_splitters=record)
+    torch.cuda.synchronize()
+    return res
+
+
+def check_levels(res, g):
+    assert len(res.levels) == len(g["levels"])
+    for lv, (rec, refs) in enumerate(zip(res.levels, g["levels"])):
+        assert len(rec.group_first) == len(refs)
+        row = 0
+        for gi, ref in enumerate(refs):
+            P = int(rec.group_npe[gi])
+            assert int(rec.sample_size[gi]) == ref["sample_size"]
+            assert int(rec.bucket_count[gi]) == ref["bucket_count"]
+            nb = ref["bucket_count"]
+            ghist = rec.seg_hist[row:row + P, :nb].astype(np.int64).sum(axis=0)
+            assert ghist.tolist() == ref["global_hist"], f"level {lv} group {gi} histogram"
+            assert [int(x) for x in rec.boundaries[gi]] == ref["boundaries"]
+            assert [int(x) for x in rec.loads[gi]] == ref["loads"]
+            assert [int(x) for x in rec.new_sizes[row:row + P]] == ref["new_sizes"]
+            if rec.splitters:
+                sk, sp = rec.splitters[gi]
+                assert [int(x) for x in sk] == ref["splitter_keys"], f"level {lv} group {gi} splitters"
+                assert [int(x) for x in sp] == ref["splitter_pos"]
+            row += P
+    for mine, ref in zip(res.reports, g["reports"]):
+        for k, v in ref.items():
+            assert mine[k] == v, (k, mine[k], v)
+
+
+@pytest.mark.parametrize("name", G.names())
+def test_golden_parity(api, name):
+    g = G.load(name)
+    keys, sizes = G.input_of(g)
+    assert G.sha_u64(keys) == g["input_sha256"]
+    res = run_gpu(api, keys, sizes, g["groups"], g["a"], g["b"], g["eps"], g["master_seed"],
+                  g["stream"])
+    out = host_u64(res.keys)
+    assert [int(x) for x in res.pe_sizes] == g["pe_sizes"]
+    assert G.sha_u64(out) == g["output_sha256"]
+    assert G.sha_i64(res.vals.cpu().numpy()) == g["origin_sha256"]
+    check_levels(res, g)
+
+
+@pytest.mark.parametrize("name", [n for n in G.names() if n.startswith("tiny")])
+def test_dropin_elements(api, name):
+    """ams_sort(net, data, params, scheme, seed) returns the reference's
+    exact per-PE Element lists."""
+    from paper_1410_6754_b200 import AmsParams, Element, SeedSpec
+
+    class Net:
+        def __init__(self, p):
+            self.p = p
+
+    g = G.load(name)
+    p = g["p"]
+    data = {pe: [Element(k, o, i) for k, o, i in g["data"][str(pe)]] for pe in range(p)}
+    out, reports = api.ams_sort(Net(p), data, AmsParams(tuple(g["groups"]), g["a"], g["b"], g["eps"]),
+                                "simple", SeedSpec(g["master_seed"], g["stream"]))
+    flat = [list(e) for pe in range(p) for e in out[pe]]
+    assert flat == g["output"]
+    assert [len(out[pe]) for pe in range(p)] == g["pe_sizes"]
+    for mine, ref in zip(reports, g["reports"]):
+        for k, v in ref.items():
+            assert mine[k] == v
+
+
+@pytest.mark.parametrize("groups,npe,dist", [
+    ((8, 8), 1 << 12, "uniform"), ((8, 8), 3000, "zipf"), ((4, 4, 4), 2048, "uniform"),
+    ((8, 32), 1 << 10, "sorted"), ((8, 32), 1 << 10, "reverse"), ((8, 32), 1 << 10, "equal"),
+    ((16,), 1 << 16, "uniform"), ((2, 8), 50_000, "few"), ((64,), 777, "uniform"),
+    ((256,), 64, "uniform"), ((8, 32), 4096, "zipf"),
+])
+def test_oracle_parity_random(api, groups, npe, dist):
+    """Seeded inputs beyond the fixtures, checked level by level against the
+    oracle (itself pinned to the reference)."""
+    p = int(np.prod(groups))
+    n = p * npe
+    rng = np.random.default_rng(hash((groups, npe, dist)) & 0xFFFF)
+    if dist == "uniform":
+        keys = rng.integers(0, 2**64, n, dtype=np.uint64)
+    elif dist == "zipf":
+        keys = O.zipf_keys(n, 11)
+    elif dist == "sorted":
+        keys = np.arange(n, dtype=np.uint64)
+    elif dist == "reverse":
+        keys = (n - 1 - np.arange(n)).astype(np.uint64)
+    elif dist == "equal":
+        keys = np.full(n, 42, dtype=np.uint64)
+    else:  # few distinct values spread over the whole range
+        keys = rng.choice(np.array([0, 1, 2**40, 2**63, 2**64 - 1], dtype=np.uint64), n)
+    sizes = [npe] * p
+    vals = np.arange(n, dtype=np.int64)
+    ref = O.ams_sort(keys, sizes, groups, None, 16, 0.1, 77, "algo/rep0", vals=vals)
+    res = run_gpu(api, keys, sizes, groups, None, 16, 0.1, 77, "algo/rep0")
+    out = host_u64(res.keys)
+    assert np.array_equal(out, ref.keys)
+    assert np.array_equal(res.vals.cpu().numpy(), ref.vals)
+    assert [int(x) for x in res.pe_sizes] == list(ref.pe_sizes)
+    for rec, infos in zip(res.levels, ref.levels):
+        for gi, info in enumerate(infos):
+            assert [int(x) for x in rec.boundaries[gi]] == list(info.plan.boundaries)
+            sk, sp = rec.splitters[gi]
+            assert np.array_equal(sk, info.splitter_keys)
+            assert np.array_equal(sp.astype(np.int64), info.splitter_pos)
+
+
+def test_ragged_and_empty_pes(api):
+    rng = np.random.default_rng(5)
+    sizes = [0, 5, 0, 0, 10_000, 1, 3, 0] + [int(x) for x in rng.integers(0, 3000, 56)]
+    n = sum(sizes)
+    keys = rng.integers(0, 1000, n).astype(np.uint64)
+    ref = O.ams_sort(keys, sizes, (8, 8), None, 16, 0.2, 3, "root", vals=np.arange(n))
+    res = run_gpu(api, keys, sizes, (8, 8), None, 16, 0.2, 3, "root")
+    assert np.array_equal(host_u64(res.keys), ref.keys)
+    assert np.array_equal(res.vals.cpu().numpy(), ref.vals)
+    assert [int(x) for x in res.pe_sizes] == list(ref.pe_sizes)
+
+
+def test_empty_input(api):
+    res = run_gpu(api, np.zeros(0, np.uint64), [0] * 4, (2, 2), None, 16, 0.2, 1, "root")
+    assert res.keys.numel() == 0 and list(res.pe_sizes) == [0] * 4
+
+
+def test_float64_and_int64_keys(api):
+    from paper_1410_6754_b200 import AmsParams, SeedSpec
+    rng = np.random.default_rng(2)
+    n = 1 << 20
+    f = rng.standard_normal(n) * 1e3
+    f[:10] = [0.0, 1.5, -1.5, np.inf, -np.inf, 1e-300, -1e-300, 3.0, 3.0, -2.0]
+    res = api.ams_sort_tensors(torch.from_numpy(f).cuda(), [n // 16] * 16, AmsParams((4, 4)),
+                               SeedSpec(1))
+    assert np.array_equal(res.keys.cpu().numpy(), np.sort(f))
+    i = rng.integers(-2**63, 2**63 - 1, n, dtype=np.int64)
+    res = api.ams_sort_tensors(torch.from_numpy(i).cuda(), [n // 16] * 16, AmsParams((16,)),
+                               SeedSpec(1))
+    assert np.array_equal(res.keys.cpu().numpy(), np.sort(i))
+
+
+def test_deterministic_repeat(api):
+    rng = np.random.default_rng(9)
+    n = 1 << 21
+    keys = rng.integers(0, 2**64, n, dtype=np.uint64)
+    a = run_gpu(api, keys, [n // 64] * 64, (8, 8), None, 16, 0.1, 1, "algo/rep0", record=False)
+    ka, va = host_u64(a.keys).copy(), a.vals.cpu().numpy().copy()
+    b = run_gpu(api, keys, [n // 64] * 64, (8, 8), None, 16, 0.1, 1, "algo/rep0", record=False)
+    assert np.array_equal(ka, host_u64(b.keys)) and np.array_equal(va, b.vals.cpu().numpy())
+
+
+@pytest.mark.parametrize("dist", ["uniform", "zipf", "sorted", "reverse", "equal"])
+def test_config2_full_size_properties(api, dist):
+    """BASELINE config 2 shape (n=2^28, p=64, (8,8), eps=0.1) at full size:
+    output == numpy.sort, per-PE sizes within (1+eps)·n/p."""
+    from paper_1410_6754_b200 import AmsParams, SeedSpec
+    n = 1 << 28
+    if dist == "uniform":
+        keys = np.random.default_rng(1).integers(0, 2**64, n, dtype=np.uint64)
+    elif dist == "zipf":
+        keys = O.zipf_keys(n, 4)
+    elif dist == "sorted":
+        keys = np.arange(n, dtype=np.uint64)
+    elif dist == "reverse":
+        keys = (n - 1 - np.arange(n)).astype(np.uint64)
+    else:
+        keys = np.full(n, 42, dtype=np.uint64)
+    d_keys = dev_u64(keys)
+    res = api.ams_sort_tensors(d_keys, [n // 64] * 64, AmsParams((8, 8), None, 16, 0.1),
+                               SeedSpec(1, "algo/rep0"), key_kind="u64")
+    out = host_u64(res.keys)
+    keys.sort(kind="stable")
+    assert np.array_equal(out, keys)
+    assert int(res.pe_sizes.max()) <= 1.1 * n / 64
+    assert sum(r["over_budget"] for r in res.reports) == 0
