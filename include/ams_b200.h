@@ -43,7 +43,7 @@ extern "C" {
 /* Kernel tile (elements per CTA tile in the level kernels) and the
  * largest bucket the CTA-local final sort handles in shared memory. */
 #define AMS_TILE 4096
-#define AMS_SMEM_SORT_CAP 8192
+#define AMS_SMEM_SORT_CAP 4096
 #define AMS_MAX_BUCKETS 4096
 
 const char* ams_last_error(void);

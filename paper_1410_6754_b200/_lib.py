@@ -17,7 +17,7 @@ from .build import LIB
 AMS_OK, AMS_EINVAL, AMS_ECUDA, AMS_ENOMEM, AMS_EINTERNAL = 0, 1, 2, 3, 4
 KEY_U64, KEY_I64, KEY_F64 = 0, 1, 2
 TILE = 4096
-SMEM_SORT_CAP = 8192
+SMEM_SORT_CAP = 4096
 MAX_BUCKETS = 4096
 KCAT_NAMES = ("sample_gather", "sample_rank", "build_classifier", "level_hist", "chunk_scan",
               "cell_base", "level_scatter", "final_ranges", "final_hist", "final_scatter",
@@ -65,11 +65,12 @@ EXPORTED = tuple(_SIGNATURES)
 
 
 def _load():
-    if not os.path.exists(LIB):
+    path = os.environ.get("AMS_LIB", LIB)  # alternative build (experiments)
+    if not os.path.exists(path):
         raise ImportError(
             f"{LIB} is missing: build it with `python -m paper_1410_6754_b200.build` "
             "(there is no CPU fallback for the AMS-sort hot path)")
-    lib = C.CDLL(LIB)
+    lib = C.CDLL(path)
     for name, (res, args) in _SIGNATURES.items():
         fn = getattr(lib, name)
         fn.restype = res

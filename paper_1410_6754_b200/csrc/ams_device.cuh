@@ -18,30 +18,44 @@ constexpr int kChunkTiles = 16;
 constexpr int kChunk = kTile * kChunkTiles;  // keys per histogram / scatter CTA
 static_assert(kItems * kThreads == kTile, "tile geometry");
 
-// Tree classifier blob (one per group) in global memory.
+// Tree classifier blob (one per group) in global memory: header, sorted
+// splitter keys and positions, and a key-range LUT whose cells hold
+// (first splitter index | splitter count << 16).
 constexpr int kMaxSpl = AMS_MAX_BUCKETS;  // room for nb-1 <= 4095 splitters
-constexpr int kMaxLutBits = 12;
+constexpr int kMaxLutBits = 13;
 constexpr int kMaxCells = 1 << kMaxLutBits;
 constexpr size_t kBlobKeys = 64;
 constexpr size_t kBlobPos = kBlobKeys + sizeof(uint64_t) * kMaxSpl;
 constexpr size_t kBlobLut = kBlobPos + sizeof(uint32_t) * kMaxSpl;
-constexpr size_t kBlobStride = 64 * 1024;
-static_assert(kBlobLut + 2 * (kMaxCells + 1) <= kBlobStride, "blob layout");
+constexpr size_t kBlobStride = 128 * 1024;
+static_assert(kBlobLut + 4 * (size_t)(kMaxCells + 1) <= kBlobStride, "blob layout");
 
 struct ClsHeader {
   uint64_t lo, hi;   // first / last splitter key
   uint32_t nspl;     // number of splitters = buckets - 1
-  uint32_t shift;    // LUT cell of key k: (k - lo) >> shift
-  uint32_t ncells;   // LUT has ncells + 1 entries
+  uint32_t shift;    // LUT cell of key k: (k - lo) >> shift, clamped
+  uint32_t ncells;   // LUT entries
   uint32_t pad;
 };
 
-// Digit classifier (final-sort partitions): bucket = clamp((k-lo)>>shift).
+// Digit classifier (final-sort partitions): digit = (k-lo) * nb / (range+1)
+// via a 64-bit multiply-high by mult ~ 2^64 nb / (range+1), so all nb
+// digits cover the key range evenly; mult == 0 means range < nb and the
+// digit is k - lo itself (one key value per digit).
 struct DigitCls {
   uint64_t lo, hi;
-  uint32_t shift;
+  uint64_t mult;
   uint32_t nb;
+  uint32_t pad;
 };
+
+// Multiplier of the scaled digit above.  Any value keeps digits monotone in
+// the key (what correctness needs); double precision only affects balance.
+__host__ __device__ inline uint64_t digit_mult(uint64_t range, uint32_t nb) {
+  if (range < (uint64_t)nb) return 0;
+  const double m = (double)nb * 18446744073709551616.0 / ((double)range + 1.0);
+  return m >= 18446744073709549568.0 ? 0xFFFFFFFFFFFFF800ULL : (uint64_t)m;
+}
 
 // Final-sort overflow record: a cell too large for the shared-memory sort.
 struct OverflowRec {
@@ -56,9 +70,11 @@ __host__ __device__ inline int bit_length64(uint64_t x) {
 #endif
 }
 
+// LUT of ~16 cells per splitter: most keys see a cell with no splitter or
+// one, so classification is one LUT load plus at most one compare.
 __host__ __device__ inline int lut_bits_for(int nspl) {
   int lg = bit_length64((uint64_t)nspl);  // ~ceil(log2(nspl+1))
-  int b = lg + 3;
+  int b = lg + 4;
   return b < 4 ? 4 : (b > kMaxLutBits ? kMaxLutBits : b);
 }
 
@@ -93,31 +109,32 @@ struct TreeView {
   ClsHeader h;
   const uint64_t* skeys;
   const uint32_t* spos;
-  const uint16_t* lut;
+  const uint32_t* lut;
 
   // Bucket of (key, pos) = number of splitters strictly below it under the
   // (key, position) order — bisect_left on tie-broken elements
-  // (ams.py:201-211).  The LUT narrows the search to the
-  // splitters whose key shares the element's cell.
+  // (ams.py:201-211).  Splitters before the key's LUT cell
+  // are all below it, those after all above; the few inside the cell
+  // (sorted) are compared one by one.
   __device__ __forceinline__ uint32_t classify(uint64_t key, uint32_t pos) const {
-    if (h.nspl == 0 || key < h.lo) return 0;
-    if (key > h.hi) return h.nspl;
-    const uint32_t cell = (uint32_t)((key - h.lo) >> h.shift);
-    uint32_t l = lut[cell], r = lut[cell + 1];
-    while (l < r) {
-      const uint32_t m = (l + r) >> 1;
-      const uint64_t sk = skeys[m];
-      const bool lt = sk < key || (sk == key && spos[m] < pos);
-      l = lt ? m + 1 : l;
-      r = lt ? r : m;
+    if (h.nspl == 0) return 0;
+    uint64_t c = (key - h.lo) >> h.shift;
+    c = key < h.lo ? 0 : (c >= h.ncells ? h.ncells - 1 : c);
+    const uint32_t rec = lut[c];
+    uint32_t b = rec & 0xFFFFu;
+    const uint32_t end = b + (rec >> 16);
+    while (b < end) {
+      const uint64_t sk = skeys[b];
+      if (!(sk < key || (sk == key && spos[b] < pos))) break;
+      ++b;
     }
-    return l;
+    return b;
   }
 };
 
 // Shared-memory bytes a tree view needs.
 __host__ __device__ inline size_t tree_smem_bytes(int nspl_cap, int cells_cap) {
-  size_t b = 64 + (size_t)nspl_cap * 12 + (size_t)(cells_cap + 1) * 2;
+  size_t b = 64 + (size_t)nspl_cap * 12 + (size_t)cells_cap * 4;
   return (b + 15) & ~(size_t)15;
 }
 
@@ -128,13 +145,13 @@ __device__ inline TreeView load_tree(const uint8_t* blob, uint8_t* smem, int nsp
   v.h = *gh;
   uint64_t* sk = reinterpret_cast<uint64_t*>(smem + 64);
   uint32_t* sp = reinterpret_cast<uint32_t*>(smem + 64 + (size_t)nspl_cap * 8);
-  uint16_t* lu = reinterpret_cast<uint16_t*>(smem + 64 + (size_t)nspl_cap * 12);
+  uint32_t* lu = reinterpret_cast<uint32_t*>(smem + 64 + (size_t)nspl_cap * 12);
   const uint64_t* gk = reinterpret_cast<const uint64_t*>(blob + kBlobKeys);
   const uint32_t* gp = reinterpret_cast<const uint32_t*>(blob + kBlobPos);
-  const uint16_t* gl = reinterpret_cast<const uint16_t*>(blob + kBlobLut);
+  const uint32_t* gl = reinterpret_cast<const uint32_t*>(blob + kBlobLut);
   for (uint32_t i = threadIdx.x; i < v.h.nspl; i += blockDim.x) { sk[i] = gk[i]; sp[i] = gp[i]; }
   if (v.h.nspl)
-    for (uint32_t i = threadIdx.x; i <= v.h.ncells; i += blockDim.x) lu[i] = gl[i];
+    for (uint32_t i = threadIdx.x; i < v.h.ncells; i += blockDim.x) lu[i] = gl[i];
   v.skeys = sk; v.spos = sp; v.lut = lu;
   return v;
 }
@@ -143,46 +160,95 @@ struct DigitView {
   DigitCls c;
   __device__ __forceinline__ uint32_t classify(uint64_t key, uint32_t) const {
     if (key <= c.lo) return 0;
-    const uint64_t d = (key - c.lo) >> c.shift;
+    const uint64_t x = key - c.lo;
+    const uint64_t d = c.mult ? __umul64hi(x, c.mult) : x;
     return d >= c.nb ? c.nb - 1 : (uint32_t)d;
   }
 };
 
-// ---- block-wide exclusive scan of a shared u32 array (n <= 64K) ----------
-// Returns the total; `scratch` needs NT/32 + 1 words.
-template <int NT>
-__device__ inline uint32_t block_excl_scan(uint32_t* a, int n, uint32_t* scratch) {
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int per = (n + NT - 1) / NT;
-  const int beg = threadIdx.x * per;
-  const int end = beg + per < n ? beg + per : n;
-  uint32_t sum = 0;
-  for (int i = beg; i < end; ++i) sum += a[i];
-  uint32_t x = sum;
+// ---- block-wide exclusive scans in shared memory ----------------------------
+// Each warp owns a contiguous range of the array and walks it 32 entries at
+// a time (consecutive lanes -> consecutive words: no bank conflicts), with
+// shuffle scans inside each 32-entry block.  `scratch` needs NT/32 + 1 words.
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x) {
+  const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
     if (lane >= o) x += y;
   }
-  if (lane == 31) scratch[w] = x;
+  return x;
+}
+
+// Exclusive scan of the per-warp totals in scratch[0..NW); returns the total.
+template <int NT>
+__device__ __forceinline__ uint32_t scan_warp_totals(uint32_t* scratch) {
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   __syncthreads();
   if (w == 0) {
-    uint32_t v = lane < NT / 32 ? scratch[lane] : 0;
-    uint32_t s = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      uint32_t y = __shfl_up_sync(0xffffffffu, s, o);
-      if (lane >= o) s += y;
-    }
-    if (lane < NT / 32) scratch[lane] = s - v;
-    if (lane == NT / 32 - 1) scratch[NT / 32] = s;
+    const uint32_t v = lane < NW ? scratch[lane] : 0;
+    const uint32_t s = warp_incl_scan(v);
+    if (lane < NW) scratch[lane] = s - v;
+    if (lane == NW - 1) scratch[NW] = s;
   }
   __syncthreads();
-  uint32_t run = scratch[w] + x - sum;
-  for (int i = beg; i < end; ++i) { uint32_t t = a[i]; a[i] = run; run += t; }
-  const uint32_t total = scratch[NT / 32];
+  return scratch[NW];
+}
+
+// VAL(i) = value of entry i (u32 array or packed u16 pairs).
+template <int NT>
+__device__ inline uint32_t block_excl_scan(uint32_t* a, int n, uint32_t* scratch) {
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int per = (((n + NW - 1) / NW) + 31) & ~31;
+  const int beg = w * per;
+  const int end = beg + per < n ? beg + per : n;
+  uint32_t sum = 0;
+  for (int i = beg + lane; i < end; i += 32) sum += a[i];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  if (lane == 0) scratch[w] = sum;
+  const uint32_t total = scan_warp_totals<NT>(scratch);
+  uint32_t carry = scratch[w];
+  for (int i0 = beg; i0 < end; i0 += 32) {
+    const int i = i0 + lane;
+    const uint32_t v = i < end ? a[i] : 0;
+    const uint32_t inc = warp_incl_scan(v);
+    if (i < end) a[i] = carry + inc - v;
+    carry += __shfl_sync(0xffffffffu, inc, 31);
+  }
   __syncthreads();
   return total;
+}
+
+// Packed 16-bit counters (two per word, low half first), scanned in place.
+template <int NT>
+__device__ inline void block_excl_scan_u16(uint32_t* wv, int nwords, uint32_t* scratch) {
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int per = (((nwords + NW - 1) / NW) + 31) & ~31;
+  const int beg = w * per;
+  const int end = beg + per < nwords ? beg + per : nwords;
+  uint32_t sum = 0;
+  for (int i = beg + lane; i < end; i += 32) { const uint32_t v = wv[i]; sum += (v & 0xFFFFu) + (v >> 16); }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  if (lane == 0) scratch[w] = sum;
+  scan_warp_totals<NT>(scratch);
+  uint32_t carry = scratch[w];
+  for (int i0 = beg; i0 < end; i0 += 32) {
+    const int i = i0 + lane;
+    const uint32_t v = i < end ? wv[i] : 0;
+    const uint32_t pair = (v & 0xFFFFu) + (v >> 16);
+    const uint32_t inc = warp_incl_scan(pair);
+    if (i < end) {
+      const uint32_t lo = carry + inc - pair;
+      wv[i] = lo | ((lo + (v & 0xFFFFu)) << 16);
+    }
+    carry += __shfl_sync(0xffffffffu, inc, 31);
+  }
+  __syncthreads();
 }
 
 }  // namespace ams

@@ -152,7 +152,7 @@ struct ams_ctx {
   int bcur = 0;
   HostBuf h_hist;
   // final sort
-  DevBuf dcls, ovf, ovf_count, fb, fb_count;
+  DevBuf dcls, ovf, ovf_count, fb, fb_count, groups, ngroups_d;
   HostBuf h_small;
   uint64_t overflow_cells = 0, fallback_cells = 0;
   // optional per-category kernel timing (CUDA events on the launching stream)
@@ -298,7 +298,7 @@ int ams_ctx_destroy(ams_ctx_t* c) {
     s->release();
   for (DevBuf* b : {&c->blobs, &c->sorted_keys, &c->sorted_pos, &c->sample_idx, &c->bounds[0], &c->bounds[1],
                     &c->chunk_tot, &c->seg_hist, &c->cell_base, &c->pieces, &c->minmax, &c->dcls,
-                    &c->ovf, &c->ovf_count, &c->fb, &c->fb_count})
+                    &c->ovf, &c->ovf_count, &c->fb, &c->fb_count, &c->groups, &c->ngroups_d})
     b->release();
   c->h_hist.release();
   c->h_small.release();
@@ -626,7 +626,9 @@ int ams_final_sort(ams_ctx_t* c, void* src, void* src_vals, void* tmp, void* tmp
   const bool vals = src_vals != nullptr;
   if (vals && (!tmp_vals || !out_vals)) return set_error(AMS_EINVAL, "missing value buffers");
   AMS_CK(cudaSetDevice(c->device));
-  constexpr uint64_t kTargetCell = 4096;
+  // Digit cells average ~78% of the shared-memory capacity: uniform keys
+  // never overflow it while the per-cell work stays large.
+  constexpr uint64_t kTargetCell = AMS_SMEM_SORT_CAP * 78 / 100;
   std::vector<uint64_t> s_off, s_len, b_off, b_len, b_lo, b_hi;
   std::vector<int32_t> b_seg;
   uint64_t total = 0, max_big = 0, small_n = 0;
@@ -674,10 +676,14 @@ int ams_final_sort(ams_ctx_t* c, void* src, void* src_vals, void* tmp, void* tmp
   void* oth = tmp;
   void* oth_v = tmp_vals;
   bool first_round = true;
+  int rounds = 0;
   while (!b_off.empty()) {
+    // Every round splits each non-constant cell into >= 2 non-empty cells,
+    // so the key ranges shrink; 64-bit keys cannot need more than 64.
+    if (++rounds > 64) return set_error(AMS_EINTERNAL, "final partition did not converge");
     const int nb_seg = (int)b_off.size();
-    const int nbits = std::min(11, std::max(1, ceil_log2_u64((max_big + kTargetCell - 1) / kTargetCell)));
-    const int nbs = 1 << nbits;
+    const int nbs = (int)std::min<uint64_t>(AMS_MAX_BUCKETS / 2,
+                                            std::max<uint64_t>(2, (max_big + kTargetCell - 1) / kTargetCell));
     std::vector<int32_t> idx(nb_seg);
     for (int i = 0; i < nb_seg; ++i) idx[i] = i;
     SegMeta m;
@@ -706,7 +712,7 @@ int ams_final_sort(ams_ctx_t* c, void* src, void* src_vals, void* tmp, void* tmp
     }
     {
       KTimer kt(c, AMS_KCAT_RANGES, 0.0);
-      AMS_CK(launch_final_ranges(c->stream, bounds, nb_seg, nbits, c->dcls.as<DigitCls>()));
+      AMS_CK(launch_final_ranges(c->stream, bounds, nb_seg, nbs, c->dcls.as<DigitCls>()));
     }
     AMS_CK(upload_segments(st, c->stream, b_off.data(), b_len.data(), idx.data(), nb_seg, nullptr,
                            0, &m, &nchunks));
@@ -731,7 +737,6 @@ int ams_final_sort(ams_ctx_t* c, void* src, void* src_vals, void* tmp, void* tmp
     AMS_CK(cudaMemsetAsync(c->ovf_count.p, 0, sizeof(unsigned int), c->stream));
     CellSource cs{};
     cs.mode = 0;
-    cs.nbits = nbits;
     cs.cell_base = c->cell_base.as<uint64_t>();
     cs.cell_cnt = c->seg_hist.as<uint32_t>();
     cs.dcls = c->dcls.as<DigitCls>();

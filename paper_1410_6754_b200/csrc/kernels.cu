@@ -16,6 +16,7 @@
 //   K9 k_smem_sort       CTA-local stable sort in shared memory (sorted(),
 //                        ams.py:310-312)
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #include "ams_device.cuh"
@@ -107,7 +108,7 @@ __global__ void __launch_bounds__(1024) k_build_cls(const uint64_t* __restrict__
   ClsHeader* h = reinterpret_cast<ClsHeader*>(blob);
   uint64_t* bk = reinterpret_cast<uint64_t*>(blob + kBlobKeys);
   uint32_t* bp = reinterpret_cast<uint32_t*>(blob + kBlobPos);
-  uint16_t* lut = reinterpret_cast<uint16_t*>(blob + kBlobLut);
+  uint32_t* lut = reinterpret_cast<uint32_t*>(blob + kBlobLut);
   for (uint32_t i = threadIdx.x; i < nspl; i += blockDim.x) {
     const uint64_t r = ((uint64_t)(i + 1) * S) / nb;
     const uint64_t k = sorted_keys[s0 + r];
@@ -125,10 +126,15 @@ __global__ void __launch_bounds__(1024) k_build_cls(const uint64_t* __restrict__
   const int bl = bit_length64(hi - lo);
   const uint32_t shift = bl > bits ? (uint32_t)(bl - bits) : 0u;
   const uint32_t ncells = (uint32_t)((hi - lo) >> shift) + 1;
-  for (uint32_t c = threadIdx.x; c < ncells; c += blockDim.x)
-    lut[c] = (uint16_t)lower_bound_smem(sk, nspl, lo + ((uint64_t)c << shift));
+  // Cell c covers keys [lo + c<<shift, lo + (c+1)<<shift); its record is
+  // (#splitters below the cell) | (#splitters inside it) << 16.
+  for (uint32_t c = threadIdx.x; c < ncells; c += blockDim.x) {
+    const uint32_t first = lower_bound_smem(sk, nspl, lo + ((uint64_t)c << shift));
+    const uint32_t next = c + 1 < ncells ? lower_bound_smem(sk, nspl, lo + ((uint64_t)(c + 1) << shift))
+                                         : nspl;
+    lut[c] = first | ((next - first) << 16);
+  }
   if (threadIdx.x == 0) {
-    lut[ncells] = (uint16_t)nspl;
     h->lo = lo; h->hi = hi; h->nspl = nspl; h->shift = shift; h->ncells = ncells; h->pad = 0;
   }
 }
@@ -139,7 +145,7 @@ __global__ void __launch_bounds__(1024) k_build_cls(const uint64_t* __restrict__
 // same-bucket items of one thread costs one atomic — sorted and
 // duplicate-heavy inputs stay cheap), then write the chunk histogram and
 // add it to the segment histogram.
-template <int KIND, bool DIGIT>
+template <int KIND, bool DIGIT, bool MINMAX>
 __global__ void __launch_bounds__(kThreads) k_hist(const uint64_t* __restrict__ src, SegMeta m,
                                                    const uint8_t* __restrict__ blobs,
                                                    const DigitCls* __restrict__ dcls, int nspl_cap,
@@ -172,24 +178,26 @@ __global__ void __launch_bounds__(kThreads) k_hist(const uint64_t* __restrict__ 
   }
   const int lane = threadIdx.x & 31;
   unsigned long long mn = ~0ULL, mx = 0;
-  for (uint64_t t0 = first; t0 < last; t0 += kTile) {
-    const uint32_t tcount = (uint32_t)min((uint64_t)kTile, last - t0);
+  auto tile = [&](const uint64_t t0, const uint32_t tcount, auto full_tag) {
+    constexpr bool FULL = decltype(full_tag)::value;
     const uint64_t base = seg_off + t0;
     uint64_t keys[kItems];
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
       const uint32_t e = i * kThreads + threadIdx.x;
-      keys[i] = e < tcount ? to_ordered<KIND>(ldg_stream(src + base + e)) : 0;
+      keys[i] = (FULL || e < tcount) ? to_ordered<KIND>(ldg_stream(src + base + e)) : 0;
     }
+    // Run-aggregated shared atomics: consecutive items of a thread that
+    // share a bucket (sorted / duplicate-heavy inputs) cost one atomic.
     uint32_t cur = kInvalid, cnt = 0;
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
       const uint32_t e = i * kThreads + threadIdx.x;
-      if (e < tcount) {
+      if (FULL || e < tcount) {
         uint32_t b;
         if constexpr (DIGIT) b = dv.classify(keys[i], 0);
         else b = tv.classify(keys[i], (uint32_t)((int64_t)(base + e) + posbase));
-        if (minmax) { mn = min(mn, (unsigned long long)keys[i]); mx = max(mx, (unsigned long long)keys[i]); }
+        if constexpr (MINMAX) { mn = min(mn, (unsigned long long)keys[i]); mx = max(mx, (unsigned long long)keys[i]); }
         if (b != cur) {
           if (cnt) atomicAdd(&hist[cur], cnt);
           cur = b;
@@ -199,6 +207,11 @@ __global__ void __launch_bounds__(kThreads) k_hist(const uint64_t* __restrict__ 
       }
     }
     if (cnt) atomicAdd(&hist[cur], cnt);
+  };
+  for (uint64_t t0 = first; t0 < last; t0 += kTile) {
+    const uint32_t tcount = (uint32_t)min((uint64_t)kTile, last - t0);
+    if (tcount == (uint32_t)kTile) tile(t0, tcount, std::true_type{});
+    else tile(t0, tcount, std::false_type{});
   }
   __syncthreads();
   for (int b = threadIdx.x; b < nb_stride; b += kThreads) {
@@ -206,7 +219,7 @@ __global__ void __launch_bounds__(kThreads) k_hist(const uint64_t* __restrict__ 
     chunk_tot[c * nb_stride + b] = v;
     if (v) atomicAdd(&seg_hist[(uint64_t)s * nb_stride + b], v);
   }
-  if (minmax) {
+  if constexpr (MINMAX) {
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
       mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
@@ -329,44 +342,26 @@ constexpr int kRankWarp = 0;     // stable, one bucket-counter array per warp
 constexpr int kRankSerial = 1;   // stable, one shared array, warps take turns
 constexpr int kRankAtomic = 2;   // unstable (keys only, order inside a run is free)
 
-// Stable rank of this lane's item among the warp's items in the same bucket:
-// a 32-lane bitonic sort of (bucket << 5 | lane) with shuffles (15 steps;
-// __match_any_sync costs ~57 SM-cycles per warp on B200, this ~20), group
-// heads by ballot, the head bumps the per-warp counter, and the rank goes
-// back to the item's lane through `xch`.
-__device__ __forceinline__ uint32_t warp_stable_rank(uint32_t b, int lane, uint32_t* whw,
-                                                     uint32_t* xch) {
-  constexpr uint32_t kNone = 0x7FFFFFFu;
-  uint32_t v = ((b == kInvalid ? kNone : b) << 5) | (uint32_t)lane;
-#pragma unroll
-  for (int k = 2; k <= 32; k <<= 1) {
-#pragma unroll
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      const uint32_t o = __shfl_xor_sync(0xffffffffu, v, j);
-      const bool up = (lane & k) == 0;
-      const bool lower = (lane & j) == 0;
-      v = (lower == up) ? min(v, o) : max(v, o);
-    }
+// Stable rank of this lane's item among the warp's items in the same bucket
+// (lower lanes first), plus the per-warp bucket counter update.  Peers are
+// found with one ballot per bucket-id bit (and one for validity):
+// __match_any_sync costs ~57 SM-cycles per warp on B200 (tools/microbench).
+__device__ __forceinline__ uint32_t warp_stable_rank(uint32_t b, int nbits, int lane, uint32_t lt,
+                                                     uint32_t* whw) {
+  const bool valid = b != kInvalid;
+  uint32_t peers = __ballot_sync(0xffffffffu, valid);
+  if (!valid) peers = ~peers;
+  for (int bit = 0; bit < nbits; ++bit) {
+    const bool x = (b >> bit) & 1u;
+    const uint32_t bal = __ballot_sync(0xffffffffu, x);
+    peers &= x ? bal : ~bal;
   }
-  const uint32_t sb = v >> 5, src = v & 31u;
-  const uint32_t prev = __shfl_up_sync(0xffffffffu, sb, 1);
-  const bool head = lane == 0 || prev != sb;
-  const uint32_t heads = __ballot_sync(0xffffffffu, head);
-  const uint32_t upto = 0xFFFFFFFFu >> (31 - lane);
-  const int start = 31 - __clz(heads & upto);
-  const uint32_t after = heads & ~upto;
-  const int next = after ? __ffs(after) - 1 : 32;
-  uint32_t old = 0;
-  if (head && sb != kNone) {
-    old = whw[sb];
-    whw[sb] = old + (uint32_t)(next - start);
-  }
-  old = __shfl_sync(0xffffffffu, old, start);
-  xch[src] = old + (uint32_t)(lane - start);
+  uint32_t cnt = 0;
+  if (valid) cnt = whw[b];
   __syncwarp();
-  const uint32_t r = xch[lane];
+  if (valid && lane == __ffs(peers) - 1) whw[b] = cnt + __popc(peers);
   __syncwarp();
-  return r;
+  return cnt + __popc(peers & lt);
 }
 
 // One CTA per chunk (the histogram kernel's chunks): the running output
@@ -388,16 +383,13 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const uint64_t* __restrict
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ int s_seg;
   __shared__ uint32_t s_scan[kWarps + 1];
-  __shared__ uint32_t s_xch[kWarps][32];
   constexpr int kHists = MODE == kRankWarp ? kWarps : 1;
   uint64_t* keys_s = reinterpret_cast<uint64_t*>(smem);
   uint64_t* vals_s = keys_s + kTile;
   int64_t* run = reinterpret_cast<int64_t*>(smem + (VALS ? 16 : 8) * (size_t)kTile);
-  int64_t* delta = run + nb_stride;
-  uint32_t* wh = reinterpret_cast<uint32_t*>(delta + nb_stride);
+  uint32_t* wh = reinterpret_cast<uint32_t*>(run + nb_stride);
   uint32_t* btot = wh + (size_t)kHists * nb_stride;
-  uint32_t* tcnt = btot + nb_stride;
-  uint16_t* bkt_s = reinterpret_cast<uint16_t*>(tcnt + nb_stride);
+  uint16_t* bkt_s = reinterpret_cast<uint16_t*>(btot + nb_stride);
   uint8_t* clsmem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(bkt_s + kTile) + 15) & ~static_cast<uintptr_t>(15));
 
@@ -424,6 +416,8 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const uint64_t* __restrict
     posbase = m.posbase[cls];
   }
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t lt = lanemask_lt();
+  const int nbits = bit_length64((uint64_t)(nb_stride - 1));
   uint32_t* whw = wh + (MODE == kRankWarp ? (size_t)w * nb_stride : 0);
   for (uint64_t t0 = first; t0 < last; t0 += kTile) {
     const uint32_t tcount = (uint32_t)min((uint64_t)kTile, last - t0);
@@ -458,7 +452,7 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const uint64_t* __restrict
 #pragma unroll
           for (int i = 0; i < kItems; ++i) {
             const uint32_t b = pk[i];
-            const uint32_t r = warp_stable_rank(b, lane, whw, s_xch[w]);
+            const uint32_t r = warp_stable_rank(b, nbits, lane, lt, whw);
             if (b != kInvalid) pk[i] = (b << 16) | r;
           }
         }
@@ -475,14 +469,9 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const uint64_t* __restrict
         acc += v;
       }
       btot[b] = acc;
-      tcnt[b] = acc;
     }
     __syncthreads();
     block_excl_scan<kThreads>(btot, nb_stride, s_scan);
-    for (int b = threadIdx.x; b < nb_stride; b += kThreads) {
-      delta[b] = run[b] - (int64_t)btot[b];
-      run[b] += tcnt[b];
-    }
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
       if (pk[i] != kInvalid) {
@@ -495,10 +484,14 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const uint64_t* __restrict
     }
     __syncthreads();
     for (uint32_t j = threadIdx.x; j < tcount; j += kThreads) {
-      const int64_t d = delta[bkt_s[j]] + (int64_t)j;
+      const uint32_t b = bkt_s[j];
+      const int64_t d = run[b] - (int64_t)btot[b] + (int64_t)j;
       dst[d] = keys_s[j];
       if constexpr (VALS) dst_vals[d] = vals_s[j];
     }
+    __syncthreads();
+    for (int b = threadIdx.x; b < nb_stride; b += kThreads)
+      run[b] += (int64_t)((b + 1 < nb_stride ? btot[b + 1] : tcount) - btot[b]);
   }
 }
 
@@ -511,22 +504,22 @@ __global__ void k_gather_bounds(const uint64_t* __restrict__ bounds, const int32
   out[2 * i + 1] = bounds[2 * sel[i] + 1];
 }
 
-__global__ void k_final_ranges(const uint64_t* __restrict__ bounds, int nseg, int nbits,
+__global__ void k_final_ranges(const uint64_t* __restrict__ bounds, int nseg, int nb,
                                DigitCls* __restrict__ out) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= nseg) return;
   const uint64_t lo = bounds[2 * s], hi = bounds[2 * s + 1];
-  const int bl = bit_length64(hi - lo);
   DigitCls d;
   d.lo = lo;
   d.hi = hi;
-  d.shift = bl > nbits ? (uint32_t)(bl - nbits) : 0u;
-  d.nb = 1u << nbits;
+  d.nb = (uint32_t)nb;
+  d.mult = digit_mult(hi - lo, d.nb);
+  d.pad = 0;
   out[s] = d;
 }
 
 // -------------------------------------------------------------------- K9
-constexpr int kSortThreads = 512;
+constexpr int kSortThreads = 256;
 constexpr int kSortWarps = kSortThreads / 32;
 constexpr int kSortCap = AMS_SMEM_SORT_CAP;
 constexpr int kSortItems = kSortCap / kSortThreads;  // per-warp iterations
@@ -556,6 +549,7 @@ __device__ __forceinline__ void cell_of(const CellSource& cs, uint64_t cid, uint
     off = cs.seg_off[cid];
     count = cs.seg_len[cid];
   } else {
+    if (cs.nrecs && cid >= *cs.nrecs) { off = 0; count = 0; return; }
     off = cs.recs[cid].off;
     count = cs.recs[cid].count;
   }
@@ -606,7 +600,6 @@ __global__ void __launch_bounds__(kSortThreads, 1)
   uint16_t* iB = iA + kSortCap;
   uint32_t* wh = reinterpret_cast<uint32_t*>(iB + kSortCap);  // [kSortWarps][kRadix]
   uint32_t* btot = wh + kSortWarps * kRadix;
-  __shared__ uint32_t s_xch[kSortWarps][32];
 
   uint64_t off, count;
   cell_of(cs, blockIdx.x, off, count);
@@ -624,6 +617,7 @@ __global__ void __launch_bounds__(kSortThreads, 1)
   if (mn != mx) {
     const int bits = bit_length64(mx - mn);
     const int passes = (bits + 7) / 8;
+    const uint32_t lt = lanemask_lt();
     const uint32_t chunk = ((n + kSortWarps - 1) / kSortWarps + 31) & ~31u;
     uint32_t* whw = wh + w * kRadix;
     for (int p = 0; p < passes; ++p) {
@@ -636,7 +630,7 @@ __global__ void __launch_bounds__(kSortThreads, 1)
         const uint32_t e = w * chunk + it * 32 + lane;
         const bool valid = (it * 32 < (int)chunk) && e < n;
         const uint32_t d = valid ? (uint32_t)(((kA[e] - mn) >> sh) & 255) : kInvalid;
-        const uint32_t r = warp_stable_rank(d, lane, whw, s_xch[w]);
+        const uint32_t r = warp_stable_rank(d, 8, lane, lt, whw);
         pk[it] = valid ? ((d << 16) | r) : kInvalid;
       }
       __syncthreads();
@@ -673,16 +667,22 @@ __global__ void __launch_bounds__(kSortThreads, 1)
   }
 }
 
-// One CTA per cell (<= kSortCap keys): counting sort of the keys into
-// ~n/2 sub-buckets by their top varying bits (shared atomics), then an
-// insertion sort of every sub-bucket (ties by input index when values
-// ride along, so the result is stable).  Cells whose keys cluster (a
-// sub-bucket above kInsertMax) go to the LSD fallback list.
-constexpr int kSubBits = 12;
-constexpr int kInsertMax = 32;
+// One CTA per cell (<= kSortCap keys), keys held in registers:
+//  1. counting sort into ~n..2n sub-buckets by the scaled key
+//     (key - min) * 2n >> bitlen(max - min), with 16-bit counters packed in
+//     pairs (shared atomics) — uniform keys land ~0.5-1 per sub-bucket;
+//  2. each key finds its final slot inside its sub-bucket: singleton (most
+//     keys) — its own; pair — one compare with the partner; larger (rare) —
+//     a rank count; ties by input index with values (stable), by slot
+//     without;
+//  3. coalesced write-out.
+// When the range is narrower than n each sub-bucket is one key value (no
+// ordering needed for keys alone).  Cells whose keys cluster (a sub-bucket
+// above kRankMax that still needs ordering) go to the LSD fallback list.
+constexpr int kRankMax = 64;
 
 template <int KIND_OUT, bool VALS>
-__global__ void __launch_bounds__(kSortThreads)
+__global__ void __launch_bounds__(kSortThreads, 4)
     k_smem_sort(const uint64_t* __restrict__ src, const uint64_t* __restrict__ src_vals,
                 uint64_t* __restrict__ out, uint64_t* __restrict__ out_vals, CellSource cs,
                 OverflowRec* __restrict__ ovf, unsigned int* __restrict__ ovf_count,
@@ -692,8 +692,9 @@ __global__ void __launch_bounds__(kSortThreads)
   __shared__ uint32_t s_scan[kSortWarps + 1];
   __shared__ uint32_t s_max[kSortWarps];
   uint64_t* kB = reinterpret_cast<uint64_t*>(smem);
-  uint32_t* cnt = reinterpret_cast<uint32_t*>(kB + kSortCap);   // [1 << kSubBits]
-  uint16_t* iB = reinterpret_cast<uint16_t*>(cnt + (1 << kSubBits));
+  uint32_t* cw = reinterpret_cast<uint32_t*>(kB + kSortCap);   // [kSortCap] words = 2*cap u16
+  const uint16_t* c16 = reinterpret_cast<const uint16_t*>(cw);
+  uint16_t* iB = reinterpret_cast<uint16_t*>(cw + kSortCap);    // input index of slot j (VALS)
 
   uint64_t off, count;
   cell_of(cs, blockIdx.x, off, count);
@@ -701,47 +702,60 @@ __global__ void __launch_bounds__(kSortThreads)
   if (big_cell<KIND_OUT, VALS>(src, src_vals, out, out_vals, off, count, ovf, ovf_count, s_mm))
     return;
   const uint32_t n = (uint32_t)count;
+  const uint32_t tid = threadIdx.x;
   uint64_t kr[kSortItems];
   uint64_t mn = ~0ULL, mx = 0;
 #pragma unroll
   for (int it = 0; it < kSortItems; ++it) {
-    const uint32_t i = it * kSortThreads + threadIdx.x;
-    kr[it] = i < n ? ldg_stream(src + off + i) : 0;
-    if (i < n) { mn = min(mn, kr[it]); mx = max(mx, kr[it]); }
+    const uint32_t i = it * kSortThreads + tid;
+    kr[it] = i < n ? ldg_stream(src + off + i) : ~0ULL;
+    mn = min(mn, kr[it]);
+    if (i < n) mx = max(mx, kr[it]);
   }
   block_minmax(mn, mx, s_mm);
   if (mn == mx) {
     const uint64_t ko = from_ordered<KIND_OUT>(mn);
-    for (uint32_t i = threadIdx.x; i < n; i += kSortThreads) {
+    for (uint32_t i = tid; i < n; i += kSortThreads) {
       out[off + i] = ko;
       if constexpr (VALS) out_vals[off + i] = src_vals[off + i];
     }
     return;
   }
-  int lg = bit_length64((uint64_t)n - 1) - 1;   // ~n/2 sub-buckets
-  lg = lg < 1 ? 1 : (lg > kSubBits ? kSubBits : lg);
-  const int bl = bit_length64(mx - mn);
-  const int sh = bl > lg ? bl - lg : 0;
-  const uint32_t nsub = (uint32_t)((mx - mn) >> sh) + 1;
-  for (uint32_t j = threadIdx.x; j < nsub; j += kSortThreads) cnt[j] = 0;
+  const uint64_t range = mx - mn;
+  const bool exact = range < 2 * (uint64_t)n;  // one key value per sub-bucket
+  // Sub-bucket = (k - mn) * 2n >> bitlen(range): in [0, 2n), monotone.
+  const int lr = bit_length64(range);
+  const uint64_t mult = exact ? 0 : ((uint64_t)(2 * n) << (64 - lr));
+  const uint32_t nsub = exact ? (uint32_t)range + 1 : 2 * n;
+  const uint32_t nwords = (nsub + 1) >> 1;
+  auto sub_of = [&](uint64_t k) -> uint32_t {
+    const uint64_t x = k - mn;
+    return exact ? (uint32_t)x : (uint32_t)__umul64hi(x, mult);
+  };
+  for (uint32_t j = tid; j < nwords; j += kSortThreads) cw[j] = 0;
   __syncthreads();
+  uint32_t sb[kSortItems];
 #pragma unroll
   for (int it = 0; it < kSortItems; ++it) {
-    const uint32_t i = it * kSortThreads + threadIdx.x;
-    if (i < n) atomicAdd(&cnt[(uint32_t)((kr[it] - mn) >> sh)], 1u);
+    sb[it] = sub_of(kr[it]);
+    if (it * kSortThreads + tid < n) atomicAdd(&cw[sb[it] >> 1], 1u << ((sb[it] & 1) * 16));
   }
   __syncthreads();
   uint32_t big = 0;
-  for (uint32_t j = threadIdx.x; j < nsub; j += kSortThreads) big = max(big, cnt[j]);
+  for (uint32_t j = tid; j < nwords; j += kSortThreads) {
+    const uint32_t v = cw[j];
+    big = max(big, max(v & 0xFFFFu, v >> 16));
+  }
 #pragma unroll
   for (int o = 16; o; o >>= 1) big = max(big, __shfl_xor_sync(0xffffffffu, big, o));
-  if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = big;
-  block_excl_scan<kSortThreads>(cnt, (int)nsub, s_scan);
+  if ((tid & 31) == 0) s_max[tid >> 5] = big;
+  block_excl_scan_u16<kSortThreads>(cw, (int)nwords, s_scan);
   big = 0;
+#pragma unroll
   for (int w = 0; w < kSortWarps; ++w) big = max(big, s_max[w]);
-  // Exact-key sub-buckets (sh == 0) hold one key each: fine without values.
-  if (big > (uint32_t)kInsertMax && (VALS || sh != 0)) {
-    if (threadIdx.x == 0) {
+  const bool need_order = VALS || !exact;
+  if (need_order && big > (uint32_t)kRankMax) {
+    if (tid == 0) {
       const unsigned int slot = atomicAdd(fb_count, 1u);
       OverflowRec r; r.off = off; r.count = count; r.lo = mn; r.hi = mx;
       fb[slot] = r;
@@ -750,39 +764,83 @@ __global__ void __launch_bounds__(kSortThreads)
   }
 #pragma unroll
   for (int it = 0; it < kSortItems; ++it) {
-    const uint32_t i = it * kSortThreads + threadIdx.x;
-    if (i < n) {
-      const uint32_t slot = atomicAdd(&cnt[(uint32_t)((kr[it] - mn) >> sh)], 1u);
+    if (it * kSortThreads + tid < n) {
+      const uint32_t sh = (sb[it] & 1) * 16;
+      const uint32_t slot = (atomicAdd(&cw[sb[it] >> 1], 1u << sh) >> sh) & 0xFFFFu;
       kB[slot] = kr[it];
-      if constexpr (VALS) iB[slot] = (uint16_t)i;
+      if constexpr (VALS) iB[slot] = (uint16_t)(it * kSortThreads + tid);
     }
   }
   __syncthreads();
-  // cnt[j] is now the end of sub-bucket j.
-  for (uint32_t j = threadIdx.x; j < nsub; j += kSortThreads) {
-    const uint32_t b0 = j ? cnt[j - 1] : 0, b1 = cnt[j];
-    for (uint32_t a = b0 + 1; a < b1; ++a) {
-      const uint64_t k = kB[a];
-      uint16_t ix = 0;
-      if constexpr (VALS) ix = iB[a];
-      uint32_t c = a;
-      while (c > b0) {
-        const uint64_t pkey = kB[c - 1];
-        bool gt = pkey > k;
-        if constexpr (VALS) gt = gt || (pkey == k && iB[c - 1] > ix);
-        if (!gt) break;
-        kB[c] = pkey;
-        if constexpr (VALS) iB[c] = iB[c - 1];
-        --c;
+  // c16[j] is now the end of sub-bucket j (= start of j + 1).  Thread per
+  // slot: the key's final position is its slot (singleton), one compare with
+  // its partner (pair) or a rank count (larger, rare); ties by input index
+  // with values (stable), by slot without.  Writes land inside the key's
+  // sub-bucket range, so a warp's stores stay coalesced.
+  for (uint32_t j = tid; j < n; j += kSortThreads) {
+    const uint64_t k = kB[j];
+    uint32_t fin = j;
+    uint16_t ix = 0;
+    if constexpr (VALS) ix = iB[j];
+    if (need_order) {
+      const uint32_t s = sub_of(k);
+      const uint32_t b0 = s ? c16[s - 1] : 0, b1 = c16[s];
+      if (b1 - b0 == 2) {
+        const uint32_t pt = b0 + b1 - 1 - j;
+        const uint64_t pkey = kB[pt];
+        bool before = k < pkey;
+        if constexpr (VALS) before = before || (k == pkey && ix < iB[pt]);
+        else before = before || (k == pkey && j < pt);
+        fin = before ? b0 : b0 + 1;
+      } else if (b1 - b0 > 2) {
+        fin = b0;
+        for (uint32_t q = b0; q < b1; ++q) {
+          const uint64_t kq = kB[q];
+          if constexpr (VALS) fin += kq < k || (kq == k && iB[q] < ix);
+          else fin += kq < k || (kq == k && q < j);
+        }
       }
-      kB[c] = k;
-      if constexpr (VALS) iB[c] = ix;
+    }
+    out[off + fin] = from_ordered<KIND_OUT>(k);
+    if constexpr (VALS) out_vals[off + fin] = src_vals[off + ix];
+  }
+}
+
+// One warp per segment: cells are loaded 32 at a time (coalesced) and the
+// greedy packing state is replicated in every lane through shuffles.
+__global__ void k_pack_cells(const uint32_t* __restrict__ cell_cnt,
+                             const uint64_t* __restrict__ cell_base, int nseg, int nb, uint32_t cap,
+                             OverflowRec* __restrict__ groups, unsigned int* __restrict__ ngroups) {
+  const int s = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (s >= nseg) return;
+  const uint32_t* cnt = cell_cnt + (size_t)s * nb;
+  const uint64_t* base = cell_base + (size_t)s * nb;
+  uint64_t g_off = 0, g_cnt = 0;
+  for (int d0 = 0; d0 < nb; d0 += 32) {
+    const bool ok = d0 + lane < nb;
+    const uint32_t c_l = ok ? cnt[d0 + lane] : 0;
+    const uint64_t b_l = ok ? base[d0 + lane] : 0;
+    for (int i = 0; i < 32; ++i) {
+      const uint32_t c = __shfl_sync(0xffffffffu, c_l, i);
+      const uint64_t bo = __shfl_sync(0xffffffffu, b_l, i);
+      if (c == 0) continue;
+      if (g_cnt + c > cap && g_cnt) {
+        if (lane == 0) {
+          const unsigned int slot = atomicAdd(ngroups, 1u);
+          OverflowRec r; r.off = g_off; r.count = g_cnt; r.lo = 0; r.hi = 0;
+          groups[slot] = r;
+        }
+        g_cnt = 0;
+      }
+      if (g_cnt == 0) g_off = bo;
+      g_cnt += c;
     }
   }
-  __syncthreads();
-  for (uint32_t i = threadIdx.x; i < n; i += kSortThreads) {
-    out[off + i] = from_ordered<KIND_OUT>(kB[i]);
-    if constexpr (VALS) out_vals[off + i] = src_vals[off + iB[i]];
+  if (g_cnt && lane == 0) {
+    const unsigned int slot = atomicAdd(ngroups, 1u);
+    OverflowRec r; r.off = g_off; r.count = g_cnt; r.lo = 0; r.hi = 0;
+    groups[slot] = r;
   }
 }
 
@@ -847,14 +905,14 @@ cudaError_t launch_hist(cudaStream_t st, const void* src, int kind, bool digit, 
   const uint64_t* s = static_cast<const uint64_t*>(src);
   cudaError_t e = cudaSuccess;
   if (digit) {
-    auto fn = k_hist<AMS_KEY_U64, true>;
+    auto fn = k_hist<AMS_KEY_U64, true, false>;
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     fn<<<(unsigned)nchunks, kThreads, smem, st>>>(s, m, blobs, dcls, nspl_cap, nb_stride,
                                                    chunk_tot, seg_hist, minmax);
   } else {
     AMS_KIND_DISPATCH(kind, K, {
-      auto fn = k_hist<K, false>;
+      auto fn = minmax ? k_hist<K, false, true> : k_hist<K, false, false>;
       e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
       fn<<<(unsigned)nchunks, kThreads, smem, st>>>(s, m, blobs, dcls, nspl_cap, nb_stride,
@@ -906,9 +964,9 @@ size_t scatter_smem_bytes(int nb_stride, int nspl_cap, int cells_cap, bool digit
                           bool stable) {
   const int mode = scatter_mode(nb_stride, stable);
   size_t b = (vals ? 16 : 8) * (size_t)kTile;                         // keys (+vals)
-  b += 16 * (size_t)nb_stride;                                        // run + delta
+  b += 8 * (size_t)nb_stride;                                         // running offsets
   b += 4 * (size_t)(mode == kRankWarp ? kWarps : 1) * nb_stride;      // bucket counters
-  b += 8 * (size_t)nb_stride;                                         // totals + tile counts
+  b += 4 * (size_t)nb_stride;                                         // tile bucket starts
   b += 2 * (size_t)kTile;                                             // bucket ids
   b = (b + 15) & ~(size_t)15;
   if (!digit) b += tree_smem_bytes(nspl_cap, cells_cap) + 16;
@@ -957,16 +1015,15 @@ cudaError_t launch_gather_bounds(cudaStream_t st, const uint64_t* bounds, const 
   return cudaGetLastError();
 }
 
-cudaError_t launch_final_ranges(cudaStream_t st, const uint64_t* bounds, int nseg, int nbits,
+cudaError_t launch_final_ranges(cudaStream_t st, const uint64_t* bounds, int nseg, int nb,
                                 DigitCls* out) {
   if (nseg == 0) return cudaSuccess;
-  k_final_ranges<<<(nseg + 127) / 128, 128, 0, st>>>(bounds, nseg, nbits, out);
+  k_final_ranges<<<(nseg + 127) / 128, 128, 0, st>>>(bounds, nseg, nb, out);
   return cudaGetLastError();
 }
 
-size_t smem_sort_bytes() {
-  return (size_t)kSortCap * 8 + ((size_t)4 << kSubBits) + (size_t)kSortCap * 2;
-}
+// keys, 2x u16 sub-bucket counters (+ value index): two CTAs per SM.
+size_t smem_sort_bytes(bool vals) { return (size_t)kSortCap * (vals ? 14 : 12); }
 
 size_t smem_sort_lsd_bytes() {
   return (size_t)kSortCap * (8 + 8 + 2 + 2) + (size_t)4 * kSortWarps * kRadix + 4 * kRadix;
@@ -977,7 +1034,7 @@ cudaError_t launch_smem_sort(cudaStream_t st, const void* src, const void* src_v
                              OverflowRec* ovf, unsigned int* ovf_count, OverflowRec* fb,
                              unsigned int* fb_count) {
   if (ncells == 0) return cudaSuccess;
-  const size_t smem = smem_sort_bytes();
+  const size_t smem = smem_sort_bytes(src_vals != nullptr);
   const uint64_t* s = static_cast<const uint64_t*>(src);
   const uint64_t* sv = static_cast<const uint64_t*>(src_vals);
   uint64_t* o = static_cast<uint64_t*>(out);
@@ -1023,6 +1080,14 @@ cudaError_t launch_smem_sort_lsd(cudaStream_t st, const void* src, const void* s
     AMS_KIND_DISPATCH(kind_out, K, AMS_SORT_GO(K, false))
   }
 #undef AMS_SORT_GO
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_cells(cudaStream_t st, const uint32_t* cell_cnt, const uint64_t* cell_base,
+                              int nseg, int nb, uint32_t cap, OverflowRec* groups,
+                              unsigned int* ngroups) {
+  if (nseg == 0) return cudaSuccess;
+  k_pack_cells<<<(nseg + 3) / 4, 128, 0, st>>>(cell_cnt, cell_base, nseg, nb, cap, groups, ngroups);
   return cudaGetLastError();
 }
 

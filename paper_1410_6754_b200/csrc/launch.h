@@ -27,7 +27,7 @@ struct GroupMeta {
 };
 
 // Work list of the shared-memory sort: mode 0 = cells of a digit
-// partition (cell id = seg << nbits | digit), mode 1 = explicit segments,
+// partition (cell id = seg * nb + digit), mode 1 = explicit segments,
 // mode 2 = records (fallback list on the device).
 struct CellSource {
   int mode;
@@ -38,6 +38,7 @@ struct CellSource {
   const uint64_t* seg_off;
   const uint64_t* seg_len;
   const OverflowRec* recs;
+  const unsigned int* nrecs;  // mode 2: record count on the device (may be null)
 };
 
 cudaError_t launch_gather_sample(cudaStream_t st, const void* src, int kind, const uint64_t* idx,
@@ -74,7 +75,7 @@ cudaError_t launch_child_bounds(cudaStream_t st, const uint8_t* blobs, const Gro
                                 int ngroups, int r, const uint64_t* parent, uint64_t* child);
 cudaError_t launch_gather_bounds(cudaStream_t st, const uint64_t* bounds, const int32_t* sel, int n,
                                  uint64_t* out);
-cudaError_t launch_final_ranges(cudaStream_t st, const uint64_t* bounds, int nseg, int nbits,
+cudaError_t launch_final_ranges(cudaStream_t st, const uint64_t* bounds, int nseg, int nb,
                                 DigitCls* out);
 // Counting + insertion sort of every cell; cells above the shared-memory
 // capacity go to `ovf` (or are copied when constant), clustered cells to `fb`.
@@ -86,6 +87,12 @@ cudaError_t launch_smem_sort(cudaStream_t st, const void* src, const void* src_v
 cudaError_t launch_smem_sort_lsd(cudaStream_t st, const void* src, const void* src_vals, void* out,
                                  void* out_vals, int kind_out, const CellSource& cs,
                                  uint64_t ncells);
+// Greedy packing of consecutive digit cells of each segment into groups of
+// at most `cap` keys (sorting a group = sorting its cells: they are
+// ordered); cells above cap become singleton groups.
+cudaError_t launch_pack_cells(cudaStream_t st, const uint32_t* cell_cnt, const uint64_t* cell_base,
+                              int nseg, int nb, uint32_t cap, OverflowRec* groups,
+                              unsigned int* ngroups);
 cudaError_t launch_map_keys(cudaStream_t st, const void* src, void* dst, uint64_t n, int from,
                             int to);
 
