@@ -143,11 +143,14 @@ int ams_read_splitters(ams_ctx_t* ctx, int group, uint64_t* keys, uint32_t* pos,
  * group h_seg_group[s] (groups are contiguous runs of segments); element
  * position for tie-breaking = buffer index + h_group_posbase[g].  Blocks
  * until the per-segment histogram is in h_seg_hist_out ([nseg][nb_stride]).
- * track_minmax: record global min/max key (for the final sort's ranges). */
+ * track_minmax: record global min/max key (for the final sort's ranges).
+ * stable (used by the following ams_level_scatter) = 0 allows any order
+ * inside one tile's bucket run: valid only for the last level without
+ * values, where only PE membership matters (F7). */
 int ams_level_classify(ams_ctx_t* ctx, const void* src, int key_kind, int nseg,
                        const uint64_t* h_seg_off, const uint64_t* h_seg_len,
                        const int32_t* h_seg_group, int ngroups, const int64_t* h_group_posbase,
-                       int nb_stride, int track_minmax, uint32_t* h_seg_hist_out);
+                       int nb_stride, int track_minmax, int stable, uint32_t* h_seg_hist_out);
 
 /* K4+K6 — stable scatter into (group, source segment, bucket) order
  * (the simple delivery layout: pieces ams.py:240-248, deliver_simple
@@ -155,15 +158,12 @@ int ams_level_classify(ams_ctx_t* ctx, const void* src, int key_kind, int nseg,
  * ams.py:252-256).  Uses the segments of the last ams_level_classify.
  * h_boundaries: [ngroups][r+1] plan boundaries; group g's output begins
  * at dst + h_group_dst_start[g].  vals may be NULL (keys only).
- * stable = 0 allows any order inside one tile's bucket run: valid only for
- * the last level without values, where only PE membership matters (F7).
  * Also derives the key bounds of the ngroups*r child groups; children
  * [child_first, child_first + child_count) are this GPU's groups at the
  * next level (all of them on a single GPU). */
 int ams_level_scatter(ams_ctx_t* ctx, const void* src, const void* src_vals, int key_kind,
                       void* dst, void* dst_vals, int r, const uint64_t* h_boundaries,
-                      const uint64_t* h_group_dst_start, int stable, int child_first,
-                      int child_count);
+                      const uint64_t* h_group_dst_start, int child_first, int child_count);
 
 /* Global min/max key seen by a track_minmax classify (ordered encoding);
  * the multi-rank driver all-reduces them and writes them back before the

@@ -52,8 +52,8 @@ _SIGNATURES = {
     "ams_level_sample": (_I, [_P, _P, _I, _U64, _P, _P, _P, _P]),
     "ams_level_splitters": (_I, [_P, _I, _P, _P, _P, _P]),
     "ams_read_splitters": (_I, [_P, _I, _P, _P, C.POINTER(_I)]),
-    "ams_level_classify": (_I, [_P, _P, _I, _I, _P, _P, _P, _I, _P, _I, _I, _P]),
-    "ams_level_scatter": (_I, [_P, _P, _P, _I, _P, _P, _I, _P, _P, _I, _I, _I]),
+    "ams_level_classify": (_I, [_P, _P, _I, _I, _P, _P, _P, _I, _P, _I, _I, _I, _P]),
+    "ams_level_scatter": (_I, [_P, _P, _P, _I, _P, _P, _I, _P, _P, _I, _I]),
     "ams_final_sort_stats": (_I, [_P, _P]),
     "ams_get_minmax": (_I, [_P, _P]),
     "ams_set_minmax": (_I, [_P, _P]),
@@ -266,22 +266,23 @@ class Context:
         return keys[: n.value].copy(), pos[: n.value].copy()
 
     def level_classify(self, src, kind, seg_off, seg_len, seg_group, group_posbase, nb_stride,
-                       track_minmax):
+                       track_minmax, stable=True):
         so, sl, sg, pb = u64(seg_off), u64(seg_len), i32(seg_group), i64(group_posbase)
         out = np.zeros((len(so), nb_stride), np.uint32)
         check(lib.ams_level_classify(self.h, ptr(src), kind, len(so), so.ctypes.data,
                                      sl.ctypes.data, sg.ctypes.data, len(pb), pb.ctypes.data,
-                                     nb_stride, int(bool(track_minmax)), out.ctypes.data))
+                                     nb_stride, int(bool(track_minmax)), int(bool(stable)),
+                                     out.ctypes.data))
         return out
 
     def level_scatter(self, src, src_vals, kind, dst, dst_vals, r, boundaries, group_dst_start,
-                      stable=True, child_first=0, child_count=None):
+                      child_first=0, child_count=None):
         b, d = u64(boundaries), u64(group_dst_start)
         if child_count is None:
             child_count = len(d) * r
         check(lib.ams_level_scatter(self.h, ptr(src), ptr(src_vals), kind, ptr(dst), ptr(dst_vals),
-                                    r, b.ctypes.data, d.ctypes.data, int(bool(stable)),
-                                    int(child_first), int(child_count)))
+                                    r, b.ctypes.data, d.ctypes.data, int(child_first),
+                                    int(child_count)))
 
     def final_sort_stats(self):
         out = np.zeros(2, np.uint64)

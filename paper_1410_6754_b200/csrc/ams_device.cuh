@@ -105,11 +105,22 @@ __device__ __forceinline__ uint64_t ldg_stream(const uint64_t* p) {
 }
 
 // ---- tree classifier in shared memory ------------------------------------
+// Shared-memory loads by 32-bit shared address (a generic pointer kept in a
+// struct compiles to generic LD.E; these stay LDS).
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint64_t lds_u64(uint32_t a) {
+  uint64_t v;
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
+  return v;
+}
+
 struct TreeView {
   ClsHeader h;
-  const uint64_t* skeys;
-  const uint32_t* spos;
-  const uint32_t* lut;
+  uint32_t skeys, spos, lut;  // shared addresses
 
   // Bucket of (key, pos) = number of splitters strictly below it under the
   // (key, position) order — bisect_left on tie-broken elements
@@ -120,13 +131,17 @@ struct TreeView {
     if (h.nspl == 0) return 0;
     uint64_t c = (key - h.lo) >> h.shift;
     c = key < h.lo ? 0 : (c >= h.ncells ? h.ncells - 1 : c);
-    const uint32_t rec = lut[c];
+    const uint32_t rec = lds_u32(lut + 4 * (uint32_t)c);
     uint32_t b = rec & 0xFFFFu;
-    const uint32_t end = b + (rec >> 16);
-    while (b < end) {
-      const uint64_t sk = skeys[b];
-      if (!(sk < key || (sk == key && spos[b] < pos))) break;
-      ++b;
+    const uint32_t inside = rec >> 16;
+    if (inside == 0) return b;
+    // Usually one splitter shares the cell: one compare; more are rare.
+    const uint64_t sk = lds_u64(skeys + 8 * b);
+    if (!(sk < key || (sk == key && lds_u32(spos + 4 * b) < pos))) return b;
+    const uint32_t end = b + inside;
+    for (++b; b < end; ++b) {
+      const uint64_t sk2 = lds_u64(skeys + 8 * b);
+      if (!(sk2 < key || (sk2 == key && lds_u32(spos + 4 * b) < pos))) break;
     }
     return b;
   }
@@ -152,7 +167,9 @@ __device__ inline TreeView load_tree(const uint8_t* blob, uint8_t* smem, int nsp
   for (uint32_t i = threadIdx.x; i < v.h.nspl; i += blockDim.x) { sk[i] = gk[i]; sp[i] = gp[i]; }
   if (v.h.nspl)
     for (uint32_t i = threadIdx.x; i < v.h.ncells; i += blockDim.x) lu[i] = gl[i];
-  v.skeys = sk; v.spos = sp; v.lut = lu;
+  v.skeys = (uint32_t)__cvta_generic_to_shared(sk);
+  v.spos = (uint32_t)__cvta_generic_to_shared(sp);
+  v.lut = (uint32_t)__cvta_generic_to_shared(lu);
   return v;
 }
 

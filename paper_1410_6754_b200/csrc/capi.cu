@@ -147,6 +147,7 @@ struct ams_ctx {
   std::vector<int32_t> group_first, group_nseg;
   SegMeta meta{};
   DevBuf chunk_tot, seg_hist, cell_base, pieces, minmax;
+  bool level_stable = true;
   // key bounds [lo, hi] of the current level's groups (ping-pong)
   DevBuf bounds[2];
   int bcur = 0;
@@ -246,7 +247,8 @@ cudaError_t upload_segments(Stage& st, cudaStream_t stream, const uint64_t* off,
   return cudaSuccess;
 }
 
-// hist -> chunk scan for a segment table whose classifiers are ready.
+// Histogram pass (classify -> chunk and segment histograms) then the chunk
+// scan, for a segment table whose classifiers are ready.
 int run_histogram(ams_ctx* c, const void* src, int kind, bool digit, const SegMeta& m,
                   uint64_t nchunks, int nb_stride, const DigitCls* dcls,
                   unsigned long long* minmax, uint64_t nelems) {
@@ -437,7 +439,7 @@ int ams_read_splitters(ams_ctx_t* c, int group, uint64_t* keys, uint32_t* pos, i
 int ams_level_classify(ams_ctx_t* c, const void* src, int key_kind, int nseg,
                        const uint64_t* h_seg_off, const uint64_t* h_seg_len,
                        const int32_t* h_seg_group, int ngroups, const int64_t* h_group_posbase,
-                       int nb_stride, int track_minmax, uint32_t* h_seg_hist_out) {
+                       int nb_stride, int track_minmax, int stable, uint32_t* h_seg_hist_out) {
   if (!c) return set_error(AMS_EINVAL, "null context");
   if (nseg < 1 || !h_seg_off || !h_seg_len || !h_seg_group || !h_group_posbase)
     return set_error(AMS_EINVAL, "bad segment list");
@@ -480,6 +482,7 @@ int ams_level_classify(ams_ctx_t* c, const void* src, int key_kind, int nseg,
   uint64_t nel = 0;
   for (int s = 0; s < nseg; ++s) nel += h_seg_len[s];
   c->level_elems = nel;
+  c->level_stable = stable != 0;
   int rc = run_histogram(c, src, key_kind, false, c->meta, c->nchunks, nb_stride, nullptr, mm,
                          nel);
   if (rc) return rc;
@@ -502,8 +505,7 @@ int ams_level_classify(ams_ctx_t* c, const void* src, int key_kind, int nseg,
 
 int ams_level_scatter(ams_ctx_t* c, const void* src, const void* src_vals, int key_kind,
                       void* dst, void* dst_vals, int r, const uint64_t* h_boundaries,
-                      const uint64_t* h_group_dst_start, int stable, int child_first,
-                      int child_count) {
+                      const uint64_t* h_group_dst_start, int child_first, int child_count) {
   if (!c) return set_error(AMS_EINVAL, "null context");
   if (c->nseg == 0) return set_error(AMS_EINVAL, "ams_level_classify must run first");
   if (r < 1 || !h_boundaries || !h_group_dst_start) return set_error(AMS_EINVAL, "bad plan");
@@ -539,11 +541,11 @@ int ams_level_scatter(ams_ctx_t* c, const void* src, const void* src_vals, int k
                             c->pieces.as<uint64_t>(), c->cell_base.as<uint64_t>()));
   }
   {
-    KTimer kt(c, stable ? AMS_KCAT_SCATTER : AMS_KCAT_SCATTER_U,
+    KTimer kt(c, c->level_stable ? AMS_KCAT_SCATTER : AMS_KCAT_SCATTER_U,
               (src_vals ? 32.0 : 16.0) * c->level_elems);
-    AMS_CK(launch_scatter(c->stream, src, src_vals, key_kind, false, stable != 0, dst, dst_vals,
-                          c->meta, c->nchunks, c->blobs.as<uint8_t>(), nullptr, c->nspl_cap,
-                          c->cells_cap, c->nb_stride, c->chunk_tot.as<uint32_t>(),
+    AMS_CK(launch_scatter(c->stream, src, src_vals, key_kind, false, c->level_stable, dst,
+                          dst_vals, c->meta, c->nchunks, c->blobs.as<uint8_t>(), nullptr,
+                          c->nspl_cap, c->cells_cap, c->nb_stride, c->chunk_tot.as<uint32_t>(),
                           c->cell_base.as<uint64_t>()));
   }
   // Key bounds of the next level's groups (this rank's children).

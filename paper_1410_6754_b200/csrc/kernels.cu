@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(kThreads) k_hist(const uint64_t* __restrict__ 
       if (FULL || e < tcount) {
         uint32_t b;
         if constexpr (DIGIT) b = dv.classify(keys[i], 0);
-        else b = tv.classify(keys[i], (uint32_t)((int64_t)(base + e) + posbase));
+        else b = tv.classify(keys[i], (uint32_t)((int64_t)base + posbase) + e);
         if constexpr (MINMAX) { mn = min(mn, (unsigned long long)keys[i]); mx = max(mx, (unsigned long long)keys[i]); }
         if (b != cur) {
           if (cnt) atomicAdd(&hist[cur], cnt);
@@ -344,17 +344,24 @@ constexpr int kRankAtomic = 2;   // unstable (keys only, order inside a run is f
 
 // Stable rank of this lane's item among the warp's items in the same bucket
 // (lower lanes first), plus the per-warp bucket counter update.  Peers are
-// found with one ballot per bucket-id bit (and one for validity):
-// __match_any_sync costs ~57 SM-cycles per warp on B200 (tools/microbench).
-__device__ __forceinline__ uint32_t warp_stable_rank(uint32_t b, int nbits, int lane, uint32_t lt,
-                                                     uint32_t* whw) {
+// found with one ballot per bucket-id bit (and one for validity unless the
+// whole warp is valid): __match_any_sync costs ~57 SM-cycles per warp on
+// B200 (tools/microbench.cu).  NBITS is a compile-time width so the vote
+// chain unrolls to ~3 instructions per bit.
+template <int NBITS>
+__device__ __forceinline__ uint32_t warp_stable_rank(uint32_t b, int lane, uint32_t lt,
+                                                     uint32_t* whw, bool all_valid) {
   const bool valid = b != kInvalid;
-  uint32_t peers = __ballot_sync(0xffffffffu, valid);
-  if (!valid) peers = ~peers;
-  for (int bit = 0; bit < nbits; ++bit) {
-    const bool x = (b >> bit) & 1u;
+  uint32_t peers = 0xffffffffu;
+  if (!all_valid) {
+    const uint32_t v = __ballot_sync(0xffffffffu, valid);
+    peers = valid ? v : ~v;
+  }
+#pragma unroll
+  for (int bit = 0; bit < NBITS; ++bit) {
+    const uint32_t x = (b >> bit) & 1u;
     const uint32_t bal = __ballot_sync(0xffffffffu, x);
-    peers &= x ? bal : ~bal;
+    peers &= ~(bal ^ (0u - x));  // lanes whose bit equals mine
   }
   uint32_t cnt = 0;
   if (valid) cnt = whw[b];
@@ -364,22 +371,29 @@ __device__ __forceinline__ uint32_t warp_stable_rank(uint32_t b, int nbits, int 
   return cnt + __popc(peers & lt);
 }
 
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
 // One CTA per chunk (the histogram kernel's chunks): the running output
-// offset of every bucket starts at cell base + the chunk's exclusive prefix;
-// each tile is classified, ranked, reordered bucket-major in shared memory
-// and written as coalesced runs, then the running offsets advance.  With a
-// stable mode the order inside a bucket is the input order — the stable
-// (cell, position) order the reference's concatenations produce.
+// offset of every bucket starts at cell base + the chunk's exclusive prefix.
+// Per tile: cp.async stages the keys in shared memory, every key is
+// classified and ranked from there, the tile is permuted bucket-major in
+// place (keys pass through registers only for that step, so the kernel fits
+// 4 CTAs per SM) and written as coalesced runs; the running offsets
+// advance.  With a stable mode the order inside a bucket is the input order
+// — the stable (cell, position) order the reference's concatenations produce.
 template <int KIND, bool DIGIT, bool VALS, int MODE>
-__global__ void __launch_bounds__(kThreads) k_scatter(const uint64_t* __restrict__ src,
-                                                      const uint64_t* __restrict__ src_vals,
-                                                      uint64_t* __restrict__ dst,
-                                                      uint64_t* __restrict__ dst_vals, SegMeta m,
-                                                      const uint8_t* __restrict__ blobs,
-                                                      const DigitCls* __restrict__ dcls,
-                                                      int nspl_cap, int nb_stride,
-                                                      const uint32_t* __restrict__ chunk_tot,
-                                                      const uint64_t* __restrict__ cell_base) {
+__global__ void __launch_bounds__(kThreads, VALS ? 2 : 4)
+    k_scatter(const uint64_t* __restrict__ src, const uint64_t* __restrict__ src_vals,
+              uint64_t* __restrict__ dst, uint64_t* __restrict__ dst_vals, SegMeta m,
+              const uint8_t* __restrict__ blobs, const DigitCls* __restrict__ dcls, int nspl_cap,
+              int nb_stride, const uint32_t* __restrict__ chunk_tot,
+              const uint64_t* __restrict__ cell_base) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ int s_seg;
   __shared__ uint32_t s_scan[kWarps + 1];
@@ -422,39 +436,50 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const uint64_t* __restrict
   for (uint64_t t0 = first; t0 < last; t0 += kTile) {
     const uint32_t tcount = (uint32_t)min((uint64_t)kTile, last - t0);
     const uint64_t base = seg_off + t0;
+    for (uint32_t j = threadIdx.x; j < tcount; j += kThreads) {
+      cp_async8(keys_s + j, src + base + j);
+      if constexpr (VALS) cp_async8(vals_s + j, src_vals + base + j);
+    }
     for (int i = threadIdx.x; i < kHists * nb_stride; i += kThreads) wh[i] = 0;
-    uint64_t keys[kItems];
-    uint64_t vals[VALS ? kItems : 1];
+    cp_async_wait_all();
+    __syncthreads();  // tile staged, counters zeroed, tree loaded
     uint32_t pk[kItems];
+    auto classify_all = [&](auto full_tag) {
+      constexpr bool FULL = decltype(full_tag)::value;
+      const uint32_t pos0 = (uint32_t)((int64_t)base + posbase);
 #pragma unroll
-    for (int i = 0; i < kItems; ++i) {
-      const uint32_t e = w * (kItems * 32) + i * 32 + lane;
-      keys[i] = e < tcount ? to_ordered<KIND>(ldg_stream(src + base + e)) : 0;
-      if constexpr (VALS) vals[i] = e < tcount ? ldg_stream(src_vals + base + e) : 0;
-    }
-    __syncthreads();  // counters zeroed, tree loaded, previous tile written out
-#pragma unroll
-    for (int i = 0; i < kItems; ++i) {
-      const uint32_t e = w * (kItems * 32) + i * 32 + lane;
-      uint32_t b = kInvalid;
-      if (e < tcount) {
-        if constexpr (DIGIT) b = dv.classify(keys[i], 0);
-        else b = tv.classify(keys[i], (uint32_t)((int64_t)(base + e) + posbase));
+      for (int i = 0; i < kItems; ++i) {
+        const uint32_t e = w * (kItems * 32) + i * 32 + lane;
+        uint32_t b = kInvalid;
+        if (FULL || e < tcount) {
+          const uint64_t key = to_ordered<KIND>(keys_s[e]);
+          if constexpr (DIGIT) b = dv.classify(key, 0);
+          else b = tv.classify(key, pos0 + e);
+        }
+        pk[i] = b;
+        if constexpr (MODE == kRankAtomic) {
+          if (FULL || b != kInvalid) pk[i] = (b << 16) | atomicAdd(&whw[b], 1u);
+        }
       }
-      pk[i] = b;
-      if constexpr (MODE == kRankAtomic) {
-        if (b != kInvalid) pk[i] = (b << 16) | atomicAdd(&whw[b], 1u);
-      }
-    }
+    };
+    if (tcount == (uint32_t)kTile) classify_all(std::true_type{});
+    else classify_all(std::false_type{});
     if constexpr (MODE != kRankAtomic) {
+      const bool full = tcount == (uint32_t)kTile;
+      auto rank_all = [&](auto nbits_tag) {
+        constexpr int NB = decltype(nbits_tag)::value;
+#pragma unroll
+        for (int i = 0; i < kItems; ++i) {
+          const uint32_t b = pk[i];
+          const uint32_t r = warp_stable_rank<NB>(b, lane, lt, whw, full);
+          if (b != kInvalid) pk[i] = (b << 16) | r;
+        }
+      };
       for (int turn = 0; turn < (MODE == kRankSerial ? kWarps : 1); ++turn) {
         if (MODE == kRankWarp || w == turn) {
-#pragma unroll
-          for (int i = 0; i < kItems; ++i) {
-            const uint32_t b = pk[i];
-            const uint32_t r = warp_stable_rank(b, nbits, lane, lt, whw);
-            if (b != kInvalid) pk[i] = (b << 16) | r;
-          }
+          if (nbits <= 7) rank_all(std::integral_constant<int, 7>{});
+          else if (nbits <= 9) rank_all(std::integral_constant<int, 9>{});
+          else rank_all(std::integral_constant<int, 12>{});
         }
         if (MODE == kRankSerial) __syncthreads();
       }
@@ -472,14 +497,26 @@ __global__ void __launch_bounds__(kThreads) k_scatter(const uint64_t* __restrict
     }
     __syncthreads();
     block_excl_scan<kThreads>(btot, nb_stride, s_scan);
+    // Permute the staged tile bucket-major in place.
+    {
+      uint64_t kr[kItems];
+      uint64_t vr[VALS ? kItems : 1];
 #pragma unroll
-    for (int i = 0; i < kItems; ++i) {
-      if (pk[i] != kInvalid) {
-        const uint32_t b = pk[i] >> 16;
-        const uint32_t slot = btot[b] + whw[b] + (pk[i] & 0xFFFFu);
-        keys_s[slot] = keys[i];
-        bkt_s[slot] = (uint16_t)b;
-        if constexpr (VALS) vals_s[slot] = vals[i];
+      for (int i = 0; i < kItems; ++i) {
+        const uint32_t e = w * (kItems * 32) + i * 32 + lane;
+        kr[i] = keys_s[e];
+        if constexpr (VALS) vr[i] = vals_s[e];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < kItems; ++i) {
+        if (pk[i] != kInvalid) {
+          const uint32_t b = pk[i] >> 16;
+          const uint32_t slot = btot[b] + whw[b] + (pk[i] & 0xFFFFu);
+          keys_s[slot] = to_ordered<KIND>(kr[i]);
+          bkt_s[slot] = (uint16_t)b;
+          if constexpr (VALS) vals_s[slot] = vr[i];
+        }
       }
     }
     __syncthreads();
@@ -630,7 +667,7 @@ __global__ void __launch_bounds__(kSortThreads, 1)
         const uint32_t e = w * chunk + it * 32 + lane;
         const bool valid = (it * 32 < (int)chunk) && e < n;
         const uint32_t d = valid ? (uint32_t)(((kA[e] - mn) >> sh) & 255) : kInvalid;
-        const uint32_t r = warp_stable_rank(d, 8, lane, lt, whw);
+        const uint32_t r = warp_stable_rank<8>(d, lane, lt, whw, false);
         pk[it] = valid ? ((d << 16) | r) : kInvalid;
       }
       __syncthreads();

@@ -196,15 +196,15 @@ class AmsSorter:
             seg_group = np.repeat(np.arange(G, dtype=np.int32), gn)
             posbase = -offs[gf].astype(np.int64)
             nb_stride = int(nb.max())
-            hist = self.ctx.level_classify(src, src_kind, offs[:-1], sizes, seg_group, posbase,
-                                           nb_stride, track_minmax=(lv == 0))
-            bnd, loads, mx, new_sizes, stats = L.plan_level(gn, nb, r, hist, with_stats)
-            dst, dst_v = work[lv % 2], work_v[lv % 2]
             # Only PE membership matters at the last level (F7): keys-only
             # runs may drop in-tile order there.
             last_level = lv == len(params.group_counts) - 1
-            self.ctx.level_scatter(src, src_v, src_kind, dst, dst_v, r, bnd, offs[gf],
-                                   stable=not (last_level and vals is None))
+            hist = self.ctx.level_classify(src, src_kind, offs[:-1], sizes, seg_group, posbase,
+                                           nb_stride, track_minmax=(lv == 0),
+                                           stable=not (last_level and vals is None))
+            bnd, loads, mx, new_sizes, stats = L.plan_level(gn, nb, r, hist, with_stats)
+            dst, dst_v = work[lv % 2], work_v[lv % 2]
+            self.ctx.level_scatter(src, src_v, src_kind, dst, dst_v, r, bnd, offs[gf])
             rec = LevelRecord(lv, r, gf.copy(), gn.copy(), sizes.copy(), drawn, nb, hist, bnd,
                               loads, mx, load_budget(n_g, r, eps_l), new_sizes, stats)
             if record_splitters:
