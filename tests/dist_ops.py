@@ -1,0 +1,114 @@
+"""CPU stand-in for CudaOps used ONLY by tests/test_dist_gloo.py: the
+device steps restated with the numpy oracle so the multi-rank orchestration
+in paper_1410_6754_b200/dist.py (sample all-gather, histogram all-gather,
+replicated plan, exchange offsets) can run over gloo without a GPU.  The
+product path never uses this (it raises without CUDA)."""
+
+import numpy as np
+import torch
+
+from oracle import ams_oracle as O
+
+U64 = np.uint64
+SIGN = np.uint64(1 << 63)
+
+
+def _u(t: torch.Tensor) -> np.ndarray:
+    return t.numpy().view(np.uint64)
+
+
+def _ordered(x: np.ndarray, kind: int) -> np.ndarray:
+    if kind == 1:  # int64
+        return x ^ SIGN
+    if kind == 2:  # float64 bits
+        neg = (x >> np.uint64(63)).astype(bool)
+        return np.where(neg, ~x, x | SIGN)
+    return x
+
+
+def _from_ordered(x: np.ndarray, kind: int) -> np.ndarray:
+    if kind == 1:
+        return x ^ SIGN
+    if kind == 2:
+        top = (x >> np.uint64(63)).astype(bool)
+        return np.where(top, x & ~SIGN, ~x)
+    return x
+
+
+class NumpyOps:
+    def __init__(self):
+        self.spl = []
+        self.lvl = None
+        self.mm = (0, 0)
+
+    def empty(self, n, dtype=torch.int64):
+        return torch.zeros(max(n, 1), dtype=dtype)
+
+    def workspace(self, n, with_vals):
+        mk = lambda: torch.zeros(max(n, 1), dtype=torch.int64)
+        return [mk(), mk()], ([mk(), mk()] if with_vals else [None, None])
+
+    def sample(self, src, kind, idx, gpos, out_keys, out_pos):
+        idx = np.asarray(idx, np.int64)
+        if len(idx):
+            _u(out_keys)[:len(idx)] = _ordered(_u(src)[idx], kind)
+            out_pos.numpy()[:len(idx)] = np.asarray(gpos, np.int64).astype(np.int32)
+
+    def splitters(self, s_keys, s_pos, soff, nb):
+        keys, pos = _u(s_keys), s_pos.numpy().astype(np.int64)
+        self.spl = []
+        for g in range(len(nb)):
+            a, b = int(soff[g]), int(soff[g + 1])
+            self.spl.append(O.select_splitters(keys[a:b].copy(), pos[a:b].copy(), int(nb[g])))
+
+    def classify(self, src, kind, offs, sizes, seg_group, posbase, nb_stride, track_minmax, stable):
+        x = _u(src)
+        hist = np.zeros((len(sizes), nb_stride), np.uint32)
+        self.lvl = []
+        lo, hi = ~np.uint64(0), np.uint64(0)
+        for s in range(len(sizes)):
+            o, n = int(offs[s]), int(sizes[s])
+            k = _ordered(x[o:o + n], kind)
+            g = int(seg_group[s])
+            pos = np.arange(o, o + n, dtype=np.int64) + int(posbase[g])
+            b = O.classify(k, pos, *self.spl[g])
+            np.add.at(hist[s], b, 1)
+            self.lvl.append((o, n, g, k, b))
+            if n:
+                lo, hi = min(lo, k.min()), max(hi, k.max())
+        if track_minmax:
+            self.mm = (int(lo), int(hi))
+        return hist
+
+    def get_minmax(self):
+        return self.mm
+
+    def set_minmax(self, lo, hi):
+        self.mm = (lo, hi)
+
+    def scatter(self, src, src_v, kind, dst, dst_v, r, bnd, dst_start, child_first, child_count):
+        d = _u(dst)
+        vs = src_v.numpy() if src_v is not None else None
+        groups = sorted({g for _, _, g, _, _ in self.lvl})
+        for g in groups:
+            segs = [t for t in self.lvl if t[2] == g]
+            keys = np.concatenate([t[3] for t in segs]) if segs else np.zeros(0, U64)
+            bk = np.concatenate([t[4] for t in segs]) if segs else np.zeros(0, np.int64)
+            j = np.concatenate([np.full(t[1], i) for i, t in enumerate(segs)]) if segs else bk
+            gid = np.searchsorted(np.asarray(bnd[g], np.int64), bk, side="right") - 1
+            order = np.argsort((gid * len(segs) + j) * (1 << 20) + bk, kind="stable")
+            st = int(dst_start[g])
+            d[st:st + len(keys)] = keys[order]
+            if vs is not None:
+                v = np.concatenate([vs[t[0]:t[0] + t[1]] for t in segs])
+                dst_v.numpy()[st:st + len(keys)] = v[order]
+
+    def final_sort(self, src, src_v, tmp, tmp_v, out, out_v, kind, offs, sizes):
+        x = _u(src)
+        o_ = _u(out)
+        for s in range(len(sizes)):
+            o, n = int(offs[s]), int(sizes[s])
+            order = np.argsort(x[o:o + n], kind="stable")
+            o_[o:o + n] = _from_ordered(x[o:o + n][order], kind)
+            if src_v is not None:
+                out_v.numpy()[o:o + n] = src_v.numpy()[o:o + n][order]

@@ -210,3 +210,37 @@ def test_config2_full_size_properties(api, dist):
     assert np.array_equal(out, keys)
     assert int(res.pe_sizes.max()) <= 1.1 * n / 64
     assert sum(r["over_budget"] for r in res.reports) == 0
+
+
+def test_distributed_path_world1_nccl():
+    """dist.sort_distributed over NCCL at world size 1 (CudaOps + the
+    exchange code on a real GPU) equals the oracle."""
+    import os
+    import socket
+    import torch.distributed as dist
+    from paper_1410_6754_b200 import AmsParams, SeedSpec
+    from paper_1410_6754_b200.api import get_sorter
+    from paper_1410_6754_b200.dist import CudaOps, sort_distributed
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        groups, npe = (8, 8), 5000
+        p = 64
+        n = p * npe
+        keys = np.random.default_rng(3).integers(0, 2**64, n, dtype=np.uint64)
+        vals = np.arange(n, dtype=np.int64)
+        ref = O.ams_sort(keys, [npe] * p, groups, None, 16, 0.1, 9, "algo/rep0", vals=vals)
+        out, ov, sizes, levels = sort_distributed(
+            dev_u64(keys), [npe] * p, AmsParams(groups, None, 16, 0.1), SeedSpec(9, "algo/rep0"),
+            CudaOps(get_sorter(0)), vals=torch.from_numpy(vals).cuda(), key_kind="u64")
+        torch.cuda.synchronize()
+        assert np.array_equal(host_u64(out), ref.keys)
+        assert np.array_equal(ov.cpu().numpy(), ref.vals)
+        assert [int(x) for x in sizes] == list(ref.pe_sizes)
+    finally:
+        dist.destroy_process_group()
