@@ -82,6 +82,22 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def committed_traffic(kernel: str, workload: str, n: int):
+    """dram read+write bytes per launch of `kernel` from the committed ncu
+    --set full capture (profiles/ncu_traffic.json), when it was taken on this
+    workload's shape; else None."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+    except Exception:
+        return None
+    if workload != d.get("workload", "cfg2") or int(d.get("n_keys", 0)) != n:
+        return None
+    k = d["kernels"].get(kernel)
+    return None if k is None else float(k["traffic"])
+
+
 # ------------------------------------------------------------------ clocks
 _REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
             0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
@@ -272,7 +288,9 @@ def ours_arm(args, w):
     t_roof_ms = b_hbm / (peak * 1e9) * 1e3
     roofline = {
         "bound": "hbm", "kernel": dname, "achieved": achieved, "peak": peak, "unit": "GB/s",
-        "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+        "frac": achieved / peak, "traffic": committed_traffic(dname, args.workload, n),
+        "traffic_source": "profiles/ncu_traffic.json (ncu --set full, same workload)",
+        "peak_source": peak_src,
         "bytes_per_launch": dbytes / max(dlaunch, 1), "avg_launch_ms": dms / max(dlaunch, 1),
         "share_of_step": dms / max(total_kernel_ms, 1e-9),
         "step": {"algorithmic_bytes": b_hbm, "t_roof_ms": t_roof_ms,
