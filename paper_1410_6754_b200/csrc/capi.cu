@@ -742,6 +742,7 @@ int ams_final_sort(ams_ctx_t* c, void* src, void* src_vals, void* tmp, void* tmp
     cs.cell_base = c->cell_base.as<uint64_t>();
     cs.cell_cnt = c->seg_hist.as<uint32_t>();
     cs.dcls = c->dcls.as<DigitCls>();
+    cs.cells_per_seg = (uint32_t)nbs;
     rc = sort_cells(c, oth, oth_v, out, out_vals, key_kind, cs, (uint64_t)nb_seg * nbs, nel);
     if (rc) return rc;
     // Cells that still exceed shared memory go round again (sort_cells synced).

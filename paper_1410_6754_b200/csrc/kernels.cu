@@ -705,18 +705,74 @@ __global__ void __launch_bounds__(kSortThreads, 1)
 }
 
 // One CTA per cell (<= kSortCap keys), keys held in registers:
-//  1. counting sort into ~n..2n sub-buckets by the scaled key
-//     (key - min) * 2n >> bitlen(max - min), with 16-bit counters packed in
-//     pairs (shared atomics) — uniform keys land ~0.5-1 per sub-bucket;
-//  2. each key finds its final slot inside its sub-bucket: singleton (most
-//     keys) — its own; pair — one compare with the partner; larger (rare) —
-//     a rank count; ties by input index with values (stable), by slot
-//     without;
-//  3. coalesced write-out.
-// When the range is narrower than n each sub-bucket is one key value (no
-// ordering needed for keys alone).  Cells whose keys cluster (a sub-bucket
-// above kRankMax that still needs ordering) go to the LSD fallback list.
+//  1. one shared atomic per key counts it into one of kSubK sub-buckets (16-
+//     bit counters packed in pairs); the atomic's return value is the key's
+//     rank inside its sub-bucket, so placement needs no second pass.
+//     Digit cells of the final partition use the partition digit refined by
+//     kSubK: sub = mulhi(key - lo, mult * kSubK) - digit * kSubK, exact since
+//     floor(floor(x*m*K / 2^64) / K) = floor(x*m / 2^64) — no min/max pass.
+//     Other cells (and digit cells whose keys cluster) scale (key - min) to
+//     2n sub-buckets by the cell's own min/max;
+//  2. register-blocked exclusive scan of the counters (thread t owns words
+//     [16t, 16t + 16); conflict-free 128-bit accesses), fused with the scan of how many
+//     multi-key sub-buckets each thread will queue;
+//  3. keys go to slot start(sub-bucket) + rank; the key of rank 1 queues its
+//     sub-bucket (one entry per sub-bucket holding >= 2 keys);
+//  4. thread per queued sub-bucket: 2 or 3 keys by a compare-exchange
+//     network; larger ones (rare) are re-queued and insertion-sorted, in
+//     place; ties by input index with values (stable), any order of equal
+//     keys without;
+//  5. coalesced (16-byte) copy to the output.
+// When the range is narrower than 2n each sub-bucket is one key value, so
+// keys alone skip step 4.  Cells whose keys cluster (a sub-bucket above
+// kRankMax that still needs ordering) go to the LSD fallback list.
 constexpr int kRankMax = 64;
+constexpr int kSubK = 2 * kSortCap;                   // sub-buckets of the refined digit
+constexpr int kScanWords = kSubK / 2 / kSortThreads;  // counter words per thread (2 sub-buckets each)
+static_assert(kScanWords % 4 == 0, "scan loads 4 words at a time");
+constexpr int kQueueCap = kSortCap / 2;               // sub-buckets with >= 2 keys
+
+// Counter layout: thread t of the scan owns logical words [16t, 16t + 16) as
+// four uint4 chunks; chunk c is stored at chunk c ^ ((t >> 1) & 3) of its
+// 64-byte block, so the 8 threads of one 128-bit shared-memory phase hit 32
+// distinct banks.  Logical word w lives at w ^ (((w >> 5) & 3) << 2); the
+// u16 counter of sub-bucket s at sw16(s).
+__device__ __forceinline__ uint32_t sw_word(uint32_t w) { return w ^ (((w >> 5) & 3u) << 2); }
+__device__ __forceinline__ uint32_t sw16(uint32_t s) { return s ^ ((s >> 3) & 0x18u); }
+
+template <bool VALS>
+__device__ __forceinline__ bool slot_after(uint64_t ka, uint16_t ia, uint64_t kb, uint16_t ib) {
+  if constexpr (VALS) return ka > kb || (ka == kb && ia > ib);
+  else return ka > kb;
+}
+
+template <bool VALS>
+__device__ __forceinline__ void cmp_swap(uint64_t& ka, uint16_t& ia, uint64_t& kb, uint16_t& ib) {
+  if (slot_after<VALS>(ka, ia, kb, ib)) {
+    const uint64_t t = ka; ka = kb; kb = t;
+    if constexpr (VALS) { const uint16_t u = ia; ia = ib; ib = u; }
+  }
+}
+
+template <bool VALS>
+__device__ __forceinline__ void insertion_sort(uint64_t* kB, uint16_t* iB, uint32_t b0, uint32_t b1) {
+  for (uint32_t a = b0 + 1; a < b1; ++a) {
+    const uint64_t ka = kB[a];
+    uint16_t ia = 0;
+    if constexpr (VALS) ia = iB[a];
+    uint32_t d = a;
+    while (d > b0) {
+      uint16_t ib = 0;
+      if constexpr (VALS) ib = iB[d - 1];
+      if (!slot_after<VALS>(kB[d - 1], ib, ka, ia)) break;
+      kB[d] = kB[d - 1];
+      if constexpr (VALS) iB[d] = ib;
+      --d;
+    }
+    kB[d] = ka;
+    if constexpr (VALS) iB[d] = ia;
+  }
+}
 
 template <int KIND_OUT, bool VALS>
 __global__ void __launch_bounds__(kSortThreads, 4)
@@ -728,10 +784,12 @@ __global__ void __launch_bounds__(kSortThreads, 4)
   __shared__ uint64_t s_mm[2 * kSortWarps];
   __shared__ uint32_t s_scan[kSortWarps + 1];
   __shared__ uint32_t s_max[kSortWarps];
+  __shared__ uint32_t s_q2;
   uint64_t* kB = reinterpret_cast<uint64_t*>(smem);
-  uint32_t* cw = reinterpret_cast<uint32_t*>(kB + kSortCap);   // [kSortCap] words = 2*cap u16
+  uint32_t* cw = reinterpret_cast<uint32_t*>(kB + kSortCap);   // [kSubK / 2] words of u16 pairs
   const uint16_t* c16 = reinterpret_cast<const uint16_t*>(cw);
-  uint16_t* iB = reinterpret_cast<uint16_t*>(cw + kSortCap);    // input index of slot j (VALS)
+  uint16_t* qB = reinterpret_cast<uint16_t*>(cw + kSubK / 2);   // queued sub-buckets
+  uint16_t* iB = qB + kQueueCap;                                // input index of slot j (VALS)
 
   uint64_t off, count;
   cell_of(cs, blockIdx.x, off, count);
@@ -740,106 +798,197 @@ __global__ void __launch_bounds__(kSortThreads, 4)
     return;
   const uint32_t n = (uint32_t)count;
   const uint32_t tid = threadIdx.x;
+  const int lane = tid & 31, wid = tid >> 5;
+  // Refined partition digit (first-round digit cells with room for x kSubK).
+  uint64_t lo = 0, mult = 0;
+  uint32_t sub0 = 0, sub_max = kSubK - 1;
+  int attempt = 1;
+  if (cs.mode == 0 && cs.dcls) {
+    const uint32_t seg = blockIdx.x / cs.cells_per_seg;
+    const DigitCls d = cs.dcls[seg];
+    if (d.mult != 0 && d.mult < (~0ULL) / kSubK) {
+      attempt = 0;
+      lo = d.lo;
+      mult = d.mult * kSubK;
+      sub0 = (blockIdx.x - seg * cs.cells_per_seg) * kSubK;
+      sub_max = d.nb * kSubK - 1;  // the partition clamps digits to nb - 1
+    }
+  }
   uint64_t kr[kSortItems];
-  uint64_t mn = ~0ULL, mx = 0;
 #pragma unroll
   for (int it = 0; it < kSortItems; ++it) {
     const uint32_t i = it * kSortThreads + tid;
     kr[it] = i < n ? ldg_stream(src + off + i) : ~0ULL;
-    mn = min(mn, kr[it]);
-    if (i < n) mx = max(mx, kr[it]);
   }
-  block_minmax(mn, mx, s_mm);
-  if (mn == mx) {
-    const uint64_t ko = from_ordered<KIND_OUT>(mn);
-    for (uint32_t i = tid; i < n; i += kSortThreads) {
-      out[off + i] = ko;
-      if constexpr (VALS) out_vals[off + i] = src_vals[off + i];
-    }
-    return;
-  }
-  const uint64_t range = mx - mn;
-  const bool exact = range < 2 * (uint64_t)n;  // one key value per sub-bucket
-  // Sub-bucket = (k - mn) * 2n >> bitlen(range): in [0, 2n), monotone.
-  const int lr = bit_length64(range);
-  const uint64_t mult = exact ? 0 : ((uint64_t)(2 * n) << (64 - lr));
-  const uint32_t nsub = exact ? (uint32_t)range + 1 : 2 * n;
-  const uint32_t nwords = (nsub + 1) >> 1;
-  auto sub_of = [&](uint64_t k) -> uint32_t {
-    const uint64_t x = k - mn;
-    return exact ? (uint32_t)x : (uint32_t)__umul64hi(x, mult);
-  };
-  for (uint32_t j = tid; j < nwords; j += kSortThreads) cw[j] = 0;
-  __syncthreads();
-  uint32_t sb[kSortItems];
+  uint4* const cw4 = reinterpret_cast<uint4*>(cw) + tid * (kScanWords / 4);
+  const uint32_t rot = (tid >> 1) & 3u;  // chunk c of this thread is stored at c ^ rot
+  uint32_t pk[kSortItems];
+  uint32_t all, qpos;
+  uint64_t hi_key = 0;
+  bool exact = false;
+  for (;; ++attempt) {
 #pragma unroll
-  for (int it = 0; it < kSortItems; ++it) {
-    sb[it] = sub_of(kr[it]);
-    if (it * kSortThreads + tid < n) atomicAdd(&cw[sb[it] >> 1], 1u << ((sb[it] & 1) * 16));
-  }
-  __syncthreads();
-  uint32_t big = 0;
-  for (uint32_t j = tid; j < nwords; j += kSortThreads) {
-    const uint32_t v = cw[j];
-    big = max(big, max(v & 0xFFFFu, v >> 16));
-  }
+    for (int c = 0; c < kScanWords / 4; ++c) cw4[c ^ rot] = make_uint4(0, 0, 0, 0);
+    if (attempt == 1) {
+      uint64_t mn = ~0ULL, mx = 0;
 #pragma unroll
-  for (int o = 16; o; o >>= 1) big = max(big, __shfl_xor_sync(0xffffffffu, big, o));
-  if ((tid & 31) == 0) s_max[tid >> 5] = big;
-  block_excl_scan_u16<kSortThreads>(cw, (int)nwords, s_scan);
-  big = 0;
-#pragma unroll
-  for (int w = 0; w < kSortWarps; ++w) big = max(big, s_max[w]);
-  const bool need_order = VALS || !exact;
-  if (need_order && big > (uint32_t)kRankMax) {
-    if (tid == 0) {
-      const unsigned int slot = atomicAdd(fb_count, 1u);
-      OverflowRec r; r.off = off; r.count = count; r.lo = mn; r.hi = mx;
-      fb[slot] = r;
-    }
-    return;
-  }
-#pragma unroll
-  for (int it = 0; it < kSortItems; ++it) {
-    if (it * kSortThreads + tid < n) {
-      const uint32_t sh = (sb[it] & 1) * 16;
-      const uint32_t slot = (atomicAdd(&cw[sb[it] >> 1], 1u << sh) >> sh) & 0xFFFFu;
-      kB[slot] = kr[it];
-      if constexpr (VALS) iB[slot] = (uint16_t)(it * kSortThreads + tid);
-    }
-  }
-  __syncthreads();
-  // c16[j] is now the end of sub-bucket j (= start of j + 1).  Thread per
-  // slot: the key's final position is its slot (singleton), one compare with
-  // its partner (pair) or a rank count (larger, rare); ties by input index
-  // with values (stable), by slot without.  Writes land inside the key's
-  // sub-bucket range, so a warp's stores stay coalesced.
-  for (uint32_t j = tid; j < n; j += kSortThreads) {
-    const uint64_t k = kB[j];
-    uint32_t fin = j;
-    uint16_t ix = 0;
-    if constexpr (VALS) ix = iB[j];
-    if (need_order) {
-      const uint32_t s = sub_of(k);
-      const uint32_t b0 = s ? c16[s - 1] : 0, b1 = c16[s];
-      if (b1 - b0 == 2) {
-        const uint32_t pt = b0 + b1 - 1 - j;
-        const uint64_t pkey = kB[pt];
-        bool before = k < pkey;
-        if constexpr (VALS) before = before || (k == pkey && ix < iB[pt]);
-        else before = before || (k == pkey && j < pt);
-        fin = before ? b0 : b0 + 1;
-      } else if (b1 - b0 > 2) {
-        fin = b0;
-        for (uint32_t q = b0; q < b1; ++q) {
-          const uint64_t kq = kB[q];
-          if constexpr (VALS) fin += kq < k || (kq == k && iB[q] < ix);
-          else fin += kq < k || (kq == k && q < j);
+      for (int it = 0; it < kSortItems; ++it) {
+        mn = min(mn, kr[it]);
+        if (it * kSortThreads + tid < n) mx = max(mx, kr[it]);
+      }
+      block_minmax(mn, mx, s_mm);  // its barriers also publish the zeroed counters
+      if (mn == mx) {
+        const uint64_t ko = from_ordered<KIND_OUT>(mn);
+        for (uint32_t i = tid; i < n; i += kSortThreads) {
+          out[off + i] = ko;
+          if constexpr (VALS) out_vals[off + i] = src_vals[off + i];
         }
+        return;
+      }
+      const uint64_t range = mx - mn;
+      exact = range < 2 * (uint64_t)n;  // one key value per sub-bucket
+      // Sub-bucket = (k - mn) * 2n >> bitlen(range): in [0, 2n), monotone.
+      lo = mn;
+      hi_key = mx;
+      mult = exact ? 0 : ((uint64_t)(2 * n) << (64 - bit_length64(range)));
+      sub0 = 0;
+      sub_max = kSubK - 1;
+    } else {
+      __syncthreads();
+    }
+    // 1. count; the atomic's old value is the rank inside the sub-bucket.
+    uint32_t nq = 0;  // sub-buckets this thread will queue (its keys of rank 1)
+#pragma unroll
+    for (int it = 0; it < kSortItems; ++it) {
+      pk[it] = 0xFFFFFFFFu;
+      if (it * kSortThreads + tid < n) {
+        const uint64_t x = kr[it] - lo;
+        const uint32_t s = exact ? (uint32_t)x : min((uint32_t)__umul64hi(x, mult), sub_max) - sub0;
+        const uint32_t sh = (s & 1) * 16;
+        const uint32_t rk = (atomicAdd(&cw[sw_word(s >> 1)], 1u << sh) >> sh) & 0xFFFFu;
+        pk[it] = (s << 16) | rk;
+        nq += rk == 1;
       }
     }
-    out[off + fin] = from_ordered<KIND_OUT>(k);
-    if constexpr (VALS) out_vals[off + fin] = src_vals[off + ix];
+    __syncthreads();
+    // 2. scan.  Packed (keys | queue entries << 16): both prefixes stay < 2^16;
+    // the per-word sums of the two u16 halves cannot carry (total <= n).
+    uint32_t tw = 0, big = 0;
+#pragma unroll
+    for (int c = 0; c < kScanWords / 4; ++c) {
+      const uint4 v = cw4[c ^ rot];
+      tw += v.x + v.y + v.z + v.w;
+      big = max(max(big, max(v.x, v.y)), max(v.z, v.w));
+      big = max(max(big, max(v.x << 16, v.y << 16)), max(v.z << 16, v.w << 16));
+    }
+    big >>= 16;  // max over the high halves and the (shifted) low halves
+    const uint32_t tot = (tw & 0xFFFFu) + (tw >> 16);
+    const uint32_t mine = tot | (nq << 16);
+    const uint32_t inc = warp_incl_scan(mine);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) big = max(big, __shfl_xor_sync(0xffffffffu, big, o));
+    if (lane == 31) s_scan[wid] = inc;
+    if (lane == 0) s_max[wid] = big;
+    all = scan_warp_totals<kSortThreads>(s_scan);
+    const uint32_t pre = s_scan[wid] + inc - mine;
+    big = 0;
+#pragma unroll
+    for (int w = 0; w < kSortWarps; ++w) big = max(big, s_max[w]);
+    if (big > (uint32_t)kRankMax && (VALS || !exact)) {
+      if (attempt == 0) continue;  // keys cluster inside the digit cell: use its min/max
+      if (tid == 0) {
+        const unsigned int slot = atomicAdd(fb_count, 1u);
+        OverflowRec r; r.off = off; r.count = count; r.lo = lo; r.hi = hi_key;
+        fb[slot] = r;
+      }
+      return;
+    }
+    // Exclusive starts, two per word: (run, run + lo) + run * 0x10001.
+    uint32_t run = (pre & 0xFFFFu) * 0x10001u;
+#pragma unroll
+    for (int c = 0; c < kScanWords / 4; ++c) {
+      uint4 v = cw4[c ^ rot];
+      uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t st = run + (w[q] << 16);
+        run += ((w[q] * 0x10001u) >> 16) * 0x10001u;
+        w[q] = st;
+      }
+      cw4[c ^ rot] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+    qpos = pre >> 16;
+    break;
+  }
+  __syncthreads();
+  // 3. place: slot = start(sub-bucket) + rank.
+#pragma unroll
+  for (int it = 0; it < kSortItems; ++it) {
+    if (pk[it] != 0xFFFFFFFFu) {
+      const uint32_t s = pk[it] >> 16, rk = pk[it] & 0xFFFFu;
+      const uint32_t slot = c16[sw16(s)] + rk;
+      kB[slot] = kr[it];
+      if constexpr (VALS) iB[slot] = (uint16_t)(it * kSortThreads + tid);
+      if (rk == 1) qB[qpos++] = (uint16_t)s;
+    }
+  }
+  if (tid == 0) s_q2 = 0;
+  __syncthreads();
+  // 4. order the multi-key sub-buckets in place.  c16[s] = start of
+  // sub-bucket s; past the last counter the starts are n.
+  if (VALS || !exact) {
+    const uint32_t nqueue = all >> 16;
+    uint16_t* q2 = qB + nqueue;  // larger sub-buckets, re-queued behind
+    for (uint32_t q = tid; q < nqueue; q += kSortThreads) {
+      const uint32_t s = qB[q];
+      const uint32_t b0 = c16[sw16(s)];
+      const uint32_t b1 = s + 1 < (uint32_t)kSubK ? c16[sw16(s + 1)] : n;
+      if (b1 - b0 > 3) {
+        q2[atomicAdd(&s_q2, 1u)] = (uint16_t)s;
+        continue;
+      }
+      const bool three = b1 - b0 == 3;
+      uint64_t k0 = kB[b0], k1 = kB[b0 + 1], k2 = three ? kB[b0 + 2] : ~0ULL;
+      uint16_t i0 = 0, i1 = 0, i2 = 0xFFFFu;
+      if constexpr (VALS) {
+        i0 = iB[b0]; i1 = iB[b0 + 1];
+        if (three) i2 = iB[b0 + 2];
+      }
+      cmp_swap<VALS>(k0, i0, k1, i1);
+      cmp_swap<VALS>(k1, i1, k2, i2);
+      cmp_swap<VALS>(k0, i0, k1, i1);
+      kB[b0] = k0; kB[b0 + 1] = k1;
+      if (three) kB[b0 + 2] = k2;
+      if constexpr (VALS) {
+        iB[b0] = i0; iB[b0 + 1] = i1;
+        if (three) iB[b0 + 2] = i2;
+      }
+    }
+    __syncthreads();
+    const uint32_t n2 = s_q2;
+    for (uint32_t q = tid; q < n2; q += kSortThreads) {
+      const uint32_t s = q2[q];
+      insertion_sort<VALS>(kB, iB, c16[sw16(s)], s + 1 < (uint32_t)kSubK ? c16[sw16(s + 1)] : n);
+    }
+    __syncthreads();
+  }
+  // 5. write-out, 16-byte stores when the output allows.
+  const uint32_t a = (uint32_t)(off & 1);
+  if (((reinterpret_cast<uintptr_t>(out) & 15) == 0) && n > 2) {
+    if (a && tid == 0) out[off] = from_ordered<KIND_OUT>(kB[0]);
+    const uint32_t np = (n - a) >> 1;
+    uint4* o4 = reinterpret_cast<uint4*>(out + off + a);
+    for (uint32_t j = tid; j < np; j += kSortThreads) {
+      const uint64_t k0 = from_ordered<KIND_OUT>(kB[a + 2 * j]);
+      const uint64_t k1 = from_ordered<KIND_OUT>(kB[a + 2 * j + 1]);
+      o4[j] = make_uint4((uint32_t)k0, (uint32_t)(k0 >> 32), (uint32_t)k1, (uint32_t)(k1 >> 32));
+    }
+    if (((n - a) & 1) && tid == 0) out[off + n - 1] = from_ordered<KIND_OUT>(kB[n - 1]);
+  } else {
+    for (uint32_t j = tid; j < n; j += kSortThreads) out[off + j] = from_ordered<KIND_OUT>(kB[j]);
+  }
+  if constexpr (VALS) {
+    for (uint32_t j = tid; j < n; j += kSortThreads) out_vals[off + j] = src_vals[off + iB[j]];
   }
 }
 
@@ -1060,7 +1209,9 @@ cudaError_t launch_final_ranges(cudaStream_t st, const uint64_t* bounds, int nse
 }
 
 // keys, 2x u16 sub-bucket counters (+ value index): two CTAs per SM.
-size_t smem_sort_bytes(bool vals) { return (size_t)kSortCap * (vals ? 14 : 12); }
+size_t smem_sort_bytes(bool vals) {
+  return (size_t)kSortCap * 12 + 2 * (size_t)kQueueCap + (vals ? 2 * (size_t)kSortCap : 0);
+}
 
 size_t smem_sort_lsd_bytes() {
   return (size_t)kSortCap * (8 + 8 + 2 + 2) + (size_t)4 * kSortWarps * kRadix + 4 * kRadix;

@@ -31,7 +31,7 @@ struct GroupMeta {
 // mode 2 = records (fallback list on the device).
 struct CellSource {
   int mode;
-  int nbits;
+  uint32_t cells_per_seg;  // mode 0: cells of one segment (cell id = seg * cells_per_seg + digit)
   const uint64_t* cell_base;
   const uint32_t* cell_cnt;
   const DigitCls* dcls;
