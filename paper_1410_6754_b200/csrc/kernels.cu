@@ -727,6 +727,10 @@ __global__ void __launch_bounds__(kSortThreads, 1)
 // keys alone skip step 4.  Cells whose keys cluster (a sub-bucket above
 // kRankMax that still needs ordering) go to the LSD fallback list.
 constexpr int kRankMax = 64;
+#ifndef AMS_SORT_CTAS
+#define AMS_SORT_CTAS 3
+#endif
+constexpr int kSortCtas = AMS_SORT_CTAS;  // resident CTAs per SM (register budget)
 constexpr int kSubK = 2 * kSortCap;                   // sub-buckets of the refined digit
 constexpr int kScanWords = kSubK / 2 / kSortThreads;  // counter words per thread (2 sub-buckets each)
 static_assert(kScanWords % 4 == 0, "scan loads 4 words at a time");
@@ -775,7 +779,7 @@ __device__ __forceinline__ void insertion_sort(uint64_t* kB, uint16_t* iB, uint3
 }
 
 template <int KIND_OUT, bool VALS>
-__global__ void __launch_bounds__(kSortThreads, 4)
+__global__ void __launch_bounds__(kSortThreads, kSortCtas)
     k_smem_sort(const uint64_t* __restrict__ src, const uint64_t* __restrict__ src_vals,
                 uint64_t* __restrict__ out, uint64_t* __restrict__ out_vals, CellSource cs,
                 OverflowRec* __restrict__ ovf, unsigned int* __restrict__ ovf_count,
