@@ -1,6 +1,7 @@
 // Internal host-side declarations shared by the C-ABI translation units.
 #pragma once
 #include <cstdint>
+#include <functional>
 #include <string>
 
 #include "../../include/ams_b200.h"
@@ -25,5 +26,8 @@ struct Mt19937 {
 };
 
 void python_sample_sorted(Mt19937& rng, uint64_t n, uint64_t k, uint64_t* out);
+
+// Runs f(0..count-1) on a persistent host worker pool (and the caller).
+void parallel_for(int count, const std::function<void(int)>& f);
 
 }  // namespace ams

@@ -18,7 +18,6 @@
 #include <cstdint>
 #include <cstring>
 #include <string>
-#include <unordered_set>
 #include <vector>
 #include <algorithm>
 
@@ -119,8 +118,18 @@ void Mt19937::init_genrand(uint32_t s) {
   index = kN;
 }
 
+// init_by_array always starts from init_genrand(19650218): computed once.
+static const Mt19937& genrand_19650218() {
+  static const Mt19937 base = [] {
+    Mt19937 m;
+    m.init_genrand(19650218U);
+    return m;
+  }();
+  return base;
+}
+
 void Mt19937::init_by_array(const uint32_t* key, int key_length) {
-  init_genrand(19650218U);
+  std::memcpy(mt, genrand_19650218().mt, sizeof mt);
   int i = 1, j = 0;
   for (int k = (kN > key_length ? kN : key_length); k; --k) {
     mt[i] = (mt[i] ^ ((mt[i - 1] ^ (mt[i - 1] >> 30)) * 1664525U)) + key[j] + (uint32_t)j;
@@ -137,24 +146,20 @@ void Mt19937::init_by_array(const uint32_t* key, int key_length) {
   index = kN;
 }
 
+// The twist is done one word at a time, as the words are consumed: word kk
+// of the new state depends on old words kk and kk + 1 and on word
+// kk + kM mod kN, which is old below kN - kM and already new above — the
+// same values the whole-array twist uses, in the same order.  Draws that
+// use few words (most sample streams) skip the rest of the twist.
 uint32_t Mt19937::next() {
   static const uint32_t mag01[2] = {0x0U, 0x9908b0dfU};
-  uint32_t y;
-  if (index >= kN) {
-    int kk;
-    for (kk = 0; kk < kN - kM; ++kk) {
-      y = (mt[kk] & 0x80000000U) | (mt[kk + 1] & 0x7fffffffU);
-      mt[kk] = mt[kk + kM] ^ (y >> 1) ^ mag01[y & 1U];
-    }
-    for (; kk < kN - 1; ++kk) {
-      y = (mt[kk] & 0x80000000U) | (mt[kk + 1] & 0x7fffffffU);
-      mt[kk] = mt[kk + (kM - kN)] ^ (y >> 1) ^ mag01[y & 1U];
-    }
-    y = (mt[kN - 1] & 0x80000000U) | (mt[0] & 0x7fffffffU);
-    mt[kN - 1] = mt[kM - 1] ^ (y >> 1) ^ mag01[y & 1U];
-    index = 0;
-  }
-  y = mt[index++];
+  if (index >= kN) index = 0;
+  const int kk = index++;
+  const int k1 = kk + 1 < kN ? kk + 1 : 0;
+  const int km = kk + kM < kN ? kk + kM : kk + kM - kN;
+  uint32_t y = (mt[kk] & 0x80000000U) | (mt[k1] & 0x7fffffffU);
+  y = mt[km] ^ (y >> 1) ^ mag01[y & 1U];
+  mt[kk] = y;
   y ^= (y >> 11);
   y ^= (y << 7) & 0x9d2c5680U;
   y ^= (y << 15) & 0xefc60000U;
@@ -198,12 +203,24 @@ void python_sample_sorted(Mt19937& rng, uint64_t n, uint64_t k, uint64_t* out) {
       pool[j] = pool[n - i - 1];
     }
   } else {
-    std::unordered_set<uint64_t> selected;
-    selected.reserve(k * 2);
+    // CPython keeps a set of the picks and redraws duplicates; an
+    // open-addressing table (reused per thread) gives the same picks.
+    thread_local std::vector<uint64_t> table;
+    uint64_t cap = 16;
+    while (cap < 4 * k) cap <<= 1;
+    table.assign(cap, ~0ULL);
+    const uint64_t mask = cap - 1;
+    auto insert = [&](uint64_t v) -> bool {  // false if already present
+      uint64_t h = (v * 0x9E3779B97F4A7C15ULL) >> 20;
+      for (;; ++h) {
+        uint64_t& e = table[h & mask];
+        if (e == v) return false;
+        if (e == ~0ULL) { e = v; return true; }
+      }
+    };
     for (uint64_t i = 0; i < k; ++i) {
       uint64_t j = rng.randbelow(n);
-      while (selected.count(j)) j = rng.randbelow(n);
-      selected.insert(j);
+      while (!insert(j)) j = rng.randbelow(n);
       out[i] = j;
     }
   }
@@ -264,8 +281,14 @@ int ams_draw_sample_positions(int64_t master_seed, const char* stream, int level
                               const uint64_t* offs, uint64_t capacity, uint64_t* out_idx,
                               uint64_t* out_gpos, uint64_t* out_group_count) {
   if (!stream) return set_error(AMS_EINVAL, "null stream");
+  // Serial pass: every PE's quota, output slot and group position.
+  struct Job {
+    int pe;
+    int group_lo;
+    uint64_t take, out, gpos;
+  };
+  std::vector<Job> jobs;
   uint64_t w = 0;
-  std::vector<uint64_t> tmp;
   for (int g = 0; g < ngroups; ++g) {
     const int first = group_first[g], P = group_npe[g];
     uint64_t n_g = 0;
@@ -281,25 +304,31 @@ int ams_draw_sample_positions(int64_t master_seed, const char* stream, int level
       const uint64_t quota = base + ((uint64_t)i < extra ? 1 : 0);
       const uint64_t take = std::min<uint64_t>(quota, sizes[pe]);
       if (w + take > capacity) return set_error(AMS_EINVAL, "sample capacity exceeded");
-      std::string sid = std::string(stream) + "/L" + std::to_string(level) + "-g" +
-                        std::to_string(first) + "/sample/pe" + std::to_string(pe);
-      std::string text = std::to_string(master_seed) + "\x1f" + sid + "\x1f";
-      uint32_t words[4];
-      int nw = stream_seed_words(text, words);
-      Mt19937 rng;
-      rng.init_by_array(words, nw);
-      tmp.resize(take);
-      python_sample_sorted(rng, sizes[pe], take, tmp.data());
-      for (uint64_t t = 0; t < take; ++t) {
-        out_idx[w] = offs[pe] + tmp[t];
-        out_gpos[w] = gpos + tmp[t];
-        ++w;
-      }
+      if (take) jobs.push_back({pe, first, take, w, gpos});
+      w += take;
       drawn += take;
       gpos += sizes[pe];
     }
     out_group_count[g] = drawn;
   }
+  // The streams are independent: draw them in parallel.
+  const std::string prefix = std::to_string(master_seed) + "\x1f" + stream + "/L" +
+                             std::to_string(level) + "-g";
+  parallel_for((int)jobs.size(), [&](int i) {
+    const Job& j = jobs[i];
+    const std::string text = prefix + std::to_string(j.group_lo) + "/sample/pe" +
+                             std::to_string(j.pe) + "\x1f";
+    uint32_t words[4];
+    const int nw = stream_seed_words(text, words);
+    Mt19937 rng;
+    rng.init_by_array(words, nw);
+    uint64_t* idx = out_idx + j.out;
+    python_sample_sorted(rng, sizes[j.pe], j.take, idx);
+    for (uint64_t t = 0; t < j.take; ++t) {
+      out_gpos[j.out + t] = j.gpos + idx[t];
+      idx[t] += offs[j.pe];
+    }
+  });
   return AMS_OK;
 }
 

@@ -532,6 +532,180 @@ __global__ void __launch_bounds__(kThreads, VALS ? 2 : 4)
   }
 }
 
+// ---- 1-D bulk copies (TMA engine) with an mbarrier -------------------------
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+// Arm `bar` for `bytes` and copy them global -> shared (16-byte aligned, size % 16 == 0).
+__device__ __forceinline__ void bulk_load(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(sdst);
+  const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(b), "r"(bytes)
+               : "memory");
+  if (bytes)
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
+            "r"(d), "l"(gsrc), "r"(bytes), "r"(b)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n}\n" ::"r"(b),
+      "r"(parity)
+      : "memory");
+}
+
+// Unstable scatter (keys only): the last level without values and the final
+// digit partition, where any order inside a (tile, bucket) run gives the same
+// result (F7).  Same chunk geometry and offsets as k_scatter.  Per tile:
+// the 16-byte-aligned body arrives by one bulk copy into one of two shared
+// buffers (the next tile's copy overlaps this tile's work); every key is
+// classified and takes a rank from one shared atomic; a register-blocked
+// scan turns the counts into tile starts and per-bucket output bases; the
+// tile is permuted bucket-major in place and written as coalesced runs.
+constexpr int kThreadsU = 512;                 // 16 warps x 8 keys per tile: 2 CTAs per SM
+constexpr int kItemsU = kTile / kThreadsU;
+constexpr int kWarpsU = kThreadsU / 32;
+
+template <int KIND, bool DIGIT>
+__global__ void __launch_bounds__(kThreadsU, 2)
+    k_scatter_u(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst, SegMeta m,
+                const uint8_t* __restrict__ blobs, const DigitCls* __restrict__ dcls, int nspl_cap,
+                int nb, const uint32_t* __restrict__ chunk_tot,
+                const uint64_t* __restrict__ cell_base) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ int s_seg;
+  __shared__ uint32_t s_scan[kWarpsU + 1];
+  __shared__ __align__(8) uint64_t s_bar[2];
+  constexpr int kBuf = kTile + 2;  // room for the odd head key
+  uint64_t* buf0 = reinterpret_cast<uint64_t*>(smem);
+  const int per = (nb + kThreadsU - 1) / kThreadsU | 1;  // buckets per scan thread (odd: no conflicts)
+  const int nbp = per * kThreadsU;
+  int64_t* run = reinterpret_cast<int64_t*>(buf0 + 2 * kBuf);  // running output offset
+  int64_t* adj = run + nbp;                                     // this tile: dst index - slot
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(adj + nbp);       // counts, then tile starts
+  uint16_t* bkt = reinterpret_cast<uint16_t*>(cnt + nbp);
+  uint8_t* clsmem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(bkt + kTile) + 15) & ~static_cast<uintptr_t>(15));
+
+  const uint64_t c = blockIdx.x;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    s_seg = upper_bound_u64(m.chunk_prefix, m.nseg + 1, c) - 1;
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int s = s_seg;
+  const uint64_t seg_off = m.off[s];
+  const uint64_t first = (c - m.chunk_prefix[s]) * (uint64_t)kChunk;
+  const uint64_t last = min(first + (uint64_t)kChunk, m.len[s]);
+  const int ntiles = (int)((last - first + kTile - 1) / kTile);
+  auto issue = [&](int t) {  // thread 0: bulk-load tile t's aligned body
+    const uint64_t base = seg_off + first + (uint64_t)t * kTile;
+    const uint32_t tc = (uint32_t)min((uint64_t)kTile, last - first - (uint64_t)t * kTile);
+    const uint32_t h = (uint32_t)(base & 1);
+    const uint64_t b0 = base + h, b1 = (base + tc) & ~1ULL;
+    const uint32_t bytes = b1 > b0 ? (uint32_t)(b1 - b0) * 8 : 0;
+    bulk_load(buf0 + (t & 1) * kBuf + 2 * h, src + b0, bytes, &s_bar[t & 1]);
+  };
+  if (tid == 0) issue(0);
+  {
+    const uint32_t* ct = chunk_tot + c * nb;
+    const uint64_t* cb = cell_base + (uint64_t)s * nb;
+    for (int b = tid; b < nb; b += kThreadsU) run[b] = (int64_t)(cb[b] + ct[b]);
+    for (int b = tid; b < nbp; b += kThreadsU) cnt[b] = 0;
+  }
+  TreeView tv;
+  DigitView dv;
+  int64_t posbase = 0;
+  const int cls = m.cls[s];
+  if constexpr (DIGIT) dv.c = dcls[cls];
+  else {
+    tv = load_tree(blobs + (size_t)cls * kBlobStride, clsmem, nspl_cap);
+    posbase = m.posbase[cls];
+  }
+  const int w = tid >> 5, lane = tid & 31;
+  __syncthreads();
+  for (int t = 0; t < ntiles; ++t) {
+    uint64_t* buf = buf0 + (t & 1) * kBuf;
+    const uint64_t base = seg_off + first + (uint64_t)t * kTile;
+    const uint32_t tc = (uint32_t)min((uint64_t)kTile, last - first - (uint64_t)t * kTile);
+    const uint32_t h = (uint32_t)(base & 1);
+    const uint32_t e_end = (uint32_t)(((base + tc) & ~1ULL) - base);  // body = [h, e_end)
+    if (tid == 0 && t + 1 < ntiles) {
+      fence_proxy_async();
+      issue(t + 1);
+    }
+    mbar_wait(&s_bar[t & 1], (uint32_t)(t >> 1) & 1u);
+    // Classify + rank.  Element e of the tile is at buf[e + 2h - h] = buf[e + h].
+    uint64_t kr[kItemsU];
+    uint32_t pk[kItemsU];
+    const uint32_t pos0 = (uint32_t)((int64_t)base + posbase);
+#pragma unroll
+    for (int i = 0; i < kItemsU; ++i) {
+      const uint32_t e = w * (kItemsU * 32) + i * 32 + lane;
+      pk[i] = kInvalid;
+      if (e < tc) {
+        const uint64_t raw = (e >= h && e < e_end) ? buf[e + h] : src[base + e];
+        const uint64_t key = to_ordered<KIND>(raw);
+        uint32_t b;
+        if constexpr (DIGIT) b = dv.classify(key, 0);
+        else b = tv.classify(key, pos0 + e);
+        kr[i] = key;
+        pk[i] = (b << 16) | atomicAdd(&cnt[b], 1u);
+      }
+    }
+    __syncthreads();
+    // Scan: thread t owns buckets [t*per, t*per + per).
+    {
+      const int b0 = tid * per;
+      uint32_t sum = 0;
+      for (int j = 0; j < per; ++j) sum += cnt[b0 + j];
+      const uint32_t inc = warp_incl_scan(sum);
+      if (lane == 31) s_scan[w] = inc;
+      scan_warp_totals<kThreadsU>(s_scan);
+      uint32_t start = s_scan[w] + inc - sum;
+      for (int j = 0; j < per; ++j) {
+        const int b = b0 + j;
+        const uint32_t v = cnt[b];
+        cnt[b] = start;
+        if (b < nb) {
+          const int64_t r = run[b];
+          adj[b] = r - (int64_t)start;
+          run[b] = r + v;
+        }
+        start += v;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < kItemsU; ++i) {
+      if (pk[i] != kInvalid) {
+        const uint32_t b = pk[i] >> 16;
+        const uint32_t slot = cnt[b] + (pk[i] & 0xFFFFu);
+        buf[slot] = kr[i];
+        bkt[slot] = (uint16_t)b;
+      }
+    }
+    __syncthreads();
+    for (uint32_t j = tid; j < tc; j += kThreadsU) dst[adj[bkt[j]] + j] = buf[j];
+    for (int j = 0; j < per; ++j) cnt[tid * per + j] = 0;
+    __syncthreads();
+  }
+}
+
 // -------------------------------------------------------------------- K7
 __global__ void k_gather_bounds(const uint64_t* __restrict__ bounds, const int32_t* __restrict__ sel,
                                 int n, uint64_t* __restrict__ out) {
@@ -1163,6 +1337,38 @@ size_t scatter_smem_bytes(int nb_stride, int nspl_cap, int cells_cap, bool digit
   return b;
 }
 
+size_t scatter_u_smem_bytes(int nb, int nspl_cap, int cells_cap, bool digit) {
+  const int per = (nb + kThreadsU - 1) / kThreadsU | 1;
+  const size_t nbp = (size_t)per * kThreadsU;
+  size_t b = 2 * 8 * (size_t)(kTile + 2) + 16 * nbp + 4 * nbp + 2 * (size_t)kTile;
+  b = (b + 15) & ~(size_t)15;
+  if (!digit) b += tree_smem_bytes(nspl_cap, cells_cap) + 16;
+  return b;
+}
+
+cudaError_t launch_scatter_u(cudaStream_t st, const void* src, int kind, bool digit, void* dst,
+                             const SegMeta& m, uint64_t nchunks, const uint8_t* blobs,
+                             const DigitCls* dcls, int nspl_cap, int cells_cap, int nb_stride,
+                             const uint32_t* chunk_tot, const uint64_t* cell_base) {
+  if (nchunks == 0) return cudaSuccess;
+  const size_t smem = scatter_u_smem_bytes(nb_stride, nspl_cap, cells_cap, digit);
+  const uint64_t* s = static_cast<const uint64_t*>(src);
+  uint64_t* d = static_cast<uint64_t*>(dst);
+  cudaError_t e = cudaSuccess;
+#define AMS_SCATTER_U_GO(K, DG)                                                               \
+  {                                                                                           \
+    auto fn = k_scatter_u<K, DG>;                                                             \
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
+    if (e != cudaSuccess) return e;                                                           \
+    fn<<<(unsigned)nchunks, kThreadsU, smem, st>>>(s, d, m, blobs, dcls, nspl_cap, nb_stride,  \
+                                                   chunk_tot, cell_base);                     \
+  }
+  if (digit) AMS_SCATTER_U_GO(AMS_KEY_U64, true)
+  else AMS_KIND_DISPATCH(kind, K, AMS_SCATTER_U_GO(K, false))
+#undef AMS_SCATTER_U_GO
+  return cudaGetLastError();
+}
+
 cudaError_t launch_scatter(cudaStream_t st, const void* src, const void* src_vals, int kind,
                            bool digit, bool stable, void* dst, void* dst_vals, const SegMeta& m,
                            uint64_t nchunks, const uint8_t* blobs, const DigitCls* dcls,
@@ -1170,6 +1376,13 @@ cudaError_t launch_scatter(cudaStream_t st, const void* src, const void* src_val
                            const uint64_t* cell_base) {
   if (nchunks == 0) return cudaSuccess;
   const bool vals = src_vals != nullptr;
+#ifndef AMS_NO_SCATTER_U
+  // The lean unstable kernel pays off with the cheap digit classifier (the
+  // final partition); the tree classifier keeps the 4-CTA kernel below.
+  if (!stable && !vals && digit)
+    return launch_scatter_u(st, src, kind, digit, dst, m, nchunks, blobs, dcls, nspl_cap,
+                            cells_cap, nb_stride, chunk_tot, cell_base);
+#endif
   const int mode = scatter_mode(nb_stride, stable);
   const size_t smem = scatter_smem_bytes(nb_stride, nspl_cap, cells_cap, digit, vals, stable);
   const uint64_t* s = static_cast<const uint64_t*>(src);

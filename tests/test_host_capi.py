@@ -55,6 +55,17 @@ def test_getrandbits_matches_cpython(x, k):
     assert [int(v) for v in got] == want
 
 
+@pytest.mark.parametrize("k", [32, 64])
+def test_getrandbits_across_state_twists(k):
+    # 64-bit draws use two words: 5000 draws run through 16 twists of the
+    # 624-word state, which the library regenerates one word at a time.
+    x = O.stream_seed_int(3, "algo/rep0/L1-g8/sample/pe9")
+    rng = random.Random(x)
+    want = [rng.getrandbits(k) for _ in range(5000)]
+    got = L.getrandbits(_words(x), k, 5000)
+    assert [int(v) for v in got] == want
+
+
 @pytest.mark.parametrize("n,k", [(32, 32), (65536, 256), (1 << 22, 231), (100, 40), (1 << 27, 9),
                                  (10, 0), (1, 1), (5, 5), (6, 6), (21, 5), (22, 6), (5000, 1727),
                                  (16405, 1727), (16406, 1727), (3, 2), (1 << 31, 100)])
