@@ -148,6 +148,8 @@ struct ams_ctx {
   SegMeta meta{};
   DevBuf chunk_tot, seg_hist, cell_base, pieces, minmax;
   bool level_stable = true;
+  DevBuf ids;  // per-key bucket bytes of the current level (nb <= 256)
+  bool level_ids = false;
   // key bounds [lo, hi] of the current level's groups (ping-pong)
   DevBuf bounds[2];
   int bcur = 0;
@@ -251,7 +253,7 @@ cudaError_t upload_segments(Stage& st, cudaStream_t stream, const uint64_t* off,
 // scan, for a segment table whose classifiers are ready.
 int run_histogram(ams_ctx* c, const void* src, int kind, bool digit, const SegMeta& m,
                   uint64_t nchunks, int nb_stride, const DigitCls* dcls,
-                  unsigned long long* minmax, uint64_t nelems) {
+                  unsigned long long* minmax, uint64_t nelems, uint8_t* ids) {
   AMS_CK(c->chunk_tot.ensure(sizeof(uint32_t) * std::max<uint64_t>(nchunks, 1) * nb_stride));
   AMS_CK(c->seg_hist.ensure(sizeof(uint32_t) * (size_t)std::max(m.nseg, 1) * nb_stride));
   AMS_CK(cudaMemsetAsync(c->seg_hist.p, 0, sizeof(uint32_t) * (size_t)m.nseg * nb_stride, c->stream));
@@ -259,7 +261,7 @@ int run_histogram(ams_ctx* c, const void* src, int kind, bool digit, const SegMe
     KTimer kt(c, digit ? AMS_KCAT_FHIST : AMS_KCAT_HIST, 8.0 * nelems);
     AMS_CK(launch_hist(c->stream, src, kind, digit, m, nchunks, c->blobs.as<uint8_t>(), dcls,
                        c->nspl_cap, c->cells_cap, nb_stride, c->chunk_tot.as<uint32_t>(),
-                       c->seg_hist.as<uint32_t>(), minmax));
+                       c->seg_hist.as<uint32_t>(), minmax, ids));
   }
   {
     KTimer kt(c, AMS_KCAT_CHUNKSCAN, 8.0 * nchunks * nb_stride);
@@ -483,8 +485,20 @@ int ams_level_classify(ams_ctx_t* c, const void* src, int key_kind, int nseg,
   for (int s = 0; s < nseg; ++s) nel += h_seg_len[s];
   c->level_elems = nel;
   c->level_stable = stable != 0;
+  // Buckets below 256: the histogram pass also stores each key's bucket as a
+  // byte at its buffer index, and the scatter reads it instead of classifying.
+  uint8_t* ids = nullptr;
+#ifndef AMS_NO_IDS
+  if (nb_stride <= 256) {
+    uint64_t span = 0;
+    for (int s = 0; s < nseg; ++s) span = std::max(span, h_seg_off[s] + h_seg_len[s]);
+    AMS_CK(c->ids.ensure(std::max<uint64_t>(span, 1)));
+    ids = c->ids.as<uint8_t>();
+  }
+#endif
+  c->level_ids = ids != nullptr;
   int rc = run_histogram(c, src, key_kind, false, c->meta, c->nchunks, nb_stride, nullptr, mm,
-                         nel);
+                         nel, ids);
   if (rc) return rc;
   if (track_minmax) {
     // The whole input is one group at the first level: its bounds are the
@@ -546,7 +560,7 @@ int ams_level_scatter(ams_ctx_t* c, const void* src, const void* src_vals, int k
     AMS_CK(launch_scatter(c->stream, src, src_vals, key_kind, false, c->level_stable, dst,
                           dst_vals, c->meta, c->nchunks, c->blobs.as<uint8_t>(), nullptr,
                           c->nspl_cap, c->cells_cap, c->nb_stride, c->chunk_tot.as<uint32_t>(),
-                          c->cell_base.as<uint64_t>()));
+                          c->cell_base.as<uint64_t>(), c->level_ids ? c->ids.as<uint8_t>() : nullptr));
   }
   // Key bounds of the next level's groups (this rank's children).
   const int nxt = 1 - c->bcur;
@@ -721,7 +735,7 @@ int ams_final_sort(ams_ctx_t* c, void* src, void* src_vals, void* tmp, void* tmp
     uint64_t nel = 0;
     for (uint64_t v : b_len) nel += v;
     int rc = run_histogram(c, cur, AMS_KEY_U64, true, m, nchunks, nbs, c->dcls.as<DigitCls>(),
-                           nullptr, nel);
+                           nullptr, nel, nullptr);
     if (rc) return rc;
     AMS_CK(c->cell_base.ensure(sizeof(uint64_t) * (size_t)nb_seg * nbs));
     {
@@ -733,7 +747,7 @@ int ams_final_sort(ams_ctx_t* c, void* src, void* src_vals, void* tmp, void* tmp
       KTimer kt(c, AMS_KCAT_FSCATTER, (vals ? 32.0 : 16.0) * nel);
       AMS_CK(launch_scatter(c->stream, cur, cur_v, AMS_KEY_U64, true, /*stable=*/vals, oth, oth_v,
                             m, nchunks, c->blobs.as<uint8_t>(), c->dcls.as<DigitCls>(), 0, 0, nbs,
-                            c->chunk_tot.as<uint32_t>(), c->cell_base.as<uint64_t>()));
+                            c->chunk_tot.as<uint32_t>(), c->cell_base.as<uint64_t>(), nullptr));
     }
     c->launches += 5;
     AMS_CK(cudaMemsetAsync(c->ovf_count.p, 0, sizeof(unsigned int), c->stream));

@@ -145,13 +145,16 @@ __global__ void __launch_bounds__(1024) k_build_cls(const uint64_t* __restrict__
 // same-bucket items of one thread costs one atomic — sorted and
 // duplicate-heavy inputs stay cheap), then write the chunk histogram and
 // add it to the segment histogram.
-template <int KIND, bool DIGIT, bool MINMAX>
+// IDS: also store every key's bucket (< 256) as a byte at its buffer index,
+// so the level's scatter does not classify again.
+template <int KIND, bool DIGIT, bool MINMAX, bool IDS>
 __global__ void __launch_bounds__(kThreads) k_hist(const uint64_t* __restrict__ src, SegMeta m,
                                                    const uint8_t* __restrict__ blobs,
                                                    const DigitCls* __restrict__ dcls, int nspl_cap,
                                                    int nb_stride, uint32_t* __restrict__ chunk_tot,
                                                    uint32_t* __restrict__ seg_hist,
-                                                   unsigned long long* __restrict__ minmax) {
+                                                   unsigned long long* __restrict__ minmax,
+                                                   uint8_t* __restrict__ ids) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ int s_seg;
   __shared__ unsigned long long s_min[kWarps], s_max[kWarps];
@@ -197,6 +200,7 @@ __global__ void __launch_bounds__(kThreads) k_hist(const uint64_t* __restrict__ 
         uint32_t b;
         if constexpr (DIGIT) b = dv.classify(keys[i], 0);
         else b = tv.classify(keys[i], (uint32_t)((int64_t)base + posbase) + e);
+        if constexpr (IDS) ids[base + e] = (uint8_t)b;
         if constexpr (MINMAX) { mn = min(mn, (unsigned long long)keys[i]); mx = max(mx, (unsigned long long)keys[i]); }
         if (b != cur) {
           if (cnt) atomicAdd(&hist[cur], cnt);
@@ -338,6 +342,7 @@ __global__ void k_child_bounds(const uint8_t* __restrict__ blobs, GroupMeta gm, 
 
 // -------------------------------------------------------------------- K6
 // Ranking modes of the scatter.
+constexpr int kClsTree = 0, kClsDigit = 1, kClsIds = 2;
 constexpr int kRankWarp = 0;     // stable, one bucket-counter array per warp
 constexpr int kRankSerial = 1;   // stable, one shared array, warps take turns
 constexpr int kRankAtomic = 2;   // unstable (keys only, order inside a run is free)
@@ -387,13 +392,15 @@ __device__ __forceinline__ void cp_async_wait_all() {
 // 4 CTAs per SM) and written as coalesced runs; the running offsets
 // advance.  With a stable mode the order inside a bucket is the input order
 // — the stable (cell, position) order the reference's concatenations produce.
-template <int KIND, bool DIGIT, bool VALS, int MODE>
+// CLS: kClsTree (splitter tree in shared memory), kClsDigit (final digit),
+// kClsIds (bucket bytes stored by the level's histogram pass).
+template <int KIND, int CLS, bool VALS, int MODE>
 __global__ void __launch_bounds__(kThreads, VALS ? 2 : 4)
     k_scatter(const uint64_t* __restrict__ src, const uint64_t* __restrict__ src_vals,
               uint64_t* __restrict__ dst, uint64_t* __restrict__ dst_vals, SegMeta m,
               const uint8_t* __restrict__ blobs, const DigitCls* __restrict__ dcls, int nspl_cap,
               int nb_stride, const uint32_t* __restrict__ chunk_tot,
-              const uint64_t* __restrict__ cell_base) {
+              const uint64_t* __restrict__ cell_base, const uint8_t* __restrict__ ids) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ int s_seg;
   __shared__ uint32_t s_scan[kWarps + 1];
@@ -423,9 +430,9 @@ __global__ void __launch_bounds__(kThreads, VALS ? 2 : 4)
   TreeView tv;
   DigitView dv;
   int64_t posbase = 0;
-  if constexpr (DIGIT) {
+  if constexpr (CLS == kClsDigit) {
     dv.c = dcls[cls];
-  } else {
+  } else if constexpr (CLS == kClsTree) {
     tv = load_tree(blobs + (size_t)cls * kBlobStride, clsmem, nspl_cap);
     posbase = m.posbase[cls];
   }
@@ -452,9 +459,13 @@ __global__ void __launch_bounds__(kThreads, VALS ? 2 : 4)
         const uint32_t e = w * (kItems * 32) + i * 32 + lane;
         uint32_t b = kInvalid;
         if (FULL || e < tcount) {
-          const uint64_t key = to_ordered<KIND>(keys_s[e]);
-          if constexpr (DIGIT) b = dv.classify(key, 0);
-          else b = tv.classify(key, pos0 + e);
+          if constexpr (CLS == kClsIds) {
+            b = ids[base + e];
+          } else {
+            const uint64_t key = to_ordered<KIND>(keys_s[e]);
+            if constexpr (CLS == kClsDigit) b = dv.classify(key, 0);
+            else b = tv.classify(key, pos0 + e);
+          }
         }
         pk[i] = b;
         if constexpr (MODE == kRankAtomic) {
@@ -1263,24 +1274,25 @@ size_t hist_smem_bytes(int nb_stride, int nspl_cap, int cells_cap, bool digit) {
 cudaError_t launch_hist(cudaStream_t st, const void* src, int kind, bool digit, const SegMeta& m,
                         uint64_t nchunks, const uint8_t* blobs, const DigitCls* dcls, int nspl_cap,
                         int cells_cap, int nb_stride, uint32_t* chunk_tot, uint32_t* seg_hist,
-                        unsigned long long* minmax) {
+                        unsigned long long* minmax, uint8_t* ids) {
   if (nchunks == 0) return cudaSuccess;
   const size_t smem = hist_smem_bytes(nb_stride, nspl_cap, cells_cap, digit);
   const uint64_t* s = static_cast<const uint64_t*>(src);
   cudaError_t e = cudaSuccess;
   if (digit) {
-    auto fn = k_hist<AMS_KEY_U64, true, false>;
+    auto fn = k_hist<AMS_KEY_U64, true, false, false>;
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     fn<<<(unsigned)nchunks, kThreads, smem, st>>>(s, m, blobs, dcls, nspl_cap, nb_stride,
-                                                   chunk_tot, seg_hist, minmax);
+                                                   chunk_tot, seg_hist, minmax, nullptr);
   } else {
     AMS_KIND_DISPATCH(kind, K, {
-      auto fn = minmax ? k_hist<K, false, true> : k_hist<K, false, false>;
+      auto fn = minmax ? (ids ? k_hist<K, false, true, true> : k_hist<K, false, true, false>)
+                       : (ids ? k_hist<K, false, false, true> : k_hist<K, false, false, false>);
       e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
       fn<<<(unsigned)nchunks, kThreads, smem, st>>>(s, m, blobs, dcls, nspl_cap, nb_stride,
-                                                     chunk_tot, seg_hist, minmax);
+                                                     chunk_tot, seg_hist, minmax, ids);
     });
   }
   return cudaGetLastError();
@@ -1373,7 +1385,7 @@ cudaError_t launch_scatter(cudaStream_t st, const void* src, const void* src_val
                            bool digit, bool stable, void* dst, void* dst_vals, const SegMeta& m,
                            uint64_t nchunks, const uint8_t* blobs, const DigitCls* dcls,
                            int nspl_cap, int cells_cap, int nb_stride, const uint32_t* chunk_tot,
-                           const uint64_t* cell_base) {
+                           const uint64_t* cell_base, const uint8_t* ids) {
   if (nchunks == 0) return cudaSuccess;
   const bool vals = src_vals != nullptr;
 #ifndef AMS_NO_SCATTER_U
@@ -1384,28 +1396,35 @@ cudaError_t launch_scatter(cudaStream_t st, const void* src, const void* src_val
                             cells_cap, nb_stride, chunk_tot, cell_base);
 #endif
   const int mode = scatter_mode(nb_stride, stable);
-  const size_t smem = scatter_smem_bytes(nb_stride, nspl_cap, cells_cap, digit, vals, stable);
+  // Bucket bytes from the histogram pass replace the tree (and its shared memory).
+  const size_t smem = scatter_smem_bytes(nb_stride, nspl_cap, cells_cap, digit || ids, vals, stable);
   const uint64_t* s = static_cast<const uint64_t*>(src);
   const uint64_t* sv = static_cast<const uint64_t*>(src_vals);
   uint64_t* d = static_cast<uint64_t*>(dst);
   uint64_t* dv = static_cast<uint64_t*>(dst_vals);
   cudaError_t e = cudaSuccess;
-#define AMS_SCATTER_GO(K, DG, V)                                                              \
+#define AMS_SCATTER_GO(K, CL, V)                                                              \
   {                                                                                           \
-    auto fn = mode == kRankWarp ? k_scatter<K, DG, V, kRankWarp>                              \
-              : mode == kRankSerial ? k_scatter<K, DG, V, kRankSerial>                        \
-                                    : k_scatter<K, DG, V, kRankAtomic>;                       \
+    auto fn = mode == kRankWarp ? k_scatter<K, CL, V, kRankWarp>                              \
+              : mode == kRankSerial ? k_scatter<K, CL, V, kRankSerial>                        \
+                                    : k_scatter<K, CL, V, kRankAtomic>;                       \
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
     if (e != cudaSuccess) return e;                                                           \
     fn<<<(unsigned)nchunks, kThreads, smem, st>>>(s, sv, d, dv, m, blobs, dcls, nspl_cap,     \
-                                                   nb_stride, chunk_tot, cell_base);          \
+                                                   nb_stride, chunk_tot, cell_base, ids);     \
   }
   if (digit) {
-    if (vals) AMS_SCATTER_GO(AMS_KEY_U64, true, true) else AMS_SCATTER_GO(AMS_KEY_U64, true, false)
+    if (vals) AMS_SCATTER_GO(AMS_KEY_U64, kClsDigit, true) else AMS_SCATTER_GO(AMS_KEY_U64, kClsDigit, false)
+  } else if (ids) {
+    if (vals) {
+      AMS_KIND_DISPATCH(kind, K, AMS_SCATTER_GO(K, kClsIds, true))
+    } else {
+      AMS_KIND_DISPATCH(kind, K, AMS_SCATTER_GO(K, kClsIds, false))
+    }
   } else if (vals) {
-    AMS_KIND_DISPATCH(kind, K, AMS_SCATTER_GO(K, false, true))
+    AMS_KIND_DISPATCH(kind, K, AMS_SCATTER_GO(K, kClsTree, true))
   } else {
-    AMS_KIND_DISPATCH(kind, K, AMS_SCATTER_GO(K, false, false))
+    AMS_KIND_DISPATCH(kind, K, AMS_SCATTER_GO(K, kClsTree, false))
   }
 #undef AMS_SCATTER_GO
   return cudaGetLastError();
