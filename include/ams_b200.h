@@ -118,6 +118,11 @@ int ams_ctx_sync(ams_ctx_t* ctx);
 int ams_ctx_set_timing(ams_ctx_t* ctx, int enable);
 int ams_ctx_kernel_stats(ams_ctx_t* ctx, double* ms, double* bytes, uint64_t* launches, int ncat);
 int ams_ctx_reset_stats(ams_ctx_t* ctx);
+/* Timed launches since the last call (timing on): category and start / end
+ * in ms from the first launch of each resolved batch (batches are resolved
+ * by ams_ctx_kernel_stats / ams_ctx_timeline).  Fills up to cap entries,
+ * *count = number available; clears the list. */
+int ams_ctx_timeline(ams_ctx_t* ctx, int* cat, float* t0, float* t1, int cap, int* count);
 
 /* K1 — sample gather (draw_sample, ams.py:157-175, data side):
  *   d_out_keys[i] = ordered(src[h_idx[i]]), d_out_pos[i] = h_gpos[i]. */

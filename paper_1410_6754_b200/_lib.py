@@ -49,6 +49,7 @@ _SIGNATURES = {
     "ams_ctx_set_timing": (_I, [_P, _I]),
     "ams_ctx_kernel_stats": (_I, [_P, _P, _P, _P, _I]),
     "ams_ctx_reset_stats": (_I, [_P]),
+    "ams_ctx_timeline": (_I, [_P, _P, _P, _P, _I, C.POINTER(_I)]),
     "ams_level_sample": (_I, [_P, _P, _I, _U64, _P, _P, _P, _P]),
     "ams_level_splitters": (_I, [_P, _I, _P, _P, _P, _P]),
     "ams_read_splitters": (_I, [_P, _I, _P, _P, C.POINTER(_I)]),
@@ -247,6 +248,19 @@ class Context:
         la = np.zeros(n, np.uint64)
         check(lib.ams_ctx_kernel_stats(self.h, ms.ctypes.data, by.ctypes.data, la.ctypes.data, n))
         return {name: (float(ms[i]), float(by[i]), int(la[i])) for i, name in enumerate(KCAT_NAMES)}
+
+    def timeline(self):
+        """[(category, start ms, end ms)] of the timed launches since the last
+        call, in launch order (times from the first launch of each batch)."""
+        cap = 1 << 16
+        cat = np.zeros(cap, np.int32)
+        t0 = np.zeros(cap, np.float32)
+        t1 = np.zeros(cap, np.float32)
+        cnt = C.c_int(0)
+        check(lib.ams_ctx_timeline(self.h, cat.ctypes.data, t0.ctypes.data, t1.ctypes.data, cap,
+                                   C.byref(cnt)))
+        n = min(cnt.value, cap)
+        return [(KCAT_NAMES[int(cat[i])], float(t0[i]), float(t1[i])) for i in range(n)]
 
     def level_sample(self, src, kind, idx, gpos, out_keys, out_pos):
         idx, gpos = u64(idx), u64(gpos)

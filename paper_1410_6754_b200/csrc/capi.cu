@@ -161,6 +161,8 @@ struct ams_ctx {
   // optional per-category kernel timing (CUDA events on the launching stream)
   bool timing = false;
   struct Timed { int cat; cudaEvent_t a, b; double bytes; };
+  struct Span { int cat; float t0, t1; };
+  std::vector<Span> timeline;  // resolved launches, ms from the first of each resolve batch
   std::vector<Timed> pending;
   std::vector<cudaEvent_t> free_events;
   double cat_ms[AMS_NUM_KCAT] = {};
@@ -207,12 +209,21 @@ struct KTimer {
 };
 
 void resolve_timing(ams_ctx* c) {
+  const cudaEvent_t origin = c->pending.empty() ? nullptr : c->pending.front().a;
   for (auto& t : c->pending) {
     float ms = 0.f;
     cudaEventSynchronize(t.b);
     cudaEventElapsedTime(&ms, t.a, t.b);
     c->cat_ms[t.cat] += ms;
     c->cat_bytes[t.cat] += t.bytes;
+    if (c->timeline.size() < (1u << 16)) {
+      float t0 = 0.f, t1 = 0.f;
+      cudaEventElapsedTime(&t0, origin, t.a);
+      cudaEventElapsedTime(&t1, origin, t.b);
+      c->timeline.push_back({t.cat, t0, t1});
+    }
+  }
+  for (auto& t : c->pending) {
     c->free_events.push_back(t.a);
     c->free_events.push_back(t.b);
   }
@@ -302,7 +313,8 @@ int ams_ctx_destroy(ams_ctx_t* c) {
     s->release();
   for (DevBuf* b : {&c->blobs, &c->sorted_keys, &c->sorted_pos, &c->sample_idx, &c->bounds[0], &c->bounds[1],
                     &c->chunk_tot, &c->seg_hist, &c->cell_base, &c->pieces, &c->minmax, &c->dcls,
-                    &c->ovf, &c->ovf_count, &c->fb, &c->fb_count, &c->groups, &c->ngroups_d})
+                    &c->ovf, &c->ovf_count, &c->fb, &c->fb_count, &c->groups, &c->ngroups_d,
+                    &c->ids})
     b->release();
   c->h_hist.release();
   c->h_small.release();
@@ -336,11 +348,27 @@ int ams_ctx_kernel_stats(ams_ctx_t* c, double* ms, double* bytes, uint64_t* laun
   return AMS_OK;
 }
 
+int ams_ctx_timeline(ams_ctx_t* c, int* cat, float* t0, float* t1, int cap, int* count) {
+  if (!c || !count) return set_error(AMS_EINVAL, "null argument");
+  AMS_CK(cudaSetDevice(c->device));
+  resolve_timing(c);
+  const int n = (int)std::min<size_t>(c->timeline.size(), (size_t)std::max(cap, 0));
+  for (int i = 0; i < n; ++i) {
+    if (cat) cat[i] = c->timeline[i].cat;
+    if (t0) t0[i] = c->timeline[i].t0;
+    if (t1) t1[i] = c->timeline[i].t1;
+  }
+  *count = (int)c->timeline.size();
+  c->timeline.clear();
+  return AMS_OK;
+}
+
 int ams_ctx_reset_stats(ams_ctx_t* c) {
   if (!c) return set_error(AMS_EINVAL, "null context");
   AMS_CK(cudaSetDevice(c->device));
   resolve_timing(c);
   for (int i = 0; i < AMS_NUM_KCAT; ++i) { c->cat_ms[i] = 0; c->cat_bytes[i] = 0; c->cat_launches[i] = 0; }
+  c->timeline.clear();
   return AMS_OK;
 }
 

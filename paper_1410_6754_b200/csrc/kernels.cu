@@ -588,12 +588,12 @@ constexpr int kThreadsU = 512;                 // 16 warps x 8 keys per tile: 2 
 constexpr int kItemsU = kTile / kThreadsU;
 constexpr int kWarpsU = kThreadsU / 32;
 
-template <int KIND, bool DIGIT>
+template <int KIND, int CLS>
 __global__ void __launch_bounds__(kThreadsU, 2)
     k_scatter_u(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst, SegMeta m,
                 const uint8_t* __restrict__ blobs, const DigitCls* __restrict__ dcls, int nspl_cap,
                 int nb, const uint32_t* __restrict__ chunk_tot,
-                const uint64_t* __restrict__ cell_base) {
+                const uint64_t* __restrict__ cell_base, const uint8_t* __restrict__ ids) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ int s_seg;
   __shared__ uint32_t s_scan[kWarpsU + 1];
@@ -642,8 +642,8 @@ __global__ void __launch_bounds__(kThreadsU, 2)
   DigitView dv;
   int64_t posbase = 0;
   const int cls = m.cls[s];
-  if constexpr (DIGIT) dv.c = dcls[cls];
-  else {
+  if constexpr (CLS == kClsDigit) dv.c = dcls[cls];
+  else if constexpr (CLS == kClsTree) {
     tv = load_tree(blobs + (size_t)cls * kBlobStride, clsmem, nspl_cap);
     posbase = m.posbase[cls];
   }
@@ -672,7 +672,8 @@ __global__ void __launch_bounds__(kThreadsU, 2)
         const uint64_t raw = (e >= h && e < e_end) ? buf[e + h] : src[base + e];
         const uint64_t key = to_ordered<KIND>(raw);
         uint32_t b;
-        if constexpr (DIGIT) b = dv.classify(key, 0);
+        if constexpr (CLS == kClsIds) b = ids[base + e];
+        else if constexpr (CLS == kClsDigit) b = dv.classify(key, 0);
         else b = tv.classify(key, pos0 + e);
         kr[i] = key;
         pk[i] = (b << 16) | atomicAdd(&cnt[b], 1u);
@@ -1358,25 +1359,32 @@ size_t scatter_u_smem_bytes(int nb, int nspl_cap, int cells_cap, bool digit) {
   return b;
 }
 
+#ifndef AMS_SCATTER_U_IDS
+#define AMS_SCATTER_U_IDS 0
+#endif
+constexpr bool kScatterUIds = AMS_SCATTER_U_IDS;
+
 cudaError_t launch_scatter_u(cudaStream_t st, const void* src, int kind, bool digit, void* dst,
                              const SegMeta& m, uint64_t nchunks, const uint8_t* blobs,
                              const DigitCls* dcls, int nspl_cap, int cells_cap, int nb_stride,
-                             const uint32_t* chunk_tot, const uint64_t* cell_base) {
+                             const uint32_t* chunk_tot, const uint64_t* cell_base,
+                             const uint8_t* ids) {
   if (nchunks == 0) return cudaSuccess;
-  const size_t smem = scatter_u_smem_bytes(nb_stride, nspl_cap, cells_cap, digit);
+  const size_t smem = scatter_u_smem_bytes(nb_stride, nspl_cap, cells_cap, digit || ids);
   const uint64_t* s = static_cast<const uint64_t*>(src);
   uint64_t* d = static_cast<uint64_t*>(dst);
   cudaError_t e = cudaSuccess;
-#define AMS_SCATTER_U_GO(K, DG)                                                               \
+#define AMS_SCATTER_U_GO(K, CL)                                                               \
   {                                                                                           \
-    auto fn = k_scatter_u<K, DG>;                                                             \
+    auto fn = k_scatter_u<K, CL>;                                                             \
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
     if (e != cudaSuccess) return e;                                                           \
-    fn<<<(unsigned)nchunks, kThreadsU, smem, st>>>(s, d, m, blobs, dcls, nspl_cap, nb_stride,  \
-                                                   chunk_tot, cell_base);                     \
+    fn<<<(unsigned)nchunks, kThreadsU, smem, st>>>(s, d, m, blobs, dcls, nspl_cap, nb_stride, \
+                                                    chunk_tot, cell_base, ids);               \
   }
-  if (digit) AMS_SCATTER_U_GO(AMS_KEY_U64, true)
-  else AMS_KIND_DISPATCH(kind, K, AMS_SCATTER_U_GO(K, false))
+  if (digit) AMS_SCATTER_U_GO(AMS_KEY_U64, kClsDigit)
+  else if (ids) AMS_KIND_DISPATCH(kind, K, AMS_SCATTER_U_GO(K, kClsIds))
+  else AMS_KIND_DISPATCH(kind, K, AMS_SCATTER_U_GO(K, kClsTree))
 #undef AMS_SCATTER_U_GO
   return cudaGetLastError();
 }
@@ -1391,9 +1399,9 @@ cudaError_t launch_scatter(cudaStream_t st, const void* src, const void* src_val
 #ifndef AMS_NO_SCATTER_U
   // The lean unstable kernel pays off with the cheap digit classifier (the
   // final partition); the tree classifier keeps the 4-CTA kernel below.
-  if (!stable && !vals && digit)
+  if (!stable && !vals && (digit || (ids && kScatterUIds)))
     return launch_scatter_u(st, src, kind, digit, dst, m, nchunks, blobs, dcls, nspl_cap,
-                            cells_cap, nb_stride, chunk_tot, cell_base);
+                            cells_cap, nb_stride, chunk_tot, cell_base, digit ? nullptr : ids);
 #endif
   const int mode = scatter_mode(nb_stride, stable);
   // Bucket bytes from the histogram pass replace the tree (and its shared memory).
