@@ -47,6 +47,10 @@ struct DigitCls {
   uint64_t mult;
   uint32_t nb;
   uint32_t pad;
+  // Cell-relative map for the cell sort (k_final_ranges): cell c starts at or
+  // after lo + c * q; sub = ((key - that) >> sh) * m32 >> 32 (m32 == 0: none).
+  uint64_t q;
+  uint32_t m32, sh;
 };
 
 // Multiplier of the scaled digit above.  Any value keeps digits monotone in

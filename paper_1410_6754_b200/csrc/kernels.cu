@@ -727,6 +727,8 @@ __global__ void k_gather_bounds(const uint64_t* __restrict__ bounds, const int32
   out[2 * i + 1] = bounds[2 * sel[i] + 1];
 }
 
+constexpr int kCellSubBuckets = 2 * AMS_SMEM_SORT_CAP;  // sub-buckets of a digit cell (= kSubK)
+
 __global__ void k_final_ranges(const uint64_t* __restrict__ bounds, int nseg, int nb,
                                DigitCls* __restrict__ out) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
@@ -738,6 +740,18 @@ __global__ void k_final_ranges(const uint64_t* __restrict__ bounds, int nseg, in
   d.nb = (uint32_t)nb;
   d.mult = digit_mult(hi - lo, d.nb);
   d.pad = 0;
+  d.q = 0;
+  d.m32 = 0;
+  d.sh = 0;
+  if (d.mult != 0) {
+    // key - lo of cell c lies in [c * 2^64 / mult, (c + 1) * 2^64 / mult):
+    // with q = floor((2^64 - 1) / mult), key - (lo + c * q) is in [0, w).
+    d.q = (~0ULL) / d.mult;
+    const uint64_t w = d.q + 2ull * d.nb + 2;
+    d.sh = (uint32_t)max(0, bit_length64(w) - 32);
+    const uint64_t w32 = ((w - 1) >> d.sh) + 1;
+    if (w32 > (uint64_t)kCellSubBuckets) d.m32 = (uint32_t)(((uint64_t)kCellSubBuckets << 32) / w32);
+  }
   out[s] = d;
 }
 
@@ -917,7 +931,11 @@ constexpr int kRankMax = 64;
 #define AMS_SORT_CTAS 3
 #endif
 constexpr int kSortCtas = AMS_SORT_CTAS;  // resident CTAs per SM (register budget)
-constexpr int kSubK = 2 * kSortCap;                   // sub-buckets of the refined digit
+#ifndef AMS_NIT_BREAK
+#define AMS_NIT_BREAK 0
+#endif
+constexpr bool kNitBreak = AMS_NIT_BREAK;
+constexpr int kSubK = kCellSubBuckets;                   // sub-buckets of the refined digit
 constexpr int kScanWords = kSubK / 2 / kSortThreads;  // counter words per thread (2 sub-buckets each)
 static_assert(kScanWords % 4 == 0, "scan loads 4 words at a time");
 constexpr int kQueueCap = kSortCap / 2;               // sub-buckets with >= 2 keys
@@ -989,24 +1007,31 @@ __global__ void __launch_bounds__(kSortThreads, kSortCtas)
   const uint32_t n = (uint32_t)count;
   const uint32_t tid = threadIdx.x;
   const int lane = tid & 31, wid = tid >> 5;
-  // Refined partition digit (first-round digit cells with room for x kSubK).
-  uint64_t lo = 0, mult = 0;
-  uint32_t sub0 = 0, sub_max = kSubK - 1;
+  // Digit cells of the first partition round: cell c of a segment holds the
+  // keys with floor((key - lo) * mult / 2^64) == c, i.e. key - lo in
+  // [c * 2^64 / mult, (c + 1) * 2^64 / mult).  With q = floor((2^64 - 1) /
+  // mult), key - (lo + c * q) is >= 0 and below q + 2c + 2 (cell nb - 1 also
+  // takes the clamped keys: the clamp below keeps its map monotone), so
+  // sub = ((key - cell_lo) >> sh) * m32 >> 32 spreads the cell over kSubK
+  // sub-buckets with one 32-bit multiply and no min/max pass.
+  uint64_t lo = 0;
+  uint32_t m32 = 0, sh = 0;
   int attempt = 1;
   if (cs.mode == 0 && cs.dcls) {
     const uint32_t seg = blockIdx.x / cs.cells_per_seg;
-    const DigitCls d = cs.dcls[seg];
-    if (d.mult != 0 && d.mult < (~0ULL) / kSubK) {
+    const DigitCls& d = cs.dcls[seg];
+    if (d.m32 != 0) {
       attempt = 0;
-      lo = d.lo;
-      mult = d.mult * kSubK;
-      sub0 = (blockIdx.x - seg * cs.cells_per_seg) * kSubK;
-      sub_max = d.nb * kSubK - 1;  // the partition clamps digits to nb - 1
+      lo = d.lo + (uint64_t)(blockIdx.x - seg * cs.cells_per_seg) * d.q;
+      m32 = d.m32;
+      sh = d.sh;
     }
   }
+  const int nit = (int)((n + kSortThreads - 1) / kSortThreads);  // items in use per thread
   uint64_t kr[kSortItems];
 #pragma unroll
   for (int it = 0; it < kSortItems; ++it) {
+    if (kNitBreak && it >= nit) break;
     const uint32_t i = it * kSortThreads + tid;
     kr[it] = i < n ? ldg_stream(src + off + i) : ~0ULL;
   }
@@ -1023,6 +1048,7 @@ __global__ void __launch_bounds__(kSortThreads, kSortCtas)
       uint64_t mn = ~0ULL, mx = 0;
 #pragma unroll
       for (int it = 0; it < kSortItems; ++it) {
+        if (kNitBreak && it >= nit) break;
         mn = min(mn, kr[it]);
         if (it * kSortThreads + tid < n) mx = max(mx, kr[it]);
       }
@@ -1037,12 +1063,13 @@ __global__ void __launch_bounds__(kSortThreads, kSortCtas)
       }
       const uint64_t range = mx - mn;
       exact = range < 2 * (uint64_t)n;  // one key value per sub-bucket
-      // Sub-bucket = (k - mn) * 2n >> bitlen(range): in [0, 2n), monotone.
+      // Sub-bucket = ((k - mn) >> sh) * m32 >> 32 in [0, 2n), monotone.
       lo = mn;
       hi_key = mx;
-      mult = exact ? 0 : ((uint64_t)(2 * n) << (64 - bit_length64(range)));
-      sub0 = 0;
-      sub_max = kSubK - 1;
+      sh = (uint32_t)max(0, bit_length64(range) - 32);
+      // floor(2n * 2^32 / w32) - 1 <= the exact quotient: sub stays below 2n.
+      m32 = exact ? 0
+                  : (uint32_t)((float)(2 * n) * 4294967296.0f / (float)((range >> sh) + 1)) - 1u;
     } else {
       __syncthreads();
     }
@@ -1050,10 +1077,12 @@ __global__ void __launch_bounds__(kSortThreads, kSortCtas)
     uint32_t nq = 0;  // sub-buckets this thread will queue (its keys of rank 1)
 #pragma unroll
     for (int it = 0; it < kSortItems; ++it) {
+      if (kNitBreak && it >= nit) break;
       pk[it] = 0xFFFFFFFFu;
       if (it * kSortThreads + tid < n) {
         const uint64_t x = kr[it] - lo;
-        const uint32_t s = exact ? (uint32_t)x : min((uint32_t)__umul64hi(x, mult), sub_max) - sub0;
+        const uint32_t s =
+            exact ? (uint32_t)x : min(__umulhi((uint32_t)(x >> sh), m32), (uint32_t)kSubK - 1);
         const uint32_t sh = (s & 1) * 16;
         const uint32_t rk = (atomicAdd(&cw[sw_word(s >> 1)], 1u << sh) >> sh) & 0xFFFFu;
         pk[it] = (s << 16) | rk;
@@ -1114,6 +1143,7 @@ __global__ void __launch_bounds__(kSortThreads, kSortCtas)
   // 3. place: slot = start(sub-bucket) + rank.
 #pragma unroll
   for (int it = 0; it < kSortItems; ++it) {
+    if (kNitBreak && it >= nit) break;
     if (pk[it] != 0xFFFFFFFFu) {
       const uint32_t s = pk[it] >> 16, rk = pk[it] & 0xFFFFu;
       const uint32_t slot = c16[sw16(s)] + rk;
