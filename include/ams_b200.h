@@ -194,6 +194,54 @@ int ams_final_sort_stats(ams_ctx_t* ctx, uint64_t out[2]);
 int ams_map_keys(ams_ctx_t* ctx, const void* src, void* dst, uint64_t n, int from_kind,
                  int to_kind);
 
+
+/* ------------------------------------------------------------------ */
+/* One-call sort: ams_sort(net, data, params, "simple", seed)           */
+/* (ams.py:271-313) on the context's GPU, the whole level loop in C++.  */
+
+#define AMS_MAX_LEVELS 8
+
+/* AmsParams (ams.py:33-65) + SeedSpec (core.py:46-71) + key encoding. */
+typedef struct {
+  int levels;                          /* k = len(group_counts) */
+  int group_counts[AMS_MAX_LEVELS];    /* r per level; product = p */
+  double oversampling;                 /* a; <= 0 selects 1.6*log10(max(n,10)) (ams.py:278-280) */
+  int overpartition;                   /* b (reference default 16) */
+  double imbalance;                    /* epsilon (reference default 0.2) */
+  int64_t master_seed;                 /* SeedSpec.master_seed */
+  const char* stream_id;               /* SeedSpec.stream_id, e.g. "algo/rep0" */
+  int key_kind;                        /* AMS_KEY_U64 / AMS_KEY_I64 / AMS_KEY_F64 */
+  int with_stats;                      /* fill the exchange maxima of the reports */
+} ams_params_t;
+
+/* One level's report (ams.py:294-308; exchange maxima simnet.py:109-124). */
+typedef struct {
+  int level, r;
+  uint64_t max_load, min_load, sample_size, plan_load, over_budget;
+  uint64_t max_words, max_msgs, max_sent_msgs, max_recv_msgs;
+} ams_level_report_t;
+
+/* Sort n = sum(pe_sizes) keys (device buffer, PE-major: PE i owns the next
+ * pe_sizes[i]) with optional 8-byte payloads into out (+ out_vals): the
+ * concatenation of the per-PE outputs of ams_sort.  out_pe_sizes[p] gets
+ * the final PE sizes, reports[levels] the level reports (either may be
+ * NULL).  Inputs are not modified; the context owns the workspace.  Runs on
+ * the context's stream and returns after the last host-side step (the
+ * device work may still be in flight). */
+int ams_sort_run(ams_ctx_t* ctx, const ams_params_t* params, int p, const uint64_t* pe_sizes,
+                 const void* keys, const void* vals, void* out, void* out_vals,
+                 uint64_t* out_pe_sizes, ams_level_report_t* reports);
+/* Records of the last ams_sort_run, level by level (host arrays; NULL
+ * skips a field): group_first/npe [G], sizes_before/new_sizes [P],
+ * drawn [G], nb [G], seg_hist [P][nb_stride], boundaries [G][r+1],
+ * loads [G][r], max_load [G], stats [G][4] (when has_stats). */
+int ams_run_level_dims(ams_ctx_t* ctx, int level, int* r, int* ngroups, int* npe, int* nb_stride,
+                       int* has_stats);
+int ams_run_level(ams_ctx_t* ctx, int level, int32_t* group_first, int32_t* group_npe,
+                  uint64_t* sizes_before, uint64_t* drawn, int32_t* nb, uint32_t* seg_hist,
+                  uint64_t* boundaries, uint64_t* loads, uint64_t* max_load, uint64_t* new_sizes,
+                  uint64_t* stats);
+
 #ifdef __cplusplus
 }
 #endif

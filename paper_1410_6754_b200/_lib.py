@@ -60,7 +60,30 @@ _SIGNATURES = {
     "ams_set_minmax": (_I, [_P, _P]),
     "ams_final_sort": (_I, [_P, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P]),
     "ams_map_keys": (_I, [_P, _P, _P, _U64, _I, _I]),
+    "ams_sort_run": (_I, [_P, _P, _I, _P, _P, _P, _P, _P, _P, _P]),
+    "ams_run_level_dims": (_I, [_P, _I, _P, _P, _P, _P, _P]),
+    "ams_run_level": (_I, [_P, _I] + [_P] * 11),
 }
+
+MAX_LEVELS = 8
+
+
+class ParamsT(C.Structure):
+    """ams_params_t (include/ams_b200.h)."""
+
+    _fields_ = [("levels", C.c_int), ("group_counts", C.c_int * MAX_LEVELS),
+                ("oversampling", C.c_double), ("overpartition", C.c_int),
+                ("imbalance", C.c_double), ("master_seed", C.c_int64),
+                ("stream_id", C.c_char_p), ("key_kind", C.c_int), ("with_stats", C.c_int)]
+
+
+class LevelReportT(C.Structure):
+    """ams_level_report_t (include/ams_b200.h)."""
+
+    _fields_ = [("level", C.c_int), ("r", C.c_int)] + [
+        (f, C.c_uint64) for f in ("max_load", "min_load", "sample_size", "plan_load",
+                                  "over_budget", "max_words", "max_msgs", "max_sent_msgs",
+                                  "max_recv_msgs")]
 
 EXPORTED = tuple(_SIGNATURES)
 
@@ -316,6 +339,32 @@ class Context:
         so, sl = u64(seg_off), u64(seg_len)
         check(lib.ams_final_sort(self.h, ptr(src), ptr(src_vals), ptr(tmp), ptr(tmp_vals), ptr(out),
                                  ptr(out_vals), key_kind, len(so), so.ctypes.data, sl.ctypes.data))
+
+    def sort_run(self, params: ParamsT, pe_sizes, keys, vals, out, out_vals):
+        """ams_sort_run: returns (final PE sizes, [LevelReportT])."""
+        sz = u64(pe_sizes)
+        out_sizes = np.zeros(max(len(sz), 1), np.uint64)
+        reps = (LevelReportT * params.levels)()
+        check(lib.ams_sort_run(self.h, C.byref(params), len(sz), sz.ctypes.data, ptr(keys),
+                               ptr(vals), ptr(out), ptr(out_vals), out_sizes.ctypes.data, reps))
+        return out_sizes[: len(sz)], list(reps)
+
+    def run_level(self, level: int) -> dict:
+        """Host records of one level of the last sort_run."""
+        r, G, P, nbs, hs = (C.c_int() for _ in range(5))
+        check(lib.ams_run_level_dims(self.h, level, C.byref(r), C.byref(G), C.byref(P),
+                                     C.byref(nbs), C.byref(hs)))
+        r, G, P, nbs = r.value, G.value, P.value, nbs.value
+        d = {"r": r, "group_first": np.zeros(G, np.int32), "group_npe": np.zeros(G, np.int32),
+             "sizes_before": np.zeros(P, np.uint64), "drawn": np.zeros(G, np.uint64),
+             "nb": np.zeros(G, np.int32), "seg_hist": np.zeros((P, nbs), np.uint32),
+             "boundaries": np.zeros((G, r + 1), np.uint64), "loads": np.zeros((G, r), np.uint64),
+             "max_load": np.zeros(G, np.uint64), "new_sizes": np.zeros(P, np.uint64),
+             "stats": np.zeros((G, 4), np.uint64) if hs.value else None}
+        order = ("group_first", "group_npe", "sizes_before", "drawn", "nb", "seg_hist",
+                 "boundaries", "loads", "max_load", "new_sizes", "stats")
+        check(lib.ams_run_level(self.h, level, *[ptr(d[k]) for k in order]))
+        return d
 
     def map_keys(self, src, dst, n, from_kind, to_kind):
         check(lib.ams_map_keys(self.h, ptr(src), ptr(dst), n, from_kind, to_kind))

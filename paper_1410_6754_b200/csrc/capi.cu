@@ -1,6 +1,7 @@
 // C ABI of the AMS-sort hot path: device context, metadata staging and the
 // level / final-sort entry points declared in include/ams_b200.h.
 #include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <string>
@@ -158,6 +159,17 @@ struct ams_ctx {
   DevBuf dcls, ovf, ovf_count, fb, fb_count, groups, ngroups_d;
   HostBuf h_small;
   uint64_t overflow_cells = 0, fallback_cells = 0;
+  // one-call driver (ams_sort_run): workspace and the last run's level records
+  DevBuf work[2], work_v[2], s_keys, s_pos;
+  struct LevelRec {
+    int r = 0, G = 0, P = 0, nb_stride = 0;
+    std::vector<int32_t> group_first, group_npe, nb;
+    std::vector<uint64_t> sizes_before, drawn, boundaries, loads, max_load, new_sizes, stats;
+    std::vector<uint32_t> hist;
+    bool has_stats = false;
+  };
+  std::vector<LevelRec> run_levels;
+  std::vector<uint64_t> run_final_sizes;
   // optional per-category kernel timing (CUDA events on the launching stream)
   bool timing = false;
   struct Timed { int cat; cudaEvent_t a, b; double bytes; };
@@ -314,7 +326,8 @@ int ams_ctx_destroy(ams_ctx_t* c) {
   for (DevBuf* b : {&c->blobs, &c->sorted_keys, &c->sorted_pos, &c->sample_idx, &c->bounds[0], &c->bounds[1],
                     &c->chunk_tot, &c->seg_hist, &c->cell_base, &c->pieces, &c->minmax, &c->dcls,
                     &c->ovf, &c->ovf_count, &c->fb, &c->fb_count, &c->groups, &c->ngroups_d,
-                    &c->ids})
+                    &c->ids, &c->work[0], &c->work[1], &c->work_v[0], &c->work_v[1], &c->s_keys,
+                    &c->s_pos})
     b->release();
   c->h_hist.release();
   c->h_small.release();
@@ -826,6 +839,206 @@ int ams_map_keys(ams_ctx_t* c, const void* src, void* dst, uint64_t n, int from_
   KTimer kt(c, AMS_KCAT_MAP, 16.0 * n);
   AMS_CK(launch_map_keys(c->stream, src, dst, n, from_kind, to_kind));
   c->launches += n ? 1 : 0;
+  return AMS_OK;
+}
+
+
+// ---------------------------------------------------------------------------
+// One-call driver: ams_sort (ams.py:271-313) with scheme "simple" on one GPU,
+// the level loop of paper_1410_6754_b200/engine.py in C++ (no Python between
+// the level steps).
+int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* pe_sizes,
+                 const void* keys, const void* vals, void* out, void* out_vals,
+                 uint64_t* out_pe_sizes, ams_level_report_t* reports) {
+  if (!c || !prm) return set_error(AMS_EINVAL, "null argument");
+  const int k = prm->levels;
+  if (k < 1 || k > AMS_MAX_LEVELS) return set_error(AMS_EINVAL, "levels outside 1..AMS_MAX_LEVELS");
+  uint64_t prod = 1;
+  for (int lv = 0; lv < k; ++lv) {  // AmsParams validation (ams.py:45-52, 61-65)
+    if (prm->group_counts[lv] < 1) return set_error(AMS_EINVAL, "group counts must be positive");
+    prod *= (uint64_t)prm->group_counts[lv];
+  }
+  if (prm->overpartition < 1) return set_error(AMS_EINVAL, "overpartitioning factor must be at least 1");
+  if (!(prm->imbalance > 0)) return set_error(AMS_EINVAL, "imbalance budget must be positive");
+  if (p < 1 || prod != (uint64_t)p)
+    return set_error(AMS_EINVAL, "group counts do not telescope " + std::to_string(p) + " PEs");
+  if (!pe_sizes || !prm->stream_id) return set_error(AMS_EINVAL, "null argument");
+  if (prm->key_kind < AMS_KEY_U64 || prm->key_kind > AMS_KEY_F64)
+    return set_error(AMS_EINVAL, "unknown key kind");
+  uint64_t n = 0;
+  for (int i = 0; i < p; ++i) n += pe_sizes[i];
+  if (n && (!keys || !out)) return set_error(AMS_EINVAL, "null key buffer");
+  const bool with_vals = vals != nullptr;
+  if (with_vals && !out_vals) return set_error(AMS_EINVAL, "values need an output buffer");
+  AMS_CK(cudaSetDevice(c->device));
+  // ams.py:278-280 and AmsParams.per_level_imbalance (ams.py:58-59).
+  const double a = prm->oversampling > 0 ? prm->oversampling
+                                         : 1.6 * std::log10((double)std::max<uint64_t>(n, 10));
+  const double eps_l = std::pow(1.0 + prm->imbalance, 1.0 / k) - 1.0;
+  const int b = prm->overpartition;
+  // Workspace (two ping-pong buffers) and one-element stand-ins for n == 0.
+  const size_t wb = 8 * (size_t)std::max<uint64_t>(n, 1);
+  for (int i = 0; i < 2; ++i) {
+    AMS_CK(c->work[i].ensure(wb));
+    if (with_vals) AMS_CK(c->work_v[i].ensure(wb));
+  }
+  const void* src = n ? keys : c->work[1].p;
+  const void* src_v = with_vals ? (n ? vals : c->work_v[1].p) : nullptr;
+  void* dst_out = n ? out : c->work[1].p;
+  void* dst_out_v = with_vals ? (n ? out_vals : c->work_v[1].p) : nullptr;
+  int src_kind = prm->key_kind;
+  std::vector<uint64_t> sizes(pe_sizes, pe_sizes + p);
+  std::vector<int32_t> gf{0}, gn{p};
+  c->run_levels.assign(k, ams_ctx::LevelRec{});
+  int rc;
+  for (int lv = 0; lv < k; ++lv) {
+    const int r = prm->group_counts[lv];
+    const int G = (int)gf.size();
+    std::vector<uint64_t> offs(p + 1, 0);
+    for (int i = 0; i < p; ++i) offs[i + 1] = offs[i] + sizes[i];
+    // ams.py:224-225 per group.
+    std::vector<uint64_t> targets(G), br(G);
+    for (int g = 0; g < G; ++g) {
+      uint64_t n_g = 0;
+      for (int i = 0; i < gn[g]; ++i) n_g += sizes[gf[g] + i];
+      br[g] = std::min<uint64_t>((uint64_t)b * r, n_g + 1);
+      const uint64_t x = br[g];
+      targets[g] = std::min<uint64_t>(n_g, std::max<uint64_t>(x - 1, (uint64_t)std::ceil(a * (double)x)));
+    }
+    uint64_t cap = 0;
+    for (uint64_t t : targets) cap += t;
+    std::vector<uint64_t> idx(std::max<uint64_t>(cap, 1)), gpos(std::max<uint64_t>(cap, 1)), drawn(G);
+    rc = ams_draw_sample_positions(prm->master_seed, prm->stream_id, lv, G, gf.data(), gn.data(),
+                                   targets.data(), sizes.data(), offs.data(), cap, idx.data(),
+                                   gpos.data(), drawn.data());
+    if (rc) return rc;
+    std::vector<int32_t> nb(G);
+    std::vector<uint64_t> soff(G + 1, 0);
+    int nb_stride = 1;
+    for (int g = 0; g < G; ++g) {
+      nb[g] = (int)std::min<uint64_t>(br[g], drawn[g] + 1);  // ams.py:228
+      if (nb[g] > AMS_MAX_BUCKETS)
+        return set_error(AMS_EINVAL, std::to_string(nb[g]) + " buckets exceed the supported " +
+                                         std::to_string(AMS_MAX_BUCKETS));
+      nb_stride = std::max(nb_stride, nb[g]);
+      soff[g + 1] = soff[g] + drawn[g];
+    }
+    const uint64_t S = soff[G];
+    AMS_CK(c->s_keys.ensure(8 * (size_t)std::max<uint64_t>(S, 1)));
+    AMS_CK(c->s_pos.ensure(4 * (size_t)std::max<uint64_t>(S, 1)));
+    if ((rc = ams_level_sample(c, src, src_kind, S, idx.data(), gpos.data(), c->s_keys.as<uint64_t>(),
+                               c->s_pos.as<uint32_t>())))
+      return rc;
+    if ((rc = ams_level_splitters(c, G, c->s_keys.as<uint64_t>(), c->s_pos.as<uint32_t>(),
+                                  soff.data(), nb.data())))
+      return rc;
+    std::vector<int32_t> seg_group(p);
+    std::vector<int64_t> posbase(G);
+    for (int g = 0; g < G; ++g) {
+      for (int i = 0; i < gn[g]; ++i) seg_group[gf[g] + i] = g;
+      posbase[g] = -(int64_t)offs[gf[g]];
+    }
+    const bool last = lv == k - 1;
+    ams_ctx::LevelRec& rec = c->run_levels[lv];
+    rec.r = r; rec.G = G; rec.P = p; rec.nb_stride = nb_stride;
+    rec.group_first = gf; rec.group_npe = gn; rec.nb = nb;
+    rec.sizes_before = sizes; rec.drawn = drawn;
+    rec.hist.assign((size_t)p * nb_stride, 0);
+    if ((rc = ams_level_classify(c, src, src_kind, p, offs.data(), sizes.data(), seg_group.data(), G,
+                                 posbase.data(), nb_stride, lv == 0, !(last && !with_vals),
+                                 rec.hist.data())))
+      return rc;
+    rec.boundaries.assign((size_t)G * (r + 1), 0);
+    rec.loads.assign((size_t)G * r, 0);
+    rec.max_load.assign(G, 0);
+    rec.new_sizes.assign(p, 0);
+    rec.has_stats = prm->with_stats != 0;
+    rec.stats.assign(rec.has_stats ? (size_t)G * 4 : 0, 0);
+    if ((rc = ams_plan_level(G, gn.data(), nb.data(), r, rec.hist.data(), nb_stride,
+                             rec.boundaries.data(), rec.loads.data(), rec.max_load.data(),
+                             rec.new_sizes.data(), rec.has_stats ? rec.stats.data() : nullptr)))
+      return rc;
+    std::vector<uint64_t> dst_start(G);
+    for (int g = 0; g < G; ++g) dst_start[g] = offs[gf[g]];
+    void* dst = c->work[lv % 2].p;
+    void* dst_v = with_vals ? c->work_v[lv % 2].p : nullptr;
+    if ((rc = ams_level_scatter(c, src, src_v, src_kind, dst, dst_v, r, rec.boundaries.data(),
+                                dst_start.data(), 0, G * r)))
+      return rc;
+    // Level report (ams.py:258-268, 294-308).
+    if (reports) {
+      ams_level_report_t& rp = reports[lv];
+      std::memset(&rp, 0, sizeof rp);
+      rp.level = lv + 1;
+      rp.r = r;
+      rp.max_load = *std::max_element(rec.new_sizes.begin(), rec.new_sizes.end());
+      rp.min_load = *std::min_element(rec.new_sizes.begin(), rec.new_sizes.end());
+      rp.sample_size = *std::max_element(drawn.begin(), drawn.end());
+      rp.plan_load = *std::max_element(rec.max_load.begin(), rec.max_load.end());
+      for (int g = 0; g < G; ++g) {
+        uint64_t n_g = 0;
+        for (int i = 0; i < gn[g]; ++i) n_g += sizes[gf[g] + i];
+        const uint64_t budget = (uint64_t)std::ceil((1.0 + eps_l) * (double)n_g / r);
+        rp.over_budget += rec.max_load[g] > budget;
+        if (rec.has_stats) {
+          rp.max_words = std::max(rp.max_words, rec.stats[4 * g + 0]);
+          rp.max_msgs = std::max(rp.max_msgs, rec.stats[4 * g + 1]);
+          rp.max_sent_msgs = std::max(rp.max_sent_msgs, rec.stats[4 * g + 2]);
+          rp.max_recv_msgs = std::max(rp.max_recv_msgs, rec.stats[4 * g + 3]);
+        }
+      }
+    }
+    src = dst;
+    src_v = dst_v;
+    src_kind = AMS_KEY_U64;
+    sizes = rec.new_sizes;
+    std::vector<int32_t> nf, nn;
+    for (int g = 0; g < G; ++g) {
+      const int step = gn[g] / r;
+      for (int t = 0; t < r; ++t) { nf.push_back(gf[g] + t * step); nn.push_back(step); }
+    }
+    gf.swap(nf);
+    gn.swap(nn);
+  }
+  // Final local sort (ams.py:310-312).
+  std::vector<uint64_t> offs(p + 1, 0);
+  for (int i = 0; i < p; ++i) offs[i + 1] = offs[i] + sizes[i];
+  void* tmp = c->work[k % 2].p;
+  void* tmp_v = with_vals ? c->work_v[k % 2].p : nullptr;
+  if ((rc = ams_final_sort(c, const_cast<void*>(src), const_cast<void*>(src_v), tmp, tmp_v, dst_out,
+                           dst_out_v, prm->key_kind, p, offs.data(), sizes.data())))
+    return rc;
+  c->run_final_sizes = sizes;
+  if (out_pe_sizes) std::memcpy(out_pe_sizes, sizes.data(), sizeof(uint64_t) * p);
+  return AMS_OK;
+}
+
+int ams_run_level_dims(ams_ctx_t* c, int level, int* r, int* ngroups, int* npe, int* nb_stride,
+                       int* has_stats) {
+  if (!c) return set_error(AMS_EINVAL, "null context");
+  if (level < 0 || level >= (int)c->run_levels.size()) return set_error(AMS_EINVAL, "no such level");
+  const ams_ctx::LevelRec& L = c->run_levels[level];
+  if (r) *r = L.r;
+  if (ngroups) *ngroups = L.G;
+  if (npe) *npe = L.P;
+  if (nb_stride) *nb_stride = L.nb_stride;
+  if (has_stats) *has_stats = L.has_stats;
+  return AMS_OK;
+}
+
+int ams_run_level(ams_ctx_t* c, int level, int32_t* group_first, int32_t* group_npe,
+                  uint64_t* sizes_before, uint64_t* drawn, int32_t* nb, uint32_t* seg_hist,
+                  uint64_t* boundaries, uint64_t* loads, uint64_t* max_load, uint64_t* new_sizes,
+                  uint64_t* stats) {
+  if (!c) return set_error(AMS_EINVAL, "null context");
+  if (level < 0 || level >= (int)c->run_levels.size()) return set_error(AMS_EINVAL, "no such level");
+  const ams_ctx::LevelRec& L = c->run_levels[level];
+  auto cp = [](auto* dst, const auto& v) {
+    if (dst && !v.empty()) std::memcpy(dst, v.data(), sizeof(v[0]) * v.size());
+  };
+  cp(group_first, L.group_first); cp(group_npe, L.group_npe); cp(sizes_before, L.sizes_before);
+  cp(drawn, L.drawn); cp(nb, L.nb); cp(seg_hist, L.hist); cp(boundaries, L.boundaries);
+  cp(loads, L.loads); cp(max_load, L.max_load); cp(new_sizes, L.new_sizes); cp(stats, L.stats);
   return AMS_OK;
 }
 

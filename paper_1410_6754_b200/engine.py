@@ -167,6 +167,10 @@ class AmsSorter:
         stream = torch.cuda.current_stream(self.device)
         self.ctx.set_stream(stream.cuda_stream)
         launches0 = self.ctx.launches
+        if not record_splitters:
+            # The whole level loop in C++ (ams_sort_run); same steps as below.
+            return self._sort_native(keys, vals, ret_out, ret_vals, out, out_vals, sizes, params,
+                                     master, stream_id, kind, with_stats, launches0, n)
         a = params.oversampling_for(n)                               # ams.py:278-280
         eps_l = params.per_level_imbalance()
         b = params.overpartition
@@ -224,3 +228,34 @@ class AmsSorter:
         tmp, tmp_v = work[k % 2], work_v[k % 2]
         self.ctx.final_sort(src, src_v, tmp, tmp_v, out, out_vals, kind, offs[:-1], sizes)
         return SortOutput(ret_out, ret_vals, sizes, levels, self.ctx.launches - launches0)
+
+    def _sort_native(self, keys, vals, ret_out, ret_vals, out, out_vals, sizes, params, master,
+                     stream_id, kind, with_stats, launches0, n):
+        prm = L.ParamsT()
+        gc = tuple(params.group_counts)
+        if len(gc) > L.MAX_LEVELS:
+            raise ValueError(f"at most {L.MAX_LEVELS} levels are supported")
+        prm.levels = len(gc)
+        for i, r in enumerate(gc):
+            prm.group_counts[i] = int(r)
+        prm.oversampling = float(params.oversampling) if params.oversampling is not None else 0.0
+        prm.overpartition = int(params.overpartition)
+        prm.imbalance = float(params.imbalance)
+        prm.master_seed = int(master)
+        prm.stream_id = stream_id.encode()
+        prm.key_kind = int(kind)
+        prm.with_stats = int(bool(with_stats))
+        final_sizes, _ = self.ctx.sort_run(prm, sizes, keys if n else None,
+                                           vals if n else None, out if n else None,
+                                           out_vals if n else None)
+        eps_l = params.per_level_imbalance()
+        levels = []
+        for lv, r in enumerate(gc):
+            d = self.ctx.run_level(lv)
+            n_g = np.add.reduceat(d["sizes_before"], d["group_first"]) if len(d["sizes_before"]) \
+                else np.zeros(len(d["group_first"]), np.uint64)
+            levels.append(LevelRecord(lv, r, d["group_first"], d["group_npe"], d["sizes_before"],
+                                      d["drawn"], d["nb"].astype(np.int64), d["seg_hist"],
+                                      d["boundaries"], d["loads"], d["max_load"],
+                                      load_budget(n_g, r, eps_l), d["new_sizes"], d["stats"]))
+        return SortOutput(ret_out, ret_vals, final_sizes, levels, self.ctx.launches - launches0)
