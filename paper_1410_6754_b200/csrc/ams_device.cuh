@@ -21,6 +21,9 @@ static_assert(kItems * kThreads == kTile, "tile geometry");
 // Tree classifier blob (one per group) in global memory: header, sorted
 // splitter keys and positions, and a key-range LUT whose cells hold
 // (first splitter index | splitter count << 16).
+#ifndef AMS_LUT_EXTRA_BITS
+#define AMS_LUT_EXTRA_BITS 6
+#endif
 constexpr int kMaxSpl = AMS_MAX_BUCKETS;  // room for nb-1 <= 4095 splitters
 constexpr int kMaxLutBits = 13;
 constexpr int kMaxCells = 1 << kMaxLutBits;
@@ -74,11 +77,11 @@ __host__ __device__ inline int bit_length64(uint64_t x) {
 #endif
 }
 
-// LUT of ~16 cells per splitter: most keys see a cell with no splitter or
+// LUT of ~64 cells per splitter: most keys see a cell with no splitter or
 // one, so classification is one LUT load plus at most one compare.
 __host__ __device__ inline int lut_bits_for(int nspl) {
   int lg = bit_length64((uint64_t)nspl);  // ~ceil(log2(nspl+1))
-  int b = lg + 4;
+  int b = lg + AMS_LUT_EXTRA_BITS;
   return b < 4 ? 4 : (b > kMaxLutBits ? kMaxLutBits : b);
 }
 

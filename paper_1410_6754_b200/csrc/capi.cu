@@ -126,8 +126,6 @@ struct Stage {
   }
 };
 
-int ceil_log2_u64(uint64_t x) { return x <= 1 ? 0 : 64 - __builtin_clzll(x - 1); }
-
 }  // namespace
 }  // namespace ams
 

@@ -453,7 +453,7 @@ __global__ void __launch_bounds__(kThreads, VALS ? 2 : 4)
     uint32_t pk[kItems];
     auto classify_all = [&](auto full_tag) {
       constexpr bool FULL = decltype(full_tag)::value;
-      const uint32_t pos0 = (uint32_t)((int64_t)base + posbase);
+      [[maybe_unused]] const uint32_t pos0 = (uint32_t)((int64_t)base + posbase);
 #pragma unroll
       for (int i = 0; i < kItems; ++i) {
         const uint32_t e = w * (kItems * 32) + i * 32 + lane;
