@@ -407,8 +407,12 @@ __global__ void __launch_bounds__(kThreads, VALS ? 2 : 4)
   constexpr int kHists = MODE == kRankWarp ? kWarps : 1;
   uint64_t* keys_s = reinterpret_cast<uint64_t*>(smem);
   uint64_t* vals_s = keys_s + kTile;
+  // Per-bucket output bases of the tile (dst index - slot); the serial mode
+  // (> kSerialAbove buckets) has no room for them and adds run - start per key.
+  constexpr bool kAdj = MODE != kRankSerial;
   int64_t* run = reinterpret_cast<int64_t*>(smem + (VALS ? 16 : 8) * (size_t)kTile);
-  uint32_t* wh = reinterpret_cast<uint32_t*>(run + nb_stride);
+  int64_t* adj = run + nb_stride;
+  uint32_t* wh = reinterpret_cast<uint32_t*>(adj + (kAdj ? nb_stride : 0));
   uint32_t* btot = wh + (size_t)kHists * nb_stride;
   uint16_t* bkt_s = reinterpret_cast<uint16_t*>(btot + nb_stride);
   uint8_t* clsmem = reinterpret_cast<uint8_t*>(
@@ -518,6 +522,15 @@ __global__ void __launch_bounds__(kThreads, VALS ? 2 : 4)
         kr[i] = keys_s[e];
         if constexpr (VALS) vr[i] = vals_s[e];
       }
+      // Output base of every bucket run of this tile; advance the running offsets.
+      if constexpr (kAdj) {
+        for (int b = threadIdx.x; b < nb_stride; b += kThreads) {
+          const uint32_t st = btot[b];
+          const int64_t r = run[b];
+          adj[b] = r - (int64_t)st;
+          run[b] = r + (int64_t)((b + 1 < nb_stride ? btot[b + 1] : tcount) - st);
+        }
+      }
       __syncthreads();
 #pragma unroll
       for (int i = 0; i < kItems; ++i) {
@@ -533,13 +546,15 @@ __global__ void __launch_bounds__(kThreads, VALS ? 2 : 4)
     __syncthreads();
     for (uint32_t j = threadIdx.x; j < tcount; j += kThreads) {
       const uint32_t b = bkt_s[j];
-      const int64_t d = run[b] - (int64_t)btot[b] + (int64_t)j;
+      const int64_t d = (kAdj ? adj[b] : run[b] - (int64_t)btot[b]) + (int64_t)j;
       dst[d] = keys_s[j];
       if constexpr (VALS) dst_vals[d] = vals_s[j];
     }
     __syncthreads();
-    for (int b = threadIdx.x; b < nb_stride; b += kThreads)
-      run[b] += (int64_t)((b + 1 < nb_stride ? btot[b + 1] : tcount) - btot[b]);
+    if constexpr (!kAdj) {
+      for (int b = threadIdx.x; b < nb_stride; b += kThreads)
+        run[b] += (int64_t)((b + 1 < nb_stride ? btot[b + 1] : tcount) - btot[b]);
+    }
   }
 }
 
@@ -1374,6 +1389,7 @@ size_t scatter_smem_bytes(int nb_stride, int nspl_cap, int cells_cap, bool digit
   b += 8 * (size_t)nb_stride;                                         // running offsets
   b += 4 * (size_t)(mode == kRankWarp ? kWarps : 1) * nb_stride;      // bucket counters
   b += 4 * (size_t)nb_stride;                                         // tile bucket starts
+  if (mode != kRankSerial) b += 8 * (size_t)nb_stride;                // tile output bases
   b += 2 * (size_t)kTile;                                             // bucket ids
   b = (b + 15) & ~(size_t)15;
   if (!digit) b += tree_smem_bytes(nspl_cap, cells_cap) + 16;
