@@ -8,6 +8,9 @@
   (optionally with 8-byte payloads), no Python objects per element.
 * :func:`ams_sort_host` — host (numpy) buffers in, host buffers out; the
   end-to-end path (H2D, sort, D2H) a user without device buffers calls.
+* :class:`HostSortPipeline` — a stream of host batches sorted with the
+  copies overlapped: the H2D of batch i+1 and the D2H of batch i-1 run on
+  their own CUDA streams while batch i sorts.
 """
 
 from __future__ import annotations
@@ -66,6 +69,77 @@ def ams_sort_host(keys: np.ndarray, pe_sizes, params, seed, vals: np.ndarray | N
     out_k = res.keys.cpu().numpy()
     out_v = res.vals.cpu().numpy() if res.vals is not None else None
     return out_k, out_v, res.pe_sizes, res.reports
+
+
+class HostSortPipeline:
+    """Sort many same-shaped host batches (pinned CPU tensors of n 8-byte
+    keys, PE-major ``pe_sizes``) end to end with copy/compute overlap.
+
+    Two device input and two output buffers alternate: while batch i sorts
+    on the compute stream, batch i+1 is copied in on a copy stream and batch
+    i-1 is copied out on another (PCIe is full duplex, so both directions run
+    at once).  Every batch still makes the full trip host -> device -> host.
+    """
+
+    def __init__(self, n: int, pe_sizes, params, seed, key_kind="u64", device=None):
+        self.dev = torch.device("cuda", torch.cuda.current_device() if device is None else int(device))
+        self.n = int(n)
+        self.pe_sizes = np.asarray(pe_sizes, dtype=np.uint64)
+        if int(self.pe_sizes.sum()) != self.n:
+            raise ValueError("pe_sizes must sum to n")
+        self.params, self.seed, self.key_kind = params, seed, key_kind
+        mk = lambda: torch.empty(max(self.n, 1), dtype=torch.int64, device=self.dev)
+        self.d_in = [mk(), mk()]
+        self.d_out = [mk(), mk()]
+        self.s_in = torch.cuda.Stream(self.dev)
+        self.s_out = torch.cuda.Stream(self.dev)
+        self.ev_in = [torch.cuda.Event(), torch.cuda.Event()]      # H2D into d_in[j] done
+        self.ev_sorted = [torch.cuda.Event(), torch.cuda.Event()]  # sort reading d_in[j] done
+        self.ev_out = [torch.cuda.Event(), torch.cuda.Event()]     # D2H from d_out[j] done
+        self.sorter = get_sorter(self.dev)
+
+    def _h2d(self, j, host):
+        with torch.cuda.stream(self.s_in):
+            self.d_in[j][: self.n].copy_(host.view(torch.int64), non_blocking=True)
+            self.ev_in[j].record(self.s_in)
+
+    def run(self, inputs, outputs, done_events=None):
+        """Sort inputs[i] into outputs[i] (pinned CPU tensors); returns the
+        final per-PE sizes of every batch.  Blocks until the last D2H ends.
+        ``done_events`` (optional list) receives one timing event per batch,
+        recorded when its D2H has completed."""
+        if len(inputs) != len(outputs):
+            raise ValueError("one output per input")
+        for t in list(inputs) + list(outputs):
+            if t.device.type != "cpu" or t.numel() != self.n or t.element_size() != 8:
+                raise ValueError("inputs/outputs must be CPU tensors of n 8-byte keys")
+        comp = torch.cuda.current_stream(self.dev)
+        sizes = []
+        if inputs:
+            self._h2d(0, inputs[0])
+        for i, (hin, hout) in enumerate(zip(inputs, outputs)):
+            j = i % 2
+            if i + 1 < len(inputs):
+                # d_in[1 - j] was last read by sort(i - 1).
+                self.s_in.wait_event(self.ev_sorted[1 - j])
+                self._h2d(1 - j, inputs[i + 1])
+            comp.wait_event(self.ev_in[j])
+            comp.wait_event(self.ev_out[j])  # d_out[j] was last read by D2H(i - 2)
+            res = self.sorter.sort(self.d_in[j][: self.n], self.pe_sizes, self.params, self.seed,
+                                   out=self.d_out[j][: self.n], key_kind=self.key_kind,
+                                   with_stats=False)
+            self.ev_sorted[j].record(comp)
+            sizes.append(res.pe_sizes)
+            with torch.cuda.stream(self.s_out):
+                self.s_out.wait_event(self.ev_sorted[j])
+                hout.view(torch.int64).copy_(self.d_out[j][: self.n], non_blocking=True)
+                self.ev_out[j].record(self.s_out)
+                if done_events is not None:
+                    ev = torch.cuda.Event(enable_timing=True)
+                    ev.record(self.s_out)
+                    done_events.append(ev)
+        self.s_out.synchronize()
+        return sizes
 
 
 def _flatten(data, p):

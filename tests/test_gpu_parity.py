@@ -253,3 +253,22 @@ def test_distributed_path_world1_nccl():
         assert [int(x) for x in sizes] == list(ref.pe_sizes)
     finally:
         dist.destroy_process_group()
+
+
+def test_host_pipeline_batches(api):
+    """HostSortPipeline: several host batches with overlapped copies, each
+    equal to the one-shot sort (and to numpy.sort)."""
+    from paper_1410_6754_b200 import AmsParams, SeedSpec
+    p, npe = 64, 5000
+    n = p * npe
+    rng = np.random.default_rng(5)
+    batches = [rng.integers(0, 2**64, n, dtype=np.uint64) for _ in range(3)]
+    ins = [torch.from_numpy(b.view(np.int64).copy()).pin_memory() for b in batches]
+    outs = [torch.empty(n, dtype=torch.int64).pin_memory() for _ in batches]
+    pipe = api.HostSortPipeline(n, [npe] * p, AmsParams((8, 8), None, 16, 0.1),
+                                SeedSpec(1, "algo/rep0"))
+    sizes = pipe.run(ins, outs)
+    for b, o, sz in zip(batches, outs, sizes):
+        assert np.array_equal(o.numpy().view(np.uint64), np.sort(b))
+        ref = O.ams_sort(b, [npe] * p, (8, 8), None, 16, 0.1, 1, "algo/rep0")
+        assert [int(x) for x in sz] == list(ref.pe_sizes)
