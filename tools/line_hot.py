@@ -22,6 +22,8 @@ for r in rows:
         continue
     # cuda rows: Line No, Source, then sass columns
     line, src = r[0], r[1]
+    if not line.isdigit():  # SASS rows under a source line (cuda,sass CSV)
+        continue
     try:
         ie = int(r[hdr.index("Instructions Executed")] or 0)
         ss = int(r[hdr.index("Warp Stall Sampling (All Samples)")] or 0)

@@ -1,0 +1,16 @@
+#!/bin/bash
+# On the GPU box: launch list of one bench run + ncu --set full of the second
+# sort's hot kernels (tools/profile_case.py).  Outputs under gpurun_out/$1/.
+#   tools/ncu_round.sh TAG [log2n]
+set -e
+cd "$(dirname "$0")/.."
+tag=${1:-prof}; log2n=${2:-28}
+out=gpurun_out/$tag; mkdir -p $out
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+  --log-file $out/launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline \
+  > $out/ncu_launches.log 2>&1 || echo "launch list failed"
+timeout 900 ncu --set full --clock-control none --import-source on \
+  -k regex:"k_hist|k_scatter|k_smem_sort" --launch-skip 7 --launch-count 7 \
+  -o $out/full -f python tools/profile_case.py $log2n 2 > $out/ncu_full.log 2>&1 || echo "full failed"
+ncu -i $out/full.ncu-rep --page raw --csv > $out/full_raw.csv 2>/dev/null || true
+ls -la $out
