@@ -67,6 +67,7 @@ __host__ __device__ inline uint64_t digit_mult(uint64_t range, uint32_t nb) {
 // Final-sort overflow record: a cell too large for the shared-memory sort.
 struct OverflowRec {
   uint64_t off, count, lo, hi;
+  uint64_t out;  // output index of the cell (== off except for fixed-capacity cells)
 };
 
 __host__ __device__ inline int bit_length64(uint64_t x) {

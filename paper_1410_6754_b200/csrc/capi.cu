@@ -4,6 +4,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -155,6 +156,11 @@ struct ams_ctx {
   HostBuf h_hist;
   // final sort
   DevBuf dcls, ovf, ovf_count, fb, fb_count, groups, ngroups_d;
+  // bucket-major final sort (fixed-capacity cells)
+  DevBuf fx_scratch, fx_fill, fx_ovf, fx_base, fx_cnt, fx_seg;
+  Stage st_fixed;
+  uint64_t fixed_segments = 0, fixed_overflow_segments = 0;
+  bool bm_final = true;  // AMS_FINAL_BM=0 keeps the (g(b), j, b) last level + PE digit partition
   HostBuf h_small;
   uint64_t overflow_cells = 0, fallback_cells = 0;
   // one-call driver (ams_sort_run): workspace and the last run's level records
@@ -292,6 +298,11 @@ int run_histogram(ams_ctx* c, const void* src, int kind, bool digit, const SegMe
   return AMS_OK;
 }
 
+int level_scatter_impl(ams_ctx_t* c, const void* src, const void* src_vals, int key_kind,
+                       void* dst, void* dst_vals, int r, const uint64_t* h_boundaries,
+                       const uint64_t* h_group_dst_start, int child_first, int child_count,
+                       bool bucket_major);
+
 }  // namespace
 
 extern "C" {
@@ -309,6 +320,7 @@ int ams_ctx_create(int device, void* stream, ams_ctx_t** out) {
   ams_ctx* c = new ams_ctx();
   c->device = device;
   c->stream = static_cast<cudaStream_t>(stream);
+  if (const char* e = std::getenv("AMS_FINAL_BM")) c->bm_final = std::atoi(e) != 0;
   *out = c;
   return AMS_OK;
 }
@@ -319,13 +331,14 @@ int ams_ctx_destroy(ams_ctx_t* c) {
   cudaStreamSynchronize(c->stream);
   resolve_timing(c);
   for (cudaEvent_t e : c->free_events) cudaEventDestroy(e);
-  for (Stage* s : {&c->st_sample, &c->st_split, &c->st_level, &c->st_scatter, &c->st_final})
+  for (Stage* s : {&c->st_sample, &c->st_split, &c->st_level, &c->st_scatter, &c->st_final, &c->st_fixed})
     s->release();
   for (DevBuf* b : {&c->blobs, &c->sorted_keys, &c->sorted_pos, &c->sample_idx, &c->bounds[0], &c->bounds[1],
                     &c->chunk_tot, &c->seg_hist, &c->cell_base, &c->pieces, &c->minmax, &c->dcls,
                     &c->ovf, &c->ovf_count, &c->fb, &c->fb_count, &c->groups, &c->ngroups_d,
                     &c->ids, &c->work[0], &c->work[1], &c->work_v[0], &c->work_v[1], &c->s_keys,
-                    &c->s_pos})
+                    &c->s_pos, &c->fx_scratch, &c->fx_fill, &c->fx_ovf, &c->fx_base, &c->fx_cnt,
+                    &c->fx_seg})
     b->release();
   c->h_hist.release();
   c->h_small.release();
@@ -559,6 +572,20 @@ int ams_level_classify(ams_ctx_t* c, const void* src, int key_kind, int nseg,
 int ams_level_scatter(ams_ctx_t* c, const void* src, const void* src_vals, int key_kind,
                       void* dst, void* dst_vals, int r, const uint64_t* h_boundaries,
                       const uint64_t* h_group_dst_start, int child_first, int child_count) {
+  return level_scatter_impl(c, src, src_vals, key_kind, dst, dst_vals, r, h_boundaries,
+                            h_group_dst_start, child_first, child_count, false);
+}
+
+}  // extern "C"
+
+namespace {
+
+// bucket_major (keys-only last level of ams_sort_run): cells in (g, b, j)
+// order instead of (g(b), j, b) — same children extents, buckets contiguous.
+int level_scatter_impl(ams_ctx_t* c, const void* src, const void* src_vals, int key_kind,
+                       void* dst, void* dst_vals, int r, const uint64_t* h_boundaries,
+                       const uint64_t* h_group_dst_start, int child_first, int child_count,
+                       bool bucket_major) {
   if (!c) return set_error(AMS_EINVAL, "null context");
   if (c->nseg == 0) return set_error(AMS_EINVAL, "ams_level_classify must run first");
   if (r < 1 || !h_boundaries || !h_group_dst_start) return set_error(AMS_EINVAL, "bad plan");
@@ -590,8 +617,12 @@ int ams_level_scatter(ams_ctx_t* c, const void* src, const void* src_vals, int k
   AMS_CK(c->cell_base.ensure(sizeof(uint64_t) * (size_t)c->nseg * c->nb_stride));
   {
     KTimer kt(c, AMS_KCAT_CELLBASE, 12.0 * c->nseg * c->nb_stride);
-    AMS_CK(launch_cell_base(c->stream, c->seg_hist.as<uint32_t>(), c->nb_stride, gm, G, r,
-                            c->pieces.as<uint64_t>(), c->cell_base.as<uint64_t>()));
+    if (bucket_major && !c->level_stable && !src_vals)
+      AMS_CK(launch_cell_base_bm(c->stream, c->seg_hist.as<uint32_t>(), c->nb_stride, gm, G,
+                                 c->cell_base.as<uint64_t>()));
+    else
+      AMS_CK(launch_cell_base(c->stream, c->seg_hist.as<uint32_t>(), c->nb_stride, gm, G, r,
+                              c->pieces.as<uint64_t>(), c->cell_base.as<uint64_t>()));
   }
   {
     KTimer kt(c, c->level_stable ? AMS_KCAT_SCATTER : AMS_KCAT_SCATTER_U,
@@ -616,6 +647,10 @@ int ams_level_scatter(ams_ctx_t* c, const void* src, const void* src_vals, int k
   c->launches += 3;
   return AMS_OK;
 }
+
+}  // namespace
+
+extern "C" {
 
 int ams_get_minmax(ams_ctx_t* c, uint64_t out[2]) {
   if (!c || !out) return set_error(AMS_EINVAL, "null argument");
@@ -671,66 +706,25 @@ int sort_cells(ams_ctx* c, const void* src, const void* src_vals, void* out, voi
   return AMS_OK;
 }
 
-}  // namespace
-
-int ams_final_sort(ams_ctx_t* c, void* src, void* src_vals, void* tmp, void* tmp_vals, void* out,
-                   void* out_vals, int key_kind, int nseg, const uint64_t* h_seg_off,
-                   const uint64_t* h_seg_len) {
-  if (!c) return set_error(AMS_EINVAL, "null context");
-  if (nseg < 0 || (nseg > 0 && (!h_seg_off || !h_seg_len))) return set_error(AMS_EINVAL, "bad segments");
+// Exact digit-partition rounds over segments that exceed shared memory:
+// histogram + stable scatter cur -> oth, then per-cell sorts into `out`;
+// cells still too big go round again with their exact key range.  Key
+// bounds of the first round come from the last level's bounds (`sel` =
+// final segment index of every entry) or, without `sel`, from lo/hi.
+int partition_rounds(ams_ctx* c, void* src, void* src_vals, void* tmp, void* tmp_vals, void* out,
+                     void* out_vals, int key_kind, std::vector<uint64_t>& b_off,
+                     std::vector<uint64_t>& b_len, std::vector<uint64_t>& b_lo,
+                     std::vector<uint64_t>& b_hi, const std::vector<int32_t>* sel) {
   const bool vals = src_vals != nullptr;
-  if (vals && (!tmp_vals || !out_vals)) return set_error(AMS_EINVAL, "missing value buffers");
-  AMS_CK(cudaSetDevice(c->device));
-  // Digit cells average ~78% of the shared-memory capacity: uniform keys
-  // never overflow it while the per-cell work stays large.
   constexpr uint64_t kTargetCell = AMS_SMEM_SORT_CAP * 78 / 100;
-  std::vector<uint64_t> s_off, s_len, b_off, b_len, b_lo, b_hi;
-  std::vector<int32_t> b_seg;
-  uint64_t total = 0, max_big = 0, small_n = 0;
-  for (int s = 0; s < nseg; ++s) {
-    total += h_seg_len[s];
-    if (h_seg_len[s] == 0) continue;
-    if (h_seg_len[s] <= (uint64_t)AMS_SMEM_SORT_CAP) {
-      s_off.push_back(h_seg_off[s]);
-      s_len.push_back(h_seg_len[s]);
-      small_n += h_seg_len[s];
-    } else {
-      b_off.push_back(h_seg_off[s]);
-      b_len.push_back(h_seg_len[s]);
-      b_seg.push_back(s);
-      max_big = std::max(max_big, h_seg_len[s]);
-    }
-  }
-  if (!b_off.empty() && c->bounds[c->bcur].cap < 16 * (size_t)nseg)
-    return set_error(AMS_EINVAL, "final segments need the key bounds of the last level");
-  const uint64_t rec_cap = total / (AMS_SMEM_SORT_CAP / 2) + 64;
-  AMS_CK(c->ovf.ensure(sizeof(OverflowRec) * rec_cap));
-  AMS_CK(c->fb.ensure(sizeof(OverflowRec) * rec_cap));
-  AMS_CK(c->ovf_count.ensure(sizeof(unsigned int)));
-  AMS_CK(c->fb_count.ensure(sizeof(unsigned int)));
-  AMS_CK(c->h_small.ensure(4096));
-  AMS_CK(cudaMemsetAsync(c->ovf_count.p, 0, sizeof(unsigned int), c->stream));
+  uint64_t max_big = 0;
+  for (uint64_t v : b_len) max_big = std::max(max_big, v);
   Stage& st = c->st_final;
-  // 1. Segments that fit in shared memory: sort straight into `out`.
-  if (!s_off.empty()) {
-    Stage& ss = c->st_sample;  // free after the levels
-    ss.reset();
-    const size_t oo = ss.put(s_off), ol = ss.put(s_len);
-    AMS_CK(ss.upload(c->stream));
-    CellSource cs{};
-    cs.mode = 1;
-    cs.seg_off = ss.dev<uint64_t>(oo);
-    cs.seg_len = ss.dev<uint64_t>(ol);
-    int rc = sort_cells(c, src, src_vals, out, out_vals, key_kind, cs, s_off.size(), small_n);
-    if (rc) return rc;
-  }
-  // 2. Large segments: digit partition src -> tmp, then per-cell sorts;
-  //    cells still above shared memory go round again (tmp -> src -> ...).
   void* cur = src;
   void* cur_v = src_vals;
   void* oth = tmp;
   void* oth_v = tmp_vals;
-  bool first_round = true;
+  bool first_round = sel != nullptr;
   int rounds = 0;
   while (!b_off.empty()) {
     // Every round splits each non-constant cell into >= 2 non-empty cells,
@@ -750,7 +744,7 @@ int ams_final_sort(ams_ctx_t* c, void* src, void* src_vals, void* tmp, void* tmp
     size_t ob;
     if (first_round) {
       // Bounds of the final segments that need a partition (segment order).
-      ob = sf.put(b_seg);
+      ob = sf.put(*sel);
     } else {
       std::vector<uint64_t> lohi(2 * (size_t)nb_seg);
       for (int i = 0; i < nb_seg; ++i) { lohi[2 * i] = b_lo[i]; lohi[2 * i + 1] = b_hi[i]; }
@@ -824,6 +818,195 @@ int ams_final_sort(ams_ctx_t* c, void* src, void* src_vals, void* tmp, void* tmp
   return AMS_OK;
 }
 
+// Final sort after a bucket-major keys-only last level: every non-empty
+// bucket (g, b) of the last level is a segment at bk_off with bk_len keys.
+// Buckets that fit in shared memory are sorted straight into `out`; the
+// others are split into fixed-capacity digit cells in scratch
+// (k_scatter_fixed: no histogram pass), whose sorts write `out`.  Buckets
+// whose cells overflowed go through the exact partition rounds from `src`.
+int final_sort_bm(ams_ctx* c, void* src, void* tmp, void* out, int key_kind,
+                  const std::vector<uint64_t>& bk_off, const std::vector<uint64_t>& bk_len,
+                  const std::vector<int32_t>& bk_g, const std::vector<int32_t>& bk_b,
+                  const uint64_t* d_group_bounds) {
+  constexpr uint64_t kCap = AMS_SMEM_SORT_CAP;
+  // Cells average ~78% of capacity: uniform keys never overflow.
+  constexpr uint64_t kTarget = kCap * 78 / 100;
+  constexpr uint64_t kMaxDigits = AMS_MAX_BUCKETS / 2;
+  std::vector<uint64_t> s_off, s_len, f_off, f_len;
+  std::vector<int32_t> f_gb;
+  std::vector<uint32_t> cell0{0};
+  uint64_t total = 0, small_n = 0, fixed_n = 0;
+  int max_nb = 2;
+  for (size_t i = 0; i < bk_off.size(); ++i) {
+    const uint64_t len = bk_len[i];
+    total += len;
+    if (len == 0) continue;
+    if (len <= kCap) {
+      s_off.push_back(bk_off[i]);
+      s_len.push_back(len);
+      small_n += len;
+      continue;
+    }
+    const uint64_t d = std::min<uint64_t>(kMaxDigits, std::max<uint64_t>(2, (len + kTarget - 1) / kTarget));
+    f_off.push_back(bk_off[i]);
+    f_len.push_back(len);
+    f_gb.push_back(bk_g[i]);
+    f_gb.push_back(bk_b[i]);
+    f_gb.push_back((int32_t)d);
+    cell0.push_back(cell0.back() + (uint32_t)d);
+    max_nb = std::max(max_nb, (int)d);
+    fixed_n += len;
+  }
+  const int nseg = (int)f_off.size();
+  const uint64_t ncells = cell0.back();
+  const uint64_t rec_cap = std::max<uint64_t>(total / (kCap / 2), ncells) + 64;
+  AMS_CK(c->ovf.ensure(sizeof(OverflowRec) * rec_cap));
+  AMS_CK(c->fb.ensure(sizeof(OverflowRec) * rec_cap));
+  AMS_CK(c->ovf_count.ensure(sizeof(unsigned int)));
+  AMS_CK(c->fb_count.ensure(sizeof(unsigned int)));
+  AMS_CK(c->h_small.ensure(4096));
+  AMS_CK(cudaMemsetAsync(c->ovf_count.p, 0, sizeof(unsigned int), c->stream));
+  if (!s_off.empty()) {
+    Stage& ss = c->st_sample;  // free after the levels
+    ss.reset();
+    const size_t oo = ss.put(s_off), ol = ss.put(s_len);
+    AMS_CK(ss.upload(c->stream));
+    CellSource cs{};
+    cs.mode = 1;
+    cs.seg_off = ss.dev<uint64_t>(oo);
+    cs.seg_len = ss.dev<uint64_t>(ol);
+    int rc = sort_cells(c, src, nullptr, out, nullptr, key_kind, cs, s_off.size(), small_n);
+    if (rc) return rc;
+  }
+  if (nseg == 0) return AMS_OK;
+  c->fixed_segments += (uint64_t)nseg;
+  Stage& sx = c->st_fixed;
+  sx.reset();
+  const size_t o_gb = sx.put(f_gb), o_c0 = sx.put(cell0), o_off = sx.put(f_off);
+  AMS_CK(sx.upload(c->stream));
+  std::vector<int32_t> idx(nseg);
+  for (int i = 0; i < nseg; ++i) idx[i] = i;
+  SegMeta m;
+  uint64_t nchunks;
+  AMS_CK(upload_segments(c->st_final, c->stream, f_off.data(), f_len.data(), idx.data(), nseg, nullptr,
+                         0, &m, &nchunks));
+  AMS_CK(c->dcls.ensure(sizeof(DigitCls) * (size_t)nseg));
+  AMS_CK(c->fx_fill.ensure(4 * (size_t)ncells));
+  AMS_CK(c->fx_ovf.ensure(4 * (size_t)nseg));
+  AMS_CK(c->fx_base.ensure(8 * (size_t)ncells));
+  AMS_CK(c->fx_cnt.ensure(4 * (size_t)ncells));
+  AMS_CK(c->fx_seg.ensure(4 * (size_t)ncells));
+  AMS_CK(c->fx_scratch.ensure(8 * kCap * (size_t)ncells));
+  AMS_CK(cudaMemsetAsync(c->fx_fill.p, 0, 4 * (size_t)ncells, c->stream));
+  AMS_CK(cudaMemsetAsync(c->fx_ovf.p, 0, 4 * (size_t)nseg, c->stream));
+  {
+    KTimer kt(c, AMS_KCAT_RANGES, 0.0);
+    AMS_CK(launch_bucket_ranges(c->stream, c->blobs.as<uint8_t>(), d_group_bounds, sx.dev<int32_t>(o_gb),
+                                nseg, c->dcls.as<DigitCls>()));
+  }
+  {
+    KTimer kt(c, AMS_KCAT_FSCATTER, 16.0 * fixed_n);
+    AMS_CK(launch_scatter_fixed(c->stream, src, AMS_KEY_U64, c->fx_scratch.p, m, nchunks, max_nb,
+                                c->dcls.as<DigitCls>(), sx.dev<uint32_t>(o_c0), c->fx_fill.as<uint32_t>(),
+                                c->fx_ovf.as<uint32_t>()));
+  }
+  {
+    KTimer kt(c, AMS_KCAT_CELLBASE, 16.0 * ncells);
+    AMS_CK(launch_fixed_cells(c->stream, c->fx_fill.as<uint32_t>(), sx.dev<uint32_t>(o_c0),
+                              sx.dev<uint64_t>(o_off), c->fx_ovf.as<uint32_t>(), nseg,
+                              c->fx_base.as<uint64_t>(), c->fx_cnt.as<uint32_t>(), c->fx_seg.as<uint32_t>()));
+  }
+  c->launches += 3;
+  CellSource cs{};
+  cs.mode = 3;
+  cs.cell_base = c->fx_base.as<uint64_t>();
+  cs.cell_cnt = c->fx_cnt.as<uint32_t>();
+  cs.dcls = c->dcls.as<DigitCls>();
+  cs.cell_seg = c->fx_seg.as<uint32_t>();
+  cs.cell0 = sx.dev<uint32_t>(o_c0);
+  int rc = sort_cells(c, c->fx_scratch.p, nullptr, out, nullptr, key_kind, cs, ncells, fixed_n);
+  if (rc) return rc;
+  // Overflowed buckets (sort_cells synced): exact partition rounds from src.
+  std::vector<uint32_t> flags(nseg);
+  AMS_CK(cudaMemcpy(flags.data(), c->fx_ovf.p, 4 * (size_t)nseg, cudaMemcpyDeviceToHost));
+  std::vector<uint64_t> o_off2, o_len2, o_lo, o_hi;
+  std::vector<DigitCls> dc;
+  for (int i = 0; i < nseg; ++i) {
+    if (!flags[i]) continue;
+    if (dc.empty()) {
+      dc.resize(nseg);
+      AMS_CK(cudaMemcpy(dc.data(), c->dcls.p, sizeof(DigitCls) * (size_t)nseg, cudaMemcpyDeviceToHost));
+    }
+    o_off2.push_back(f_off[i]);
+    o_len2.push_back(f_len[i]);
+    o_lo.push_back(dc[i].lo);
+    o_hi.push_back(dc[i].hi);
+  }
+  c->fixed_overflow_segments += o_off2.size();
+  if (!o_off2.empty())
+    return partition_rounds(c, src, nullptr, tmp, nullptr, out, nullptr, key_kind, o_off2, o_len2, o_lo,
+                            o_hi, nullptr);
+  return AMS_OK;
+}
+
+}  // namespace
+
+int ams_final_sort(ams_ctx_t* c, void* src, void* src_vals, void* tmp, void* tmp_vals, void* out,
+                   void* out_vals, int key_kind, int nseg, const uint64_t* h_seg_off,
+                   const uint64_t* h_seg_len) {
+  if (!c) return set_error(AMS_EINVAL, "null context");
+  if (nseg < 0 || (nseg > 0 && (!h_seg_off || !h_seg_len))) return set_error(AMS_EINVAL, "bad segments");
+  const bool vals = src_vals != nullptr;
+  if (vals && (!tmp_vals || !out_vals)) return set_error(AMS_EINVAL, "missing value buffers");
+  AMS_CK(cudaSetDevice(c->device));
+  std::vector<uint64_t> s_off, s_len, b_off, b_len, b_lo, b_hi;
+  std::vector<int32_t> b_seg;
+  uint64_t total = 0, small_n = 0;
+  for (int s = 0; s < nseg; ++s) {
+    total += h_seg_len[s];
+    if (h_seg_len[s] == 0) continue;
+    if (h_seg_len[s] <= (uint64_t)AMS_SMEM_SORT_CAP) {
+      s_off.push_back(h_seg_off[s]);
+      s_len.push_back(h_seg_len[s]);
+      small_n += h_seg_len[s];
+    } else {
+      b_off.push_back(h_seg_off[s]);
+      b_len.push_back(h_seg_len[s]);
+      b_seg.push_back(s);
+    }
+  }
+  if (!b_off.empty() && c->bounds[c->bcur].cap < 16 * (size_t)nseg)
+    return set_error(AMS_EINVAL, "final segments need the key bounds of the last level");
+  const uint64_t rec_cap = total / (AMS_SMEM_SORT_CAP / 2) + 64;
+  AMS_CK(c->ovf.ensure(sizeof(OverflowRec) * rec_cap));
+  AMS_CK(c->fb.ensure(sizeof(OverflowRec) * rec_cap));
+  AMS_CK(c->ovf_count.ensure(sizeof(unsigned int)));
+  AMS_CK(c->fb_count.ensure(sizeof(unsigned int)));
+  AMS_CK(c->h_small.ensure(4096));
+  AMS_CK(cudaMemsetAsync(c->ovf_count.p, 0, sizeof(unsigned int), c->stream));
+  // 1. Segments that fit in shared memory: sort straight into `out`.
+  if (!s_off.empty()) {
+    Stage& ss = c->st_sample;  // free after the levels
+    ss.reset();
+    const size_t oo = ss.put(s_off), ol = ss.put(s_len);
+    AMS_CK(ss.upload(c->stream));
+    CellSource cs{};
+    cs.mode = 1;
+    cs.seg_off = ss.dev<uint64_t>(oo);
+    cs.seg_len = ss.dev<uint64_t>(ol);
+    int rc = sort_cells(c, src, src_vals, out, out_vals, key_kind, cs, s_off.size(), small_n);
+    if (rc) return rc;
+  }
+  // 2. Large segments: digit partition src -> tmp, then per-cell sorts;
+  //    cells still above shared memory go round again (tmp -> src -> ...).
+  if (!b_off.empty()) {
+    int rc = partition_rounds(c, src, src_vals, tmp, tmp_vals, out, out_vals, key_kind, b_off, b_len,
+                              b_lo, b_hi, &b_seg);
+    if (rc) return rc;
+  }
+  return AMS_OK;
+}
+
 int ams_final_sort_stats(ams_ctx_t* c, uint64_t out[2]) {
   if (!c || !out) return set_error(AMS_EINVAL, "null argument");
   out[0] = c->overflow_cells;
@@ -889,6 +1072,7 @@ int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* p
   std::vector<int32_t> gf{0}, gn{p};
   c->run_levels.assign(k, ams_ctx::LevelRec{});
   int rc;
+  bool used_bm = false;
   for (int lv = 0; lv < k; ++lv) {
     const int r = prm->group_counts[lv];
     const int G = (int)gf.size();
@@ -960,9 +1144,11 @@ int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* p
     for (int g = 0; g < G; ++g) dst_start[g] = offs[gf[g]];
     void* dst = c->work[lv % 2].p;
     void* dst_v = with_vals ? c->work_v[lv % 2].p : nullptr;
-    if ((rc = ams_level_scatter(c, src, src_v, src_kind, dst, dst_v, r, rec.boundaries.data(),
-                                dst_start.data(), 0, G * r)))
+    const bool bm = last && !with_vals && c->bm_final;
+    if ((rc = level_scatter_impl(c, src, src_v, src_kind, dst, dst_v, r, rec.boundaries.data(),
+                                 dst_start.data(), 0, G * r, bm)))
       return rc;
+    used_bm = bm;
     // Level report (ams.py:258-268, 294-308).
     if (reports) {
       ams_level_report_t& rp = reports[lv];
@@ -1003,9 +1189,31 @@ int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* p
   for (int i = 0; i < p; ++i) offs[i + 1] = offs[i] + sizes[i];
   void* tmp = c->work[k % 2].p;
   void* tmp_v = with_vals ? c->work_v[k % 2].p : nullptr;
-  if ((rc = ams_final_sort(c, const_cast<void*>(src), const_cast<void*>(src_v), tmp, tmp_v, dst_out,
-                           dst_out_v, prm->key_kind, p, offs.data(), sizes.data())))
+  if (used_bm) {
+    // Buckets of the bucket-major last level, in output order.
+    const ams_ctx::LevelRec& L = c->run_levels[k - 1];
+    std::vector<uint64_t> bo, bl;
+    std::vector<int32_t> bg, bb;
+    uint64_t at = 0;
+    for (int g = 0; g < L.G; ++g) {
+      for (int b = 0; b < L.nb[g]; ++b) {
+        uint64_t h = 0;
+        for (int j = 0; j < L.group_npe[g]; ++j)
+          h += L.hist[(size_t)(L.group_first[g] + j) * L.nb_stride + b];
+        bo.push_back(at);
+        bl.push_back(h);
+        bg.push_back(g);
+        bb.push_back(b);
+        at += h;
+      }
+    }
+    if ((rc = final_sort_bm(c, const_cast<void*>(src), tmp, dst_out, prm->key_kind, bo, bl, bg, bb,
+                            c->bounds[1 - c->bcur].as<uint64_t>())))
+      return rc;
+  } else if ((rc = ams_final_sort(c, const_cast<void*>(src), const_cast<void*>(src_v), tmp, tmp_v, dst_out,
+                                  dst_out_v, prm->key_kind, p, offs.data(), sizes.data()))) {
     return rc;
+  }
   c->run_final_sizes = sizes;
   if (out_pe_sizes) std::memcpy(out_pe_sizes, sizes.data(), sizeof(uint64_t) * p);
   return AMS_OK;

@@ -306,6 +306,38 @@ __global__ void __launch_bounds__(256) k_cell_base(const uint32_t* __restrict__ 
   }
 }
 
+// Bucket-major variant for a keys-only last level (only PE membership
+// matters there, F7): cell (j, b) of group g starts at dst_start + sum of
+// the group's earlier buckets + bucket b of earlier segments, so every
+// bucket is contiguous and the children (consecutive bucket ranges) keep
+// the same extents as in the (g(b), j, b) order.  One CTA per group.
+__global__ void __launch_bounds__(256) k_cell_base_bm(const uint32_t* __restrict__ seg_hist, int nb_stride,
+                                                      GroupMeta gm, uint64_t* __restrict__ cell_base) {
+  __shared__ uint64_t tot[AMS_MAX_BUCKETS];
+  const int g = blockIdx.x;
+  const int first = gm.first[g], P = gm.nseg[g];
+  const int nb = nb_stride;  // buckets beyond a group's count are empty columns
+  // Column sums (bucket totals of the group).
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+    uint64_t sum = 0;
+    for (int j = 0; j < P; ++j) sum += seg_hist[(uint64_t)(first + j) * nb_stride + b];
+    tot[b] = sum;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t acc = gm.dst_start[g];
+    for (int b = 0; b < nb; ++b) { const uint64_t t = tot[b]; tot[b] = acc; acc += t; }
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+    uint64_t run = tot[b];
+    for (int j = 0; j < P; ++j) {
+      cell_base[(uint64_t)(first + j) * nb_stride + b] = run;
+      run += seg_hist[(uint64_t)(first + j) * nb_stride + b];
+    }
+  }
+}
+
 // Digit partition: cell (s, d) starts at off[s] + sum of earlier digits.
 __global__ void k_digit_base(const uint32_t* __restrict__ seg_hist, int nb_stride, SegMeta m,
                              uint64_t* __restrict__ cell_base) {
@@ -733,6 +765,198 @@ __global__ void __launch_bounds__(kThreadsU, 2)
   }
 }
 
+// Fixed-capacity digit partition (keys only, the final sort of a bucket-major
+// last level): segments are the last level's buckets, each split into nb_s
+// digit cells of capacity kSortCap in `dst` (cell ci at dst[ci * kSortCap]).
+// No histogram pass: every (tile, digit) run reserves its room with one
+// global atomic on the cell's fill counter, so a cell's keys land in any
+// order (only membership matters: F7).  A cell that would exceed its
+// capacity flags its segment; the host re-partitions such segments exactly
+// from `src`, which this kernel does not modify.
+template <int KIND>
+__global__ void __launch_bounds__(kThreadsU, 2)
+    k_scatter_fixed(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst, SegMeta m,
+                    const DigitCls* __restrict__ dcls, const uint32_t* __restrict__ cell0,
+                    uint32_t* __restrict__ fill, uint32_t* __restrict__ seg_ovf) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ int s_seg;
+  __shared__ uint32_t s_scan[kWarpsU + 1];
+  __shared__ uint32_t s_clip;
+  __shared__ __align__(8) uint64_t s_bar[2];
+  constexpr int kBuf = kTile + 2;
+  uint64_t* buf0 = reinterpret_cast<uint64_t*>(smem);
+  const int tid = threadIdx.x;
+  const uint64_t c = blockIdx.x;
+  if (tid == 0) {
+    s_seg = upper_bound_u64(m.chunk_prefix, m.nseg + 1, c) - 1;
+    s_clip = 0;
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int s = s_seg;
+  DigitView dv;
+  dv.c = dcls[s];
+  const int nb = (int)dv.c.nb;
+  const int per = (nb + kThreadsU - 1) / kThreadsU | 1;
+  const int nbp = per * kThreadsU;
+  int64_t* adj = reinterpret_cast<int64_t*>(buf0 + 2 * kBuf);  // this tile: dst index - slot
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(adj + nbp);       // counts, then tile starts
+  int32_t* lim = reinterpret_cast<int32_t*>(cnt + nbp);         // writable keys of the run
+  uint16_t* bkt = reinterpret_cast<uint16_t*>(lim + nbp);
+  const uint64_t seg_off = m.off[s];
+  const uint64_t first = (c - m.chunk_prefix[s]) * (uint64_t)kChunk;
+  const uint64_t last = min(first + (uint64_t)kChunk, m.len[s]);
+  const int ntiles = (int)((last - first + kTile - 1) / kTile);
+  const uint64_t cbase = cell0[s];
+  auto issue = [&](int t) {
+    const uint64_t base = seg_off + first + (uint64_t)t * kTile;
+    const uint32_t tc = (uint32_t)min((uint64_t)kTile, last - first - (uint64_t)t * kTile);
+    const uint32_t h = (uint32_t)(base & 1);
+    const uint64_t b0 = base + h, b1 = (base + tc) & ~1ULL;
+    const uint32_t bytes = b1 > b0 ? (uint32_t)(b1 - b0) * 8 : 0;
+    bulk_load(buf0 + (t & 1) * kBuf + 2 * h, src + b0, bytes, &s_bar[t & 1]);
+  };
+  if (tid == 0) issue(0);
+  for (int b = tid; b < nbp; b += kThreadsU) cnt[b] = 0;
+  const int w = tid >> 5, lane = tid & 31;
+  __syncthreads();
+  for (int t = 0; t < ntiles; ++t) {
+    uint64_t* buf = buf0 + (t & 1) * kBuf;
+    const uint64_t base = seg_off + first + (uint64_t)t * kTile;
+    const uint32_t tc = (uint32_t)min((uint64_t)kTile, last - first - (uint64_t)t * kTile);
+    const uint32_t h = (uint32_t)(base & 1);
+    const uint32_t e_end = (uint32_t)(((base + tc) & ~1ULL) - base);
+    if (tid == 0 && t + 1 < ntiles) {
+      fence_proxy_async();
+      issue(t + 1);
+    }
+    mbar_wait(&s_bar[t & 1], (uint32_t)(t >> 1) & 1u);
+    uint64_t kr[kItemsU];
+    uint32_t pk[kItemsU];
+#pragma unroll
+    for (int i = 0; i < kItemsU; ++i) {
+      const uint32_t e = w * (kItemsU * 32) + i * 32 + lane;
+      pk[i] = kInvalid;
+      if (e < tc) {
+        const uint64_t key = to_ordered<KIND>((e >= h && e < e_end) ? buf[e + h] : src[base + e]);
+        const uint32_t b = dv.classify(key, 0);
+        kr[i] = key;
+        pk[i] = (b << 16) | atomicAdd(&cnt[b], 1u);
+      }
+    }
+    __syncthreads();
+    {
+      const int b0 = tid * per;
+      uint32_t sum = 0;
+      for (int j = 0; j < per; ++j) sum += cnt[b0 + j];
+      const uint32_t inc = warp_incl_scan(sum);
+      if (lane == 31) s_scan[w] = inc;
+      scan_warp_totals<kThreadsU>(s_scan);
+      uint32_t start = s_scan[w] + inc - sum;
+      for (int j = 0; j < per; ++j) {
+        const int b = b0 + j;
+        const uint32_t v = cnt[b];
+        cnt[b] = start;
+        if (v) {
+          // Reserve this run's room in cell (s, b).
+          const uint32_t at = atomicAdd(&fill[cbase + b], v);
+          adj[b] = (int64_t)((cbase + b) * (uint64_t)AMS_SMEM_SORT_CAP + at) - (int64_t)start;
+          const int32_t room = (int32_t)AMS_SMEM_SORT_CAP - (int32_t)at;
+          lim[b] = (int32_t)start + room;  // slots below lim are written
+          if ((uint32_t)max(room, 0) < v) {
+            s_clip = 1;
+            seg_ovf[s] = 1;
+          }
+        }
+        start += v;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < kItemsU; ++i) {
+      if (pk[i] != kInvalid) {
+        const uint32_t b = pk[i] >> 16;
+        const uint32_t slot = cnt[b] + (pk[i] & 0xFFFFu);
+        buf[slot] = kr[i];
+        bkt[slot] = (uint16_t)b;
+      }
+    }
+    __syncthreads();
+    if (!s_clip) {
+      for (uint32_t j = tid; j < tc; j += kThreadsU) dst[adj[bkt[j]] + j] = buf[j];
+    } else {
+      for (uint32_t j = tid; j < tc; j += kThreadsU) {
+        const uint32_t b = bkt[j];
+        if ((int32_t)j < lim[b]) dst[adj[b] + j] = buf[j];
+      }
+    }
+    for (int j = 0; j < per; ++j) cnt[tid * per + j] = 0;
+    __syncthreads();
+  }
+}
+
+// Output base of every fixed-capacity cell: one warp per segment scans its
+// cells' fill counts (segments flagged as overflowed get empty cells: the
+// host partitions them again).  Also records each cell's segment.
+__global__ void k_fixed_cells(const uint32_t* __restrict__ fill, const uint32_t* __restrict__ cell0,
+                              const uint64_t* __restrict__ seg_off, const uint32_t* __restrict__ seg_ovf,
+                              int nseg, uint64_t* __restrict__ out_base, uint32_t* __restrict__ cnt,
+                              uint32_t* __restrict__ cell_seg) {
+  const int s = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (s >= nseg) return;
+  const uint32_t c0 = cell0[s], c1 = cell0[s + 1];
+  const bool ovf = seg_ovf[s] != 0;
+  uint64_t run = seg_off[s];
+  for (uint32_t ci0 = c0; ci0 < c1; ci0 += 32) {
+    const uint32_t ci = ci0 + lane;
+    const uint32_t v = (ci < c1 && !ovf) ? fill[ci] : 0;
+    const uint32_t inc = warp_incl_scan(v);
+    if (ci < c1) {
+      out_base[ci] = run + inc - v;
+      cnt[ci] = v;
+      cell_seg[ci] = (uint32_t)s;
+    }
+    run += __shfl_sync(0xffffffffu, inc, 31);
+  }
+}
+
+// Digit classifier of every bucket segment of a bucket-major last level:
+// bucket b of group g holds keys between splitter b-1 and splitter b (the
+// group's bounds at the open ends); nb digits each (per segment).
+__global__ void k_bucket_ranges(const uint8_t* __restrict__ blobs, const uint64_t* __restrict__ gbounds,
+                                const int32_t* __restrict__ seg_gb, int nseg, DigitCls* __restrict__ out) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= nseg) return;
+  const int g = seg_gb[3 * s], b = seg_gb[3 * s + 1];
+  const uint8_t* blob = blobs + (size_t)g * kBlobStride;
+  const ClsHeader* h = reinterpret_cast<const ClsHeader*>(blob);
+  const uint64_t* bk = reinterpret_cast<const uint64_t*>(blob + kBlobKeys);
+  uint64_t lo = gbounds[2 * g], hi = gbounds[2 * g + 1];
+  if (b > 0) lo = max(lo, bk[b - 1]);
+  if ((uint32_t)b < h->nspl) hi = min(hi, bk[b]);
+  if (hi < lo) hi = lo;
+  DigitCls d;
+  d.lo = lo;
+  d.hi = hi;
+  d.nb = (uint32_t)seg_gb[3 * s + 2];
+  d.mult = digit_mult(hi - lo, d.nb);
+  d.pad = 0;
+  d.q = 0;
+  d.m32 = 0;
+  d.sh = 0;
+  if (d.mult != 0) {
+    d.q = (~0ULL) / d.mult;
+    const uint64_t w = d.q + 2ull * d.nb + 2;
+    d.sh = (uint32_t)max(0, bit_length64(w) - 32);
+    const uint64_t w32 = ((w - 1) >> d.sh) + 1;
+    if (w32 > (uint64_t)(2 * AMS_SMEM_SORT_CAP)) d.m32 = (uint32_t)(((uint64_t)(2 * AMS_SMEM_SORT_CAP) << 32) / w32);
+  }
+  out[s] = d;
+}
+
 // -------------------------------------------------------------------- K7
 __global__ void k_gather_bounds(const uint64_t* __restrict__ bounds, const int32_t* __restrict__ sel,
                                 int n, uint64_t* __restrict__ out) {
@@ -793,17 +1017,24 @@ __device__ __forceinline__ void block_minmax(uint64_t& mn, uint64_t& mx, uint64_
 }
 
 __device__ __forceinline__ void cell_of(const CellSource& cs, uint64_t cid, uint64_t& off,
-                                        uint64_t& count) {
+                                        uint64_t& count, uint64_t& oo) {
   if (cs.mode == 0) {
     off = cs.cell_base[cid];
     count = cs.cell_cnt[cid];
+    oo = off;
   } else if (cs.mode == 1) {
     off = cs.seg_off[cid];
     count = cs.seg_len[cid];
-  } else {
-    if (cs.nrecs && cid >= *cs.nrecs) { off = 0; count = 0; return; }
+    oo = off;
+  } else if (cs.mode == 2) {
+    if (cs.nrecs && cid >= *cs.nrecs) { off = 0; count = 0; oo = 0; return; }
     off = cs.recs[cid].off;
     count = cs.recs[cid].count;
+    oo = cs.recs[cid].out;
+  } else {  // fixed-capacity cells: source slot cid, output base from k_fixed_cells
+    off = cid * (uint64_t)AMS_SMEM_SORT_CAP;
+    count = cs.cell_cnt[cid];
+    oo = cs.cell_base[cid];
   }
 }
 
@@ -813,7 +1044,8 @@ __device__ __forceinline__ void cell_of(const CellSource& cs, uint64_t cid, uint
 template <int KIND_OUT, bool VALS>
 __device__ bool big_cell(const uint64_t* __restrict__ src, const uint64_t* __restrict__ src_vals,
                          uint64_t* __restrict__ out, uint64_t* __restrict__ out_vals, uint64_t off,
-                         uint64_t count, OverflowRec* ovf, unsigned int* ovf_count, uint64_t* s_mm) {
+                         uint64_t oo, uint64_t count, OverflowRec* ovf, unsigned int* ovf_count,
+                         uint64_t* s_mm) {
   if (count <= (uint64_t)kSortCap) return false;
   uint64_t mn = ~0ULL, mx = 0;
   for (uint64_t i = threadIdx.x; i < count; i += blockDim.x) {
@@ -824,12 +1056,12 @@ __device__ bool big_cell(const uint64_t* __restrict__ src, const uint64_t* __res
   if (mn == mx) {
     const uint64_t ko = from_ordered<KIND_OUT>(mn);
     for (uint64_t i = threadIdx.x; i < count; i += blockDim.x) {
-      out[off + i] = ko;
-      if constexpr (VALS) out_vals[off + i] = src_vals[off + i];
+      out[oo + i] = ko;
+      if constexpr (VALS) out_vals[oo + i] = src_vals[off + i];
     }
   } else if (threadIdx.x == 0) {
     const unsigned int slot = atomicAdd(ovf_count, 1u);
-    OverflowRec r; r.off = off; r.count = count; r.lo = mn; r.hi = mx;
+    OverflowRec r; r.off = off; r.count = count; r.lo = mn; r.hi = mx; r.out = oo;
     ovf[slot] = r;
   }
   return true;
@@ -853,8 +1085,8 @@ __global__ void __launch_bounds__(kSortThreads, 1)
   uint32_t* wh = reinterpret_cast<uint32_t*>(iB + kSortCap);  // [kSortWarps][kRadix]
   uint32_t* btot = wh + kSortWarps * kRadix;
 
-  uint64_t off, count;
-  cell_of(cs, blockIdx.x, off, count);
+  uint64_t off, count, oo;
+  cell_of(cs, blockIdx.x, off, count, oo);
   if (count == 0 || count > (uint64_t)kSortCap) return;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t n = (uint32_t)count;
@@ -914,8 +1146,8 @@ __global__ void __launch_bounds__(kSortThreads, 1)
     }
   }
   for (uint32_t i = threadIdx.x; i < n; i += kSortThreads) {
-    out[off + i] = from_ordered<KIND_OUT>(kA[i]);
-    if constexpr (VALS) out_vals[off + i] = src_vals[off + iA[i]];
+    out[oo + i] = from_ordered<KIND_OUT>(kA[i]);
+    if constexpr (VALS) out_vals[oo + i] = src_vals[off + iA[i]];
   }
 }
 
@@ -1014,10 +1246,10 @@ __global__ void __launch_bounds__(kSortThreads, kSortCtas)
   uint16_t* qB = reinterpret_cast<uint16_t*>(cw + kSubK / 2);   // queued sub-buckets
   uint16_t* iB = qB + kQueueCap;                                // input index of slot j (VALS)
 
-  uint64_t off, count;
-  cell_of(cs, blockIdx.x, off, count);
+  uint64_t off, count, oo;
+  cell_of(cs, blockIdx.x, off, count, oo);
   if (count == 0) return;
-  if (big_cell<KIND_OUT, VALS>(src, src_vals, out, out_vals, off, count, ovf, ovf_count, s_mm))
+  if (big_cell<KIND_OUT, VALS>(src, src_vals, out, out_vals, off, oo, count, ovf, ovf_count, s_mm))
     return;
   const uint32_t n = (uint32_t)count;
   const uint32_t tid = threadIdx.x;
@@ -1032,12 +1264,19 @@ __global__ void __launch_bounds__(kSortThreads, kSortCtas)
   uint64_t lo = 0;
   uint32_t m32 = 0, sh = 0;
   int attempt = 1;
-  if (cs.mode == 0 && cs.dcls) {
-    const uint32_t seg = blockIdx.x / cs.cells_per_seg;
+  if ((cs.mode == 0 || cs.mode == 3) && cs.dcls) {
+    uint32_t seg, digit;
+    if (cs.mode == 0) {
+      seg = blockIdx.x / cs.cells_per_seg;
+      digit = blockIdx.x - seg * cs.cells_per_seg;
+    } else {
+      seg = cs.cell_seg[blockIdx.x];
+      digit = blockIdx.x - cs.cell0[seg];
+    }
     const DigitCls& d = cs.dcls[seg];
     if (d.m32 != 0) {
       attempt = 0;
-      lo = d.lo + (uint64_t)(blockIdx.x - seg * cs.cells_per_seg) * d.q;
+      lo = d.lo + (uint64_t)digit * d.q;
       m32 = d.m32;
       sh = d.sh;
     }
@@ -1071,8 +1310,8 @@ __global__ void __launch_bounds__(kSortThreads, kSortCtas)
       if (mn == mx) {
         const uint64_t ko = from_ordered<KIND_OUT>(mn);
         for (uint32_t i = tid; i < n; i += kSortThreads) {
-          out[off + i] = ko;
-          if constexpr (VALS) out_vals[off + i] = src_vals[off + i];
+          out[oo + i] = ko;
+          if constexpr (VALS) out_vals[oo + i] = src_vals[off + i];
         }
         return;
       }
@@ -1132,7 +1371,7 @@ __global__ void __launch_bounds__(kSortThreads, kSortCtas)
       if (attempt == 0) continue;  // keys cluster inside the digit cell: use its min/max
       if (tid == 0) {
         const unsigned int slot = atomicAdd(fb_count, 1u);
-        OverflowRec r; r.off = off; r.count = count; r.lo = lo; r.hi = hi_key;
+        OverflowRec r; r.off = off; r.count = count; r.lo = lo; r.hi = hi_key; r.out = oo;
         fb[slot] = r;
       }
       return;
@@ -1208,22 +1447,22 @@ __global__ void __launch_bounds__(kSortThreads, kSortCtas)
     __syncthreads();
   }
   // 5. write-out, 16-byte stores when the output allows.
-  const uint32_t a = (uint32_t)(off & 1);
+  const uint32_t a = (uint32_t)(oo & 1);
   if (((reinterpret_cast<uintptr_t>(out) & 15) == 0) && n > 2) {
-    if (a && tid == 0) out[off] = from_ordered<KIND_OUT>(kB[0]);
+    if (a && tid == 0) out[oo] = from_ordered<KIND_OUT>(kB[0]);
     const uint32_t np = (n - a) >> 1;
-    uint4* o4 = reinterpret_cast<uint4*>(out + off + a);
+    uint4* o4 = reinterpret_cast<uint4*>(out + oo + a);
     for (uint32_t j = tid; j < np; j += kSortThreads) {
       const uint64_t k0 = from_ordered<KIND_OUT>(kB[a + 2 * j]);
       const uint64_t k1 = from_ordered<KIND_OUT>(kB[a + 2 * j + 1]);
       o4[j] = make_uint4((uint32_t)k0, (uint32_t)(k0 >> 32), (uint32_t)k1, (uint32_t)(k1 >> 32));
     }
-    if (((n - a) & 1) && tid == 0) out[off + n - 1] = from_ordered<KIND_OUT>(kB[n - 1]);
+    if (((n - a) & 1) && tid == 0) out[oo + n - 1] = from_ordered<KIND_OUT>(kB[n - 1]);
   } else {
-    for (uint32_t j = tid; j < n; j += kSortThreads) out[off + j] = from_ordered<KIND_OUT>(kB[j]);
+    for (uint32_t j = tid; j < n; j += kSortThreads) out[oo + j] = from_ordered<KIND_OUT>(kB[j]);
   }
   if constexpr (VALS) {
-    for (uint32_t j = tid; j < n; j += kSortThreads) out_vals[off + j] = src_vals[off + iB[j]];
+    for (uint32_t j = tid; j < n; j += kSortThreads) out_vals[oo + j] = src_vals[off + iB[j]];
   }
 }
 
@@ -1249,7 +1488,7 @@ __global__ void k_pack_cells(const uint32_t* __restrict__ cell_cnt,
       if (g_cnt + c > cap && g_cnt) {
         if (lane == 0) {
           const unsigned int slot = atomicAdd(ngroups, 1u);
-          OverflowRec r; r.off = g_off; r.count = g_cnt; r.lo = 0; r.hi = 0;
+          OverflowRec r; r.off = g_off; r.count = g_cnt; r.lo = 0; r.hi = 0; r.out = g_off;
           groups[slot] = r;
         }
         g_cnt = 0;
@@ -1260,7 +1499,7 @@ __global__ void k_pack_cells(const uint32_t* __restrict__ cell_cnt,
   }
   if (g_cnt && lane == 0) {
     const unsigned int slot = atomicAdd(ngroups, 1u);
-    OverflowRec r; r.off = g_off; r.count = g_cnt; r.lo = 0; r.hi = 0;
+    OverflowRec r; r.off = g_off; r.count = g_cnt; r.lo = 0; r.hi = 0; r.out = g_off;
     groups[slot] = r;
   }
 }
@@ -1357,6 +1596,13 @@ cudaError_t launch_cell_base(cudaStream_t st, const uint32_t* seg_hist, int nb_s
   if (ngroups == 0) return cudaSuccess;
   const size_t smem = sizeof(uint64_t) * (size_t)r;
   k_cell_base<<<ngroups, 256, smem, st>>>(seg_hist, nb_stride, gm, r, pieces, cell_base);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cell_base_bm(cudaStream_t st, const uint32_t* seg_hist, int nb_stride,
+                                const GroupMeta& gm, int ngroups, uint64_t* cell_base) {
+  if (ngroups == 0) return cudaSuccess;
+  k_cell_base_bm<<<ngroups, 256, 0, st>>>(seg_hist, nb_stride, gm, cell_base);
   return cudaGetLastError();
 }
 
@@ -1566,6 +1812,45 @@ cudaError_t launch_pack_cells(cudaStream_t st, const uint32_t* cell_cnt, const u
                               unsigned int* ngroups) {
   if (nseg == 0) return cudaSuccess;
   k_pack_cells<<<(nseg + 3) / 4, 128, 0, st>>>(cell_cnt, cell_base, nseg, nb, cap, groups, ngroups);
+  return cudaGetLastError();
+}
+
+size_t scatter_fixed_smem_bytes(int nb) {
+  const int per = (nb + kThreadsU - 1) / kThreadsU | 1;
+  const size_t nbp = (size_t)per * kThreadsU;
+  return 2 * 8 * (size_t)(kTile + 2) + 16 * nbp + 2 * (size_t)kTile;
+}
+
+cudaError_t launch_scatter_fixed(cudaStream_t st, const void* src, int kind, void* dst,
+                                 const SegMeta& m, uint64_t nchunks, int max_nb,
+                                 const DigitCls* dcls, const uint32_t* cell0, uint32_t* fill,
+                                 uint32_t* seg_ovf) {
+  if (nchunks == 0) return cudaSuccess;
+  const size_t smem = scatter_fixed_smem_bytes(max_nb);
+  const uint64_t* s = static_cast<const uint64_t*>(src);
+  uint64_t* d = static_cast<uint64_t*>(dst);
+  cudaError_t e = cudaSuccess;
+  (void)kind;  // the last level's output holds order-mapped u64 keys
+  auto fn = k_scatter_fixed<AMS_KEY_U64>;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  fn<<<(unsigned)nchunks, kThreadsU, smem, st>>>(s, d, m, dcls, cell0, fill, seg_ovf);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fixed_cells(cudaStream_t st, const uint32_t* fill, const uint32_t* cell0,
+                               const uint64_t* seg_off, const uint32_t* seg_ovf, int nseg,
+                               uint64_t* out_base, uint32_t* cnt, uint32_t* cell_seg) {
+  if (nseg == 0) return cudaSuccess;
+  k_fixed_cells<<<(nseg + 7) / 8, 256, 0, st>>>(fill, cell0, seg_off, seg_ovf, nseg, out_base, cnt,
+                                                 cell_seg);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bucket_ranges(cudaStream_t st, const uint8_t* blobs, const uint64_t* gbounds,
+                                 const int32_t* seg_gb, int nseg, DigitCls* out) {
+  if (nseg == 0) return cudaSuccess;
+  k_bucket_ranges<<<(nseg + 127) / 128, 128, 0, st>>>(blobs, gbounds, seg_gb, nseg, out);
   return cudaGetLastError();
 }
 

@@ -28,7 +28,8 @@ struct GroupMeta {
 
 // Work list of the shared-memory sort: mode 0 = cells of a digit
 // partition (cell id = seg * nb + digit), mode 1 = explicit segments,
-// mode 2 = records (fallback list on the device).
+// mode 2 = records (fallback list on the device), mode 3 = fixed-capacity
+// digit cells.
 struct CellSource {
   int mode;
   uint32_t cells_per_seg;  // mode 0: cells of one segment (cell id = seg * cells_per_seg + digit)
@@ -39,6 +40,11 @@ struct CellSource {
   const uint64_t* seg_len;
   const OverflowRec* recs;
   const unsigned int* nrecs;  // mode 2: record count on the device (may be null)
+  // mode 3 = fixed-capacity cells (k_scatter_fixed): cell ci at src[ci * cap],
+  // count cell_cnt[ci], output at cell_base[ci]; digit classifier of its
+  // segment cell_seg[ci], whose first cell is cell0[seg].
+  const uint32_t* cell_seg;
+  const uint32_t* cell0;
 };
 
 cudaError_t launch_gather_sample(cudaStream_t st, const void* src, int kind, const uint64_t* idx,
@@ -59,6 +65,9 @@ cudaError_t launch_chunk_scan(cudaStream_t st, uint32_t* chunk_tot, const SegMet
 cudaError_t launch_cell_base(cudaStream_t st, const uint32_t* seg_hist, int nb_stride,
                              const GroupMeta& gm, int ngroups, int r, uint64_t* pieces,
                              uint64_t* cell_base);
+// Bucket-major cell bases (keys-only last level): buckets contiguous per group.
+cudaError_t launch_cell_base_bm(cudaStream_t st, const uint32_t* seg_hist, int nb_stride,
+                                const GroupMeta& gm, int ngroups, uint64_t* cell_base);
 cudaError_t launch_digit_base(cudaStream_t st, const uint32_t* seg_hist, int nb_stride,
                               const SegMeta& m, uint64_t* cell_base);
 size_t scatter_smem_bytes(int nb_stride, int nspl_cap, int cells_cap, bool digit, bool vals,
@@ -93,6 +102,19 @@ cudaError_t launch_smem_sort_lsd(cudaStream_t st, const void* src, const void* s
 cudaError_t launch_pack_cells(cudaStream_t st, const uint32_t* cell_cnt, const uint64_t* cell_base,
                               int nseg, int nb, uint32_t cap, OverflowRec* groups,
                               unsigned int* ngroups);
+// Fixed-capacity digit partition of bucket segments (keys only): cells of
+// AMS_SMEM_SORT_CAP slots in dst, fill counts in `fill`, overflow flags per
+// segment in seg_ovf (see k_scatter_fixed).
+cudaError_t launch_scatter_fixed(cudaStream_t st, const void* src, int kind, void* dst,
+                                 const SegMeta& m, uint64_t nchunks, int max_nb,
+                                 const DigitCls* dcls, const uint32_t* cell0, uint32_t* fill,
+                                 uint32_t* seg_ovf);
+cudaError_t launch_fixed_cells(cudaStream_t st, const uint32_t* fill, const uint32_t* cell0,
+                               const uint64_t* seg_off, const uint32_t* seg_ovf, int nseg,
+                               uint64_t* out_base, uint32_t* cnt, uint32_t* cell_seg);
+// seg_gb[3*s] = (group, bucket, digits) of every bucket segment.
+cudaError_t launch_bucket_ranges(cudaStream_t st, const uint8_t* blobs, const uint64_t* gbounds,
+                                 const int32_t* seg_gb, int nseg, DigitCls* out);
 cudaError_t launch_map_keys(cudaStream_t st, const void* src, void* dst, uint64_t n, int from,
                             int to);
 
