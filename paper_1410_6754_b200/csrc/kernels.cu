@@ -796,9 +796,10 @@ __global__ void __launch_bounds__(kThreadsU, 2)
   }
   __syncthreads();
   const int s = s_seg;
-  DigitView dv;
-  dv.c = dcls[s];
-  const int nb = (int)dv.c.nb;
+  const DigitCls dc = dcls[s];
+  const int nb = (int)dc.nb;
+  const uint64_t dlo = dc.lo;
+  const uint32_t dsh = dc.sh, dm = dc.m32, dmax = dc.nb - 1;
   const int per = (nb + kThreadsU - 1) / kThreadsU | 1;
   const int nbp = per * kThreadsU;
   int64_t* adj = reinterpret_cast<int64_t*>(buf0 + 2 * kBuf);  // this tile: dst index - slot
@@ -810,13 +811,14 @@ __global__ void __launch_bounds__(kThreadsU, 2)
   const uint64_t last = min(first + (uint64_t)kChunk, m.len[s]);
   const int ntiles = (int)((last - first + kTile - 1) / kTile);
   const uint64_t cbase = cell0[s];
+  // Tile t = keys [base, base + tc); the copy starts at the 16-byte boundary
+  // base - h and is rounded up to whole 16-byte units (the source buffer is
+  // padded by two keys), so key e of the tile sits at buf[e + h].
   auto issue = [&](int t) {
     const uint64_t base = seg_off + first + (uint64_t)t * kTile;
     const uint32_t tc = (uint32_t)min((uint64_t)kTile, last - first - (uint64_t)t * kTile);
     const uint32_t h = (uint32_t)(base & 1);
-    const uint64_t b0 = base + h, b1 = (base + tc) & ~1ULL;
-    const uint32_t bytes = b1 > b0 ? (uint32_t)(b1 - b0) * 8 : 0;
-    bulk_load(buf0 + (t & 1) * kBuf + 2 * h, src + b0, bytes, &s_bar[t & 1]);
+    bulk_load(buf0 + (t & 1) * kBuf, src + (base - h), ((tc + h + 1) & ~1u) * 8, &s_bar[t & 1]);
   };
   if (tid == 0) issue(0);
   for (int b = tid; b < nbp; b += kThreadsU) cnt[b] = 0;
@@ -827,25 +829,31 @@ __global__ void __launch_bounds__(kThreadsU, 2)
     const uint64_t base = seg_off + first + (uint64_t)t * kTile;
     const uint32_t tc = (uint32_t)min((uint64_t)kTile, last - first - (uint64_t)t * kTile);
     const uint32_t h = (uint32_t)(base & 1);
-    const uint32_t e_end = (uint32_t)(((base + tc) & ~1ULL) - base);
     if (tid == 0 && t + 1 < ntiles) {
       fence_proxy_async();
       issue(t + 1);
     }
     mbar_wait(&s_bar[t & 1], (uint32_t)(t >> 1) & 1u);
+    const uint64_t* tb = buf + h;
     uint64_t kr[kItemsU];
     uint32_t pk[kItemsU];
+    auto classify_all = [&](auto full_tag) {
+      constexpr bool FULL = decltype(full_tag)::value;
 #pragma unroll
-    for (int i = 0; i < kItemsU; ++i) {
-      const uint32_t e = w * (kItemsU * 32) + i * 32 + lane;
-      pk[i] = kInvalid;
-      if (e < tc) {
-        const uint64_t key = to_ordered<KIND>((e >= h && e < e_end) ? buf[e + h] : src[base + e]);
-        const uint32_t b = dv.classify(key, 0);
-        kr[i] = key;
-        pk[i] = (b << 16) | atomicAdd(&cnt[b], 1u);
+      for (int i = 0; i < kItemsU; ++i) {
+        const uint32_t e = w * (kItemsU * 32) + i * 32 + lane;
+        pk[i] = kInvalid;
+        if (FULL || e < tc) {
+          const uint64_t key = to_ordered<KIND>(tb[e]);
+          const uint64_t x = key - dlo;
+          const uint32_t b = dm ? min(__umulhi((uint32_t)(x >> dsh), dm), dmax) : (uint32_t)x;
+          kr[i] = key;
+          pk[i] = (b << 16) | atomicAdd(&cnt[b], 1u);
+        }
       }
-    }
+    };
+    if (tc == (uint32_t)kTile) classify_all(std::true_type{});
+    else classify_all(std::false_type{});
     __syncthreads();
     {
       const int b0 = tid * per;
@@ -938,22 +946,21 @@ __global__ void k_bucket_ranges(const uint8_t* __restrict__ blobs, const uint64_
   if (b > 0) lo = max(lo, bk[b - 1]);
   if ((uint32_t)b < h->nspl) hi = min(hi, bk[b]);
   if (hi < lo) hi = lo;
+  // 32-bit digit: x32 = (key - lo) >> sh (range below 2^32 after the shift),
+  // digit = umulhi(x32, m) with m = floor(nb * 2^32 / (R + 1)), R = range >> sh:
+  // monotone and below nb; m == 0: range < nb, the digit is key - lo itself.
   DigitCls d;
   d.lo = lo;
   d.hi = hi;
   d.nb = (uint32_t)seg_gb[3 * s + 2];
-  d.mult = digit_mult(hi - lo, d.nb);
+  d.mult = 0;
   d.pad = 0;
-  d.q = 0;
-  d.m32 = 0;
-  d.sh = 0;
-  if (d.mult != 0) {
-    d.q = (~0ULL) / d.mult;
-    const uint64_t w = d.q + 2ull * d.nb + 2;
-    d.sh = (uint32_t)max(0, bit_length64(w) - 32);
-    const uint64_t w32 = ((w - 1) >> d.sh) + 1;
-    if (w32 > (uint64_t)(2 * AMS_SMEM_SORT_CAP)) d.m32 = (uint32_t)(((uint64_t)(2 * AMS_SMEM_SORT_CAP) << 32) / w32);
-  }
+  const uint64_t range = hi - lo;
+  d.sh = (uint32_t)max(0, bit_length64(range) - 32);
+  const uint64_t R = range >> d.sh;
+  d.m32 = R + 1 <= (uint64_t)d.nb ? 0u : (uint32_t)(((uint64_t)d.nb << 32) / (R + 1));
+  const uint64_t mk = (uint64_t)d.m32 * (uint64_t)(2 * AMS_SMEM_SORT_CAP);
+  d.q = mk < (1ull << 32) ? mk : 0;  // sub-bucket multiplier of the cell sort
   out[s] = d;
 }
 
@@ -1261,24 +1268,31 @@ __global__ void __launch_bounds__(kSortThreads, kSortCtas)
   // takes the clamped keys: the clamp below keeps its map monotone), so
   // sub = ((key - cell_lo) >> sh) * m32 >> 32 spreads the cell over kSubK
   // sub-buckets with one 32-bit multiply and no min/max pass.
+  // Fixed-capacity cells (mode 3, k_bucket_ranges): cell c of a bucket holds
+  // the keys with umulhi(x32, m) == c, x32 = (key - lo) >> sh, so
+  // sub = umulhi(x32, m * kSubK) - c * kSubK is in [0, kSubK) exactly
+  // (floor(floor(y * K) / K) = floor(y)); q holds m * kSubK (0: no refine).
   uint64_t lo = 0;
-  uint32_t m32 = 0, sh = 0;
+  uint32_t m32 = 0, sh = 0, sub0 = 0;
   int attempt = 1;
-  if ((cs.mode == 0 || cs.mode == 3) && cs.dcls) {
-    uint32_t seg, digit;
-    if (cs.mode == 0) {
-      seg = blockIdx.x / cs.cells_per_seg;
-      digit = blockIdx.x - seg * cs.cells_per_seg;
-    } else {
-      seg = cs.cell_seg[blockIdx.x];
-      digit = blockIdx.x - cs.cell0[seg];
-    }
+  if (cs.mode == 0 && cs.dcls) {
+    const uint32_t seg = blockIdx.x / cs.cells_per_seg;
     const DigitCls& d = cs.dcls[seg];
     if (d.m32 != 0) {
       attempt = 0;
-      lo = d.lo + (uint64_t)digit * d.q;
+      lo = d.lo + (uint64_t)(blockIdx.x - seg * cs.cells_per_seg) * d.q;
       m32 = d.m32;
       sh = d.sh;
+    }
+  } else if (cs.mode == 3) {
+    const uint32_t seg = cs.cell_seg[blockIdx.x];
+    const DigitCls& d = cs.dcls[seg];
+    if (d.q != 0) {
+      attempt = 0;
+      lo = d.lo;
+      m32 = (uint32_t)d.q;
+      sh = d.sh;
+      sub0 = (blockIdx.x - cs.cell0[seg]) * (uint32_t)kSubK;
     }
   }
   const int nit = (int)((n + kSortThreads - 1) / kSortThreads);  // items in use per thread
@@ -1324,6 +1338,7 @@ __global__ void __launch_bounds__(kSortThreads, kSortCtas)
       // floor(2n * 2^32 / w32) - 1 <= the exact quotient: sub stays below 2n.
       m32 = exact ? 0
                   : (uint32_t)((float)(2 * n) * 4294967296.0f / (float)((range >> sh) + 1)) - 1u;
+      sub0 = 0;
     } else {
       __syncthreads();
     }
@@ -1336,7 +1351,7 @@ __global__ void __launch_bounds__(kSortThreads, kSortCtas)
       if (it * kSortThreads + tid < n) {
         const uint64_t x = kr[it] - lo;
         const uint32_t s =
-            exact ? (uint32_t)x : min(__umulhi((uint32_t)(x >> sh), m32), (uint32_t)kSubK - 1);
+            exact ? (uint32_t)x : min(__umulhi((uint32_t)(x >> sh), m32) - sub0, (uint32_t)kSubK - 1);
         const uint32_t sh = (s & 1) * 16;
         const uint32_t rk = (atomicAdd(&cw[sw_word(s >> 1)], 1u << sh) >> sh) & 0xFFFFu;
         pk[it] = (s << 16) | rk;
