@@ -1002,7 +1002,10 @@ __global__ void k_final_ranges(const uint64_t* __restrict__ bounds, int nseg, in
 }
 
 // -------------------------------------------------------------------- K9
-constexpr int kSortThreads = 256;
+#ifndef AMS_SORT_THREADS
+#define AMS_SORT_THREADS 256
+#endif
+constexpr int kSortThreads = AMS_SORT_THREADS;
 constexpr int kSortWarps = kSortThreads / 32;
 constexpr int kSortCap = AMS_SMEM_SORT_CAP;
 constexpr int kSortItems = kSortCap / kSortThreads;  // per-warp iterations
@@ -1192,15 +1195,22 @@ constexpr bool kNitBreak = AMS_NIT_BREAK;
 constexpr int kSubK = kCellSubBuckets;                   // sub-buckets of the refined digit
 constexpr int kScanWords = kSubK / 2 / kSortThreads;  // counter words per thread (2 sub-buckets each)
 static_assert(kScanWords % 4 == 0, "scan loads 4 words at a time");
+constexpr int kScanChunks = kScanWords / 4;  // uint4 chunks per thread (4 at 256 threads, 2 at 512)
+static_assert(kScanChunks == 2 || kScanChunks == 4, "swizzle covers 2 or 4 chunks per thread");
+constexpr int kLgChunks = kScanChunks == 4 ? 2 : 1;
 constexpr int kQueueCap = kSortCap / 2;               // sub-buckets with >= 2 keys
 
 // Counter layout: thread t of the scan owns logical words [16t, 16t + 16) as
-// four uint4 chunks; chunk c is stored at chunk c ^ ((t >> 1) & 3) of its
-// 64-byte block, so the 8 threads of one 128-bit shared-memory phase hit 32
-// distinct banks.  Logical word w lives at w ^ (((w >> 5) & 3) << 2); the
-// u16 counter of sub-bucket s at sw16(s).
-__device__ __forceinline__ uint32_t sw_word(uint32_t w) { return w ^ (((w >> 5) & 3u) << 2); }
-__device__ __forceinline__ uint32_t sw16(uint32_t s) { return s ^ ((s >> 3) & 0x18u); }
+// four uint4 chunks (256 threads; [8t, 8t + 8) as two at 512); chunk c is
+// stored at chunk c ^ rot(t) of its block, so the 8 threads of one 128-bit
+// shared-memory phase hit 32 distinct banks.  Logical word w lives at
+// sw_word(w); the u16 counter of sub-bucket s at sw16(s).
+__device__ __forceinline__ uint32_t sw_word(uint32_t w) {
+  return w ^ (((w >> 5) & (uint32_t)(kScanChunks - 1)) << 2);
+}
+__device__ __forceinline__ uint32_t sw16(uint32_t s) {
+  return s ^ (((s >> 6) & (uint32_t)(kScanChunks - 1)) << 3);
+}
 
 template <bool VALS>
 __device__ __forceinline__ bool slot_after(uint64_t ka, uint16_t ia, uint64_t kb, uint16_t ib) {
@@ -1304,7 +1314,9 @@ __global__ void __launch_bounds__(kSortThreads, kSortCtas)
     kr[it] = i < n ? ldg_stream(src + off + i) : ~0ULL;
   }
   uint4* const cw4 = reinterpret_cast<uint4*>(cw) + tid * (kScanWords / 4);
-  const uint32_t rot = (tid >> 1) & 3u;  // chunk c of this thread is stored at c ^ rot
+  // chunk c of this thread is stored at c ^ rot: the 8 threads of one
+  // 128-bit shared-memory phase then cover 32 distinct banks.
+  const uint32_t rot = (tid >> (3 - kLgChunks)) & (uint32_t)(kScanChunks - 1);
   uint32_t pk[kSortItems];
   uint32_t all, qpos;
   uint64_t hi_key = 0;
