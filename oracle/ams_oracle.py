@@ -1,7 +1,7 @@
 """CPU oracle for the AMS-sort hot path — TEST INFRASTRUCTURE ONLY.
 
 This module restates the reference algorithm (`mlpsort.ams.ams_sort` with
-``scheme="simple"``) with numpy arrays so the GPU path can be checked at
+``scheme="simple"`` or ``"deterministic"``) with numpy arrays so the GPU path can be checked at
 sizes the pure-Python reference cannot reach.  It is the *checker*: only
 ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
 ``--impl reference`` legs may import it.  The product path
@@ -194,13 +194,132 @@ def _exchange_stats(piece_sizes: np.ndarray, sub_sizes: int, members: list):
             "max_sent_msgs": ms, "max_recv_msgs": mr}
 
 
+def deterministic_plan(piece_sizes: np.ndarray, group_lo: int = 0):
+    """Member assignment of ``deliver_deterministic`` (delivery.py:188-306):
+    small pieces (size * 2 * p * r <= n) go whole to member
+    ``small_index // r`` of their subgroup; large pieces fill the members'
+    residual quota capacity (delivery.py:78-80) by merging the two prefix
+    sums, one member after another.  Returns ``slices[(j, g)] = [(t,
+    offset, length), ...]`` (t = member of subgroup g) and the new member
+    sizes (members in group order).  Raises ValueError for a piece above
+    ceil(n/p) (delivery.py:212-217) and RuntimeError when the residual
+    capacities cannot hold the large pieces (delivery.py:274-276)."""
+    P, r = piece_sizes.shape
+    if P % r != 0:
+        raise ValueError(f"{P} PEs cannot form {r} groups")
+    sub = P // r
+    n = int(piece_sizes.sum())
+    cap = -(-n // P)
+    for j in range(P):
+        for g in range(r):
+            if int(piece_sizes[j, g]) > cap:
+                raise ValueError(f"piece ({group_lo + j},{g}) larger than ceil(n/p): "
+                                 f"{int(piece_sizes[j, g])} > {cap}")
+
+    def is_small(size):
+        return size * 2 * P * r <= n
+
+    slices = {}
+    for g in range(r):
+        m_g = int(piece_sizes[:, g].sum())
+        caps = [(m_g * (t + 1)) // sub - (m_g * t) // sub for t in range(sub)]
+        small_load = [0] * sub
+        small_index = 0
+        larges = []
+        for j in range(P):
+            size = int(piece_sizes[j, g])
+            if size == 0:
+                continue
+            if not is_small(size):
+                larges.append((j, size))
+                continue
+            t = small_index // r
+            small_index += 1
+            small_load[t] += size
+            slices[(j, g)] = [(t, 0, size)]
+        bounds = [0]
+        for t in range(sub):
+            bounds.append(bounds[-1] + max(0, caps[t] - small_load[t]))
+        pos = 0
+        for j, size in larges:
+            t = int(np.searchsorted(bounds, pos, side="right")) - 1   # bisect_right
+            covered = 0
+            cuts = []
+            while covered < size:
+                if t >= sub:
+                    raise RuntimeError("residual capacities cannot hold the large pieces")
+                take = min(pos + size, bounds[t + 1]) - (pos + covered)
+                if take > 0:
+                    cuts.append((t, covered, take))
+                    covered += take
+                t += 1
+            slices[(j, g)] = cuts
+            pos += size
+    new_sizes = [0] * P
+    for (j, g), cuts in slices.items():
+        for t, _, ln in cuts:
+            new_sizes[g * sub + t] += ln
+    return slices, new_sizes
+
+
+def _deterministic_stats(piece_sizes: np.ndarray, slices: dict):
+    """Data-exchange shape of the deterministic delivery's data messages
+    (``_execute``, delivery.py:109-120, counted by simnet.py:294-335)."""
+    P, r = piece_sizes.shape
+    sub = P // r
+    sw = np.zeros(P, np.int64); rw = np.zeros(P, np.int64)
+    sm = np.zeros(P, np.int64); rm = np.zeros(P, np.int64)
+    for (j, g), cuts in slices.items():
+        for t, _, ln in cuts:
+            dest = g * sub + t
+            if ln > 0 and dest != j:
+                sw[j] += ln; rw[dest] += ln; sm[j] += 1; rm[dest] += 1
+    hs, hr = int(sw.max(initial=0)), int(rw.max(initial=0))
+    ms, mr = int(sm.max(initial=0)), int(rm.max(initial=0))
+    return {"max_words": max(hs, hr), "max_msgs": max(ms, mr),
+            "max_sent_msgs": ms, "max_recv_msgs": mr}
+
+
+def deterministic_relayout(e_layout: np.ndarray, piece_sizes: np.ndarray, slices: dict,
+                           new_sizes: list) -> np.ndarray:
+    """Member arrays of the deterministic delivery from the simple group
+    layout E (pieces (j, g) source-major inside each subgroup g): member
+    (g, t) receives its slices in source order (inbox order, simnet.py:324-325)."""
+    P, r = piece_sizes.shape
+    sub = P // r
+    g_start = np.concatenate([[0], np.cumsum(piece_sizes.sum(axis=0))]).astype(np.int64)
+    p_start = np.zeros((P, r), np.int64)
+    for g in range(r):
+        p_start[:, g] = g_start[g] + np.concatenate([[0], np.cumsum(piece_sizes[:, g])[:-1]])
+    out = np.empty_like(e_layout)
+    at = 0
+    for D in range(P):
+        g, t = divmod(D, sub)
+        for j in range(P):
+            for tt, off, ln in slices.get((j, g), ()):
+                if tt == t:
+                    s0 = int(p_start[j, g]) + off
+                    out[at:at + ln] = e_layout[s0:s0 + ln]
+                    at += ln
+    assert at == len(e_layout) and at == sum(new_sizes)
+    return out
+
+
 def ams_level(buf: np.ndarray, sizes: list, r: int, b: int, a: float,
               master_seed: int, stream: str, level: int, group_lo: int,
-              vals: np.ndarray | None = None, with_stats: bool = False):
+              vals: np.ndarray | None = None, with_stats: bool = False,
+              scheme: str = "simple", org: np.ndarray | None = None):
     """One level on one group whose member arrays are consecutive in
     ``buf`` (ams.py:214-268).  Returns the new group buffer (the stable
-    ``(g, j, b)`` order of SURVEY §8 layout contract), new member sizes and
-    a LevelInfo."""
+    ``(g, j, b)`` order of SURVEY §8 layout contract, or the deterministic
+    delivery's member arrays), new member sizes, a LevelInfo and the new
+    origin tags.
+
+    ``org`` = origin of every element (its index in the sort's input): the
+    reference breaks key ties by ``(origin_pe, origin_pos)`` (core.py:19-43).
+    Under "simple" delivery origin order equals group-buffer order (SURVEY
+    F6); "deterministic" delivery can place a later source's piece in an
+    earlier member, so ties are broken by the carried origin here."""
     P = len(sizes)
     n_g = int(sum(sizes))
     offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
@@ -218,9 +337,17 @@ def ams_level(buf: np.ndarray, sizes: list, r: int, b: int, a: float,
     s_pos = np.asarray(s_idx, dtype=np.int64)
     drawn = len(s_pos)
     br = min(br, drawn + 1)                                    # ams.py:228
-    sk, sp = select_splitters(buf[s_pos], s_pos, br)
-    pos = np.arange(n_g, dtype=np.int64)
-    bucket = classify(buf, pos, sk, sp)
+    if org is None:
+        org = np.arange(n_g, dtype=np.int64)
+    s_org = org[s_pos]
+    if br <= 1:
+        sk = np.zeros(0, dtype=U64); so = sp = np.zeros(0, dtype=np.int64)
+    else:                                                      # ams.py:178-198
+        order_s = np.lexsort((s_org, buf[s_pos]))
+        ranks = sorted({(i * drawn) // br for i in range(1, br)})
+        sel = order_s[np.asarray(ranks, dtype=np.int64)]
+        sk, so, sp = buf[s_pos][sel], s_org[sel], s_pos[sel]
+    bucket = classify(buf, org, sk, so)
     member = np.repeat(np.arange(P, dtype=np.int64), sizes)
     hist = np.zeros((P, br), dtype=np.int64)
     np.add.at(hist, (member, bucket), 1)
@@ -232,20 +359,33 @@ def ams_level(buf: np.ndarray, sizes: list, r: int, b: int, a: float,
     order = np.argsort(comp, kind="stable")                    # F10 layout
     out = buf[order]
     out_vals = vals[order] if vals is not None else None
+    out_org = org[order]
     sub = P // r
-    new_sizes = []
-    for g in range(r):                                         # delivery.py:78-80
-        m = int(plan.loads[g])
-        for t in range(sub):
-            new_sizes.append((m * (t + 1)) // sub - (m * t) // sub)
+    pieces = np.zeros((P, r), np.int64)
+    for g in range(r):
+        pieces[:, g] = hist[:, bnd[g]:bnd[g + 1]].sum(axis=1)
+    if scheme == "deterministic":                              # delivery.py:188-306
+        slices, new_sizes = deterministic_plan(pieces, group_lo)
+        out = deterministic_relayout(out, pieces, slices, new_sizes)
+        out_org = deterministic_relayout(out_org, pieces, slices, new_sizes)
+        if out_vals is not None:
+            out_vals = deterministic_relayout(out_vals, pieces, slices, new_sizes)
+    elif scheme == "simple":
+        new_sizes = []
+        for g in range(r):                                     # delivery.py:78-80
+            m = int(plan.loads[g])
+            for t in range(sub):
+                new_sizes.append((m * (t + 1)) // sub - (m * t) // sub)
+    else:
+        raise ValueError(f"unknown delivery scheme {scheme!r}")
     info = LevelInfo(level, group_lo, n_g, br, drawn, sk, sp, hist, plan,
                      new_sizes)
     if with_stats:
-        pieces = np.zeros((P, r), np.int64)
-        for g in range(r):
-            pieces[:, g] = hist[:, bnd[g]:bnd[g + 1]].sum(axis=1)
-        info.stats = _exchange_stats(pieces, sub, list(range(P)))
-    return out, out_vals, new_sizes, info
+        if scheme == "deterministic":
+            info.stats = _deterministic_stats(pieces, slices)
+        else:
+            info.stats = _exchange_stats(pieces, sub, list(range(P)))
+    return out, out_vals, new_sizes, info, out_org
 
 
 @dataclass
@@ -266,8 +406,9 @@ def ams_sort(keys: np.ndarray, pe_sizes: list, group_counts: tuple,
              oversampling: float | None = None, overpartition: int = 16,
              imbalance: float = 0.2, master_seed: int = 0,
              stream: str = "root", vals: np.ndarray | None = None,
-             with_stats: bool = True) -> SortResult:
-    """Restatement of ``ams_sort`` with ``scheme="simple"`` (ams.py:271-313).
+             with_stats: bool = True, scheme: str = "simple") -> SortResult:
+    """Restatement of ``ams_sort`` (ams.py:271-313) with ``scheme`` "simple"
+    (delivery.py:151-180) or "deterministic" (delivery.py:188-306).
     ``keys`` is the PE-major concatenation of the per-PE inputs (uint64)."""
     keys = np.ascontiguousarray(keys, dtype=U64)
     p = len(pe_sizes)
@@ -279,6 +420,7 @@ def ams_sort(keys: np.ndarray, pe_sizes: list, group_counts: tuple,
     eps_l = (1.0 + imbalance) ** (1.0 / k) - 1.0               # ams.py:58-59
     buf = keys.copy()
     vbuf = None if vals is None else np.asarray(vals).copy()
+    obuf = np.arange(n, dtype=np.int64)                        # origin tags
     sizes = [int(s) for s in pe_sizes]
     groups = [(0, p)]                                          # (lo, count)
     all_levels = []
@@ -286,17 +428,19 @@ def ams_sort(keys: np.ndarray, pe_sizes: list, group_counts: tuple,
     for lv, r in enumerate(group_counts):
         offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
         new_buf = np.empty_like(buf)
+        new_obuf = np.empty_like(obuf)
         new_vbuf = None if vbuf is None else np.empty_like(vbuf)
         new_sizes = list(sizes)
         infos = []
         next_groups = []
         for lo, cnt in groups:
             gs, ge = int(offs[lo]), int(offs[lo + cnt])
-            out, out_v, ns, info = ams_level(
+            out, out_v, ns, info, out_o = ams_level(
                 buf[gs:ge], sizes[lo:lo + cnt], r, overpartition, a,
                 master_seed, stream, lv, lo,
-                None if vbuf is None else vbuf[gs:ge], with_stats)
+                None if vbuf is None else vbuf[gs:ge], with_stats, scheme, obuf[gs:ge])
             new_buf[gs:ge] = out
+            new_obuf[gs:ge] = out_o
             if new_vbuf is not None:
                 new_vbuf[gs:ge] = out_v
             new_sizes[lo:lo + cnt] = ns
@@ -305,7 +449,7 @@ def ams_sort(keys: np.ndarray, pe_sizes: list, group_counts: tuple,
             infos.append(info)
             step = cnt // r
             next_groups.extend((lo + i * step, step) for i in range(r))
-        buf, vbuf, sizes, groups = new_buf, new_vbuf, new_sizes, next_groups
+        buf, vbuf, obuf, sizes, groups = new_buf, new_vbuf, new_obuf, new_sizes, next_groups
         all_levels.append(infos)
         rep = {"level": lv + 1, "r": r, "max_load": max(sizes),
                "min_load": min(sizes),
@@ -316,11 +460,12 @@ def ams_sort(keys: np.ndarray, pe_sizes: list, group_counts: tuple,
             for key in ("max_words", "max_msgs", "max_sent_msgs", "max_recv_msgs"):
                 rep[key] = max(i.stats[key] for i in infos)
         reports.append(rep)
-    # Final local sort, stable by key (ams.py:310-312; F6).
+    # Final local sort by (key, origin) (ams.py:310-312; a stable key sort
+    # under "simple", F6).
     offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
     for pe in range(p):
         s, e = int(offs[pe]), int(offs[pe + 1])
-        order = np.argsort(buf[s:e], kind="stable")
+        order = np.lexsort((obuf[s:e], buf[s:e]))
         buf[s:e] = buf[s:e][order]
         if vbuf is not None:
             vbuf[s:e] = vbuf[s:e][order]

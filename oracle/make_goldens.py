@@ -40,7 +40,7 @@ def sha_i64(values) -> str:
 
 
 def run_case(name, data, p, groups, a, b, eps, master_seed, stream, meta,
-             store_data=False):
+             store_data=False, scheme="simple"):
     mp = reference_loader.load()
     from mlpsort import ams
     from mlpsort.core import SeedSpec
@@ -107,7 +107,20 @@ def run_case(name, data, p, groups, a, b, eps, master_seed, stream, meta,
                                overpartition=b, imbalance=eps)
         seed = SeedSpec(master_seed, stream)
         t0 = time.perf_counter()
-        out, reports = ams.ams_sort(net, data, params, "simple", seed)
+        try:
+            out, reports = ams.ams_sort(net, data, params, scheme, seed)
+        except (ValueError, RuntimeError) as exc:
+            # The reference rejects this input (e.g. deliver_deterministic's
+            # piece bound, delivery.py:212-217): the fixture pins the error.
+            rec = dict(meta)
+            rec.update({"name": name, "p": p, "groups": list(groups), "a": a, "b": b,
+                        "eps": eps, "master_seed": master_seed, "stream": stream,
+                        "scheme": scheme, "input_pe_sizes": [len(data[pe]) for pe in range(p)],
+                        "error": {"type": type(exc).__name__, "message": str(exc)}})
+            if store_data:
+                rec["data"] = {str(pe): [[int(e.key), e.origin_pe, e.origin_pos]
+                                         for e in data[pe]] for pe in range(p)}
+            return rec
         wall = time.perf_counter() - t0
     finally:
         ams.ams_level = orig_level
@@ -118,7 +131,7 @@ def run_case(name, data, p, groups, a, b, eps, master_seed, stream, meta,
     rec.update({
         "name": name, "p": p, "groups": list(groups), "a": a, "b": b,
         "eps": eps, "master_seed": master_seed, "stream": stream,
-        "scheme": "simple",
+        "scheme": scheme,
         "input_pe_sizes": [len(data[pe]) for pe in range(p)],
         "input_sha256": sha_u64(in_keys),
         "output_sha256": sha_u64([e.key for e in flat]),
@@ -154,12 +167,12 @@ def cases():
     """(name, builder) pairs; builders return the fixture dict."""
     out = []
 
-    def cfg(name, dist, p, npe, groups, a, b, eps, seed, store=False):
+    def cfg(name, dist, p, npe, groups, a, b, eps, seed, store=False, scheme="simple"):
         def build():
             data = generated(dist, p, npe, seed)
             meta = {"dist": dist, "n_per_pe": npe, "input_seed": seed}
             return run_case(name, data, p, groups, a, b, eps, seed, "algo/rep0",
-                            meta, store_data=store)
+                            meta, store_data=store, scheme=scheme)
         out.append((name, build))
 
     # SURVEY §8(d) config 1, full size.
@@ -180,12 +193,28 @@ def cases():
         cfg(f"cfg4_scaled_{dist.replace(':', '')}", dist, 256, 256, (8, 32),
             None, 16, 0.1, 4)
 
-    def tiny(name, spec, groups, b=16, eps=0.2, seed=9):
+    # deliver_deterministic (the CLI / bench default scheme, delivery.py:188-306):
+    # it places members differently from "simple" on sorted / equal inputs.
+    for dist in ("uniform", "sorted", "reverse", "equal", "zipf:1.1"):
+        for groups, p in (((4, 4), 16), ((8, 2), 16), ((2, 2, 4), 16)):
+            tag = dist.replace(":", "") + "_" + "x".join(map(str, groups))
+            cfg(f"det_{tag}", dist, p, 250, groups, None, 8, 0.2, 5, scheme="deterministic")
+    cfg("det_cfg2_scaled", "uniform", 64, 1 << 12, (8, 8), None, 16, 0.1, 1,
+        scheme="deterministic")
+    for dist in ("sorted", "equal"):
+        cfg(f"det_cfg4_scaled_{dist}", dist, 256, 128, (8, 32), None, 16, 0.1, 4,
+            scheme="deterministic")
+        # at (8, 8) sorted / equal inputs place members differently.
+        cfg(f"det_cfg2_scaled_{dist}", dist, 64, 1 << 12, (8, 8), None, 16, 0.1, 1,
+            scheme="deterministic")
+        cfg(f"simple_cfg2_scaled_{dist}", dist, 64, 1 << 12, (8, 8), None, 16, 0.1, 1)
+
+    def tiny(name, spec, groups, b=16, eps=0.2, seed=9, scheme="simple"):
         def build():
             data = explicit(spec)
             p = len(spec)
             return run_case(name, data, p, groups, None, b, eps, seed, "root",
-                            {"dist": "explicit"}, store_data=True)
+                            {"dist": "explicit"}, store_data=True, scheme=scheme)
         out.append((name, build))
 
     # test_ams.py:292-299 shape, with scheme simple.
@@ -201,6 +230,15 @@ def cases():
     rng = _r.Random(77)
     tiny("tiny_ragged", {pe: [rng.randrange(50) for _ in range(rng.randrange(0, 40))]
                          for pe in range(8)}, (2, 4), b=4, seed=3)
+    rng = _r.Random(77)
+    tiny("det_tiny_ragged", {pe: [rng.randrange(50) for _ in range(rng.randrange(0, 40))]
+                             for pe in range(8)}, (2, 4), b=4, seed=3, scheme="deterministic")
+    rng = _r.Random(5)
+    tiny("det_tiny_mixed", {pe: [rng.randrange(1 << 30) for _ in range(20 + 3 * pe)]
+                            for pe in range(8)}, (2, 4), b=4, seed=8, scheme="deterministic")
+    # One big PE: its piece exceeds ceil(n/p) (delivery.py:212-217 ValueError).
+    tiny("det_tiny_big_piece", {0: list(range(100)), 1: [5], 2: [7], 3: [9]}, (2, 2), b=4,
+         seed=2, scheme="deterministic")
     return out
 
 

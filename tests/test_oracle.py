@@ -44,13 +44,19 @@ def run_oracle(g):
     keys, sizes = G.input_of(g)
     vals = np.arange(len(keys), dtype=np.int64)
     res = O.ams_sort(keys, sizes, tuple(g["groups"]), g["a"], g["b"], g["eps"],
-                     g["master_seed"], g["stream"], vals=vals)
+                     g["master_seed"], g["stream"], vals=vals, scheme=g.get("scheme", "simple"))
     return res, keys
 
 
 @pytest.mark.parametrize("name", FAST)
 def test_oracle_matches_reference_golden(name):
     g = G.load(name)
+    if "error" in g:  # the reference rejects this input: same exception class and message
+        exc = {"ValueError": ValueError, "RuntimeError": RuntimeError}[g["error"]["type"]]
+        with pytest.raises(exc) as ei:
+            run_oracle(g)
+        assert str(ei.value) == g["error"]["message"]
+        return
     res, keys = run_oracle(g)
     check_against_golden(g, res, keys)
     assert np.array_equal(res.keys, np.sort(keys))
