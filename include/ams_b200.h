@@ -83,6 +83,18 @@ int ams_plan_level(int ngroups, const int32_t* group_npe, const int32_t* group_n
                    const uint32_t* seg_hist, int nb_stride, uint64_t* out_boundaries,
                    uint64_t* out_loads, uint64_t* out_max_load, uint64_t* out_new_sizes,
                    uint64_t* out_stats);
+/* deliver_deterministic (delivery.py:188-306) for one group: P members in r
+ * subgroups, pieces[P][r] = piece sizes; pe0 = first member's PE id (error
+ * messages).  Writes the new member sizes [P] and slices {src, dst, len}
+ * (src relative to the group's simple layout: subgroup, source member,
+ * bucket; dst relative to the group's new member arrays, receivers
+ * concatenating by source, simnet.py:324-325); slice_cap >= P*(r+1) is
+ * enough.  stats[4] as ams_plan_level (NULL skips).  AMS_EINVAL for a piece
+ * above ceil(n/p) (delivery.py:212-217), AMS_EINTERNAL when the residual
+ * capacities cannot hold the large pieces (delivery.py:274-276). */
+int ams_deliver_deterministic(int P, int r, int pe0, const uint64_t* pieces, uint64_t* out_new_sizes,
+                              uint64_t* out_slices, int slice_cap, int* out_nslices,
+                              uint64_t* out_stats);
 
 /* ------------------------------------------------------------------ */
 /* Device context: one per GPU (one process per GPU).                  */
@@ -202,6 +214,11 @@ int ams_map_keys(ams_ctx_t* ctx, const void* src, void* dst, uint64_t n, int fro
 #define AMS_MAX_LEVELS 8
 
 /* AmsParams (ams.py:33-65) + SeedSpec (core.py:46-71) + key encoding. */
+/* Delivery schemes (delivery.py:439-455 SCHEMES): "simple" (151-180) and
+ * "deterministic" (188-306, the reference CLI default). */
+#define AMS_SCHEME_SIMPLE 0
+#define AMS_SCHEME_DETERMINISTIC 1
+
 typedef struct {
   int levels;                          /* k = len(group_counts) */
   int group_counts[AMS_MAX_LEVELS];    /* r per level; product = p */
@@ -212,6 +229,7 @@ typedef struct {
   const char* stream_id;               /* SeedSpec.stream_id, e.g. "algo/rep0" */
   int key_kind;                        /* AMS_KEY_U64 / AMS_KEY_I64 / AMS_KEY_F64 */
   int with_stats;                      /* fill the exchange maxima of the reports */
+  int scheme;                          /* AMS_SCHEME_SIMPLE / AMS_SCHEME_DETERMINISTIC */
 } ams_params_t;
 
 /* One level's report (ams.py:294-308; exchange maxima simnet.py:109-124). */

@@ -41,6 +41,7 @@ _SIGNATURES = {
     "ams_scan_groups": (_I, [_P, _I, _I, _U64, _P, _P, _P]),
     "ams_group_plan": (_I, [_P, _I, _I, _P, _P, _P]),
     "ams_plan_level": (_I, [_I, _P, _P, _I, _P, _I, _P, _P, _P, _P, _P]),
+    "ams_deliver_deterministic": (_I, [_I, _I, _I, _P, _P, _P, _I, _P, _P]),
     "ams_ctx_create": (_I, [_I, _P, C.POINTER(_P)]),
     "ams_ctx_destroy": (_I, [_P]),
     "ams_ctx_set_stream": (_I, [_P, _P]),
@@ -74,7 +75,8 @@ class ParamsT(C.Structure):
     _fields_ = [("levels", C.c_int), ("group_counts", C.c_int * MAX_LEVELS),
                 ("oversampling", C.c_double), ("overpartition", C.c_int),
                 ("imbalance", C.c_double), ("master_seed", C.c_int64),
-                ("stream_id", C.c_char_p), ("key_kind", C.c_int), ("with_stats", C.c_int)]
+                ("stream_id", C.c_char_p), ("key_kind", C.c_int), ("with_stats", C.c_int),
+                ("scheme", C.c_int)]
 
 
 class LevelReportT(C.Structure):
@@ -223,6 +225,22 @@ def plan_level(group_npe, group_nb, r: int, seg_hist: np.ndarray, with_stats: bo
                              bnd.ctypes.data, loads.ctypes.data, mx.ctypes.data,
                              new_sizes.ctypes.data, ptr(stats)))
     return bnd, loads, mx, new_sizes, stats
+
+
+def deliver_deterministic(pieces: np.ndarray, pe0: int = 0, with_stats: bool = True):
+    """Host restatement of deliver_deterministic's member assignment
+    (delivery.py:188-306) for one group: pieces [P][r] -> (new member sizes,
+    slices [k][3] = (src, dst, len) relative to the group's simple layout /
+    new member arrays, stats[4] or None)."""
+    pc = np.ascontiguousarray(pieces, dtype=np.uint64)
+    P, r = pc.shape
+    ns = np.zeros(P, np.uint64)
+    slices = np.zeros((P * (r + 1), 3), np.uint64)
+    cnt = C.c_int(0)
+    stats = np.zeros(4, np.uint64) if with_stats else None
+    check(lib.ams_deliver_deterministic(P, r, int(pe0), pc.ctypes.data, ns.ctypes.data,
+                                        slices.ctypes.data, P * (r + 1), C.byref(cnt), ptr(stats)))
+    return ns, slices[:cnt.value].copy(), stats
 
 
 # ---------------------------------------------------------------- device context

@@ -24,7 +24,7 @@ from .params import Element, as_params
 
 _SORTERS: dict = {}
 
-SUPPORTED_SCHEMES = ("simple",)
+SUPPORTED_SCHEMES = ("simple", "deterministic")
 
 
 def get_sorter(device=None) -> AmsSorter:
@@ -40,7 +40,7 @@ def _check_scheme(scheme: str):
     if scheme not in SUPPORTED_SCHEMES:
         raise ValueError(
             f"delivery scheme {scheme!r} is not implemented on the B200 path; "
-            f"supported: {SUPPORTED_SCHEMES} (the reference's 'simple' layout, delivery.py:151-180)")
+            f"supported: {SUPPORTED_SCHEMES} (delivery.py:151-180, 188-306)")
 
 
 def ams_sort_tensors(keys: torch.Tensor, pe_sizes, params, seed, vals: torch.Tensor | None = None,
@@ -51,7 +51,7 @@ def ams_sort_tensors(keys: torch.Tensor, pe_sizes, params, seed, vals: torch.Ten
     _check_scheme(scheme)
     return get_sorter(keys.device).sort(keys, pe_sizes, params, seed, vals=vals, out=out,
                                         out_vals=out_vals, key_kind=key_kind,
-                                        record_splitters=record_splitters)
+                                        record_splitters=record_splitters, scheme=scheme)
 
 
 def ams_sort_host(keys: np.ndarray, pe_sizes, params, seed, vals: np.ndarray | None = None,
@@ -196,7 +196,7 @@ def ams_sort(net, data, params, scheme: str, seed):
     dev = torch.device("cuda", torch.cuda.current_device())
     d_keys = torch.from_numpy(keys.view(np.int64)).to(dev)
     d_vals = torch.arange(n, dtype=torch.int64, device=dev)
-    res = ams_sort_tensors(d_keys, sizes, params, seed, vals=d_vals, key_kind=kind)
+    res = ams_sort_tensors(d_keys, sizes, params, seed, vals=d_vals, key_kind=kind, scheme=scheme)
     order = res.vals.cpu().numpy()
     out, start = {}, 0
     for pe in range(p):

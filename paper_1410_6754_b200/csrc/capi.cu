@@ -132,6 +132,8 @@ struct Stage {
 
 using namespace ams;
 
+constexpr uint64_t kCopyItemKeys = 8192;  // keys per relayout work item (k_copy_ranges CTA)
+
 struct ams_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -161,6 +163,10 @@ struct ams_ctx {
   Stage st_fixed;
   uint64_t fixed_segments = 0, fixed_overflow_segments = 0;
   bool bm_final = true;  // AMS_FINAL_BM=0 keeps the (g(b), j, b) last level + PE digit partition
+  // deterministic delivery: origin tags (tie-breaks) and relayout work items
+  const uint64_t* level_tags = nullptr;
+  DevBuf tags0;
+  Stage st_copy;
   HostBuf h_small;
   uint64_t overflow_cells = 0, fallback_cells = 0;
   // one-call driver (ams_sort_run): workspace and the last run's level records
@@ -272,6 +278,7 @@ cudaError_t upload_segments(Stage& st, cudaStream_t stream, const uint64_t* off,
   m->chunk_prefix = st.dev<uint64_t>(o_cp);
   m->posbase = posbase ? st.dev<int64_t>(o_pb) : nullptr;
   m->nseg = nseg;
+  m->tags = nullptr;
   *nchunks = cp[nseg];
   return cudaSuccess;
 }
@@ -302,6 +309,9 @@ int level_scatter_impl(ams_ctx_t* c, const void* src, const void* src_vals, int 
                        void* dst, void* dst_vals, int r, const uint64_t* h_boundaries,
                        const uint64_t* h_group_dst_start, int child_first, int child_count,
                        bool bucket_major);
+int level_sample_impl(ams_ctx_t* c, const void* src, int key_kind, uint64_t count,
+                      const uint64_t* h_idx, const uint64_t* h_gpos, uint64_t* d_out_keys,
+                      uint32_t* d_out_pos, const uint64_t* tags);
 
 }  // namespace
 
@@ -331,14 +341,15 @@ int ams_ctx_destroy(ams_ctx_t* c) {
   cudaStreamSynchronize(c->stream);
   resolve_timing(c);
   for (cudaEvent_t e : c->free_events) cudaEventDestroy(e);
-  for (Stage* s : {&c->st_sample, &c->st_split, &c->st_level, &c->st_scatter, &c->st_final, &c->st_fixed})
+  for (Stage* s : {&c->st_sample, &c->st_split, &c->st_level, &c->st_scatter, &c->st_final, &c->st_fixed,
+                   &c->st_copy})
     s->release();
   for (DevBuf* b : {&c->blobs, &c->sorted_keys, &c->sorted_pos, &c->sample_idx, &c->bounds[0], &c->bounds[1],
                     &c->chunk_tot, &c->seg_hist, &c->cell_base, &c->pieces, &c->minmax, &c->dcls,
                     &c->ovf, &c->ovf_count, &c->fb, &c->fb_count, &c->groups, &c->ngroups_d,
                     &c->ids, &c->work[0], &c->work[1], &c->work_v[0], &c->work_v[1], &c->s_keys,
                     &c->s_pos, &c->fx_scratch, &c->fx_fill, &c->fx_ovf, &c->fx_base, &c->fx_cnt,
-                    &c->fx_seg})
+                    &c->fx_seg, &c->tags0})
     b->release();
   c->h_hist.release();
   c->h_small.release();
@@ -406,6 +417,17 @@ int ams_ctx_sync(ams_ctx_t* c) {
 int ams_level_sample(ams_ctx_t* c, const void* src, int key_kind, uint64_t count,
                      const uint64_t* h_idx, const uint64_t* h_gpos, uint64_t* d_out_keys,
                      uint32_t* d_out_pos) {
+  return level_sample_impl(c, src, key_kind, count, h_idx, h_gpos, d_out_keys, d_out_pos, nullptr);
+}
+
+}  // extern "C"
+
+namespace {
+
+// tags != NULL: the sample's tie-break value is its origin tag.
+int level_sample_impl(ams_ctx_t* c, const void* src, int key_kind, uint64_t count,
+                      const uint64_t* h_idx, const uint64_t* h_gpos, uint64_t* d_out_keys,
+                      uint32_t* d_out_pos, const uint64_t* tags) {
   if (!c) return set_error(AMS_EINVAL, "null context");
   if (count == 0) return AMS_OK;
   if (!src || !h_idx || !h_gpos || !d_out_keys || !d_out_pos)
@@ -418,11 +440,15 @@ int ams_level_sample(ams_ctx_t* c, const void* src, int key_kind, uint64_t count
   {
     KTimer kt(c, AMS_KCAT_SAMPLE, 12.0 * count);
     AMS_CK(launch_gather_sample(c->stream, src, key_kind, st.dev<uint64_t>(oi),
-                                st.dev<uint64_t>(og), count, d_out_keys, d_out_pos));
+                                st.dev<uint64_t>(og), count, d_out_keys, d_out_pos, tags));
   }
   c->launches += 1;
   return AMS_OK;
 }
+
+}  // namespace
+
+extern "C" {
 
 int ams_level_splitters(ams_ctx_t* c, int ngroups, const uint64_t* d_sample_keys,
                         const uint32_t* d_sample_pos, const uint64_t* h_soff, const int32_t* h_nb) {
@@ -521,6 +547,7 @@ int ams_level_classify(ams_ctx_t* c, const void* src, int key_kind, int nseg,
   }
   AMS_CK(upload_segments(c->st_level, c->stream, h_seg_off, h_seg_len, h_seg_group, nseg,
                          h_group_posbase, ngroups, &c->meta, &c->nchunks));
+  c->meta.tags = c->level_tags;  // origin tags of this level's buffer (deterministic, levels >= 2)
   c->nseg = nseg;
   c->nb_stride = nb_stride;
   unsigned long long* mm = nullptr;
@@ -949,6 +976,54 @@ int final_sort_bm(ams_ctx* c, void* src, void* tmp, void* out, int key_kind,
   return AMS_OK;
 }
 
+// Final sort with explicit per-segment key bounds [lo, hi] (no last-level
+// bounds needed): small segments straight into `out`, the rest through
+// the exact partition rounds.
+int final_sort_lohi(ams_ctx* c, void* src, void* src_vals, void* tmp, void* tmp_vals, void* out,
+                    void* out_vals, int key_kind, int nseg, const uint64_t* h_seg_off,
+                    const uint64_t* h_seg_len, const std::vector<uint64_t>& lo,
+                    const std::vector<uint64_t>& hi) {
+  std::vector<uint64_t> s_off, s_len, b_off, b_len, b_lo, b_hi;
+  uint64_t total = 0, small_n = 0;
+  for (int s = 0; s < nseg; ++s) {
+    total += h_seg_len[s];
+    if (h_seg_len[s] == 0) continue;
+    if (h_seg_len[s] <= (uint64_t)AMS_SMEM_SORT_CAP) {
+      s_off.push_back(h_seg_off[s]);
+      s_len.push_back(h_seg_len[s]);
+      small_n += h_seg_len[s];
+    } else {
+      b_off.push_back(h_seg_off[s]);
+      b_len.push_back(h_seg_len[s]);
+      b_lo.push_back(lo[s]);
+      b_hi.push_back(hi[s]);
+    }
+  }
+  const uint64_t rec_cap = total / (AMS_SMEM_SORT_CAP / 2) + 64;
+  AMS_CK(c->ovf.ensure(sizeof(OverflowRec) * rec_cap));
+  AMS_CK(c->fb.ensure(sizeof(OverflowRec) * rec_cap));
+  AMS_CK(c->ovf_count.ensure(sizeof(unsigned int)));
+  AMS_CK(c->fb_count.ensure(sizeof(unsigned int)));
+  AMS_CK(c->h_small.ensure(4096));
+  AMS_CK(cudaMemsetAsync(c->ovf_count.p, 0, sizeof(unsigned int), c->stream));
+  if (!s_off.empty()) {
+    Stage& ss = c->st_sample;
+    ss.reset();
+    const size_t oo = ss.put(s_off), ol = ss.put(s_len);
+    AMS_CK(ss.upload(c->stream));
+    CellSource cs{};
+    cs.mode = 1;
+    cs.seg_off = ss.dev<uint64_t>(oo);
+    cs.seg_len = ss.dev<uint64_t>(ol);
+    int rc = sort_cells(c, src, src_vals, out, out_vals, key_kind, cs, s_off.size(), small_n);
+    if (rc) return rc;
+  }
+  if (!b_off.empty())
+    return partition_rounds(c, src, src_vals, tmp, tmp_vals, out, out_vals, key_kind, b_off, b_len, b_lo,
+                            b_hi, nullptr);
+  return AMS_OK;
+}
+
 }  // namespace
 
 int ams_final_sort(ams_ctx_t* c, void* src, void* src_vals, void* tmp, void* tmp_vals, void* out,
@@ -1049,8 +1124,17 @@ int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* p
   uint64_t n = 0;
   for (int i = 0; i < p; ++i) n += pe_sizes[i];
   if (n && (!keys || !out)) return set_error(AMS_EINVAL, "null key buffer");
-  const bool with_vals = vals != nullptr;
-  if (with_vals && !out_vals) return set_error(AMS_EINVAL, "values need an output buffer");
+  const bool user_vals = vals != nullptr;
+  if (user_vals && !out_vals) return set_error(AMS_EINVAL, "values need an output buffer");
+  if (prm->scheme != AMS_SCHEME_SIMPLE && prm->scheme != AMS_SCHEME_DETERMINISTIC)
+    return set_error(AMS_EINVAL, "unknown delivery scheme");
+  // Deterministic delivery (delivery.py:188-306) can put a later source's
+  // piece into an earlier member, so group-buffer order stops being origin
+  // order: origin tags travel as the values and break key ties
+  // from level 2 on (and order the final sort); user values are gathered by
+  // tag at the end.
+  const bool det = prm->scheme == AMS_SCHEME_DETERMINISTIC && n > 0;
+  const bool with_vals = user_vals || det;
   AMS_CK(cudaSetDevice(c->device));
   // ams.py:278-280 and AmsParams.per_level_imbalance (ams.py:58-59).
   const double a = prm->oversampling > 0 ? prm->oversampling
@@ -1064,10 +1148,15 @@ int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* p
     AMS_CK(c->work[i].ensure(wb));
     if (with_vals) AMS_CK(c->work_v[i].ensure(wb));
   }
+  if (det) {
+    AMS_CK(c->tags0.ensure(wb));
+    AMS_CK(launch_iota(c->stream, c->tags0.p, n));
+    c->launches += 1;
+  }
   const void* src = n ? keys : c->work[1].p;
-  const void* src_v = with_vals ? (n ? vals : c->work_v[1].p) : nullptr;
+  const void* src_v = det ? c->tags0.p : (with_vals ? (n ? vals : c->work_v[1].p) : nullptr);
   void* dst_out = n ? out : c->work[1].p;
-  void* dst_out_v = with_vals ? (n ? out_vals : c->work_v[1].p) : nullptr;
+  void* dst_out_v = with_vals ? (n && !det ? out_vals : c->work_v[1].p) : nullptr;
   int src_kind = prm->key_kind;
   std::vector<uint64_t> sizes(pe_sizes, pe_sizes + p);
   std::vector<int32_t> gf{0}, gn{p};
@@ -1109,8 +1198,9 @@ int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* p
     const uint64_t S = soff[G];
     AMS_CK(c->s_keys.ensure(8 * (size_t)std::max<uint64_t>(S, 1)));
     AMS_CK(c->s_pos.ensure(4 * (size_t)std::max<uint64_t>(S, 1)));
-    if ((rc = ams_level_sample(c, src, src_kind, S, idx.data(), gpos.data(), c->s_keys.as<uint64_t>(),
-                               c->s_pos.as<uint32_t>())))
+    const uint64_t* tie_tags = det && lv > 0 ? static_cast<const uint64_t*>(src_v) : nullptr;
+    if ((rc = level_sample_impl(c, src, src_kind, S, idx.data(), gpos.data(), c->s_keys.as<uint64_t>(),
+                                c->s_pos.as<uint32_t>(), tie_tags)))
       return rc;
     if ((rc = ams_level_splitters(c, G, c->s_keys.as<uint64_t>(), c->s_pos.as<uint32_t>(),
                                   soff.data(), nb.data())))
@@ -1127,10 +1217,11 @@ int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* p
     rec.group_first = gf; rec.group_npe = gn; rec.nb = nb;
     rec.sizes_before = sizes; rec.drawn = drawn;
     rec.hist.assign((size_t)p * nb_stride, 0);
-    if ((rc = ams_level_classify(c, src, src_kind, p, offs.data(), sizes.data(), seg_group.data(), G,
-                                 posbase.data(), nb_stride, lv == 0, !(last && !with_vals),
-                                 rec.hist.data())))
-      return rc;
+    c->level_tags = tie_tags;
+    rc = ams_level_classify(c, src, src_kind, p, offs.data(), sizes.data(), seg_group.data(), G,
+                            posbase.data(), nb_stride, lv == 0, !(last && !with_vals), rec.hist.data());
+    c->level_tags = nullptr;
+    if (rc) return rc;
     rec.boundaries.assign((size_t)G * (r + 1), 0);
     rec.loads.assign((size_t)G * r, 0);
     rec.max_load.assign(G, 0);
@@ -1146,9 +1237,56 @@ int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* p
     void* dst = c->work[lv % 2].p;
     void* dst_v = with_vals ? c->work_v[lv % 2].p : nullptr;
     const bool bm = last && !with_vals && c->bm_final;
-    if ((rc = level_scatter_impl(c, src, src_v, src_kind, dst, dst_v, r, rec.boundaries.data(),
+    // Deterministic delivery where subgroups have several members: member
+    // assignment per group (host), the simple layout into scratch, then the
+    // slices copied to the members' arrays in receive order.
+    const bool relayout = det && gn[0] / r > 1;
+    std::vector<uint64_t> items;
+    if (relayout) {
+      std::vector<uint64_t> pieces, slices;
+      for (int g = 0; g < G; ++g) {
+        const int P = gn[g];
+        pieces.assign((size_t)P * r, 0);
+        for (int j = 0; j < P; ++j)
+          for (int t = 0; t < r; ++t)
+            for (uint64_t bb = rec.boundaries[(size_t)g * (r + 1) + t];
+                 bb < rec.boundaries[(size_t)g * (r + 1) + t + 1]; ++bb)
+              pieces[(size_t)j * r + t] += rec.hist[(size_t)(gf[g] + j) * nb_stride + bb];
+        slices.assign(3 * (size_t)P * (r + 1), 0);
+        int ns = 0;
+        if ((rc = ams_deliver_deterministic(P, r, gf[g], pieces.data(), rec.new_sizes.data() + gf[g],
+                                            slices.data(), P * (r + 1), &ns,
+                                            rec.has_stats ? rec.stats.data() + 4 * (size_t)g : nullptr)))
+          return rc;
+        for (int q = 0; q < ns; ++q) {
+          const uint64_t s0 = dst_start[g] + slices[3 * q], d0 = dst_start[g] + slices[3 * q + 1];
+          for (uint64_t o = 0; o < slices[3 * q + 2]; o += kCopyItemKeys) {
+            items.push_back(s0 + o);
+            items.push_back(d0 + o);
+            items.push_back(std::min<uint64_t>(kCopyItemKeys, slices[3 * q + 2] - o));
+          }
+        }
+      }
+    }
+    void* sdst = dst;
+    void* sdst_v = dst_v;
+    if (relayout) {  // scratch for the simple layout: the free work buffer / the output
+      sdst = lv == 0 ? c->work[1].p : dst_out;
+      sdst_v = lv == 0 ? c->work_v[1].p : c->tags0.p;
+    }
+    if ((rc = level_scatter_impl(c, src, src_v, src_kind, sdst, sdst_v, r, rec.boundaries.data(),
                                  dst_start.data(), 0, G * r, bm)))
       return rc;
+    if (relayout) {
+      Stage& sc = c->st_copy;
+      sc.reset();
+      const size_t oi = sc.put(items);
+      AMS_CK(sc.upload(c->stream));
+      KTimer kt(c, AMS_KCAT_SCATTER, 32.0 * (double)n);
+      AMS_CK(launch_copy_ranges(c->stream, sc.dev<uint64_t>(oi), (int)(items.size() / 3), sdst, dst,
+                                sdst_v, dst_v, n));
+      c->launches += 1;
+    }
     used_bm = bm;
     // Level report (ams.py:258-268, 294-308).
     if (reports) {
@@ -1211,6 +1349,27 @@ int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* p
     if ((rc = final_sort_bm(c, const_cast<void*>(src), tmp, dst_out, prm->key_kind, bo, bl, bg, bb,
                             c->bounds[1 - c->bcur].as<uint64_t>())))
       return rc;
+  } else if (det && !user_vals) {
+    // Keys only: equal keys are indistinguishable, so a key sort suffices.
+    if ((rc = ams_final_sort(c, const_cast<void*>(src), nullptr, tmp, nullptr, dst_out, nullptr,
+                             prm->key_kind, p, offs.data(), sizes.data())))
+      return rc;
+  } else if (det) {
+    // Final order (key, origin): each PE by tag, then stably by key; the
+    // user's values are gathered by the sorted tags.
+    void* K = const_cast<void*>(src);
+    void* T = const_cast<void*>(src_v);
+    void* W = c->work[k % 2].p;
+    void* X = c->tags0.p;
+    std::vector<uint64_t> lo(p, 0), hi(p, n - 1);
+    if ((rc = final_sort_lohi(c, T, K, out, out_vals, X, W, AMS_KEY_U64, p, offs.data(), sizes.data(),
+                              lo, hi)))
+      return rc;
+    if ((rc = ams_final_sort(c, W, X, K, T, dst_out, c->work_v[k % 2].p, prm->key_kind, p, offs.data(),
+                             sizes.data())))
+      return rc;
+    AMS_CK(launch_gather_vals(c->stream, vals, c->work_v[k % 2].p, out_vals, n));
+    c->launches += 1;
   } else if ((rc = ams_final_sort(c, const_cast<void*>(src), const_cast<void*>(src_v), tmp, tmp_v, dst_out,
                                   dst_out_v, prm->key_kind, p, offs.data(), sizes.data()))) {
     return rc;

@@ -1,8 +1,9 @@
 // Consecutive-bucket grouping and the per-level delivery bookkeeping,
 // restated natively.
 //
-// Reference: _scan / scan_groups / optimal_group_plan (ams.py:78-154) and
-// the simple delivery's quota slots (delivery.py:78-106, 138-180) with the
+// Reference: _scan / scan_groups / optimal_group_plan (ams.py:78-154), the
+// simple delivery's quota slots (delivery.py:78-106, 138-180), the
+// deterministic delivery's member assignment (delivery.py:188-306) and the
 // exchange shape Network.exchange records (simnet.py:294-335).
 #include <algorithm>
 #include <cmath>
@@ -202,6 +203,124 @@ int ams_plan_level(int ngroups, const int32_t* group_npe, const int32_t* group_n
       exchange_stats(pieces, P, r, out_stats + (size_t)g * 4);
     }
     seg0 += P;
+  }
+  return AMS_OK;
+}
+
+// deliver_deterministic (delivery.py:188-306) for one group of P members
+// and r subgroups (members [g*P/r, (g+1)*P/r) form subgroup g), from the
+// piece sizes [P][r] (member j's buckets of group g).  Small pieces
+// (size*2*P*r <= n) go whole to member small_index / r of their subgroup;
+// large pieces fill the members' residual quota capacities in member order
+// (the merge of two prefix sums), so one piece spans consecutive members.
+// Receivers concatenate in source order (simnet.py:324-325).  Output, per
+// slice: {src, dst, len} with src relative to the start of the group's
+// simple layout (subgroup-major, then source member, then bucket) and dst
+// relative to the start of the group's new member arrays; new_sizes [P];
+// stats [4] as ams_plan_level (NULL: skip).
+int ams_deliver_deterministic(int P, int r, int pe0, const uint64_t* pieces, uint64_t* out_new_sizes,
+                              uint64_t* out_slices, int slice_cap, int* out_nslices,
+                              uint64_t* out_stats) {
+  if (P < 1 || r < 1 || P % r != 0)
+    return set_error(AMS_EINVAL, std::to_string(P) + " PEs cannot form " + std::to_string(r) + " groups");
+  const int sub = P / r;
+  unsigned __int128 n = 0;
+  for (int i = 0; i < P * r; ++i) n += pieces[i];
+  const uint64_t cap = (uint64_t)((n + (unsigned)P - 1) / (unsigned)P);  // ceil(n/p)
+  for (int j = 0; j < P; ++j)
+    for (int g = 0; g < r; ++g)
+      if (pieces[(size_t)j * r + g] > cap)
+        return set_error(AMS_EINVAL, "piece (" + std::to_string(pe0 + j) + "," + std::to_string(g) +
+                                         ") larger than ceil(n/p): " +
+                                         std::to_string(pieces[(size_t)j * r + g]) + " > " +
+                                         std::to_string(cap));
+  auto is_small = [&](uint64_t size) {
+    return (unsigned __int128)size * 2u * (unsigned)P * (unsigned)r <= n;
+  };
+  struct Cut { int j, g, t; uint64_t off, len; };
+  std::vector<Cut> cuts;
+  for (int g = 0; g < r; ++g) {
+    uint64_t m_g = 0;
+    for (int j = 0; j < P; ++j) m_g += pieces[(size_t)j * r + g];
+    std::vector<int64_t> small_load(sub, 0);
+    std::vector<std::pair<int, uint64_t>> larges;
+    uint64_t small_index = 0;
+    for (int j = 0; j < P; ++j) {
+      const uint64_t size = pieces[(size_t)j * r + g];
+      if (size == 0) continue;
+      if (!is_small(size)) { larges.push_back({j, size}); continue; }
+      const int t = (int)(small_index / (uint64_t)r);
+      ++small_index;
+      small_load[t] += (int64_t)size;
+      cuts.push_back({j, g, t, 0, size});
+    }
+    std::vector<uint64_t> bounds(sub + 1, 0);
+    for (int t = 0; t < sub; ++t) {
+      const uint64_t lo = (uint64_t)(((unsigned __int128)m_g * t) / sub);
+      const uint64_t hi = (uint64_t)(((unsigned __int128)m_g * (t + 1)) / sub);
+      const int64_t res = std::max<int64_t>(0, (int64_t)(hi - lo) - small_load[t]);
+      bounds[t + 1] = bounds[t] + (uint64_t)res;
+    }
+    uint64_t pos = 0;
+    for (const auto& [j, size] : larges) {
+      // bisect_right(bounds, pos) - 1
+      int t = (int)(std::upper_bound(bounds.begin(), bounds.end(), pos) - bounds.begin()) - 1;
+      uint64_t covered = 0;
+      while (covered < size) {
+        if (t >= sub) return set_error(AMS_EINTERNAL, "residual capacities cannot hold the large pieces");
+        const int64_t take = (int64_t)std::min(pos + size, bounds[t + 1]) - (int64_t)(pos + covered);
+        if (take > 0) {
+          cuts.push_back({j, g, t, covered, (uint64_t)take});
+          covered += (uint64_t)take;
+        }
+        ++t;
+      }
+      pos += size;
+    }
+  }
+  if ((int)cuts.size() > slice_cap) return set_error(AMS_EINTERNAL, "slice buffer too small");
+  // New member sizes and receive order (by source member).
+  std::vector<uint64_t> ns(P, 0);
+  for (const Cut& c : cuts) ns[(size_t)c.g * sub + c.t] += c.len;
+  std::vector<uint64_t> mbase(P + 1, 0);
+  for (int d = 0; d < P; ++d) mbase[d + 1] = mbase[d] + ns[d];
+  std::vector<uint64_t> gstart(r + 1, 0), pstart((size_t)P * r, 0);
+  for (int g = 0; g < r; ++g) {
+    uint64_t run = gstart[g];
+    for (int j = 0; j < P; ++j) { pstart[(size_t)j * r + g] = run; run += pieces[(size_t)j * r + g]; }
+    gstart[g + 1] = run;
+  }
+  std::vector<int> order(cuts.size());
+  for (size_t i = 0; i < cuts.size(); ++i) order[i] = (int)i;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+    const int da = cuts[a].g * sub + cuts[a].t, db = cuts[b].g * sub + cuts[b].t;
+    return da != db ? da < db : cuts[a].j < cuts[b].j;
+  });
+  std::vector<uint64_t> fill(P, 0);
+  std::vector<uint64_t> sw(P, 0), rw(P, 0), sm(P, 0), rm(P, 0);
+  int k = 0;
+  for (int i : order) {
+    const Cut& c = cuts[i];
+    const int d = c.g * sub + c.t;
+    out_slices[3 * k + 0] = pstart[(size_t)c.j * r + c.g] + c.off;
+    out_slices[3 * k + 1] = mbase[d] + fill[d];
+    out_slices[3 * k + 2] = c.len;
+    fill[d] += c.len;
+    if (c.len > 0 && d != c.j) { sw[c.j] += c.len; rw[d] += c.len; sm[c.j] += 1; rm[d] += 1; }
+    ++k;
+  }
+  *out_nslices = k;
+  std::copy(ns.begin(), ns.end(), out_new_sizes);
+  if (out_stats) {
+    uint64_t hs = 0, hr = 0, ms = 0, mr = 0;
+    for (int j = 0; j < P; ++j) {
+      hs = std::max(hs, sw[j]); hr = std::max(hr, rw[j]);
+      ms = std::max(ms, sm[j]); mr = std::max(mr, rm[j]);
+    }
+    out_stats[0] = std::max(hs, hr);
+    out_stats[1] = std::max(ms, mr);
+    out_stats[2] = ms;
+    out_stats[3] = mr;
   }
   return AMS_OK;
 }

@@ -41,11 +41,38 @@ constexpr uint32_t kInvalid = 0xFFFFFFFFu;
 template <int KIND>
 __global__ void k_gather_sample(const uint64_t* __restrict__ src, const uint64_t* __restrict__ idx,
                                 const uint64_t* __restrict__ gpos, uint64_t n,
-                                uint64_t* __restrict__ out_keys, uint32_t* __restrict__ out_pos) {
+                                uint64_t* __restrict__ out_keys, uint32_t* __restrict__ out_pos,
+                                const uint64_t* __restrict__ tags) {
   const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   out_keys[i] = to_ordered<KIND>(src[idx[i]]);
-  out_pos[i] = (uint32_t)gpos[i];
+  out_pos[i] = tags ? (uint32_t)tags[idx[i]] : (uint32_t)gpos[i];
+}
+
+// Deterministic delivery relayout: work item w copies up to kCopyItem keys
+// of one range (ranges pre-split on the host).
+constexpr uint64_t kCopyItem = 8192;
+__global__ void k_copy_ranges(const uint64_t* __restrict__ items, const uint64_t* __restrict__ src,
+                              uint64_t* __restrict__ dst, const uint64_t* __restrict__ src_vals,
+                              uint64_t* __restrict__ dst_vals) {
+  const uint64_t s0 = items[3 * blockIdx.x], d0 = items[3 * blockIdx.x + 1], len = items[3 * blockIdx.x + 2];
+  for (uint64_t i = threadIdx.x; i < len; i += blockDim.x) {
+    dst[d0 + i] = src[s0 + i];
+    if (src_vals) dst_vals[d0 + i] = src_vals[s0 + i];
+  }
+}
+
+__global__ void k_iota(uint64_t* __restrict__ dst, uint64_t n) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    dst[i] = i;
+}
+
+__global__ void k_gather_vals(const uint64_t* __restrict__ vals, const uint64_t* __restrict__ idx,
+                              uint64_t* __restrict__ out, uint64_t n) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = vals[idx[i]];
 }
 
 // -------------------------------------------------------------------- K2
@@ -147,7 +174,7 @@ __global__ void __launch_bounds__(1024) k_build_cls(const uint64_t* __restrict__
 // add it to the segment histogram.
 // IDS: also store every key's bucket (< 256) as a byte at its buffer index,
 // so the level's scatter does not classify again.
-template <int KIND, bool DIGIT, bool MINMAX, bool IDS>
+template <int KIND, bool DIGIT, bool MINMAX, bool IDS, bool TAGS = false>
 __global__ void __launch_bounds__(kThreads) k_hist(const uint64_t* __restrict__ src, SegMeta m,
                                                    const uint8_t* __restrict__ blobs,
                                                    const DigitCls* __restrict__ dcls, int nspl_cap,
@@ -199,6 +226,7 @@ __global__ void __launch_bounds__(kThreads) k_hist(const uint64_t* __restrict__ 
       if (FULL || e < tcount) {
         uint32_t b;
         if constexpr (DIGIT) b = dv.classify(keys[i], 0);
+        else if constexpr (TAGS) b = tv.classify(keys[i], (uint32_t)m.tags[base + e]);
         else b = tv.classify(keys[i], (uint32_t)((int64_t)base + posbase) + e);
         if constexpr (IDS) ids[base + e] = (uint8_t)b;
         if constexpr (MINMAX) { mn = min(mn, (unsigned long long)keys[i]); mx = max(mx, (unsigned long long)keys[i]); }
@@ -375,6 +403,7 @@ __global__ void k_child_bounds(const uint8_t* __restrict__ blobs, GroupMeta gm, 
 // -------------------------------------------------------------------- K6
 // Ranking modes of the scatter.
 constexpr int kClsTree = 0, kClsDigit = 1, kClsIds = 2;
+constexpr int kClsTreeTags = 3;  // tree, tie-break by the carried origin tag (the values)
 constexpr int kRankWarp = 0;     // stable, one bucket-counter array per warp
 constexpr int kRankSerial = 1;   // stable, one shared array, warps take turns
 constexpr int kRankAtomic = 2;   // unstable (keys only, order inside a run is free)
@@ -468,7 +497,7 @@ __global__ void __launch_bounds__(kThreads, VALS ? 2 : 4)
   int64_t posbase = 0;
   if constexpr (CLS == kClsDigit) {
     dv.c = dcls[cls];
-  } else if constexpr (CLS == kClsTree) {
+  } else if constexpr (CLS == kClsTree || CLS == kClsTreeTags) {
     tv = load_tree(blobs + (size_t)cls * kBlobStride, clsmem, nspl_cap);
     posbase = m.posbase[cls];
   }
@@ -500,6 +529,7 @@ __global__ void __launch_bounds__(kThreads, VALS ? 2 : 4)
           } else {
             const uint64_t key = to_ordered<KIND>(keys_s[e]);
             if constexpr (CLS == kClsDigit) b = dv.classify(key, 0);
+            else if constexpr (CLS == kClsTreeTags) b = tv.classify(key, (uint32_t)vals_s[e]);
             else b = tv.classify(key, pos0 + e);
           }
         }
@@ -1553,11 +1583,36 @@ __global__ void k_map_keys(const uint64_t* __restrict__ src, uint64_t* __restric
 
 cudaError_t launch_gather_sample(cudaStream_t st, const void* src, int kind, const uint64_t* idx,
                                  const uint64_t* gpos, uint64_t n, uint64_t* out_keys,
-                                 uint32_t* out_pos) {
+                                 uint32_t* out_pos, const uint64_t* tags) {
   if (n == 0) return cudaSuccess;
   const unsigned blocks = (unsigned)((n + 255) / 256);
   AMS_KIND_DISPATCH(kind, K, k_gather_sample<K><<<blocks, 256, 0, st>>>(
-      static_cast<const uint64_t*>(src), idx, gpos, n, out_keys, out_pos));
+      static_cast<const uint64_t*>(src), idx, gpos, n, out_keys, out_pos, tags));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_copy_ranges(cudaStream_t st, const uint64_t* items, int nitems, const void* src,
+                               void* dst, const void* src_vals, void* dst_vals, uint64_t) {
+  if (nitems == 0) return cudaSuccess;
+  k_copy_ranges<<<(unsigned)nitems, 256, 0, st>>>(items, static_cast<const uint64_t*>(src),
+                                                  static_cast<uint64_t*>(dst),
+                                                  static_cast<const uint64_t*>(src_vals),
+                                                  static_cast<uint64_t*>(dst_vals));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_iota(cudaStream_t st, void* dst, uint64_t n) {
+  if (n == 0) return cudaSuccess;
+  const unsigned blocks = (unsigned)std::min<uint64_t>((n + 255) / 256, 148 * 16);
+  k_iota<<<blocks, 256, 0, st>>>(static_cast<uint64_t*>(dst), n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_vals(cudaStream_t st, const void* vals, const void* idx, void* out, uint64_t n) {
+  if (n == 0) return cudaSuccess;
+  const unsigned blocks = (unsigned)std::min<uint64_t>((n + 255) / 256, 148 * 16);
+  k_gather_vals<<<blocks, 256, 0, st>>>(static_cast<const uint64_t*>(vals),
+                                        static_cast<const uint64_t*>(idx), static_cast<uint64_t*>(out), n);
   return cudaGetLastError();
 }
 
@@ -1597,6 +1652,13 @@ cudaError_t launch_hist(cudaStream_t st, const void* src, int kind, bool digit, 
     if (e != cudaSuccess) return e;
     fn<<<(unsigned)nchunks, kThreads, smem, st>>>(s, m, blobs, dcls, nspl_cap, nb_stride,
                                                    chunk_tot, seg_hist, minmax, nullptr);
+  } else if (m.tags) {
+    // Origin-tag tie-breaks (deterministic delivery, levels >= 2): keys are order-mapped u64.
+    auto fn = ids ? k_hist<AMS_KEY_U64, false, false, true, true> : k_hist<AMS_KEY_U64, false, false, false, true>;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    fn<<<(unsigned)nchunks, kThreads, smem, st>>>(s, m, blobs, dcls, nspl_cap, nb_stride, chunk_tot,
+                                                   seg_hist, minmax, ids);
   } else {
     AMS_KIND_DISPATCH(kind, K, {
       auto fn = minmax ? (ids ? k_hist<K, false, true, true> : k_hist<K, false, true, false>)
@@ -1742,6 +1804,9 @@ cudaError_t launch_scatter(cudaStream_t st, const void* src, const void* src_val
   }
   if (digit) {
     if (vals) AMS_SCATTER_GO(AMS_KEY_U64, kClsDigit, true) else AMS_SCATTER_GO(AMS_KEY_U64, kClsDigit, false)
+  } else if (m.tags && !ids) {
+    if (!vals || mode == kRankAtomic) return cudaErrorInvalidValue;  // tags travel as the values
+    AMS_SCATTER_GO(AMS_KEY_U64, kClsTreeTags, true)
   } else if (ids) {
     if (vals) {
       AMS_KIND_DISPATCH(kind, K, AMS_SCATTER_GO(K, kClsIds, true))

@@ -16,6 +16,7 @@ struct SegMeta {
   const uint64_t* chunk_prefix;  // [nseg+1] first global chunk of each segment
   const int64_t* posbase;        // [ncls] tie-break position = index + posbase
   int nseg;
+  const uint64_t* tags;          // origin tags (deterministic delivery, levels >= 2): tie-break by tag
 };
 
 // Groups of one level (contiguous runs of segments).
@@ -47,9 +48,18 @@ struct CellSource {
   const uint32_t* cell0;
 };
 
+// tags != NULL: the sample's tie-break value is its origin tag (tags[idx]),
+// else its group position gpos.
 cudaError_t launch_gather_sample(cudaStream_t st, const void* src, int kind, const uint64_t* idx,
                                  const uint64_t* gpos, uint64_t n, uint64_t* out_keys,
-                                 uint32_t* out_pos);
+                                 uint32_t* out_pos, const uint64_t* tags);
+// Copy ranges {src, dst, len} of keys (and values) — the deterministic
+// delivery's relayout.
+cudaError_t launch_copy_ranges(cudaStream_t st, const uint64_t* ranges, int nranges, const void* src,
+                               void* dst, const void* src_vals, void* dst_vals, uint64_t total);
+cudaError_t launch_iota(cudaStream_t st, void* dst, uint64_t n);
+// out[i] = vals[idx[i]]
+cudaError_t launch_gather_vals(cudaStream_t st, const void* vals, const void* idx, void* out, uint64_t n);
 cudaError_t launch_sample_rank(cudaStream_t st, int ngroups, uint64_t max_s, const uint64_t* keys,
                                const uint32_t* pos, const uint64_t* soff, uint64_t* sorted_keys,
                                uint32_t* sorted_pos);

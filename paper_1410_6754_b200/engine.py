@@ -40,6 +40,10 @@ def key_kind_of(t: torch.Tensor, key_kind=None) -> int:
     return _KIND_OF_DTYPE[t.dtype]
 
 
+# Delivery schemes (delivery.py:439-455 SCHEMES) the device path implements.
+SCHEMES = {"simple": 0, "deterministic": 1}  # AMS_SCHEME_SIMPLE / AMS_SCHEME_DETERMINISTIC
+
+
 @dataclass
 class LevelRecord:
     """Host-side facts of one level (all groups), for reports and parity."""
@@ -130,11 +134,16 @@ class AmsSorter:
     # -- main entry ---------------------------------------------------------
     def sort(self, keys: torch.Tensor, pe_sizes, params: AmsParams, seed, vals=None, out=None,
              out_vals=None, key_kind=None, record_splitters: bool = False,
-             with_stats: bool = True) -> SortOutput:
+             with_stats: bool = True, scheme: str = "simple") -> SortOutput:
         """Sort ``keys`` (1-D, PE-major: PE i owns the next ``pe_sizes[i]``
-        keys) exactly as ams_sort(scheme="simple") orders them; returns the
-        sorted keys (concatenation of per-PE outputs), per-PE sizes and
-        per-level records."""
+        keys) exactly as ams_sort(scheme) orders them ("simple" or
+        "deterministic"); returns the sorted keys (concatenation of per-PE
+        outputs), per-PE sizes and per-level records."""
+        if scheme not in SCHEMES:
+            raise ValueError(f"unknown delivery scheme {scheme!r}; supported: {tuple(SCHEMES)}")
+        if record_splitters and scheme != "simple":
+            raise ValueError("record_splitters runs the per-level host driver, which implements "
+                             "the simple scheme only")
         params = as_params(params)
         master, stream_id = as_seed(seed)
         if keys.dim() != 1 or not keys.is_cuda:
@@ -170,7 +179,8 @@ class AmsSorter:
         if not record_splitters:
             # The whole level loop in C++ (ams_sort_run); same steps as below.
             return self._sort_native(keys, vals, ret_out, ret_vals, out, out_vals, sizes, params,
-                                     master, stream_id, kind, with_stats, launches0, n)
+                                     master, stream_id, kind, with_stats, launches0, n,
+                                     SCHEMES[scheme])
         a = params.oversampling_for(n)                               # ams.py:278-280
         eps_l = params.per_level_imbalance()
         b = params.overpartition
@@ -230,7 +240,7 @@ class AmsSorter:
         return SortOutput(ret_out, ret_vals, sizes, levels, self.ctx.launches - launches0)
 
     def _sort_native(self, keys, vals, ret_out, ret_vals, out, out_vals, sizes, params, master,
-                     stream_id, kind, with_stats, launches0, n):
+                     stream_id, kind, with_stats, launches0, n, scheme=0):
         prm = L.ParamsT()
         gc = tuple(params.group_counts)
         if len(gc) > L.MAX_LEVELS:
@@ -245,6 +255,7 @@ class AmsSorter:
         prm.stream_id = stream_id.encode()
         prm.key_kind = int(kind)
         prm.with_stats = int(bool(with_stats))
+        prm.scheme = int(scheme)
         final_sizes, _ = self.ctx.sort_run(prm, sizes, keys if n else None,
                                            vals if n else None, out if n else None,
                                            out_vals if n else None)

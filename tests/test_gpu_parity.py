@@ -7,6 +7,8 @@ reference when the sample streams are the same; per-PE sizes within
 (1+eps)·n/p where the reference met its budget; stable payload order.
 """
 
+import re
+
 import numpy as np
 import pytest
 import torch
@@ -31,13 +33,14 @@ def host_u64(t: torch.Tensor) -> np.ndarray:
     return t.cpu().numpy().view(np.uint64)
 
 
-def run_gpu(api, keys, sizes, groups, a, b, eps, master, stream, vals=True, record=True):
+def run_gpu(api, keys, sizes, groups, a, b, eps, master, stream, vals=True, record=True,
+            scheme="simple"):
     from paper_1410_6754_b200 import AmsParams, SeedSpec
     d_keys = dev_u64(keys)
     d_vals = torch.arange(len(keys), dtype=torch.int64, device="cuda") if vals else None
     res = api.ams_sort_tensors(d_keys, sizes, AmsParams(tuple(groups), a, b, eps),
                                SeedSpec(master, stream), vals=d_vals, key_kind="u64",
-                               record_splitters=record)
+                               record_splitters=record, scheme=scheme)
     torch.cuda.synchronize()
     return res
 
@@ -74,10 +77,19 @@ def test_golden_parity(api, name, native):
     Python level loop over the level entry points (which also reads the
     splitters back for comparison)."""
     g = G.load(name)
+    scheme = g.get("scheme", "simple")
+    if scheme != "simple" and not native:
+        pytest.skip("the per-level host driver implements the simple scheme only")
     keys, sizes = G.input_of(g)
+    if "error" in g:  # the reference rejects this input: same exception class and message
+        exc = {"ValueError": ValueError, "RuntimeError": RuntimeError}[g["error"]["type"]]
+        with pytest.raises(exc, match=re.escape(g["error"]["message"])):
+            run_gpu(api, keys, sizes, g["groups"], g["a"], g["b"], g["eps"], g["master_seed"],
+                    g["stream"], record=False, scheme=scheme)
+        return
     assert G.sha_u64(keys) == g["input_sha256"]
     res = run_gpu(api, keys, sizes, g["groups"], g["a"], g["b"], g["eps"], g["master_seed"],
-                  g["stream"], record=not native)
+                  g["stream"], record=not native, scheme=scheme)
     out = host_u64(res.keys)
     assert [int(x) for x in res.pe_sizes] == g["pe_sizes"]
     assert G.sha_u64(out) == g["output_sha256"]
@@ -85,7 +97,7 @@ def test_golden_parity(api, name, native):
     check_levels(res, g)
 
 
-@pytest.mark.parametrize("name", [n for n in G.names() if n.startswith("tiny")])
+@pytest.mark.parametrize("name", [n for n in G.names() if n.startswith(("tiny", "det_tiny"))])
 def test_dropin_elements(api, name):
     """ams_sort(net, data, params, scheme, seed) returns the reference's
     exact per-PE Element lists."""
@@ -98,8 +110,13 @@ def test_dropin_elements(api, name):
     g = G.load(name)
     p = g["p"]
     data = {pe: [Element(k, o, i) for k, o, i in g["data"][str(pe)]] for pe in range(p)}
-    out, reports = api.ams_sort(Net(p), data, AmsParams(tuple(g["groups"]), g["a"], g["b"], g["eps"]),
-                                "simple", SeedSpec(g["master_seed"], g["stream"]))
+    call = lambda: api.ams_sort(Net(p), data, AmsParams(tuple(g["groups"]), g["a"], g["b"], g["eps"]),
+                                g.get("scheme", "simple"), SeedSpec(g["master_seed"], g["stream"]))
+    if "error" in g:
+        with pytest.raises(ValueError, match=re.escape(g["error"]["message"])):
+            call()
+        return
+    out, reports = call()
     flat = [list(e) for pe in range(p) for e in out[pe]]
     assert flat == g["output"]
     assert [len(out[pe]) for pe in range(p)] == g["pe_sizes"]
@@ -148,6 +165,49 @@ def test_oracle_parity_random(api, groups, npe, dist, native):
                 sk, sp = rec.splitters[gi]
                 assert np.array_equal(sk, info.splitter_keys)
                 assert np.array_equal(sp.astype(np.int64), info.splitter_pos)
+    for mine, theirs in zip(res.reports, ref.reports):
+        for k, v in theirs.items():
+            assert mine[k] == v, (k, mine[k], v)
+
+
+@pytest.mark.parametrize("groups,npe,dist", [
+    ((8, 8), 1 << 12, "equal"), ((8, 8), 1 << 12, "sorted"), ((8, 8), 3000, "zipf"),
+    ((4, 4, 4), 1024, "few"), ((8, 32), 1 << 9, "equal"), ((2, 8), 5000, "uniform"),
+])
+@pytest.mark.parametrize("with_vals", [True, False], ids=["kv", "keys"])
+def test_oracle_parity_deterministic(api, groups, npe, dist, with_vals):
+    """scheme="deterministic" (delivery.py:188-306): member placement by the
+    two-phase assignment, ties broken by the carried origin tags."""
+    p = int(np.prod(groups))
+    n = p * npe
+    rng = np.random.default_rng(hash((groups, npe, dist, 7)) & 0xFFFF)
+    if dist == "uniform":
+        keys = rng.integers(0, 2**64, n, dtype=np.uint64)
+    elif dist == "zipf":
+        keys = O.zipf_keys(n, 13)
+    elif dist == "sorted":
+        keys = np.arange(n, dtype=np.uint64)
+    elif dist == "equal":
+        keys = np.full(n, 42, dtype=np.uint64)
+    else:
+        keys = rng.choice(np.array([0, 1, 2**40, 2**63, 2**64 - 1], dtype=np.uint64), n)
+    sizes = [npe] * p
+    vals = np.arange(n, dtype=np.int64)
+    ref = O.ams_sort(keys, sizes, groups, None, 16, 0.1, 78, "algo/rep0", vals=vals,
+                     scheme="deterministic")
+    res = run_gpu(api, keys, sizes, groups, None, 16, 0.1, 78, "algo/rep0", vals=with_vals,
+                  record=False, scheme="deterministic")
+    assert np.array_equal(host_u64(res.keys), ref.keys)
+    if with_vals:
+        assert np.array_equal(res.vals.cpu().numpy(), ref.vals)
+    assert [int(x) for x in res.pe_sizes] == list(ref.pe_sizes)
+    for rec, infos in zip(res.levels, ref.levels):
+        row = 0
+        for gi, info in enumerate(infos):
+            assert [int(x) for x in rec.boundaries[gi]] == list(info.plan.boundaries)
+            P = len(info.new_sizes)
+            assert [int(x) for x in rec.new_sizes[row:row + P]] == list(info.new_sizes)
+            row += P
     for mine, theirs in zip(res.reports, ref.reports):
         for k, v in theirs.items():
             assert mine[k] == v, (k, mine[k], v)

@@ -166,3 +166,58 @@ def test_errors_map_to_valueerror():
         L.group_plan([1, 2], 0)
     with pytest.raises(ValueError):
         L.plan_level([3], [4], 2, np.zeros((3, 4), np.uint32))  # 3 PEs cannot form 2 groups
+
+
+def test_deterministic_delivery_matches_oracle_random():
+    """The native deliver_deterministic assignment (delivery.py:188-306)
+    equals the oracle's restatement: sizes, receive-order layout, exchange
+    stats and the reference's error messages."""
+    rng = np.random.default_rng(0)
+    for trial in range(600):
+        r, sub = int(rng.integers(1, 6)), int(rng.integers(1, 6))
+        P = r * sub
+        if trial % 3 == 0:
+            pcs = rng.integers(0, 50, (P, r))
+        elif trial % 3 == 1:
+            pcs = rng.integers(0, 3, (P, r)) * rng.integers(0, 100, (P, r))
+        else:
+            pcs = np.zeros((P, r), np.int64)
+            for j in range(P):
+                pcs[j, rng.integers(0, r)] = rng.integers(0, 40)
+        try:
+            slices, sizes = O.deterministic_plan(pcs.astype(np.int64), 3)
+            err = None
+        except (ValueError, RuntimeError) as e:
+            err = (type(e), str(e))
+        if err:
+            with pytest.raises(err[0], match=re.escape(err[1])):
+                L.deliver_deterministic(pcs, 3)
+            continue
+        ns, sl, st = L.deliver_deterministic(pcs, 3)
+        assert [int(x) for x in ns] == sizes
+        e_layout = np.arange(int(pcs.sum()))
+        want = O.deterministic_relayout(e_layout, pcs.astype(np.int64), slices, sizes)
+        got = np.empty_like(e_layout)
+        for s0, d0, ln in sl:
+            got[int(d0):int(d0 + ln)] = e_layout[int(s0):int(s0 + ln)]
+        assert np.array_equal(got, want)
+        ref = O._deterministic_stats(pcs.astype(np.int64), slices)
+        assert [int(x) for x in st] == [ref[k] for k in ("max_words", "max_msgs", "max_sent_msgs",
+                                                         "max_recv_msgs")]
+
+
+@pytest.mark.parametrize("name", ["det_cfg2_scaled_equal", "det_reverse_2x2x4", "det_tiny_mixed"])
+def test_deterministic_delivery_matches_golden(name):
+    """Piece sizes from the oracle's level histograms and plans -> the native
+    assignment gives the reference's new member sizes (golden fixtures)."""
+    g = G.load(name)
+    keys, sizes = G.input_of(g)
+    res = O.ams_sort(keys, sizes, tuple(g["groups"]), g["a"], g["b"], g["eps"],
+                     g["master_seed"], g["stream"], scheme="deterministic")
+    for lv, infos in enumerate(res.levels):
+        r = g["groups"][lv]
+        for info, ref in zip(infos, g["levels"][lv]):
+            bnd = info.plan.boundaries
+            pcs = np.stack([info.hist[:, bnd[t]:bnd[t + 1]].sum(axis=1) for t in range(r)], axis=1)
+            ns, _, _ = L.deliver_deterministic(pcs, info.group_lo)
+            assert [int(x) for x in ns] == ref["new_sizes"]
