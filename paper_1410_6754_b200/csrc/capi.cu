@@ -1142,7 +1142,8 @@ int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* p
   const double eps_l = std::pow(1.0 + prm->imbalance, 1.0 / k) - 1.0;
   const int b = prm->overpartition;
   // Workspace (two ping-pong buffers) and one-element stand-ins for n == 0.
-  // +2 keys: the fixed-capacity partition reads whole 16-byte units past a segment end.
+  // +2 keys: the fixed-capacity partition (k_scatter_fixed) copies whole
+  // 16-byte units past a segment end.
   const size_t wb = 8 * ((size_t)std::max<uint64_t>(n, 1) + 2);
   for (int i = 0; i < 2; ++i) {
     AMS_CK(c->work[i].ensure(wb));

@@ -700,13 +700,14 @@ __global__ void __launch_bounds__(kThreadsU, 2)
   const uint64_t first = (c - m.chunk_prefix[s]) * (uint64_t)kChunk;
   const uint64_t last = min(first + (uint64_t)kChunk, m.len[s]);
   const int ntiles = (int)((last - first + kTile - 1) / kTile);
-  auto issue = [&](int t) {  // thread 0: bulk-load tile t's aligned body
+  // Tile t = keys [base, base + tc); the copy covers whole 16-byte units
+  // from the boundary base - h, so key e of the tile sits at buf[e + h]; when
+  // tc + h is odd the last key is outside the copy and thread 0 adds it.
+  auto issue = [&](int t) {
     const uint64_t base = seg_off + first + (uint64_t)t * kTile;
     const uint32_t tc = (uint32_t)min((uint64_t)kTile, last - first - (uint64_t)t * kTile);
     const uint32_t h = (uint32_t)(base & 1);
-    const uint64_t b0 = base + h, b1 = (base + tc) & ~1ULL;
-    const uint32_t bytes = b1 > b0 ? (uint32_t)(b1 - b0) * 8 : 0;
-    bulk_load(buf0 + (t & 1) * kBuf + 2 * h, src + b0, bytes, &s_bar[t & 1]);
+    bulk_load(buf0 + (t & 1) * kBuf, src + (base - h), ((tc + h) & ~1u) * 8, &s_bar[t & 1]);
   };
   if (tid == 0) issue(0);
   {
@@ -731,31 +732,38 @@ __global__ void __launch_bounds__(kThreadsU, 2)
     const uint64_t base = seg_off + first + (uint64_t)t * kTile;
     const uint32_t tc = (uint32_t)min((uint64_t)kTile, last - first - (uint64_t)t * kTile);
     const uint32_t h = (uint32_t)(base & 1);
-    const uint32_t e_end = (uint32_t)(((base + tc) & ~1ULL) - base);  // body = [h, e_end)
     if (tid == 0 && t + 1 < ntiles) {
       fence_proxy_async();
       issue(t + 1);
     }
     mbar_wait(&s_bar[t & 1], (uint32_t)(t >> 1) & 1u);
-    // Classify + rank.  Element e of the tile is at buf[e + 2h - h] = buf[e + h].
+    if ((tc + h) & 1) {  // the last key is outside the 16-byte copy
+      if (tid == 0) buf[tc - 1 + h] = src[base + tc - 1];
+      __syncthreads();
+    }
+    const uint64_t* tb = buf + h;
     uint64_t kr[kItemsU];
     uint32_t pk[kItemsU];
     const uint32_t pos0 = (uint32_t)((int64_t)base + posbase);
+    auto classify_all = [&](auto full_tag) {
+      constexpr bool FULL = decltype(full_tag)::value;
 #pragma unroll
-    for (int i = 0; i < kItemsU; ++i) {
-      const uint32_t e = w * (kItemsU * 32) + i * 32 + lane;
-      pk[i] = kInvalid;
-      if (e < tc) {
-        const uint64_t raw = (e >= h && e < e_end) ? buf[e + h] : src[base + e];
-        const uint64_t key = to_ordered<KIND>(raw);
-        uint32_t b;
-        if constexpr (CLS == kClsIds) b = ids[base + e];
-        else if constexpr (CLS == kClsDigit) b = dv.classify(key, 0);
-        else b = tv.classify(key, pos0 + e);
-        kr[i] = key;
-        pk[i] = (b << 16) | atomicAdd(&cnt[b], 1u);
+      for (int i = 0; i < kItemsU; ++i) {
+        const uint32_t e = w * (kItemsU * 32) + i * 32 + lane;
+        pk[i] = kInvalid;
+        if (FULL || e < tc) {
+          const uint64_t key = to_ordered<KIND>(tb[e]);
+          uint32_t b;
+          if constexpr (CLS == kClsIds) b = ids[base + e];
+          else if constexpr (CLS == kClsDigit) b = dv.classify(key, 0);
+          else b = tv.classify(key, pos0 + e);
+          kr[i] = key;
+          pk[i] = (b << 16) | atomicAdd(&cnt[b], 1u);
+        }
       }
-    }
+    };
+    if (tc == (uint32_t)kTile) classify_all(std::true_type{});
+    else classify_all(std::false_type{});
     __syncthreads();
     // Scan: thread t owns buckets [t*per, t*per + per).
     {
@@ -842,8 +850,9 @@ __global__ void __launch_bounds__(kThreadsU, 2)
   const int ntiles = (int)((last - first + kTile - 1) / kTile);
   const uint64_t cbase = cell0[s];
   // Tile t = keys [base, base + tc); the copy starts at the 16-byte boundary
-  // base - h and is rounded up to whole 16-byte units (the source buffer is
-  // padded by two keys), so key e of the tile sits at buf[e + h].
+  // base - h and is rounded up to whole 16-byte units (the source is the
+  // last level's work buffer, padded by two keys), so key e of the tile sits
+  // at buf[e + h].
   auto issue = [&](int t) {
     const uint64_t base = seg_off + first + (uint64_t)t * kTile;
     const uint32_t tc = (uint32_t)min((uint64_t)kTile, last - first - (uint64_t)t * kTile);
