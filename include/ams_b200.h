@@ -200,6 +200,10 @@ int ams_final_sort(ams_ctx_t* ctx, void* src, void* src_vals, void* tmp, void* t
 /* Cells of the final sort that needed another partition round / the LSD
  * fallback, summed since the context was created: out = {overflow, fallback}. */
 int ams_final_sort_stats(ams_ctx_t* ctx, uint64_t out[2]);
+/* Buckets of bucket-major keys-only last levels that took the fixed-capacity
+ * partition, and those of them whose cells overflowed (re-partitioned
+ * exactly), summed since the context was created: out = {buckets, overflowed}. */
+int ams_final_sort_fixed_stats(ams_ctx_t* ctx, uint64_t out[2]);
 
 /* Plain copy with key mapping (used for the p == 1 / k == 0 edge and the
  * host-buffer end-to-end path). */

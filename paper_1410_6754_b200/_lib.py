@@ -57,6 +57,7 @@ _SIGNATURES = {
     "ams_level_classify": (_I, [_P, _P, _I, _I, _P, _P, _P, _I, _P, _I, _I, _I, _P]),
     "ams_level_scatter": (_I, [_P, _P, _P, _I, _P, _P, _I, _P, _P, _I, _I]),
     "ams_final_sort_stats": (_I, [_P, _P]),
+    "ams_final_sort_fixed_stats": (_I, [_P, _P]),
     "ams_get_minmax": (_I, [_P, _P]),
     "ams_set_minmax": (_I, [_P, _P]),
     "ams_final_sort": (_I, [_P, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P]),
@@ -342,7 +343,10 @@ class Context:
     def final_sort_stats(self):
         out = np.zeros(2, np.uint64)
         check(lib.ams_final_sort_stats(self.h, out.ctypes.data))
-        return {"overflow_cells": int(out[0]), "fallback_cells": int(out[1])}
+        fx = np.zeros(2, np.uint64)
+        check(lib.ams_final_sort_fixed_stats(self.h, fx.ctypes.data))
+        return {"overflow_cells": int(out[0]), "fallback_cells": int(out[1]),
+                "fixed_buckets": int(fx[0]), "fixed_overflow_buckets": int(fx[1])}
 
     def get_minmax(self):
         out = np.zeros(2, np.uint64)

@@ -147,11 +147,23 @@ struct TreeView {
     const uint64_t sk = lds_u64(skeys + 8 * b);
     if (!(sk < key || (sk == key && lds_u32(spos + 4 * b) < pos))) return b;
     const uint32_t end = b + inside;
-    for (++b; b < end; ++b) {
-      const uint64_t sk2 = lds_u64(skeys + 8 * b);
-      if (!(sk2 < key || (sk2 == key && lds_u32(spos + 4 * b) < pos))) break;
+    if (inside <= 8) {
+      for (++b; b < end; ++b) {
+        const uint64_t sk2 = lds_u64(skeys + 8 * b);
+        if (!(sk2 < key || (sk2 == key && lds_u32(spos + 4 * b) < pos))) break;
+      }
+      return b;
     }
-    return b;
+    // Many splitters in one cell (duplicate-heavy keys: runs of equal
+    // splitter keys told apart by position): lower bound by (key, pos).
+    uint32_t lo = b + 1, hi = end;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      const uint64_t sk2 = lds_u64(skeys + 8 * mid);
+      if (sk2 < key || (sk2 == key && lds_u32(spos + 4 * mid) < pos)) lo = mid + 1;
+      else hi = mid;
+    }
+    return lo;
   }
 };
 

@@ -163,6 +163,7 @@ struct ams_ctx {
   Stage st_fixed;
   uint64_t fixed_segments = 0, fixed_overflow_segments = 0;
   bool bm_final = true;  // AMS_FINAL_BM=0 keeps the (g(b), j, b) last level + PE digit partition
+  int fixed_fill_pct = 88;  // AMS_FIXED_FILL: mean fill of the fixed-capacity cells (percent)
   // deterministic delivery: origin tags (tie-breaks) and relayout work items
   const uint64_t* level_tags = nullptr;
   DevBuf tags0;
@@ -331,6 +332,7 @@ int ams_ctx_create(int device, void* stream, ams_ctx_t** out) {
   c->device = device;
   c->stream = static_cast<cudaStream_t>(stream);
   if (const char* e = std::getenv("AMS_FINAL_BM")) c->bm_final = std::atoi(e) != 0;
+  if (const char* e = std::getenv("AMS_FIXED_FILL")) c->fixed_fill_pct = std::min(99, std::max(10, std::atoi(e)));
   *out = c;
   return AMS_OK;
 }
@@ -856,8 +858,9 @@ int final_sort_bm(ams_ctx* c, void* src, void* tmp, void* out, int key_kind,
                   const std::vector<int32_t>& bk_g, const std::vector<int32_t>& bk_b,
                   const uint64_t* d_group_bounds) {
   constexpr uint64_t kCap = AMS_SMEM_SORT_CAP;
-  // Cells average ~78% of capacity: uniform keys never overflow.
-  constexpr uint64_t kTarget = kCap * 78 / 100;
+  // Cells average fixed_fill_pct of capacity: with keys uniform inside a
+  // bucket a cell's count is ~ N(target, sqrt(target)), far below capacity.
+  const uint64_t kTarget = kCap * (uint64_t)c->fixed_fill_pct / 100;
   constexpr uint64_t kMaxDigits = AMS_MAX_BUCKETS / 2;
   std::vector<uint64_t> s_off, s_len, f_off, f_len;
   std::vector<int32_t> f_gb;
@@ -1079,6 +1082,13 @@ int ams_final_sort(ams_ctx_t* c, void* src, void* src_vals, void* tmp, void* tmp
                               b_lo, b_hi, &b_seg);
     if (rc) return rc;
   }
+  return AMS_OK;
+}
+
+int ams_final_sort_fixed_stats(ams_ctx_t* c, uint64_t out[2]) {
+  if (!c || !out) return set_error(AMS_EINVAL, "null argument");
+  out[0] = c->fixed_segments;
+  out[1] = c->fixed_overflow_segments;
   return AMS_OK;
 }
 

@@ -894,6 +894,16 @@ __global__ void __launch_bounds__(kThreadsU, 2)
     if (tc == (uint32_t)kTile) classify_all(std::true_type{});
     else classify_all(std::false_type{});
     __syncthreads();
+    if (dm == 0) {
+      // One key value per cell: only the counts matter (no capacity bound).
+      for (int b = tid; b < nbp; b += kThreadsU) {
+        const uint32_t v = cnt[b];
+        if (v) atomicAdd(&fill[cbase + b], v);
+        cnt[b] = 0;
+      }
+      __syncthreads();
+      continue;
+    }
     {
       const int b0 = tid * per;
       uint32_t sum = 0;
@@ -985,17 +995,20 @@ __global__ void k_bucket_ranges(const uint8_t* __restrict__ blobs, const uint64_
   if (b > 0) lo = max(lo, bk[b - 1]);
   if ((uint32_t)b < h->nspl) hi = min(hi, bk[b]);
   if (hi < lo) hi = lo;
-  // 32-bit digit: x32 = (key - lo) >> sh (range below 2^32 after the shift),
-  // digit = umulhi(x32, m) with m = floor(nb * 2^32 / (R + 1)), R = range >> sh:
-  // monotone and below nb; m == 0: range < nb, the digit is key - lo itself.
+  // 32-bit digit: x32 = (key - lo) >> sh, digit = umulhi(x32, m) with
+  // m = floor(nb * 2^32 / (R + 1)), R = range >> sh: monotone and below nb;
+  // m == 0: range < nb, the digit is key - lo itself (every cell holds one
+  // key value: the partition only counts, the cell sort fills).
   DigitCls d;
   d.lo = lo;
   d.hi = hi;
   d.nb = (uint32_t)seg_gb[3 * s + 2];
   d.mult = 0;
   d.pad = 0;
+  // R < 2^26 keeps m >= 64 nb (the floor of m costs < 1/64 of a cell) and
+  // m * 2 * cap below 2^32 for nb <= 2048.
   const uint64_t range = hi - lo;
-  d.sh = (uint32_t)max(0, bit_length64(range) - 32);
+  d.sh = (uint32_t)max(0, bit_length64(range) - 26);
   const uint64_t R = range >> d.sh;
   d.m32 = R + 1 <= (uint64_t)d.nb ? 0u : (uint32_t)(((uint64_t)d.nb << 32) / (R + 1));
   const uint64_t mk = (uint64_t)d.m32 * (uint64_t)(2 * AMS_SMEM_SORT_CAP);
@@ -1305,6 +1318,17 @@ __global__ void __launch_bounds__(kSortThreads, kSortCtas)
   uint64_t off, count, oo;
   cell_of(cs, blockIdx.x, off, count, oo);
   if (count == 0) return;
+  if (cs.mode == 3) {
+    // Fixed-capacity cells of a bucket whose digits are key values (m == 0)
+    // were only counted: the cell is `count` copies of lo + digit.
+    const uint32_t seg = cs.cell_seg[blockIdx.x];
+    const DigitCls& d = cs.dcls[seg];
+    if (d.m32 == 0) {
+      const uint64_t ko = from_ordered<KIND_OUT>(d.lo + (blockIdx.x - cs.cell0[seg]));
+      for (uint64_t i = threadIdx.x; i < count; i += blockDim.x) out[oo + i] = ko;
+      return;
+    }
+  }
   if (big_cell<KIND_OUT, VALS>(src, src_vals, out, out_vals, off, oo, count, ovf, ovf_count, s_mm))
     return;
   const uint32_t n = (uint32_t)count;
