@@ -1,6 +1,8 @@
 // C ABI of the AMS-sort hot path: device context, metadata staging and the
 // level / final-sort entry points declared in include/ams_b200.h.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -163,6 +165,7 @@ struct ams_ctx {
   Stage st_fixed;
   uint64_t fixed_segments = 0, fixed_overflow_segments = 0;
   bool bm_final = true;  // AMS_FINAL_BM=0 keeps the (g(b), j, b) last level + PE digit partition
+  bool host_trace = false;  // AMS_HOST_TRACE=1: host-side step times of ams_sort_run on stderr
   int fixed_fill_pct = 88;  // AMS_FIXED_FILL: mean fill of the fixed-capacity cells (percent)
   // deterministic delivery: origin tags (tie-breaks) and relayout work items
   const uint64_t* level_tags = nullptr;
@@ -332,6 +335,7 @@ int ams_ctx_create(int device, void* stream, ams_ctx_t** out) {
   c->device = device;
   c->stream = static_cast<cudaStream_t>(stream);
   if (const char* e = std::getenv("AMS_FINAL_BM")) c->bm_final = std::atoi(e) != 0;
+  if (const char* e = std::getenv("AMS_HOST_TRACE")) c->host_trace = std::atoi(e) != 0;
   if (const char* e = std::getenv("AMS_FIXED_FILL")) c->fixed_fill_pct = std::min(99, std::max(10, std::atoi(e)));
   *out = c;
   return AMS_OK;
@@ -1113,6 +1117,30 @@ int ams_map_keys(ams_ctx_t* c, const void* src, void* dst, uint64_t n, int from_
 // One-call driver: ams_sort (ams.py:271-313) with scheme "simple" on one GPU,
 // the level loop of paper_1410_6754_b200/engine.py in C++ (no Python between
 // the level steps).
+namespace {
+// Host-side step timer of ams_sort_run (AMS_HOST_TRACE=1).
+struct HostTrace {
+  bool on;
+  std::chrono::steady_clock::time_point t0, last;
+  std::string line;
+  explicit HostTrace(bool on_) : on(on_) { t0 = last = std::chrono::steady_clock::now(); }
+  void mark(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    char buf[96];
+    std::snprintf(buf, sizeof buf, " %s=%.0f", what,
+                  std::chrono::duration<double, std::micro>(now - last).count());
+    line += buf;
+    last = now;
+  }
+  ~HostTrace() {
+    if (!on) return;
+    std::fprintf(stderr, "ams_sort_run host us:%s total=%.0f\n", line.c_str(),
+                 std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count());
+  }
+};
+}  // namespace
+
 int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* pe_sizes,
                  const void* keys, const void* vals, void* out, void* out_vals,
                  uint64_t* out_pe_sizes, ams_level_report_t* reports) {
@@ -1172,6 +1200,8 @@ int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* p
   std::vector<uint64_t> sizes(pe_sizes, pe_sizes + p);
   std::vector<int32_t> gf{0}, gn{p};
   c->run_levels.assign(k, ams_ctx::LevelRec{});
+  HostTrace tr(c->host_trace);
+  tr.mark("setup");
   int rc;
   bool used_bm = false;
   for (int lv = 0; lv < k; ++lv) {
@@ -1195,6 +1225,7 @@ int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* p
                                    targets.data(), sizes.data(), offs.data(), cap, idx.data(),
                                    gpos.data(), drawn.data());
     if (rc) return rc;
+    tr.mark("draw");
     std::vector<int32_t> nb(G);
     std::vector<uint64_t> soff(G + 1, 0);
     int nb_stride = 1;
@@ -1229,10 +1260,12 @@ int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* p
     rec.sizes_before = sizes; rec.drawn = drawn;
     rec.hist.assign((size_t)p * nb_stride, 0);
     c->level_tags = tie_tags;
+    tr.mark("sample");
     rc = ams_level_classify(c, src, src_kind, p, offs.data(), sizes.data(), seg_group.data(), G,
                             posbase.data(), nb_stride, lv == 0, !(last && !with_vals), rec.hist.data());
     c->level_tags = nullptr;
     if (rc) return rc;
+    tr.mark("classify+sync");
     rec.boundaries.assign((size_t)G * (r + 1), 0);
     rec.loads.assign((size_t)G * r, 0);
     rec.max_load.assign(G, 0);
@@ -1285,9 +1318,11 @@ int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* p
       sdst = lv == 0 ? c->work[1].p : dst_out;
       sdst_v = lv == 0 ? c->work_v[1].p : c->tags0.p;
     }
+    tr.mark("plan");
     if ((rc = level_scatter_impl(c, src, src_v, src_kind, sdst, sdst_v, r, rec.boundaries.data(),
                                  dst_start.data(), 0, G * r, bm)))
       return rc;
+    tr.mark("scatter");
     if (relayout) {
       Stage& sc = c->st_copy;
       sc.reset();
@@ -1339,6 +1374,7 @@ int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* p
   for (int i = 0; i < p; ++i) offs[i + 1] = offs[i] + sizes[i];
   void* tmp = c->work[k % 2].p;
   void* tmp_v = with_vals ? c->work_v[k % 2].p : nullptr;
+  tr.mark("levels-end");
   if (used_bm) {
     // Buckets of the bucket-major last level, in output order.
     const ams_ctx::LevelRec& L = c->run_levels[k - 1];
@@ -1385,6 +1421,7 @@ int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* p
                                   dst_out_v, prm->key_kind, p, offs.data(), sizes.data()))) {
     return rc;
   }
+  tr.mark("final");
   c->run_final_sizes = sizes;
   if (out_pe_sizes) std::memcpy(out_pe_sizes, sizes.data(), sizeof(uint64_t) * p);
   return AMS_OK;

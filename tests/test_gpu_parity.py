@@ -213,6 +213,59 @@ def test_oracle_parity_deterministic(api, groups, npe, dist, with_vals):
             assert mine[k] == v, (k, mine[k], v)
 
 
+@pytest.mark.parametrize("groups,b,npe,dist", [
+    ((4,), 4, 1 << 18, "uniform"), ((2, 4), 4, 1 << 18, "zipf"), ((4,), 4, 300_001, "equal"),
+    ((2, 2, 2), 2, 1 << 18, "few"), ((2, 4), 4, 1 << 18, "sorted"), ((4,), 4, 199_999, "reverse"),
+    ((16,), 16, 1 << 16, "uniform"), ((4,), 4, 1 << 18, "f64"), ((2, 2), 4, 1 << 19, "narrow"),
+    ((4,), 4, 1 << 18, "clustered"), ((8, 8), 16, 1 << 12, "uniform"),
+])
+def test_oracle_parity_keys_only(api, groups, b, npe, dist):
+    """Keys-only sorts take the bucket-major last level and the
+    fixed-capacity final partition (buckets above shared memory; counting-
+    only cells for few-valued buckets, exact rounds for overflowed buckets):
+    same output, per-PE sizes and plans as the oracle."""
+    from paper_1410_6754_b200 import AmsParams, SeedSpec
+    p = int(np.prod(groups))
+    n = p * npe
+    rng = np.random.default_rng(hash((groups, npe, dist, 3)) & 0xFFFF)
+    if dist == "uniform":
+        keys = rng.integers(0, 2**64, n, dtype=np.uint64)
+    elif dist == "zipf":
+        keys = O.zipf_keys(n, 12)
+    elif dist == "equal":
+        keys = np.full(n, 7, dtype=np.uint64)
+    elif dist == "sorted":
+        keys = np.arange(n, dtype=np.uint64)
+    elif dist == "reverse":
+        keys = (n - 1 - np.arange(n)).astype(np.uint64)
+    elif dist == "f64":  # order-mapped doubles: density doubles across binade boundaries
+        keys = O.f64_to_ordered_u64(rng.random(n))
+    elif dist == "narrow":  # few distinct values per bucket: counting-only cells
+        keys = rng.integers(1000, 1000 + 20_000, n).astype(np.uint64)
+    elif dist == "clustered":  # dense clusters inside wide buckets: cells overflow
+        centers = rng.integers(0, 2**60, 6, dtype=np.uint64)
+        keys = centers[rng.integers(0, 6, n)] + rng.integers(0, 1 << 16, n).astype(np.uint64)
+    else:
+        keys = rng.choice(np.array([0, 1, 2**40, 2**63, 2**64 - 1], dtype=np.uint64), n)
+    sizes = [npe] * p
+    ref = O.ams_sort(keys, sizes, groups, None, b, 0.1, 79, "algo/rep0", with_stats=False)
+    ctx = api.get_sorter(0).ctx
+    before = ctx.final_sort_stats()
+    res = api.ams_sort_tensors(dev_u64(keys), sizes, AmsParams(tuple(groups), None, b, 0.1),
+                               SeedSpec(79, "algo/rep0"), key_kind="u64")
+    torch.cuda.synchronize()
+    after = ctx.final_sort_stats()
+    if npe * p // (int(np.prod(groups)) * b) > 2 * 4096:  # buckets well above shared memory
+        assert after["fixed_buckets"] > before["fixed_buckets"]  # the fixed-capacity path ran
+    if dist == "clustered":  # and its exact fallback
+        assert after["fixed_overflow_buckets"] > before["fixed_overflow_buckets"]
+    assert np.array_equal(host_u64(res.keys), ref.keys)
+    assert [int(x) for x in res.pe_sizes] == list(ref.pe_sizes)
+    for rec, infos in zip(res.levels, ref.levels):
+        for gi, info in enumerate(infos):
+            assert [int(x) for x in rec.boundaries[gi]] == list(info.plan.boundaries)
+
+
 def test_ragged_and_empty_pes(api):
     rng = np.random.default_rng(5)
     sizes = [0, 5, 0, 0, 10_000, 1, 3, 0] + [int(x) for x in rng.integers(0, 3000, 56)]
