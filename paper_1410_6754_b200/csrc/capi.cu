@@ -57,26 +57,41 @@ struct DevBuf {
   template <class T> T* as() const { return static_cast<T*>(p); }
 };
 
+// Pinned host memory mapped into the device address space.  Small host <->
+// device transfers of the sort go through it with a copy kernel, not the
+// copy engines: a host pipeline's multi-GiB H2D / D2H of other batches
+// occupy those, and a small cudaMemcpy queued behind one would stall the
+// sort for the whole transfer.
 struct HostBuf {
-  void* p = nullptr;
+  void* p = nullptr;   // host address
+  void* dp = nullptr;  // device address of the same bytes
   size_t cap = 0;
   cudaError_t ensure(size_t bytes) {
     if (bytes <= cap) return cudaSuccess;
     if (p) cudaFreeHost(p);
-    p = nullptr;
+    p = dp = nullptr;
     cap = 0;
     size_t want = std::max<size_t>(bytes, 4096);
-    cudaError_t e = cudaMallocHost(&p, want);
+    cudaError_t e = cudaHostAlloc(&p, want, cudaHostAllocMapped | cudaHostAllocPortable);
+    if (e != cudaSuccess) return e;
+    e = cudaHostGetDevicePointer(&dp, p, 0);
     if (e == cudaSuccess) cap = want;
     return e;
   }
   void release() {
     if (p) cudaFreeHost(p);
-    p = nullptr;
+    p = dp = nullptr;
     cap = 0;
   }
   template <class T> T* as() const { return static_cast<T*>(p); }
 };
+
+// Device -> mapped host copy on `st` (no copy engine); the caller syncs.
+cudaError_t to_host(HostBuf& h, const void* dsrc, size_t bytes, cudaStream_t st) {
+  cudaError_t e = h.ensure(bytes);
+  if (e != cudaSuccess) return e;
+  return launch_copy_bytes(st, h.dp, dsrc, bytes);
+}
 
 // Packs small host arrays, uploads them with one async copy from pinned
 // memory, and keeps the device copy until the next upload on this stage.
@@ -112,8 +127,7 @@ struct Stage {
     if ((e = h.ensure(bytes)) != cudaSuccess) return e;
     if ((e = d.ensure(bytes)) != cudaSuccess) return e;
     std::memcpy(h.p, pack.data(), pack.size());
-    if ((e = cudaMemcpyAsync(d.p, h.p, pack.size(), cudaMemcpyHostToDevice, st)) != cudaSuccess)
-      return e;
+    if ((e = launch_copy_bytes(st, d.p, h.dp, pack.size())) != cudaSuccess) return e;
     if ((e = cudaEventRecord(ev, st)) != cudaSuccess) return e;
     pending = true;
     return cudaSuccess;
@@ -171,7 +185,7 @@ struct ams_ctx {
   const uint64_t* level_tags = nullptr;
   DevBuf tags0;
   Stage st_copy;
-  HostBuf h_small;
+  HostBuf h_small, h_big;
   uint64_t overflow_cells = 0, fallback_cells = 0;
   // one-call driver (ams_sort_run): workspace and the last run's level records
   DevBuf work[2], work_v[2], s_keys, s_pos;
@@ -359,6 +373,7 @@ int ams_ctx_destroy(ams_ctx_t* c) {
     b->release();
   c->h_hist.release();
   c->h_small.release();
+  c->h_big.release();
   delete c;
   return AMS_OK;
 }
@@ -563,7 +578,7 @@ int ams_level_classify(ams_ctx_t* c, const void* src, int key_kind, int nseg,
     AMS_CK(c->h_small.ensure(64));
     AMS_CK(cudaStreamSynchronize(c->stream));
     std::memcpy(c->h_small.p, init, sizeof init);
-    AMS_CK(cudaMemcpyAsync(c->minmax.p, c->h_small.p, sizeof init, cudaMemcpyHostToDevice, c->stream));
+    AMS_CK(launch_copy_bytes(c->stream, c->minmax.p, c->h_small.dp, sizeof init));
     mm = c->minmax.as<unsigned long long>();
   }
   uint64_t nel = 0;
@@ -589,14 +604,13 @@ int ams_level_classify(ams_ctx_t* c, const void* src, int key_kind, int nseg,
     // The whole input is one group at the first level: its bounds are the
     // global key range.
     AMS_CK(c->bounds[0].ensure(16 * (size_t)ngroups));
-    AMS_CK(cudaMemcpyAsync(c->bounds[0].p, c->minmax.p, 16, cudaMemcpyDeviceToDevice, c->stream));
+    AMS_CK(launch_copy_bytes(c->stream, c->bounds[0].p, c->minmax.p, 16));
     c->bcur = 0;
   } else if (!c->bounds[c->bcur].p || c->bounds[c->bcur].cap < 16 * (size_t)ngroups) {
     return set_error(AMS_EINVAL, "no key bounds for these groups (first level needs track_minmax)");
   }
   const size_t hb = sizeof(uint32_t) * (size_t)nseg * nb_stride;
-  AMS_CK(c->h_hist.ensure(hb));
-  AMS_CK(cudaMemcpyAsync(c->h_hist.p, c->seg_hist.p, hb, cudaMemcpyDeviceToHost, c->stream));
+  AMS_CK(to_host(c->h_hist, c->seg_hist.p, hb, c->stream));
   AMS_CK(cudaStreamSynchronize(c->stream));
   if (h_seg_hist_out) std::memcpy(h_seg_hist_out, c->h_hist.p, hb);
   return AMS_OK;
@@ -674,8 +688,8 @@ int level_scatter_impl(ams_ctx_t* c, const void* src, const void* src_vals, int 
                                c->bounds[c->bcur].as<uint64_t>(), c->bounds[nxt].as<uint64_t>()));
   }
   if (child_first > 0 && child_count > 0)
-    AMS_CK(cudaMemcpyAsync(c->bounds[nxt].p, c->bounds[nxt].as<uint64_t>() + 2 * child_first,
-                           16 * (size_t)child_count, cudaMemcpyDeviceToDevice, c->stream));
+    AMS_CK(launch_copy_bytes(c->stream, c->bounds[nxt].p, c->bounds[nxt].as<uint64_t>() + 2 * child_first,
+                             16 * (size_t)child_count));
   c->bcur = nxt;
   c->launches += 3;
   return AMS_OK;
@@ -689,7 +703,7 @@ int ams_get_minmax(ams_ctx_t* c, uint64_t out[2]) {
   if (!c || !out) return set_error(AMS_EINVAL, "null argument");
   if (!c->minmax.p) return set_error(AMS_EINVAL, "no min/max recorded");
   AMS_CK(cudaSetDevice(c->device));
-  AMS_CK(cudaMemcpyAsync(c->h_small.p, c->minmax.p, 16, cudaMemcpyDeviceToHost, c->stream));
+  AMS_CK(to_host(c->h_small, c->minmax.p, 16, c->stream));
   AMS_CK(cudaStreamSynchronize(c->stream));
   std::memcpy(out, c->h_small.p, 16);
   return AMS_OK;
@@ -702,9 +716,9 @@ int ams_set_minmax(ams_ctx_t* c, const uint64_t in[2]) {
   AMS_CK(c->h_small.ensure(64));
   AMS_CK(cudaStreamSynchronize(c->stream));
   std::memcpy(c->h_small.p, in, 16);
-  AMS_CK(cudaMemcpyAsync(c->minmax.p, c->h_small.p, 16, cudaMemcpyHostToDevice, c->stream));
+  AMS_CK(launch_copy_bytes(c->stream, c->minmax.p, c->h_small.dp, 16));
   AMS_CK(c->bounds[c->bcur].ensure(16));
-  AMS_CK(cudaMemcpyAsync(c->bounds[c->bcur].p, c->minmax.p, 16, cudaMemcpyDeviceToDevice, c->stream));
+  AMS_CK(launch_copy_bytes(c->stream, c->bounds[c->bcur].p, c->minmax.p, 16));
   return AMS_OK;
 }
 
@@ -724,7 +738,7 @@ int sort_cells(ams_ctx* c, const void* src, const void* src_vals, void* out, voi
   }
   c->launches += 1;
   unsigned int nfb = 0;
-  AMS_CK(cudaMemcpyAsync(c->h_small.p, c->fb_count.p, sizeof nfb, cudaMemcpyDeviceToHost, c->stream));
+  AMS_CK(to_host(c->h_small, c->fb_count.p, sizeof nfb, c->stream));
   AMS_CK(cudaStreamSynchronize(c->stream));
   std::memcpy(&nfb, c->h_small.p, sizeof nfb);
   c->fallback_cells += nfb;
@@ -827,13 +841,17 @@ int partition_rounds(ams_ctx* c, void* src, void* src_vals, void* tmp, void* tmp
     if (rc) return rc;
     // Cells that still exceed shared memory go round again (sort_cells synced).
     unsigned int novf = 0;
-    AMS_CK(cudaMemcpy(&novf, c->ovf_count.p, sizeof novf, cudaMemcpyDeviceToHost));
+    AMS_CK(to_host(c->h_small, c->ovf_count.p, sizeof novf, c->stream));
+    AMS_CK(cudaStreamSynchronize(c->stream));
+    std::memcpy(&novf, c->h_small.p, sizeof novf);
     b_off.clear(); b_len.clear(); b_lo.clear(); b_hi.clear();
     max_big = 0;
     c->overflow_cells += novf;
     if (novf) {
       std::vector<OverflowRec> recs(novf);
-      AMS_CK(cudaMemcpy(recs.data(), c->ovf.p, sizeof(OverflowRec) * novf, cudaMemcpyDeviceToHost));
+      AMS_CK(to_host(c->h_big, c->ovf.p, sizeof(OverflowRec) * novf, c->stream));
+      AMS_CK(cudaStreamSynchronize(c->stream));
+      std::memcpy(recs.data(), c->h_big.p, sizeof(OverflowRec) * novf);
       std::sort(recs.begin(), recs.end(),
                 [](const OverflowRec& a, const OverflowRec& b) { return a.off < b.off; });
       for (const OverflowRec& r : recs) {
@@ -962,14 +980,18 @@ int final_sort_bm(ams_ctx* c, void* src, void* tmp, void* out, int key_kind,
   if (rc) return rc;
   // Overflowed buckets (sort_cells synced): exact partition rounds from src.
   std::vector<uint32_t> flags(nseg);
-  AMS_CK(cudaMemcpy(flags.data(), c->fx_ovf.p, 4 * (size_t)nseg, cudaMemcpyDeviceToHost));
+  AMS_CK(to_host(c->h_big, c->fx_ovf.p, 4 * (size_t)nseg, c->stream));
+  AMS_CK(cudaStreamSynchronize(c->stream));
+  std::memcpy(flags.data(), c->h_big.p, 4 * (size_t)nseg);
   std::vector<uint64_t> o_off2, o_len2, o_lo, o_hi;
   std::vector<DigitCls> dc;
   for (int i = 0; i < nseg; ++i) {
     if (!flags[i]) continue;
     if (dc.empty()) {
       dc.resize(nseg);
-      AMS_CK(cudaMemcpy(dc.data(), c->dcls.p, sizeof(DigitCls) * (size_t)nseg, cudaMemcpyDeviceToHost));
+      AMS_CK(to_host(c->h_big, c->dcls.p, sizeof(DigitCls) * (size_t)nseg, c->stream));
+      AMS_CK(cudaStreamSynchronize(c->stream));
+      std::memcpy(dc.data(), c->h_big.p, sizeof(DigitCls) * (size_t)nseg);
     }
     o_off2.push_back(f_off[i]);
     o_len2.push_back(f_len[i]);

@@ -62,6 +62,20 @@ __global__ void k_copy_ranges(const uint64_t* __restrict__ items, const uint64_t
   }
 }
 
+// Small transfers between device memory and mapped pinned host memory
+// (16-byte units while both sides allow, then bytes).
+__global__ void k_copy_bytes(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src, size_t bytes) {
+  const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (size_t)gridDim.x * blockDim.x;
+  size_t head = 0;
+  if ((((uintptr_t)dst | (uintptr_t)src) & 15) == 0) {
+    const size_t n16 = bytes / 16;
+    for (size_t i = tid; i < n16; i += nt)
+      reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+    head = n16 * 16;
+  }
+  for (size_t i = head + tid; i < bytes; i += nt) dst[i] = src[i];
+}
+
 __global__ void k_iota(uint64_t* __restrict__ dst, uint64_t n) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x)
@@ -1631,6 +1645,13 @@ cudaError_t launch_copy_ranges(cudaStream_t st, const uint64_t* items, int nitem
                                                   static_cast<uint64_t*>(dst),
                                                   static_cast<const uint64_t*>(src_vals),
                                                   static_cast<uint64_t*>(dst_vals));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_copy_bytes(cudaStream_t st, void* dst, const void* src, size_t bytes) {
+  if (bytes == 0) return cudaSuccess;
+  const unsigned blocks = (unsigned)std::min<size_t>((bytes + 4095) / 4096, 64);
+  k_copy_bytes<<<blocks, 256, 0, st>>>(static_cast<uint8_t*>(dst), static_cast<const uint8_t*>(src), bytes);
   return cudaGetLastError();
 }
 
