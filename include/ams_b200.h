@@ -95,6 +95,13 @@ int ams_plan_level(int ngroups, const int32_t* group_npe, const int32_t* group_n
 int ams_deliver_deterministic(int P, int r, int pe0, const uint64_t* pieces, uint64_t* out_new_sizes,
                               uint64_t* out_slices, int slice_cap, int* out_nslices,
                               uint64_t* out_stats);
+/* deliver_simple_permuted (delivery.py:151-185): as above, subgroup g's
+ * sending members enumerated in the Feistel order of stream
+ * "{level_stream}/deliver/order-g{g}" (core.py:96-159), level_stream =
+ * "{SeedSpec.stream_id}/L{level}-g{first PE of the group}". */
+int ams_deliver_permuted(int P, int r, int64_t master_seed, const char* level_stream,
+                         const uint64_t* pieces, uint64_t* out_new_sizes, uint64_t* out_slices,
+                         int slice_cap, int* out_nslices, uint64_t* out_stats);
 
 /* ------------------------------------------------------------------ */
 /* Device context: one per GPU (one process per GPU).                  */
@@ -218,10 +225,12 @@ int ams_map_keys(ams_ctx_t* ctx, const void* src, void* dst, uint64_t n, int fro
 #define AMS_MAX_LEVELS 8
 
 /* AmsParams (ams.py:33-65) + SeedSpec (core.py:46-71) + key encoding. */
-/* Delivery schemes (delivery.py:439-455 SCHEMES): "simple" (151-180) and
- * "deterministic" (188-306, the reference CLI default). */
+/* Delivery schemes (delivery.py:439-455 SCHEMES): "simple" (151-180),
+ * "deterministic" (188-306, the reference CLI default) and "permuted"
+ * (183-185). */
 #define AMS_SCHEME_SIMPLE 0
 #define AMS_SCHEME_DETERMINISTIC 1
+#define AMS_SCHEME_PERMUTED 2
 
 typedef struct {
   int levels;                          /* k = len(group_counts) */
@@ -233,7 +242,7 @@ typedef struct {
   const char* stream_id;               /* SeedSpec.stream_id, e.g. "algo/rep0" */
   int key_kind;                        /* AMS_KEY_U64 / AMS_KEY_I64 / AMS_KEY_F64 */
   int with_stats;                      /* fill the exchange maxima of the reports */
-  int scheme;                          /* AMS_SCHEME_SIMPLE / AMS_SCHEME_DETERMINISTIC */
+  int scheme;                          /* AMS_SCHEME_SIMPLE / _DETERMINISTIC / _PERMUTED */
 } ams_params_t;
 
 /* One level's report (ams.py:294-308; exchange maxima simnet.py:109-124). */

@@ -194,6 +194,82 @@ def _exchange_stats(piece_sizes: np.ndarray, sub_sizes: int, members: list):
             "max_sent_msgs": ms, "max_recv_msgs": mr}
 
 
+def key64(master_seed: int, stream_id: str, index: int) -> int:
+    """``SeedSpec.key64`` (core.py:69-71): the first 8 bytes (big endian) of
+    blake2b-128 of ``f"{master}\x1f{stream}\x1fk{index}"``."""
+    text = f"{master_seed}\x1f{stream_id}\x1fk{index}"
+    return int.from_bytes(hashlib.blake2b(text.encode(), digest_size=16).digest()[:8], "big")
+
+
+def _mix64(x: int) -> int:
+    """splitmix64 finalizer (core.py:74-79)."""
+    m = 0xFFFFFFFFFFFFFFFF
+    x &= m
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & m
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & m
+    return x ^ (x >> 31)
+
+
+def feistel_order(n: int, master_seed: int, stream_id: str) -> list:
+    """``sorted(range(n), key=feistel_new(n, seed).apply)`` (delivery.py:
+    131-134; core.py:96-159): four keyed digit-pair rounds over the padded
+    square domain side**2, cycle-walking values >= n."""
+    side = math.isqrt(n)
+    if side * side < n:
+        side += 1
+    tables = [[_mix64(b ^ key64(master_seed, stream_id, i)) % side for b in range(side)]
+              for i in range(4)]
+
+    def apply(i):
+        x = i
+        for _ in range(side * side):
+            hi, lo = divmod(x, side)
+            for t in tables:
+                lo, hi = hi, (lo + t[hi]) % side
+            x = lo + hi * side
+            if x < n:
+                return x
+        raise RuntimeError("cycle walk failed to terminate; broken bijection")
+
+    return sorted(range(n), key=apply)
+
+
+def permuted_plan(piece_sizes: np.ndarray, master_seed: int, level_stream: str):
+    """``deliver_simple_permuted`` (delivery.py:151-185): each subgroup g
+    enumerates the sending members in the Feistel order of stream
+    ``{level_stream}/deliver/order-g{g}``; member t owns numbers
+    ``[m t / p', m (t+1) / p')`` of that enumeration.  Returns slices like
+    :func:`deterministic_plan` and the new member sizes."""
+    P, r = piece_sizes.shape
+    if P % r != 0:
+        raise ValueError(f"{P} PEs cannot form {r} groups")
+    sub = P // r
+    slices = {}
+    new_sizes = [0] * P
+    for g in range(r):
+        order = feistel_order(P, master_seed, f"{level_stream}/deliver/order-g{g}")
+        m = int(piece_sizes[:, g].sum())
+        start = 0
+        for j in order:
+            size = int(piece_sizes[j, g])
+            if size:
+                cuts = []
+                t = ((start + 1) * sub + m - 1) // m - 1          # _slice_range
+                covered = 0
+                while covered < size and t < sub:
+                    hi = (m * (t + 1)) // sub
+                    take = min(start + size, hi) - (start + covered)
+                    if take > 0:
+                        cuts.append((t, covered, take))
+                        covered += take
+                    t += 1
+                slices[(j, g)] = cuts
+            start += size
+        for t in range(sub):
+            new_sizes[g * sub + t] = (m * (t + 1)) // sub - (m * t) // sub
+    return slices, new_sizes
+
+
 def deterministic_plan(piece_sizes: np.ndarray, group_lo: int = 0):
     """Member assignment of ``deliver_deterministic`` (delivery.py:188-306):
     small pieces (size * 2 * p * r <= n) go whole to member
@@ -364,8 +440,12 @@ def ams_level(buf: np.ndarray, sizes: list, r: int, b: int, a: float,
     pieces = np.zeros((P, r), np.int64)
     for g in range(r):
         pieces[:, g] = hist[:, bnd[g]:bnd[g + 1]].sum(axis=1)
-    if scheme == "deterministic":                              # delivery.py:188-306
-        slices, new_sizes = deterministic_plan(pieces, group_lo)
+    if scheme in ("deterministic", "permuted"):                # delivery.py:151-306
+        if scheme == "deterministic":
+            slices, new_sizes = deterministic_plan(pieces, group_lo)
+        else:
+            slices, new_sizes = permuted_plan(pieces, master_seed,
+                                              f"{stream}/L{level}-g{group_lo}")
         out = deterministic_relayout(out, pieces, slices, new_sizes)
         out_org = deterministic_relayout(out_org, pieces, slices, new_sizes)
         if out_vals is not None:
@@ -381,7 +461,7 @@ def ams_level(buf: np.ndarray, sizes: list, r: int, b: int, a: float,
     info = LevelInfo(level, group_lo, n_g, br, drawn, sk, sp, hist, plan,
                      new_sizes)
     if with_stats:
-        if scheme == "deterministic":
+        if scheme in ("deterministic", "permuted"):
             info.stats = _deterministic_stats(pieces, slices)
         else:
             info.stats = _exchange_stats(pieces, sub, list(range(P)))

@@ -209,6 +209,16 @@ def cases():
             scheme="deterministic")
         cfg(f"simple_cfg2_scaled_{dist}", dist, 64, 1 << 12, (8, 8), None, 16, 0.1, 1)
 
+    # deliver_simple_permuted (delivery.py:183-185): Feistel enumeration orders.
+    for dist in ("uniform", "sorted", "equal", "zipf:1.1"):
+        for groups, p in (((4, 4), 16), ((2, 2, 4), 16)):
+            tag = dist.replace(":", "") + "_" + "x".join(map(str, groups))
+            cfg(f"perm_{tag}", dist, p, 250, groups, None, 8, 0.2, 5, scheme="permuted")
+    cfg("perm_cfg2_scaled_equal", "equal", 64, 1 << 12, (8, 8), None, 16, 0.1, 1,
+        scheme="permuted")
+    cfg("perm_cfg3_scaled", "uniform", 256, 1 << 9, (8, 32), None, 16, 0.1, 2,
+        scheme="permuted")
+
     def tiny(name, spec, groups, b=16, eps=0.2, seed=9, scheme="simple"):
         def build():
             data = explicit(spec)
@@ -236,6 +246,9 @@ def cases():
     rng = _r.Random(5)
     tiny("det_tiny_mixed", {pe: [rng.randrange(1 << 30) for _ in range(20 + 3 * pe)]
                             for pe in range(8)}, (2, 4), b=4, seed=8, scheme="deterministic")
+    rng = _r.Random(6)
+    tiny("perm_tiny_ragged", {pe: [rng.randrange(60) for _ in range(rng.randrange(0, 30))]
+                              for pe in range(8)}, (2, 4), b=4, seed=4, scheme="permuted")
     # One big PE: its piece exceeds ceil(n/p) (delivery.py:212-217 ValueError).
     tiny("det_tiny_big_piece", {0: list(range(100)), 1: [5], 2: [7], 3: [9]}, (2, 2), b=4,
          seed=2, scheme="deterministic")

@@ -42,6 +42,7 @@ _SIGNATURES = {
     "ams_group_plan": (_I, [_P, _I, _I, _P, _P, _P]),
     "ams_plan_level": (_I, [_I, _P, _P, _I, _P, _I, _P, _P, _P, _P, _P]),
     "ams_deliver_deterministic": (_I, [_I, _I, _I, _P, _P, _P, _I, _P, _P]),
+    "ams_deliver_permuted": (_I, [_I, _I, _I64, C.c_char_p, _P, _P, _P, _I, _P, _P]),
     "ams_ctx_create": (_I, [_I, _P, C.POINTER(_P)]),
     "ams_ctx_destroy": (_I, [_P]),
     "ams_ctx_set_stream": (_I, [_P, _P]),
@@ -241,6 +242,22 @@ def deliver_deterministic(pieces: np.ndarray, pe0: int = 0, with_stats: bool = T
     stats = np.zeros(4, np.uint64) if with_stats else None
     check(lib.ams_deliver_deterministic(P, r, int(pe0), pc.ctypes.data, ns.ctypes.data,
                                         slices.ctypes.data, P * (r + 1), C.byref(cnt), ptr(stats)))
+    return ns, slices[:cnt.value].copy(), stats
+
+
+def deliver_permuted(pieces: np.ndarray, master_seed: int, level_stream: str,
+                     with_stats: bool = True):
+    """Host restatement of deliver_simple_permuted's slices
+    (delivery.py:151-185): as :func:`deliver_deterministic`."""
+    pc = np.ascontiguousarray(pieces, dtype=np.uint64)
+    P, r = pc.shape
+    ns = np.zeros(P, np.uint64)
+    slices = np.zeros((P * (r + 1), 3), np.uint64)
+    cnt = C.c_int(0)
+    stats = np.zeros(4, np.uint64) if with_stats else None
+    check(lib.ams_deliver_permuted(P, r, int(master_seed), level_stream.encode(), pc.ctypes.data,
+                                   ns.ctypes.data, slices.ctypes.data, P * (r + 1), C.byref(cnt),
+                                   ptr(stats)))
     return ns, slices[:cnt.value].copy(), stats
 
 

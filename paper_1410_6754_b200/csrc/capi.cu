@@ -1186,14 +1186,17 @@ int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* p
   if (n && (!keys || !out)) return set_error(AMS_EINVAL, "null key buffer");
   const bool user_vals = vals != nullptr;
   if (user_vals && !out_vals) return set_error(AMS_EINVAL, "values need an output buffer");
-  if (prm->scheme != AMS_SCHEME_SIMPLE && prm->scheme != AMS_SCHEME_DETERMINISTIC)
+  if (prm->scheme != AMS_SCHEME_SIMPLE && prm->scheme != AMS_SCHEME_DETERMINISTIC &&
+      prm->scheme != AMS_SCHEME_PERMUTED)
     return set_error(AMS_EINVAL, "unknown delivery scheme");
   // Deterministic delivery (delivery.py:188-306) can put a later source's
   // piece into an earlier member, so group-buffer order stops being origin
   // order: origin tags travel as the values and break key ties
   // from level 2 on (and order the final sort); user values are gathered by
   // tag at the end.
-  const bool det = prm->scheme == AMS_SCHEME_DETERMINISTIC && n > 0;
+  // (The permuted scheme's receivers also concatenate by source id while
+  // the enumeration follows the permutation: same treatment.)
+  const bool det = prm->scheme != AMS_SCHEME_SIMPLE && n > 0;
   const bool with_vals = user_vals || det;
   AMS_CK(cudaSetDevice(c->device));
   // ams.py:278-280 and AmsParams.per_level_imbalance (ams.py:58-59).
@@ -1320,10 +1323,17 @@ int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* p
               pieces[(size_t)j * r + t] += rec.hist[(size_t)(gf[g] + j) * nb_stride + bb];
         slices.assign(3 * (size_t)P * (r + 1), 0);
         int ns = 0;
-        if ((rc = ams_deliver_deterministic(P, r, gf[g], pieces.data(), rec.new_sizes.data() + gf[g],
-                                            slices.data(), P * (r + 1), &ns,
-                                            rec.has_stats ? rec.stats.data() + 4 * (size_t)g : nullptr)))
-          return rc;
+        uint64_t* st4 = rec.has_stats ? rec.stats.data() + 4 * (size_t)g : nullptr;
+        if (prm->scheme == AMS_SCHEME_PERMUTED) {
+          const std::string ls = std::string(prm->stream_id) + "/L" + std::to_string(lv) + "-g" +
+                                 std::to_string(gf[g]);
+          rc = ams_deliver_permuted(P, r, prm->master_seed, ls.c_str(), pieces.data(),
+                                    rec.new_sizes.data() + gf[g], slices.data(), P * (r + 1), &ns, st4);
+        } else {
+          rc = ams_deliver_deterministic(P, r, gf[g], pieces.data(), rec.new_sizes.data() + gf[g],
+                                         slices.data(), P * (r + 1), &ns, st4);
+        }
+        if (rc) return rc;
         for (int q = 0; q < ns; ++q) {
           const uint64_t s0 = dst_start[g] + slices[3 * q], d0 = dst_start[g] + slices[3 * q + 1];
           for (uint64_t o = 0; o < slices[3 * q + 2]; o += kCopyItemKeys) {

@@ -122,6 +122,65 @@ void exchange_stats(const std::vector<uint64_t>& pieces, int P, int r, uint64_t 
   out[3] = mr;
 }
 
+// One slice of a delivery: elements [off, off + len) of piece (member j,
+// subgroup g) go to member t of subgroup g.
+struct Cut { int j, g, t; uint64_t off, len; };
+
+// Slices -> {src, dst, len} (src in the group's simple layout: subgroup,
+// source member, bucket; dst in the new member arrays, receivers
+// concatenating by source, simnet.py:324-325), new member sizes and the
+// data-exchange shape (simnet.py:294-335).
+int emit_slices(int P, int r, const uint64_t* pieces, const std::vector<Cut>& cuts,
+                uint64_t* out_new_sizes, uint64_t* out_slices, int slice_cap, int* out_nslices,
+                uint64_t* out_stats) {
+  const int sub = P / r;
+  if ((int)cuts.size() > slice_cap) return set_error(AMS_EINTERNAL, "slice buffer too small");
+  // New member sizes and receive order (by source member).
+  std::vector<uint64_t> ns(P, 0);
+  for (const Cut& c : cuts) ns[(size_t)c.g * sub + c.t] += c.len;
+  std::vector<uint64_t> mbase(P + 1, 0);
+  for (int d = 0; d < P; ++d) mbase[d + 1] = mbase[d] + ns[d];
+  std::vector<uint64_t> gstart(r + 1, 0), pstart((size_t)P * r, 0);
+  for (int g = 0; g < r; ++g) {
+    uint64_t run = gstart[g];
+    for (int j = 0; j < P; ++j) { pstart[(size_t)j * r + g] = run; run += pieces[(size_t)j * r + g]; }
+    gstart[g + 1] = run;
+  }
+  std::vector<int> order(cuts.size());
+  for (size_t i = 0; i < cuts.size(); ++i) order[i] = (int)i;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+    const int da = cuts[a].g * sub + cuts[a].t, db = cuts[b].g * sub + cuts[b].t;
+    return da != db ? da < db : cuts[a].j < cuts[b].j;
+  });
+  std::vector<uint64_t> fill(P, 0);
+  std::vector<uint64_t> sw(P, 0), rw(P, 0), sm(P, 0), rm(P, 0);
+  int k = 0;
+  for (int i : order) {
+    const Cut& c = cuts[i];
+    const int d = c.g * sub + c.t;
+    out_slices[3 * k + 0] = pstart[(size_t)c.j * r + c.g] + c.off;
+    out_slices[3 * k + 1] = mbase[d] + fill[d];
+    out_slices[3 * k + 2] = c.len;
+    fill[d] += c.len;
+    if (c.len > 0 && d != c.j) { sw[c.j] += c.len; rw[d] += c.len; sm[c.j] += 1; rm[d] += 1; }
+    ++k;
+  }
+  *out_nslices = k;
+  std::copy(ns.begin(), ns.end(), out_new_sizes);
+  if (out_stats) {
+    uint64_t hs = 0, hr = 0, ms = 0, mr = 0;
+    for (int j = 0; j < P; ++j) {
+      hs = std::max(hs, sw[j]); hr = std::max(hr, rw[j]);
+      ms = std::max(ms, sm[j]); mr = std::max(mr, rm[j]);
+    }
+    out_stats[0] = std::max(hs, hr);
+    out_stats[1] = std::max(ms, mr);
+    out_stats[2] = ms;
+    out_stats[3] = mr;
+  }
+  return AMS_OK;
+}
+
 }  // namespace
 }  // namespace ams
 
@@ -237,7 +296,6 @@ int ams_deliver_deterministic(int P, int r, int pe0, const uint64_t* pieces, uin
   auto is_small = [&](uint64_t size) {
     return (unsigned __int128)size * 2u * (unsigned)P * (unsigned)r <= n;
   };
-  struct Cut { int j, g, t; uint64_t off, len; };
   std::vector<Cut> cuts;
   for (int g = 0; g < r; ++g) {
     uint64_t m_g = 0;
@@ -278,51 +336,82 @@ int ams_deliver_deterministic(int P, int r, int pe0, const uint64_t* pieces, uin
       pos += size;
     }
   }
-  if ((int)cuts.size() > slice_cap) return set_error(AMS_EINTERNAL, "slice buffer too small");
-  // New member sizes and receive order (by source member).
-  std::vector<uint64_t> ns(P, 0);
-  for (const Cut& c : cuts) ns[(size_t)c.g * sub + c.t] += c.len;
-  std::vector<uint64_t> mbase(P + 1, 0);
-  for (int d = 0; d < P; ++d) mbase[d + 1] = mbase[d] + ns[d];
-  std::vector<uint64_t> gstart(r + 1, 0), pstart((size_t)P * r, 0);
+  return emit_slices(P, r, pieces, cuts, out_new_sizes, out_slices, slice_cap, out_nslices, out_stats);
+}
+
+// deliver_simple_permuted (delivery.py:151-185): subgroup g enumerates the
+// sending members in the order sorted(range(P), key=feistel.apply) of the
+// seeded permutation of stream "{level_stream}/deliver/order-g{g}"
+// (core.py:96-159: four keyed digit-pair rounds over side^2, cycle
+// walking); member t owns numbers [m t / p', m (t+1) / p') of it.  Output
+// as ams_deliver_deterministic.
+int ams_deliver_permuted(int P, int r, int64_t master_seed, const char* level_stream,
+                         const uint64_t* pieces, uint64_t* out_new_sizes, uint64_t* out_slices,
+                         int slice_cap, int* out_nslices, uint64_t* out_stats) {
+  if (P < 1 || r < 1 || P % r != 0)
+    return set_error(AMS_EINVAL, std::to_string(P) + " PEs cannot form " + std::to_string(r) + " groups");
+  if (!level_stream) return set_error(AMS_EINVAL, "null stream id");
+  const int sub = P / r;
+  uint64_t side = (uint64_t)std::sqrt((double)P);
+  while (side * side > (uint64_t)P) --side;
+  while (side * side < (uint64_t)P) ++side;
+  auto mix64 = [](uint64_t x) {
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
+    return x ^ (x >> 31);
+  };
+  std::vector<Cut> cuts;
+  std::vector<uint64_t> tables(4 * side), perm(P);
+  std::vector<int> order(P);
   for (int g = 0; g < r; ++g) {
-    uint64_t run = gstart[g];
-    for (int j = 0; j < P; ++j) { pstart[(size_t)j * r + g] = run; run += pieces[(size_t)j * r + g]; }
-    gstart[g + 1] = run;
-  }
-  std::vector<int> order(cuts.size());
-  for (size_t i = 0; i < cuts.size(); ++i) order[i] = (int)i;
-  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
-    const int da = cuts[a].g * sub + cuts[a].t, db = cuts[b].g * sub + cuts[b].t;
-    return da != db ? da < db : cuts[a].j < cuts[b].j;
-  });
-  std::vector<uint64_t> fill(P, 0);
-  std::vector<uint64_t> sw(P, 0), rw(P, 0), sm(P, 0), rm(P, 0);
-  int k = 0;
-  for (int i : order) {
-    const Cut& c = cuts[i];
-    const int d = c.g * sub + c.t;
-    out_slices[3 * k + 0] = pstart[(size_t)c.j * r + c.g] + c.off;
-    out_slices[3 * k + 1] = mbase[d] + fill[d];
-    out_slices[3 * k + 2] = c.len;
-    fill[d] += c.len;
-    if (c.len > 0 && d != c.j) { sw[c.j] += c.len; rw[d] += c.len; sm[c.j] += 1; rm[d] += 1; }
-    ++k;
-  }
-  *out_nslices = k;
-  std::copy(ns.begin(), ns.end(), out_new_sizes);
-  if (out_stats) {
-    uint64_t hs = 0, hr = 0, ms = 0, mr = 0;
-    for (int j = 0; j < P; ++j) {
-      hs = std::max(hs, sw[j]); hr = std::max(hr, rw[j]);
-      ms = std::max(ms, sm[j]); mr = std::max(mr, rm[j]);
+    const std::string stream = std::string(level_stream) + "/deliver/order-g" + std::to_string(g);
+    for (int i = 0; i < 4; ++i) {  // SeedSpec.key64(i), core.py:69-71
+      const std::string text = std::to_string(master_seed) + "\x1f" + stream + "\x1fk" + std::to_string(i);
+      uint8_t d[16];
+      blake2b_128(reinterpret_cast<const uint8_t*>(text.data()), text.size(), d);
+      uint64_t key = 0;
+      for (int b = 0; b < 8; ++b) key = (key << 8) | d[b];
+      for (uint64_t v = 0; v < side; ++v) tables[i * side + v] = mix64(v ^ key) % side;
     }
-    out_stats[0] = std::max(hs, hr);
-    out_stats[1] = std::max(ms, mr);
-    out_stats[2] = ms;
-    out_stats[3] = mr;
+    for (int j = 0; j < P; ++j) {
+      uint64_t x = (uint64_t)j;
+      for (uint64_t it = 0; it < side * side; ++it) {
+        uint64_t hi = x / side, lo = x % side;
+        for (int i = 0; i < 4; ++i) {
+          const uint64_t nhi = (lo + tables[i * side + hi]) % side;
+          lo = hi;
+          hi = nhi;
+        }
+        x = lo + hi * side;
+        if (x < (uint64_t)P) break;
+      }
+      perm[j] = x;
+    }
+    for (int j = 0; j < P; ++j) order[j] = j;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return perm[a] < perm[b]; });
+    uint64_t m = 0;
+    for (int j = 0; j < P; ++j) m += pieces[(size_t)j * r + g];
+    uint64_t start = 0;
+    for (int j : order) {
+      const uint64_t size = pieces[(size_t)j * r + g];
+      if (size) {  // _slice_range (delivery.py:83-106)
+        int t = (int)((((unsigned __int128)(start + 1) * sub + m - 1) / m) - 1);
+        uint64_t covered = 0;
+        while (covered < size && t < sub) {
+          const uint64_t hi = (uint64_t)(((unsigned __int128)m * (t + 1)) / sub);
+          const int64_t take = (int64_t)std::min(start + size, hi) - (int64_t)(start + covered);
+          if (take > 0) {
+            cuts.push_back({j, g, t, covered, (uint64_t)take});
+            covered += (uint64_t)take;
+          }
+          ++t;
+        }
+        if (covered != size) return set_error(AMS_EINTERNAL, "quota mapping failed to cover a piece");
+      }
+      start += size;
+    }
   }
-  return AMS_OK;
+  return emit_slices(P, r, pieces, cuts, out_new_sizes, out_slices, slice_cap, out_nslices, out_stats);
 }
 
 }  // extern "C"

@@ -97,7 +97,7 @@ def test_golden_parity(api, name, native):
     check_levels(res, g)
 
 
-@pytest.mark.parametrize("name", [n for n in G.names() if n.startswith(("tiny", "det_tiny"))])
+@pytest.mark.parametrize("name", [n for n in G.names() if n.startswith(("tiny", "det_tiny", "perm_tiny"))])
 def test_dropin_elements(api, name):
     """ams_sort(net, data, params, scheme, seed) returns the reference's
     exact per-PE Element lists."""
@@ -175,9 +175,11 @@ def test_oracle_parity_random(api, groups, npe, dist, native):
     ((4, 4, 4), 1024, "few"), ((8, 32), 1 << 9, "equal"), ((2, 8), 5000, "uniform"),
 ])
 @pytest.mark.parametrize("with_vals", [True, False], ids=["kv", "keys"])
-def test_oracle_parity_deterministic(api, groups, npe, dist, with_vals):
-    """scheme="deterministic" (delivery.py:188-306): member placement by the
-    two-phase assignment, ties broken by the carried origin tags."""
+@pytest.mark.parametrize("scheme", ["deterministic", "permuted"])
+def test_oracle_parity_deterministic(api, groups, npe, dist, with_vals, scheme):
+    """scheme="deterministic" (delivery.py:188-306: two-phase assignment)
+    and "permuted" (delivery.py:183-185: Feistel enumeration): member
+    placement differs from "simple", ties broken by the carried origin tags."""
     p = int(np.prod(groups))
     n = p * npe
     rng = np.random.default_rng(hash((groups, npe, dist, 7)) & 0xFFFF)
@@ -193,10 +195,9 @@ def test_oracle_parity_deterministic(api, groups, npe, dist, with_vals):
         keys = rng.choice(np.array([0, 1, 2**40, 2**63, 2**64 - 1], dtype=np.uint64), n)
     sizes = [npe] * p
     vals = np.arange(n, dtype=np.int64)
-    ref = O.ams_sort(keys, sizes, groups, None, 16, 0.1, 78, "algo/rep0", vals=vals,
-                     scheme="deterministic")
+    ref = O.ams_sort(keys, sizes, groups, None, 16, 0.1, 78, "algo/rep0", vals=vals, scheme=scheme)
     res = run_gpu(api, keys, sizes, groups, None, 16, 0.1, 78, "algo/rep0", vals=with_vals,
-                  record=False, scheme="deterministic")
+                  record=False, scheme=scheme)
     assert np.array_equal(host_u64(res.keys), ref.keys)
     if with_vals:
         assert np.array_equal(res.vals.cpu().numpy(), ref.vals)

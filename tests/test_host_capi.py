@@ -221,3 +221,26 @@ def test_deterministic_delivery_matches_golden(name):
             pcs = np.stack([info.hist[:, bnd[t]:bnd[t + 1]].sum(axis=1) for t in range(r)], axis=1)
             ns, _, _ = L.deliver_deterministic(pcs, info.group_lo)
             assert [int(x) for x in ns] == ref["new_sizes"]
+
+
+def test_permuted_delivery_matches_oracle_random():
+    """The native deliver_simple_permuted slices (Feistel enumeration,
+    delivery.py:151-185, core.py:96-159) equal the oracle's restatement."""
+    rng = np.random.default_rng(1)
+    for trial in range(300):
+        r, sub = int(rng.integers(1, 6)), int(rng.integers(1, 6))
+        P = r * sub
+        pcs = rng.integers(0, 40, (P, r)) * (rng.random((P, r)) < 0.7)
+        ls = f"algo/rep0/L{trial % 3}-g{trial % 7}"
+        slices, sizes = O.permuted_plan(pcs.astype(np.int64), 5, ls)
+        ns, sl, st = L.deliver_permuted(pcs, 5, ls)
+        assert [int(x) for x in ns] == sizes
+        e_layout = np.arange(int(pcs.sum()))
+        want = O.deterministic_relayout(e_layout, pcs.astype(np.int64), slices, sizes)
+        got = np.empty_like(e_layout)
+        for s0, d0, ln in sl:
+            got[int(d0):int(d0 + ln)] = e_layout[int(s0):int(s0 + ln)]
+        assert np.array_equal(got, want)
+        ref = O._deterministic_stats(pcs.astype(np.int64), slices)
+        assert [int(x) for x in st] == [ref[k] for k in ("max_words", "max_msgs", "max_sent_msgs",
+                                                         "max_recv_msgs")]
