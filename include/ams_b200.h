@@ -102,6 +102,12 @@ int ams_deliver_deterministic(int P, int r, int pe0, const uint64_t* pieces, uin
 int ams_deliver_permuted(int P, int r, int64_t master_seed, const char* level_stream,
                          const uint64_t* pieces, uint64_t* out_new_sizes, uint64_t* out_slices,
                          int slice_cap, int* out_nslices, uint64_t* out_stats);
+/* deliver_randomized (delivery.py:318-436, default delegation factor
+ * 309-315): chunking, Feistel delegation, per-holder CPython shuffles;
+ * slice_cap >= P*(2r+2) is enough.  Output as ams_deliver_deterministic. */
+int ams_deliver_randomized(int P, int r, int64_t master_seed, const char* level_stream,
+                           const uint64_t* pieces, uint64_t* out_new_sizes, uint64_t* out_slices,
+                           int slice_cap, int* out_nslices, uint64_t* out_stats);
 
 /* ------------------------------------------------------------------ */
 /* Device context: one per GPU (one process per GPU).                  */
@@ -226,11 +232,12 @@ int ams_map_keys(ams_ctx_t* ctx, const void* src, void* dst, uint64_t n, int fro
 
 /* AmsParams (ams.py:33-65) + SeedSpec (core.py:46-71) + key encoding. */
 /* Delivery schemes (delivery.py:439-455 SCHEMES): "simple" (151-180),
- * "deterministic" (188-306, the reference CLI default) and "permuted"
- * (183-185). */
+ * "deterministic" (188-306, the reference CLI default), "permuted"
+ * (183-185) and "randomized" (318-436). */
 #define AMS_SCHEME_SIMPLE 0
 #define AMS_SCHEME_DETERMINISTIC 1
 #define AMS_SCHEME_PERMUTED 2
+#define AMS_SCHEME_RANDOMIZED 3
 
 typedef struct {
   int levels;                          /* k = len(group_counts) */
@@ -242,7 +249,7 @@ typedef struct {
   const char* stream_id;               /* SeedSpec.stream_id, e.g. "algo/rep0" */
   int key_kind;                        /* AMS_KEY_U64 / AMS_KEY_I64 / AMS_KEY_F64 */
   int with_stats;                      /* fill the exchange maxima of the reports */
-  int scheme;                          /* AMS_SCHEME_SIMPLE / _DETERMINISTIC / _PERMUTED */
+  int scheme;                          /* AMS_SCHEME_SIMPLE / _DETERMINISTIC / _PERMUTED / _RANDOMIZED */
 } ams_params_t;
 
 /* One level's report (ams.py:294-308; exchange maxima simnet.py:109-124). */

@@ -270,6 +270,97 @@ def permuted_plan(piece_sizes: np.ndarray, master_seed: int, level_stream: str):
     return slices, new_sizes
 
 
+def default_delegation_factor(p: int, r: int) -> int:
+    """delivery.py:309-315."""
+    if r * p <= 2:
+        return 1
+    a = 0.5 * (math.sqrt(1.0 + r / math.log(r * p / 2.0)) - 1.0)
+    return max(1, math.floor(a))
+
+
+def feistel_apply_all(n: int, master_seed: int, stream_id: str) -> list:
+    """``[feistel_new(n, seed).apply(i) for i in range(n)]`` (core.py:96-159)."""
+    order = feistel_order(n, master_seed, stream_id)
+    perm = [0] * n
+    for rank, i in enumerate(order):
+        perm[i] = rank
+    return perm
+
+
+def randomized_plan(piece_sizes: np.ndarray, master_seed: int, level_stream: str):
+    """``deliver_randomized`` (delivery.py:318-436) with the default
+    delegation factor: pieces above s = ceil(a n / (r p)) are cut into
+    s-element chunks (plus a remainder); full chunks are delegated to holder
+    ``feistel(rank) % p`` (stream ``…/deliver/delegate``); subgroup g numbers
+    the chunks holder by holder in the Feistel order of ``…/deliver/order-g{g}``,
+    each holder's chunks in ``Random(…/deliver/reorder-g{g}-h{holder}).shuffle``
+    order; members own quota slots of that numbering."""
+    P, r = piece_sizes.shape
+    if P % r != 0:
+        raise ValueError(f"{P} PEs cannot form {r} groups")
+    sub = P // r
+    n = int(piece_sizes.sum())
+    a = default_delegation_factor(P, r)
+    s = max(1, -(-(a * n) // (r * P)))
+    chunks = []
+    for j in range(P):
+        for g in range(r):
+            size = int(piece_sizes[j, g])
+            if size == 0:
+                continue
+            if size > s:
+                whole, rem = divmod(size, s)
+                for c in range(whole):
+                    chunks.append((j, g, c * s, s, True))
+                if rem:
+                    chunks.append((j, g, whole * s, rem, False))
+            else:
+                chunks.append((j, g, 0, size, False))
+    dstream = f"{level_stream}/deliver"
+    large = [i for i, ch in enumerate(chunks) if ch[4]]
+    holder_of = {}
+    if large:
+        perm = feistel_apply_all(len(large), master_seed, f"{dstream}/delegate")
+        for rank, cid in enumerate(large):
+            holder_of[cid] = perm[rank] % P
+    held = {}
+    for cid, (j, g, off, ln, lg) in enumerate(chunks):
+        held.setdefault((g, holder_of.get(cid, j)), []).append(cid)
+    start_of = {}
+    totals = [0] * r
+    for g in range(r):
+        running = 0
+        for holder in feistel_order(P, master_seed, f"{dstream}/order-g{g}"):
+            mine = held.get((g, holder), [])
+            if not mine:
+                continue
+            rng = random.Random(stream_seed_int(master_seed, f"{dstream}/reorder-g{g}-h{holder}"))
+            rng.shuffle(mine)
+            for cid in mine:
+                start_of[cid] = running
+                running += chunks[cid][3]
+        totals[g] = running
+    slices = {}
+    for cid, (j, g, off, ln, lg) in enumerate(chunks):
+        m, start = totals[g], start_of[cid]
+        t = ((start + 1) * sub + m - 1) // m - 1               # _slice_range
+        covered = 0
+        while covered < ln and t < sub:
+            hi = (m * (t + 1)) // sub
+            take = min(start + ln, hi) - (start + covered)
+            if take > 0:
+                slices.setdefault((j, g), []).append((t, off + covered, take))
+                covered += take
+            t += 1
+    for key in slices:
+        slices[key].sort(key=lambda c: c[1])
+    new_sizes = [0] * P
+    for g in range(r):
+        for t in range(sub):
+            new_sizes[g * sub + t] = (totals[g] * (t + 1)) // sub - (totals[g] * t) // sub
+    return slices, new_sizes
+
+
 def deterministic_plan(piece_sizes: np.ndarray, group_lo: int = 0):
     """Member assignment of ``deliver_deterministic`` (delivery.py:188-306):
     small pieces (size * 2 * p * r <= n) go whole to member
@@ -440,12 +531,15 @@ def ams_level(buf: np.ndarray, sizes: list, r: int, b: int, a: float,
     pieces = np.zeros((P, r), np.int64)
     for g in range(r):
         pieces[:, g] = hist[:, bnd[g]:bnd[g + 1]].sum(axis=1)
-    if scheme in ("deterministic", "permuted"):                # delivery.py:151-306
+    if scheme in ("deterministic", "permuted", "randomized"):  # delivery.py:151-436
         if scheme == "deterministic":
             slices, new_sizes = deterministic_plan(pieces, group_lo)
-        else:
+        elif scheme == "permuted":
             slices, new_sizes = permuted_plan(pieces, master_seed,
                                               f"{stream}/L{level}-g{group_lo}")
+        else:
+            slices, new_sizes = randomized_plan(pieces, master_seed,
+                                                f"{stream}/L{level}-g{group_lo}")
         out = deterministic_relayout(out, pieces, slices, new_sizes)
         out_org = deterministic_relayout(out_org, pieces, slices, new_sizes)
         if out_vals is not None:
@@ -461,7 +555,7 @@ def ams_level(buf: np.ndarray, sizes: list, r: int, b: int, a: float,
     info = LevelInfo(level, group_lo, n_g, br, drawn, sk, sp, hist, plan,
                      new_sizes)
     if with_stats:
-        if scheme in ("deterministic", "permuted"):
+        if scheme in ("deterministic", "permuted", "randomized"):
             info.stats = _deterministic_stats(pieces, slices)
         else:
             info.stats = _exchange_stats(pieces, sub, list(range(P)))

@@ -216,6 +216,13 @@ def cases():
             cfg(f"perm_{tag}", dist, p, 250, groups, None, 8, 0.2, 5, scheme="permuted")
     cfg("perm_cfg2_scaled_equal", "equal", 64, 1 << 12, (8, 8), None, 16, 0.1, 1,
         scheme="permuted")
+    # deliver_randomized (delivery.py:318-436): chunking, delegation, shuffles.
+    for dist in ("uniform", "sorted", "equal", "zipf:1.1"):
+        for groups, p in (((4, 4), 16), ((2, 2, 4), 16), ((8, 2), 16)):
+            tag = dist.replace(":", "") + "_" + "x".join(map(str, groups))
+            cfg(f"rand_{tag}", dist, p, 250, groups, None, 8, 0.2, 5, scheme="randomized")
+    cfg("rand_cfg2_scaled_sorted", "sorted", 64, 1 << 12, (8, 8), None, 16, 0.1, 1,
+        scheme="randomized")
     cfg("perm_cfg3_scaled", "uniform", 256, 1 << 9, (8, 32), None, 16, 0.1, 2,
         scheme="permuted")
 
@@ -249,6 +256,9 @@ def cases():
     rng = _r.Random(6)
     tiny("perm_tiny_ragged", {pe: [rng.randrange(60) for _ in range(rng.randrange(0, 30))]
                               for pe in range(8)}, (2, 4), b=4, seed=4, scheme="permuted")
+    rng = _r.Random(8)
+    tiny("rand_tiny_ragged", {pe: [rng.randrange(60) for _ in range(rng.randrange(0, 30))]
+                              for pe in range(8)}, (2, 4), b=4, seed=4, scheme="randomized")
     # One big PE: its piece exceeds ceil(n/p) (delivery.py:212-217 ValueError).
     tiny("det_tiny_big_piece", {0: list(range(100)), 1: [5], 2: [7], 3: [9]}, (2, 2), b=4,
          seed=2, scheme="deterministic")

@@ -43,6 +43,7 @@ _SIGNATURES = {
     "ams_plan_level": (_I, [_I, _P, _P, _I, _P, _I, _P, _P, _P, _P, _P]),
     "ams_deliver_deterministic": (_I, [_I, _I, _I, _P, _P, _P, _I, _P, _P]),
     "ams_deliver_permuted": (_I, [_I, _I, _I64, C.c_char_p, _P, _P, _P, _I, _P, _P]),
+    "ams_deliver_randomized": (_I, [_I, _I, _I64, C.c_char_p, _P, _P, _P, _I, _P, _P]),
     "ams_ctx_create": (_I, [_I, _P, C.POINTER(_P)]),
     "ams_ctx_destroy": (_I, [_P]),
     "ams_ctx_set_stream": (_I, [_P, _P]),
@@ -245,20 +246,31 @@ def deliver_deterministic(pieces: np.ndarray, pe0: int = 0, with_stats: bool = T
     return ns, slices[:cnt.value].copy(), stats
 
 
+def _deliver_seeded(fn, pieces, master_seed, level_stream, with_stats):
+    pc = np.ascontiguousarray(pieces, dtype=np.uint64)
+    P, r = pc.shape
+    cap = P * (2 * r + 2) + 16
+    ns = np.zeros(P, np.uint64)
+    slices = np.zeros((cap, 3), np.uint64)
+    cnt = C.c_int(0)
+    stats = np.zeros(4, np.uint64) if with_stats else None
+    check(fn(P, r, int(master_seed), level_stream.encode(), pc.ctypes.data, ns.ctypes.data,
+             slices.ctypes.data, cap, C.byref(cnt), ptr(stats)))
+    return ns, slices[:cnt.value].copy(), stats
+
+
 def deliver_permuted(pieces: np.ndarray, master_seed: int, level_stream: str,
                      with_stats: bool = True):
     """Host restatement of deliver_simple_permuted's slices
     (delivery.py:151-185): as :func:`deliver_deterministic`."""
-    pc = np.ascontiguousarray(pieces, dtype=np.uint64)
-    P, r = pc.shape
-    ns = np.zeros(P, np.uint64)
-    slices = np.zeros((P * (r + 1), 3), np.uint64)
-    cnt = C.c_int(0)
-    stats = np.zeros(4, np.uint64) if with_stats else None
-    check(lib.ams_deliver_permuted(P, r, int(master_seed), level_stream.encode(), pc.ctypes.data,
-                                   ns.ctypes.data, slices.ctypes.data, P * (r + 1), C.byref(cnt),
-                                   ptr(stats)))
-    return ns, slices[:cnt.value].copy(), stats
+    return _deliver_seeded(lib.ams_deliver_permuted, pieces, master_seed, level_stream, with_stats)
+
+
+def deliver_randomized(pieces: np.ndarray, master_seed: int, level_stream: str,
+                       with_stats: bool = True):
+    """Host restatement of deliver_randomized's slices (delivery.py:318-436):
+    as :func:`deliver_deterministic`."""
+    return _deliver_seeded(lib.ams_deliver_randomized, pieces, master_seed, level_stream, with_stats)
 
 
 # ---------------------------------------------------------------- device context

@@ -24,7 +24,7 @@ from .params import Element, as_params
 
 _SORTERS: dict = {}
 
-SUPPORTED_SCHEMES = ("simple", "deterministic", "permuted")
+SUPPORTED_SCHEMES = ("simple", "deterministic", "permuted", "randomized")
 
 
 def get_sorter(device=None) -> AmsSorter:
@@ -40,7 +40,7 @@ def _check_scheme(scheme: str):
     if scheme not in SUPPORTED_SCHEMES:
         raise ValueError(
             f"delivery scheme {scheme!r} is not implemented on the B200 path; "
-            f"supported: {SUPPORTED_SCHEMES} (delivery.py:151-306)")
+            f"supported: {SUPPORTED_SCHEMES} (delivery.py:151-455)")
 
 
 def ams_sort_tensors(keys: torch.Tensor, pe_sizes, params, seed, vals: torch.Tensor | None = None,

@@ -1186,8 +1186,7 @@ int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* p
   if (n && (!keys || !out)) return set_error(AMS_EINVAL, "null key buffer");
   const bool user_vals = vals != nullptr;
   if (user_vals && !out_vals) return set_error(AMS_EINVAL, "values need an output buffer");
-  if (prm->scheme != AMS_SCHEME_SIMPLE && prm->scheme != AMS_SCHEME_DETERMINISTIC &&
-      prm->scheme != AMS_SCHEME_PERMUTED)
+  if (prm->scheme < AMS_SCHEME_SIMPLE || prm->scheme > AMS_SCHEME_RANDOMIZED)
     return set_error(AMS_EINVAL, "unknown delivery scheme");
   // Deterministic delivery (delivery.py:188-306) can put a later source's
   // piece into an earlier member, so group-buffer order stops being origin
@@ -1310,8 +1309,11 @@ int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* p
     // assignment per group (host), the simple layout into scratch, then the
     // slices copied to the members' arrays in receive order.
     const bool relayout = det && gn[0] / r > 1;
+    // Randomized delivery chunks large pieces into several messages even
+    // with one member per subgroup: its planner also supplies those stats.
+    const bool plan_slices = relayout || (prm->scheme == AMS_SCHEME_RANDOMIZED && rec.has_stats && n > 0);
     std::vector<uint64_t> items;
-    if (relayout) {
+    if (plan_slices) {
       std::vector<uint64_t> pieces, slices;
       for (int g = 0; g < G; ++g) {
         const int P = gn[g];
@@ -1321,20 +1323,23 @@ int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* p
             for (uint64_t bb = rec.boundaries[(size_t)g * (r + 1) + t];
                  bb < rec.boundaries[(size_t)g * (r + 1) + t + 1]; ++bb)
               pieces[(size_t)j * r + t] += rec.hist[(size_t)(gf[g] + j) * nb_stride + bb];
-        slices.assign(3 * (size_t)P * (r + 1), 0);
+        const int cap = P * (2 * r + 2) + 16;
+        slices.assign(3 * (size_t)cap, 0);
         int ns = 0;
         uint64_t* st4 = rec.has_stats ? rec.stats.data() + 4 * (size_t)g : nullptr;
-        if (prm->scheme == AMS_SCHEME_PERMUTED) {
-          const std::string ls = std::string(prm->stream_id) + "/L" + std::to_string(lv) + "-g" +
-                                 std::to_string(gf[g]);
+        const std::string ls = std::string(prm->stream_id) + "/L" + std::to_string(lv) + "-g" +
+                               std::to_string(gf[g]);
+        if (prm->scheme == AMS_SCHEME_PERMUTED)
           rc = ams_deliver_permuted(P, r, prm->master_seed, ls.c_str(), pieces.data(),
-                                    rec.new_sizes.data() + gf[g], slices.data(), P * (r + 1), &ns, st4);
-        } else {
+                                    rec.new_sizes.data() + gf[g], slices.data(), cap, &ns, st4);
+        else if (prm->scheme == AMS_SCHEME_RANDOMIZED)
+          rc = ams_deliver_randomized(P, r, prm->master_seed, ls.c_str(), pieces.data(),
+                                      rec.new_sizes.data() + gf[g], slices.data(), cap, &ns, st4);
+        else
           rc = ams_deliver_deterministic(P, r, gf[g], pieces.data(), rec.new_sizes.data() + gf[g],
-                                         slices.data(), P * (r + 1), &ns, st4);
-        }
+                                         slices.data(), cap, &ns, st4);
         if (rc) return rc;
-        for (int q = 0; q < ns; ++q) {
+        for (int q = 0; relayout && q < ns; ++q) {
           const uint64_t s0 = dst_start[g] + slices[3 * q], d0 = dst_start[g] + slices[3 * q + 1];
           for (uint64_t o = 0; o < slices[3 * q + 2]; o += kCopyItemKeys) {
             items.push_back(s0 + o);

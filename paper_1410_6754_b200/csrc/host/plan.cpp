@@ -122,6 +122,60 @@ void exchange_stats(const std::vector<uint64_t>& pieces, int P, int r, uint64_t 
   out[3] = mr;
 }
 
+// feistel_new(n, SeedSpec(master, stream)).apply(i) for every i
+// (core.py:96-159): four rounds (lo, hi) -> (hi, (lo + T_k[hi]) mod side)
+// over side^2 >= n, T_k[v] = splitmix64(v ^ key64(k)) mod side, cycle
+// walking values >= n; key64(k) = first 8 bytes (big endian) of
+// blake2b-128("{master}\x1f{stream}\x1fk{k}") (core.py:69-71).
+std::vector<uint64_t> feistel_perm(uint64_t n, int64_t master_seed, const std::string& stream) {
+  uint64_t side = (uint64_t)std::sqrt((double)n);
+  while (side * side > n) --side;
+  while (side * side < n) ++side;
+  auto mix64 = [](uint64_t x) {
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
+    return x ^ (x >> 31);
+  };
+  std::vector<uint64_t> tables(4 * side), perm(n);
+  for (int i = 0; i < 4; ++i) {
+    const std::string text = std::to_string(master_seed) + "\x1f" + stream + "\x1fk" + std::to_string(i);
+    uint8_t d[16];
+    blake2b_128(reinterpret_cast<const uint8_t*>(text.data()), text.size(), d);
+    uint64_t key = 0;
+    for (int b = 0; b < 8; ++b) key = (key << 8) | d[b];
+    for (uint64_t v = 0; v < side; ++v) tables[i * side + v] = mix64(v ^ key) % side;
+  }
+  for (uint64_t j = 0; j < n; ++j) {
+    uint64_t x = j;
+    for (uint64_t it = 0; it < side * side; ++it) {
+      uint64_t hi = x / side, lo = x % side;
+      for (int i = 0; i < 4; ++i) {
+        const uint64_t nhi = (lo + tables[i * side + hi]) % side;
+        lo = hi;
+        hi = nhi;
+      }
+      x = lo + hi * side;
+      if (x < n) break;
+    }
+    perm[j] = x;
+  }
+  return perm;
+}
+
+// sorted(range(n), key=feistel.apply): the enumeration order (delivery.py:131-134).
+std::vector<int> feistel_order(int n, int64_t master_seed, const std::string& stream) {
+  const std::vector<uint64_t> perm = feistel_perm((uint64_t)n, master_seed, stream);
+  std::vector<int> order(n);
+  for (int j = 0; j < n; ++j) order[j] = j;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return perm[a] < perm[b]; });
+  return order;
+}
+
+// _slice_range (delivery.py:83-106): numbers [start, start + size) of a
+// subgroup with m numbers over `sub` members -> cuts (piece offset base + ...).
+bool slice_range(int j, int g, int sub, uint64_t m, uint64_t start, uint64_t size, uint64_t base,
+                 std::vector<struct Cut>& cuts);
+
 // One slice of a delivery: elements [off, off + len) of piece (member j,
 // subgroup g) go to member t of subgroup g.
 struct Cut { int j, g, t; uint64_t off, len; };
@@ -130,6 +184,23 @@ struct Cut { int j, g, t; uint64_t off, len; };
 // source member, bucket; dst in the new member arrays, receivers
 // concatenating by source, simnet.py:324-325), new member sizes and the
 // data-exchange shape (simnet.py:294-335).
+bool slice_range(int j, int g, int sub, uint64_t m, uint64_t start, uint64_t size, uint64_t base,
+                 std::vector<Cut>& cuts) {
+  if (size == 0 || m == 0) return true;
+  int t = (int)((((unsigned __int128)(start + 1) * sub + m - 1) / m) - 1);
+  uint64_t covered = 0;
+  while (covered < size && t < sub) {
+    const uint64_t hi = (uint64_t)(((unsigned __int128)m * (t + 1)) / sub);
+    const int64_t take = (int64_t)std::min(start + size, hi) - (int64_t)(start + covered);
+    if (take > 0) {
+      cuts.push_back({j, g, t, base + covered, (uint64_t)take});
+      covered += (uint64_t)take;
+    }
+    ++t;
+  }
+  return covered == size;
+}
+
 int emit_slices(int P, int r, const uint64_t* pieces, const std::vector<Cut>& cuts,
                 uint64_t* out_new_sizes, uint64_t* out_slices, int slice_cap, int* out_nslices,
                 uint64_t* out_stats) {
@@ -150,7 +221,8 @@ int emit_slices(int P, int r, const uint64_t* pieces, const std::vector<Cut>& cu
   for (size_t i = 0; i < cuts.size(); ++i) order[i] = (int)i;
   std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
     const int da = cuts[a].g * sub + cuts[a].t, db = cuts[b].g * sub + cuts[b].t;
-    return da != db ? da < db : cuts[a].j < cuts[b].j;
+    if (da != db) return da < db;
+    return cuts[a].j != cuts[b].j ? cuts[a].j < cuts[b].j : cuts[a].off < cuts[b].off;
   });
   std::vector<uint64_t> fill(P, 0);
   std::vector<uint64_t> sw(P, 0), rw(P, 0), sm(P, 0), rm(P, 0);
@@ -352,64 +424,101 @@ int ams_deliver_permuted(int P, int r, int64_t master_seed, const char* level_st
     return set_error(AMS_EINVAL, std::to_string(P) + " PEs cannot form " + std::to_string(r) + " groups");
   if (!level_stream) return set_error(AMS_EINVAL, "null stream id");
   const int sub = P / r;
-  uint64_t side = (uint64_t)std::sqrt((double)P);
-  while (side * side > (uint64_t)P) --side;
-  while (side * side < (uint64_t)P) ++side;
-  auto mix64 = [](uint64_t x) {
-    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
-    x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
-    return x ^ (x >> 31);
-  };
   std::vector<Cut> cuts;
-  std::vector<uint64_t> tables(4 * side), perm(P);
-  std::vector<int> order(P);
   for (int g = 0; g < r; ++g) {
-    const std::string stream = std::string(level_stream) + "/deliver/order-g" + std::to_string(g);
-    for (int i = 0; i < 4; ++i) {  // SeedSpec.key64(i), core.py:69-71
-      const std::string text = std::to_string(master_seed) + "\x1f" + stream + "\x1fk" + std::to_string(i);
-      uint8_t d[16];
-      blake2b_128(reinterpret_cast<const uint8_t*>(text.data()), text.size(), d);
-      uint64_t key = 0;
-      for (int b = 0; b < 8; ++b) key = (key << 8) | d[b];
-      for (uint64_t v = 0; v < side; ++v) tables[i * side + v] = mix64(v ^ key) % side;
-    }
-    for (int j = 0; j < P; ++j) {
-      uint64_t x = (uint64_t)j;
-      for (uint64_t it = 0; it < side * side; ++it) {
-        uint64_t hi = x / side, lo = x % side;
-        for (int i = 0; i < 4; ++i) {
-          const uint64_t nhi = (lo + tables[i * side + hi]) % side;
-          lo = hi;
-          hi = nhi;
-        }
-        x = lo + hi * side;
-        if (x < (uint64_t)P) break;
-      }
-      perm[j] = x;
-    }
-    for (int j = 0; j < P; ++j) order[j] = j;
-    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return perm[a] < perm[b]; });
+    const std::vector<int> order =
+        feistel_order(P, master_seed, std::string(level_stream) + "/deliver/order-g" + std::to_string(g));
     uint64_t m = 0;
     for (int j = 0; j < P; ++j) m += pieces[(size_t)j * r + g];
     uint64_t start = 0;
     for (int j : order) {
       const uint64_t size = pieces[(size_t)j * r + g];
-      if (size) {  // _slice_range (delivery.py:83-106)
-        int t = (int)((((unsigned __int128)(start + 1) * sub + m - 1) / m) - 1);
-        uint64_t covered = 0;
-        while (covered < size && t < sub) {
-          const uint64_t hi = (uint64_t)(((unsigned __int128)m * (t + 1)) / sub);
-          const int64_t take = (int64_t)std::min(start + size, hi) - (int64_t)(start + covered);
-          if (take > 0) {
-            cuts.push_back({j, g, t, covered, (uint64_t)take});
-            covered += (uint64_t)take;
-          }
-          ++t;
-        }
-        if (covered != size) return set_error(AMS_EINTERNAL, "quota mapping failed to cover a piece");
-      }
+      if (!slice_range(j, g, sub, m, start, size, 0, cuts))
+        return set_error(AMS_EINTERNAL, "quota mapping failed to cover a piece");
       start += size;
     }
+  }
+  return emit_slices(P, r, pieces, cuts, out_new_sizes, out_slices, slice_cap, out_nslices, out_stats);
+}
+
+// deliver_randomized (delivery.py:318-436) with the default delegation
+// factor (309-315): pieces above s = ceil(a n / (r p)) are cut into
+// s-element chunks plus a remainder; full chunks go to holder
+// feistel(rank) % p ("…/deliver/delegate"); subgroup g numbers its chunks
+// holder by holder in the Feistel order of "…/deliver/order-g{g}", each
+// holder's chunks in Random("…/deliver/reorder-g{g}-h{holder}").shuffle
+// order (CPython's shuffle over MT19937 randbelow); members own quota
+// slots of that numbering.  Output as ams_deliver_deterministic.
+int ams_deliver_randomized(int P, int r, int64_t master_seed, const char* level_stream,
+                           const uint64_t* pieces, uint64_t* out_new_sizes, uint64_t* out_slices,
+                           int slice_cap, int* out_nslices, uint64_t* out_stats) {
+  if (P < 1 || r < 1 || P % r != 0)
+    return set_error(AMS_EINVAL, std::to_string(P) + " PEs cannot form " + std::to_string(r) + " groups");
+  if (!level_stream) return set_error(AMS_EINVAL, "null stream id");
+  const int sub = P / r;
+  uint64_t n = 0;
+  for (int i = 0; i < P * r; ++i) n += pieces[i];
+  uint64_t a = 1;
+  if ((uint64_t)r * P > 2) {
+    const double x = 0.5 * (std::sqrt(1.0 + r / std::log(r * (double)P / 2.0)) - 1.0);
+    a = std::max<uint64_t>(1, (uint64_t)std::floor(x));
+  }
+  const uint64_t rp = (uint64_t)r * P;
+  const uint64_t s = std::max<uint64_t>(1, (a * n + rp - 1) / rp);
+  struct Chunk { int j, g; uint64_t off, len; bool large; };
+  std::vector<Chunk> chunks;
+  for (int j = 0; j < P; ++j)
+    for (int g = 0; g < r; ++g) {
+      const uint64_t size = pieces[(size_t)j * r + g];
+      if (size == 0) continue;
+      if (size > s) {
+        const uint64_t whole = size / s, rem = size % s;
+        for (uint64_t c = 0; c < whole; ++c) chunks.push_back({j, g, c * s, s, true});
+        if (rem) chunks.push_back({j, g, whole * s, rem, false});
+      } else {
+        chunks.push_back({j, g, 0, size, false});
+      }
+    }
+  const std::string ds = std::string(level_stream) + "/deliver";
+  std::vector<int> holder(chunks.size());
+  for (size_t i = 0; i < chunks.size(); ++i) holder[i] = chunks[i].j;
+  std::vector<size_t> large;
+  for (size_t i = 0; i < chunks.size(); ++i)
+    if (chunks[i].large) large.push_back(i);
+  if (!large.empty()) {
+    const std::vector<uint64_t> perm = feistel_perm(large.size(), master_seed, ds + "/delegate");
+    for (size_t rank = 0; rank < large.size(); ++rank) holder[large[rank]] = (int)(perm[rank] % (uint64_t)P);
+  }
+  std::vector<std::vector<size_t>> held((size_t)r * P);
+  for (size_t i = 0; i < chunks.size(); ++i) held[(size_t)chunks[i].g * P + holder[i]].push_back(i);
+  std::vector<uint64_t> start_of(chunks.size(), 0), totals(r, 0);
+  for (int g = 0; g < r; ++g) {
+    uint64_t running = 0;
+    for (int h : feistel_order(P, master_seed, ds + "/order-g" + std::to_string(g))) {
+      std::vector<size_t>& mine = held[(size_t)g * P + h];
+      if (mine.empty()) continue;
+      uint32_t words[4];
+      const int nw = stream_seed_words(std::to_string(master_seed) + "\x1f" + ds + "/reorder-g" +
+                                           std::to_string(g) + "-h" + std::to_string(h) + "\x1f",
+                                       words);
+      Mt19937 rng;
+      rng.init_by_array(words, nw);
+      for (size_t i = mine.size() - 1; i >= 1; --i) {  // Random.shuffle
+        const size_t k = (size_t)rng.randbelow(i + 1);
+        std::swap(mine[i], mine[k]);
+      }
+      for (size_t cid : mine) {
+        start_of[cid] = running;
+        running += chunks[cid].len;
+      }
+    }
+    totals[g] = running;
+  }
+  std::vector<Cut> cuts;
+  for (size_t cid = 0; cid < chunks.size(); ++cid) {
+    const Chunk& ch = chunks[cid];
+    if (!slice_range(ch.j, ch.g, sub, totals[ch.g], start_of[cid], ch.len, ch.off, cuts))
+      return set_error(AMS_EINTERNAL, "quota mapping failed to cover a piece");
   }
   return emit_slices(P, r, pieces, cuts, out_new_sizes, out_slices, slice_cap, out_nslices, out_stats);
 }

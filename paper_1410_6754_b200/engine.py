@@ -41,7 +41,7 @@ def key_kind_of(t: torch.Tensor, key_kind=None) -> int:
 
 
 # Delivery schemes (delivery.py:439-455 SCHEMES) the device path implements.
-SCHEMES = {"simple": 0, "deterministic": 1, "permuted": 2}  # AMS_SCHEME_*
+SCHEMES = {"simple": 0, "deterministic": 1, "permuted": 2, "randomized": 3}  # AMS_SCHEME_*
 
 
 @dataclass

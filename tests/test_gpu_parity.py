@@ -97,7 +97,8 @@ def test_golden_parity(api, name, native):
     check_levels(res, g)
 
 
-@pytest.mark.parametrize("name", [n for n in G.names() if n.startswith(("tiny", "det_tiny", "perm_tiny"))])
+@pytest.mark.parametrize("name", [n for n in G.names()
+                                  if n.startswith(("tiny", "det_tiny", "perm_tiny", "rand_tiny"))])
 def test_dropin_elements(api, name):
     """ams_sort(net, data, params, scheme, seed) returns the reference's
     exact per-PE Element lists."""
@@ -175,7 +176,7 @@ def test_oracle_parity_random(api, groups, npe, dist, native):
     ((4, 4, 4), 1024, "few"), ((8, 32), 1 << 9, "equal"), ((2, 8), 5000, "uniform"),
 ])
 @pytest.mark.parametrize("with_vals", [True, False], ids=["kv", "keys"])
-@pytest.mark.parametrize("scheme", ["deterministic", "permuted"])
+@pytest.mark.parametrize("scheme", ["deterministic", "permuted", "randomized"])
 def test_oracle_parity_deterministic(api, groups, npe, dist, with_vals, scheme):
     """scheme="deterministic" (delivery.py:188-306: two-phase assignment)
     and "permuted" (delivery.py:183-185: Feistel enumeration): member

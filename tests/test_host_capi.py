@@ -223,17 +223,24 @@ def test_deterministic_delivery_matches_golden(name):
             assert [int(x) for x in ns] == ref["new_sizes"]
 
 
-def test_permuted_delivery_matches_oracle_random():
-    """The native deliver_simple_permuted slices (Feistel enumeration,
-    delivery.py:151-185, core.py:96-159) equal the oracle's restatement."""
+@pytest.mark.parametrize("scheme", ["permuted", "randomized"])
+def test_seeded_delivery_matches_oracle_random(scheme):
+    """The native deliver_simple_permuted (Feistel enumeration,
+    delivery.py:151-185, core.py:96-159) and deliver_randomized (chunking,
+    delegation, CPython shuffles, delivery.py:318-436) slices equal the
+    oracle's restatements."""
+    planner, native = {"permuted": (O.permuted_plan, L.deliver_permuted),
+                       "randomized": (O.randomized_plan, L.deliver_randomized)}[scheme]
     rng = np.random.default_rng(1)
     for trial in range(300):
         r, sub = int(rng.integers(1, 6)), int(rng.integers(1, 6))
         P = r * sub
         pcs = rng.integers(0, 40, (P, r)) * (rng.random((P, r)) < 0.7)
+        if trial % 4 == 0:
+            pcs[0, 0] = 400  # one large piece: chunked and delegated
         ls = f"algo/rep0/L{trial % 3}-g{trial % 7}"
-        slices, sizes = O.permuted_plan(pcs.astype(np.int64), 5, ls)
-        ns, sl, st = L.deliver_permuted(pcs, 5, ls)
+        slices, sizes = planner(pcs.astype(np.int64), 5, ls)
+        ns, sl, st = native(pcs, 5, ls)
         assert [int(x) for x in ns] == sizes
         e_layout = np.arange(int(pcs.sum()))
         want = O.deterministic_relayout(e_layout, pcs.astype(np.int64), slices, sizes)
