@@ -22,6 +22,11 @@
 #include "ams_device.cuh"
 #include "launch.h"
 
+// Sub-buckets of the cell sort per key of capacity (A/B knob).
+#ifndef AMS_SUBK_MULT
+#define AMS_SUBK_MULT 2
+#endif
+
 namespace ams {
 
 namespace {
@@ -1025,7 +1030,7 @@ __global__ void k_bucket_ranges(const uint8_t* __restrict__ blobs, const uint64_
   d.sh = (uint32_t)max(0, bit_length64(range) - 26);
   const uint64_t R = range >> d.sh;
   d.m32 = R + 1 <= (uint64_t)d.nb ? 0u : (uint32_t)(((uint64_t)d.nb << 32) / (R + 1));
-  const uint64_t mk = (uint64_t)d.m32 * (uint64_t)(2 * AMS_SMEM_SORT_CAP);
+  const uint64_t mk = (uint64_t)d.m32 * (uint64_t)(AMS_SUBK_MULT * AMS_SMEM_SORT_CAP);
   d.q = mk < (1ull << 32) ? mk : 0;  // sub-bucket multiplier of the cell sort
   out[s] = d;
 }
@@ -1039,7 +1044,7 @@ __global__ void k_gather_bounds(const uint64_t* __restrict__ bounds, const int32
   out[2 * i + 1] = bounds[2 * sel[i] + 1];
 }
 
-constexpr int kCellSubBuckets = 2 * AMS_SMEM_SORT_CAP;  // sub-buckets of a digit cell (= kSubK)
+constexpr int kCellSubBuckets = AMS_SUBK_MULT * AMS_SMEM_SORT_CAP;  // sub-buckets of a digit cell (= kSubK)
 
 __global__ void k_final_ranges(const uint64_t* __restrict__ bounds, int nseg, int nb,
                                DigitCls* __restrict__ out) {
@@ -1419,14 +1424,15 @@ __global__ void __launch_bounds__(kSortThreads, kSortCtas)
         return;
       }
       const uint64_t range = mx - mn;
-      exact = range < 2 * (uint64_t)n;  // one key value per sub-bucket
-      // Sub-bucket = ((k - mn) >> sh) * m32 >> 32 in [0, 2n), monotone.
+      const uint32_t nsub = min(2 * n, (uint32_t)kSubK);
+      exact = range < (uint64_t)nsub;  // one key value per sub-bucket
+      // Sub-bucket = ((k - mn) >> sh) * m32 >> 32 in [0, nsub), monotone.
       lo = mn;
       hi_key = mx;
       sh = (uint32_t)max(0, bit_length64(range) - 32);
       // floor(2n * 2^32 / w32) - 1 <= the exact quotient: sub stays below 2n.
       m32 = exact ? 0
-                  : (uint32_t)((float)(2 * n) * 4294967296.0f / (float)((range >> sh) + 1)) - 1u;
+                  : (uint32_t)((float)nsub * 4294967296.0f / (float)((range >> sh) + 1)) - 1u;
       sub0 = 0;
     } else {
       __syncthreads();
