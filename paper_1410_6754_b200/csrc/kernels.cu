@@ -95,26 +95,33 @@ __global__ void k_gather_vals(const uint64_t* __restrict__ vals, const uint64_t*
 }
 
 // -------------------------------------------------------------------- K2
-// rank_i = #{j : (k_j, p_j) < (k_i, p_i)} over the group's sample; every
-// warp walks the sample 32 elements at a time and broadcasts them with
-// __shfl_sync (the all-gather + rank-by-counting of fastsort.py:57-108).
+// rank_i = #{j : (k_j, p_j) < (k_i, p_i)} over the group's sample (the
+// all-gather + rank-by-counting of fastsort.py:57-108).  A CTA ranks 64
+// elements: warp w owns elements (w & 1) * 32 + lane and counts over the
+// w >> 1 quarter of the sample, 32 sample elements at a time broadcast
+// with __shfl_sync; the four partial counts meet in shared memory.
+constexpr int kRankElems = 64, kRankSplit = 4;
 __global__ void __launch_bounds__(256) k_sample_rank(const uint64_t* __restrict__ keys,
                                                      const uint32_t* __restrict__ pos,
                                                      const uint64_t* __restrict__ soff,
                                                      uint64_t* __restrict__ sorted_keys,
                                                      uint32_t* __restrict__ sorted_pos) {
+  __shared__ uint32_t part[kRankSplit][kRankElems];
   const int g = blockIdx.y;
   const uint64_t s0 = soff[g], S = soff[g + 1] - s0;
-  const uint64_t first = (uint64_t)blockIdx.x * blockDim.x;
+  const uint64_t first = (uint64_t)blockIdx.x * kRankElems;
   if (first >= S) return;
-  const uint64_t i = first + threadIdx.x;
-  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int slot = (w & 1) * 32 + lane, quarter = w >> 1;
+  const uint64_t i = first + slot;
   const bool mine = i < S;
   const uint64_t ki = mine ? keys[s0 + i] : ~0ULL;
   const uint32_t pi = mine ? pos[s0 + i] : 0xFFFFFFFFu;
+  const uint64_t per = ((S + kRankSplit - 1) / kRankSplit + 31) & ~31ULL;
+  const uint64_t j0 = quarter * per, j1 = min(S, j0 + per);
   uint32_t cnt = 0;
-  for (uint64_t c = 0; c < S; c += 32) {
-    const bool ok = c + lane < S;
+  for (uint64_t c = j0; c < j1; c += 32) {
+    const bool ok = c + lane < j1;
     const uint64_t kl = ok ? keys[s0 + c + lane] : ~0ULL;
     const uint32_t pl = ok ? pos[s0 + c + lane] : 0xFFFFFFFFu;
 #pragma unroll 8
@@ -124,9 +131,17 @@ __global__ void __launch_bounds__(256) k_sample_rank(const uint64_t* __restrict_
       cnt += (kj < ki) | ((kj == ki) & (pj < pi));
     }
   }
-  if (mine) {
-    sorted_keys[s0 + cnt] = ki;
-    sorted_pos[s0 + cnt] = pi;
+  part[quarter][slot] = cnt;
+  __syncthreads();
+  if (threadIdx.x < kRankElems) {
+    const uint64_t e = first + threadIdx.x;
+    if (e < S) {
+      uint32_t rank = 0;
+#pragma unroll
+      for (int q = 0; q < kRankSplit; ++q) rank += part[q][threadIdx.x];
+      sorted_keys[s0 + rank] = keys[s0 + e];
+      sorted_pos[s0 + rank] = pos[s0 + e];
+    }
   }
 }
 
@@ -1680,7 +1695,7 @@ cudaError_t launch_sample_rank(cudaStream_t st, int ngroups, uint64_t max_s, con
                                const uint32_t* pos, const uint64_t* soff, uint64_t* sorted_keys,
                                uint32_t* sorted_pos) {
   if (ngroups == 0 || max_s == 0) return cudaSuccess;
-  dim3 grid((unsigned)((max_s + 255) / 256), (unsigned)ngroups);
+  dim3 grid((unsigned)((max_s + kRankElems - 1) / kRankElems), (unsigned)ngroups);
   k_sample_rank<<<grid, 256, 0, st>>>(keys, pos, soff, sorted_keys, sorted_pos);
   return cudaGetLastError();
 }
