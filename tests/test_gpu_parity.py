@@ -221,7 +221,8 @@ def test_oracle_parity_deterministic(api, groups, npe, dist, with_vals, scheme):
     ((16,), 16, 1 << 16, "uniform"), ((4,), 4, 1 << 18, "f64"), ((2, 2), 4, 1 << 19, "narrow"),
     ((4,), 4, 1 << 18, "clustered"), ((8, 8), 16, 1 << 12, "uniform"),
 ])
-def test_oracle_parity_keys_only(api, groups, b, npe, dist):
+@pytest.mark.parametrize("with_stats", [True, False], ids=["stats", "nostats"])
+def test_oracle_parity_keys_only(api, groups, b, npe, dist, with_stats):
     """Keys-only sorts take the bucket-major last level and the
     fixed-capacity final partition (buckets above shared memory; counting-
     only cells for few-valued buckets, exact rounds for overflowed buckets):
@@ -253,8 +254,8 @@ def test_oracle_parity_keys_only(api, groups, b, npe, dist):
     ref = O.ams_sort(keys, sizes, groups, None, b, 0.1, 79, "algo/rep0", with_stats=False)
     ctx = api.get_sorter(0).ctx
     before = ctx.final_sort_stats()
-    res = api.ams_sort_tensors(dev_u64(keys), sizes, AmsParams(tuple(groups), None, b, 0.1),
-                               SeedSpec(79, "algo/rep0"), key_kind="u64")
+    res = api.get_sorter(0).sort(dev_u64(keys), sizes, AmsParams(tuple(groups), None, b, 0.1),
+                                 SeedSpec(79, "algo/rep0"), key_kind="u64", with_stats=with_stats)
     torch.cuda.synchronize()
     after = ctx.final_sort_stats()
     if npe * p // (int(np.prod(groups)) * b) > 2 * 4096:  # buckets well above shared memory
@@ -266,6 +267,10 @@ def test_oracle_parity_keys_only(api, groups, b, npe, dist):
     for rec, infos in zip(res.levels, ref.levels):
         for gi, info in enumerate(infos):
             assert [int(x) for x in rec.boundaries[gi]] == list(info.plan.boundaries)
+        assert [int(x) for x in rec.new_sizes] == [s for info in infos for s in info.new_sizes]
+    for mine, theirs in zip(res.reports, ref.reports):
+        for k, v in theirs.items():
+            assert mine[k] == v, (k, mine[k], v)
 
 
 def test_ragged_and_empty_pes(api):
