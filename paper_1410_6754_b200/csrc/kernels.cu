@@ -1591,6 +1591,177 @@ __global__ void __launch_bounds__(kSortThreads, kSortCtas)
   }
 }
 
+// Keys-only sort of the fixed-capacity digit cells (mode 3), the hot final
+// step of a bucket-major last level.  Same counting sort as k_smem_sort,
+// specialised: the cell's refined digit is always available (no min/max
+// attempt), counters are whole 32-bit words (no packed halves), the item
+// loop runs over the cell's used items only (uniform bound), and equal keys
+// need no tie order.
+//   1. sub = umulhi((key - lo) >> sh, m * K) - digit * K in [0, K); one
+//      shared atomic per key gives its rank in the sub-bucket;
+//   2. block scan of the K counters (thread t owns words [32t, 32t + 32),
+//      uint4 chunk c stored at c ^ (t & 7): conflict-free) fused with the
+//      count of sub-buckets holding >= 2 keys;
+//   3. place; the key of rank 1 queues its sub-bucket;
+//   4. a thread per queued sub-bucket sorts it in place (2-3 keys by a
+//      network, more by insertion; above kRankMax the cell goes to the LSD
+//      fallback list);
+//   5. 16-byte stores to the output.
+// Cells without a refined digit (m * K >= 2^32) go to the LSD list; cells
+// of counting-only buckets (m == 0) are one key value: filled directly.
+constexpr int kFxThreads = 256;
+constexpr int kFxItems = kSortCap / kFxThreads;   // 16
+constexpr int kFxWords = kSubK / kFxThreads;      // 32 counters per scan thread
+static_assert(kFxWords == 32, "fixed-cell counter layout assumes 32 words per thread");
+__device__ __forceinline__ uint32_t fx_sw(uint32_t s) { return s ^ (((s >> 5) & 7u) << 2); }
+
+template <int KIND_OUT>
+__global__ void __launch_bounds__(kFxThreads, 3)
+    k_cell_sort_fixed(const uint64_t* __restrict__ src, uint64_t* __restrict__ out, CellSource cs,
+                      OverflowRec* __restrict__ fb, unsigned int* __restrict__ fb_count) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ uint32_t s_scan[kFxThreads / 32 + 1];
+  __shared__ uint32_t s_big[kFxThreads / 32];
+  uint64_t* kB = reinterpret_cast<uint64_t*>(smem);
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(kB + kSortCap);
+  uint16_t* q = reinterpret_cast<uint16_t*>(cnt + kSubK);
+  const uint32_t cid = blockIdx.x;
+  const uint32_t n = cs.cell_cnt[cid];
+  if (n == 0) return;
+  const uint64_t off = (uint64_t)cid * kSortCap, oo = cs.cell_base[cid];
+  const uint32_t seg = cs.cell_seg[cid];
+  const DigitCls& d = cs.dcls[seg];
+  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint32_t digit = cid - cs.cell0[seg];
+  if (d.m32 == 0) {  // counting-only bucket: one key value per cell
+    const uint64_t ko = from_ordered<KIND_OUT>(d.lo + digit);
+    for (uint32_t i = tid; i < n; i += kFxThreads) out[oo + i] = ko;
+    return;
+  }
+  if (d.q == 0) {
+    if (tid == 0) {
+      OverflowRec r; r.off = off; r.count = n; r.lo = 0; r.hi = 0; r.out = oo;
+      fb[atomicAdd(fb_count, 1u)] = r;
+    }
+    return;
+  }
+  const uint64_t lo = d.lo;
+  const uint32_t sh = d.sh, mk = (uint32_t)d.q, sub0 = digit * (uint32_t)kSubK;
+  uint4* const cw4 = reinterpret_cast<uint4*>(cnt) + tid * (kFxWords / 4);
+  const uint32_t rot = tid & 7u;
+#pragma unroll
+  for (int c = 0; c < kFxWords / 4; ++c) cw4[c ^ rot] = make_uint4(0, 0, 0, 0);
+  const uint32_t nit = (n + kFxThreads - 1) / kFxThreads;  // uniform
+  uint64_t kr[kFxItems];
+  uint32_t pk[kFxItems];
+#pragma unroll
+  for (int it = 0; it < kFxItems; ++it) {
+    const uint32_t i = it * kFxThreads + tid;
+    kr[it] = (it < (int)nit && i < n) ? ldg_stream(src + off + i) : 0;
+  }
+  __syncthreads();  // counters zeroed
+  uint32_t nq = 0;
+#pragma unroll
+  for (int it = 0; it < kFxItems; ++it) {
+    if (it < (int)nit) {
+      pk[it] = 0xFFFFFFFFu;
+      if (it * kFxThreads + tid < n) {
+        const uint32_t sb = __umulhi((uint32_t)((kr[it] - lo) >> sh), mk) - sub0;
+        const uint32_t rk = atomicAdd(&cnt[fx_sw(sb)], 1u);
+        pk[it] = (sb << 12) | rk;
+        nq += rk == 1;
+      }
+    }
+  }
+  __syncthreads();
+  // Scan: 32 counters per thread, plus the queue count and the largest sub-bucket.
+  uint32_t tw = 0, big = 0;
+#pragma unroll
+  for (int c = 0; c < kFxWords / 4; ++c) {
+    const uint4 v = cw4[c ^ rot];
+    tw += v.x + v.y + v.z + v.w;
+    big = max(big, max(max(v.x, v.y), max(v.z, v.w)));
+  }
+  const uint32_t mine = tw | (nq << 16);  // both prefixes < 2^16
+  const uint32_t inc = warp_incl_scan(mine);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) big = max(big, __shfl_xor_sync(0xffffffffu, big, o));
+  if (lane == 31) s_scan[wid] = inc;
+  if (lane == 0) s_big[wid] = big;
+  scan_warp_totals<kFxThreads>(s_scan);
+  const uint32_t pre = s_scan[wid] + inc - mine;
+  big = 0;
+#pragma unroll
+  for (int w = 0; w < kFxThreads / 32; ++w) big = max(big, s_big[w]);
+  if (big > (uint32_t)kRankMax) {  // clustered keys: LSD fallback
+    if (tid == 0) {
+      OverflowRec r; r.off = off; r.count = n; r.lo = 0; r.hi = 0; r.out = oo;
+      fb[atomicAdd(fb_count, 1u)] = r;
+    }
+    return;
+  }
+  uint32_t run = pre & 0xFFFFu;
+#pragma unroll
+  for (int c = 0; c < kFxWords / 4; ++c) {
+    uint4 w4 = cw4[c ^ rot];
+    uint32_t t;
+    t = w4.x; w4.x = run; run += t;
+    t = w4.y; w4.y = run; run += t;
+    t = w4.z; w4.z = run; run += t;
+    t = w4.w; w4.w = run; run += t;
+    cw4[c ^ rot] = w4;
+  }
+  uint32_t qpos = pre >> 16;
+  __syncthreads();
+#pragma unroll
+  for (int it = 0; it < kFxItems; ++it) {
+    if (it < (int)nit && pk[it] != 0xFFFFFFFFu) {
+      const uint32_t sb = pk[it] >> 12, rk = pk[it] & 0xFFFu;
+      kB[cnt[fx_sw(sb)] + rk] = kr[it];
+      if (rk == 1) q[qpos++] = (uint16_t)sb;
+    }
+  }
+  __syncthreads();
+  const uint32_t nqueue = s_scan[kFxThreads / 32] >> 16;
+  for (uint32_t i = tid; i < nqueue; i += kFxThreads) {
+    const uint32_t sb = q[i];
+    const uint32_t b0 = cnt[fx_sw(sb)];
+    const uint32_t b1 = sb + 1 < (uint32_t)kSubK ? cnt[fx_sw(sb + 1)] : n;
+    if (b1 - b0 <= 3) {
+      uint64_t k0 = kB[b0], k1 = kB[b0 + 1];
+      if (b1 - b0 == 3) {
+        uint64_t k2 = kB[b0 + 2];
+        if (k0 > k1) { const uint64_t t = k0; k0 = k1; k1 = t; }
+        if (k1 > k2) { const uint64_t t = k1; k1 = k2; k2 = t; }
+        if (k0 > k1) { const uint64_t t = k0; k0 = k1; k1 = t; }
+        kB[b0 + 2] = k2;
+      } else if (k0 > k1) {
+        const uint64_t t = k0; k0 = k1; k1 = t;
+      }
+      kB[b0] = k0;
+      kB[b0 + 1] = k1;
+    } else {
+      for (uint32_t a = b0 + 1; a < b1; ++a) {
+        const uint64_t ka = kB[a];
+        uint32_t e = a;
+        while (e > b0 && kB[e - 1] > ka) { kB[e] = kB[e - 1]; --e; }
+        kB[e] = ka;
+      }
+    }
+  }
+  __syncthreads();
+  const uint32_t a = (uint32_t)(oo & 1);
+  if (a && tid == 0) out[oo] = from_ordered<KIND_OUT>(kB[0]);
+  const uint32_t np = (n - a) >> 1;
+  uint4* o4 = reinterpret_cast<uint4*>(out + oo + a);
+  for (uint32_t j = tid; j < np; j += kFxThreads) {
+    const uint64_t k0 = from_ordered<KIND_OUT>(kB[a + 2 * j]);
+    const uint64_t k1 = from_ordered<KIND_OUT>(kB[a + 2 * j + 1]);
+    o4[j] = make_uint4((uint32_t)k0, (uint32_t)(k0 >> 32), (uint32_t)k1, (uint32_t)(k1 >> 32));
+  }
+  if (((n - a) & 1) && tid == 0) out[oo + n - 1] = from_ordered<KIND_OUT>(kB[n - 1]);
+}
+
 // One warp per segment: cells are loaded 32 at a time (coalesced) and the
 // greedy packing state is replicated in every lane through shuffles.
 __global__ void k_pack_cells(const uint32_t* __restrict__ cell_cnt,
@@ -1920,11 +2091,28 @@ size_t smem_sort_lsd_bytes() {
   return (size_t)kSortCap * (8 + 8 + 2 + 2) + (size_t)4 * kSortWarps * kRadix + 4 * kRadix;
 }
 
+#ifndef AMS_FX_SORT
+#define AMS_FX_SORT 1
+#endif
+
 cudaError_t launch_smem_sort(cudaStream_t st, const void* src, const void* src_vals, void* out,
                              void* out_vals, int kind_out, const CellSource& cs, uint64_t ncells,
                              OverflowRec* ovf, unsigned int* ovf_count, OverflowRec* fb,
                              unsigned int* fb_count) {
   if (ncells == 0) return cudaSuccess;
+  if (AMS_FX_SORT && cs.mode == 3 && !src_vals && (out != nullptr) &&
+      ((reinterpret_cast<uintptr_t>(out) & 15) == 0)) {
+    const size_t smem = (size_t)kSortCap * 8 + (size_t)kSubK * 4 + 2 * (size_t)kQueueCap;
+    cudaError_t e = cudaSuccess;
+    AMS_KIND_DISPATCH(kind_out, K, {
+      auto fn = k_cell_sort_fixed<K>;
+      e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      fn<<<(unsigned)ncells, kFxThreads, smem, st>>>(static_cast<const uint64_t*>(src),
+                                                     static_cast<uint64_t*>(out), cs, fb, fb_count);
+    });
+    return cudaGetLastError();
+  }
   const size_t smem = smem_sort_bytes(src_vals != nullptr);
   const uint64_t* s = static_cast<const uint64_t*>(src);
   const uint64_t* sv = static_cast<const uint64_t*>(src_vals);
