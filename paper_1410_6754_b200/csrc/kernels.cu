@@ -1609,14 +1609,29 @@ __global__ void __launch_bounds__(kSortThreads, kSortCtas)
 //   5. 16-byte stores to the output.
 // Cells without a refined digit (m * K >= 2^32) go to the LSD list; cells
 // of counting-only buckets (m == 0) are one key value: filled directly.
+#ifndef AMS_FX_U16
+#define AMS_FX_U16 1
+#endif
 constexpr int kFxThreads = 256;
 constexpr int kFxItems = kSortCap / kFxThreads;   // 16
-constexpr int kFxWords = kSubK / kFxThreads;      // 32 counters per scan thread
-static_assert(kFxWords == 32, "fixed-cell counter layout assumes 32 words per thread");
-__device__ __forceinline__ uint32_t fx_sw(uint32_t s) { return s ^ (((s >> 5) & 7u) << 2); }
+constexpr int kFxCtas = AMS_FX_U16 ? 4 : 3;
+// Counters: 32-bit words, or (AMS_FX_U16) pairs of 16-bit halves.
+constexpr int kFxWords = kSubK / kFxThreads / (AMS_FX_U16 ? 2 : 1);  // counter words per scan thread
+static_assert(kFxWords == 32 || kFxWords == 16, "fixed-cell counter layout");
+constexpr int kFxChunks = kFxWords / 4;
+__device__ __forceinline__ uint32_t fx_sw(uint32_t w) {
+  // word w belongs to scan thread w / kFxWords, whose chunk c sits at c ^ rot(thread)
+  return w ^ (((w >> 5) & (uint32_t)(kFxChunks - 1)) << 2);
+}
+
+// Start of sub-bucket s after the scan.
+__device__ __forceinline__ uint32_t fx_start(const uint32_t* cnt, const uint16_t* c16, uint32_t s) {
+  if constexpr (AMS_FX_U16) return c16[2 * fx_sw(s >> 1) + (s & 1)];
+  else return cnt[fx_sw(s)];
+}
 
 template <int KIND_OUT>
-__global__ void __launch_bounds__(kFxThreads, 3)
+__global__ void __launch_bounds__(kFxThreads, kFxCtas)
     k_cell_sort_fixed(const uint64_t* __restrict__ src, uint64_t* __restrict__ out, CellSource cs,
                       OverflowRec* __restrict__ fb, unsigned int* __restrict__ fb_count) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -1624,7 +1639,8 @@ __global__ void __launch_bounds__(kFxThreads, 3)
   __shared__ uint32_t s_big[kFxThreads / 32];
   uint64_t* kB = reinterpret_cast<uint64_t*>(smem);
   uint32_t* cnt = reinterpret_cast<uint32_t*>(kB + kSortCap);
-  uint16_t* q = reinterpret_cast<uint16_t*>(cnt + kSubK);
+  uint16_t* q = reinterpret_cast<uint16_t*>(cnt + kFxWords * kFxThreads);
+  const uint16_t* c16 = reinterpret_cast<const uint16_t*>(cnt);
   const uint32_t cid = blockIdx.x;
   const uint32_t n = cs.cell_cnt[cid];
   if (n == 0) return;
@@ -1648,7 +1664,7 @@ __global__ void __launch_bounds__(kFxThreads, 3)
   const uint64_t lo = d.lo;
   const uint32_t sh = d.sh, mk = (uint32_t)d.q, sub0 = digit * (uint32_t)kSubK;
   uint4* const cw4 = reinterpret_cast<uint4*>(cnt) + tid * (kFxWords / 4);
-  const uint32_t rot = tid & 7u;
+  const uint32_t rot = (kFxChunks == 8 ? tid : tid >> 1) & (uint32_t)(kFxChunks - 1);
 #pragma unroll
   for (int c = 0; c < kFxWords / 4; ++c) cw4[c ^ rot] = make_uint4(0, 0, 0, 0);
   const uint32_t nit = (n + kFxThreads - 1) / kFxThreads;  // uniform
@@ -1667,7 +1683,13 @@ __global__ void __launch_bounds__(kFxThreads, 3)
       pk[it] = 0xFFFFFFFFu;
       if (it * kFxThreads + tid < n) {
         const uint32_t sb = __umulhi((uint32_t)((kr[it] - lo) >> sh), mk) - sub0;
-        const uint32_t rk = atomicAdd(&cnt[fx_sw(sb)], 1u);
+        uint32_t rk;
+        if constexpr (AMS_FX_U16) {
+          const uint32_t hs = (sb & 1) * 16;
+          rk = (atomicAdd(&cnt[fx_sw(sb >> 1)], 1u << hs) >> hs) & 0xFFFFu;
+        } else {
+          rk = atomicAdd(&cnt[fx_sw(sb)], 1u);
+        }
         pk[it] = (sb << 12) | rk;
         nq += rk == 1;
       }
@@ -1681,6 +1703,12 @@ __global__ void __launch_bounds__(kFxThreads, 3)
     const uint4 v = cw4[c ^ rot];
     tw += v.x + v.y + v.z + v.w;
     big = max(big, max(max(v.x, v.y), max(v.z, v.w)));
+    if constexpr (AMS_FX_U16)
+      big = max(big, max(max(v.x << 16, v.y << 16), max(v.z << 16, v.w << 16)));
+  }
+  if constexpr (AMS_FX_U16) {
+    big >>= 16;
+    tw = (tw & 0xFFFFu) + (tw >> 16);  // halves cannot carry: total <= n
   }
   const uint32_t mine = tw | (nq << 16);  // both prefixes < 2^16
   const uint32_t inc = warp_incl_scan(mine);
@@ -1704,12 +1732,19 @@ __global__ void __launch_bounds__(kFxThreads, 3)
 #pragma unroll
   for (int c = 0; c < kFxWords / 4; ++c) {
     uint4 w4 = cw4[c ^ rot];
-    uint32_t t;
-    t = w4.x; w4.x = run; run += t;
-    t = w4.y; w4.y = run; run += t;
-    t = w4.z; w4.z = run; run += t;
-    t = w4.w; w4.w = run; run += t;
-    cw4[c ^ rot] = w4;
+    uint32_t wv[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+    for (int qq = 0; qq < 4; ++qq) {
+      const uint32_t t = wv[qq];
+      if constexpr (AMS_FX_U16) {  // (start of low half, start of high half)
+        wv[qq] = run | ((run + (t & 0xFFFFu)) << 16);
+        run += (t & 0xFFFFu) + (t >> 16);
+      } else {
+        wv[qq] = run;
+        run += t;
+      }
+    }
+    cw4[c ^ rot] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
   }
   uint32_t qpos = pre >> 16;
   __syncthreads();
@@ -1717,7 +1752,7 @@ __global__ void __launch_bounds__(kFxThreads, 3)
   for (int it = 0; it < kFxItems; ++it) {
     if (it < (int)nit && pk[it] != 0xFFFFFFFFu) {
       const uint32_t sb = pk[it] >> 12, rk = pk[it] & 0xFFFu;
-      kB[cnt[fx_sw(sb)] + rk] = kr[it];
+      kB[fx_start(cnt, c16, sb) + rk] = kr[it];
       if (rk == 1) q[qpos++] = (uint16_t)sb;
     }
   }
@@ -1725,8 +1760,8 @@ __global__ void __launch_bounds__(kFxThreads, 3)
   const uint32_t nqueue = s_scan[kFxThreads / 32] >> 16;
   for (uint32_t i = tid; i < nqueue; i += kFxThreads) {
     const uint32_t sb = q[i];
-    const uint32_t b0 = cnt[fx_sw(sb)];
-    const uint32_t b1 = sb + 1 < (uint32_t)kSubK ? cnt[fx_sw(sb + 1)] : n;
+    const uint32_t b0 = fx_start(cnt, c16, sb);
+    const uint32_t b1 = sb + 1 < (uint32_t)kSubK ? fx_start(cnt, c16, sb + 1) : n;
     if (b1 - b0 <= 3) {
       uint64_t k0 = kB[b0], k1 = kB[b0 + 1];
       if (b1 - b0 == 3) {
@@ -2102,7 +2137,7 @@ cudaError_t launch_smem_sort(cudaStream_t st, const void* src, const void* src_v
   if (ncells == 0) return cudaSuccess;
   if (AMS_FX_SORT && cs.mode == 3 && !src_vals && (out != nullptr) &&
       ((reinterpret_cast<uintptr_t>(out) & 15) == 0)) {
-    const size_t smem = (size_t)kSortCap * 8 + (size_t)kSubK * 4 + 2 * (size_t)kQueueCap;
+    const size_t smem = (size_t)kSortCap * 8 + (size_t)kFxWords * kFxThreads * 4 + 2 * (size_t)kQueueCap;
     cudaError_t e = cudaSuccess;
     AMS_KIND_DISPATCH(kind_out, K, {
       auto fn = k_cell_sort_fixed<K>;
