@@ -1654,14 +1654,25 @@ __global__ void __launch_bounds__(kFxThreads, kFxCtas)
     for (uint32_t i = tid; i < n; i += kFxThreads) out[oo + i] = ko;
     return;
   }
+  // No refined digit (m * K >= 2^32, dense keys): then sh == 0 and the cell
+  // is the keys with key - lo in [ceil(digit 2^32 / m), ceil((digit+1) 2^32 / m)),
+  // at most K values wide — one sub-bucket per key value (exact: no fix-ups).
+  bool exact = false;
+  uint64_t lo = d.lo;
   if (d.q == 0) {
-    if (tid == 0) {
-      OverflowRec r; r.off = off; r.count = n; r.lo = 0; r.hi = 0; r.out = oo;
-      fb[atomicAdd(fb_count, 1u)] = r;
+    const uint64_t m = d.m32;
+    const uint64_t x0 = (((uint64_t)digit << 32) + m - 1) / m;
+    const uint64_t x1 = (((uint64_t)(digit + 1) << 32) + m - 1) / m;
+    if (d.sh != 0 || x1 - x0 > (uint64_t)kSubK) {
+      if (tid == 0) {
+        OverflowRec r; r.off = off; r.count = n; r.lo = 0; r.hi = 0; r.out = oo;
+        fb[atomicAdd(fb_count, 1u)] = r;
+      }
+      return;
     }
-    return;
+    exact = true;
+    lo += x0;
   }
-  const uint64_t lo = d.lo;
   const uint32_t sh = d.sh, mk = (uint32_t)d.q, sub0 = digit * (uint32_t)kSubK;
   uint4* const cw4 = reinterpret_cast<uint4*>(cnt) + tid * (kFxWords / 4);
   const uint32_t rot = (kFxChunks == 8 ? tid : tid >> 1) & (uint32_t)(kFxChunks - 1);
@@ -1682,7 +1693,7 @@ __global__ void __launch_bounds__(kFxThreads, kFxCtas)
     if (it < (int)nit) {
       pk[it] = 0xFFFFFFFFu;
       if (it * kFxThreads + tid < n) {
-        const uint32_t sb = __umulhi((uint32_t)((kr[it] - lo) >> sh), mk) - sub0;
+        const uint32_t sb = exact ? (uint32_t)(kr[it] - lo) : __umulhi((uint32_t)((kr[it] - lo) >> sh), mk) - sub0;
         uint32_t rk;
         if constexpr (AMS_FX_U16) {
           const uint32_t hs = (sb & 1) * 16;
@@ -1721,7 +1732,7 @@ __global__ void __launch_bounds__(kFxThreads, kFxCtas)
   big = 0;
 #pragma unroll
   for (int w = 0; w < kFxThreads / 32; ++w) big = max(big, s_big[w]);
-  if (big > (uint32_t)kRankMax) {  // clustered keys: LSD fallback
+  if (!exact && big > (uint32_t)kRankMax) {  // clustered keys: LSD fallback
     if (tid == 0) {
       OverflowRec r; r.off = off; r.count = n; r.lo = 0; r.hi = 0; r.out = oo;
       fb[atomicAdd(fb_count, 1u)] = r;
@@ -1757,7 +1768,7 @@ __global__ void __launch_bounds__(kFxThreads, kFxCtas)
     }
   }
   __syncthreads();
-  const uint32_t nqueue = s_scan[kFxThreads / 32] >> 16;
+  const uint32_t nqueue = exact ? 0 : s_scan[kFxThreads / 32] >> 16;  // exact: one value per sub-bucket
   for (uint32_t i = tid; i < nqueue; i += kFxThreads) {
     const uint32_t sb = q[i];
     const uint32_t b0 = fx_start(cnt, c16, sb);

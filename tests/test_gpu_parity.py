@@ -262,6 +262,9 @@ def test_oracle_parity_keys_only(api, groups, b, npe, dist, with_stats):
         assert after["fixed_buckets"] > before["fixed_buckets"]  # the fixed-capacity path ran
     if dist == "clustered":  # and its exact fallback
         assert after["fixed_overflow_buckets"] > before["fixed_overflow_buckets"]
+    if dist in ("uniform", "sorted", "reverse", "narrow", "equal"):
+        # these never need the LSD fallback (dense ranges take the exact cell map)
+        assert after["fallback_cells"] == before["fallback_cells"]
     assert np.array_equal(host_u64(res.keys), ref.keys)
     assert [int(x) for x in res.pe_sizes] == list(ref.pe_sizes)
     for rec, infos in zip(res.levels, ref.levels):
