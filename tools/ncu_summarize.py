@@ -26,6 +26,7 @@ CATS = [
     ("k_scatter_u<0, 1>", "final_scatter"),
     ("k_scatter<0, 1, 0, 2>", "final_scatter"),
     ("k_smem_sort<0, 0", "smem_sort"),
+    ("k_cell_sort_fixed<0>", "smem_sort"),
     ("k_bucket_sort", "smem_sort"),
 ]
 ALG = {"smem_sort": 16, "level_scatter": 16, "level_scatter_unstable": 16, "final_scatter": 16,
