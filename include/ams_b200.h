@@ -194,6 +194,14 @@ int ams_level_classify(ams_ctx_t* ctx, const void* src, int key_kind, int nseg,
 int ams_level_scatter(ams_ctx_t* ctx, const void* src, const void* src_vals, int key_kind,
                       void* dst, void* dst_vals, int r, const uint64_t* h_boundaries,
                       const uint64_t* h_group_dst_start, int child_first, int child_count);
+/* As ams_level_scatter; flags AMS_SCATTER_BUCKET_MAJOR (keys-only last
+ * level, where only PE membership matters: ams.py:310-312) lays
+ * every group out bucket by bucket, for ams_final_sort_buckets. */
+#define AMS_SCATTER_BUCKET_MAJOR 1
+int ams_level_scatter_ex(ams_ctx_t* ctx, const void* src, const void* src_vals, int key_kind,
+                         void* dst, void* dst_vals, int r, const uint64_t* h_boundaries,
+                         const uint64_t* h_group_dst_start, int child_first, int child_count,
+                         int flags);
 
 /* Global min/max key seen by a track_minmax classify (ordered encoding);
  * the multi-rank driver all-reduces them and writes them back before the
@@ -209,6 +217,14 @@ int ams_set_minmax(ams_ctx_t* ctx, const uint64_t in[2]);
 int ams_final_sort(ams_ctx_t* ctx, void* src, void* src_vals, void* tmp, void* tmp_vals,
                    void* out, void* out_vals, int key_kind, int nseg, const uint64_t* h_seg_off,
                    const uint64_t* h_seg_len);
+/* Final local sort (keys only) after a bucket-major last level: nbk buckets
+ * in output order, bucket i = bk_len[i] keys at bk_off[i], bucket bk_bucket[i]
+ * of the last level's group bk_group[i].  Buckets above shared memory are
+ * split into fixed-capacity digit cells in one pass (no histogram); cells
+ * are sorted in shared memory; overflowing buckets take exact rounds. */
+int ams_final_sort_buckets(ams_ctx_t* ctx, void* src, void* tmp, void* out, int key_kind, int nbk,
+                           const uint64_t* bk_off, const uint64_t* bk_len, const int32_t* bk_group,
+                           const int32_t* bk_bucket);
 
 /* Cells of the final sort that needed another partition round / the LSD
  * fallback, summed since the context was created: out = {overflow, fallback}. */

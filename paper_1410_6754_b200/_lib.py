@@ -60,6 +60,8 @@ _SIGNATURES = {
     "ams_level_scatter": (_I, [_P, _P, _P, _I, _P, _P, _I, _P, _P, _I, _I]),
     "ams_final_sort_stats": (_I, [_P, _P]),
     "ams_final_sort_fixed_stats": (_I, [_P, _P]),
+    "ams_level_scatter_ex": (_I, [_P, _P, _P, _I, _P, _P, _I, _P, _P, _I, _I, _I]),
+    "ams_final_sort_buckets": (_I, [_P, _P, _P, _P, _I, _I, _P, _P, _P, _P]),
     "ams_get_minmax": (_I, [_P, _P]),
     "ams_set_minmax": (_I, [_P, _P]),
     "ams_final_sort": (_I, [_P, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P]),
@@ -91,6 +93,7 @@ class LevelReportT(C.Structure):
                                   "max_recv_msgs")]
 
 EXPORTED = tuple(_SIGNATURES)
+BUCKET_MAJOR = 1  # AMS_SCATTER_BUCKET_MAJOR
 
 
 def _load():
@@ -361,13 +364,18 @@ class Context:
         return out
 
     def level_scatter(self, src, src_vals, kind, dst, dst_vals, r, boundaries, group_dst_start,
-                      child_first=0, child_count=None):
+                      child_first=0, child_count=None, bucket_major=False):
         b, d = u64(boundaries), u64(group_dst_start)
         if child_count is None:
             child_count = len(d) * r
-        check(lib.ams_level_scatter(self.h, ptr(src), ptr(src_vals), kind, ptr(dst), ptr(dst_vals),
-                                    r, b.ctypes.data, d.ctypes.data, int(child_first),
-                                    int(child_count)))
+        check(lib.ams_level_scatter_ex(self.h, ptr(src), ptr(src_vals), kind, ptr(dst), ptr(dst_vals),
+                                       r, b.ctypes.data, d.ctypes.data, int(child_first),
+                                       int(child_count), BUCKET_MAJOR if bucket_major else 0))
+
+    def final_sort_buckets(self, src, tmp, out, key_kind, bk_off, bk_len, bk_group, bk_bucket):
+        bo, bl, bg, bb = u64(bk_off), u64(bk_len), i32(bk_group), i32(bk_bucket)
+        check(lib.ams_final_sort_buckets(self.h, ptr(src), ptr(tmp), ptr(out), key_kind, len(bo),
+                                         bo.ctypes.data, bl.ctypes.data, bg.ctypes.data, bb.ctypes.data))
 
     def final_sort_stats(self):
         out = np.zeros(2, np.uint64)

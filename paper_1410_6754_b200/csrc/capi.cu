@@ -1111,6 +1111,29 @@ int ams_final_sort(ams_ctx_t* c, void* src, void* src_vals, void* tmp, void* tmp
   return AMS_OK;
 }
 
+int ams_level_scatter_ex(ams_ctx_t* c, const void* src, const void* src_vals, int key_kind,
+                         void* dst, void* dst_vals, int r, const uint64_t* h_boundaries,
+                         const uint64_t* h_group_dst_start, int child_first, int child_count,
+                         int flags) {
+  return level_scatter_impl(c, src, src_vals, key_kind, dst, dst_vals, r, h_boundaries,
+                            h_group_dst_start, child_first, child_count,
+                            (flags & AMS_SCATTER_BUCKET_MAJOR) != 0);
+}
+
+int ams_final_sort_buckets(ams_ctx_t* c, void* src, void* tmp, void* out, int key_kind, int nbk,
+                           const uint64_t* bk_off, const uint64_t* bk_len, const int32_t* bk_group,
+                           const int32_t* bk_bucket) {
+  if (!c) return set_error(AMS_EINVAL, "null context");
+  if (nbk < 0 || (nbk > 0 && (!bk_off || !bk_len || !bk_group || !bk_bucket)))
+    return set_error(AMS_EINVAL, "bad bucket list");
+  if (nbk > 0 && c->bounds[1 - c->bcur].cap == 0)
+    return set_error(AMS_EINVAL, "no key bounds of the last level's groups");
+  AMS_CK(cudaSetDevice(c->device));
+  std::vector<uint64_t> bo(bk_off, bk_off + nbk), bl(bk_len, bk_len + nbk);
+  std::vector<int32_t> bg(bk_group, bk_group + nbk), bb(bk_bucket, bk_bucket + nbk);
+  return final_sort_bm(c, src, tmp, out, key_kind, bo, bl, bg, bb, c->bounds[1 - c->bcur].as<uint64_t>());
+}
+
 int ams_final_sort_fixed_stats(ams_ctx_t* c, uint64_t out[2]) {
   if (!c || !out) return set_error(AMS_EINVAL, "null argument");
   out[0] = c->fixed_segments;

@@ -34,7 +34,7 @@ import torch
 import torch.distributed as dist
 
 from . import _lib as L
-from .engine import LevelRecord, load_budget, level_targets, key_kind_of
+from .engine import LevelRecord, bucket_table, load_budget, level_targets, key_kind_of
 from .params import as_params, as_seed
 
 
@@ -70,12 +70,16 @@ class CudaOps:
     def set_minmax(self, lo, hi):
         self.ctx.set_minmax(lo, hi)
 
-    def scatter(self, src, src_v, kind, dst, dst_v, r, bnd, dst_start, child_first, child_count):
+    def scatter(self, src, src_v, kind, dst, dst_v, r, bnd, dst_start, child_first, child_count,
+                bucket_major=False):
         self.ctx.level_scatter(src, src_v, kind, dst, dst_v, r, bnd, dst_start, child_first,
-                               child_count)
+                               child_count, bucket_major=bucket_major)
 
     def final_sort(self, src, src_v, tmp, tmp_v, out, out_v, kind, offs, sizes):
         self.ctx.final_sort(src, src_v, tmp, tmp_v, out, out_v, kind, offs, sizes)
+
+    def final_sort_buckets(self, src, tmp, out, kind, bk_off, bk_len, bk_group, bk_bucket):
+        self.ctx.final_sort_buckets(src, tmp, out, kind, bk_off, bk_len, bk_group, bk_bucket)
 
 
 def _u64_to_i64(x: int) -> int:
@@ -238,6 +242,7 @@ def sort_distributed(keys: torch.Tensor, pe_sizes_local, params, seed, ops, vals
     gf = (pe_lo + np.arange(gpr, dtype=np.int64) * step).astype(np.int32)
     gn = np.full(gpr, step, np.int32)
     buf = 1
+    final_buckets = None
     for lv in range(1, len(params.group_counts)):
         r = params.group_counts[lv]
         offs = np.zeros(p + 1, np.uint64)          # positions in the local buffer
@@ -264,7 +269,12 @@ def sort_distributed(keys: torch.Tensor, pe_sizes_local, params, seed, ops, vals
                             False, not (last_level and vals is None))
         bnd, loads, mx, new_local, stats = L.plan_level(gn, nb, r, hist)
         dst, dst_v = work[buf], work_v[buf]
-        ops.scatter(src, src_v, src_kind, dst, dst_v, r, bnd, offs[gf], 0, G * r)
+        # Keys-only last level: bucket-major groups for the fixed-capacity final sort.
+        bucket_major = last_level and vals is None
+        ops.scatter(src, src_v, src_kind, dst, dst_v, r, bnd, offs[gf], 0, G * r,
+                    bucket_major=bucket_major)
+        if bucket_major:
+            final_buckets = bucket_table(hist, gf - pe_lo, gn, nb, offs[gf])
         rec = LevelRecord(lv, r, gf.copy(), gn.copy(), sizes[loc].copy(), drawn, nb, hist, bnd,
                           loads, mx, load_budget(n_g, r, eps_l), new_local, stats)
         levels.append(rec)
@@ -285,5 +295,8 @@ def sort_distributed(keys: torch.Tensor, pe_sizes_local, params, seed, ops, vals
     offs = np.zeros(pl + 1, np.uint64)
     np.cumsum(local_final, out=offs[1:])
     tmp, tmp_v = work[buf], work_v[buf]
-    ops.final_sort(src, src_v, tmp, tmp_v, out, out_vals, kind, offs[:-1], local_final)
+    if final_buckets is not None:
+        ops.final_sort_buckets(src, tmp, out, kind, *final_buckets)
+    else:
+        ops.final_sort(src, src_v, tmp, tmp_v, out, out_vals, kind, offs[:-1], local_final)
     return out[:n_out], (out_vals[:n_out] if out_vals is not None else None), local_final, levels

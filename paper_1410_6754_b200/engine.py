@@ -94,6 +94,23 @@ class SortOutput:
         return [lv.report() for lv in self.levels]
 
 
+def bucket_table(seg_hist: np.ndarray, group_first, group_npe, nb, group_start):
+    """Buckets of a bucket-major (keys-only) last level in output order:
+    (offset, length, group, bucket) arrays for ams_final_sort_buckets.  Group
+    g starts at group_start[g]; its bucket b holds the sum over the group's
+    members of seg_hist[member][b]."""
+    off, ln, grp, bkt = [], [], [], []
+    for g, (f, c) in enumerate(zip(group_first, group_npe)):
+        tot = seg_hist[int(f):int(f) + int(c), :int(nb[g])].astype(np.uint64).sum(axis=0)
+        starts = int(group_start[g]) + np.concatenate([[0], np.cumsum(tot)[:-1]]).astype(np.uint64)
+        off.append(starts)
+        ln.append(tot)
+        grp.append(np.full(len(tot), g, np.int32))
+        bkt.append(np.arange(len(tot), dtype=np.int32))
+    cat = lambda xs, dt: np.concatenate(xs).astype(dt) if xs else np.zeros(0, dt)
+    return cat(off, np.uint64), cat(ln, np.uint64), cat(grp, np.int32), cat(bkt, np.int32)
+
+
 def level_targets(n_g: np.ndarray, r: int, b: int, a: float):
     """br and sample target per group (ams.py:224-225)."""
     br = np.minimum(b * r, n_g + 1).astype(np.int64)
@@ -218,7 +235,12 @@ class AmsSorter:
                                            stable=not (last_level and vals is None))
             bnd, loads, mx, new_sizes, stats = L.plan_level(gn, nb, r, hist, with_stats)
             dst, dst_v = work[lv % 2], work_v[lv % 2]
-            self.ctx.level_scatter(src, src_v, src_kind, dst, dst_v, r, bnd, offs[gf])
+            # Keys-only last level: bucket-major groups for the fixed-capacity final sort.
+            bucket_major = last_level and vals is None
+            self.ctx.level_scatter(src, src_v, src_kind, dst, dst_v, r, bnd, offs[gf],
+                                   bucket_major=bucket_major)
+            if bucket_major:
+                final_buckets = bucket_table(hist, gf, gn, nb, offs[gf])
             rec = LevelRecord(lv, r, gf.copy(), gn.copy(), sizes.copy(), drawn, nb, hist, bnd,
                               loads, mx, load_budget(n_g, r, eps_l), new_sizes, stats)
             if record_splitters:
@@ -236,7 +258,10 @@ class AmsSorter:
         offs = np.zeros(p + 1, np.uint64)
         np.cumsum(sizes, out=offs[1:])
         tmp, tmp_v = work[k % 2], work_v[k % 2]
-        self.ctx.final_sort(src, src_v, tmp, tmp_v, out, out_vals, kind, offs[:-1], sizes)
+        if vals is None:
+            self.ctx.final_sort_buckets(src, tmp, out, kind, *final_buckets)
+        else:
+            self.ctx.final_sort(src, src_v, tmp, tmp_v, out, out_vals, kind, offs[:-1], sizes)
         return SortOutput(ret_out, ret_vals, sizes, levels, self.ctx.launches - launches0)
 
     def _sort_native(self, keys, vals, ret_out, ret_vals, out, out_vals, sizes, params, master,

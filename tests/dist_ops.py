@@ -86,7 +86,8 @@ class NumpyOps:
     def set_minmax(self, lo, hi):
         self.mm = (lo, hi)
 
-    def scatter(self, src, src_v, kind, dst, dst_v, r, bnd, dst_start, child_first, child_count):
+    def scatter(self, src, src_v, kind, dst, dst_v, r, bnd, dst_start, child_first, child_count,
+                bucket_major=False):
         d = _u(dst)
         vs = src_v.numpy() if src_v is not None else None
         groups = sorted({g for _, _, g, _, _ in self.lvl})
@@ -96,12 +97,22 @@ class NumpyOps:
             bk = np.concatenate([t[4] for t in segs]) if segs else np.zeros(0, np.int64)
             j = np.concatenate([np.full(t[1], i) for i, t in enumerate(segs)]) if segs else bk
             gid = np.searchsorted(np.asarray(bnd[g], np.int64), bk, side="right") - 1
-            order = np.argsort((gid * len(segs) + j) * (1 << 20) + bk, kind="stable")
+            if bucket_major:  # (bucket, source) order: buckets contiguous (keys-only last level)
+                order = np.argsort(bk * len(segs) + j, kind="stable")
+            else:
+                order = np.argsort((gid * len(segs) + j) * (1 << 20) + bk, kind="stable")
             st = int(dst_start[g])
             d[st:st + len(keys)] = keys[order]
             if vs is not None:
                 v = np.concatenate([vs[t[0]:t[0] + t[1]] for t in segs])
                 dst_v.numpy()[st:st + len(keys)] = v[order]
+
+    def final_sort_buckets(self, src, tmp, out, kind, bk_off, bk_len, bk_group, bk_bucket):
+        x = _u(src)
+        o_ = _u(out)
+        for o, n in zip(bk_off, bk_len):
+            o, n = int(o), int(n)
+            o_[o:o + n] = _from_ordered(np.sort(x[o:o + n]), kind)
 
     def final_sort(self, src, src_v, tmp, tmp_v, out, out_v, kind, offs, sizes):
         x = _u(src)

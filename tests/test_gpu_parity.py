@@ -221,8 +221,9 @@ def test_oracle_parity_deterministic(api, groups, npe, dist, with_vals, scheme):
     ((16,), 16, 1 << 16, "uniform"), ((4,), 4, 1 << 18, "f64"), ((2, 2), 4, 1 << 19, "narrow"),
     ((4,), 4, 1 << 18, "clustered"), ((8, 8), 16, 1 << 12, "uniform"),
 ])
-@pytest.mark.parametrize("with_stats", [True, False], ids=["stats", "nostats"])
-def test_oracle_parity_keys_only(api, groups, b, npe, dist, with_stats):
+@pytest.mark.parametrize("with_stats,record", [(True, False), (False, False), (True, True)],
+                         ids=["stats", "nostats", "py_levels"])
+def test_oracle_parity_keys_only(api, groups, b, npe, dist, with_stats, record):
     """Keys-only sorts take the bucket-major last level and the
     fixed-capacity final partition (buckets above shared memory; counting-
     only cells for few-valued buckets, exact rounds for overflowed buckets):
@@ -255,7 +256,8 @@ def test_oracle_parity_keys_only(api, groups, b, npe, dist, with_stats):
     ctx = api.get_sorter(0).ctx
     before = ctx.final_sort_stats()
     res = api.get_sorter(0).sort(dev_u64(keys), sizes, AmsParams(tuple(groups), None, b, 0.1),
-                                 SeedSpec(79, "algo/rep0"), key_kind="u64", with_stats=with_stats)
+                                 SeedSpec(79, "algo/rep0"), key_kind="u64", with_stats=with_stats,
+                                 record_splitters=record)
     torch.cuda.synchronize()
     after = ctx.final_sort_stats()
     if npe * p // (int(np.prod(groups)) * b) > 2 * 4096:  # buckets well above shared memory
@@ -361,19 +363,22 @@ def test_distributed_path_world1_nccl():
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("nccl", rank=0, world_size=1)
     try:
-        groups, npe = (8, 8), 5000
-        p = 64
-        n = p * npe
-        keys = np.random.default_rng(3).integers(0, 2**64, n, dtype=np.uint64)
-        vals = np.arange(n, dtype=np.int64)
-        ref = O.ams_sort(keys, [npe] * p, groups, None, 16, 0.1, 9, "algo/rep0", vals=vals)
-        out, ov, sizes, levels = sort_distributed(
-            dev_u64(keys), [npe] * p, AmsParams(groups, None, 16, 0.1), SeedSpec(9, "algo/rep0"),
-            CudaOps(get_sorter(0)), vals=torch.from_numpy(vals).cuda(), key_kind="u64")
-        torch.cuda.synchronize()
-        assert np.array_equal(host_u64(out), ref.keys)
-        assert np.array_equal(ov.cpu().numpy(), ref.vals)
-        assert [int(x) for x in sizes] == list(ref.pe_sizes)
+        for groups, npe, b, with_vals in (((8, 8), 5000, 16, True), ((2, 4), 1 << 17, 4, False)):
+            p = int(np.prod(groups))
+            n = p * npe
+            keys = np.random.default_rng(3).integers(0, 2**64, n, dtype=np.uint64)
+            vals = np.arange(n, dtype=np.int64)
+            ref = O.ams_sort(keys, [npe] * p, groups, None, b, 0.1, 9, "algo/rep0", vals=vals)
+            # keys only: the last level goes bucket-major into the fixed-capacity final sort
+            out, ov, sizes, levels = sort_distributed(
+                dev_u64(keys), [npe] * p, AmsParams(groups, None, b, 0.1), SeedSpec(9, "algo/rep0"),
+                CudaOps(get_sorter(0)), vals=torch.from_numpy(vals).cuda() if with_vals else None,
+                key_kind="u64")
+            torch.cuda.synchronize()
+            assert np.array_equal(host_u64(out), ref.keys)
+            if with_vals:
+                assert np.array_equal(ov.cpu().numpy(), ref.vals)
+            assert [int(x) for x in sizes] == list(ref.pe_sizes)
     finally:
         dist.destroy_process_group()
 
