@@ -1808,44 +1808,6 @@ __global__ void __launch_bounds__(kFxThreads, kFxCtas)
   if (((n - a) & 1) && tid == 0) out[oo + n - 1] = from_ordered<KIND_OUT>(kB[n - 1]);
 }
 
-// One warp per segment: cells are loaded 32 at a time (coalesced) and the
-// greedy packing state is replicated in every lane through shuffles.
-__global__ void k_pack_cells(const uint32_t* __restrict__ cell_cnt,
-                             const uint64_t* __restrict__ cell_base, int nseg, int nb, uint32_t cap,
-                             OverflowRec* __restrict__ groups, unsigned int* __restrict__ ngroups) {
-  const int s = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (s >= nseg) return;
-  const uint32_t* cnt = cell_cnt + (size_t)s * nb;
-  const uint64_t* base = cell_base + (size_t)s * nb;
-  uint64_t g_off = 0, g_cnt = 0;
-  for (int d0 = 0; d0 < nb; d0 += 32) {
-    const bool ok = d0 + lane < nb;
-    const uint32_t c_l = ok ? cnt[d0 + lane] : 0;
-    const uint64_t b_l = ok ? base[d0 + lane] : 0;
-    for (int i = 0; i < 32; ++i) {
-      const uint32_t c = __shfl_sync(0xffffffffu, c_l, i);
-      const uint64_t bo = __shfl_sync(0xffffffffu, b_l, i);
-      if (c == 0) continue;
-      if (g_cnt + c > cap && g_cnt) {
-        if (lane == 0) {
-          const unsigned int slot = atomicAdd(ngroups, 1u);
-          OverflowRec r; r.off = g_off; r.count = g_cnt; r.lo = 0; r.hi = 0; r.out = g_off;
-          groups[slot] = r;
-        }
-        g_cnt = 0;
-      }
-      if (g_cnt == 0) g_off = bo;
-      g_cnt += c;
-    }
-  }
-  if (g_cnt && lane == 0) {
-    const unsigned int slot = atomicAdd(ngroups, 1u);
-    OverflowRec r; r.off = g_off; r.count = g_cnt; r.lo = 0; r.hi = 0; r.out = g_off;
-    groups[slot] = r;
-  }
-}
-
 template <int FROM, int TO>
 __global__ void k_map_keys(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst, uint64_t n) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -2205,53 +2167,6 @@ cudaError_t launch_smem_sort_lsd(cudaStream_t st, const void* src, const void* s
     AMS_KIND_DISPATCH(kind_out, K, AMS_SORT_GO(K, false))
   }
 #undef AMS_SORT_GO
-  return cudaGetLastError();
-}
-
-cudaError_t launch_pack_cells(cudaStream_t st, const uint32_t* cell_cnt, const uint64_t* cell_base,
-                              int nseg, int nb, uint32_t cap, OverflowRec* groups,
-                              unsigned int* ngroups) {
-  if (nseg == 0) return cudaSuccess;
-  k_pack_cells<<<(nseg + 3) / 4, 128, 0, st>>>(cell_cnt, cell_base, nseg, nb, cap, groups, ngroups);
-  return cudaGetLastError();
-}
-
-size_t scatter_fixed_smem_bytes(int nb) {
-  const int per = (nb + kThreadsU - 1) / kThreadsU | 1;
-  const size_t nbp = (size_t)per * kThreadsU;
-  return 2 * 8 * (size_t)(kTile + 2) + 16 * nbp + 2 * (size_t)kTile;
-}
-
-cudaError_t launch_scatter_fixed(cudaStream_t st, const void* src, int kind, void* dst,
-                                 const SegMeta& m, uint64_t nchunks, int max_nb,
-                                 const DigitCls* dcls, const uint32_t* cell0, uint32_t* fill,
-                                 uint32_t* seg_ovf) {
-  if (nchunks == 0) return cudaSuccess;
-  const size_t smem = scatter_fixed_smem_bytes(max_nb);
-  const uint64_t* s = static_cast<const uint64_t*>(src);
-  uint64_t* d = static_cast<uint64_t*>(dst);
-  cudaError_t e = cudaSuccess;
-  (void)kind;  // the last level's output holds order-mapped u64 keys
-  auto fn = k_scatter_fixed<AMS_KEY_U64>;
-  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  fn<<<(unsigned)nchunks, kThreadsU, smem, st>>>(s, d, m, dcls, cell0, fill, seg_ovf);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_fixed_cells(cudaStream_t st, const uint32_t* fill, const uint32_t* cell0,
-                               const uint64_t* seg_off, const uint32_t* seg_ovf, int nseg,
-                               uint64_t* out_base, uint32_t* cnt, uint32_t* cell_seg) {
-  if (nseg == 0) return cudaSuccess;
-  k_fixed_cells<<<(nseg + 7) / 8, 256, 0, st>>>(fill, cell0, seg_off, seg_ovf, nseg, out_base, cnt,
-                                                 cell_seg);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_bucket_ranges(cudaStream_t st, const uint8_t* blobs, const uint64_t* gbounds,
-                                 const int32_t* seg_gb, int nseg, DigitCls* out) {
-  if (nseg == 0) return cudaSuccess;
-  k_bucket_ranges<<<(nseg + 127) / 128, 128, 0, st>>>(blobs, gbounds, seg_gb, nseg, out);
   return cudaGetLastError();
 }
 

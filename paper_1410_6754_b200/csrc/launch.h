@@ -108,12 +108,6 @@ cudaError_t launch_smem_sort(cudaStream_t st, const void* src, const void* src_v
 cudaError_t launch_smem_sort_lsd(cudaStream_t st, const void* src, const void* src_vals, void* out,
                                  void* out_vals, int kind_out, const CellSource& cs,
                                  uint64_t ncells);
-// Greedy packing of consecutive digit cells of each segment into groups of
-// at most `cap` keys (sorting a group = sorting its cells: they are
-// ordered); cells above cap become singleton groups.
-cudaError_t launch_pack_cells(cudaStream_t st, const uint32_t* cell_cnt, const uint64_t* cell_base,
-                              int nseg, int nb, uint32_t cap, OverflowRec* groups,
-                              unsigned int* ngroups);
 // Fixed-capacity digit partition of bucket segments (keys only): cells of
 // AMS_SMEM_SORT_CAP slots in dst, fill counts in `fill`, overflow flags per
 // segment in seg_ovf (see k_scatter_fixed).
