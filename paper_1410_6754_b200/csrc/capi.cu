@@ -173,7 +173,7 @@ struct ams_ctx {
   int bcur = 0;
   HostBuf h_hist;
   // final sort
-  DevBuf dcls, ovf, ovf_count, fb, fb_count, groups, ngroups_d;
+  DevBuf dcls, ovf, ovf_count, fb, fb_count;
   // bucket-major final sort (fixed-capacity cells)
   DevBuf fx_scratch, fx_fill, fx_ovf, fx_base, fx_cnt, fx_seg;
   Stage st_fixed;
@@ -366,7 +366,7 @@ int ams_ctx_destroy(ams_ctx_t* c) {
     s->release();
   for (DevBuf* b : {&c->blobs, &c->sorted_keys, &c->sorted_pos, &c->sample_idx, &c->bounds[0], &c->bounds[1],
                     &c->chunk_tot, &c->seg_hist, &c->cell_base, &c->pieces, &c->minmax, &c->dcls,
-                    &c->ovf, &c->ovf_count, &c->fb, &c->fb_count, &c->groups, &c->ngroups_d,
+                    &c->ovf, &c->ovf_count, &c->fb, &c->fb_count,
                     &c->ids, &c->work[0], &c->work[1], &c->work_v[0], &c->work_v[1], &c->s_keys,
                     &c->s_pos, &c->fx_scratch, &c->fx_fill, &c->fx_ovf, &c->fx_base, &c->fx_cnt,
                     &c->fx_seg, &c->tags0})
