@@ -295,6 +295,15 @@ int ams_run_level(ams_ctx_t* ctx, int level, int32_t* group_first, int32_t* grou
                   uint64_t* sizes_before, uint64_t* drawn, int32_t* nb, uint32_t* seg_hist,
                   uint64_t* boundaries, uint64_t* loads, uint64_t* max_load, uint64_t* new_sizes,
                   uint64_t* stats);
+/* Id of the last ams_sort_run on the context (1, 2, ...); the records of the
+ * last 8 runs stay readable by id (run 0 = the last run). */
+uint64_t ams_run_id(const ams_ctx_t* ctx);
+int ams_run_level_dims_at(ams_ctx_t* ctx, uint64_t run, int level, int* r, int* ngroups, int* npe,
+                          int* nb_stride, int* has_stats);
+int ams_run_level_at(ams_ctx_t* ctx, uint64_t run, int level, int32_t* group_first, int32_t* group_npe,
+                     uint64_t* sizes_before, uint64_t* drawn, int32_t* nb, uint32_t* seg_hist,
+                     uint64_t* boundaries, uint64_t* loads, uint64_t* max_load, uint64_t* new_sizes,
+                     uint64_t* stats);
 
 #ifdef __cplusplus
 }

@@ -60,6 +60,9 @@ _SIGNATURES = {
     "ams_level_scatter": (_I, [_P, _P, _P, _I, _P, _P, _I, _P, _P, _I, _I]),
     "ams_final_sort_stats": (_I, [_P, _P]),
     "ams_final_sort_fixed_stats": (_I, [_P, _P]),
+    "ams_run_id": (C.c_uint64, [_P]),
+    "ams_run_level_dims_at": (_I, [_P, C.c_uint64, _I, _P, _P, _P, _P, _P]),
+    "ams_run_level_at": (_I, [_P, C.c_uint64, _I] + [_P] * 11),
     "ams_level_scatter_ex": (_I, [_P, _P, _P, _I, _P, _P, _I, _P, _P, _I, _I, _I]),
     "ams_final_sort_buckets": (_I, [_P, _P, _P, _P, _I, _I, _P, _P, _P, _P]),
     "ams_get_minmax": (_I, [_P, _P]),
@@ -408,11 +411,15 @@ class Context:
                                ptr(vals), ptr(out), ptr(out_vals), out_sizes.ctypes.data, reps))
         return out_sizes[: len(sz)], list(reps)
 
-    def run_level(self, level: int) -> dict:
-        """Host records of one level of the last sort_run."""
+    def run_id(self) -> int:
+        """Id of the last sort_run (its records stay readable for 8 runs)."""
+        return int(lib.ams_run_id(self.h))
+
+    def run_level(self, level: int, run: int = 0) -> dict:
+        """Host records of one level of sort_run `run` (0 = the last)."""
         r, G, P, nbs, hs = (C.c_int() for _ in range(5))
-        check(lib.ams_run_level_dims(self.h, level, C.byref(r), C.byref(G), C.byref(P),
-                                     C.byref(nbs), C.byref(hs)))
+        check(lib.ams_run_level_dims_at(self.h, int(run), level, C.byref(r), C.byref(G), C.byref(P),
+                                        C.byref(nbs), C.byref(hs)))
         r, G, P, nbs = r.value, G.value, P.value, nbs.value
         d = {"r": r, "group_first": np.zeros(G, np.int32), "group_npe": np.zeros(G, np.int32),
              "sizes_before": np.zeros(P, np.uint64), "drawn": np.zeros(G, np.uint64),
@@ -422,7 +429,7 @@ class Context:
              "stats": np.zeros((G, 4), np.uint64) if hs.value else None}
         order = ("group_first", "group_npe", "sizes_before", "drawn", "nb", "seg_hist",
                  "boundaries", "loads", "max_load", "new_sizes", "stats")
-        check(lib.ams_run_level(self.h, level, *[ptr(d[k]) for k in order]))
+        check(lib.ams_run_level_at(self.h, int(run), level, *[ptr(d[k]) for k in order]))
         return d
 
     def map_keys(self, src, dst, n, from_kind, to_kind):

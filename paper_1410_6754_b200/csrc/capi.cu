@@ -198,6 +198,10 @@ struct ams_ctx {
   };
   std::vector<LevelRec> run_levels;
   std::vector<uint64_t> run_final_sizes;
+  // records of the last kRunHistory runs (run id, levels), newest last
+  static constexpr size_t kRunHistory = 8;
+  uint64_t run_id = 0;
+  std::vector<std::pair<uint64_t, std::vector<LevelRec>>> run_history;
   // optional per-category kernel timing (CUDA events on the launching stream)
   bool timing = false;
   struct Timed { int cat; cudaEvent_t a, b; double bytes; };
@@ -1482,16 +1486,51 @@ int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* p
     return rc;
   }
   tr.mark("final");
+  c->run_id += 1;
+  c->run_history.emplace_back(c->run_id, std::move(c->run_levels));
+  c->run_levels.clear();
+  if (c->run_history.size() > ams_ctx::kRunHistory) c->run_history.erase(c->run_history.begin());
   c->run_final_sizes = sizes;
   if (out_pe_sizes) std::memcpy(out_pe_sizes, sizes.data(), sizeof(uint64_t) * p);
   return AMS_OK;
 }
 
+uint64_t ams_run_id(const ams_ctx_t* c) { return c ? c->run_id : 0; }
+
+}  // extern "C"
+
+namespace {
+// Records of run `id` (0 = the last run); null when no longer kept.
+const std::vector<ams_ctx::LevelRec>* run_records(const ams_ctx* c, uint64_t id) {
+  if (id == 0) return c->run_history.empty() ? nullptr : &c->run_history.back().second;
+  for (const auto& h : c->run_history)
+    if (h.first == id) return &h.second;
+  return nullptr;
+}
+}  // namespace
+
+extern "C" {
+
 int ams_run_level_dims(ams_ctx_t* c, int level, int* r, int* ngroups, int* npe, int* nb_stride,
                        int* has_stats) {
+  return ams_run_level_dims_at(c, 0, level, r, ngroups, npe, nb_stride, has_stats);
+}
+
+int ams_run_level(ams_ctx_t* c, int level, int32_t* group_first, int32_t* group_npe,
+                  uint64_t* sizes_before, uint64_t* drawn, int32_t* nb, uint32_t* seg_hist,
+                  uint64_t* boundaries, uint64_t* loads, uint64_t* max_load, uint64_t* new_sizes,
+                  uint64_t* stats) {
+  return ams_run_level_at(c, 0, level, group_first, group_npe, sizes_before, drawn, nb, seg_hist,
+                          boundaries, loads, max_load, new_sizes, stats);
+}
+
+int ams_run_level_dims_at(ams_ctx_t* c, uint64_t run, int level, int* r, int* ngroups, int* npe,
+                          int* nb_stride, int* has_stats) {
   if (!c) return set_error(AMS_EINVAL, "null context");
-  if (level < 0 || level >= (int)c->run_levels.size()) return set_error(AMS_EINVAL, "no such level");
-  const ams_ctx::LevelRec& L = c->run_levels[level];
+  const std::vector<ams_ctx::LevelRec>* rl = run_records(c, run);
+  if (!rl) return set_error(AMS_EINVAL, "records of that run are no longer kept");
+  if (level < 0 || level >= (int)rl->size()) return set_error(AMS_EINVAL, "no such level");
+  const ams_ctx::LevelRec& L = (*rl)[level];
   if (r) *r = L.r;
   if (ngroups) *ngroups = L.G;
   if (npe) *npe = L.P;
@@ -1500,13 +1539,15 @@ int ams_run_level_dims(ams_ctx_t* c, int level, int* r, int* ngroups, int* npe, 
   return AMS_OK;
 }
 
-int ams_run_level(ams_ctx_t* c, int level, int32_t* group_first, int32_t* group_npe,
-                  uint64_t* sizes_before, uint64_t* drawn, int32_t* nb, uint32_t* seg_hist,
-                  uint64_t* boundaries, uint64_t* loads, uint64_t* max_load, uint64_t* new_sizes,
-                  uint64_t* stats) {
+int ams_run_level_at(ams_ctx_t* c, uint64_t run, int level, int32_t* group_first, int32_t* group_npe,
+                     uint64_t* sizes_before, uint64_t* drawn, int32_t* nb, uint32_t* seg_hist,
+                     uint64_t* boundaries, uint64_t* loads, uint64_t* max_load, uint64_t* new_sizes,
+                     uint64_t* stats) {
   if (!c) return set_error(AMS_EINVAL, "null context");
-  if (level < 0 || level >= (int)c->run_levels.size()) return set_error(AMS_EINVAL, "no such level");
-  const ams_ctx::LevelRec& L = c->run_levels[level];
+  const std::vector<ams_ctx::LevelRec>* rl = run_records(c, run);
+  if (!rl) return set_error(AMS_EINVAL, "records of that run are no longer kept");
+  if (level < 0 || level >= (int)rl->size()) return set_error(AMS_EINVAL, "no such level");
+  const ams_ctx::LevelRec& L = (*rl)[level];
   auto cp = [](auto* dst, const auto& v) {
     if (dst && !v.empty()) std::memcpy(dst, v.data(), sizeof(v[0]) * v.size());
   };

@@ -2170,6 +2170,45 @@ cudaError_t launch_smem_sort_lsd(cudaStream_t st, const void* src, const void* s
   return cudaGetLastError();
 }
 
+size_t scatter_fixed_smem_bytes(int nb) {
+  const int per = (nb + kThreadsU - 1) / kThreadsU | 1;
+  const size_t nbp = (size_t)per * kThreadsU;
+  return 2 * 8 * (size_t)(kTile + 2) + 16 * nbp + 2 * (size_t)kTile;
+}
+
+cudaError_t launch_scatter_fixed(cudaStream_t st, const void* src, int kind, void* dst,
+                                 const SegMeta& m, uint64_t nchunks, int max_nb,
+                                 const DigitCls* dcls, const uint32_t* cell0, uint32_t* fill,
+                                 uint32_t* seg_ovf) {
+  if (nchunks == 0) return cudaSuccess;
+  const size_t smem = scatter_fixed_smem_bytes(max_nb);
+  const uint64_t* s = static_cast<const uint64_t*>(src);
+  uint64_t* d = static_cast<uint64_t*>(dst);
+  cudaError_t e = cudaSuccess;
+  (void)kind;  // the last level's output holds order-mapped u64 keys
+  auto fn = k_scatter_fixed<AMS_KEY_U64>;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  fn<<<(unsigned)nchunks, kThreadsU, smem, st>>>(s, d, m, dcls, cell0, fill, seg_ovf);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fixed_cells(cudaStream_t st, const uint32_t* fill, const uint32_t* cell0,
+                               const uint64_t* seg_off, const uint32_t* seg_ovf, int nseg,
+                               uint64_t* out_base, uint32_t* cnt, uint32_t* cell_seg) {
+  if (nseg == 0) return cudaSuccess;
+  k_fixed_cells<<<(nseg + 7) / 8, 256, 0, st>>>(fill, cell0, seg_off, seg_ovf, nseg, out_base, cnt,
+                                                 cell_seg);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bucket_ranges(cudaStream_t st, const uint8_t* blobs, const uint64_t* gbounds,
+                                 const int32_t* seg_gb, int nseg, DigitCls* out) {
+  if (nseg == 0) return cudaSuccess;
+  k_bucket_ranges<<<(nseg + 127) / 128, 128, 0, st>>>(blobs, gbounds, seg_gb, nseg, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_map_keys(cudaStream_t st, const void* src, void* dst, uint64_t n, int from,
                             int to) {
   if (n == 0) return cudaSuccess;

@@ -86,8 +86,16 @@ class SortOutput:
     keys: torch.Tensor
     vals: torch.Tensor | None
     pe_sizes: np.ndarray
-    levels: list
+    _levels: object  # list of LevelRecord, or a callable building it on first use
     launches: int
+
+    @property
+    def levels(self) -> list:
+        """Per-level records; the one-call driver's are read from the context on
+        first use (it keeps the last 8 runs), off the sort's critical path."""
+        if callable(self._levels):
+            self._levels = self._levels()
+        return self._levels
 
     @property
     def reports(self) -> list:
@@ -285,13 +293,17 @@ class AmsSorter:
                                            vals if n else None, out if n else None,
                                            out_vals if n else None)
         eps_l = params.per_level_imbalance()
-        levels = []
-        for lv, r in enumerate(gc):
-            d = self.ctx.run_level(lv)
-            n_g = np.add.reduceat(d["sizes_before"], d["group_first"]) if len(d["sizes_before"]) \
-                else np.zeros(len(d["group_first"]), np.uint64)
-            levels.append(LevelRecord(lv, r, d["group_first"], d["group_npe"], d["sizes_before"],
-                                      d["drawn"], d["nb"].astype(np.int64), d["seg_hist"],
-                                      d["boundaries"], d["loads"], d["max_load"],
-                                      load_budget(n_g, r, eps_l), d["new_sizes"], d["stats"]))
+        ctx, run = self.ctx, self.ctx.run_id()
+
+        def levels():
+            recs = []
+            for lv, r in enumerate(gc):
+                d = ctx.run_level(lv, run)
+                n_g = np.add.reduceat(d["sizes_before"], d["group_first"]) if len(d["sizes_before"]) \
+                    else np.zeros(len(d["group_first"]), np.uint64)
+                recs.append(LevelRecord(lv, r, d["group_first"], d["group_npe"], d["sizes_before"],
+                                        d["drawn"], d["nb"].astype(np.int64), d["seg_hist"],
+                                        d["boundaries"], d["loads"], d["max_load"],
+                                        load_budget(n_g, r, eps_l), d["new_sizes"], d["stats"]))
+            return recs
         return SortOutput(ret_out, ret_vals, final_sizes, levels, self.ctx.launches - launches0)
