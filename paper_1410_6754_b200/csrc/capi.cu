@@ -166,8 +166,9 @@ struct ams_ctx {
   SegMeta meta{};
   DevBuf chunk_tot, seg_hist, cell_base, pieces, minmax;
   bool level_stable = true;
-  DevBuf ids;  // per-key bucket bytes of the current level (nb <= 256)
+  DevBuf ids;  // per-key bucket ids of the current level (bytes, or u16 above 256 buckets)
   bool level_ids = false;
+  int level_id_bytes = 1;
   // key bounds [lo, hi] of the current level's groups (ping-pong)
   DevBuf bounds[2];
   int bcur = 0;
@@ -309,7 +310,7 @@ cudaError_t upload_segments(Stage& st, cudaStream_t stream, const uint64_t* off,
 // scan, for a segment table whose classifiers are ready.
 int run_histogram(ams_ctx* c, const void* src, int kind, bool digit, const SegMeta& m,
                   uint64_t nchunks, int nb_stride, const DigitCls* dcls,
-                  unsigned long long* minmax, uint64_t nelems, uint8_t* ids) {
+                  unsigned long long* minmax, uint64_t nelems, uint8_t* ids, int id_bytes = 1) {
   AMS_CK(c->chunk_tot.ensure(sizeof(uint32_t) * std::max<uint64_t>(nchunks, 1) * nb_stride));
   AMS_CK(c->seg_hist.ensure(sizeof(uint32_t) * (size_t)std::max(m.nseg, 1) * nb_stride));
   AMS_CK(cudaMemsetAsync(c->seg_hist.p, 0, sizeof(uint32_t) * (size_t)m.nseg * nb_stride, c->stream));
@@ -317,7 +318,7 @@ int run_histogram(ams_ctx* c, const void* src, int kind, bool digit, const SegMe
     KTimer kt(c, digit ? AMS_KCAT_FHIST : AMS_KCAT_HIST, 8.0 * nelems);
     AMS_CK(launch_hist(c->stream, src, kind, digit, m, nchunks, c->blobs.as<uint8_t>(), dcls,
                        c->nspl_cap, c->cells_cap, nb_stride, c->chunk_tot.as<uint32_t>(),
-                       c->seg_hist.as<uint32_t>(), minmax, ids));
+                       c->seg_hist.as<uint32_t>(), minmax, ids, id_bytes));
   }
   {
     KTimer kt(c, AMS_KCAT_CHUNKSCAN, 8.0 * nchunks * nb_stride);
@@ -589,20 +590,23 @@ int ams_level_classify(ams_ctx_t* c, const void* src, int key_kind, int nseg,
   for (int s = 0; s < nseg; ++s) nel += h_seg_len[s];
   c->level_elems = nel;
   c->level_stable = stable != 0;
-  // Buckets below 256: the histogram pass also stores each key's bucket as a
-  // byte at its buffer index, and the scatter reads it instead of classifying.
+  // The histogram pass also stores each key's bucket at its buffer index (a
+  // byte up to 256 buckets, else 16 bits); the scatter reads it instead of
+  // classifying again.
   uint8_t* ids = nullptr;
+  int id_bytes = nb_stride <= 256 ? 1 : 2;  // u16 ids up to AMS_MAX_BUCKETS buckets
 #ifndef AMS_NO_IDS
-  if (nb_stride <= 256) {
+  {
     uint64_t span = 0;
     for (int s = 0; s < nseg; ++s) span = std::max(span, h_seg_off[s] + h_seg_len[s]);
-    AMS_CK(c->ids.ensure(std::max<uint64_t>(span, 1)));
+    AMS_CK(c->ids.ensure((size_t)id_bytes * std::max<uint64_t>(span, 1)));
     ids = c->ids.as<uint8_t>();
   }
 #endif
   c->level_ids = ids != nullptr;
+  c->level_id_bytes = id_bytes;
   int rc = run_histogram(c, src, key_kind, false, c->meta, c->nchunks, nb_stride, nullptr, mm,
-                         nel, ids);
+                         nel, ids, id_bytes);
   if (rc) return rc;
   if (track_minmax) {
     // The whole input is one group at the first level: its bounds are the
@@ -681,7 +685,8 @@ int level_scatter_impl(ams_ctx_t* c, const void* src, const void* src_vals, int 
     AMS_CK(launch_scatter(c->stream, src, src_vals, key_kind, false, c->level_stable, dst,
                           dst_vals, c->meta, c->nchunks, c->blobs.as<uint8_t>(), nullptr,
                           c->nspl_cap, c->cells_cap, c->nb_stride, c->chunk_tot.as<uint32_t>(),
-                          c->cell_base.as<uint64_t>(), c->level_ids ? c->ids.as<uint8_t>() : nullptr));
+                          c->cell_base.as<uint64_t>(), c->level_ids ? c->ids.as<uint8_t>() : nullptr,
+                          c->level_id_bytes));
   }
   // Key bounds of the next level's groups (this rank's children).
   const int nxt = 1 - c->bcur;

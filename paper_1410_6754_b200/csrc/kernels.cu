@@ -208,7 +208,8 @@ __global__ void __launch_bounds__(1024) k_build_cls(const uint64_t* __restrict__
 // add it to the segment histogram.
 // IDS: also store every key's bucket (< 256) as a byte at its buffer index,
 // so the level's scatter does not classify again.
-template <int KIND, bool DIGIT, bool MINMAX, bool IDS, bool TAGS = false>
+// IDS: 0 = none, 1 = bucket bytes (<= 256 buckets), 2 = 16-bit bucket ids.
+template <int KIND, bool DIGIT, bool MINMAX, int IDS, bool TAGS = false>
 __global__ void __launch_bounds__(kThreads) k_hist(const uint64_t* __restrict__ src, SegMeta m,
                                                    const uint8_t* __restrict__ blobs,
                                                    const DigitCls* __restrict__ dcls, int nspl_cap,
@@ -262,7 +263,8 @@ __global__ void __launch_bounds__(kThreads) k_hist(const uint64_t* __restrict__ 
         if constexpr (DIGIT) b = dv.classify(keys[i], 0);
         else if constexpr (TAGS) b = tv.classify(keys[i], (uint32_t)m.tags[base + e]);
         else b = tv.classify(keys[i], (uint32_t)((int64_t)base + posbase) + e);
-        if constexpr (IDS) ids[base + e] = (uint8_t)b;
+        if constexpr (IDS == 1) ids[base + e] = (uint8_t)b;
+        if constexpr (IDS == 2) reinterpret_cast<uint16_t*>(ids)[base + e] = (uint16_t)b;
         if constexpr (MINMAX) { mn = min(mn, (unsigned long long)keys[i]); mx = max(mx, (unsigned long long)keys[i]); }
         if (b != cur) {
           if (cnt) atomicAdd(&hist[cur], cnt);
@@ -438,6 +440,7 @@ __global__ void k_child_bounds(const uint8_t* __restrict__ blobs, GroupMeta gm, 
 // Ranking modes of the scatter.
 constexpr int kClsTree = 0, kClsDigit = 1, kClsIds = 2;
 constexpr int kClsTreeTags = 3;  // tree, tie-break by the carried origin tag (the values)
+constexpr int kClsIds16 = 4;     // 16-bit bucket ids stored by the histogram pass (> 256 buckets)
 constexpr int kRankWarp = 0;     // stable, one bucket-counter array per warp
 constexpr int kRankSerial = 1;   // stable, one shared array, warps take turns
 constexpr int kRankAtomic = 2;   // unstable (keys only, order inside a run is free)
@@ -560,6 +563,8 @@ __global__ void __launch_bounds__(kThreads, VALS ? 2 : 4)
         if (FULL || e < tcount) {
           if constexpr (CLS == kClsIds) {
             b = ids[base + e];
+          } else if constexpr (CLS == kClsIds16) {
+            b = reinterpret_cast<const uint16_t*>(ids)[base + e];
           } else {
             const uint64_t key = to_ordered<KIND>(keys_s[e]);
             if constexpr (CLS == kClsDigit) b = dv.classify(key, 0);
@@ -1895,28 +1900,31 @@ size_t hist_smem_bytes(int nb_stride, int nspl_cap, int cells_cap, bool digit) {
 cudaError_t launch_hist(cudaStream_t st, const void* src, int kind, bool digit, const SegMeta& m,
                         uint64_t nchunks, const uint8_t* blobs, const DigitCls* dcls, int nspl_cap,
                         int cells_cap, int nb_stride, uint32_t* chunk_tot, uint32_t* seg_hist,
-                        unsigned long long* minmax, uint8_t* ids) {
+                        unsigned long long* minmax, uint8_t* ids, int id_bytes) {
   if (nchunks == 0) return cudaSuccess;
   const size_t smem = hist_smem_bytes(nb_stride, nspl_cap, cells_cap, digit);
   const uint64_t* s = static_cast<const uint64_t*>(src);
   cudaError_t e = cudaSuccess;
   if (digit) {
-    auto fn = k_hist<AMS_KEY_U64, true, false, false>;
+    auto fn = k_hist<AMS_KEY_U64, true, false, 0>;
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     fn<<<(unsigned)nchunks, kThreads, smem, st>>>(s, m, blobs, dcls, nspl_cap, nb_stride,
                                                    chunk_tot, seg_hist, minmax, nullptr);
   } else if (m.tags) {
     // Origin-tag tie-breaks (deterministic delivery, levels >= 2): keys are order-mapped u64.
-    auto fn = ids ? k_hist<AMS_KEY_U64, false, false, true, true> : k_hist<AMS_KEY_U64, false, false, false, true>;
+    auto fn = !ids ? k_hist<AMS_KEY_U64, false, false, 0, true>
+              : id_bytes == 2 ? k_hist<AMS_KEY_U64, false, false, 2, true> : k_hist<AMS_KEY_U64, false, false, 1, true>;
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     fn<<<(unsigned)nchunks, kThreads, smem, st>>>(s, m, blobs, dcls, nspl_cap, nb_stride, chunk_tot,
                                                    seg_hist, minmax, ids);
   } else {
     AMS_KIND_DISPATCH(kind, K, {
-      auto fn = minmax ? (ids ? k_hist<K, false, true, true> : k_hist<K, false, true, false>)
-                       : (ids ? k_hist<K, false, false, true> : k_hist<K, false, false, false>);
+      auto fn = minmax ? (!ids ? k_hist<K, false, true, 0>
+                                : id_bytes == 2 ? k_hist<K, false, true, 2> : k_hist<K, false, true, 1>)
+                       : (!ids ? k_hist<K, false, false, 0>
+                               : id_bytes == 2 ? k_hist<K, false, false, 2> : k_hist<K, false, false, 1>);
       e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
       fn<<<(unsigned)nchunks, kThreads, smem, st>>>(s, m, blobs, dcls, nspl_cap, nb_stride,
@@ -2028,13 +2036,13 @@ cudaError_t launch_scatter(cudaStream_t st, const void* src, const void* src_val
                            bool digit, bool stable, void* dst, void* dst_vals, const SegMeta& m,
                            uint64_t nchunks, const uint8_t* blobs, const DigitCls* dcls,
                            int nspl_cap, int cells_cap, int nb_stride, const uint32_t* chunk_tot,
-                           const uint64_t* cell_base, const uint8_t* ids) {
+                           const uint64_t* cell_base, const uint8_t* ids, int id_bytes) {
   if (nchunks == 0) return cudaSuccess;
   const bool vals = src_vals != nullptr;
 #ifndef AMS_NO_SCATTER_U
   // The lean unstable kernel pays off with the cheap digit classifier (the
   // final partition); the tree classifier keeps the 4-CTA kernel below.
-  if (!stable && !vals && (digit || (ids && kScatterUIds)))
+  if (!stable && !vals && (digit || (ids && id_bytes == 1 && kScatterUIds)))
     return launch_scatter_u(st, src, kind, digit, dst, m, nchunks, blobs, dcls, nspl_cap,
                             cells_cap, nb_stride, chunk_tot, cell_base, digit ? nullptr : ids);
 #endif
@@ -2061,6 +2069,12 @@ cudaError_t launch_scatter(cudaStream_t st, const void* src, const void* src_val
   } else if (m.tags && !ids) {
     if (!vals || mode == kRankAtomic) return cudaErrorInvalidValue;  // tags travel as the values
     AMS_SCATTER_GO(AMS_KEY_U64, kClsTreeTags, true)
+  } else if (ids && id_bytes == 2) {
+    if (vals) {
+      AMS_KIND_DISPATCH(kind, K, AMS_SCATTER_GO(K, kClsIds16, true))
+    } else {
+      AMS_KIND_DISPATCH(kind, K, AMS_SCATTER_GO(K, kClsIds16, false))
+    }
   } else if (ids) {
     if (vals) {
       AMS_KIND_DISPATCH(kind, K, AMS_SCATTER_GO(K, kClsIds, true))

@@ -72,7 +72,7 @@ size_t hist_smem_bytes(int nb_stride, int nspl_cap, int cells_cap, bool digit);
 cudaError_t launch_hist(cudaStream_t st, const void* src, int kind, bool digit, const SegMeta& m,
                         uint64_t nchunks, const uint8_t* blobs, const DigitCls* dcls, int nspl_cap,
                         int cells_cap, int nb_stride, uint32_t* chunk_tot, uint32_t* seg_hist,
-                        unsigned long long* minmax, uint8_t* ids);
+                        unsigned long long* minmax, uint8_t* ids, int id_bytes = 1);
 cudaError_t launch_chunk_scan(cudaStream_t st, uint32_t* chunk_tot, const SegMeta& m, int nb_stride);
 cudaError_t launch_cell_base(cudaStream_t st, const uint32_t* seg_hist, int nb_stride,
                              const GroupMeta& gm, int ngroups, int r, uint64_t* pieces,
@@ -90,7 +90,7 @@ cudaError_t launch_scatter(cudaStream_t st, const void* src, const void* src_val
                            bool digit, bool stable, void* dst, void* dst_vals, const SegMeta& m,
                            uint64_t nchunks, const uint8_t* blobs, const DigitCls* dcls,
                            int nspl_cap, int cells_cap, int nb_stride, const uint32_t* chunk_tot,
-                           const uint64_t* cell_base, const uint8_t* ids);
+                           const uint64_t* cell_base, const uint8_t* ids, int id_bytes = 1);
 // Child-group key bounds [2*(g*r+t)] from parent bounds [2*g] and the plan.
 cudaError_t launch_child_bounds(cudaStream_t st, const uint8_t* blobs, const GroupMeta& gm,
                                 int ngroups, int r, const uint64_t* parent, uint64_t* child);
