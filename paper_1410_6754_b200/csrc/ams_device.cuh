@@ -38,7 +38,7 @@ struct ClsHeader {
   uint32_t nspl;     // number of splitters = buckets - 1
   uint32_t shift;    // LUT cell of key k: (k - lo) >> shift, clamped
   uint32_t ncells;   // LUT entries
-  uint32_t pad;
+  uint32_t max_inside;  // most splitters in one LUT cell (> 8: duplicate-heavy splitters)
 };
 
 // Digit classifier (final-sort partitions): digit = (k-lo) * nb / (range+1)
@@ -135,7 +135,11 @@ struct TreeView {
   // (ams.py:201-211).  Splitters before the key's LUT cell
   // are all below it, those after all above; the few inside the cell
   // (sorted) are compared one by one.
-  __device__ __forceinline__ uint32_t classify(uint64_t key, uint32_t pos) const {
+  // hint: a likely answer (the thread's previous bucket); checked only in
+  // the rare many-splitter cells, where consecutive keys of duplicate-heavy
+  // inputs keep landing in the same bucket.
+  __device__ __forceinline__ uint32_t classify(uint64_t key, uint32_t pos,
+                                               uint32_t hint = 0xFFFFFFFFu) const {
     if (h.nspl == 0) return 0;
     uint64_t c = (key - h.lo) >> h.shift;
     c = key < h.lo ? 0 : (c >= h.ncells ? h.ncells - 1 : c);
@@ -155,7 +159,18 @@ struct TreeView {
       return b;
     }
     // Many splitters in one cell (duplicate-heavy keys: runs of equal
-    // splitter keys told apart by position): lower bound by (key, pos).
+    // splitter keys told apart by position): the hint if it brackets
+    // (key, pos), else the lower bound by (key, pos).
+    if (hint > b && hint <= end) {
+      const uint64_t pk = lds_u64(skeys + 8 * (hint - 1));
+      const bool above_prev = pk < key || (pk == key && lds_u32(spos + 4 * (hint - 1)) < pos);
+      bool below_next = true;
+      if (hint < end) {
+        const uint64_t nk = lds_u64(skeys + 8 * hint);
+        below_next = !(nk < key || (nk == key && lds_u32(spos + 4 * hint) < pos));
+      }
+      if (above_prev && below_next) return hint;
+    }
     uint32_t lo = b + 1, hi = end;
     while (lo < hi) {
       const uint32_t mid = (lo + hi) >> 1;

@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(1024) k_build_cls(const uint64_t* __restrict__
   }
   __syncthreads();
   if (nspl == 0) {
-    if (threadIdx.x == 0) { h->lo = 0; h->hi = 0; h->nspl = 0; h->shift = 0; h->ncells = 0; h->pad = 0; }
+    if (threadIdx.x == 0) { h->lo = 0; h->hi = 0; h->nspl = 0; h->shift = 0; h->ncells = 0; h->max_inside = 0; }
     return;
   }
   const uint64_t lo = sk[0], hi = sk[nspl - 1];
@@ -189,14 +189,22 @@ __global__ void __launch_bounds__(1024) k_build_cls(const uint64_t* __restrict__
   const uint32_t ncells = (uint32_t)((hi - lo) >> shift) + 1;
   // Cell c covers keys [lo + c<<shift, lo + (c+1)<<shift); its record is
   // (#splitters below the cell) | (#splitters inside it) << 16.
+  __shared__ uint32_t s_inside;
+  if (threadIdx.x == 0) s_inside = 0;
+  __syncthreads();
+  uint32_t my_inside = 0;
   for (uint32_t c = threadIdx.x; c < ncells; c += blockDim.x) {
     const uint32_t first = lower_bound_smem(sk, nspl, lo + ((uint64_t)c << shift));
     const uint32_t next = c + 1 < ncells ? lower_bound_smem(sk, nspl, lo + ((uint64_t)(c + 1) << shift))
                                          : nspl;
     lut[c] = first | ((next - first) << 16);
+    my_inside = max(my_inside, next - first);
   }
+  atomicMax(&s_inside, my_inside);
+  __syncthreads();
   if (threadIdx.x == 0) {
-    h->lo = lo; h->hi = hi; h->nspl = nspl; h->shift = shift; h->ncells = ncells; h->pad = 0;
+    h->lo = lo; h->hi = hi; h->nspl = nspl; h->shift = shift; h->ncells = ncells;
+    h->max_inside = s_inside;
   }
 }
 
@@ -209,7 +217,11 @@ __global__ void __launch_bounds__(1024) k_build_cls(const uint64_t* __restrict__
 // IDS: also store every key's bucket (< 256) as a byte at its buffer index,
 // so the level's scatter does not classify again.
 // IDS: 0 = none, 1 = bucket bytes (<= 256 buckets), 2 = 16-bit bucket ids.
-template <int KIND, bool DIGIT, bool MINMAX, int IDS, bool TAGS = false>
+// DUP (tree classifiers): the launch is a pair; DUP = 1 does the groups
+// whose LUT has no cell with more than 8 splitters, DUP = 2 the others
+// (duplicate-heavy keys), trying the thread's previous bucket first in
+// the binary search.  Each CTA of the other variant exits at once.
+template <int KIND, bool DIGIT, bool MINMAX, int IDS, bool TAGS = false, int DUP = 1>
 __global__ void __launch_bounds__(kThreads) k_hist(const uint64_t* __restrict__ src, SegMeta m,
                                                    const uint8_t* __restrict__ blobs,
                                                    const DigitCls* __restrict__ dcls, int nspl_cap,
@@ -237,12 +249,18 @@ __global__ void __launch_bounds__(kThreads) k_hist(const uint64_t* __restrict__ 
   if constexpr (DIGIT) {
     dv.c = dcls[cls];
   } else {
+    if ((DUP == 2) != (reinterpret_cast<const ClsHeader*>(blobs + (size_t)cls * kBlobStride)->max_inside > 8))
+      return;  // the other variant of the pair classifies this group
     tv = load_tree(blobs + (size_t)cls * kBlobStride, clsmem, nspl_cap);
     posbase = m.posbase[cls];
     __syncthreads();
   }
   const int lane = threadIdx.x & 31;
   unsigned long long mn = ~0ULL, mx = 0;
+  // hint (DUP == 2): this thread's last bucket of the previous tile, tried
+  // first in the many-splitter LUT cells; fixed for the tile, so the items'
+  // classifications stay independent.
+  uint32_t hint = kInvalid;
   auto tile = [&](const uint64_t t0, const uint32_t tcount, auto full_tag) {
     constexpr bool FULL = decltype(full_tag)::value;
     const uint64_t base = seg_off + t0;
@@ -261,8 +279,8 @@ __global__ void __launch_bounds__(kThreads) k_hist(const uint64_t* __restrict__ 
       if (FULL || e < tcount) {
         uint32_t b;
         if constexpr (DIGIT) b = dv.classify(keys[i], 0);
-        else if constexpr (TAGS) b = tv.classify(keys[i], (uint32_t)m.tags[base + e]);
-        else b = tv.classify(keys[i], (uint32_t)((int64_t)base + posbase) + e);
+        else if constexpr (TAGS) b = tv.classify(keys[i], (uint32_t)m.tags[base + e], hint);
+        else b = tv.classify(keys[i], (uint32_t)((int64_t)base + posbase) + e, hint);
         if constexpr (IDS == 1) ids[base + e] = (uint8_t)b;
         if constexpr (IDS == 2) reinterpret_cast<uint16_t*>(ids)[base + e] = (uint16_t)b;
         if constexpr (MINMAX) { mn = min(mn, (unsigned long long)keys[i]); mx = max(mx, (unsigned long long)keys[i]); }
@@ -275,6 +293,7 @@ __global__ void __launch_bounds__(kThreads) k_hist(const uint64_t* __restrict__ 
       }
     }
     if (cnt) atomicAdd(&hist[cur], cnt);
+    if constexpr (DUP == 2) hint = cur;
   };
   for (uint64_t t0 = first; t0 < last; t0 += kTile) {
     const uint32_t tcount = (uint32_t)min((uint64_t)kTile, last - t0);
@@ -541,6 +560,17 @@ __global__ void __launch_bounds__(kThreads, VALS ? 2 : 4)
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t lt = lanemask_lt();
   const int nbits = bit_length64((uint64_t)(nb_stride - 1));
+  // Unstable mode: a chunk whose first and last key share a bucket (sorted /
+  // duplicate-heavy input) ranks warps of one bucket with one atomic.
+  bool runs = false;
+  if constexpr (MODE == kRankAtomic && (CLS == kClsIds || CLS == kClsIds16)) {
+    if (last > first) {
+      const uint64_t i0 = seg_off + first, i1 = seg_off + last - 1;
+      runs = CLS == kClsIds ? ids[i0] == ids[i1]
+                            : reinterpret_cast<const uint16_t*>(ids)[i0] ==
+                                  reinterpret_cast<const uint16_t*>(ids)[i1];
+    }
+  }
   uint32_t* whw = wh + (MODE == kRankWarp ? (size_t)w * nb_stride : 0);
   for (uint64_t t0 = first; t0 < last; t0 += kTile) {
     const uint32_t tcount = (uint32_t)min((uint64_t)kTile, last - t0);
@@ -553,8 +583,9 @@ __global__ void __launch_bounds__(kThreads, VALS ? 2 : 4)
     cp_async_wait_all();
     __syncthreads();  // tile staged, counters zeroed, tree loaded
     uint32_t pk[kItems];
-    auto classify_all = [&](auto full_tag) {
+    auto classify_all = [&](auto full_tag, auto runs_tag) {
       constexpr bool FULL = decltype(full_tag)::value;
+      constexpr bool RUNS = decltype(runs_tag)::value;
       [[maybe_unused]] const uint32_t pos0 = (uint32_t)((int64_t)base + posbase);
 #pragma unroll
       for (int i = 0; i < kItems; ++i) {
@@ -574,12 +605,29 @@ __global__ void __launch_bounds__(kThreads, VALS ? 2 : 4)
         }
         pk[i] = b;
         if constexpr (MODE == kRankAtomic) {
-          if (FULL || b != kInvalid) pk[i] = (b << 16) | atomicAdd(&whw[b], 1u);
+          // A warp whose 32 keys share one bucket (sorted / duplicate-heavy
+          // input) takes one atomic instead of 32 colliding ones.
+          if constexpr (RUNS) {
+            const uint32_t b0 = __shfl_sync(0xffffffffu, b, 0);
+            if (__all_sync(0xffffffffu, b == b0) && b0 != kInvalid) {
+              uint32_t base0 = 0;
+              if (lane == 0) base0 = atomicAdd(&whw[b0], 32u);
+              pk[i] = (b0 << 16) | (__shfl_sync(0xffffffffu, base0, 0) + lane);
+            } else if (FULL || b != kInvalid) {
+              pk[i] = (b << 16) | atomicAdd(&whw[b], 1u);
+            }
+          } else {
+            if (FULL || b != kInvalid) pk[i] = (b << 16) | atomicAdd(&whw[b], 1u);
+          }
         }
       }
     };
-    if (tcount == (uint32_t)kTile) classify_all(std::true_type{});
-    else classify_all(std::false_type{});
+    if (tcount == (uint32_t)kTile) {
+      if (runs) classify_all(std::true_type{}, std::true_type{});
+      else classify_all(std::true_type{}, std::false_type{});
+    } else {
+      classify_all(std::false_type{}, std::false_type{});
+    }
     if constexpr (MODE != kRankAtomic) {
       const bool full = tcount == (uint32_t)kTile;
       auto rank_all = [&](auto nbits_tag) {
@@ -926,6 +974,15 @@ __global__ void __launch_bounds__(kThreadsU, 2)
           const uint64_t x = key - dlo;
           const uint32_t b = dm ? min(__umulhi((uint32_t)(x >> dsh), dm), dmax) : (uint32_t)x;
           kr[i] = key;
+          if (FULL && dm == 0) {  // counting cells (few values): one atomic per uniform warp
+            const uint32_t b0 = __shfl_sync(0xffffffffu, b, 0);
+            if (__all_sync(0xffffffffu, b == b0)) {
+              uint32_t base0 = 0;
+              if (lane == 0) base0 = atomicAdd(&cnt[b0], 32u);
+              pk[i] = (b0 << 16) | (__shfl_sync(0xffffffffu, base0, 0) + lane);
+              continue;
+            }
+          }
           pk[i] = (b << 16) | atomicAdd(&cnt[b], 1u);
         }
       }
@@ -1913,23 +1970,35 @@ cudaError_t launch_hist(cudaStream_t st, const void* src, int kind, bool digit, 
                                                    chunk_tot, seg_hist, minmax, nullptr);
   } else if (m.tags) {
     // Origin-tag tie-breaks (deterministic delivery, levels >= 2): keys are order-mapped u64.
-    auto fn = !ids ? k_hist<AMS_KEY_U64, false, false, 0, true>
-              : id_bytes == 2 ? k_hist<AMS_KEY_U64, false, false, 2, true> : k_hist<AMS_KEY_U64, false, false, 1, true>;
-    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    fn<<<(unsigned)nchunks, kThreads, smem, st>>>(s, m, blobs, dcls, nspl_cap, nb_stride, chunk_tot,
-                                                   seg_hist, minmax, ids);
+#define AMS_HIST_TAGS(D)                                                                          \
+  {                                                                                               \
+    auto fn = !ids ? k_hist<AMS_KEY_U64, false, false, 0, true, D>                                \
+              : id_bytes == 2 ? k_hist<AMS_KEY_U64, false, false, 2, true, D>                     \
+                              : k_hist<AMS_KEY_U64, false, false, 1, true, D>;                    \
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);         \
+    if (e != cudaSuccess) return e;                                                               \
+    fn<<<(unsigned)nchunks, kThreads, smem, st>>>(s, m, blobs, dcls, nspl_cap, nb_stride, chunk_tot, \
+                                                   seg_hist, minmax, ids);                        \
+  }
+    AMS_HIST_TAGS(1)
+    AMS_HIST_TAGS(2)
+#undef AMS_HIST_TAGS
   } else {
-    AMS_KIND_DISPATCH(kind, K, {
-      auto fn = minmax ? (!ids ? k_hist<K, false, true, 0>
-                                : id_bytes == 2 ? k_hist<K, false, true, 2> : k_hist<K, false, true, 1>)
-                       : (!ids ? k_hist<K, false, false, 0>
-                               : id_bytes == 2 ? k_hist<K, false, false, 2> : k_hist<K, false, false, 1>);
-      e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      fn<<<(unsigned)nchunks, kThreads, smem, st>>>(s, m, blobs, dcls, nspl_cap, nb_stride,
-                                                     chunk_tot, seg_hist, minmax, ids);
-    });
+#define AMS_HIST_TREE(K, D)                                                                       \
+  {                                                                                               \
+    auto fn = minmax ? (!ids ? k_hist<K, false, true, 0, false, D>                                \
+                       : id_bytes == 2 ? k_hist<K, false, true, 2, false, D>                      \
+                                       : k_hist<K, false, true, 1, false, D>)                     \
+                     : (!ids ? k_hist<K, false, false, 0, false, D>                               \
+                       : id_bytes == 2 ? k_hist<K, false, false, 2, false, D>                     \
+                                       : k_hist<K, false, false, 1, false, D>);                   \
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);         \
+    if (e != cudaSuccess) return e;                                                               \
+    fn<<<(unsigned)nchunks, kThreads, smem, st>>>(s, m, blobs, dcls, nspl_cap, nb_stride,         \
+                                                   chunk_tot, seg_hist, minmax, ids);             \
+  }
+    AMS_KIND_DISPATCH(kind, K, { AMS_HIST_TREE(K, 1) AMS_HIST_TREE(K, 2) });
+#undef AMS_HIST_TREE
   }
   return cudaGetLastError();
 }
