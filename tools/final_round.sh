@@ -8,4 +8,4 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/fina
 timeout 600 python bench.py > gpurun_out/final/bench.json 2> gpurun_out/final/bench.err; echo "bench rc=$?"
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/final/bench_ref.json 2>&1; echo "ref rc=$?"
 bash tools/workloads.sh 3 > gpurun_out/final/workloads.txt 2>&1
-KSKIP=6 KCOUNT=6 bash tools/ncu_round.sh final 28 > /dev/null 2>&1; echo "ncu done"
+bash tools/ncu_round.sh final 28 > /dev/null 2>&1; echo "ncu done"

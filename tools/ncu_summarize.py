@@ -55,16 +55,20 @@ def main():
         cat = next((c for pat, c in CATS if pat in name), None)
         if cat is None:
             continue
+        dup_variant = "k_hist<" in name and name.split("(")[0].rstrip().endswith(", 2>")
+        if dup_variant:  # the duplicate-heavy half of a histogram launch pair
+            cat = cat + " [dup variant, exits]"
         rd = f(r, hdr, "dram__bytes_read.sum") * scale.get(units[hdr.index("dram__bytes_read.sum")], 1)
         wr = f(r, hdr, "dram__bytes_write.sum") * scale.get(units[hdr.index("dram__bytes_write.sum")], 1)
         ms = f(r, hdr, "gpu__time_duration.sum")
         if units[hdr.index("gpu__time_duration.sum")] == "us":
             ms /= 1e3
         inst = f(r, hdr, "smsp__inst_executed.sum")
-        alg = ALG[cat] * n
+        alg = 0 if dup_variant else ALG[cat] * n
         tmpl = name.split("(")[0].replace("void ", "")
         rec = {"template": tmpl, "dram_bytes_read": rd, "dram_bytes_write": wr, "traffic": rd + wr,
-               "algorithmic_bytes": alg, "traffic_over_algorithmic": (rd + wr) / alg, "ncu_ms": ms,
+               "algorithmic_bytes": alg, "traffic_over_algorithmic": (rd + wr) / alg if alg else None,
+               "ncu_ms": ms,
                "warp_inst_per_key": inst / n,
                "ipc": f(r, hdr, "sm__inst_executed.avg.per_cycle_active"),
                "warps_active_pct": f(r, hdr, "sm__warps_active.avg.pct_of_peak_sustained_active"),
@@ -76,7 +80,7 @@ def main():
             i += 1
         out[key] = rec
         print(f"| {key} | `{tmpl}` | {ms:.3f} | {(rd + wr) / 1e9:.3f} | {alg / 1e9:.3f} | "
-              f"{(rd + wr) / alg:.3f} | {inst / n:.2f} | {rec['ipc']:.2f} | {rec['warps_active_pct']:.0f} | "
+              f"{((rd + wr) / alg) if alg else 0:.3f} | {inst / n:.2f} | {rec['ipc']:.2f} | {rec['warps_active_pct']:.0f} | "
               f"{rec['regs']:.0f} |")
     if "--write" in sys.argv:
         d = {"source": "ncu --set full --clock-control none, tools/profile_case.py 28 2 (cfg2: 2^28 u64, "
