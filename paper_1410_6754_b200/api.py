@@ -19,6 +19,7 @@ import numpy as np
 import torch
 
 from . import _lib as L
+from . import ledger
 from .engine import AmsSorter, SortOutput
 from .params import Element, as_params
 
@@ -156,8 +157,11 @@ def _flatten(data, p):
 def ams_sort(net, data, params, scheme: str, seed):
     """Drop-in for ``mlpsort.ams.ams_sort`` (ams.py:271-313).
 
-    ``net`` only needs ``.p`` (the reference's ``Network``); the simulated
-    ledger is not charged (cost accounting is not part of the B200 path).
+    ``net`` needs ``.p`` (the reference's ``Network``).  When it also has a
+    ``ledger`` and ``scheme == "simple"``, the ledger is charged exactly as
+    the reference charges it (phases, per-PE words/messages, modeled time;
+    ``ledger.charge_sort`` from the device run's level records).  Other
+    schemes leave the ledger untouched.
     Elements keep their identity: the returned lists hold the caller's own
     Element objects.  Requires origin tags that increase along the PE-major
     concatenation (as ``generate_input`` produces, bench.py:176), which makes
@@ -196,7 +200,11 @@ def ams_sort(net, data, params, scheme: str, seed):
     dev = torch.device("cuda", torch.cuda.current_device())
     d_keys = torch.from_numpy(keys.view(np.int64)).to(dev)
     d_vals = torch.arange(n, dtype=torch.int64, device=dev)
-    res = ams_sort_tensors(d_keys, sizes, params, seed, vals=d_vals, key_kind=kind, scheme=scheme)
+    charge = scheme == "simple" and getattr(net, "ledger", None) is not None
+    res = ams_sort_tensors(d_keys, sizes, params, seed, vals=d_vals, key_kind=kind, scheme=scheme,
+                           record_splitters=charge)
+    if charge:
+        ledger.charge_sort(net, res.levels, params, params.oversampling_for(n))
     order = res.vals.cpu().numpy()
     out, start = {}, 0
     for pe in range(p):

@@ -1,0 +1,118 @@
+"""Ledger parity: the reference's ``CostLedger`` state
+after ``ams_sort(scheme="simple")`` replayed from per-level facts.
+
+Fixtures: ``tests/golden/ledger/cases.json`` from the real reference
+(``oracle/make_ledger_goldens.py``).  CPU tests feed the ledger replay with the
+oracle's level facts; the GPU test feeds it with the device run's level records
+through the drop-in ``api.ams_sort``.
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from paper_1410_6754_b200 import ledger as LG
+
+CASES_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "ledger",
+                          "cases.json")
+
+
+def cases():
+    with open(CASES_PATH) as f:
+        return json.load(f)
+
+
+def case_keys(c):
+    return np.random.default_rng(c["key_seed"]).integers(0, 2**64, sum(c["sizes"]),
+                                                         dtype=np.uint64)
+
+
+def ledger_state(ledger) -> dict:
+    phases = {
+        name: {"modeled_time": t.modeled_time, "sent_words": list(t.sent_words),
+               "recv_words": list(t.recv_words), "sent_msgs": list(t.sent_msgs),
+               "recv_msgs": list(t.recv_msgs), "coll_words": list(t.coll_words)}
+        for name, t in ledger.phases.items()
+    }
+    return {"modeled_time": ledger.modeled_time, "sent_words": list(ledger.sent_words),
+            "recv_words": list(ledger.recv_words), "sent_msgs": list(ledger.sent_msgs),
+            "recv_msgs": list(ledger.recv_msgs), "coll_words": list(ledger.coll_words),
+            "phases": phases, "phase_summary": ledger.phase_summary()}
+
+
+def assert_ledger(ledger, ref):
+    mine = ledger_state(ledger)
+    assert list(mine["phases"]) == list(ref["phases"])      # phase order too
+    for name in ref["phases"]:
+        for k, v in ref["phases"][name].items():
+            assert mine["phases"][name][k] == v, (name, k)
+    for k in ("sent_words", "recv_words", "sent_msgs", "recv_msgs", "coll_words"):
+        assert mine[k] == ref[k], k
+    assert mine["modeled_time"] == ref["modeled_time"]       # bit-exact float
+    assert mine["phase_summary"] == ref["phase_summary"]
+
+
+@pytest.mark.parametrize("c", cases(), ids=lambda c: c["name"])
+def test_ledger_from_oracle_levels(c):
+    from oracle import ams_oracle as O
+
+    keys = case_keys(c)
+    res = O.ams_sort(keys, c["sizes"], tuple(c["groups"]), oversampling=c["a"],
+                     overpartition=c["b"], imbalance=c["eps"], master_seed=c["master_seed"],
+                     stream=c["stream"])
+    a = c["a"] if c["a"] is not None else O.default_oversampling(len(keys))
+    net = LG.Network(len(c["sizes"]), LG.CostParams(alpha=c["alpha"], beta=c["beta"]))
+    for lv, infos in enumerate(res.levels):
+        for info in infos:
+            LG.charge_group_level(net, info.group_lo, info.hist, info.plan.boundaries,
+                                  c["groups"][lv], c["b"], a, info.splitter_pos)
+    assert_ledger(net.ledger, c["ledger"])
+
+
+def test_stand_in_ledger_semantics():
+    net = LG.Network(3, LG.CostParams(alpha=2.0, beta=0.5))
+    with net.ledger.phase("x"):
+        net.ledger.charge_collective([0, 1], 4, 3.0)
+        net.ledger.record_exchange([2, 0, 0], [0, 0, 2], [1, 0, 0], [0, 0, 1], 3.0)
+    with pytest.raises(RuntimeError):
+        net.ledger.record_exchange([1, 0, 0], [0, 0, 0], [0, 0, 0], [0, 0, 0], 0.0)
+    assert net.ledger.phase_summary()["x"] == {"modeled_time": 6.0, "max_words": 6,
+                                               "max_msgs": 1}
+    with pytest.raises(ValueError):
+        LG.CostParams(alpha=-1.0)
+    with pytest.raises(ValueError):
+        LG.Network(0)
+
+
+def test_bucket_count_mismatch_rejected():
+    hist = np.array([[3, 2], [1, 4]])
+    net = LG.Network(2)
+    with pytest.raises(ValueError):
+        LG.charge_group_level(net, 0, hist, [0, 1, 2], 2, 16, 10.0, [4])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("c", cases(), ids=lambda c: c["name"])
+def test_ledger_through_dropin_api(c):
+    """The drop-in ``ams_sort`` charges the caller's ledger like the reference."""
+    from paper_1410_6754_b200 import api
+    from paper_1410_6754_b200.params import AmsParams, Element, SeedSpec
+
+    keys = case_keys(c)
+    data, off = {}, 0
+    for pe, s in enumerate(c["sizes"]):
+        data[pe] = [Element(int(k), pe, i) for i, k in enumerate(keys[off:off + s])]
+        off += s
+    net = LG.Network(len(c["sizes"]), LG.CostParams(alpha=c["alpha"], beta=c["beta"]))
+    params = AmsParams(tuple(c["groups"]), oversampling=c["a"], overpartition=c["b"],
+                       imbalance=c["eps"])
+    out, reports = api.ams_sort(net, data, params, "simple",
+                                SeedSpec(c["master_seed"], c["stream"]))
+    assert_ledger(net.ledger, c["ledger"])
+    for mine, ref in zip(reports, c["reports"]):
+        for k, v in ref.items():
+            assert mine[k] == v, (k, mine[k], v)
+    flat = sorted(int(k) for k in keys)
+    assert [e.key for pe in range(len(c["sizes"])) for e in out[pe]] == flat
