@@ -39,6 +39,17 @@ CASES = [
 ]
 
 
+OUT_RECORDS = os.path.join(ROOT, "tests", "golden", "ledger", "records.jsonl")
+RECORD_CONFIGS = [
+    dict(pes=16, n_per_pe=2048, levels=1, groups=(16,), seed=3, reps=2, dist="uniform"),
+    dict(pes=64, n_per_pe=256, levels=2, groups=(8, 8), seed=4, dist="zipf:1.1",
+         alpha=0.5, beta=2.0),
+    dict(pes=16, n_per_pe=500, levels=2, groups=(4, 4), seed=5, dist="reverse", a=3.0, b=8,
+         eps=0.3),
+    dict(pes=8, n_per_pe=300, levels=1, groups=(8,), seed=6, dist="equal"),
+]
+
+
 def case_sizes(spec, npe):
     if isinstance(spec, list):
         return list(spec)
@@ -96,6 +107,18 @@ def main():
     with open(OUT, "w") as f:
         json.dump(out, f, separators=(",", ":"))
     print("wrote", OUT)
+
+    # Whole experiment records (bench.py:180-242) for delivery "simple":
+    # what ``run_experiment`` writes as JSONL, ledger phases included.
+    from mlpsort.bench import ExperimentConfig, run_experiment
+    recs = []
+    for kw in RECORD_CONFIGS:
+        cfg = ExperimentConfig(algo="ams", delivery="simple", verify=True, **kw)
+        for rec in run_experiment(cfg):
+            recs.append(json.dumps(rec, separators=(",", ":")))
+    with open(OUT_RECORDS, "w") as f:
+        f.write("\n".join(recs) + "\n")
+    print("wrote", OUT_RECORDS, len(recs))
 
 
 if __name__ == "__main__":

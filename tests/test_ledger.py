@@ -116,3 +116,91 @@ def test_ledger_through_dropin_api(c):
             assert mine[k] == v, (k, mine[k], v)
     flat = sorted(int(k) for k in keys)
     assert [e.key for pe in range(len(c["sizes"])) for e in out[pe]] == flat
+
+
+# --------------------------------------------------------------------------
+# Whole experiment records (bench.py:180-242), delivery "simple"
+
+RECORDS_PATH = os.path.join(os.path.dirname(CASES_PATH), "records.jsonl")
+PHASES = ("splitter_selection", "bucket_processing", "data_delivery", "local_sorting")
+
+
+def records():
+    with open(RECORDS_PATH) as f:
+        return [line for line in f.read().splitlines() if line]
+
+
+def experiment_record(ref: dict, a: float, pe_sizes, reports, net, verdict: str) -> str:
+    """The record ``bench._run_once`` assembles (bench.py:207-242), from our
+    sort's outputs and ledger; ``ref`` supplies the config fields."""
+    pes, n_per_pe = ref["pes"], ref["n_per_pe"]
+    avg = pes * n_per_pe / pes if pes else 0.0
+    levels = [dict(r) for r in reports]
+    for lv in levels:
+        lv["imbalance"] = (lv["max_load"] / avg) if avg else 0.0
+    phases = {name: {"modeled_time": 0.0, "max_words": 0, "max_msgs": 0} for name in PHASES}
+    phases.update(net.ledger.phase_summary())
+    loads = [int(x) for x in pe_sizes]
+    rec = {k: ref[k] for k in ("schema", "algo", "pes", "n_per_pe", "levels", "groups")}
+    rec["a"] = a
+    rec.update({k: ref[k] for k in ("b", "eps", "delivery", "dist", "alpha", "beta", "seed",
+                                    "rep")})
+    rec.update({
+        "verified": verdict,
+        "final_max_load": max(loads),
+        "final_imbalance": (max(loads) / avg) if avg else 0.0,
+        "modeled_time": net.ledger.modeled_time,
+        "max_sent_msgs": max(net.ledger.sent_msgs),
+        "max_recv_msgs": max(net.ledger.recv_msgs),
+        "phases": phases,
+        "level_reports": levels,
+    })
+    return json.dumps(rec, separators=(",", ":"))
+
+
+def record_input(ref):
+    from oracle import ams_oracle as O
+    return O.reference_input(ref["dist"], ref["pes"], ref["n_per_pe"], ref["seed"], ref["rep"])
+
+
+@pytest.mark.parametrize("line", records(), ids=lambda s: json.loads(s)["dist"])
+def test_record_from_oracle_levels(line):
+    from oracle import ams_oracle as O
+
+    ref = json.loads(line)
+    keys = record_input(ref)
+    groups = tuple(ref["groups"])
+    res = O.ams_sort(keys, [ref["n_per_pe"]] * ref["pes"], groups, oversampling=ref["a"],
+                     overpartition=ref["b"], imbalance=ref["eps"], master_seed=ref["seed"],
+                     stream=f"algo/rep{ref['rep']}")
+    net = LG.Network(ref["pes"], LG.CostParams(alpha=ref["alpha"], beta=ref["beta"]))
+    for lv, infos in enumerate(res.levels):
+        for info in infos:
+            LG.charge_group_level(net, info.group_lo, info.hist, info.plan.boundaries,
+                                  groups[lv], ref["b"], ref["a"], info.splitter_pos)
+    verdict = "pass" if np.array_equal(res.keys, np.sort(keys)) else "fail"
+    assert experiment_record(ref, ref["a"], res.pe_sizes, res.reports, net, verdict) == line
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("line", records(), ids=lambda s: json.loads(s)["dist"])
+def test_record_through_dropin_api(line):
+    """``run_experiment``'s record, byte for byte, with the sort on the GPU."""
+    from paper_1410_6754_b200 import api
+    from paper_1410_6754_b200.params import AmsParams, Element, SeedSpec
+
+    ref = json.loads(line)
+    keys = record_input(ref)
+    npe = ref["n_per_pe"]
+    data = {pe: [Element(int(k), pe, i) for i, k in enumerate(keys[pe * npe:(pe + 1) * npe])]
+            for pe in range(ref["pes"])}
+    net = LG.Network(ref["pes"], LG.CostParams(alpha=ref["alpha"], beta=ref["beta"]))
+    params = AmsParams(tuple(ref["groups"]), oversampling=ref["a"], overpartition=ref["b"],
+                       imbalance=ref["eps"])
+    out, reports = api.ams_sort(net, data, params, "simple",
+                                SeedSpec(ref["seed"], "algo").derive(f"rep{ref['rep']}"))
+    flat = [e for pe in range(ref["pes"]) for e in out[pe]]
+    expected = sorted(e for seq in data.values() for e in seq)
+    verdict = "pass" if flat == expected else "fail"
+    sizes = [len(out[pe]) for pe in range(ref["pes"])]
+    assert experiment_record(ref, ref["a"], sizes, reports, net, verdict) == line
