@@ -266,6 +266,9 @@ typedef struct {
   int key_kind;                        /* AMS_KEY_U64 / AMS_KEY_I64 / AMS_KEY_F64 */
   int with_stats;                      /* fill the exchange maxima of the reports */
   int scheme;                          /* AMS_SCHEME_SIMPLE / _DETERMINISTIC / _PERMUTED / _RANDOMIZED */
+  int record_holders;                  /* keep, per level and PE, how many splitters were drawn from
+                                          the PE (the ledger's extract_by_ranks charge,
+                                          fastsort.py:111-130; one small D2H per level) */
 } ams_params_t;
 
 /* One level's report (ams.py:294-308; exchange maxima simnet.py:109-124). */
@@ -304,6 +307,10 @@ int ams_run_level_at(ams_ctx_t* ctx, uint64_t run, int level, int32_t* group_fir
                      uint64_t* sizes_before, uint64_t* drawn, int32_t* nb, uint32_t* seg_hist,
                      uint64_t* boundaries, uint64_t* loads, uint64_t* max_load, uint64_t* new_sizes,
                      uint64_t* stats);
+/* Per PE [P]: number of that level's splitters drawn from the PE's sample
+ * (replaces the holder bookkeeping of extract_by_ranks, fastsort.py:111-130,
+ * for CostLedger parity); needs params.record_holders. */
+int ams_run_level_holders_at(ams_ctx_t* ctx, uint64_t run, int level, uint32_t* holders);
 
 #ifdef __cplusplus
 }

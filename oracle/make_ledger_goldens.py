@@ -36,6 +36,16 @@ CASES = [
     ("three_level_16", 16, 256, (2, 2, 4), None, 16, 0.3, 15, 3, 1.0, 0.5),
     ("ragged_6", [0, 37, 5, 200, 1, 90], None, (2, 3), 2.0, 4, 0.2, 16, 9, 1.0, 1.0),
     ("single_pe", 1, 1000, (1,), None, 16, 0.1, 17, 2, 1.0, 1.0),
+    # other delivery schemes (scheme, dist)
+    ("det_two_level_64", 64, 512, (8, 8), None, 16, 0.1, 12, 1, 1.0, 1.0, "deterministic"),
+    ("det_non_pow2_12", 12, 300, (3, 4), 4.0, 4, 0.2, 14, 7, 2.5, 0.75, "deterministic"),
+    ("det_sorted_16", 16, 400, (4, 4), None, 8, 0.2, 18, 4, 0.3, 1.7, "deterministic", "sorted"),
+    ("det_reverse_8", 8, 333, (8,), None, 16, 0.2, 19, 6, 1.0, 1.0, "deterministic", "reverse"),
+    ("det_three_level_16", 16, 256, (2, 2, 4), None, 16, 0.3, 15, 3, 1.0, 0.5, "deterministic"),
+    ("perm_two_level_64", 64, 512, (8, 8), None, 16, 0.1, 12, 1, 1.0, 1.0, "permuted"),
+    ("perm_sorted_16", 16, 400, (4, 4), None, 8, 0.2, 18, 4, 0.3, 1.7, "permuted", "sorted"),
+    ("perm_ragged_6", [0, 37, 5, 200, 1, 90], None, (2, 3), 2.0, 4, 0.2, 16, 9, 1.0, 1.0,
+     "permuted"),
 ]
 
 
@@ -47,6 +57,13 @@ RECORD_CONFIGS = [
     dict(pes=16, n_per_pe=500, levels=2, groups=(4, 4), seed=5, dist="reverse", a=3.0, b=8,
          eps=0.3),
     dict(pes=8, n_per_pe=300, levels=1, groups=(8,), seed=6, dist="equal"),
+    # the CLI / bench default delivery (bench.py:50)
+    dict(pes=16, n_per_pe=1024, levels=2, groups=(4, 4), seed=7, dist="uniform",
+         delivery="deterministic"),
+    dict(pes=32, n_per_pe=256, levels=2, groups=(4, 8), seed=8, dist="sorted",
+         delivery="deterministic"),
+    dict(pes=16, n_per_pe=512, levels=2, groups=(4, 4), seed=9, dist="uniform",
+         delivery="permuted"),
 ]
 
 
@@ -56,8 +73,13 @@ def case_sizes(spec, npe):
     return [npe] * spec
 
 
-def case_keys(sizes, seed):
-    return np.random.default_rng(seed).integers(0, 2**64, sum(sizes), dtype=np.uint64)
+def case_keys(sizes, seed, dist="uniform"):
+    n = sum(sizes)
+    if dist == "sorted":
+        return np.arange(n, dtype=np.uint64)
+    if dist == "reverse":
+        return (n - 1 - np.arange(n)).astype(np.uint64)
+    return np.random.default_rng(seed).integers(0, 2**64, n, dtype=np.uint64)
 
 
 def ledger_state(ledger) -> dict:
@@ -86,9 +108,11 @@ def main():
     from mlpsort.simnet import CostParams, Network
 
     out = []
-    for name, spec, npe, groups, a, b, eps, kseed, mseed, alpha, beta in CASES:
+    for name, spec, npe, groups, a, b, eps, kseed, mseed, alpha, beta, *rest in CASES:
+        scheme = rest[0] if rest else "simple"
+        dist = rest[1] if len(rest) > 1 else "uniform"
         sizes = case_sizes(spec, npe)
-        keys = case_keys(sizes, kseed)
+        keys = case_keys(sizes, kseed, dist)
         data, off = {}, 0
         for pe, s in enumerate(sizes):
             data[pe] = [Element(int(k), pe, i) for i, k in enumerate(keys[off:off + s])]
@@ -96,11 +120,11 @@ def main():
         net = Network(len(sizes), CostParams(alpha=alpha, beta=beta))
         params = AmsParams(groups, oversampling=a, overpartition=b, imbalance=eps)
         seed = SeedSpec(mseed, "algo").derive("rep0")
-        _, reports = ams_sort(net, data, params, "simple", seed)
+        _, reports = ams_sort(net, data, params, scheme, seed)
         out.append({
             "name": name, "sizes": sizes, "groups": list(groups), "a": a, "b": b,
             "eps": eps, "key_seed": kseed, "master_seed": mseed, "stream": "algo/rep0",
-            "alpha": alpha, "beta": beta, "reports": reports,
+            "alpha": alpha, "beta": beta, "scheme": scheme, "dist": dist, "reports": reports,
             "ledger": ledger_state(net.ledger),
         })
         print(name, net.ledger.modeled_time)
@@ -108,12 +132,12 @@ def main():
         json.dump(out, f, separators=(",", ":"))
     print("wrote", OUT)
 
-    # Whole experiment records (bench.py:180-242) for delivery "simple":
+    # Whole experiment records (bench.py:180-242):
     # what ``run_experiment`` writes as JSONL, ledger phases included.
     from mlpsort.bench import ExperimentConfig, run_experiment
     recs = []
     for kw in RECORD_CONFIGS:
-        cfg = ExperimentConfig(algo="ams", delivery="simple", verify=True, **kw)
+        cfg = ExperimentConfig(algo="ams", verify=True, **{"delivery": "simple", **kw})
         for rec in run_experiment(cfg):
             recs.append(json.dumps(rec, separators=(",", ":")))
     with open(OUT_RECORDS, "w") as f:

@@ -63,6 +63,7 @@ _SIGNATURES = {
     "ams_run_id": (C.c_uint64, [_P]),
     "ams_run_level_dims_at": (_I, [_P, C.c_uint64, _I, _P, _P, _P, _P, _P]),
     "ams_run_level_at": (_I, [_P, C.c_uint64, _I] + [_P] * 11),
+    "ams_run_level_holders_at": (_I, [_P, C.c_uint64, _I, _P]),
     "ams_level_scatter_ex": (_I, [_P, _P, _P, _I, _P, _P, _I, _P, _P, _I, _I, _I]),
     "ams_final_sort_buckets": (_I, [_P, _P, _P, _P, _I, _I, _P, _P, _P, _P]),
     "ams_get_minmax": (_I, [_P, _P]),
@@ -84,7 +85,7 @@ class ParamsT(C.Structure):
                 ("oversampling", C.c_double), ("overpartition", C.c_int),
                 ("imbalance", C.c_double), ("master_seed", C.c_int64),
                 ("stream_id", C.c_char_p), ("key_kind", C.c_int), ("with_stats", C.c_int),
-                ("scheme", C.c_int)]
+                ("scheme", C.c_int), ("record_holders", C.c_int)]
 
 
 class LevelReportT(C.Structure):
@@ -431,6 +432,12 @@ class Context:
                  "boundaries", "loads", "max_load", "new_sizes", "stats")
         check(lib.ams_run_level_at(self.h, int(run), level, *[ptr(d[k]) for k in order]))
         return d
+
+    def run_level_holders(self, level: int, npe: int, run: int = 0) -> np.ndarray:
+        """Per PE: splitters of that level drawn from the PE (record_holders runs)."""
+        out = np.zeros(max(npe, 1), np.uint32)
+        check(lib.ams_run_level_holders_at(self.h, int(run), level, out.ctypes.data))
+        return out[:npe]
 
     def map_keys(self, src, dst, n, from_kind, to_kind):
         check(lib.ams_map_keys(self.h, ptr(src), ptr(dst), n, from_kind, to_kind))

@@ -21,7 +21,7 @@ import torch
 from . import _lib as L
 from . import ledger
 from .engine import AmsSorter, SortOutput
-from .params import Element, as_params
+from .params import Element, as_params, as_seed
 
 _SORTERS: dict = {}
 
@@ -46,13 +46,14 @@ def _check_scheme(scheme: str):
 
 def ams_sort_tensors(keys: torch.Tensor, pe_sizes, params, seed, vals: torch.Tensor | None = None,
                      scheme: str = "simple", key_kind=None, out=None, out_vals=None,
-                     record_splitters: bool = False) -> SortOutput:
+                     record_splitters: bool = False, record_holders: bool = False) -> SortOutput:
     """Sort device keys laid out PE-major (``pe_sizes``); returns a
     :class:`~paper_1410_6754_b200.engine.SortOutput`."""
     _check_scheme(scheme)
     return get_sorter(keys.device).sort(keys, pe_sizes, params, seed, vals=vals, out=out,
                                         out_vals=out_vals, key_kind=key_kind,
-                                        record_splitters=record_splitters, scheme=scheme)
+                                        record_splitters=record_splitters, scheme=scheme,
+                                        record_holders=record_holders)
 
 
 def ams_sort_host(keys: np.ndarray, pe_sizes, params, seed, vals: np.ndarray | None = None,
@@ -158,10 +159,11 @@ def ams_sort(net, data, params, scheme: str, seed):
     """Drop-in for ``mlpsort.ams.ams_sort`` (ams.py:271-313).
 
     ``net`` needs ``.p`` (the reference's ``Network``).  When it also has a
-    ``ledger`` and ``scheme == "simple"``, the ledger is charged exactly as
+    ``ledger`` and ``scheme`` is "simple", "deterministic" or "permuted",
+    the ledger is charged exactly as
     the reference charges it (phases, per-PE words/messages, modeled time;
-    ``ledger.charge_sort`` from the device run's level records).  Other
-    schemes leave the ledger untouched.
+    ``ledger.charge_sort`` from the device run's level records).  The
+    "randomized" scheme leaves the ledger untouched.
     Elements keep their identity: the returned lists hold the caller's own
     Element objects.  Requires origin tags that increase along the PE-major
     concatenation (as ``generate_input`` produces, bench.py:176), which makes
@@ -200,11 +202,12 @@ def ams_sort(net, data, params, scheme: str, seed):
     dev = torch.device("cuda", torch.cuda.current_device())
     d_keys = torch.from_numpy(keys.view(np.int64)).to(dev)
     d_vals = torch.arange(n, dtype=torch.int64, device=dev)
-    charge = scheme == "simple" and getattr(net, "ledger", None) is not None
+    charge = scheme in ledger.CHARGED_SCHEMES and getattr(net, "ledger", None) is not None
     res = ams_sort_tensors(d_keys, sizes, params, seed, vals=d_vals, key_kind=kind, scheme=scheme,
-                           record_splitters=charge)
+                           record_holders=charge)
     if charge:
-        ledger.charge_sort(net, res.levels, params, params.oversampling_for(n))
+        ledger.charge_sort(net, res.levels, params, params.oversampling_for(n), scheme,
+                           *as_seed(seed))
     order = res.vals.cpu().numpy()
     out, start = {}, 0
     for pe in range(p):

@@ -1,6 +1,7 @@
 // C ABI of the AMS-sort hot path: device context, metadata staging and the
 // level / final-sort entry points declared in include/ams_b200.h.
 #include <algorithm>
+#include <unordered_map>
 #include <chrono>
 #include <cstdio>
 #include <cmath>
@@ -195,6 +196,7 @@ struct ams_ctx {
     std::vector<int32_t> group_first, group_npe, nb;
     std::vector<uint64_t> sizes_before, drawn, boundaries, loads, max_load, new_sizes, stats;
     std::vector<uint32_t> hist;
+    std::vector<uint32_t> holders;  // per PE: splitters drawn from it (record_holders)
     bool has_stats = false;
   };
   std::vector<LevelRec> run_levels;
@@ -1195,6 +1197,34 @@ struct HostTrace {
 };
 }  // namespace
 
+// Per PE, how many of its level's splitters were drawn from it (host
+// bookkeeping for the ledger; one D2H of the sample tags and of every
+// group's splitter tags).
+static int splitter_holders(ams_ctx_t* c, int G, uint64_t S, const uint64_t* soff,
+                            const uint64_t* idx, const uint64_t* offs, int p,
+                            std::vector<uint32_t>* out) {
+  std::vector<uint32_t> spos(S);
+  AMS_CK(cudaMemcpyAsync(spos.data(), c->s_pos.p, 4 * S, cudaMemcpyDeviceToHost, c->stream));
+  AMS_CK(cudaStreamSynchronize(c->stream));
+  out->assign(p, 0);
+  std::vector<uint32_t> pos(AMS_MAX_BUCKETS);
+  for (int g = 0; g < G; ++g) {
+    int nspl = 0;
+    int rc = ams_read_splitters(c, g, nullptr, pos.data(), &nspl);
+    if (rc) return rc;
+    std::unordered_map<uint32_t, int> pe_of;
+    pe_of.reserve(2 * (soff[g + 1] - soff[g]));
+    for (uint64_t i = soff[g]; i < soff[g + 1]; ++i)
+      pe_of[spos[i]] = (int)(std::upper_bound(offs, offs + p + 1, idx[i]) - offs) - 1;
+    for (int j = 0; j < nspl; ++j) {
+      auto it = pe_of.find(pos[j]);
+      if (it == pe_of.end()) return set_error(AMS_EINTERNAL, "splitter not found in the sample");
+      (*out)[it->second] += 1;
+    }
+  }
+  return AMS_OK;
+}
+
 int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* pe_sizes,
                  const void* keys, const void* vals, void* out, void* out_vals,
                  uint64_t* out_pe_sizes, ams_level_report_t* reports) {
@@ -1303,6 +1333,14 @@ int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* p
     if ((rc = ams_level_splitters(c, G, c->s_keys.as<uint64_t>(), c->s_pos.as<uint32_t>(),
                                   soff.data(), nb.data())))
       return rc;
+    std::vector<uint32_t> holders;
+    if (prm->record_holders && S) {
+      // Member each splitter was drawn from (the holder that contributes it
+      // to extract_by_ranks, fastsort.py:111-130): splitters carry the
+      // sample element's unique position (or origin tag) value.
+      if ((rc = splitter_holders(c, G, S, soff.data(), idx.data(), offs.data(), p, &holders)))
+        return rc;
+    }
     std::vector<int32_t> seg_group(p);
     std::vector<int64_t> posbase(G);
     for (int g = 0; g < G; ++g) {
@@ -1314,6 +1352,7 @@ int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* p
     rec.r = r; rec.G = G; rec.P = p; rec.nb_stride = nb_stride;
     rec.group_first = gf; rec.group_npe = gn; rec.nb = nb;
     rec.sizes_before = sizes; rec.drawn = drawn;
+    rec.holders = std::move(holders);
     rec.hist.assign((size_t)p * nb_stride, 0);
     c->level_tags = tie_tags;
     tr.mark("sample");
@@ -1559,6 +1598,23 @@ int ams_run_level_at(ams_ctx_t* c, uint64_t run, int level, int32_t* group_first
   cp(group_first, L.group_first); cp(group_npe, L.group_npe); cp(sizes_before, L.sizes_before);
   cp(drawn, L.drawn); cp(nb, L.nb); cp(seg_hist, L.hist); cp(boundaries, L.boundaries);
   cp(loads, L.loads); cp(max_load, L.max_load); cp(new_sizes, L.new_sizes); cp(stats, L.stats);
+  return AMS_OK;
+}
+
+int ams_run_level_holders_at(ams_ctx_t* c, uint64_t run, int level, uint32_t* holders) {
+  if (!c || !holders) return set_error(AMS_EINVAL, "null argument");
+  const std::vector<ams_ctx::LevelRec>* rl = run_records(c, run);
+  if (!rl) return set_error(AMS_EINVAL, "records of that run are no longer kept");
+  if (level < 0 || level >= (int)rl->size()) return set_error(AMS_EINVAL, "no such level");
+  const ams_ctx::LevelRec& L = (*rl)[level];
+  if (L.holders.empty()) {
+    std::memset(holders, 0, 4 * (size_t)L.P);  // no sample (n == 0) or not recorded
+    bool any = false;
+    for (uint64_t d : L.drawn) any = any || d;
+    if (any) return set_error(AMS_EINVAL, "splitter holders were not recorded (record_holders)");
+    return AMS_OK;
+  }
+  std::memcpy(holders, L.holders.data(), 4 * L.holders.size());
   return AMS_OK;
 }
 

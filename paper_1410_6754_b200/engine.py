@@ -63,6 +63,7 @@ class LevelRecord:
     new_sizes: np.ndarray         # (P_total,)
     stats: np.ndarray | None      # (G, 4) exchange stats
     splitters: list = field(default_factory=list)  # per group (keys, pos) if recorded
+    holders: np.ndarray | None = None  # per PE: splitters drawn from it (record_holders)
 
     def report(self) -> dict:
         """The per-level dict ams_sort returns (ams.py:296-308)."""
@@ -159,7 +160,8 @@ class AmsSorter:
     # -- main entry ---------------------------------------------------------
     def sort(self, keys: torch.Tensor, pe_sizes, params: AmsParams, seed, vals=None, out=None,
              out_vals=None, key_kind=None, record_splitters: bool = False,
-             with_stats: bool = True, scheme: str = "simple") -> SortOutput:
+             with_stats: bool = True, scheme: str = "simple",
+             record_holders: bool = False) -> SortOutput:
         """Sort ``keys`` (1-D, PE-major: PE i owns the next ``pe_sizes[i]``
         keys) exactly as ams_sort(scheme) orders them ("simple" or
         "deterministic"); returns the sorted keys (concatenation of per-PE
@@ -205,7 +207,7 @@ class AmsSorter:
             # The whole level loop in C++ (ams_sort_run); same steps as below.
             return self._sort_native(keys, vals, ret_out, ret_vals, out, out_vals, sizes, params,
                                      master, stream_id, kind, with_stats, launches0, n,
-                                     SCHEMES[scheme])
+                                     SCHEMES[scheme], record_holders)
         a = params.oversampling_for(n)                               # ams.py:278-280
         eps_l = params.per_level_imbalance()
         b = params.overpartition
@@ -273,7 +275,7 @@ class AmsSorter:
         return SortOutput(ret_out, ret_vals, sizes, levels, self.ctx.launches - launches0)
 
     def _sort_native(self, keys, vals, ret_out, ret_vals, out, out_vals, sizes, params, master,
-                     stream_id, kind, with_stats, launches0, n, scheme=0):
+                     stream_id, kind, with_stats, launches0, n, scheme=0, record_holders=False):
         prm = L.ParamsT()
         gc = tuple(params.group_counts)
         if len(gc) > L.MAX_LEVELS:
@@ -289,6 +291,7 @@ class AmsSorter:
         prm.key_kind = int(kind)
         prm.with_stats = int(bool(with_stats))
         prm.scheme = int(scheme)
+        prm.record_holders = int(bool(record_holders))
         final_sizes, _ = self.ctx.sort_run(prm, sizes, keys if n else None,
                                            vals if n else None, out if n else None,
                                            out_vals if n else None)
@@ -305,5 +308,7 @@ class AmsSorter:
                                         d["drawn"], d["nb"].astype(np.int64), d["seg_hist"],
                                         d["boundaries"], d["loads"], d["max_load"],
                                         load_budget(n_g, r, eps_l), d["new_sizes"], d["stats"]))
+                if record_holders:
+                    recs[-1].holders = ctx.run_level_holders(lv, len(d["sizes_before"]), run)
             return recs
         return SortOutput(ret_out, ret_vals, final_sizes, levels, self.ctx.launches - launches0)

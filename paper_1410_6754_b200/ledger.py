@@ -12,8 +12,8 @@ from those, in the reference's call order (so float sums match bit for bit),
 onto any object with the reference ledger's methods — the user's own
 ``mlpsort.simnet.Network``, or the stand-in :class:`Network` below.
 
-Scope: ``scheme="simple"`` (delivery.py:138-180).  Host bookkeeping only; no
-device work happens here.
+Scope: schemes "simple", "deterministic" and "permuted" (delivery.py:138-306).
+Host bookkeeping only; no device work happens here.
 """
 
 from __future__ import annotations
@@ -166,14 +166,122 @@ def _charge_gossip(ledger, alpha, beta, members, counts) -> None:
         ledger.charge_collective(members, per, max(per.values()) * beta + _log2_ceil(n) * alpha)
 
 
-def charge_group_level(net, lo: int, hist: np.ndarray, boundaries, r: int, b: int, a: float,
-                       splitter_pos) -> None:
-    """Charges of one ``ams_level`` call (ams.py:214-268) on the group of PEs
-    ``lo .. lo+P-1`` with scheme "simple".
+CHARGED_SCHEMES = ("simple", "deterministic", "permuted")
 
-    hist:        (P, br) per-member bucket histogram (row sums = member sizes)
-    boundaries:  plan boundaries (r+1)
-    splitter_pos: position in the group buffer of each splitter (br-1)
+
+def _exchange(net, lo: int, P: int, msgs) -> None:
+    """``Network.exchange`` accounting (simnet.py:294-335) of one group's
+    messages ``(src member, dest member, words)``; self-messages are free."""
+    p_all = net.p
+    sw, rw = [0] * p_all, [0] * p_all
+    sm, rm = [0] * p_all, [0] * p_all
+    for s, d, w in msgs:
+        if w == 0 or s == d:
+            continue
+        sw[lo + s] += w
+        rw[lo + d] += w
+        sm[lo + s] += 1
+        rm[lo + d] += 1
+    members = range(lo, lo + P)
+    h = max(max(sw[pe] for pe in members), max(rw[pe] for pe in members))
+    m = max(max(sm[pe] for pe in members), max(rm[pe] for pe in members))
+    net.ledger.record_exchange(sw, rw, sm, rm, h * net.params.beta + m * net.params.alpha)
+
+
+def _simple_messages(pieces: np.ndarray, r: int):
+    """deliver_simple's slices (delivery.py:78-104, 151-180): piece (j, g) at
+    numbers [start, start+size) of subgroup g, cut along the quota slots."""
+    P = pieces.shape[0]
+    sub = P // r
+    starts = np.cumsum(pieces, axis=0) - pieces                      # source order
+    totals = pieces.sum(axis=0)
+    t = np.arange(sub + 1, dtype=np.int64)
+    msgs = []
+    for g in range(r):
+        cut = (int(totals[g]) * t) // sub
+        s0 = starts[:, g][:, None]
+        s1 = (starts[:, g] + pieces[:, g])[:, None]
+        take = np.minimum(s1, cut[None, 1:]) - np.maximum(s0, cut[None, :-1])
+        for j, d in zip(*np.nonzero(take > 0)):
+            msgs.append((int(j), g * sub + int(d), int(take[j, d])))
+    return msgs
+
+
+def _planned_messages(pieces: np.ndarray, r: int, slices: np.ndarray, new_sizes):
+    """Messages of a planner's slices (src offset in the group's simple
+    layout, dst offset in the new member arrays, length), each tagged with its
+    piece (j, g): [(src member, dest member, words, j, g)]."""
+    P = pieces.shape[0]
+    order = [(g, j) for g in range(r) for j in range(P)]             # (g, j, b) layout
+    flat = np.array([pieces[j, g] for g, j in order], dtype=np.int64)
+    pstart = np.concatenate([[0], np.cumsum(flat)])[:-1]
+    nz = np.nonzero(flat)[0]
+    noff = np.concatenate([[0], np.cumsum(np.asarray(new_sizes, dtype=np.int64))])
+    out = []
+    for src, dst, ln in np.asarray(slices, dtype=np.int64).reshape(-1, 3):
+        k = nz[np.searchsorted(pstart[nz], src, side="right") - 1]
+        g, j = order[k]
+        d = int(np.searchsorted(noff, dst, side="right") - 1)
+        out.append((j, d, int(ln), j, g))
+    return out
+
+
+def _charge_delivery(net, lo: int, pieces: np.ndarray, r: int, scheme: str,
+                     master_seed, level_stream) -> None:
+    ledger, alpha = net.ledger, net.params.alpha
+    P = pieces.shape[0]
+    members = list(range(lo, lo + P))
+    if scheme == "simple":                                           # delivery.py:151-180
+        _charge_vector(ledger, alpha, net.params.beta, members, r)
+        _exchange(net, lo, P, _simple_messages(pieces, r))
+        return
+    from . import _lib as L
+    if scheme == "permuted":                                         # delivery.py:183-185
+        new_sizes, slices, _ = L.deliver_permuted(pieces, master_seed, level_stream, False)
+        _charge_vector(ledger, alpha, net.params.beta, members, r)
+        _exchange(net, lo, P, [m[:3] for m in _planned_messages(pieces, r, slices, new_sizes)])
+        return
+    if scheme != "deterministic":
+        raise ValueError(f"ledger charges of scheme {scheme!r} are not modelled")
+    # deliver_deterministic (delivery.py:188-306)
+    new_sizes, slices, _ = L.deliver_deterministic(pieces, lo, False)
+    msgs = _planned_messages(pieces, r, slices, new_sizes)
+    n = int(pieces.sum())
+    sub = P // r
+    _charge_vector(ledger, alpha, net.params.beta, members, 2 * r)
+    large = [(j, g) for g in range(r) for j in range(P)
+             if pieces[j, g] > 0 and not int(pieces[j, g]) * 2 * P * r <= n]
+    # descriptors (g, idx, size) to coordinator sub[idx // r], bundled per edge
+    desc: dict = {}
+    for j, g in large:
+        key = (j, g * sub + j // r)
+        desc[key] = desc.get(key, 0) + 3
+    _exchange(net, lo, P, [(s, d, w) for (s, d), w in sorted(desc.items())])
+    if sub > 1:                                                      # group-local merge
+        ledger.charge_collective(members, 0, alpha * _log2_ceil(sub))
+    # replies (g, dest, offset, length) per cut, coordinator -> origin, bundled
+    cuts: dict = {}
+    for _, _, _, j, g in msgs:
+        cuts[(j, g)] = cuts.get((j, g), 0) + 1
+    rep: dict = {}
+    for j, g in large:
+        key = (g * sub + j // r, j)
+        rep[key] = rep.get(key, 0) + 4 * cuts[(j, g)]
+    _exchange(net, lo, P, [(s, d, w) for (s, d), w in sorted(rep.items())])
+    _exchange(net, lo, P, [m[:3] for m in msgs])
+
+
+def charge_group_level(net, lo: int, hist: np.ndarray, boundaries, r: int, b: int, a: float,
+                       splitter_pos=None, holders=None, scheme: str = "simple",
+                       master_seed: int | None = None, level_stream: str | None = None) -> None:
+    """Charges of one ``ams_level`` call (ams.py:214-268) on the group of PEs
+    ``lo .. lo+P-1``.
+
+    hist:         (P, br) per-member bucket histogram (row sums = member sizes)
+    boundaries:   plan boundaries (r+1)
+    splitter_pos: position in the group buffer of each splitter (br-1), or
+    holders:      per member, how many splitters were drawn from it
+    level_stream: "{stream}/L{level}-g{lo}" (the permuted scheme's Feistel orders)
     """
     ledger, alpha, beta = net.ledger, net.params.alpha, net.params.beta
     hist = np.asarray(hist, dtype=np.int64)
@@ -210,13 +318,15 @@ def charge_group_level(net, lo: int, hist: np.ndarray, boundaries, r: int, b: in
                                    int(takes[idx].sum()))
                 # extract_by_ranks (fastsort.py:111-130): the holders of the
                 # wanted ranks gossip them to every member.
-                pos = np.asarray(splitter_pos, dtype=np.int64)
-                if len(pos) != len(wanted):
-                    raise ValueError("one splitter position per wanted rank expected")
-                offs = np.concatenate([[0], np.cumsum(sizes)])
-                holder = np.searchsorted(offs, pos, side="right") - 1
-                contrib = np.bincount(holder, minlength=P)[:P]
-                _charge_gossip(ledger, alpha, beta, members, contrib)
+                if holders is None:
+                    pos = np.asarray(splitter_pos, dtype=np.int64)
+                    offs = np.concatenate([[0], np.cumsum(sizes)])
+                    holders = np.bincount(np.searchsorted(offs, pos, side="right") - 1,
+                                          minlength=P)[:P]
+                holders = np.asarray(holders, dtype=np.int64)
+                if len(holders) != P or int(holders.sum()) != len(wanted):
+                    raise ValueError("one splitter holder per wanted rank expected")
+                _charge_gossip(ledger, alpha, beta, members, holders)
             else:                                                    # ams.py:195-197
                 ledger.charge_collective(
                     members, drawn, 2 * (drawn * beta + _log2_ceil(P) * alpha))
@@ -224,49 +334,31 @@ def charge_group_level(net, lo: int, hist: np.ndarray, boundaries, r: int, b: in
     with ledger.phase(PHASE_BUCKETS):                                # ams.py:236-237
         _charge_vector(ledger, alpha, beta, members, br)
 
-    with ledger.phase(PHASE_DELIVERY):                               # delivery.py:138-180
-        _charge_vector(ledger, alpha, beta, members, r)
+    with ledger.phase(PHASE_DELIVERY):
         bnd = np.asarray(boundaries, dtype=np.int64)
         pieces = np.stack([hist[:, bnd[g]:bnd[g + 1]].sum(axis=1) for g in range(r)], axis=1)
-        starts = np.cumsum(pieces, axis=0) - pieces                  # source order
-        totals = pieces.sum(axis=0)
-        sub = P // r
-        p_all = net.p
-        sw, rw = [0] * p_all, [0] * p_all
-        sm, rm = [0] * p_all, [0] * p_all
-        t = np.arange(sub + 1, dtype=np.int64)
-        src = np.arange(P)
-        for g in range(r):
-            cut = (int(totals[g]) * t) // sub                        # quota slots
-            s0 = starts[:, g][:, None]
-            s1 = (starts[:, g] + pieces[:, g])[:, None]
-            take = np.minimum(s1, cut[None, 1:]) - np.maximum(s0, cut[None, :-1])
-            take = np.where(take > 0, take, 0)
-            dest = g * sub + np.arange(sub)
-            take[src[:, None] == dest[None, :]] = 0                  # self-messages are free
-            for j, d in zip(*np.nonzero(take)):
-                w = int(take[j, d])
-                s_pe, d_pe = lo + int(j), lo + int(dest[d])
-                sw[s_pe] += w
-                rw[d_pe] += w
-                sm[s_pe] += 1
-                rm[d_pe] += 1
-        h = max(max(sw[pe] for pe in members), max(rw[pe] for pe in members))
-        m = max(max(sm[pe] for pe in members), max(rm[pe] for pe in members))
-        ledger.record_exchange(sw, rw, sm, rm, h * beta + m * alpha)  # simnet.py:294-335
+        _charge_delivery(net, lo, pieces, r, scheme, master_seed, level_stream)
 
 
-def charge_sort(net, levels, params, a: float) -> None:
+def charge_sort(net, levels, params, a: float, scheme: str = "simple",
+                master_seed: int | None = None, stream_id: str | None = None) -> None:
     """Every level's charges (ams.py:284-290), group by group in PE order, from
-    the device run's level records (recorded splitters required)."""
+    the device run's level records (splitter holders or recorded splitters)."""
+    if scheme not in CHARGED_SCHEMES:
+        raise ValueError(f"ledger charges of scheme {scheme!r} are not modelled")
     b = params.overpartition
     for rec in levels:
-        if not rec.splitters:
-            raise ValueError("ledger charging needs the recorded splitters of every level")
+        if rec.holders is None and not rec.splitters:
+            raise ValueError("ledger charging needs each level's splitter holders")
         for gi in range(len(rec.group_first)):
             lo, P = int(rec.group_first[gi]), int(rec.group_npe[gi])
             br = int(rec.bucket_count[gi])
             hist = np.asarray(rec.seg_hist[lo:lo + P, :br], dtype=np.int64)
-            _, pos = rec.splitters[gi]
-            charge_group_level(net, lo, hist, rec.boundaries[gi], rec.r, b, a,
-                               np.asarray(pos, dtype=np.int64)[:max(br - 1, 0)])
+            if rec.holders is not None:
+                kw = {"holders": np.asarray(rec.holders[lo:lo + P], dtype=np.int64)}
+            else:
+                _, pos = rec.splitters[gi]
+                kw = {"splitter_pos": np.asarray(pos, dtype=np.int64)[:max(br - 1, 0)]}
+            charge_group_level(net, lo, hist, rec.boundaries[gi], rec.r, b, a, scheme=scheme,
+                               master_seed=master_seed,
+                               level_stream=f"{stream_id}/L{rec.level}-g{lo}", **kw)

@@ -25,8 +25,13 @@ def cases():
 
 
 def case_keys(c):
-    return np.random.default_rng(c["key_seed"]).integers(0, 2**64, sum(c["sizes"]),
-                                                         dtype=np.uint64)
+    n = sum(c["sizes"])
+    dist = c.get("dist", "uniform")
+    if dist == "sorted":
+        return np.arange(n, dtype=np.uint64)
+    if dist == "reverse":
+        return (n - 1 - np.arange(n)).astype(np.uint64)
+    return np.random.default_rng(c["key_seed"]).integers(0, 2**64, n, dtype=np.uint64)
 
 
 def ledger_state(ledger) -> dict:
@@ -61,13 +66,15 @@ def test_ledger_from_oracle_levels(c):
     keys = case_keys(c)
     res = O.ams_sort(keys, c["sizes"], tuple(c["groups"]), oversampling=c["a"],
                      overpartition=c["b"], imbalance=c["eps"], master_seed=c["master_seed"],
-                     stream=c["stream"])
+                     stream=c["stream"], scheme=c["scheme"])
     a = c["a"] if c["a"] is not None else O.default_oversampling(len(keys))
     net = LG.Network(len(c["sizes"]), LG.CostParams(alpha=c["alpha"], beta=c["beta"]))
     for lv, infos in enumerate(res.levels):
         for info in infos:
             LG.charge_group_level(net, info.group_lo, info.hist, info.plan.boundaries,
-                                  c["groups"][lv], c["b"], a, info.splitter_pos)
+                                  c["groups"][lv], c["b"], a, info.splitter_pos,
+                                  scheme=c["scheme"], master_seed=c["master_seed"],
+                                  level_stream=f"{c['stream']}/L{lv}-g{info.group_lo}")
     assert_ledger(net.ledger, c["ledger"])
 
 
@@ -108,7 +115,7 @@ def test_ledger_through_dropin_api(c):
     net = LG.Network(len(c["sizes"]), LG.CostParams(alpha=c["alpha"], beta=c["beta"]))
     params = AmsParams(tuple(c["groups"]), oversampling=c["a"], overpartition=c["b"],
                        imbalance=c["eps"])
-    out, reports = api.ams_sort(net, data, params, "simple",
+    out, reports = api.ams_sort(net, data, params, c["scheme"],
                                 SeedSpec(c["master_seed"], c["stream"]))
     assert_ledger(net.ledger, c["ledger"])
     for mine, ref in zip(reports, c["reports"]):
@@ -119,7 +126,7 @@ def test_ledger_through_dropin_api(c):
 
 
 # --------------------------------------------------------------------------
-# Whole experiment records (bench.py:180-242), delivery "simple"
+# Whole experiment records (bench.py:180-242)
 
 RECORDS_PATH = os.path.join(os.path.dirname(CASES_PATH), "records.jsonl")
 PHASES = ("splitter_selection", "bucket_processing", "data_delivery", "local_sorting")
@@ -163,7 +170,7 @@ def record_input(ref):
     return O.reference_input(ref["dist"], ref["pes"], ref["n_per_pe"], ref["seed"], ref["rep"])
 
 
-@pytest.mark.parametrize("line", records(), ids=lambda s: json.loads(s)["dist"])
+@pytest.mark.parametrize("line", records(), ids=lambda s: "{delivery}-{dist}-{rep}".format(**json.loads(s)))
 def test_record_from_oracle_levels(line):
     from oracle import ams_oracle as O
 
@@ -172,18 +179,20 @@ def test_record_from_oracle_levels(line):
     groups = tuple(ref["groups"])
     res = O.ams_sort(keys, [ref["n_per_pe"]] * ref["pes"], groups, oversampling=ref["a"],
                      overpartition=ref["b"], imbalance=ref["eps"], master_seed=ref["seed"],
-                     stream=f"algo/rep{ref['rep']}")
+                     stream=f"algo/rep{ref['rep']}", scheme=ref["delivery"])
     net = LG.Network(ref["pes"], LG.CostParams(alpha=ref["alpha"], beta=ref["beta"]))
     for lv, infos in enumerate(res.levels):
         for info in infos:
             LG.charge_group_level(net, info.group_lo, info.hist, info.plan.boundaries,
-                                  groups[lv], ref["b"], ref["a"], info.splitter_pos)
+                                  groups[lv], ref["b"], ref["a"], info.splitter_pos,
+                                  scheme=ref["delivery"], master_seed=ref["seed"],
+                                  level_stream=f"algo/rep{ref['rep']}/L{lv}-g{info.group_lo}")
     verdict = "pass" if np.array_equal(res.keys, np.sort(keys)) else "fail"
     assert experiment_record(ref, ref["a"], res.pe_sizes, res.reports, net, verdict) == line
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("line", records(), ids=lambda s: json.loads(s)["dist"])
+@pytest.mark.parametrize("line", records(), ids=lambda s: "{delivery}-{dist}-{rep}".format(**json.loads(s)))
 def test_record_through_dropin_api(line):
     """``run_experiment``'s record, byte for byte, with the sort on the GPU."""
     from paper_1410_6754_b200 import api
@@ -197,7 +206,7 @@ def test_record_through_dropin_api(line):
     net = LG.Network(ref["pes"], LG.CostParams(alpha=ref["alpha"], beta=ref["beta"]))
     params = AmsParams(tuple(ref["groups"]), oversampling=ref["a"], overpartition=ref["b"],
                        imbalance=ref["eps"])
-    out, reports = api.ams_sort(net, data, params, "simple",
+    out, reports = api.ams_sort(net, data, params, ref["delivery"],
                                 SeedSpec(ref["seed"], "algo").derive(f"rep{ref['rep']}"))
     flat = [e for pe in range(ref["pes"]) for e in out[pe]]
     expected = sorted(e for seq in data.values() for e in seq)
