@@ -44,6 +44,11 @@ CASES = [
     ("det_three_level_16", 16, 256, (2, 2, 4), None, 16, 0.3, 15, 3, 1.0, 0.5, "deterministic"),
     ("perm_two_level_64", 64, 512, (8, 8), None, 16, 0.1, 12, 1, 1.0, 1.0, "permuted"),
     ("perm_sorted_16", 16, 400, (4, 4), None, 8, 0.2, 18, 4, 0.3, 1.7, "permuted", "sorted"),
+    ("rand_two_level_64", 64, 512, (8, 8), None, 16, 0.1, 12, 1, 1.0, 1.0, "randomized"),
+    ("rand_sorted_16", 16, 400, (4, 4), None, 8, 0.2, 18, 4, 0.3, 1.7, "randomized", "sorted"),
+    ("rand_reverse_32", 32, 200, (4, 8), None, 16, 0.2, 20, 8, 1.0, 1.0, "randomized",
+     "reverse"),
+    ("rand_flat_8", 8, 900, (8,), 3.0, 4, 0.2, 21, 10, 0.6, 1.1, "randomized", "sorted"),
     ("perm_ragged_6", [0, 37, 5, 200, 1, 90], None, (2, 3), 2.0, 4, 0.2, 16, 9, 1.0, 1.0,
      "permuted"),
 ]
@@ -64,6 +69,8 @@ RECORD_CONFIGS = [
          delivery="deterministic"),
     dict(pes=16, n_per_pe=512, levels=2, groups=(4, 4), seed=9, dist="uniform",
          delivery="permuted"),
+    dict(pes=16, n_per_pe=512, levels=2, groups=(4, 4), seed=10, dist="sorted",
+         delivery="randomized"),
 ]
 
 

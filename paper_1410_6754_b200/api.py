@@ -159,11 +159,10 @@ def ams_sort(net, data, params, scheme: str, seed):
     """Drop-in for ``mlpsort.ams.ams_sort`` (ams.py:271-313).
 
     ``net`` needs ``.p`` (the reference's ``Network``).  When it also has a
-    ``ledger`` and ``scheme`` is "simple", "deterministic" or "permuted",
-    the ledger is charged exactly as
+    ``ledger``, the ledger is charged exactly as
     the reference charges it (phases, per-PE words/messages, modeled time;
-    ``ledger.charge_sort`` from the device run's level records).  The
-    "randomized" scheme leaves the ledger untouched.
+    ``ledger.charge_sort`` from the device run's level records), for every
+    scheme of the reference's ``SCHEMES`` registry.
     Elements keep their identity: the returned lists hold the caller's own
     Element objects.  Requires origin tags that increase along the PE-major
     concatenation (as ``generate_input`` produces, bench.py:176), which makes

@@ -12,7 +12,7 @@ from those, in the reference's call order (so float sums match bit for bit),
 onto any object with the reference ledger's methods — the user's own
 ``mlpsort.simnet.Network``, or the stand-in :class:`Network` below.
 
-Scope: schemes "simple", "deterministic" and "permuted" (delivery.py:138-306).
+Scope: the whole ``SCHEMES`` registry (delivery.py:138-455).
 Host bookkeeping only; no device work happens here.
 """
 
@@ -166,7 +166,113 @@ def _charge_gossip(ledger, alpha, beta, members, counts) -> None:
         ledger.charge_collective(members, per, max(per.values()) * beta + _log2_ceil(n) * alpha)
 
 
-CHARGED_SCHEMES = ("simple", "deterministic", "permuted")
+CHARGED_SCHEMES = ("simple", "deterministic", "permuted", "randomized")
+
+
+def _mix64(x: int) -> int:
+    """splitmix64 finalizer (core.py:74-79)."""
+    x &= 0xFFFFFFFFFFFFFFFF
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & 0xFFFFFFFFFFFFFFFF
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & 0xFFFFFFFFFFFFFFFF
+    return x ^ (x >> 31)
+
+
+def _feistel(n: int, seed):
+    """``feistel_new(n, seed).apply`` (core.py:96-155): four keyed digit-pair
+    rounds on the padded square domain, cycle-walked below n."""
+    side = math.isqrt(n)
+    if side * side < n:
+        side += 1
+    tables = [[_mix64(v ^ seed.key64(k)) % side for v in range(side)] for k in range(4)]
+
+    def apply(i: int) -> int:
+        x = i
+        for _ in range(side * side):
+            hi, lo = divmod(x, side)
+            for t in tables:
+                lo, hi = hi, (lo + t[hi]) % side
+            x = lo + hi * side
+            if x < n:
+                return x
+        raise RuntimeError("cycle walk failed to terminate")
+    return apply
+
+
+def _default_delegation_factor(p: int, r: int) -> int:
+    """delivery.py:309-315."""
+    if r * p <= 2:
+        return 1
+    a = 0.5 * (math.sqrt(1.0 + r / math.log(r * p / 2.0)) - 1.0)
+    return max(1, math.floor(a))
+
+
+def _charge_randomized(net, lo: int, pieces: np.ndarray, r: int, master_seed: int,
+                       level_stream: str) -> None:
+    """deliver_randomized's charges (delivery.py:318-436): delegation
+    exchange, enumeration prefix sum, reply exchange, data exchange."""
+    from .params import SeedSpec
+
+    P = pieces.shape[0]
+    members = list(range(lo, lo + P))
+    sub = P // r
+    seed = SeedSpec(master_seed, f"{level_stream}/deliver")
+    n = int(pieces.sum())
+    s = max(1, math.ceil(_default_delegation_factor(P, r) * n / (r * P)))
+    chunks = []                                      # (idx, g, length, large)
+    for idx in range(P):
+        for g in range(r):
+            size = int(pieces[idx, g])
+            if size == 0:
+                continue
+            if size > s:
+                whole, rem = divmod(size, s)
+                chunks.extend((idx, g, s, True) for _ in range(whole))
+                if rem:
+                    chunks.append((idx, g, rem, False))
+            else:
+                chunks.append((idx, g, size, False))
+    large_ids = [i for i, ch in enumerate(chunks) if ch[3]]
+    holder_of = {}
+    if large_ids:
+        perm = _feistel(len(large_ids), seed.derive("delegate"))
+        for rank, cid in enumerate(large_ids):
+            holder_of[cid] = perm(rank) % P
+    words: dict = {}                                 # (g, idx, offset, length) each
+    for cid in large_ids:
+        key = (chunks[cid][0], holder_of[cid])
+        words[key] = words.get(key, 0) + 4
+    _exchange(net, lo, P, [(a, b, w) for (a, b), w in words.items()])
+    held: dict = {}
+    for cid, (idx, g, _, _) in enumerate(chunks):
+        held.setdefault((g, holder_of.get(cid, idx)), []).append(cid)
+    start_of, totals = {}, [0] * r
+    for g in range(r):
+        order = _feistel(P, seed.derive(f"order-g{g}"))
+        running = 0
+        for holder in sorted(range(P), key=order):
+            mine = held.get((g, holder), [])
+            if not mine:
+                continue
+            seed.derive(f"reorder-g{g}-h{holder}").rng().shuffle(mine)
+            for cid in mine:
+                start_of[cid] = running
+                running += chunks[cid][2]
+        totals[g] = running
+    _charge_vector(net.ledger, net.params.alpha, net.params.beta, members, r)
+    words = {}                                       # (g, offset, start) each
+    for cid in large_ids:
+        idx, holder = chunks[cid][0], holder_of[cid]
+        if holder != idx:
+            words[(holder, idx)] = words.get((holder, idx), 0) + 3
+    _exchange(net, lo, P, [(a, b, w) for (a, b), w in words.items()])
+    msgs = []
+    for cid, (idx, g, length, _) in enumerate(chunks):
+        m, st = totals[g], start_of[cid]
+        for t in range(sub):                         # quota slots (delivery.py:78-104)
+            take = min(st + length, (m * (t + 1)) // sub) - max(st, (m * t) // sub)
+            if take > 0:
+                msgs.append((idx, g * sub + t, take))
+    _exchange(net, lo, P, msgs)
 
 
 def _exchange(net, lo: int, P: int, msgs) -> None:
@@ -241,6 +347,9 @@ def _charge_delivery(net, lo: int, pieces: np.ndarray, r: int, scheme: str,
         _charge_vector(ledger, alpha, net.params.beta, members, r)
         _exchange(net, lo, P, [m[:3] for m in _planned_messages(pieces, r, slices, new_sizes)])
         return
+    if scheme == "randomized":
+        _charge_randomized(net, lo, pieces, r, master_seed, level_stream)
+        return
     if scheme != "deterministic":
         raise ValueError(f"ledger charges of scheme {scheme!r} are not modelled")
     # deliver_deterministic (delivery.py:188-306)
@@ -281,7 +390,7 @@ def charge_group_level(net, lo: int, hist: np.ndarray, boundaries, r: int, b: in
     boundaries:   plan boundaries (r+1)
     splitter_pos: position in the group buffer of each splitter (br-1), or
     holders:      per member, how many splitters were drawn from it
-    level_stream: "{stream}/L{level}-g{lo}" (the permuted scheme's Feistel orders)
+    level_stream: "{stream}/L{level}-g{lo}" (the seeded schemes' Feistel orders)
     """
     ledger, alpha, beta = net.ledger, net.params.alpha, net.params.beta
     hist = np.asarray(hist, dtype=np.int64)
