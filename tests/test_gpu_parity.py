@@ -70,16 +70,20 @@ def check_levels(res, g):
             assert mine[k] == v, (k, mine[k], v)
 
 
-@pytest.mark.parametrize("name", G.names())
-@pytest.mark.parametrize("native", [True, False], ids=["c_driver", "py_levels"])
+NON_SIMPLE = ("det_", "perm_", "rand_")  # fixtures of the other delivery schemes
+
+
+@pytest.mark.parametrize("name,native",
+                         [(n, True) for n in G.names()]
+                         + [(n, False) for n in G.names() if not n.startswith(NON_SIMPLE)],
+                         ids=lambda v: {True: "c_driver", False: "py_levels"}.get(v, v)
+                         if isinstance(v, bool) else v)
 def test_golden_parity(api, name, native):
-    """Both host drivers: the one-call C++ ams_sort_run (native) and the
-    Python level loop over the level entry points (which also reads the
-    splitters back for comparison)."""
+    """Both host drivers: the one-call C++ ams_sort_run (native) and, for
+    scheme="simple", the Python level loop over the level entry points
+    (which also reads the splitters back for comparison)."""
     g = G.load(name)
     scheme = g.get("scheme", "simple")
-    if scheme != "simple" and not native:
-        pytest.skip("the per-level host driver implements the simple scheme only")
     keys, sizes = G.input_of(g)
     if "error" in g:  # the reference rejects this input: same exception class and message
         exc = {"ValueError": ValueError, "RuntimeError": RuntimeError}[g["error"]["type"]]
@@ -95,6 +99,16 @@ def test_golden_parity(api, name, native):
     assert G.sha_u64(out) == g["output_sha256"]
     assert G.sha_i64(res.vals.cpu().numpy()) == g["origin_sha256"]
     check_levels(res, g)
+
+
+@pytest.mark.parametrize("scheme", ["deterministic", "permuted", "randomized"])
+def test_per_level_driver_rejects_other_schemes(api, scheme):
+    """record_splitters runs the per-level host driver, which implements the
+    simple scheme only: the other schemes fail loudly instead of silently
+    delivering with simple's placement."""
+    keys = np.arange(64, dtype=np.uint64)[::-1].copy()
+    with pytest.raises(ValueError, match="simple scheme only"):
+        run_gpu(api, keys, [8] * 8, [8], None, 16, 0.1, 1, "s", record=True, scheme=scheme)
 
 
 @pytest.mark.parametrize("name", [n for n in G.names()
