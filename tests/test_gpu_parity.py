@@ -360,6 +360,61 @@ def test_config2_full_size_properties(api, dist):
     assert sum(r["over_budget"] for r in res.reports) == 0
 
 
+def _wrap_checksums(t: torch.Tensor):
+    """Multiset checksums of 64-bit patterns (wrapping int64 sums of x and x^2)."""
+    x = t.view(torch.int64)
+    return int(x.sum()), int((x * x).sum())
+
+
+def _check_sorted_perm(inp: torch.Tensor, res, n: int, p: int, eps: float):
+    out = res.keys
+    assert out.numel() == n
+    assert bool((out[1:] >= out[:-1]).all())
+    assert _wrap_checksums(out) == _wrap_checksums(inp)
+    assert int(np.asarray(res.pe_sizes).sum()) == n
+    assert int(np.asarray(res.pe_sizes).max()) <= (1 + eps) * n / p
+
+
+def test_config3_full_size_properties(api):
+    """BASELINE config 3 shape at full size (n=2^30 float64 uniform [0,1),
+    p=256, groups (8,32), eps=0.1), checked on the device: non-decreasing,
+    same multiset checksums as the input, per-PE sizes within (1+eps)·n/p."""
+    from paper_1410_6754_b200 import AmsParams, SeedSpec
+    n, p = 1 << 30, 256
+    g = torch.Generator(device="cuda").manual_seed(2)
+    keys = torch.rand(n, dtype=torch.float64, device="cuda", generator=g)
+    res = api.ams_sort_tensors(keys, [n // p] * p, AmsParams((8, 32), None, 16, 0.1),
+                               SeedSpec(2, "algo/rep0"), key_kind="f64")
+    torch.cuda.synchronize()
+    _check_sorted_perm(keys, res, n, p, 0.1)
+    assert sum(r["over_budget"] for r in res.reports) == 0
+    del res, keys
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("scheme", ["deterministic", "permuted", "randomized"])
+def test_config2_full_size_schemes(api, scheme):
+    """Config 2 shape (n=2^28 uint64, p=64, (8,8)) at full size through the
+    other delivery schemes, with origin payloads: sorted output, and the
+    payload is the permutation that gathers the input into it."""
+    from paper_1410_6754_b200 import AmsParams, SeedSpec
+    n, p = 1 << 28, 64
+    g = torch.Generator(device="cuda").manual_seed(1)
+    keys = torch.randint(-2**63, 2**63 - 1, (n,), dtype=torch.int64, device="cuda", generator=g)
+    vals = torch.arange(n, dtype=torch.int64, device="cuda")
+    res = api.ams_sort_tensors(keys, [n // p] * p, AmsParams((8, 8), None, 16, 0.1),
+                               SeedSpec(1, "algo/rep0"), vals=vals, key_kind="u64",
+                               scheme=scheme)
+    torch.cuda.synchronize()
+    flip = torch.tensor(-(2**63), dtype=torch.int64, device="cuda")
+    signed = res.keys.view(torch.int64) ^ flip  # unsigned order as signed order
+    assert bool((signed[1:] >= signed[:-1]).all())
+    assert torch.equal(keys[res.vals], res.keys.view(torch.int64))
+    assert int(np.asarray(res.pe_sizes).sum()) == n
+    del res, keys, vals, signed
+    torch.cuda.empty_cache()
+
+
 def test_distributed_path_world1_nccl():
     """dist.sort_distributed over NCCL at world size 1 (CudaOps + the
     exchange code on a real GPU) equals the oracle."""
