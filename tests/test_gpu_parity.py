@@ -392,6 +392,31 @@ def test_config3_full_size_properties(api):
     torch.cuda.empty_cache()
 
 
+@pytest.mark.parametrize("dist", ["skewed", "sorted", "reverse", "equal"])
+def test_config4_full_size_properties(api, dist):
+    """Config 4 shape at full size (n=2^30 uint64, p=256, (8,32)), inputs made
+    on the device: sorted, reverse sorted, all equal (42) and a skewed
+    duplicate-heavy draw over 2^10 values (u^8 * 1024; a stand-in for the
+    Zipf input, whose generator is host-side).  Checked on the device."""
+    from paper_1410_6754_b200 import AmsParams, SeedSpec
+    n, p = 1 << 30, 256
+    if dist == "sorted":
+        keys = torch.arange(n, dtype=torch.int64, device="cuda")
+    elif dist == "reverse":
+        keys = torch.arange(n - 1, -1, -1, dtype=torch.int64, device="cuda")
+    elif dist == "equal":
+        keys = torch.full((n,), 42, dtype=torch.int64, device="cuda")
+    else:
+        g = torch.Generator(device="cuda").manual_seed(4)
+        keys = (torch.rand(n, device="cuda", generator=g).pow_(8) * 1024).to(torch.int64)
+    res = api.ams_sort_tensors(keys, [n // p] * p, AmsParams((8, 32), None, 16, 0.1),
+                               SeedSpec(4, "algo/rep0"), key_kind="u64")
+    torch.cuda.synchronize()
+    _check_sorted_perm(keys, res, n, p, 0.1)  # keys < 2^63: signed order = unsigned
+    del res, keys
+    torch.cuda.empty_cache()
+
+
 @pytest.mark.parametrize("scheme", ["deterministic", "permuted", "randomized"])
 def test_config2_full_size_schemes(api, scheme):
     """Config 2 shape (n=2^28 uint64, p=64, (8,8)) at full size through the
