@@ -102,13 +102,19 @@ def _allgather_var(t: torch.Tensor, count: int, world: int, group=None):
 
 
 def sort_distributed(keys: torch.Tensor, pe_sizes_local, params, seed, ops, vals=None, out=None,
-                     out_vals=None, key_kind=None, group=None):
+                     out_vals=None, key_kind=None, group=None, scheme: str = "simple"):
     """Sort this rank's PEs as part of one global ams_sort(scheme="simple").
+    The multi-GPU driver implements the simple delivery scheme only; any
+    other ``scheme`` raises ValueError (single-GPU ``ams_sort_tensors``
+    implements all four).
 
     ``keys`` holds this rank's PEs (PE-major), ``pe_sizes_local`` their
     sizes; PE ids are rank-major (rank k owns PEs [k*p/G, (k+1)*p/G)).
     Returns (sorted local keys, vals, local per-PE sizes, level records); the
     rank-ordered concatenation of the outputs is the global sort."""
+    if scheme != "simple":
+        raise ValueError(f"the multi-GPU driver implements the simple delivery scheme only, "
+                         f"not {scheme!r}")
     params = as_params(params)
     master, stream_id = as_seed(seed)
     world = dist.get_world_size(group)

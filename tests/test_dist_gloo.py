@@ -101,3 +101,13 @@ def test_rejects_groups_straddling_ranks():
     keys = np.arange(64, dtype=np.uint64)
     with pytest.raises(RuntimeError, match="multiple of the 4 ranks"):
         run_world(4, keys, [8] * 8, (2, 4))
+
+
+@pytest.mark.parametrize("scheme", ["deterministic", "permuted", "randomized"])
+def test_rejects_other_schemes(scheme):
+    """The multi-GPU driver implements scheme="simple" only and says so
+    before touching the process group."""
+    from paper_1410_6754_b200 import dist as D
+    with pytest.raises(ValueError, match="simple delivery scheme only"):
+        D.sort_distributed(torch.zeros(8, dtype=torch.int64), [4, 4], (2,), 1, ops=None,
+                           scheme=scheme)
