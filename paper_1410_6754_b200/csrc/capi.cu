@@ -34,6 +34,24 @@ namespace {
       return set_error(AMS_ECUDA, std::string(#call) + ": " + cudaGetErrorString(_e)); \
   } while (0)
 
+// Makes `dev` current for one C-ABI call and restores the caller's device
+// on return (a sort on cuda:1 must not leave a thread on cuda:1).
+struct DeviceGuard {
+  int prev = -1;
+  cudaError_t err = cudaSuccess;
+  explicit DeviceGuard(int dev) {
+    err = cudaGetDevice(&prev);
+    if (err == cudaSuccess && prev != dev) err = cudaSetDevice(dev);
+    else prev = -1;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+#define AMS_ON_DEVICE(dev)  \
+  DeviceGuard _ams_dg(dev); \
+  AMS_CK(_ams_dg.err)
+
 struct DevBuf {
   void* p = nullptr;
   size_t cap = 0;
@@ -351,7 +369,7 @@ int ams_ctx_create(int device, void* stream, ams_ctx_t** out) {
   AMS_CK(cudaGetDeviceCount(&ndev));
   if (device < 0 || device >= ndev)
     return set_error(AMS_EINVAL, "device " + std::to_string(device) + " out of range");
-  AMS_CK(cudaSetDevice(device));
+  AMS_ON_DEVICE(device);
   ams_ctx* c = new ams_ctx();
   c->device = device;
   c->stream = static_cast<cudaStream_t>(stream);
@@ -364,7 +382,7 @@ int ams_ctx_create(int device, void* stream, ams_ctx_t** out) {
 
 int ams_ctx_destroy(ams_ctx_t* c) {
   if (!c) return AMS_OK;
-  cudaSetDevice(c->device);
+  DeviceGuard dg(c->device);
   cudaStreamSynchronize(c->stream);
   resolve_timing(c);
   for (cudaEvent_t e : c->free_events) cudaEventDestroy(e);
@@ -401,7 +419,7 @@ int ams_ctx_set_timing(ams_ctx_t* c, int enable) {
 
 int ams_ctx_kernel_stats(ams_ctx_t* c, double* ms, double* bytes, uint64_t* launches, int ncat) {
   if (!c) return set_error(AMS_EINVAL, "null context");
-  AMS_CK(cudaSetDevice(c->device));
+  AMS_ON_DEVICE(c->device);
   resolve_timing(c);
   for (int i = 0; i < ncat && i < AMS_NUM_KCAT; ++i) {
     if (ms) ms[i] = c->cat_ms[i];
@@ -413,7 +431,7 @@ int ams_ctx_kernel_stats(ams_ctx_t* c, double* ms, double* bytes, uint64_t* laun
 
 int ams_ctx_timeline(ams_ctx_t* c, int* cat, float* t0, float* t1, int cap, int* count) {
   if (!c || !count) return set_error(AMS_EINVAL, "null argument");
-  AMS_CK(cudaSetDevice(c->device));
+  AMS_ON_DEVICE(c->device);
   resolve_timing(c);
   const int n = (int)std::min<size_t>(c->timeline.size(), (size_t)std::max(cap, 0));
   for (int i = 0; i < n; ++i) {
@@ -428,7 +446,7 @@ int ams_ctx_timeline(ams_ctx_t* c, int* cat, float* t0, float* t1, int cap, int*
 
 int ams_ctx_reset_stats(ams_ctx_t* c) {
   if (!c) return set_error(AMS_EINVAL, "null context");
-  AMS_CK(cudaSetDevice(c->device));
+  AMS_ON_DEVICE(c->device);
   resolve_timing(c);
   for (int i = 0; i < AMS_NUM_KCAT; ++i) { c->cat_ms[i] = 0; c->cat_bytes[i] = 0; c->cat_launches[i] = 0; }
   c->timeline.clear();
@@ -437,7 +455,7 @@ int ams_ctx_reset_stats(ams_ctx_t* c) {
 
 int ams_ctx_sync(ams_ctx_t* c) {
   if (!c) return set_error(AMS_EINVAL, "null context");
-  AMS_CK(cudaSetDevice(c->device));
+  AMS_ON_DEVICE(c->device);
   AMS_CK(cudaStreamSynchronize(c->stream));
   return AMS_OK;
 }
@@ -460,7 +478,7 @@ int level_sample_impl(ams_ctx_t* c, const void* src, int key_kind, uint64_t coun
   if (count == 0) return AMS_OK;
   if (!src || !h_idx || !h_gpos || !d_out_keys || !d_out_pos)
     return set_error(AMS_EINVAL, "null argument");
-  AMS_CK(cudaSetDevice(c->device));
+  AMS_ON_DEVICE(c->device);
   Stage& st = c->st_sample;
   st.reset();
   const size_t oi = st.put(h_idx, count), og = st.put(h_gpos, count);
@@ -482,7 +500,7 @@ int ams_level_splitters(ams_ctx_t* c, int ngroups, const uint64_t* d_sample_keys
                         const uint32_t* d_sample_pos, const uint64_t* h_soff, const int32_t* h_nb) {
   if (!c) return set_error(AMS_EINVAL, "null context");
   if (ngroups < 1 || !h_soff || !h_nb) return set_error(AMS_EINVAL, "bad group list");
-  AMS_CK(cudaSetDevice(c->device));
+  AMS_ON_DEVICE(c->device);
   uint64_t max_s = 0;
   int max_nb = 1, cells_cap = 1;
   for (int g = 0; g < ngroups; ++g) {
@@ -531,7 +549,7 @@ int ams_level_splitters(ams_ctx_t* c, int ngroups, const uint64_t* d_sample_keys
 int ams_read_splitters(ams_ctx_t* c, int group, uint64_t* keys, uint32_t* pos, int* nspl) {
   if (!c) return set_error(AMS_EINVAL, "null context");
   if (group < 0 || group >= c->ngroups) return set_error(AMS_EINVAL, "group out of range");
-  AMS_CK(cudaSetDevice(c->device));
+  AMS_ON_DEVICE(c->device);
   ClsHeader h;
   const uint8_t* blob = c->blobs.as<uint8_t>() + (size_t)group * kBlobStride;
   AMS_CK(cudaMemcpyAsync(&h, blob, sizeof h, cudaMemcpyDeviceToHost, c->stream));
@@ -556,7 +574,7 @@ int ams_level_classify(ams_ctx_t* c, const void* src, int key_kind, int nseg,
   int max_nb = 1;
   for (int g = 0; g < ngroups; ++g) max_nb = std::max(max_nb, c->group_nb[g]);
   if (nb_stride < max_nb) return set_error(AMS_EINVAL, "nb_stride smaller than the bucket count");
-  AMS_CK(cudaSetDevice(c->device));
+  AMS_ON_DEVICE(c->device);
   // Groups are contiguous runs of segments.
   c->group_first.assign(ngroups, -1);
   c->group_nseg.assign(ngroups, 0);
@@ -651,7 +669,7 @@ int level_scatter_impl(ams_ctx_t* c, const void* src, const void* src_vals, int 
   const int G = c->ngroups;
   if (child_first < 0 || child_count < 0 || child_first + child_count > G * r)
     return set_error(AMS_EINVAL, "child group range outside the level's children");
-  AMS_CK(cudaSetDevice(c->device));
+  AMS_ON_DEVICE(c->device);
   for (int g = 0; g < G; ++g) {
     const uint64_t* b = h_boundaries + (size_t)g * (r + 1);
     if (b[0] != 0 || b[r] != (uint64_t)c->group_nb[g])
@@ -713,7 +731,7 @@ extern "C" {
 int ams_get_minmax(ams_ctx_t* c, uint64_t out[2]) {
   if (!c || !out) return set_error(AMS_EINVAL, "null argument");
   if (!c->minmax.p) return set_error(AMS_EINVAL, "no min/max recorded");
-  AMS_CK(cudaSetDevice(c->device));
+  AMS_ON_DEVICE(c->device);
   AMS_CK(to_host(c->h_small, c->minmax.p, 16, c->stream));
   AMS_CK(cudaStreamSynchronize(c->stream));
   std::memcpy(out, c->h_small.p, 16);
@@ -722,7 +740,7 @@ int ams_get_minmax(ams_ctx_t* c, uint64_t out[2]) {
 
 int ams_set_minmax(ams_ctx_t* c, const uint64_t in[2]) {
   if (!c || !in) return set_error(AMS_EINVAL, "null argument");
-  AMS_CK(cudaSetDevice(c->device));
+  AMS_ON_DEVICE(c->device);
   AMS_CK(c->minmax.ensure(16));
   AMS_CK(c->h_small.ensure(64));
   AMS_CK(cudaStreamSynchronize(c->stream));
@@ -1073,7 +1091,7 @@ int ams_final_sort(ams_ctx_t* c, void* src, void* src_vals, void* tmp, void* tmp
   if (nseg < 0 || (nseg > 0 && (!h_seg_off || !h_seg_len))) return set_error(AMS_EINVAL, "bad segments");
   const bool vals = src_vals != nullptr;
   if (vals && (!tmp_vals || !out_vals)) return set_error(AMS_EINVAL, "missing value buffers");
-  AMS_CK(cudaSetDevice(c->device));
+  AMS_ON_DEVICE(c->device);
   std::vector<uint64_t> s_off, s_len, b_off, b_len, b_lo, b_hi;
   std::vector<int32_t> b_seg;
   uint64_t total = 0, small_n = 0;
@@ -1139,7 +1157,7 @@ int ams_final_sort_buckets(ams_ctx_t* c, void* src, void* tmp, void* out, int ke
     return set_error(AMS_EINVAL, "bad bucket list");
   if (nbk > 0 && c->bounds[1 - c->bcur].cap == 0)
     return set_error(AMS_EINVAL, "no key bounds of the last level's groups");
-  AMS_CK(cudaSetDevice(c->device));
+  AMS_ON_DEVICE(c->device);
   std::vector<uint64_t> bo(bk_off, bk_off + nbk), bl(bk_len, bk_len + nbk);
   std::vector<int32_t> bg(bk_group, bk_group + nbk), bb(bk_bucket, bk_bucket + nbk);
   return final_sort_bm(c, src, tmp, out, key_kind, bo, bl, bg, bb, c->bounds[1 - c->bcur].as<uint64_t>());
@@ -1161,7 +1179,7 @@ int ams_final_sort_stats(ams_ctx_t* c, uint64_t out[2]) {
 
 int ams_map_keys(ams_ctx_t* c, const void* src, void* dst, uint64_t n, int from_kind, int to_kind) {
   if (!c) return set_error(AMS_EINVAL, "null context");
-  AMS_CK(cudaSetDevice(c->device));
+  AMS_ON_DEVICE(c->device);
   KTimer kt(c, AMS_KCAT_MAP, 16.0 * n);
   AMS_CK(launch_map_keys(c->stream, src, dst, n, from_kind, to_kind));
   c->launches += n ? 1 : 0;
@@ -1259,7 +1277,7 @@ int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* p
   // the enumeration follows the permutation: same treatment.)
   const bool det = prm->scheme != AMS_SCHEME_SIMPLE && n > 0;
   const bool with_vals = user_vals || det;
-  AMS_CK(cudaSetDevice(c->device));
+  AMS_ON_DEVICE(c->device);
   // ams.py:278-280 and AmsParams.per_level_imbalance (ams.py:58-59).
   const double a = prm->oversampling > 0 ? prm->oversampling
                                          : 1.6 * std::log10((double)std::max<uint64_t>(n, 10));

@@ -34,7 +34,7 @@ import torch
 import torch.distributed as dist
 
 from . import _lib as L
-from .engine import LevelRecord, bucket_table, load_budget, level_targets, key_kind_of
+from .engine import LevelRecord, bucket_table, check_out, load_budget, level_targets, key_kind_of
 from .params import as_params, as_seed
 
 
@@ -48,7 +48,8 @@ class CudaOps:
 
     # buffers -------------------------------------------------------------
     def empty(self, n, dtype=torch.int64):
-        return torch.empty(max(n, 1), dtype=dtype, device=self.device)
+        # +2: bulk tile loads cover whole 16-byte units past a segment end
+        return torch.empty(max(n, 1) + 2, dtype=dtype, device=self.device)
 
     def workspace(self, n, with_vals):
         return self.sorter.workspace(n, with_vals)
@@ -294,6 +295,9 @@ def sort_distributed(keys: torch.Tensor, pe_sizes_local, params, seed, ops, vals
         gn = np.repeat(step, r).astype(np.int32)
     local_final = sizes[pe_lo:pe_lo + pl].astype(np.uint64)
     n_out = int(local_final.sum())
+    if isinstance(out, torch.Tensor) and out.is_cuda:
+        check_out(out, n_out, dev, "out")
+        check_out(out_vals, n_out, dev, "out_vals")
     if out is None:
         out = torch.empty(max(n_out, 1), dtype=keys.dtype, device=dev)
     if vals is not None and out_vals is None:

@@ -32,6 +32,18 @@ _KIND_NAMES = {"u64": L.KEY_U64, "uint64": L.KEY_U64, "i64": L.KEY_I64, "int64":
                "f64": L.KEY_F64, "float64": L.KEY_F64}
 
 
+def check_out(t, n: int, device, name: str) -> None:
+    """A caller-supplied output buffer must hold n contiguous 8-byte
+    elements on the sort's device: the native driver writes n keys there and
+    also uses ``out`` as relayout scratch."""
+    if t is None:
+        return
+    if not isinstance(t, torch.Tensor) or t.device != device:
+        raise ValueError(f"{name} must be a tensor on {device}")
+    if t.element_size() != 8 or not t.is_contiguous() or t.numel() < n:
+        raise ValueError(f"{name} must be a contiguous tensor of at least {n} 8-byte elements")
+
+
 def key_kind_of(t: torch.Tensor, key_kind=None) -> int:
     if key_kind is not None:
         return _KIND_NAMES[key_kind] if isinstance(key_kind, str) else int(key_kind)
@@ -153,7 +165,9 @@ class AmsSorter:
         key = (n, with_vals)
         if key not in self._work:
             self._work.clear()
-            mk = lambda: torch.empty(max(n, 1), dtype=torch.int64, device=self.device)
+            # +2 keys: the fixed-capacity partition's bulk loads cover whole
+            # 16-byte units past a bucket's end (k_scatter_fixed).
+            mk = lambda: torch.empty(max(n, 1) + 2, dtype=torch.int64, device=self.device)
             self._work[key] = ([mk(), mk()], [mk(), mk()] if with_vals else [None, None])
         return self._work[key]
 
@@ -163,9 +177,11 @@ class AmsSorter:
              with_stats: bool = True, scheme: str = "simple",
              record_holders: bool = False) -> SortOutput:
         """Sort ``keys`` (1-D, PE-major: PE i owns the next ``pe_sizes[i]``
-        keys) exactly as ams_sort(scheme) orders them ("simple" or
-        "deterministic"); returns the sorted keys (concatenation of per-PE
-        outputs), per-PE sizes and per-level records."""
+        keys) exactly as ams_sort(scheme) orders them (every scheme of the
+        reference's SCHEMES registry; the per-level host driver,
+        ``record_splitters=True``, runs "simple" only); returns the sorted
+        keys (concatenation of per-PE outputs), per-PE sizes and per-level
+        records."""
         if scheme not in SCHEMES:
             raise ValueError(f"unknown delivery scheme {scheme!r}; supported: {tuple(SCHEMES)}")
         if record_splitters and scheme != "simple":
@@ -182,8 +198,13 @@ class AmsSorter:
         n = int(sizes.sum())
         if n != keys.numel():
             raise ValueError(f"pe_sizes sum to {n}, keys has {keys.numel()} elements")
-        if vals is not None and (vals.numel() != n or vals.element_size() != 8 or not vals.is_cuda):
-            raise ValueError("vals must be a CUDA tensor of n 8-byte values")
+        if vals is not None and (vals.numel() != n or vals.element_size() != 8 or not vals.is_cuda
+                                 or vals.device != keys.device):
+            raise ValueError("vals must be a CUDA tensor of n 8-byte values on the keys' device")
+        check_out(out, n, keys.device, "out")
+        if out_vals is not None and vals is None:
+            raise ValueError("out_vals given without vals")
+        check_out(out_vals, n, keys.device, "out_vals")
         keys = keys.contiguous()
         if vals is not None:
             vals = vals.contiguous()

@@ -9,8 +9,9 @@ device run already returns per level and group (``engine.LevelRecord``):
 member sizes, the per-member bucket histogram, the plan boundaries and the
 splitter positions.  :func:`charge_sort` replays the reference's charges
 from those, in the reference's call order (so float sums match bit for bit),
-onto any object with the reference ledger's methods — the user's own
-``mlpsort.simnet.Network``, or the stand-in :class:`Network` below.
+onto the caller's ``net`` (the reference's ``mlpsort.simnet.Network`` or any
+object with its ``.params.alpha/.beta`` and a ledger with ``phase``,
+``record_exchange`` and ``charge_collective``; simnet.py:139-256).
 
 Scope: the whole ``SCHEMES`` registry (delivery.py:138-455).
 Host bookkeeping only; no device work happens here.
@@ -19,7 +20,6 @@ Host bookkeeping only; no device work happens here.
 from __future__ import annotations
 
 import math
-from dataclasses import dataclass
 
 import numpy as np
 
@@ -31,119 +31,6 @@ PHASE_DELIVERY = "data_delivery"           # ams.py:250
 def _log2_ceil(n: int) -> int:
     """simnet.py:258-259."""
     return (n - 1).bit_length() if n > 1 else 0
-
-
-# --------------------------------------------------------------------------
-# Stand-ins with the reference's interface (simnet.py:42-50, 123-256, 262-290)
-
-@dataclass(frozen=True)
-class CostParams:
-    """Message startup cost (alpha) and per-word cost (beta); simnet.py:42-50."""
-
-    alpha: float = 1.0
-    beta: float = 1.0
-
-    def __post_init__(self):
-        if self.alpha < 0 or self.beta < 0:
-            raise ValueError("cost parameters must be non-negative")
-
-
-class _PhaseTally:
-    __slots__ = ("modeled_time", "sent_words", "recv_words", "sent_msgs",
-                 "recv_msgs", "coll_words")
-
-    def __init__(self, p: int):
-        self.modeled_time = 0.0
-        self.sent_words = [0] * p
-        self.recv_words = [0] * p
-        self.sent_msgs = [0] * p
-        self.recv_msgs = [0] * p
-        self.coll_words = [0] * p
-
-
-class CostLedger:
-    """Per-PE exchange / collective counters with phase breakdown, same
-    methods and semantics as the reference's (simnet.py:139-256)."""
-
-    def __init__(self, p: int, params: CostParams):
-        self.p = p
-        self.params = params
-        self.modeled_time = 0.0
-        self.sent_words = [0] * p
-        self.recv_words = [0] * p
-        self.sent_msgs = [0] * p
-        self.recv_msgs = [0] * p
-        self.coll_words = [0] * p
-        self._phase = "setup"
-        self.phases: dict[str, _PhaseTally] = {}
-
-    class _Scope:
-        def __init__(self, ledger, name):
-            self.ledger, self.name = ledger, name
-
-        def __enter__(self):
-            self.prev, self.ledger._phase = self.ledger._phase, self.name
-            return self.ledger
-
-        def __exit__(self, *exc):
-            self.ledger._phase = self.prev
-            return False
-
-    def phase(self, name: str):
-        return CostLedger._Scope(self, name)
-
-    def _tally(self) -> _PhaseTally:
-        t = self.phases.get(self._phase)
-        if t is None:
-            t = self.phases[self._phase] = _PhaseTally(self.p)
-        return t
-
-    def record_exchange(self, sw, rw, sm, rm, cost: float) -> None:
-        if sum(sw) != sum(rw) or sum(sm) != sum(rm):
-            raise RuntimeError("exchange lost or duplicated traffic")
-        t = self._tally()
-        for pe in range(self.p):
-            if sw[pe] or rw[pe] or sm[pe] or rm[pe]:
-                for name, vec in (("sent_words", sw), ("recv_words", rw),
-                                  ("sent_msgs", sm), ("recv_msgs", rm)):
-                    getattr(self, name)[pe] += vec[pe]
-                    getattr(t, name)[pe] += vec[pe]
-        self.modeled_time += cost
-        t.modeled_time += cost
-
-    def charge_collective(self, members, words_per_member, time: float) -> None:
-        t = self._tally()
-        per = ({pe: words_per_member for pe in members}
-               if isinstance(words_per_member, int) else words_per_member)
-        for pe, w in per.items():
-            self.coll_words[pe] += w
-            t.coll_words[pe] += w
-        self.modeled_time += time
-        t.modeled_time += time
-
-    def phase_summary(self) -> dict:
-        out = {}
-        for name, t in self.phases.items():
-            out[name] = {
-                "modeled_time": t.modeled_time,
-                "max_words": max((max(t.sent_words[pe], t.recv_words[pe]) + t.coll_words[pe]
-                                  for pe in range(self.p)), default=0),
-                "max_msgs": max((max(t.sent_msgs[pe], t.recv_msgs[pe])
-                                 for pe in range(self.p)), default=0),
-            }
-        return out
-
-
-class Network:
-    """``p`` PEs plus their ledger (simnet.py:262-273), for callers without
-    the reference package."""
-
-    def __init__(self, p: int, params: CostParams | None = None):
-        if p < 1:
-            raise ValueError("need at least one PE")
-        self.p = p
-        self.params = params or CostParams()
-        self.ledger = CostLedger(p, self.params)
 
 
 # --------------------------------------------------------------------------

@@ -95,8 +95,13 @@ class SeedSpec:
 
 
 def as_seed(seed) -> tuple[int, str]:
-    """(master_seed, stream_id) of our SeedSpec or the reference's."""
-    return int(seed.master_seed), str(seed.stream_id)
+    """(master_seed, stream_id) of our SeedSpec or the reference's.  The seed
+    crosses the C ABI as int64 and is hashed there as its decimal text
+    (core.py:52-55 hashes f"{master_seed}"), so it must fit in int64."""
+    m = int(seed.master_seed)
+    if not -(1 << 63) <= m < (1 << 63):
+        raise ValueError(f"master_seed {m} outside the supported int64 range")
+    return m, str(seed.stream_id)
 
 
 def as_params(params) -> AmsParams:

@@ -14,6 +14,7 @@ import numpy as np
 import pytest
 
 from paper_1410_6754_b200 import ledger as LG
+from tests.simnet_standin import Costs, Net
 
 CASES_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "ledger",
                           "cases.json")
@@ -68,7 +69,7 @@ def test_ledger_from_oracle_levels(c):
                      overpartition=c["b"], imbalance=c["eps"], master_seed=c["master_seed"],
                      stream=c["stream"], scheme=c["scheme"])
     a = c["a"] if c["a"] is not None else O.default_oversampling(len(keys))
-    net = LG.Network(len(c["sizes"]), LG.CostParams(alpha=c["alpha"], beta=c["beta"]))
+    net = Net(len(c["sizes"]), Costs(alpha=c["alpha"], beta=c["beta"]))
     for lv, infos in enumerate(res.levels):
         for info in infos:
             LG.charge_group_level(net, info.group_lo, info.hist, info.plan.boundaries,
@@ -79,7 +80,7 @@ def test_ledger_from_oracle_levels(c):
 
 
 def test_stand_in_ledger_semantics():
-    net = LG.Network(3, LG.CostParams(alpha=2.0, beta=0.5))
+    net = Net(3, Costs(alpha=2.0, beta=0.5))
     with net.ledger.phase("x"):
         net.ledger.charge_collective([0, 1], 4, 3.0)
         net.ledger.record_exchange([2, 0, 0], [0, 0, 2], [1, 0, 0], [0, 0, 1], 3.0)
@@ -88,14 +89,14 @@ def test_stand_in_ledger_semantics():
     assert net.ledger.phase_summary()["x"] == {"modeled_time": 6.0, "max_words": 6,
                                                "max_msgs": 1}
     with pytest.raises(ValueError):
-        LG.CostParams(alpha=-1.0)
+        Costs(alpha=-1.0)
     with pytest.raises(ValueError):
-        LG.Network(0)
+        Net(0)
 
 
 def test_bucket_count_mismatch_rejected():
     hist = np.array([[3, 2], [1, 4]])
-    net = LG.Network(2)
+    net = Net(2)
     with pytest.raises(ValueError):
         LG.charge_group_level(net, 0, hist, [0, 1, 2], 2, 16, 10.0, [4])
 
@@ -112,7 +113,7 @@ def test_ledger_through_dropin_api(c):
     for pe, s in enumerate(c["sizes"]):
         data[pe] = [Element(int(k), pe, i) for i, k in enumerate(keys[off:off + s])]
         off += s
-    net = LG.Network(len(c["sizes"]), LG.CostParams(alpha=c["alpha"], beta=c["beta"]))
+    net = Net(len(c["sizes"]), Costs(alpha=c["alpha"], beta=c["beta"]))
     params = AmsParams(tuple(c["groups"]), oversampling=c["a"], overpartition=c["b"],
                        imbalance=c["eps"])
     out, reports = api.ams_sort(net, data, params, c["scheme"],
@@ -180,7 +181,7 @@ def test_record_from_oracle_levels(line):
     res = O.ams_sort(keys, [ref["n_per_pe"]] * ref["pes"], groups, oversampling=ref["a"],
                      overpartition=ref["b"], imbalance=ref["eps"], master_seed=ref["seed"],
                      stream=f"algo/rep{ref['rep']}", scheme=ref["delivery"])
-    net = LG.Network(ref["pes"], LG.CostParams(alpha=ref["alpha"], beta=ref["beta"]))
+    net = Net(ref["pes"], Costs(alpha=ref["alpha"], beta=ref["beta"]))
     for lv, infos in enumerate(res.levels):
         for info in infos:
             LG.charge_group_level(net, info.group_lo, info.hist, info.plan.boundaries,
@@ -203,7 +204,7 @@ def test_record_through_dropin_api(line):
     npe = ref["n_per_pe"]
     data = {pe: [Element(int(k), pe, i) for i, k in enumerate(keys[pe * npe:(pe + 1) * npe])]
             for pe in range(ref["pes"])}
-    net = LG.Network(ref["pes"], LG.CostParams(alpha=ref["alpha"], beta=ref["beta"]))
+    net = Net(ref["pes"], Costs(alpha=ref["alpha"], beta=ref["beta"]))
     params = AmsParams(tuple(ref["groups"]), oversampling=ref["a"], overpartition=ref["b"],
                        imbalance=ref["eps"])
     out, reports = api.ams_sort(net, data, params, ref["delivery"],
