@@ -89,3 +89,64 @@ def test_plan_hand_cases():
     assert O.group_plan([5, 3, 4, 2, 6], 1).max_load == 20
     assert O.group_plan([5, 3, 4, 2, 6], 7).max_load == 6
     assert O.group_plan([0, 0, 0], 2).max_load == 0
+
+
+# ---------------------------------------------------------------------------
+# The full-size oracle (oracle/fullsize.py) used by the GPU tests at 2^28-2^30
+# keys: same splitters, histograms, plans, member sizes and output as the
+# pinned oracle and the reference's fixtures.
+
+def _check_fullsize_against_golden(g):
+    from oracle import fullsize as F
+    keys, sizes = G.input_of(g)
+    res = F.ams_sort_fullsize(keys, sizes, tuple(g["groups"]), g["a"], g["b"], g["eps"],
+                              g["master_seed"], g["stream"], threads=4)
+    assert list(res.pe_sizes) == g["pe_sizes"]
+    assert G.sha_u64(res.keys) == g["output_sha256"]
+    for facts, ref in zip(res.levels, g["levels"]):
+        assert len(facts) == len(ref)
+        for f, rg in zip(facts, ref):
+            assert f.group_lo == rg["group_lo"] and f.n_g == rg["n_g"]
+            assert f.sample_size == rg["sample_size"] and f.bucket_count == rg["bucket_count"]
+            assert [int(x) for x in f.splitter_keys] == rg["splitter_keys"]
+            assert [int(x) for x in f.hist.sum(axis=0)] == rg["global_hist"]
+            assert list(f.boundaries) == rg["boundaries"] and list(f.loads) == rg["loads"]
+            assert f.new_sizes == rg["new_sizes"]
+
+
+SIMPLE_FAST = [n for n in FAST if G.load(n).get("scheme", "simple") == "simple"
+               and "error" not in G.load(n)]
+
+
+@pytest.mark.parametrize("name", SIMPLE_FAST + ["cfg2_scaled", "cfg3_scaled"])
+def test_fullsize_oracle_matches_reference_golden(name):
+    _check_fullsize_against_golden(G.load(name))
+
+
+@pytest.mark.parametrize("groups,npe,dist", [
+    ((8, 8), 700, "uniform"), ((8, 32), 90, "zipf"), ((4, 2, 2), 333, "equal"),
+    ((16,), 1000, "sorted"), ((8, 4), 257, "reverse"), ((256,), 40, "uniform"),
+])
+def test_fullsize_matches_oracle(groups, npe, dist):
+    """Per-level histograms, plans, member sizes and the final buffer equal
+    ams_oracle.ams_sort's (ragged PE sizes too)."""
+    from oracle import fullsize as F
+    p = int(np.prod(groups))
+    rng = np.random.default_rng(npe)
+    sizes = [int(x) for x in rng.integers(npe // 2, 2 * npe, p)]
+    n = sum(sizes)
+    keys = {"uniform": lambda: rng.integers(0, 2**64, n, dtype=np.uint64),
+            "zipf": lambda: O.zipf_keys(n, 7),
+            "equal": lambda: np.full(n, 5, np.uint64),
+            "sorted": lambda: np.arange(n, dtype=np.uint64),
+            "reverse": lambda: (n - 1 - np.arange(n)).astype(np.uint64)}[dist]()
+    ref = O.ams_sort(keys, sizes, groups, None, 16, 0.1, 3, "algo/rep0", with_stats=False)
+    res = F.ams_sort_fullsize(keys, sizes, groups, None, 16, 0.1, 3, "algo/rep0", threads=3)
+    assert np.array_equal(res.keys, ref.keys)
+    assert list(res.pe_sizes) == list(ref.pe_sizes)
+    for facts, infos in zip(res.levels, ref.levels):
+        for f, info in zip(facts, infos):
+            assert np.array_equal(f.hist, info.hist)
+            assert tuple(f.boundaries) == tuple(info.plan.boundaries)
+            assert f.new_sizes == list(info.new_sizes)
+            assert np.array_equal(f.splitter_keys, info.splitter_keys)
