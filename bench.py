@@ -49,7 +49,14 @@ WORKLOADS = {
                   groups=(8, 32), a=None, eps=0.1, seed=4, gen="reverse", dtype="u64"),
     "cfg4d": dict(desc="n=2^30 uint64 all equal (42), p=256, (8,32)", log2n=30, p=256,
                   groups=(8, 32), a=None, eps=0.1, seed=4, gen="equal", dtype="u64"),
+    "cfg5k1": dict(desc="KV sweep point: n/GPU=2^24 uint64 keys + uint64 payload (origin index), "
+                        "uniform default_rng(3), p=256, k=1 (256,)", log2n=24, p=256,
+                   groups=(256,), a=None, eps=0.1, seed=3, gen="uniform", dtype="u64", kv=True),
+    "cfg5k2": dict(desc="KV sweep point: n/GPU=2^24 uint64 keys + uint64 payload (origin index), "
+                        "uniform default_rng(3), p=256, k=2 (8,32)", log2n=24, p=256,
+                   groups=(8, 32), a=None, eps=0.1, seed=3, gen="uniform", dtype="u64", kv=True),
 }
+CFG5_LOG2N = (10, 12, 14, 16, 18, 20, 22, 24)   # n/GPU of BASELINE config 5
 
 
 def gen_keys(w: dict, log2n: int) -> np.ndarray:
@@ -296,8 +303,14 @@ def ours_arm(args, w):
     ctx = sorter.ctx
     out = torch.empty_like(keys_dev)
 
+    kv = bool(w.get("kv"))
+    vals_dev = torch.arange(n, dtype=torch.int64, device="cuda") if kv else None
+    out_vals = torch.empty_like(vals_dev) if kv else None
+    width = 16 if kv else 8   # bytes per element moved (key + payload)
+
     def step():
-        return sorter.sort(keys_dev, sizes, params, seed, out=out, key_kind=kind, with_stats=False)
+        return sorter.sort(keys_dev, sizes, params, seed, vals=vals_dev, out=out, out_vals=out_vals,
+                           key_kind=kind, with_stats=False)
 
     for _ in range(max(args.warmup, 0)):
         res = step()
@@ -325,6 +338,8 @@ def ours_arm(args, w):
     ms_per_step = elapsed_ms / args.steps
     value = n / (ms_per_step / 1e3)
     ok_sorted, ok_bound = verify_device(torch, out, keys_dev, res.pe_sizes, w["eps"], p, kind)
+    if kv:  # payload = origin index: it must gather the input into the output
+        ok_sorted = ok_sorted and bool(torch.equal(keys_dev[out_vals], out))
 
     peak, peak_src = measured_peak()
     # dominant kernel = largest share of device time in the timed region
@@ -333,7 +348,7 @@ def ours_arm(args, w):
     achieved = dbytes / (dms / 1e3) / 1e9 if dms > 0 else 0.0
     total_kernel_ms = sum(v[0] for v in stats.values())
     k = len(w["groups"])
-    b_hbm = 2 * 8 * n * (k + 1)
+    b_hbm = 2 * width * n * (k + 1)
     t_roof_ms = b_hbm / (peak * 1e9) * 1e3
     roofline = {
         "bound": "hbm", "kernel": dname, "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -354,7 +369,9 @@ def ours_arm(args, w):
     # keys host -> device (pinned), sorts and copies the result back; the
     # pipeline overlaps step i's sort with step i+1's H2D and step i-1's D2H.
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and kv:
+        e2e = kv_e2e(torch, kt_host, sizes, params, seed, kind, args.steps)
+    elif not args.no_e2e:
         from paper_1410_6754_b200.api import HostSortPipeline
         h_in = kt_host.pin_memory()
         h_out = torch.empty_like(h_in).pin_memory()
@@ -385,24 +402,133 @@ def ours_arm(args, w):
         rate, sample = cpu_port_rate(w)
         cpu = {"value": rate, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample,
                "host_cpus": os.cpu_count()}
+    sweeps = None
+    if args.sweeps and args.workload == "cfg2":
+        sweeps = {"cfg5": cfg5_sweep(torch, sorter, peak), "cfg1": small_point(torch, sorter, peak)}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": kind, "data": "synthetic",
+        "scaling": "weak" if kv else "strong", "vs_baseline": None, "dtype": kind,
+        "data": "synthetic",
         "config": {"workload": args.workload, "desc": w["desc"], "n": n, "p": p,
                    "groups": list(w["groups"]), "eps": w["eps"], "a": w["a"], "b": 16,
                    "scheme": "simple", "sample_mode": "parity (reference seeded streams)",
-                   "l2": "inputs (8 B x n) larger than the 126 MB L2 between steps",
+                   "payload": "u64 origin index" if kv else None,
+                   "l2": (f"inputs ({width} B x n = {width * n / 2**20:.0f} MiB) "
+                          + ("larger than" if width * n > 126 * 2**20 else "NOT larger than")
+                          + " the 126 MB L2 between steps"),
                    "parallelism": f"{p} PEs on {world} GPU(s)"},
         "verified": {"sorted_and_checksum": ok_sorted, "pe_size_bound": ok_bound},
         "gpu_launches": launches, "launches_per_step": launches / args.steps,
         "roofline": roofline, "kernels": kernels, "final_sort_cells": fstats, "clocks": clk,
         "e2e": e2e, "cpu_baseline": cpu,
     }
+    if sweeps is not None:
+        line["sweeps"] = sweeps
     if rank == 0:
         print(json.dumps(line), flush=True)
     return 0
+
+
+def _time_steps(torch, fn, steps: int, warmup: int) -> float:
+    """ms per call of fn, CUDA events on the current stream around `steps`
+    back-to-back calls after `warmup` untimed ones."""
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps
+
+
+def cfg5_sweep(torch, sorter, peak):
+    """BASELINE config 5 on this GPU (weak scaling: n = n/GPU at N=1): uint64
+    keys + uint64 payload (origin index), uniform default_rng(3), p=256,
+    k=1 (256,) and k=2 (8,32), n/GPU = 2^10..2^24; keys/s and the fraction of
+    the HBM roofline 2*16*n*(k+1) B / peak.  Every point is
+    checked: payload gathers the input into the sorted output."""
+    from paper_1410_6754_b200 import AmsParams, SeedSpec
+    out = {}
+    for groups in ((256,), (8, 32)):
+        k = len(groups)
+        pts = []
+        for lg in CFG5_LOG2N:
+            n = 1 << lg
+            keys = torch.from_numpy(np.random.default_rng(3).integers(0, 2**64, n, dtype=np.uint64)
+                                    .view(np.int64)).cuda()
+            vals = torch.arange(n, dtype=torch.int64, device="cuda")
+            ok_, ov_ = torch.empty_like(keys), torch.empty_like(vals)
+            params = AmsParams(groups, None, 16, 0.1)
+            seed = SeedSpec(3, "algo/rep0")
+
+            def fn():
+                return sorter.sort(keys, [n // 256] * 256, params, seed, vals=vals, out=ok_,
+                                   out_vals=ov_, key_kind="u64", with_stats=False)
+            steps = 20 if lg <= 20 else 10
+            ms = _time_steps(torch, fn, steps, 3)
+            flip = -(2**63)
+            o = ok_ ^ flip
+            ok = bool((o[1:] >= o[:-1]).all()) and bool(torch.equal(keys[ov_], ok_))
+            t_roof = 2 * 16 * n * (k + 1) / (peak * 1e9) * 1e3
+            pts.append({"n_per_gpu": n, "ms_per_step": ms, "keys_per_s": n / (ms / 1e3),
+                        "t_roof_ms": t_roof, "frac": t_roof / ms, "verified": ok})
+        out[f"k{k}"] = pts
+    return {"desc": "config 5 KV sweep, one GPU (n = n/GPU), p=256, w=16 B, CUDA events", **out}
+
+
+def small_point(torch, sorter, peak):
+    """BASELINE config 1 on the GPU (n=2^20 from the reference's own
+    generate_input(seed 0), p=16, (16,), a=16): latency-bound."""
+    from paper_1410_6754_b200 import AmsParams, SeedSpec
+    w = WORKLOADS["cfg1"]
+    keys_h = gen_keys(w, 20)
+    keys = torch.from_numpy(keys_h.view(np.int64)).cuda()
+    out = torch.empty_like(keys)
+    params = AmsParams((16,), 16.0, 16, 0.1)
+    seed = SeedSpec(0, "algo/rep0")
+
+    def fn():
+        return sorter.sort(keys, [1 << 16] * 16, params, seed, out=out, key_kind="u64",
+                           with_stats=False)
+    ms = _time_steps(torch, fn, 50, 5)
+    ok = bool(np.array_equal(out.cpu().numpy().view(np.uint64), np.sort(keys_h)))
+    t_roof = 2 * 8 * (1 << 20) * 2 / (peak * 1e9) * 1e3
+    return {"desc": w["desc"], "ms_per_step": ms, "keys_per_s": (1 << 20) / (ms / 1e3),
+            "t_roof_ms": t_roof, "frac": t_roof / ms, "verified": ok}
+
+
+def kv_e2e(torch, kt_host, sizes, params, seed, kind, steps):
+    """End to end for key+payload workloads through the public tensor API:
+    each step copies keys and payloads host -> device (pinned), sorts, and
+    copies both results back; wall time over the steps."""
+    from paper_1410_6754_b200 import ams_sort_tensors
+    n = kt_host.numel()
+    h_k = kt_host.pin_memory()
+    h_v = torch.arange(n, dtype=torch.int64).pin_memory()
+    o_k, o_v = torch.empty_like(h_k).pin_memory(), torch.empty_like(h_v).pin_memory()
+
+    def fn():
+        dk = h_k.to("cuda", non_blocking=True)
+        dv = h_v.to("cuda", non_blocking=True)
+        r = ams_sort_tensors(dk, sizes, params, seed, vals=dv, key_kind=kind)
+        o_k.copy_(r.keys, non_blocking=True)
+        o_v.copy_(r.vals, non_blocking=True)
+    fn()
+    torch.cuda.synchronize()
+    ke = max(2, min(steps, 8))
+    t0 = time.perf_counter()
+    for _ in range(ke):
+        fn()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    return {"value": n * ke / wall, "unit": UNIT, "h2d_bytes_per_step": 16 * n,
+            "d2h_bytes_per_step": 16 * n, "ms_per_step": wall * 1e3 / ke, "steps": ke,
+            "api": "paper_1410_6754_b200.ams_sort_tensors (pinned host keys + payloads)"}
 
 
 def gen_local_keys(w: dict, log2n: int, rank: int, world: int) -> np.ndarray:
@@ -593,6 +719,8 @@ def main():
     ap.add_argument("--workload", default=None, choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-sweeps", dest="sweeps", action="store_false",
+                    help="skip the config 5 KV sweep and config 1 point added to the default line")
     ap.add_argument("--dist", action="store_true",
                     help="use the multi-GPU (torch.distributed) path even on one GPU")
     args = ap.parse_args()
