@@ -233,15 +233,6 @@ int ams_final_sort_stats(ams_ctx_t* ctx, uint64_t out[2]);
  * partition, and those of them whose cells overflowed (re-partitioned
  * exactly), summed since the context was created: out = {buckets, overflowed}. */
 int ams_final_sort_fixed_stats(ams_ctx_t* ctx, uint64_t out[2]);
-/* Keys-only last levels run in one pass into fixed-capacity bucket regions
- * (no histogram pass; ams_sort_run): out = {such levels, levels redone
- * exactly because a region ran full}, summed since the context was created. */
-int ams_region_stats(ams_ctx_t* ctx, uint64_t out[2]);
-/* Region capacity slack of those levels: a bucket holding k sample elements
- * of a group (n_g keys, sample S) gets n_g/S * (k + factor*sqrt(k) + 8) + 64
- * slots (default factor 5; negative: 2 slots, so every such level takes the
- * exact fallback — a test hook).  It never changes results. */
-int ams_ctx_set_region_factor(ams_ctx_t* ctx, double factor);
 
 /* Plain copy with key mapping (used for the p == 1 / k == 0 edge and the
  * host-buffer end-to-end path). */

@@ -60,8 +60,6 @@ _SIGNATURES = {
     "ams_level_scatter": (_I, [_P, _P, _P, _I, _P, _P, _I, _P, _P, _I, _I]),
     "ams_final_sort_stats": (_I, [_P, _P]),
     "ams_final_sort_fixed_stats": (_I, [_P, _P]),
-    "ams_region_stats": (_I, [_P, _P]),
-    "ams_ctx_set_region_factor": (_I, [_P, C.c_double]),
     "ams_run_id": (C.c_uint64, [_P]),
     "ams_run_level_dims_at": (_I, [_P, C.c_uint64, _I, _P, _P, _P, _P, _P]),
     "ams_run_level_at": (_I, [_P, C.c_uint64, _I] + [_P] * 11),
@@ -388,14 +386,8 @@ class Context:
         check(lib.ams_final_sort_stats(self.h, out.ctypes.data))
         fx = np.zeros(2, np.uint64)
         check(lib.ams_final_sort_fixed_stats(self.h, fx.ctypes.data))
-        rg = np.zeros(2, np.uint64)
-        check(lib.ams_region_stats(self.h, rg.ctypes.data))
         return {"overflow_cells": int(out[0]), "fallback_cells": int(out[1]),
-                "fixed_buckets": int(fx[0]), "fixed_overflow_buckets": int(fx[1]),
-                "region_levels": int(rg[0]), "region_fallbacks": int(rg[1])}
-
-    def set_region_factor(self, factor: float):
-        check(lib.ams_ctx_set_region_factor(self.h, float(factor)))
+                "fixed_buckets": int(fx[0]), "fixed_overflow_buckets": int(fx[1])}
 
     def get_minmax(self):
         out = np.zeros(2, np.uint64)

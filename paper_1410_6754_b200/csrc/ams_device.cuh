@@ -115,14 +115,16 @@ __device__ __forceinline__ uint64_t ldg_stream(const uint64_t* p) {
 // ---- tree classifier in shared memory ------------------------------------
 // Shared-memory loads by 32-bit shared address (a generic pointer kept in a
 // struct compiles to generic LD.E; these stay LDS).
+// The "memory" clobber keeps them after the __syncthreads() that publishes
+// the tree (the compiler may otherwise hoist them above the barrier).
 __device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
   uint32_t v;
-  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
   return v;
 }
 __device__ __forceinline__ uint64_t lds_u64(uint32_t a) {
   uint64_t v;
-  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a) : "memory");
   return v;
 }
 

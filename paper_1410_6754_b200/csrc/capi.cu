@@ -201,12 +201,6 @@ struct ams_ctx {
   bool bm_final = true;  // AMS_FINAL_BM=0 keeps the (g(b), j, b) last level + PE digit partition
   bool host_trace = false;  // AMS_HOST_TRACE=1: host-side step times of ams_sort_run on stderr
   int fixed_fill_pct = 88;  // AMS_FIXED_FILL: mean fill of the fixed-capacity cells (percent)
-  // keys-only last level without a histogram pass (k_scatter_cap): fixed-
-  // capacity (group, bucket) regions, their fill counters and overflow flag
-  DevBuf regions, r_fill, r_ovf;
-  Stage st_regions;
-  double region_factor = 5.0;  // capacity = u * (k + factor * sqrt(k) + 8): k = the bucket's sample count
-  uint64_t cap_levels = 0, cap_fallbacks = 0;
   // deterministic delivery: origin tags (tie-breaks) and relayout work items
   const uint64_t* level_tags = nullptr;
   DevBuf tags0;
@@ -393,14 +387,14 @@ int ams_ctx_destroy(ams_ctx_t* c) {
   resolve_timing(c);
   for (cudaEvent_t e : c->free_events) cudaEventDestroy(e);
   for (Stage* s : {&c->st_sample, &c->st_split, &c->st_level, &c->st_scatter, &c->st_final, &c->st_fixed,
-                   &c->st_copy, &c->st_regions})
+                   &c->st_copy})
     s->release();
   for (DevBuf* b : {&c->blobs, &c->sorted_keys, &c->sorted_pos, &c->sample_idx, &c->bounds[0], &c->bounds[1],
                     &c->chunk_tot, &c->seg_hist, &c->cell_base, &c->pieces, &c->minmax, &c->dcls,
                     &c->ovf, &c->ovf_count, &c->fb, &c->fb_count,
                     &c->ids, &c->work[0], &c->work[1], &c->work_v[0], &c->work_v[1], &c->s_keys,
                     &c->s_pos, &c->fx_scratch, &c->fx_fill, &c->fx_ovf, &c->fx_base, &c->fx_cnt,
-                    &c->fx_seg, &c->tags0, &c->regions, &c->r_fill, &c->r_ovf})
+                    &c->fx_seg, &c->tags0})
     b->release();
   c->h_hist.release();
   c->h_small.release();
@@ -910,40 +904,33 @@ int partition_rounds(ams_ctx* c, void* src, void* src_vals, void* tmp, void* tmp
 // others are split into fixed-capacity digit cells in scratch
 // (k_scatter_fixed: no histogram pass), whose sorts write `out`.  Buckets
 // whose cells overflowed go through the exact partition rounds from `src`.
-// bk_out (optional): output index of every bucket when the buckets do not sit
-// at their output positions in `src` (the fixed-capacity regions of
-// k_scatter_cap); tmp2 is then a second n-key scratch buffer.
 int final_sort_bm(ams_ctx* c, void* src, void* tmp, void* out, int key_kind,
                   const std::vector<uint64_t>& bk_off, const std::vector<uint64_t>& bk_len,
                   const std::vector<int32_t>& bk_g, const std::vector<int32_t>& bk_b,
-                  const uint64_t* d_group_bounds, const std::vector<uint64_t>* bk_out = nullptr,
-                  void* tmp2 = nullptr) {
+                  const uint64_t* d_group_bounds) {
   constexpr uint64_t kCap = AMS_SMEM_SORT_CAP;
   // Cells average fixed_fill_pct of capacity: with keys uniform inside a
   // bucket a cell's count is ~ N(target, sqrt(target)), far below capacity.
   const uint64_t kTarget = kCap * (uint64_t)c->fixed_fill_pct / 100;
   constexpr uint64_t kMaxDigits = AMS_MAX_BUCKETS / 2;
-  std::vector<uint64_t> s_off, s_len, s_out, f_off, f_len, f_out;
+  std::vector<uint64_t> s_off, s_len, f_off, f_len;
   std::vector<int32_t> f_gb;
   std::vector<uint32_t> cell0{0};
   uint64_t total = 0, small_n = 0, fixed_n = 0;
   int max_nb = 2;
   for (size_t i = 0; i < bk_off.size(); ++i) {
     const uint64_t len = bk_len[i];
-    const uint64_t oo = bk_out ? (*bk_out)[i] : bk_off[i];
     total += len;
     if (len == 0) continue;
     if (len <= kCap) {
       s_off.push_back(bk_off[i]);
       s_len.push_back(len);
-      s_out.push_back(oo);
       small_n += len;
       continue;
     }
     const uint64_t d = std::min<uint64_t>(kMaxDigits, std::max<uint64_t>(2, (len + kTarget - 1) / kTarget));
     f_off.push_back(bk_off[i]);
     f_len.push_back(len);
-    f_out.push_back(oo);
     f_gb.push_back(bk_g[i]);
     f_gb.push_back(bk_b[i]);
     f_gb.push_back((int32_t)d);
@@ -964,13 +951,11 @@ int final_sort_bm(ams_ctx* c, void* src, void* tmp, void* out, int key_kind,
     Stage& ss = c->st_sample;  // free after the levels
     ss.reset();
     const size_t oo = ss.put(s_off), ol = ss.put(s_len);
-    const size_t ou = bk_out ? ss.put(s_out) : 0;
     AMS_CK(ss.upload(c->stream));
     CellSource cs{};
     cs.mode = 1;
     cs.seg_off = ss.dev<uint64_t>(oo);
     cs.seg_len = ss.dev<uint64_t>(ol);
-    cs.seg_out = bk_out ? ss.dev<uint64_t>(ou) : nullptr;
     int rc = sort_cells(c, src, nullptr, out, nullptr, key_kind, cs, s_off.size(), small_n);
     if (rc) return rc;
   }
@@ -978,7 +963,7 @@ int final_sort_bm(ams_ctx* c, void* src, void* tmp, void* out, int key_kind,
   c->fixed_segments += (uint64_t)nseg;
   Stage& sx = c->st_fixed;
   sx.reset();
-  const size_t o_gb = sx.put(f_gb), o_c0 = sx.put(cell0), o_off = sx.put(f_out);
+  const size_t o_gb = sx.put(f_gb), o_c0 = sx.put(cell0), o_off = sx.put(f_off);
   AMS_CK(sx.upload(c->stream));
   std::vector<int32_t> idx(nseg);
   for (int i = 0; i < nseg; ++i) idx[i] = i;
@@ -1027,7 +1012,7 @@ int final_sort_bm(ams_ctx* c, void* src, void* tmp, void* out, int key_kind,
   AMS_CK(to_host(c->h_big, c->fx_ovf.p, 4 * (size_t)nseg, c->stream));
   AMS_CK(cudaStreamSynchronize(c->stream));
   std::memcpy(flags.data(), c->h_big.p, 4 * (size_t)nseg);
-  std::vector<uint64_t> o_off2, o_len2, o_lo, o_hi, moves;
+  std::vector<uint64_t> o_off2, o_len2, o_lo, o_hi;
   std::vector<DigitCls> dc;
   for (int i = 0; i < nseg; ++i) {
     if (!flags[i]) continue;
@@ -1041,31 +1026,12 @@ int final_sort_bm(ams_ctx* c, void* src, void* tmp, void* out, int key_kind,
     o_len2.push_back(f_len[i]);
     o_lo.push_back(dc[i].lo);
     o_hi.push_back(dc[i].hi);
-    if (bk_out) {  // the partition rounds work in output positions: move the bucket there first
-      for (uint64_t o = 0; o < f_len[i]; o += kCopyItemKeys) {
-        moves.push_back(f_off[i] + o);
-        moves.push_back(f_out[i] + o);
-        moves.push_back(std::min<uint64_t>(kCopyItemKeys, f_len[i] - o));
-      }
-      o_off2.back() = f_out[i];
-    }
   }
   c->fixed_overflow_segments += o_off2.size();
-  if (o_off2.empty()) return AMS_OK;
-  if (bk_out) {
-    if (!tmp2) return set_error(AMS_EINTERNAL, "bucket relocation needs a second scratch buffer");
-    Stage& sc = c->st_copy;
-    sc.reset();
-    const size_t oi = sc.put(moves);
-    AMS_CK(sc.upload(c->stream));
-    AMS_CK(launch_copy_ranges(c->stream, sc.dev<uint64_t>(oi), (int)(moves.size() / 3), src, tmp2,
-                              nullptr, nullptr, 0));
-    c->launches += 1;
-    return partition_rounds(c, tmp2, nullptr, tmp, nullptr, out, nullptr, key_kind, o_off2, o_len2, o_lo,
+  if (!o_off2.empty())
+    return partition_rounds(c, src, nullptr, tmp, nullptr, out, nullptr, key_kind, o_off2, o_len2, o_lo,
                             o_hi, nullptr);
-  }
-  return partition_rounds(c, src, nullptr, tmp, nullptr, out, nullptr, key_kind, o_off2, o_len2, o_lo,
-                          o_hi, nullptr);
+  return AMS_OK;
 }
 
 // Final sort with explicit per-segment key bounds [lo, hi] (no last-level
@@ -1204,20 +1170,6 @@ int ams_final_sort_fixed_stats(ams_ctx_t* c, uint64_t out[2]) {
   return AMS_OK;
 }
 
-int ams_region_stats(ams_ctx_t* c, uint64_t out[2]) {
-  if (!c || !out) return set_error(AMS_EINVAL, "null argument");
-  out[0] = c->cap_levels;
-  out[1] = c->cap_fallbacks;
-  return AMS_OK;
-}
-
-int ams_ctx_set_region_factor(ams_ctx_t* c, double factor) {
-  if (!c) return set_error(AMS_EINVAL, "null context");
-  if (factor != factor) return set_error(AMS_EINVAL, "region factor is NaN");
-  c->region_factor = factor;
-  return AMS_OK;
-}
-
 int ams_final_sort_stats(ams_ctx_t* c, uint64_t out[2]) {
   if (!c || !out) return set_error(AMS_EINVAL, "null argument");
   out[0] = c->overflow_cells;
@@ -1261,110 +1213,6 @@ struct HostTrace {
                  std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count());
   }
 };
-}  // namespace
-
-namespace {
-
-// Keys-only last level in one pass (k_scatter_cap): classify every key with
-// its group's splitter tree and move it into the fixed-capacity region of its
-// (group, bucket), counting the per-member histogram on the way.  Capacities
-// come from the splitters' sample ranks: bucket b of a group holds k_b sample
-// elements, so it expects k_b * n_g / S keys (the Gamma(k_b) spread of a
-// sample gap); the region gets u * (k_b + f * sqrt(k_b) + 8) + 64 slots.
-// On return *overflowed says whether a region ran full (the caller then
-// redoes the level exactly); otherwise h_hist holds the (P, nb_stride)
-// histogram and bk_src the region start of every (group, bucket).
-int last_level_regions(ams_ctx* c, const void* src, int kind, int nseg, const uint64_t* seg_off,
-                       const uint64_t* seg_len, const int32_t* seg_group, int G, const int64_t* posbase,
-                       const std::vector<uint64_t>& n_g, const std::vector<uint64_t>& S_g,
-                       const std::vector<int32_t>& nb, int nb_stride, bool track_minmax,
-                       uint32_t* h_hist, std::vector<uint64_t>& bk_src, bool* overflowed) {
-  std::vector<uint64_t> rbase((size_t)G * nb_stride, 0);
-  std::vector<uint32_t> rcap((size_t)G * nb_stride, 0);
-  uint64_t at = 0;
-  for (int g = 0; g < G; ++g) {
-    const uint64_t S = S_g[g];
-    const int nbg = nb[g];
-    for (int b = 0; b < nbg; ++b) {
-      uint64_t cap;
-      if (nbg == 1 || S == 0) {
-        cap = n_g[g];
-      } else {
-        // splitter i = sorted sample at rank ((i+1) S) / nb (ams.py:190)
-        auto rank = [&](int i) { return (uint64_t)(((unsigned __int128)(i + 1) * S) / (unsigned)nbg); };
-        const uint64_t lo = b == 0 ? 0 : rank(b - 1) + 1;
-        const uint64_t hi = b == nbg - 1 ? S - 1 : rank(b);
-        const double k = (double)(hi >= lo ? hi - lo + 1 : 1);
-        const double u = (double)n_g[g] / (double)S;
-        cap = (uint64_t)std::ceil(u * (k + c->region_factor * std::sqrt(k) + 8.0)) + 64;
-        cap = std::min<uint64_t>(cap, n_g[g]);
-        if (c->region_factor < 0) cap = 2;  // test hook: every region overflows
-      }
-      cap = std::min<uint64_t>((cap + 1) & ~1ull, 0xFFFFFFF0ull);  // even: 16-byte aligned bases
-      rbase[(size_t)g * nb_stride + b] = at;
-      rcap[(size_t)g * nb_stride + b] = (uint32_t)cap;
-      at += cap;
-    }
-  }
-  AMS_CK(c->regions.ensure(8 * (at + 2)));
-  AMS_CK(c->r_fill.ensure(4 * rbase.size()));
-  AMS_CK(c->r_ovf.ensure(16));
-  AMS_CK(c->seg_hist.ensure(sizeof(uint32_t) * (size_t)std::max(nseg, 1) * nb_stride));
-  AMS_CK(cudaMemsetAsync(c->r_fill.p, 0, 4 * rbase.size(), c->stream));
-  AMS_CK(cudaMemsetAsync(c->r_ovf.p, 0, 16, c->stream));
-  AMS_CK(cudaMemsetAsync(c->seg_hist.p, 0, sizeof(uint32_t) * (size_t)nseg * nb_stride, c->stream));
-  Stage& st = c->st_regions;
-  st.reset();
-  const size_t ob = st.put(rbase), oc = st.put(rcap);
-  AMS_CK(st.upload(c->stream));
-  AMS_CK(upload_segments(c->st_level, c->stream, seg_off, seg_len, seg_group, nseg, posbase, G, &c->meta,
-                         &c->nchunks));
-  c->meta.tags = nullptr;
-  unsigned long long* mm = nullptr;
-  if (track_minmax) {
-    AMS_CK(c->minmax.ensure(16));
-    const unsigned long long init[2] = {~0ULL, 0ULL};
-    AMS_CK(c->h_small.ensure(64));
-    AMS_CK(cudaStreamSynchronize(c->stream));
-    std::memcpy(c->h_small.p, init, sizeof init);
-    AMS_CK(launch_copy_bytes(c->stream, c->minmax.p, c->h_small.dp, sizeof init));
-    mm = c->minmax.as<unsigned long long>();
-  }
-  uint64_t nel = 0;
-  for (int i = 0; i < nseg; ++i) nel += seg_len[i];
-  {
-    KTimer kt(c, AMS_KCAT_SCATTER_U, 16.0 * (double)nel);
-    AMS_CK(launch_scatter_cap(c->stream, src, kind, c->regions.p, c->meta, c->nchunks, c->blobs.as<uint8_t>(),
-                              c->nspl_cap, c->cells_cap, nb_stride, st.dev<uint64_t>(ob), st.dev<uint32_t>(oc),
-                              c->r_fill.as<uint32_t>(), c->seg_hist.as<uint32_t>(), c->r_ovf.as<unsigned int>(),
-                              mm));
-  }
-  c->launches += 1;
-  c->cap_levels += 1;
-  if (track_minmax) {
-    AMS_CK(c->bounds[0].ensure(16 * (size_t)G));
-    AMS_CK(launch_copy_bytes(c->stream, c->bounds[0].p, c->minmax.p, 16));
-    c->bcur = 0;
-  }
-  // The level's one host read: histogram and overflow flag (mapped memory).
-  const size_t hb = sizeof(uint32_t) * (size_t)nseg * nb_stride;
-  AMS_CK(c->h_hist.ensure(hb + 16));
-  AMS_CK(launch_copy_bytes(c->stream, c->h_hist.dp, c->seg_hist.p, hb));
-  AMS_CK(launch_copy_bytes(c->stream, static_cast<uint8_t*>(c->h_hist.dp) + ((hb + 15) & ~(size_t)15),
-                           c->r_ovf.p, 4));
-  AMS_CK(cudaStreamSynchronize(c->stream));
-  uint32_t flag = 0;
-  std::memcpy(&flag, static_cast<uint8_t*>(c->h_hist.p) + ((hb + 15) & ~(size_t)15), 4);
-  *overflowed = flag != 0;
-  if (*overflowed) {
-    c->cap_fallbacks += 1;
-    return AMS_OK;
-  }
-  std::memcpy(h_hist, c->h_hist.p, hb);
-  bk_src = std::move(rbase);
-  return AMS_OK;
-}
-
 }  // namespace
 
 // Per PE, how many of its level's splitters were drawn from it (host
@@ -1459,9 +1307,7 @@ int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* p
   HostTrace tr(c->host_trace);
   tr.mark("setup");
   int rc;
-  bool used_bm = false, used_cap = false;
-  std::vector<uint64_t> cap_src;         // region start of every (group, bucket) (k_scatter_cap)
-  const uint64_t* cap_bounds = nullptr;  // key bounds of the last level's groups
+  bool used_bm = false;
   for (int lv = 0; lv < k; ++lv) {
     const int r = prm->group_counts[lv];
     const int G = (int)gf.size();
@@ -1528,29 +1374,10 @@ int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* p
     rec.hist.assign((size_t)p * nb_stride, 0);
     c->level_tags = tie_tags;
     tr.mark("sample");
-    // Keys-only last level: one pass into fixed-capacity bucket regions (no
-    // histogram pass); the exact histogram + scatter only if a region overflowed.
-    const bool bm = last && !with_vals && c->bm_final;
-    bool cap_ok = false;
-    if (bm) {
-      std::vector<uint64_t> ng(G, 0);
-      for (int g = 0; g < G; ++g)
-        for (int i = 0; i < gn[g]; ++i) ng[g] += sizes[gf[g] + i];
-      bool ovf = false;
-      if ((rc = last_level_regions(c, src, src_kind, p, offs.data(), sizes.data(), seg_group.data(), G,
-                                   posbase.data(), ng, drawn, nb, nb_stride, lv == 0, rec.hist.data(),
-                                   cap_src, &ovf)))
-        return rc;
-      cap_ok = !ovf;
-      cap_bounds = c->bounds[c->bcur].as<uint64_t>();
-    }
-    if (!cap_ok) {
-      rc = ams_level_classify(c, src, src_kind, p, offs.data(), sizes.data(), seg_group.data(), G,
-                              posbase.data(), nb_stride, lv == 0, !(last && !with_vals), rec.hist.data());
-      c->level_tags = nullptr;
-      if (rc) return rc;
-    }
+    rc = ams_level_classify(c, src, src_kind, p, offs.data(), sizes.data(), seg_group.data(), G,
+                            posbase.data(), nb_stride, lv == 0, !(last && !with_vals), rec.hist.data());
     c->level_tags = nullptr;
+    if (rc) return rc;
     tr.mark("classify+sync");
     rec.boundaries.assign((size_t)G * (r + 1), 0);
     rec.loads.assign((size_t)G * r, 0);
@@ -1564,8 +1391,9 @@ int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* p
       return rc;
     std::vector<uint64_t> dst_start(G);
     for (int g = 0; g < G; ++g) dst_start[g] = offs[gf[g]];
-    void* dst = cap_ok ? c->regions.p : c->work[lv % 2].p;
+    void* dst = c->work[lv % 2].p;
     void* dst_v = with_vals ? c->work_v[lv % 2].p : nullptr;
+    const bool bm = last && !with_vals && c->bm_final;
     // Deterministic delivery where subgroups have several members: member
     // assignment per group (host), the simple layout into scratch, then the
     // slices copied to the members' arrays in receive order.
@@ -1617,8 +1445,8 @@ int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* p
       sdst_v = lv == 0 ? c->work_v[1].p : c->tags0.p;
     }
     tr.mark("plan");
-    if (!cap_ok && (rc = level_scatter_impl(c, src, src_v, src_kind, sdst, sdst_v, r, rec.boundaries.data(),
-                                         dst_start.data(), 0, G * r, bm)))
+    if ((rc = level_scatter_impl(c, src, src_v, src_kind, sdst, sdst_v, r, rec.boundaries.data(),
+                                 dst_start.data(), 0, G * r, bm)))
       return rc;
     tr.mark("scatter");
     if (relayout) {
@@ -1632,7 +1460,6 @@ int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* p
       c->launches += 1;
     }
     used_bm = bm;
-    used_cap = cap_ok;
     // Level report (ams.py:258-268, 294-308).
     if (reports) {
       ams_level_report_t& rp = reports[lv];
@@ -1675,10 +1502,9 @@ int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* p
   void* tmp_v = with_vals ? c->work_v[k % 2].p : nullptr;
   tr.mark("levels-end");
   if (used_bm) {
-    // Buckets of the bucket-major last level, in output order (and, after
-    // k_scatter_cap, where their regions start).
+    // Buckets of the bucket-major last level, in output order.
     const ams_ctx::LevelRec& L = c->run_levels[k - 1];
-    std::vector<uint64_t> bo, bl, bout;
+    std::vector<uint64_t> bo, bl;
     std::vector<int32_t> bg, bb;
     uint64_t at = 0;
     for (int g = 0; g < L.G; ++g) {
@@ -1686,21 +1512,16 @@ int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* p
         uint64_t h = 0;
         for (int j = 0; j < L.group_npe[g]; ++j)
           h += L.hist[(size_t)(L.group_first[g] + j) * L.nb_stride + b];
-        bo.push_back(used_cap ? cap_src[(size_t)g * L.nb_stride + b] : at);
-        bout.push_back(at);
+        bo.push_back(at);
         bl.push_back(h);
         bg.push_back(g);
         bb.push_back(b);
         at += h;
       }
     }
-    if (used_cap)
-      rc = final_sort_bm(c, c->regions.p, c->work[0].p, dst_out, prm->key_kind, bo, bl, bg, bb, cap_bounds,
-                         &bout, c->work[1].p);
-    else
-      rc = final_sort_bm(c, const_cast<void*>(src), tmp, dst_out, prm->key_kind, bo, bl, bg, bb,
-                         c->bounds[1 - c->bcur].as<uint64_t>());
-    if (rc) return rc;
+    if ((rc = final_sort_bm(c, const_cast<void*>(src), tmp, dst_out, prm->key_kind, bo, bl, bg, bb,
+                            c->bounds[1 - c->bcur].as<uint64_t>())))
+      return rc;
   } else if (det && !user_vals) {
     // Keys only: equal keys are indistinguishable, so a key sort suffices.
     if ((rc = ams_final_sort(c, const_cast<void*>(src), nullptr, tmp, nullptr, dst_out, nullptr,

@@ -886,6 +886,10 @@ __global__ void __launch_bounds__(kThreadsU, 2)
     __syncthreads();
     for (uint32_t j = tid; j < tc; j += kThreadsU) dst[adj[bkt[j]] + j] = buf[j];
     for (int j = 0; j < per; ++j) cnt[tid * per + j] = 0;
+    // This thread's generic-proxy writes into the tile buffer (the in-place
+    // permutation) must be ordered before the bulk copy (async proxy) that
+    // refills the buffer two tiles on: every writer fences, then the barrier.
+    fence_proxy_async();
     __syncthreads();
   }
 }
@@ -1046,192 +1050,11 @@ __global__ void __launch_bounds__(kThreadsU, 2)
       }
     }
     for (int j = 0; j < per; ++j) cnt[tid * per + j] = 0;
+    // This thread's generic-proxy writes into the tile buffer (the in-place
+    // permutation) must be ordered before the bulk copy (async proxy) that
+    // refills the buffer two tiles on: every writer fences, then the barrier.
+    fence_proxy_async();
     __syncthreads();
-  }
-}
-
-// Keys-only last level in one pass (no histogram pass before it): only PE
-// membership matters there (F7), and a PE's keys are the buckets of a
-// consecutive range, so every key goes to the fixed-capacity region of its
-// (group, bucket) in any order.  Per tile: the bulk copy stages 4096 keys, the
-// group's splitter tree classifies them (ams.py:201-211), a shared atomic per
-// key (one per warp when the warp's 32 keys share a bucket) ranks them, and
-// every (tile, bucket) run reserves room in its region with one global atomic;
-// the tile is permuted bucket-major in shared memory and written as runs.  The
-// per-segment histogram (the plan's input, ams.py:236-238) is counted on the
-// way: shared counters over the chunk, one global atomic per bucket at the end.
-// A run that would pass its region's capacity writes what fits and raises
-// *ovf; the host then redoes the level exactly (histogram + scatter) from
-// `src`, which this kernel does not modify.  MINMAX: also the key range (the
-// first level's group bounds).
-template <int KIND, bool MINMAX>
-__global__ void __launch_bounds__(kThreadsU, 2)
-    k_scatter_cap(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst, SegMeta m,
-                  const uint8_t* __restrict__ blobs, int nspl_cap, int nb,
-                  const uint64_t* __restrict__ rbase, const uint32_t* __restrict__ rcap,
-                  uint32_t* __restrict__ fill, uint32_t* __restrict__ seg_hist,
-                  unsigned int* __restrict__ ovf, unsigned long long* __restrict__ minmax) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  __shared__ int s_seg;
-  __shared__ uint32_t s_scan[kWarpsU + 1];
-  __shared__ uint32_t s_clip;
-  __shared__ __align__(8) uint64_t s_bar[2];
-  __shared__ unsigned long long s_mn[kWarpsU], s_mx[kWarpsU];
-  constexpr int kBuf = kTile + 2;
-  uint64_t* buf0 = reinterpret_cast<uint64_t*>(smem);
-  const int tid = threadIdx.x;
-  const uint64_t c = blockIdx.x;
-  if (tid == 0) {
-    s_seg = upper_bound_u64(m.chunk_prefix, m.nseg + 1, c) - 1;
-    s_clip = 0;
-    mbar_init(&s_bar[0], 1);
-    mbar_init(&s_bar[1], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  const int s = s_seg;
-  const int per = (nb + kThreadsU - 1) / kThreadsU | 1;  // buckets per scan thread (odd: no conflicts)
-  const int nbp = per * kThreadsU;
-  int64_t* adj = reinterpret_cast<int64_t*>(buf0 + 2 * kBuf);  // this tile: dst index - slot
-  uint32_t* cnt = reinterpret_cast<uint32_t*>(adj + nbp);       // counts, then tile starts
-  int32_t* lim = reinterpret_cast<int32_t*>(cnt + nbp);         // writable slots of the run
-  uint32_t* shist = reinterpret_cast<uint32_t*>(lim + nbp);     // chunk histogram
-  uint16_t* bkt = reinterpret_cast<uint16_t*>(shist + nbp);
-  uint8_t* clsmem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(bkt + kTile) + 15) & ~static_cast<uintptr_t>(15));
-  const uint64_t seg_off = m.off[s];
-  const uint64_t first = (c - m.chunk_prefix[s]) * (uint64_t)kChunk;
-  const uint64_t last = min(first + (uint64_t)kChunk, m.len[s]);
-  const int ntiles = (int)((last - first + kTile - 1) / kTile);
-  const int g = m.cls[s];
-  const uint64_t* rb = rbase + (size_t)g * nb;
-  const uint32_t* rc = rcap + (size_t)g * nb;
-  uint32_t* rf = fill + (size_t)g * nb;
-  auto issue = [&](int t) {
-    const uint64_t base = seg_off + first + (uint64_t)t * kTile;
-    const uint32_t tc = (uint32_t)min((uint64_t)kTile, last - first - (uint64_t)t * kTile);
-    const uint32_t h = (uint32_t)(base & 1);
-    bulk_load(buf0 + (t & 1) * kBuf, src + (base - h), ((tc + h) & ~1u) * 8, &s_bar[t & 1]);
-  };
-  if (tid == 0 && ntiles > 0) issue(0);
-  for (int b = tid; b < nbp; b += kThreadsU) { cnt[b] = 0; shist[b] = 0; }
-  const TreeView tv = load_tree(blobs + (size_t)g * kBlobStride, clsmem, nspl_cap);
-  const int64_t posbase = m.posbase[g];
-  const int w = tid >> 5, lane = tid & 31;
-  unsigned long long mn = ~0ULL, mx = 0;
-  uint32_t hint = kInvalid;
-  __syncthreads();
-  for (int t = 0; t < ntiles; ++t) {
-    uint64_t* buf = buf0 + (t & 1) * kBuf;
-    const uint64_t base = seg_off + first + (uint64_t)t * kTile;
-    const uint32_t tc = (uint32_t)min((uint64_t)kTile, last - first - (uint64_t)t * kTile);
-    const uint32_t h = (uint32_t)(base & 1);
-    if (tid == 0 && t + 1 < ntiles) {
-      fence_proxy_async();
-      issue(t + 1);
-    }
-    mbar_wait(&s_bar[t & 1], (uint32_t)(t >> 1) & 1u);
-    if ((tc + h) & 1) {  // the last key is outside the 16-byte copy
-      if (tid == 0) buf[tc - 1 + h] = src[base + tc - 1];
-      __syncthreads();
-    }
-    const uint64_t* tb = buf + h;
-    const uint32_t pos0 = (uint32_t)((int64_t)base + posbase);
-    uint64_t kr[kItemsU];
-    uint32_t pk[kItemsU];
-    auto classify_all = [&](auto full_tag) {
-      constexpr bool FULL = decltype(full_tag)::value;
-#pragma unroll
-      for (int i = 0; i < kItemsU; ++i) {
-        const uint32_t e = w * (kItemsU * 32) + i * 32 + lane;
-        pk[i] = kInvalid;
-        if (FULL || e < tc) {
-          const uint64_t key = to_ordered<KIND>(tb[e]);
-          const uint32_t b = tv.classify(key, pos0 + e, hint);
-          kr[i] = key;
-          if constexpr (MINMAX) { mn = min(mn, (unsigned long long)key); mx = max(mx, (unsigned long long)key); }
-          if (FULL) {  // a warp whose keys share a bucket takes one atomic
-            const uint32_t b0 = __shfl_sync(0xffffffffu, b, 0);
-            if (__all_sync(0xffffffffu, b == b0)) {
-              uint32_t base0 = 0;
-              if (lane == 0) base0 = atomicAdd(&cnt[b0], 32u);
-              pk[i] = (b0 << 16) | (__shfl_sync(0xffffffffu, base0, 0) + lane);
-              continue;
-            }
-          }
-          pk[i] = (b << 16) | atomicAdd(&cnt[b], 1u);
-        }
-      }
-    };
-    if (tc == (uint32_t)kTile) classify_all(std::true_type{});
-    else classify_all(std::false_type{});
-    if (pk[kItemsU - 1] != kInvalid) hint = pk[kItemsU - 1] >> 16;
-    __syncthreads();
-    {
-      const int b0 = tid * per;
-      uint32_t sum = 0;
-      for (int j = 0; j < per; ++j) sum += cnt[b0 + j];
-      const uint32_t inc = warp_incl_scan(sum);
-      if (lane == 31) s_scan[w] = inc;
-      scan_warp_totals<kThreadsU>(s_scan);
-      uint32_t start = s_scan[w] + inc - sum;
-      for (int j = 0; j < per; ++j) {
-        const int b = b0 + j;
-        const uint32_t v = cnt[b];
-        cnt[b] = start;
-        if (v) {
-          shist[b] += v;
-          const uint32_t at = atomicAdd(&rf[b], v);  // reserve the run's room in region (g, b)
-          adj[b] = (int64_t)(rb[b] + at) - (int64_t)start;
-          const int64_t room = (int64_t)rc[b] - (int64_t)at;
-          lim[b] = (int32_t)max((int64_t)0, min((int64_t)v, room)) + (int32_t)start;
-          if (room < (int64_t)v) {
-            s_clip = 1;
-            *ovf = 1u;
-          }
-        }
-        start += v;
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < kItemsU; ++i) {
-      if (pk[i] != kInvalid) {
-        const uint32_t b = pk[i] >> 16;
-        const uint32_t slot = cnt[b] + (pk[i] & 0xFFFFu);
-        buf[slot] = kr[i];
-        bkt[slot] = (uint16_t)b;
-      }
-    }
-    __syncthreads();
-    if (!s_clip) {
-      for (uint32_t j = tid; j < tc; j += kThreadsU) dst[adj[bkt[j]] + j] = buf[j];
-    } else {
-      for (uint32_t j = tid; j < tc; j += kThreadsU) {
-        const uint32_t b = bkt[j];
-        if ((int32_t)j < lim[b]) dst[adj[b] + j] = buf[j];
-      }
-    }
-    for (int j = 0; j < per; ++j) cnt[tid * per + j] = 0;
-    __syncthreads();
-  }
-  for (int b = tid; b < nb; b += kThreadsU) {
-    const uint32_t v = shist[b];
-    if (v) atomicAdd(&seg_hist[(uint64_t)s * nb + b], v);
-  }
-  if constexpr (MINMAX) {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-      mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    }
-    if (lane == 0) { s_mn[w] = mn; s_mx[w] = mx; }
-    __syncthreads();
-    if (tid == 0) {
-      for (int ww = 1; ww < kWarpsU; ++ww) { mn = min(mn, s_mn[ww]); mx = max(mx, s_mx[ww]); }
-      atomicMin(&minmax[0], mn);
-      atomicMax(&minmax[1], mx);
-    }
   }
 }
 
@@ -1368,7 +1191,7 @@ __device__ __forceinline__ void cell_of(const CellSource& cs, uint64_t cid, uint
   } else if (cs.mode == 1) {
     off = cs.seg_off[cid];
     count = cs.seg_len[cid];
-    oo = cs.seg_out ? cs.seg_out[cid] : off;
+    oo = off;
   } else if (cs.mode == 2) {
     if (cs.nrecs && cid >= *cs.nrecs) { off = 0; count = 0; oo = 0; return; }
     off = cs.recs[cid].off;
@@ -2458,37 +2281,6 @@ cudaError_t launch_scatter_fixed(cudaStream_t st, const void* src, int kind, voi
   e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   fn<<<(unsigned)nchunks, kThreadsU, smem, st>>>(s, d, m, dcls, cell0, fill, seg_ovf);
-  return cudaGetLastError();
-}
-
-size_t scatter_cap_smem_bytes(int nb, int nspl_cap, int cells_cap) {
-  const int per = (nb + kThreadsU - 1) / kThreadsU | 1;
-  const size_t nbp = (size_t)per * kThreadsU;
-  size_t b = 2 * 8 * (size_t)(kTile + 2) + 20 * nbp + 2 * (size_t)kTile;
-  b = (b + 15) & ~(size_t)15;
-  return b + tree_smem_bytes(nspl_cap, cells_cap) + 16;
-}
-
-cudaError_t launch_scatter_cap(cudaStream_t st, const void* src, int kind, void* dst, const SegMeta& m,
-                               uint64_t nchunks, const uint8_t* blobs, int nspl_cap, int cells_cap,
-                               int nb, const uint64_t* rbase, const uint32_t* rcap, uint32_t* fill,
-                               uint32_t* seg_hist, unsigned int* ovf, unsigned long long* minmax) {
-  if (nchunks == 0) return cudaSuccess;
-  const size_t smem = scatter_cap_smem_bytes(nb, nspl_cap, cells_cap);
-  const uint64_t* s = static_cast<const uint64_t*>(src);
-  uint64_t* d = static_cast<uint64_t*>(dst);
-  cudaError_t e = cudaSuccess;
-#define AMS_CAP_GO(K, MM)                                                                        \
-  {                                                                                              \
-    auto fn = k_scatter_cap<K, MM>;                                                              \
-    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);        \
-    if (e != cudaSuccess) return e;                                                              \
-    fn<<<(unsigned)nchunks, kThreadsU, smem, st>>>(s, d, m, blobs, nspl_cap, nb, rbase, rcap, fill, \
-                                                    seg_hist, ovf, minmax);                      \
-  }
-  if (minmax) AMS_KIND_DISPATCH(kind, K, AMS_CAP_GO(K, true))
-  else AMS_KIND_DISPATCH(kind, K, AMS_CAP_GO(K, false))
-#undef AMS_CAP_GO
   return cudaGetLastError();
 }
 

@@ -39,7 +39,6 @@ struct CellSource {
   const DigitCls* dcls;
   const uint64_t* seg_off;
   const uint64_t* seg_len;
-  const uint64_t* seg_out;   // mode 1: output index of each segment (null: same as seg_off)
   const OverflowRec* recs;
   const unsigned int* nrecs;  // mode 2: record count on the device (may be null)
   // mode 3 = fixed-capacity cells (k_scatter_fixed): cell ci at src[ci * cap],
@@ -116,15 +115,6 @@ cudaError_t launch_scatter_fixed(cudaStream_t st, const void* src, int kind, voi
                                  const SegMeta& m, uint64_t nchunks, int max_nb,
                                  const DigitCls* dcls, const uint32_t* cell0, uint32_t* fill,
                                  uint32_t* seg_ovf);
-// Keys-only last level without a histogram pass: every key to the
-// fixed-capacity region of its (group, bucket) (rbase/rcap/fill indexed
-// g * nb + b, group g = m.cls[segment]), per-segment histogram counted into
-// seg_hist[s * nb + b]; *ovf set when a region overflowed (see k_scatter_cap).
-size_t scatter_cap_smem_bytes(int nb, int nspl_cap, int cells_cap);
-cudaError_t launch_scatter_cap(cudaStream_t st, const void* src, int kind, void* dst, const SegMeta& m,
-                               uint64_t nchunks, const uint8_t* blobs, int nspl_cap, int cells_cap,
-                               int nb, const uint64_t* rbase, const uint32_t* rcap, uint32_t* fill,
-                               uint32_t* seg_hist, unsigned int* ovf, unsigned long long* minmax);
 cudaError_t launch_fixed_cells(cudaStream_t st, const uint32_t* fill, const uint32_t* cell0,
                                const uint64_t* seg_off, const uint32_t* seg_ovf, int nseg,
                                uint64_t* out_base, uint32_t* cnt, uint32_t* cell_seg);

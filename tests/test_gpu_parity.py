@@ -426,3 +426,4 @@ def test_host_pipeline_batches(api):
         assert np.array_equal(o.numpy().view(np.uint64), np.sort(b))
         ref = O.ams_sort(b, [npe] * p, (8, 8), None, 16, 0.1, 1, "algo/rep0")
         assert [int(x) for x in sz] == list(ref.pe_sizes)
+
