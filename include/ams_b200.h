@@ -203,6 +203,31 @@ int ams_level_scatter_ex(ams_ctx_t* ctx, const void* src, const void* src_vals, 
                          const uint64_t* h_group_dst_start, int child_first, int child_count,
                          int flags);
 
+/* ---- multi-GPU level 1 over NVLink (one process per GPU) ----------------
+ * The first level's single group spans every GPU: each GPU
+ * scatters its PEs' keys straight into the receive buffers of the GPUs that
+ * own the destination groups (Network.exchange, simnet.py:294-335: group g's
+ * buffer is the concatenation of the source PEs' pieces in PE order).
+ *
+ * ams_peer_buffer: library-owned device buffer `slot` (0..7) of at least
+ * `bytes`, its address and the 64-byte CUDA IPC handle peers open; *grown = 1
+ * when it was (re)allocated, so peers must re-open it.
+ * ams_peer_open: map a peer process's buffer (cudaIpcOpenMemHandle with lazy
+ * peer access; cached per handle); ams_peer_close_all unmaps them.
+ * ams_level_scatter_peers: after ams_level_classify of the local PEs (one
+ * group), bucket b of local segment s goes to buffer dst[bucket_dst[b]] at
+ * index cell_base[s * nb + b] + its stable rank (values to dst_vals[...]).
+ * Also derives the key bounds of children [child_first, child_first +
+ * child_count) of the r children (this GPU's next-level groups).  The
+ * caller synchronises the GPUs before and after (its barrier). */
+int ams_peer_buffer(ams_ctx_t* ctx, int slot, uint64_t bytes, void** dptr, void* ipc_handle, int* grown);
+int ams_peer_open(ams_ctx_t* ctx, const void* ipc_handle, void** dptr);
+int ams_peer_close_all(ams_ctx_t* ctx);
+int ams_level_scatter_peers(ams_ctx_t* ctx, const void* src, const void* src_vals, int key_kind, int ndst,
+                            void* const* dst, void* const* dst_vals, const int32_t* bucket_dst,
+                            const uint64_t* cell_base, int r, const uint64_t* h_boundaries, int child_first,
+                            int child_count);
+
 /* Global min/max key seen by a track_minmax classify (ordered encoding);
  * the multi-rank driver all-reduces them and writes them back before the
  * final sort so every rank's key ranges are true bounds. */

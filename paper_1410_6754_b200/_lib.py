@@ -67,6 +67,10 @@ _SIGNATURES = {
     "ams_level_scatter_ex": (_I, [_P, _P, _P, _I, _P, _P, _I, _P, _P, _I, _I, _I]),
     "ams_final_sort_buckets": (_I, [_P, _P, _P, _P, _I, _I, _P, _P, _P, _P]),
     "ams_get_minmax": (_I, [_P, _P]),
+    "ams_peer_buffer": (_I, [_P, _I, C.c_uint64, _P, _P, _P]),
+    "ams_peer_open": (_I, [_P, _P, _P]),
+    "ams_peer_close_all": (_I, [_P]),
+    "ams_level_scatter_peers": (_I, [_P, _P, _P, _I, _I, _P, _P, _P, _P, _I, _P, _I, _I]),
     "ams_set_minmax": (_I, [_P, _P]),
     "ams_final_sort": (_I, [_P, _P, _P, _P, _P, _P, _P, _I, _I, _P, _P]),
     "ams_map_keys": (_I, [_P, _P, _P, _U64, _I, _I]),
@@ -388,6 +392,34 @@ class Context:
         check(lib.ams_final_sort_fixed_stats(self.h, fx.ctypes.data))
         return {"overflow_cells": int(out[0]), "fallback_cells": int(out[1]),
                 "fixed_buckets": int(fx[0]), "fixed_overflow_buckets": int(fx[1])}
+
+    # -- multi-GPU level 1 (peer buffers over NVLink) --------------------------
+    def peer_buffer(self, slot: int, nbytes: int):
+        """(device address, 64-byte IPC handle, grown) of library buffer `slot`."""
+        p = C.c_void_p()
+        h = (C.c_ubyte * 64)()
+        g = C.c_int()
+        check(lib.ams_peer_buffer(self.h, int(slot), int(nbytes), C.byref(p), h, C.byref(g)))
+        return int(p.value), bytes(h), bool(g.value)
+
+    def peer_open(self, handle: bytes) -> int:
+        p = C.c_void_p()
+        hb = (C.c_ubyte * 64).from_buffer_copy(handle)
+        check(lib.ams_peer_open(self.h, hb, C.byref(p)))
+        return int(p.value)
+
+    def peer_close_all(self):
+        check(lib.ams_peer_close_all(self.h))
+
+    def level_scatter_peers(self, src, src_vals, kind, dst_ptrs, dst_vals_ptrs, bucket_dst, cell_base,
+                            r, boundaries, child_first, child_count):
+        nd = len(dst_ptrs)
+        dp = (C.c_void_p * nd)(*dst_ptrs)
+        dv = (C.c_void_p * nd)(*dst_vals_ptrs) if dst_vals_ptrs is not None else None
+        bd, cb, bnd = i32(bucket_dst), u64(cell_base), u64(boundaries)
+        check(lib.ams_level_scatter_peers(self.h, ptr(src), ptr(src_vals), kind, nd, dp, dv, bd.ctypes.data,
+                                          cb.ctypes.data, int(r), bnd.ctypes.data, int(child_first),
+                                          int(child_count)))
 
     def get_minmax(self):
         out = np.zeros(2, np.uint64)

@@ -201,6 +201,10 @@ struct ams_ctx {
   bool bm_final = true;  // AMS_FINAL_BM=0 keeps the (g(b), j, b) last level + PE digit partition
   bool host_trace = false;  // AMS_HOST_TRACE=1: host-side step times of ams_sort_run on stderr
   int fixed_fill_pct = 88;  // AMS_FIXED_FILL: mean fill of the fixed-capacity cells (percent)
+  // multi-GPU: buffers peers map (CUDA IPC) and the peers' buffers mapped here
+  DevBuf peer_buf[8];
+  std::vector<std::pair<std::string, void*>> peer_open;  // (handle bytes, mapped address)
+  Stage st_peers;
   // deterministic delivery: origin tags (tie-breaks) and relayout work items
   const uint64_t* level_tags = nullptr;
   DevBuf tags0;
@@ -396,6 +400,9 @@ int ams_ctx_destroy(ams_ctx_t* c) {
                     &c->s_pos, &c->fx_scratch, &c->fx_fill, &c->fx_ovf, &c->fx_base, &c->fx_cnt,
                     &c->fx_seg, &c->tags0})
     b->release();
+  for (auto& po : c->peer_open) cudaIpcCloseMemHandle(po.second);
+  for (DevBuf& b : c->peer_buf) b.release();
+  c->st_peers.release();
   c->h_hist.release();
   c->h_small.release();
   c->h_big.release();
@@ -727,6 +734,97 @@ int level_scatter_impl(ams_ctx_t* c, const void* src, const void* src_vals, int 
 }  // namespace
 
 extern "C" {
+
+int ams_peer_buffer(ams_ctx_t* c, int slot, uint64_t bytes, void** dptr, void* ipc_handle, int* grown) {
+  if (!c || !dptr || !ipc_handle) return set_error(AMS_EINVAL, "null argument");
+  if (slot < 0 || slot >= 8) return set_error(AMS_EINVAL, "peer buffer slot outside 0..7");
+  AMS_ON_DEVICE(c->device);
+  DevBuf& b = c->peer_buf[slot];
+  const bool grow = bytes > b.cap || !b.p;
+  if (grow) AMS_CK(b.ensure(std::max<uint64_t>(bytes, 256)));
+  cudaIpcMemHandle_t h;
+  AMS_CK(cudaIpcGetMemHandle(&h, b.p));
+  std::memcpy(ipc_handle, &h, sizeof h);
+  *dptr = b.p;
+  if (grown) *grown = grow ? 1 : 0;
+  return AMS_OK;
+}
+
+int ams_peer_open(ams_ctx_t* c, const void* ipc_handle, void** dptr) {
+  if (!c || !ipc_handle || !dptr) return set_error(AMS_EINVAL, "null argument");
+  AMS_ON_DEVICE(c->device);
+  const std::string key(static_cast<const char*>(ipc_handle), sizeof(cudaIpcMemHandle_t));
+  for (const auto& po : c->peer_open)
+    if (po.first == key) { *dptr = po.second; return AMS_OK; }
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, ipc_handle, sizeof h);
+  void* p = nullptr;
+  AMS_CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+  c->peer_open.emplace_back(key, p);
+  *dptr = p;
+  return AMS_OK;
+}
+
+int ams_peer_close_all(ams_ctx_t* c) {
+  if (!c) return set_error(AMS_EINVAL, "null context");
+  AMS_ON_DEVICE(c->device);
+  AMS_CK(cudaStreamSynchronize(c->stream));
+  for (auto& po : c->peer_open) AMS_CK(cudaIpcCloseMemHandle(po.second));
+  c->peer_open.clear();
+  return AMS_OK;
+}
+
+int ams_level_scatter_peers(ams_ctx_t* c, const void* src, const void* src_vals, int key_kind, int ndst,
+                            void* const* dst, void* const* dst_vals, const int32_t* bucket_dst,
+                            const uint64_t* cell_base, int r, const uint64_t* h_boundaries, int child_first,
+                            int child_count) {
+  if (!c || !src || !dst || !bucket_dst || !cell_base || !h_boundaries) return set_error(AMS_EINVAL, "null argument");
+  if (c->nseg == 0) return set_error(AMS_EINVAL, "ams_level_classify must run first");
+  if (c->ngroups != 1) return set_error(AMS_EINVAL, "the peer scatter takes a single-group level");
+  if ((src_vals == nullptr) != (dst_vals == nullptr))
+    return set_error(AMS_EINVAL, "values must be given for both source and destination");
+  if (!c->level_stable || !c->level_ids) return set_error(AMS_EINVAL, "the peer scatter is stable, from stored ids");
+  if (r < 1 || child_first < 0 || child_count < 0 || child_first + child_count > r)
+    return set_error(AMS_EINVAL, "child group range outside the level's children");
+  AMS_ON_DEVICE(c->device);
+  const int nb = c->nb_stride;
+  std::vector<uint64_t> bd(nb), bvd(nb, 0);
+  for (int b = 0; b < nb; ++b) {
+    const int d = bucket_dst[b];
+    if (d < 0 || d >= ndst) return set_error(AMS_EINVAL, "bucket destination out of range");
+    bd[b] = reinterpret_cast<uint64_t>(dst[d]);
+    if (src_vals) bvd[b] = reinterpret_cast<uint64_t>(dst_vals[d]);
+  }
+  Stage& st = c->st_peers;
+  st.reset();
+  const size_t oc = st.put(cell_base, (size_t)c->nseg * nb), ob = st.put(bd), ov = st.put(bvd);
+  const size_t oq = st.put(h_boundaries, (size_t)r + 1);
+  const int32_t zero = 0, one = 1;
+  const size_t of = st.put(&zero, 1), on = st.put(&one, 1), os = st.put(&cell_base[0], 1);
+  AMS_CK(st.upload(c->stream));
+  {
+    KTimer kt(c, AMS_KCAT_SCATTER, (src_vals ? 32.0 : 16.0) * c->level_elems);
+    AMS_CK(launch_scatter_peers(c->stream, src, src_vals, key_kind, c->meta, c->nchunks, nb,
+                                c->chunk_tot.as<uint32_t>(), st.dev<uint64_t>(oc), c->ids.as<uint8_t>(),
+                                c->level_id_bytes, st.dev<uint64_t>(ob), src_vals ? st.dev<uint64_t>(ov) : nullptr));
+  }
+  // Key bounds of this rank's children (the later levels' groups).
+  GroupMeta gm;
+  gm.first = st.dev<int32_t>(of);
+  gm.nseg = st.dev<int32_t>(on);
+  gm.bnd = st.dev<uint64_t>(oq);
+  gm.dst_start = st.dev<uint64_t>(os);
+  const int nxt = 1 - c->bcur;
+  AMS_CK(c->bounds[nxt].ensure(16 * (size_t)std::max(r, 1)));
+  AMS_CK(launch_child_bounds(c->stream, c->blobs.as<uint8_t>(), gm, 1, r, c->bounds[c->bcur].as<uint64_t>(),
+                             c->bounds[nxt].as<uint64_t>()));
+  if (child_first > 0 && child_count > 0)
+    AMS_CK(launch_copy_bytes(c->stream, c->bounds[nxt].p, c->bounds[nxt].as<uint64_t>() + 2 * child_first,
+                             16 * (size_t)child_count));
+  c->bcur = nxt;
+  c->launches += 2;
+  return AMS_OK;
+}
 
 int ams_get_minmax(ams_ctx_t* c, uint64_t out[2]) {
   if (!c || !out) return set_error(AMS_EINVAL, "null argument");

@@ -511,13 +511,18 @@ __device__ __forceinline__ void cp_async_wait_all() {
 // — the stable (cell, position) order the reference's concatenations produce.
 // CLS: kClsTree (splitter tree in shared memory), kClsDigit (final digit),
 // kClsIds (bucket bytes stored by the level's histogram pass).
-template <int KIND, int CLS, bool VALS, int MODE>
+// PEERS (multi-GPU level 1): bucket b's runs go to the buffer at address
+// bucket_dst[b] (values: bucket_vdst[b]) — this GPU's own or a peer GPU's,
+// mapped over NVLink — at the cell bases' indices; dst / dst_vals are unused.
+template <int KIND, int CLS, bool VALS, int MODE, bool PEERS = false>
 __global__ void __launch_bounds__(kThreads, VALS ? 2 : 4)
     k_scatter(const uint64_t* __restrict__ src, const uint64_t* __restrict__ src_vals,
               uint64_t* __restrict__ dst, uint64_t* __restrict__ dst_vals, SegMeta m,
               const uint8_t* __restrict__ blobs, const DigitCls* __restrict__ dcls, int nspl_cap,
               int nb_stride, const uint32_t* __restrict__ chunk_tot,
-              const uint64_t* __restrict__ cell_base, const uint8_t* __restrict__ ids) {
+              const uint64_t* __restrict__ cell_base, const uint8_t* __restrict__ ids,
+              const uint64_t* __restrict__ bucket_dst = nullptr,
+              const uint64_t* __restrict__ bucket_vdst = nullptr) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ int s_seg;
   __shared__ uint32_t s_scan[kWarps + 1];
@@ -696,8 +701,13 @@ __global__ void __launch_bounds__(kThreads, VALS ? 2 : 4)
     for (uint32_t j = threadIdx.x; j < tcount; j += kThreads) {
       const uint32_t b = bkt_s[j];
       const int64_t d = (kAdj ? adj[b] : run[b] - (int64_t)btot[b]) + (int64_t)j;
-      dst[d] = keys_s[j];
-      if constexpr (VALS) dst_vals[d] = vals_s[j];
+      if constexpr (PEERS) {
+        reinterpret_cast<uint64_t*>(__ldg(bucket_dst + b))[d] = keys_s[j];
+        if constexpr (VALS) reinterpret_cast<uint64_t*>(__ldg(bucket_vdst + b))[d] = vals_s[j];
+      } else {
+        dst[d] = keys_s[j];
+        if constexpr (VALS) dst_vals[d] = vals_s[j];
+      }
     }
     __syncthreads();
     if constexpr (!kAdj) {
@@ -2139,7 +2149,8 @@ cudaError_t launch_scatter(cudaStream_t st, const void* src, const void* src_val
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
     if (e != cudaSuccess) return e;                                                           \
     fn<<<(unsigned)nchunks, kThreads, smem, st>>>(s, sv, d, dv, m, blobs, dcls, nspl_cap,     \
-                                                   nb_stride, chunk_tot, cell_base, ids);     \
+                                                   nb_stride, chunk_tot, cell_base, ids,      \
+                                                   nullptr, nullptr);                          \
   }
   if (digit) {
     if (vals) AMS_SCATTER_GO(AMS_KEY_U64, kClsDigit, true) else AMS_SCATTER_GO(AMS_KEY_U64, kClsDigit, false)
@@ -2164,6 +2175,37 @@ cudaError_t launch_scatter(cudaStream_t st, const void* src, const void* src_val
     AMS_KIND_DISPATCH(kind, K, AMS_SCATTER_GO(K, kClsTree, false))
   }
 #undef AMS_SCATTER_GO
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scatter_peers(cudaStream_t st, const void* src, const void* src_vals, int kind,
+                                 const SegMeta& m, uint64_t nchunks, int nb_stride,
+                                 const uint32_t* chunk_tot, const uint64_t* cell_base, const uint8_t* ids,
+                                 int id_bytes, const uint64_t* bucket_dst, const uint64_t* bucket_vdst) {
+  if (nchunks == 0) return cudaSuccess;
+  if (!ids || nb_stride > kSerialAbove) return cudaErrorInvalidValue;  // stable warp ranks from stored ids
+  const bool vals = src_vals != nullptr;
+  const size_t smem = scatter_smem_bytes(nb_stride, 0, 0, true, vals, true);
+  const uint64_t* s = static_cast<const uint64_t*>(src);
+  const uint64_t* sv = static_cast<const uint64_t*>(src_vals);
+  cudaError_t e = cudaSuccess;
+#define AMS_PEERS_GO(K, CL, V)                                                                      \
+  {                                                                                                 \
+    auto fn = k_scatter<K, CL, V, kRankWarp, true>;                                                 \
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);           \
+    if (e != cudaSuccess) return e;                                                                 \
+    fn<<<(unsigned)nchunks, kThreads, smem, st>>>(s, sv, nullptr, nullptr, m, nullptr, nullptr, 0,  \
+                                                   nb_stride, chunk_tot, cell_base, ids, bucket_dst, \
+                                                   bucket_vdst);                                    \
+  }
+  if (id_bytes == 2) {
+    if (vals) { AMS_KIND_DISPATCH(kind, K, AMS_PEERS_GO(K, kClsIds16, true)) }
+    else { AMS_KIND_DISPATCH(kind, K, AMS_PEERS_GO(K, kClsIds16, false)) }
+  } else {
+    if (vals) { AMS_KIND_DISPATCH(kind, K, AMS_PEERS_GO(K, kClsIds, true)) }
+    else { AMS_KIND_DISPATCH(kind, K, AMS_PEERS_GO(K, kClsIds, false)) }
+  }
+#undef AMS_PEERS_GO
   return cudaGetLastError();
 }
 

@@ -91,6 +91,13 @@ cudaError_t launch_scatter(cudaStream_t st, const void* src, const void* src_val
                            uint64_t nchunks, const uint8_t* blobs, const DigitCls* dcls,
                            int nspl_cap, int cells_cap, int nb_stride, const uint32_t* chunk_tot,
                            const uint64_t* cell_base, const uint8_t* ids, int id_bytes = 1);
+// Stable level scatter from stored bucket ids whose bucket b lands in the
+// buffer at device address bucket_dst[b] (values bucket_vdst[b]) at index
+// cell_base[seg][b] + rank: the multi-GPU level 1 (peer buffers over NVLink).
+cudaError_t launch_scatter_peers(cudaStream_t st, const void* src, const void* src_vals, int kind,
+                                 const SegMeta& m, uint64_t nchunks, int nb_stride,
+                                 const uint32_t* chunk_tot, const uint64_t* cell_base, const uint8_t* ids,
+                                 int id_bytes, const uint64_t* bucket_dst, const uint64_t* bucket_vdst);
 // Child-group key bounds [2*(g*r+t)] from parent bounds [2*g] and the plan.
 cudaError_t launch_child_bounds(cudaStream_t st, const uint8_t* blobs, const GroupMeta& gm,
                                 int ngroups, int r, const uint64_t* parent, uint64_t* child);

@@ -4,17 +4,22 @@ PE layout: logical PEs are fixed; PE i lives on rank
 ``i * G // p``.  The first level's single group spans every rank:
 
     sample positions    every rank computes the whole group's draw
-                        (C++ restatement of draw_sample, ams.py:157-175)
+                        (C++ restatement of draw_sample, ams.py:157-175), so
+                        every rank also knows how many sample elements each
+                        rank holds
     sample all-gather   local sample elements -> full sample on every rank
                         (the all-gather of fastsort.py:84-93 / gossip_merge)
     splitters           replicated, identical on every rank
-    classify            local PEs; histogram all-gather (the allreduce of
-                        ams.py:236-237, which deliver_simple also needs)
+    classify            local PEs; one all-gather of the histograms and the
+                        key range (the allreduce of ams.py:236-237, which
+                        deliver_simple also needs)
     plan                replicated (optimal_group_plan, ams.py:238)
-    scatter + exchange  local scatter in (group, PE, bucket) order, then one
-                        point-to-point chunk per (source rank, group)
-                        (Network.exchange, simnet.py:294-335; receive
-                        order = source order, ams.py:252-256)
+    scatter = exchange  every rank writes its PEs' pieces straight into the
+                        receive buffers of the groups' owner GPUs (peer
+                        pointers over NVLink, mapped with CUDA IPC), at the
+                        offsets of Network.exchange (simnet.py:294-335):
+                        group g's buffer is its source PEs' pieces in PE order
+                        (ams.py:252-256) — no send buffer, no copy kernel
 
 Groups of the first level must not straddle ranks (``group_counts[0] % G
 == 0``), so every later level and the final sort are rank-local.
@@ -38,6 +43,15 @@ from .engine import LevelRecord, bucket_table, check_out, load_budget, level_tar
 from .params import as_params, as_seed
 
 
+class _DeviceView:
+    """A library-owned device buffer exposed to torch without a copy."""
+
+    def __init__(self, addr: int, n: int, device_index: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i8", "data": (addr, False),
+                                         "version": 3}
+        self.device_index = device_index
+
+
 class CudaOps:
     """Device work of one rank: the C ABI on this rank's GPU."""
 
@@ -45,6 +59,9 @@ class CudaOps:
         self.sorter = sorter
         self.ctx = sorter.ctx
         self.device = sorter.device
+        self._caps = None     # replicated receive-buffer capacity (keys) of every rank
+        self._peers = None    # per rank: (keys address, values address) as mapped here
+        self._vals = None
 
     # buffers -------------------------------------------------------------
     def empty(self, n, dtype=torch.int64):
@@ -76,6 +93,55 @@ class CudaOps:
         self.ctx.level_scatter(src, src_v, kind, dst, dst_v, r, bnd, dst_start, child_first,
                                child_count, bucket_major=bucket_major)
 
+    def exchange(self, src, src_v, kind, need, cell_base, bucket_dst, r, bnd, child_first,
+                 child_count, group=None):
+        """Level 1 across the GPUs: make every rank's receive buffer hold at
+        least need[rank] keys, map the peers' buffers, and scatter this
+        rank's pieces straight into them (ams_level_scatter_peers).  Returns
+        this rank's receive buffers (keys, values) as tensors."""
+        world = len(need)
+        rank = dist.get_rank(group) if world > 1 else 0
+        with_vals = src_v is not None
+        # Capacities follow one deterministic rule on every rank, so a rank
+        # knows without asking whether any peer re-allocated.
+        caps = [max(int(x), 1) for x in need]
+        grow = self._caps is None or self._vals != with_vals or any(
+            c > old for c, old in zip(caps, self._caps))
+        if grow:
+            caps = [max(c + c // 4, old) if self._caps else c + c // 4
+                    for c, old in zip(caps, self._caps or caps)]
+        cap = (self._caps if not grow else caps)[rank]
+        kp, kh, _ = self.ctx.peer_buffer(0, 8 * (cap + 2))
+        vp, vh = 0, b""
+        if with_vals:
+            vp, vh, _ = self.ctx.peer_buffer(1, 8 * (cap + 2))
+        if grow:
+            if world > 1:
+                torch.cuda.current_stream(self.device).synchronize()
+                got = [None] * world
+                dist.all_gather_object(got, (kh, vh), group=group)
+                self.ctx.peer_close_all()
+                self._peers = [(kp, vp) if k == rank else
+                               (self.ctx.peer_open(h[0]), self.ctx.peer_open(h[1]) if with_vals else 0)
+                               for k, h in enumerate(got)]
+            else:
+                self._peers = [(kp, vp)]
+            self._caps, self._vals = caps, with_vals
+        if world > 1:  # receivers are done with their buffers (previous sort's later levels)
+            torch.cuda.current_stream(self.device).synchronize()
+            dist.barrier(group=group)
+        self.ctx.level_scatter_peers(src, src_v, kind, [q[0] for q in self._peers],
+                                     [q[1] for q in self._peers] if with_vals else None,
+                                     bucket_dst, cell_base, r, bnd, child_first, child_count)
+        if world > 1:  # every piece has landed before anyone reads
+            torch.cuda.current_stream(self.device).synchronize()
+            dist.barrier(group=group)
+        n = int(need[rank])
+        recv = torch.as_tensor(_DeviceView(kp, cap + 2, self.device.index), device=self.device)
+        recv_v = (torch.as_tensor(_DeviceView(vp, cap + 2, self.device.index), device=self.device)
+                  if with_vals else None)
+        return recv, recv_v
+
     def final_sort(self, src, src_v, tmp, tmp_v, out, out_v, kind, offs, sizes):
         self.ctx.final_sort(src, src_v, tmp, tmp_v, out, out_v, kind, offs, sizes)
 
@@ -87,19 +153,48 @@ def _u64_to_i64(x: int) -> int:
     return x - (1 << 64) if x >= (1 << 63) else x
 
 
-def _allgather_var(t: torch.Tensor, count: int, world: int, group=None):
-    """All-gather variable-length 1-D tensors; returns the rank-ordered
-    concatenation and the per-rank counts."""
-    counts = torch.tensor([count], dtype=torch.int64, device=t.device)
-    all_counts = [torch.zeros_like(counts) for _ in range(world)]
-    dist.all_gather(all_counts, counts, group=group)
-    cs = [int(c.item()) for c in all_counts]
-    mx = max(max(cs), 1)
-    pad = torch.zeros(mx, dtype=t.dtype, device=t.device)
-    pad[:count] = t[:count]
-    outs = [torch.zeros_like(pad) for _ in range(world)]
-    dist.all_gather(outs, pad, group=group)
-    return torch.cat([o[:c] for o, c in zip(outs, cs)]), cs
+def level1_cell_base(hist: np.ndarray, bnd: np.ndarray, rank: int, world: int, pl: int,
+                     bucket_major: bool):
+    """Destination of every (local source PE, bucket) run of level 1.
+
+    ``hist`` is the (p, nb) histogram of all PEs, ``bnd`` the plan's group
+    boundaries; group g lives on rank g // (r / world) and its buffer there
+    starts after the rank's earlier groups.  In the (g(b), j, b) order of
+    deliver_simple (SURVEY §8 layout contract step 5) run (j, b) starts at
+    start(g) + sum_{j' < j} piece(j', g) + sum_{b' in [B_g, b)} H[j][b'];
+    bucket-major (keys-only last level) at start(g) + sum_{b' in [B_g, b)}
+    total(b') + sum_{j' < j} H[j'][b].  Returns (cell_base[pl, nb] for this
+    rank's PEs, bucket -> owner rank, keys each rank receives)."""
+    p, nb = hist.shape
+    r = len(bnd) - 1
+    gpr = r // world
+    H = hist.astype(np.int64)
+    g_of_b = np.searchsorted(bnd, np.arange(nb), side="right") - 1
+    owner = (g_of_b // gpr).astype(np.int32)
+    tot_b = H.sum(axis=0)
+    m_g = np.array([tot_b[bnd[g]:bnd[g + 1]].sum() for g in range(r)], np.int64)
+    g_start = np.zeros(r, np.int64)          # start of group g in its owner's buffer
+    for k in range(world):
+        gs = np.arange(k * gpr, (k + 1) * gpr)
+        g_start[gs] = np.concatenate([[0], np.cumsum(m_g[gs])[:-1]])
+    need = np.array([m_g[k * gpr:(k + 1) * gpr].sum() for k in range(world)], np.int64)
+    base = np.zeros((pl, nb), np.int64)
+    mine = slice(rank * pl, (rank + 1) * pl)
+    for g in range(r):
+        b0, b1 = int(bnd[g]), int(bnd[g + 1])
+        if b1 == b0:
+            continue
+        blk = H[:, b0:b1]                                   # (p, buckets of g)
+        if bucket_major:
+            col = np.concatenate([[0], np.cumsum(blk.sum(axis=0))[:-1]])       # earlier buckets
+            above = np.cumsum(blk, axis=0) - blk                                # earlier PEs, same bucket
+            base[:, b0:b1] = g_start[g] + col[None, :] + above[mine]
+        else:
+            piece = blk.sum(axis=1)
+            before_j = np.concatenate([[0], np.cumsum(piece)[:-1]])             # earlier source PEs
+            within = np.cumsum(blk, axis=1) - blk                               # earlier buckets of j
+            base[:, b0:b1] = g_start[g] + before_j[mine][:, None] + within[mine]
+    return base.astype(np.uint64), owner, need
 
 
 def sort_distributed(keys: torch.Tensor, pe_sizes_local, params, seed, ops, vals=None, out=None,
@@ -140,25 +235,37 @@ def sort_distributed(keys: torch.Tensor, pe_sizes_local, params, seed, ops, vals
     a = params.oversampling_for(n)                                   # ams.py:278-280
     eps_l = params.per_level_imbalance()
     b = params.overpartition
+    k_levels = len(params.group_counts)
     levels = []
 
     # ---------------- level 1: one group over all ranks --------------------
     lv, r = 0, r1
     goffs = np.zeros(p + 1, np.uint64)
     np.cumsum(sizes, out=goffs[1:])
-    rank_off = int(goffs[pe_lo])
+    rank_offs = goffs[np.arange(world + 1) * pl]                     # first key of every rank
+    rank_off = int(rank_offs[rank])
     n_g = np.array([n], np.uint64)
     br, target = level_targets(n_g, r, b, a)
     gf, gn = np.zeros(1, np.int32), np.array([p], np.int32)
     idx, gpos, drawn = L.draw_sample_positions(master, stream_id, lv, gf, gn, target, sizes,
                                                goffs[:-1])
-    mine = (idx >= rank_off) & (idx < rank_off + n_local)
+    # The draw is replicated, so every rank knows every rank's share of the
+    # sample: one fixed-size all-gather of (key, position) pairs.
+    owner_of = np.searchsorted(rank_offs, idx, side="right") - 1
+    counts = np.bincount(owner_of, minlength=world) if len(idx) else np.zeros(world, np.int64)
+    mine = owner_of == rank
     l_idx, l_gpos = idx[mine] - np.uint64(rank_off), gpos[mine]
-    cnt = len(l_idx)
+    cnt = int(counts[rank])
+    width = max(int(counts.max()), 1)
     s_keys, s_pos = ops.empty(cnt, torch.int64), ops.empty(cnt, torch.int32)
     ops.sample(keys, kind, l_idx, l_gpos, s_keys, s_pos)
-    all_keys, _ = _allgather_var(s_keys, cnt, world, group)
-    all_pos, _ = _allgather_var(s_pos, cnt, world, group)
+    pack = torch.zeros(2 * width, dtype=torch.int64, device=dev)
+    pack[:cnt] = s_keys[:cnt]
+    pack[width:width + cnt] = s_pos[:cnt].to(torch.int64)
+    packs = [torch.zeros_like(pack) for _ in range(world)]
+    dist.all_gather(packs, pack, group=group)
+    all_keys = torch.cat([q[:int(c)] for q, c in zip(packs, counts)])
+    all_pos = torch.cat([q[width:width + int(c)] for q, c in zip(packs, counts)]).to(torch.int32)
     S = int(drawn.sum())
     assert all_keys.numel() == S
     nb = np.minimum(br, drawn.astype(np.int64) + 1)                    # ams.py:228
@@ -167,80 +274,39 @@ def sort_distributed(keys: torch.Tensor, pe_sizes_local, params, seed, ops, vals
     loffs = np.zeros(pl + 1, np.uint64)
     np.cumsum(local_sizes, out=loffs[1:])
     nb_stride = int(nb.max())
-    last_level = len(params.group_counts) == 1
     hist_l = ops.classify(keys, kind, loffs[:-1], local_sizes, np.zeros(pl, np.int32),
-                          np.array([rank_off], np.int64), nb_stride, True,
-                          not (last_level and vals is None))
-    # Global key range (ordered encoding) and histograms.
+                          np.array([rank_off], np.int64), nb_stride, True, True)
+    # Histograms and key range (ordered encoding) of every rank: one all-gather.
     lo, hi = ops.get_minmax()
-    mm = torch.tensor([_u64_to_i64(lo) ^ -(1 << 63), _u64_to_i64(hi) ^ -(1 << 63)],
-                      dtype=torch.int64, device=dev)
-    mins = mm[:1].clone()
-    maxs = mm[1:].clone()
-    dist.all_reduce(mins, op=dist.ReduceOp.MIN, group=group)
-    dist.all_reduce(maxs, op=dist.ReduceOp.MAX, group=group)
-    glo = (int(mins.item()) ^ -(1 << 63)) & ((1 << 64) - 1)
-    ghi = (int(maxs.item()) ^ -(1 << 63)) & ((1 << 64) - 1)
-    ops.set_minmax(glo, ghi)
-    ht = torch.from_numpy(hist_l.astype(np.int64)).to(dev)
+    ht = torch.from_numpy(np.concatenate([hist_l.astype(np.int64).ravel(),
+                                          [_u64_to_i64(lo), _u64_to_i64(hi)]])).to(dev)
     hts = [torch.zeros_like(ht) for _ in range(world)]
     dist.all_gather(hts, ht, group=group)
-    hist = np.concatenate([h.cpu().numpy() for h in hts]).astype(np.uint32)
+    got = [h.cpu().numpy() for h in hts]
+    hist = np.concatenate([x[:-2].reshape(pl, nb_stride) for x in got]).astype(np.uint32)
+    los = [int(x[-2]) & ((1 << 64) - 1) for x in got if x[-2] != -1 or x[-1] != 0]
+    his = [int(x[-1]) & ((1 << 64) - 1) for x in got if x[-2] != -1 or x[-1] != 0]
+    if los:
+        ops.set_minmax(min(los), max(his))
     bnd, loads, mx, new_sizes, stats = L.plan_level(gn, nb, r, hist)
-    # Local scatter into (group, local PE, bucket) order.
-    work, work_v = ops.workspace(max(n_local, int(new_sizes.reshape(world, -1).sum(1).max())),
-                                 vals is not None)
-    send, send_v = ops.empty(n_local), (ops.empty(n_local) if vals is not None else None)
+    # Keys-only single level: buckets contiguous for the final sort (F7).
+    bucket_major = k_levels == 1 and vals is None
+    cell_base, bucket_dst, need = level1_cell_base(hist, bnd[0].astype(np.int64), rank, world,
+                                                    pl, bucket_major)
     gpr = r // world                                               # groups per rank
-    ops.scatter(keys, vals, kind, send, send_v, r, bnd, np.zeros(1, np.uint64),
-                rank * gpr, gpr)
-    # Pieces: elements of (source PE j, destination group g).
-    pieces = np.zeros((p, r), np.int64)
-    for g in range(r):
-        pieces[:, g] = hist[:, int(bnd[0, g]):int(bnd[0, g + 1])].sum(axis=1)
-    per_rank = pieces.reshape(world, pl, r).sum(axis=1)            # [src rank, g]
-    m_g = per_rank.sum(axis=0)
-    # Send my chunk of group g to its owner; receive (source s, my group g)
-    # at E_g offset sum_{s' < s} per_rank[s', g] (source order).
-    recv = work[0]
-    recv_v = work_v[0]
-    my_groups = range(rank * gpr, (rank + 1) * gpr)
-    g_start = np.concatenate([[0], np.cumsum([m_g[g] for g in my_groups])])
-    send_off = np.concatenate([[0], np.cumsum(per_rank[rank])])
-    ops_list, copies = [], []
-    for g in range(r):
-        owner = g // gpr
-        c0, c1 = int(send_off[g]), int(send_off[g + 1])
-        if c1 == c0:
-            continue
-        if owner == rank:
-            continue
-        ops_list.append(dist.P2POp(dist.isend, send[c0:c1], owner, group))
-        if send_v is not None:
-            ops_list.append(dist.P2POp(dist.isend, send_v[c0:c1], owner, group))
-    for li, g in enumerate(my_groups):
-        for s in range(world):
-            c = int(per_rank[s, g])
-            if c == 0:
-                continue
-            o = int(g_start[li]) + int(per_rank[:s, g].sum())
-            if s == rank:
-                c0 = int(send_off[g])
-                copies.append((recv[o:o + c], send[c0:c0 + c]))
-                if send_v is not None:
-                    copies.append((recv_v[o:o + c], send_v[c0:c0 + c]))
-                continue
-            ops_list.append(dist.P2POp(dist.irecv, recv[o:o + c], s, group))
-            if send_v is not None:
-                ops_list.append(dist.P2POp(dist.irecv, recv_v[o:o + c], s, group))
-    for dst_t, src_t in copies:
-        dst_t.copy_(src_t)
-    if ops_list:
-        for req in dist.batch_isend_irecv(ops_list):
-            req.wait()
+    recv, recv_v = ops.exchange(keys, vals, kind, need, cell_base, bucket_dst, r, bnd[0],
+                                rank * gpr, gpr, group=group)
     rec = LevelRecord(lv, r, gf, gn, sizes.copy(), drawn, nb, hist, bnd, loads, mx,
                       load_budget(n_g, r, eps_l), new_sizes, stats)
     levels.append(rec)
+    my_groups = np.arange(rank * gpr, (rank + 1) * gpr)
+    final_buckets = None
+    if bucket_major:  # this rank's buckets in output order (level1_cell_base's layout)
+        tot = hist.astype(np.int64).sum(axis=0)
+        bk = np.arange(int(bnd[0][my_groups[0]]), int(bnd[0][my_groups[-1] + 1]), dtype=np.int32)
+        ln = tot[bk].astype(np.uint64)
+        off = np.concatenate([[0], np.cumsum(ln)[:-1]]).astype(np.uint64)
+        final_buckets = (off, ln, np.zeros(len(bk), np.int32), bk)
 
     # ---------------- later levels: rank-local ------------------------------
     sizes = new_sizes.astype(np.uint64)           # global-length; local entries used
@@ -248,9 +314,10 @@ def sort_distributed(keys: torch.Tensor, pe_sizes_local, params, seed, ops, vals
     step = p // r
     gf = (pe_lo + np.arange(gpr, dtype=np.int64) * step).astype(np.int32)
     gn = np.full(gpr, step, np.int32)
-    buf = 1
-    final_buckets = None
-    for lv in range(1, len(params.group_counts)):
+    n_recv = int(need[rank])
+    work, work_v = ops.workspace(max(n_recv, 1), vals is not None)
+    buf = 0
+    for lv in range(1, k_levels):
         r = params.group_counts[lv]
         offs = np.zeros(p + 1, np.uint64)          # positions in the local buffer
         np.cumsum(np.where((np.arange(p) >= pe_lo) & (np.arange(p) < pe_lo + pl), sizes, 0),
@@ -271,7 +338,7 @@ def sort_distributed(keys: torch.Tensor, pe_sizes_local, params, seed, ops, vals
         seg_group = np.repeat(np.arange(G, dtype=np.int32), gn)
         posbase = -offs[gf].astype(np.int64)
         nb_stride = int(nb.max())
-        last_level = lv == len(params.group_counts) - 1
+        last_level = lv == k_levels - 1
         hist = ops.classify(src, src_kind, offs[loc], sizes[loc], seg_group, posbase, nb_stride,
                             False, not (last_level and vals is None))
         bnd, loads, mx, new_local, stats = L.plan_level(gn, nb, r, hist)

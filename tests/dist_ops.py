@@ -107,6 +107,41 @@ class NumpyOps:
                 v = np.concatenate([vs[t[0]:t[0] + t[1]] for t in segs])
                 dst_v.numpy()[st:st + len(keys)] = v[order]
 
+    def exchange(self, src, src_v, kind, need, cell_base, bucket_dst, r, bnd, child_first,
+                 child_count, group=None):
+        """The peer scatter's semantics over gloo: every local key goes to
+        rank bucket_dst[b] at index cell_base[s][b] + its rank among the
+        earlier keys of (segment s, bucket b)."""
+        import torch.distributed as dist
+        world = len(need)
+        rank = dist.get_rank(group)
+        vs = src_v.numpy() if src_v is not None else None
+        parts = [[] for _ in range(world)]
+        for s, (o, n, g, k, b) in enumerate(self.lvl):
+            b = np.asarray(b, np.int64)
+            order = np.argsort(b, kind="stable")
+            bs = b[order]
+            first = np.searchsorted(bs, bs, side="left")
+            rank_in = np.empty(n, np.int64)
+            rank_in[order] = np.arange(n) - first
+            dest = np.asarray(bucket_dst, np.int64)[b]
+            idx = np.asarray(cell_base, np.int64)[s][b] + rank_in
+            v = vs[o:o + n] if vs is not None else None
+            for d in range(world):
+                sel = dest == d
+                parts[d].append((idx[sel], k[sel], None if v is None else v[sel]))
+        got = [None] * world
+        dist.all_gather_object(got, parts, group=group)
+        recv = torch.zeros(max(int(need[rank]), 1), dtype=torch.int64)
+        recv_v = torch.zeros_like(recv) if src_v is not None else None
+        for q in got:
+            for idx, k, v in q[rank]:
+                recv.numpy().view(np.uint64)[idx] = k
+                if recv_v is not None:
+                    recv_v.numpy()[idx] = v
+        self.mm_children = None
+        return recv, recv_v
+
     def final_sort_buckets(self, src, tmp, out, kind, bk_off, bk_len, bk_group, bk_bucket):
         x = _u(src)
         o_ = _u(out)

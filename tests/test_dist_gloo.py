@@ -111,3 +111,28 @@ def test_rejects_other_schemes(scheme):
     with pytest.raises(ValueError, match="simple delivery scheme only"):
         D.sort_distributed(torch.zeros(8, dtype=torch.int64), [4, 4], (2,), 1, ops=None,
                            scheme=scheme)
+
+
+@pytest.mark.parametrize("world,groups,npe,dist_kind", [
+    (2, (8, 8), 600, "uniform"),
+    (4, (8, 2), 500, "zipf"),
+    (2, (8,), 900, "uniform"),
+    (4, (4, 2, 2), 300, "equal"),
+    (2, (16,), 700, "sorted"),
+])
+def test_distributed_keys_only_matches_oracle(world, groups, npe, dist_kind):
+    """Keys only: the last level goes bucket-major into the fixed-capacity
+    final sort, single-level runs straight from the level-1 exchange."""
+    p = int(np.prod(groups))
+    n = p * npe
+    rng = np.random.default_rng(world * 10 + npe)
+    keys = {"uniform": lambda: rng.integers(0, 2**64, n, dtype=np.uint64),
+            "zipf": lambda: O.zipf_keys(n, 3), "equal": lambda: np.full(n, 7, dtype=np.uint64),
+            "sorted": lambda: np.arange(n, dtype=np.uint64)}[dist_kind]()
+    pe_sizes = [npe] * p
+    ref = O.ams_sort(keys, pe_sizes, groups, None, 16, 0.1, 5, "algo/rep0")
+    res = run_world(world, keys, pe_sizes, groups, None)
+    assert np.array_equal(np.concatenate([r[1] for r in res]), ref.keys)
+    assert sum((r[3] for r in res), []) == list(ref.pe_sizes)
+    for r in res:
+        assert [int(x) for x in r[4][0][0]] == list(ref.levels[0][0].plan.boundaries)

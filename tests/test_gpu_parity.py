@@ -372,43 +372,6 @@ def test_config2_full_size_schemes(api, scheme):
     torch.cuda.empty_cache()
 
 
-def test_distributed_path_world1_nccl():
-    """dist.sort_distributed over NCCL at world size 1 (CudaOps + the
-    exchange code on a real GPU) equals the oracle."""
-    import os
-    import socket
-    import torch.distributed as dist
-    from paper_1410_6754_b200 import AmsParams, SeedSpec
-    from paper_1410_6754_b200.api import get_sorter
-    from paper_1410_6754_b200.dist import CudaOps, sort_distributed
-
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    port = s.getsockname()[1]
-    s.close()
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("nccl", rank=0, world_size=1)
-    try:
-        for groups, npe, b, with_vals in (((8, 8), 5000, 16, True), ((2, 4), 1 << 17, 4, False)):
-            p = int(np.prod(groups))
-            n = p * npe
-            keys = np.random.default_rng(3).integers(0, 2**64, n, dtype=np.uint64)
-            vals = np.arange(n, dtype=np.int64)
-            ref = O.ams_sort(keys, [npe] * p, groups, None, b, 0.1, 9, "algo/rep0", vals=vals)
-            # keys only: the last level goes bucket-major into the fixed-capacity final sort
-            out, ov, sizes, levels = sort_distributed(
-                dev_u64(keys), [npe] * p, AmsParams(groups, None, b, 0.1), SeedSpec(9, "algo/rep0"),
-                CudaOps(get_sorter(0)), vals=torch.from_numpy(vals).cuda() if with_vals else None,
-                key_kind="u64")
-            torch.cuda.synchronize()
-            assert np.array_equal(host_u64(out), ref.keys)
-            if with_vals:
-                assert np.array_equal(ov.cpu().numpy(), ref.vals)
-            assert [int(x) for x in sizes] == list(ref.pe_sizes)
-    finally:
-        dist.destroy_process_group()
-
-
 def test_host_pipeline_batches(api):
     """HostSortPipeline: several host batches with overlapped copies, each
     equal to the one-shot sort (and to numpy.sort)."""
