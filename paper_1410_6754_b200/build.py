@@ -3,8 +3,10 @@
     python -m paper_1410_6754_b200.build [--force]
 
 The library is the C ABI of include/ams_b200.h; it is loaded with ctypes by
-``paper_1410_6754_b200._lib``.  Built artefacts stay in-tree (git-ignored)
-so they travel to the GPU box with the repo snapshot.
+``paper_1410_6754_b200._lib``.  Every source is compiled to an object under
+``lib/obj`` (in parallel, only when it or a header changed) and the objects
+are linked into the shared library.  Built artefacts stay in-tree
+(git-ignored) so they travel to the GPU box with the repo snapshot.
 """
 
 from __future__ import annotations
@@ -13,17 +15,18 @@ import glob
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB_DIR = os.path.join(PKG, "lib")
+OBJ_DIR = os.path.join(LIB_DIR, "obj")
 LIB = os.path.join(LIB_DIR, "libams_b200.so")
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "-shared",
-         "--expt-relaxed-constexpr"]
+FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr"]
 
 
 def sources():
@@ -31,30 +34,46 @@ def sources():
                   glob.glob(os.path.join(CSRC, "host", "*.cpp")))
 
 
-def deps():
-    return sources() + sorted(glob.glob(os.path.join(CSRC, "*.h")) +
-                              glob.glob(os.path.join(CSRC, "*.cuh")) +
-                              glob.glob(os.path.join(ROOT, "include", "*.h")))
+def headers():
+    return sorted(glob.glob(os.path.join(CSRC, "*.h")) +
+                  glob.glob(os.path.join(CSRC, "*.cuh")) +
+                  glob.glob(os.path.join(ROOT, "include", "*.h")))
+
+
+def obj_of(src: str) -> str:
+    return os.path.join(OBJ_DIR, os.path.basename(src) + ".o")
+
+
+def stale(target: str, deps) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(p) > t for p in deps)
 
 
 def up_to_date() -> bool:
-    if not os.path.exists(LIB):
-        return False
-    t = os.path.getmtime(LIB)
-    return all(os.path.getmtime(p) <= t for p in deps())
+    return not stale(LIB, sources() + headers())
+
+
+def _run(cmd, verbose):
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"nvcc failed ({res.returncode}):\n{res.stdout}\n{res.stderr}")
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return LIB
-    os.makedirs(LIB_DIR, exist_ok=True)
+    os.makedirs(OBJ_DIR, exist_ok=True)
+    hdrs = headers()
+    todo = [s for s in sources() if force or stale(obj_of(s), [s] + hdrs)]
+    inc = ["-I", os.path.join(ROOT, "include")]
+    with ThreadPoolExecutor(max_workers=max(1, min(len(todo), os.cpu_count() or 1))) as pool:
+        list(pool.map(lambda s: _run([NVCC, *ARCH, *FLAGS, *inc, "-c", s, "-o", obj_of(s)], verbose), todo))
     tmp = LIB + ".tmp"
-    cmd = [NVCC, *ARCH, *FLAGS, "-I", os.path.join(ROOT, "include"), *sources(), "-o", tmp]
-    if verbose:
-        print(" ".join(cmd))
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    if res.returncode != 0:
-        raise RuntimeError(f"nvcc failed ({res.returncode}):\n{res.stdout}\n{res.stderr}")
+    _run([NVCC, *ARCH, "-shared", *[obj_of(s) for s in sources()], "-o", tmp], verbose)
     os.replace(tmp, LIB)
     return LIB
 

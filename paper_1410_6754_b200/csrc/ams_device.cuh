@@ -305,4 +305,110 @@ __device__ inline void block_excl_scan_u16(uint32_t* wv, int nwords, uint32_t* s
   __syncthreads();
 }
 
+
+// ---- helpers shared by the kernel translation units -------------------------
+// Unstable scatters (k_scatter_u, k_scatter_fixed): 16 warps x 8 keys per tile, 2 CTAs per SM.
+constexpr int kThreadsU = 512;
+constexpr int kItemsU = kTile / kThreadsU;
+constexpr int kWarpsU = kThreadsU / 32;
+// Sub-buckets of the cell sort: two per key of cell capacity.
+constexpr int kCellSubBuckets = 2 * AMS_SMEM_SORT_CAP;
+
+__device__ __forceinline__ int upper_bound_u64(const uint64_t* a, int n, uint64_t x) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (a[mid] <= x) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+constexpr uint32_t kInvalid = 0xFFFFFFFFu;
+
+// Ranking modes of the scatter.
+constexpr int kClsTree = 0, kClsDigit = 1, kClsIds = 2;
+constexpr int kClsTreeTags = 3;  // tree, tie-break by the carried origin tag (the values)
+constexpr int kClsIds16 = 4;     // 16-bit bucket ids stored by the histogram pass (> 256 buckets)
+constexpr int kRankWarp = 0;     // stable, one bucket-counter array per warp
+constexpr int kRankSerial = 1;   // stable, one shared array, warps take turns
+constexpr int kRankAtomic = 2;   // unstable (keys only, order inside a run is free)
+
+// Stable rank of this lane's item among the warp's items in the same bucket
+// (lower lanes first), plus the per-warp bucket counter update.  Peers are
+// found with one ballot per bucket-id bit (and one for validity unless the
+// whole warp is valid): __match_any_sync costs ~57 SM-cycles per warp on
+// B200 (tools/microbench.cu).  NBITS is a compile-time width so the vote
+// chain unrolls to ~3 instructions per bit.
+template <int NBITS>
+__device__ __forceinline__ uint32_t warp_stable_rank(uint32_t b, int lane, uint32_t lt,
+                                                     uint32_t* whw, bool all_valid) {
+  const bool valid = b != kInvalid;
+  uint32_t peers = 0xffffffffu;
+  if (!all_valid) {
+    const uint32_t v = __ballot_sync(0xffffffffu, valid);
+    peers = valid ? v : ~v;
+  }
+#pragma unroll
+  for (int bit = 0; bit < NBITS; ++bit) {
+    const uint32_t x = (b >> bit) & 1u;
+    const uint32_t bal = __ballot_sync(0xffffffffu, x);
+    peers &= ~(bal ^ (0u - x));  // lanes whose bit equals mine
+  }
+  uint32_t cnt = 0;
+  if (valid) cnt = whw[b];
+  __syncwarp();
+  if (valid && lane == __ffs(peers) - 1) whw[b] = cnt + __popc(peers);
+  __syncwarp();
+  return cnt + __popc(peers & lt);
+}
+
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
+// ---- 1-D bulk copies (TMA engine) with an mbarrier -------------------------
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+// Arm `bar` for `bytes` and copy them global -> shared (16-byte aligned, size % 16 == 0).
+__device__ __forceinline__ void bulk_load(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(sdst);
+  const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(b), "r"(bytes)
+               : "memory");
+  if (bytes)
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
+            "r"(d), "l"(gsrc), "r"(bytes), "r"(b)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n}\n" ::"r"(b),
+      "r"(parity)
+      : "memory");
+}
+
 }  // namespace ams
+
+#define AMS_KIND_DISPATCH(kind, K, ...)          \
+  switch (kind) {                                \
+    case AMS_KEY_I64: { constexpr int K = AMS_KEY_I64; __VA_ARGS__; } break; \
+    case AMS_KEY_F64: { constexpr int K = AMS_KEY_F64; __VA_ARGS__; } break; \
+    default: { constexpr int K = AMS_KEY_U64; __VA_ARGS__; } break;          \
+  }
+

@@ -695,16 +695,19 @@ int level_scatter_impl(ams_ctx_t* c, const void* src, const void* src_vals, int 
   gm.nseg = st.dev<int32_t>(on);
   gm.bnd = st.dev<uint64_t>(ob);
   gm.dst_start = st.dev<uint64_t>(od);
-  AMS_CK(c->pieces.ensure(sizeof(uint64_t) * (size_t)c->nseg * r));
+  const bool bm = bucket_major && !c->level_stable && !src_vals;
+  AMS_CK(c->pieces.ensure(sizeof(uint64_t) * std::max((size_t)(2 * c->nseg + G) * r,
+                                                      (size_t)G * c->nb_stride)));
   AMS_CK(c->cell_base.ensure(sizeof(uint64_t) * (size_t)c->nseg * c->nb_stride));
   {
     KTimer kt(c, AMS_KCAT_CELLBASE, 12.0 * c->nseg * c->nb_stride);
-    if (bucket_major && !c->level_stable && !src_vals)
+    if (bm)
       AMS_CK(launch_cell_base_bm(c->stream, c->seg_hist.as<uint32_t>(), c->nb_stride, gm, G,
-                                 c->cell_base.as<uint64_t>()));
+                                 c->pieces.as<uint64_t>(), c->cell_base.as<uint64_t>()));
     else
-      AMS_CK(launch_cell_base(c->stream, c->seg_hist.as<uint32_t>(), c->nb_stride, gm, G, r,
-                              c->pieces.as<uint64_t>(), c->cell_base.as<uint64_t>()));
+      AMS_CK(launch_cell_base(c->stream, c->seg_hist.as<uint32_t>(), c->nb_stride, gm, G, c->nseg,
+                              c->meta.cls, r, c->pieces.as<uint64_t>(), c->cell_base.as<uint64_t>()));
+    c->launches += bm ? 1 : 2;
   }
   {
     KTimer kt(c, c->level_stable ? AMS_KCAT_SCATTER : AMS_KCAT_SCATTER_U,

@@ -74,12 +74,15 @@ cudaError_t launch_hist(cudaStream_t st, const void* src, int kind, bool digit, 
                         int cells_cap, int nb_stride, uint32_t* chunk_tot, uint32_t* seg_hist,
                         unsigned long long* minmax, uint8_t* ids, int id_bytes = 1);
 cudaError_t launch_chunk_scan(cudaStream_t st, uint32_t* chunk_tot, const SegMeta& m, int nb_stride);
+// seg_group: [nseg] group of every segment; pieces: scratch of
+// (2 * nseg + ngroups) * r entries.  Three launches.
 cudaError_t launch_cell_base(cudaStream_t st, const uint32_t* seg_hist, int nb_stride,
-                             const GroupMeta& gm, int ngroups, int r, uint64_t* pieces,
-                             uint64_t* cell_base);
-// Bucket-major cell bases (keys-only last level): buckets contiguous per group.
+                             const GroupMeta& gm, int ngroups, int nseg, const int32_t* seg_group, int r,
+                             uint64_t* pieces, uint64_t* cell_base);
+// Bucket-major cell bases (keys-only last level): buckets contiguous per
+// group.  tot: scratch of ngroups * nb_stride entries.  Two launches.
 cudaError_t launch_cell_base_bm(cudaStream_t st, const uint32_t* seg_hist, int nb_stride,
-                                const GroupMeta& gm, int ngroups, uint64_t* cell_base);
+                                const GroupMeta& gm, int ngroups, uint64_t* tot, uint64_t* cell_base);
 cudaError_t launch_digit_base(cudaStream_t st, const uint32_t* seg_hist, int nb_stride,
                               const SegMeta& m, uint64_t* cell_base);
 size_t scatter_smem_bytes(int nb_stride, int nspl_cap, int cells_cap, bool digit, bool vals,

@@ -19,7 +19,11 @@ for groups, b, npe, vals, scheme, dist in [
         ((2, 4), 4, 1 << 14, True, "simple", "uniform"),        # KV: exact digit rounds
         ((4, 4), 8, 3001, True, "deterministic", "few"),        # tags + relayout
         ((4, 4), 8, 3001, False, "randomized", "uniform"),
-        ((8,), 4, 20000, False, "simple", "clustered")]:        # overflow fallback
+        ((8,), 4, 20000, False, "simple", "clustered"),         # overflow fallback
+        ((256,), 16, 300, True, "simple", "uniform"),           # 4096 buckets: serial stable ranks
+        ((256,), 16, 300, False, "simple", "uniform"),          # 4096 buckets, bucket-major keys-only
+        ((2, 32), 16, 2000, True, "simple", "uniform"),         # 512 buckets: 16-bit stored ids
+        ((2, 2), 4, 0, False, "simple", "uniform")]:            # empty input
     p = int(np.prod(groups))
     n = p * npe
     if dist == "uniform":
