@@ -337,6 +337,45 @@ int ams_run_level_at(ams_ctx_t* ctx, uint64_t run, int level, int32_t* group_fir
  * for CostLedger parity); needs params.record_holders. */
 int ams_run_level_holders_at(ams_ctx_t* ctx, uint64_t run, int level, uint32_t* holders);
 
+/* ------------------------------------------------------------------ */
+/* RLM-sort (recurse-last multiway mergesort, rlm.py:86-132): SURVEY     */
+/* section 8(f) row 4.                                                   */
+
+/* deliver_simple (delivery.py:151-180) for one group from its piece sizes
+ * [P][r]: the new member sizes (quota slots, delivery.py:78-80) and the
+ * exchange stats (NULL skips); the member arrays are consecutive slices of
+ * the group's simple layout. */
+int ams_deliver_simple(int P, int r, const uint64_t* pieces, uint64_t* out_new_sizes,
+                       uint64_t* out_stats);
+
+/* One level's report (rlm.py:118-131). */
+typedef struct {
+  int level, r;
+  uint64_t max_load, min_load;
+  uint64_t max_words, max_msgs, max_sent_msgs, max_recv_msgs;
+} ams_rlm_report_t;
+
+/* rlm_sort (rlm.py:86-132) of n = sum(pe_sizes) keys (device buffer,
+ * PE-major) with LevelPlan(p, group_counts) (rlm.py:22-45; AMS_EINVAL with
+ * the reference's messages when the counts do not telescope p) and the
+ * delivery `scheme` (AMS_SCHEME_*, streams "{stream_id}/L{lv}-g{lo}/deliver"
+ * as rlm.py:101-110).  Writes the concatenation of the per-PE outputs to
+ * out; out_origin (optional, u64[n]) gets every output element's index in
+ * the input (its Element identity, core.py:19-43); out_vals (with vals) the
+ * payloads in output order.  out_pe_sizes[p] and reports[levels] may be
+ * NULL.  Cut positions come from an exact device selection (the unique
+ * result of multiselect_many, multiselect.py:45-137). */
+int ams_rlm_sort_run(ams_ctx_t* ctx, int levels, const int32_t* group_counts, int scheme,
+                     int64_t master_seed, const char* stream_id, int key_kind, int p,
+                     const uint64_t* pe_sizes, const void* keys, const void* vals, void* out,
+                     void* out_origin, void* out_vals, uint64_t* out_pe_sizes,
+                     ams_rlm_report_t* reports);
+/* Records of the last ams_rlm_sort_run: group_first/npe [G], sizes_before /
+ * new_sizes [P], cuts [P][r+1] (_cut_points, rlm.py:53-83), stats [G][4]. */
+int ams_rlm_level_dims(ams_ctx_t* ctx, int level, int* r, int* ngroups, int* npe);
+int ams_rlm_level(ams_ctx_t* ctx, int level, int32_t* group_first, int32_t* group_npe,
+                  uint64_t* sizes_before, uint64_t* cuts, uint64_t* new_sizes, uint64_t* stats);
+
 #ifdef __cplusplus
 }
 #endif

@@ -77,6 +77,10 @@ _SIGNATURES = {
     "ams_sort_run": (_I, [_P, _P, _I, _P, _P, _P, _P, _P, _P, _P]),
     "ams_run_level_dims": (_I, [_P, _I, _P, _P, _P, _P, _P]),
     "ams_run_level": (_I, [_P, _I] + [_P] * 11),
+    "ams_deliver_simple": (_I, [_I, _I, _P, _P, _P]),
+    "ams_rlm_sort_run": (_I, [_P, _I, _P, _I, _I64, C.c_char_p, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "ams_rlm_level_dims": (_I, [_P, _I, _P, _P, _P]),
+    "ams_rlm_level": (_I, [_P, _I] + [_P] * 6),
 }
 
 MAX_LEVELS = 8
@@ -99,6 +103,14 @@ class LevelReportT(C.Structure):
         (f, C.c_uint64) for f in ("max_load", "min_load", "sample_size", "plan_load",
                                   "over_budget", "max_words", "max_msgs", "max_sent_msgs",
                                   "max_recv_msgs")]
+
+class RlmReportT(C.Structure):
+    """ams_rlm_report_t (include/ams_b200.h)."""
+
+    _fields_ = [("level", C.c_int), ("r", C.c_int)] + [
+        (f, C.c_uint64) for f in ("max_load", "min_load", "max_words", "max_msgs",
+                                  "max_sent_msgs", "max_recv_msgs")]
+
 
 EXPORTED = tuple(_SIGNATURES)
 BUCKET_MAJOR = 1  # AMS_SCATTER_BUCKET_MAJOR
@@ -443,6 +455,31 @@ class Context:
         check(lib.ams_sort_run(self.h, C.byref(params), len(sz), sz.ctypes.data, ptr(keys),
                                ptr(vals), ptr(out), ptr(out_vals), out_sizes.ctypes.data, reps))
         return out_sizes[: len(sz)], list(reps)
+
+    def rlm_sort_run(self, group_counts, scheme: int, master_seed: int, stream_id: str, key_kind: int,
+                     pe_sizes, keys, vals, out, out_origin, out_vals):
+        """ams_rlm_sort_run: returns (final PE sizes, [RlmReportT])."""
+        sz = u64(pe_sizes)
+        gc = np.ascontiguousarray(group_counts, dtype=np.int32)
+        out_sizes = np.zeros(max(len(sz), 1), np.uint64)
+        reps = (RlmReportT * max(len(gc), 1))()
+        check(lib.ams_rlm_sort_run(self.h, len(gc), gc.ctypes.data, int(scheme), int(master_seed),
+                                   stream_id.encode(), int(key_kind), len(sz), sz.ctypes.data, ptr(keys),
+                                   ptr(vals), ptr(out), ptr(out_origin), ptr(out_vals),
+                                   out_sizes.ctypes.data, reps))
+        return out_sizes[: len(sz)], list(reps)[: len(gc)]
+
+    def rlm_level(self, level: int) -> dict:
+        """Host records of one level of the last rlm_sort_run."""
+        r, G, P = (C.c_int() for _ in range(3))
+        check(lib.ams_rlm_level_dims(self.h, level, C.byref(r), C.byref(G), C.byref(P)))
+        r, G, P = r.value, G.value, P.value
+        d = {"r": r, "group_first": np.zeros(G, np.int32), "group_npe": np.zeros(G, np.int32),
+             "sizes_before": np.zeros(P, np.uint64), "cuts": np.zeros((P, r + 1), np.uint64),
+             "new_sizes": np.zeros(P, np.uint64), "stats": np.zeros((G, 4), np.uint64)}
+        order = ("group_first", "group_npe", "sizes_before", "cuts", "new_sizes", "stats")
+        check(lib.ams_rlm_level(self.h, level, *[d[k].ctypes.data for k in order]))
+        return d
 
     def run_id(self) -> int:
         """Id of the last sort_run (its records stay readable for 8 runs)."""

@@ -25,219 +25,9 @@ int set_error(int code, const std::string& msg) {
   return code;
 }
 
-namespace {
-
-#define AMS_CK(call)                                                                   \
-  do {                                                                                 \
-    cudaError_t _e = (call);                                                           \
-    if (_e != cudaSuccess)                                                             \
-      return set_error(AMS_ECUDA, std::string(#call) + ": " + cudaGetErrorString(_e)); \
-  } while (0)
-
-// Makes `dev` current for one C-ABI call and restores the caller's device
-// on return (a sort on cuda:1 must not leave a thread on cuda:1).
-struct DeviceGuard {
-  int prev = -1;
-  cudaError_t err = cudaSuccess;
-  explicit DeviceGuard(int dev) {
-    err = cudaGetDevice(&prev);
-    if (err == cudaSuccess && prev != dev) err = cudaSetDevice(dev);
-    else prev = -1;
-  }
-  ~DeviceGuard() {
-    if (prev >= 0) cudaSetDevice(prev);
-  }
-};
-#define AMS_ON_DEVICE(dev)  \
-  DeviceGuard _ams_dg(dev); \
-  AMS_CK(_ams_dg.err)
-
-struct DevBuf {
-  void* p = nullptr;
-  size_t cap = 0;
-  cudaError_t ensure(size_t bytes) {
-    if (bytes <= cap) return cudaSuccess;
-    if (p) {
-      cudaError_t e = cudaFree(p);
-      if (e != cudaSuccess) return e;
-      p = nullptr;
-      cap = 0;
-    }
-    size_t want = std::max<size_t>(bytes, 256);
-    cudaError_t e = cudaMalloc(&p, want);
-    if (e == cudaSuccess) cap = want;
-    return e;
-  }
-  void release() {
-    if (p) cudaFree(p);
-    p = nullptr;
-    cap = 0;
-  }
-  template <class T> T* as() const { return static_cast<T*>(p); }
-};
-
-// Pinned host memory mapped into the device address space.  Small host <->
-// device transfers of the sort go through it with a copy kernel, not the
-// copy engines: a host pipeline's multi-GiB H2D / D2H of other batches
-// occupy those, and a small cudaMemcpy queued behind one would stall the
-// sort for the whole transfer.
-struct HostBuf {
-  void* p = nullptr;   // host address
-  void* dp = nullptr;  // device address of the same bytes
-  size_t cap = 0;
-  cudaError_t ensure(size_t bytes) {
-    if (bytes <= cap) return cudaSuccess;
-    if (p) cudaFreeHost(p);
-    p = dp = nullptr;
-    cap = 0;
-    size_t want = std::max<size_t>(bytes, 4096);
-    cudaError_t e = cudaHostAlloc(&p, want, cudaHostAllocMapped | cudaHostAllocPortable);
-    if (e != cudaSuccess) return e;
-    e = cudaHostGetDevicePointer(&dp, p, 0);
-    if (e == cudaSuccess) cap = want;
-    return e;
-  }
-  void release() {
-    if (p) cudaFreeHost(p);
-    p = dp = nullptr;
-    cap = 0;
-  }
-  template <class T> T* as() const { return static_cast<T*>(p); }
-};
-
-// Device -> mapped host copy on `st` (no copy engine); the caller syncs.
-cudaError_t to_host(HostBuf& h, const void* dsrc, size_t bytes, cudaStream_t st) {
-  cudaError_t e = h.ensure(bytes);
-  if (e != cudaSuccess) return e;
-  return launch_copy_bytes(st, h.dp, dsrc, bytes);
-}
-
-// Packs small host arrays, uploads them with one async copy from pinned
-// memory, and keeps the device copy until the next upload on this stage.
-struct Stage {
-  std::vector<uint8_t> pack;
-  HostBuf h;
-  DevBuf d;
-  cudaEvent_t ev = nullptr;
-  bool pending = false;
-
-  void reset() { pack.clear(); }
-  template <class T>
-  size_t put(const T* src, size_t n) {
-    size_t off = (pack.size() + 15) & ~(size_t)15;
-    pack.resize(off + sizeof(T) * n);
-    if (n) std::memcpy(pack.data() + off, src, sizeof(T) * n);
-    return off;
-  }
-  template <class T>
-  size_t put(const std::vector<T>& v) { return put(v.data(), v.size()); }
-  cudaError_t upload(cudaStream_t st) {
-    cudaError_t e;
-    if (!ev) {
-      e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-      if (e != cudaSuccess) return e;
-    }
-    if (pending) {
-      e = cudaEventSynchronize(ev);
-      if (e != cudaSuccess) return e;
-      pending = false;
-    }
-    const size_t bytes = std::max<size_t>(pack.size(), 16);
-    if ((e = h.ensure(bytes)) != cudaSuccess) return e;
-    if ((e = d.ensure(bytes)) != cudaSuccess) return e;
-    std::memcpy(h.p, pack.data(), pack.size());
-    if ((e = launch_copy_bytes(st, d.p, h.dp, pack.size())) != cudaSuccess) return e;
-    if ((e = cudaEventRecord(ev, st)) != cudaSuccess) return e;
-    pending = true;
-    return cudaSuccess;
-  }
-  template <class T> const T* dev(size_t off) const {
-    return reinterpret_cast<const T*>(static_cast<const uint8_t*>(d.p) + off);
-  }
-  void release() {
-    h.release();
-    d.release();
-    if (ev) cudaEventDestroy(ev);
-    ev = nullptr;
-  }
-};
-
-}  // namespace
 }  // namespace ams
 
-using namespace ams;
-
-constexpr uint64_t kCopyItemKeys = 8192;  // keys per relayout work item (k_copy_ranges CTA)
-
-struct ams_ctx {
-  int device = 0;
-  cudaStream_t stream = nullptr;
-  uint64_t launches = 0;
-  Stage st_sample, st_split, st_level, st_scatter, st_final;
-  // splitters / classifiers of the current level
-  DevBuf blobs, sorted_keys, sorted_pos, sample_idx;
-  std::vector<int32_t> group_nb;
-  int nspl_cap = 0, cells_cap = 0;
-  // level state (classify -> scatter)
-  int nseg = 0, ngroups = 0, nb_stride = 0;
-  uint64_t nchunks = 0, level_elems = 0;
-  std::vector<int32_t> group_first, group_nseg;
-  SegMeta meta{};
-  DevBuf chunk_tot, seg_hist, cell_base, pieces, minmax;
-  bool level_stable = true;
-  DevBuf ids;  // per-key bucket ids of the current level (bytes, or u16 above 256 buckets)
-  bool level_ids = false;
-  int level_id_bytes = 1;
-  // key bounds [lo, hi] of the current level's groups (ping-pong)
-  DevBuf bounds[2];
-  int bcur = 0;
-  HostBuf h_hist;
-  // final sort
-  DevBuf dcls, ovf, ovf_count, fb, fb_count;
-  // bucket-major final sort (fixed-capacity cells)
-  DevBuf fx_scratch, fx_fill, fx_ovf, fx_base, fx_cnt, fx_seg;
-  Stage st_fixed;
-  uint64_t fixed_segments = 0, fixed_overflow_segments = 0;
-  bool bm_final = true;  // AMS_FINAL_BM=0 keeps the (g(b), j, b) last level + PE digit partition
-  bool host_trace = false;  // AMS_HOST_TRACE=1: host-side step times of ams_sort_run on stderr
-  int fixed_fill_pct = 88;  // AMS_FIXED_FILL: mean fill of the fixed-capacity cells (percent)
-  // multi-GPU: buffers peers map (CUDA IPC) and the peers' buffers mapped here
-  DevBuf peer_buf[8];
-  std::vector<std::pair<std::string, void*>> peer_open;  // (handle bytes, mapped address)
-  Stage st_peers;
-  // deterministic delivery: origin tags (tie-breaks) and relayout work items
-  const uint64_t* level_tags = nullptr;
-  DevBuf tags0;
-  Stage st_copy;
-  HostBuf h_small, h_big;
-  uint64_t overflow_cells = 0, fallback_cells = 0;
-  // one-call driver (ams_sort_run): workspace and the last run's level records
-  DevBuf work[2], work_v[2], s_keys, s_pos;
-  struct LevelRec {
-    int r = 0, G = 0, P = 0, nb_stride = 0;
-    std::vector<int32_t> group_first, group_npe, nb;
-    std::vector<uint64_t> sizes_before, drawn, boundaries, loads, max_load, new_sizes, stats;
-    std::vector<uint32_t> hist;
-    std::vector<uint32_t> holders;  // per PE: splitters drawn from it (record_holders)
-    bool has_stats = false;
-  };
-  std::vector<LevelRec> run_levels;
-  std::vector<uint64_t> run_final_sizes;
-  // records of the last kRunHistory runs (run id, levels), newest last
-  static constexpr size_t kRunHistory = 8;
-  uint64_t run_id = 0;
-  std::vector<std::pair<uint64_t, std::vector<LevelRec>>> run_history;
-  // optional per-category kernel timing (CUDA events on the launching stream)
-  bool timing = false;
-  struct Timed { int cat; cudaEvent_t a, b; double bytes; };
-  struct Span { int cat; float t0, t1; };
-  std::vector<Span> timeline;  // resolved launches, ms from the first of each resolve batch
-  std::vector<Timed> pending;
-  std::vector<cudaEvent_t> free_events;
-  double cat_ms[AMS_NUM_KCAT] = {};
-  double cat_bytes[AMS_NUM_KCAT] = {};
-  uint64_t cat_launches[AMS_NUM_KCAT] = {};
-};
+#include "ctx.h"
 
 namespace {
 
@@ -301,18 +91,35 @@ void resolve_timing(ams_ctx* c) {
 
 // Chunk prefix of a segment list (a chunk = kChunk keys of one segment,
 // one CTA of the histogram and scatter kernels).
-void chunk_layout(const uint64_t* len, int nseg, std::vector<uint64_t>& chunk_prefix) {
+void chunk_layout(const uint64_t* len, int nseg, uint64_t chunk, std::vector<uint64_t>& chunk_prefix) {
   chunk_prefix.assign(nseg + 1, 0);
   for (int s = 0; s < nseg; ++s)
-    chunk_prefix[s + 1] = chunk_prefix[s] + (len[s] + kChunk - 1) / kChunk;
+    chunk_prefix[s + 1] = chunk_prefix[s] + (len[s] + chunk - 1) / chunk;
+}
+
+// Keys per chunk: kChunk for inputs that fill the GPU several times over,
+// fewer (whole tiles) for small inputs so that about kFillCtas CTAs exist
+// (config 1 at 2^20 keys has 16 chunks of kChunk: a tenth of the SMs); with
+// many buckets a chunk stays >= 4 keys per bucket (its histogram row is
+// nb_stride words of scan work).
+constexpr uint64_t kFillCtas = 148 * 8;
+uint32_t pick_chunk(const uint64_t* len, int nseg, int nb_stride) {
+  uint64_t total = 0;
+  for (int s = 0; s < nseg; ++s) total += len[s];
+  uint64_t c = (total / kFillCtas + kTile - 1) / kTile * kTile;
+  c = std::max<uint64_t>(c, (uint64_t)kTile);
+  c = std::max<uint64_t>(c, std::min<uint64_t>((uint64_t)kChunk, 4 * (uint64_t)std::max(nb_stride, 1) / kTile * kTile));
+  return (uint32_t)std::min<uint64_t>(c, (uint64_t)kChunk);
 }
 
 // Upload a segment table; returns the device-side SegMeta.
 cudaError_t upload_segments(Stage& st, cudaStream_t stream, const uint64_t* off,
                             const uint64_t* len, const int32_t* cls, int nseg,
-                            const int64_t* posbase, int ncls, SegMeta* m, uint64_t* nchunks) {
+                            const int64_t* posbase, int ncls, SegMeta* m, uint64_t* nchunks,
+                            int nb_stride) {
   std::vector<uint64_t> cp;
-  chunk_layout(len, nseg, cp);
+  m->chunk = pick_chunk(len, nseg, nb_stride);
+  chunk_layout(len, nseg, m->chunk, cp);
   st.reset();
   const size_t o_off = st.put(off, nseg), o_len = st.put(len, nseg), o_cls = st.put(cls, nseg);
   const size_t o_cp = st.put(cp);
@@ -391,14 +198,15 @@ int ams_ctx_destroy(ams_ctx_t* c) {
   resolve_timing(c);
   for (cudaEvent_t e : c->free_events) cudaEventDestroy(e);
   for (Stage* s : {&c->st_sample, &c->st_split, &c->st_level, &c->st_scatter, &c->st_final, &c->st_fixed,
-                   &c->st_copy})
+                   &c->st_copy, &c->st_rlm})
     s->release();
   for (DevBuf* b : {&c->blobs, &c->sorted_keys, &c->sorted_pos, &c->sample_idx, &c->bounds[0], &c->bounds[1],
                     &c->chunk_tot, &c->seg_hist, &c->cell_base, &c->pieces, &c->minmax, &c->dcls,
                     &c->ovf, &c->ovf_count, &c->fb, &c->fb_count,
                     &c->ids, &c->work[0], &c->work[1], &c->work_v[0], &c->work_v[1], &c->s_keys,
                     &c->s_pos, &c->fx_scratch, &c->fx_fill, &c->fx_ovf, &c->fx_base, &c->fx_cnt,
-                    &c->fx_seg, &c->tags0})
+                    &c->fx_seg, &c->tags0, &c->rank_tmp_keys, &c->rank_tmp_pos, &c->rlm_buf[0],
+                    &c->rlm_buf[1], &c->rlm_buf[2], &c->rlm_cuts, &c->rlm_skey})
     b->release();
   for (auto& po : c->peer_open) cudaIpcCloseMemHandle(po.second);
   for (DevBuf& b : c->peer_buf) b.release();
@@ -535,9 +343,17 @@ int ams_level_splitters(ams_ctx_t* c, int ngroups, const uint64_t* d_sample_keys
   AMS_CK(c->sorted_pos.ensure(sizeof(uint32_t) * std::max<uint64_t>(total, 1)));
   {
     KTimer kt(c, AMS_KCAT_RANK, 24.0 * total);
+    uint64_t* tk = nullptr;
+    uint32_t* tp = nullptr;
+    if (max_s > kSampleRankPairsMax) {
+      AMS_CK(c->rank_tmp_keys.ensure(sizeof(uint64_t) * total));
+      AMS_CK(c->rank_tmp_pos.ensure(sizeof(uint32_t) * total));
+      tk = c->rank_tmp_keys.as<uint64_t>();
+      tp = c->rank_tmp_pos.as<uint32_t>();
+    }
     AMS_CK(launch_sample_rank(c->stream, ngroups, max_s, d_sample_keys, d_sample_pos,
                               st.dev<uint64_t>(os), c->sorted_keys.as<uint64_t>(),
-                              c->sorted_pos.as<uint32_t>()));
+                              c->sorted_pos.as<uint32_t>(), tk, tp));
   }
   {
     KTimer kt(c, AMS_KCAT_CLS, 12.0 * total);
@@ -599,18 +415,16 @@ int ams_level_classify(ams_ctx_t* c, const void* src, int key_kind, int nseg,
     if (n_g >= 0xFFFFFFFFull) return set_error(AMS_EINVAL, "group too large for 32-bit positions");
   }
   AMS_CK(upload_segments(c->st_level, c->stream, h_seg_off, h_seg_len, h_seg_group, nseg,
-                         h_group_posbase, ngroups, &c->meta, &c->nchunks));
+                         h_group_posbase, ngroups, &c->meta, &c->nchunks, nb_stride));
   c->meta.tags = c->level_tags;  // origin tags of this level's buffer (deterministic, levels >= 2)
   c->nseg = nseg;
   c->nb_stride = nb_stride;
   unsigned long long* mm = nullptr;
   if (track_minmax) {
     AMS_CK(c->minmax.ensure(16));
-    const unsigned long long init[2] = {~0ULL, 0ULL};
-    AMS_CK(c->h_small.ensure(64));
-    AMS_CK(cudaStreamSynchronize(c->stream));
-    std::memcpy(c->h_small.p, init, sizeof init);
-    AMS_CK(launch_copy_bytes(c->stream, c->minmax.p, c->h_small.dp, sizeof init));
+    // {min, max} = {~0, 0}: two byte fills, no host round trip.
+    AMS_CK(cudaMemsetAsync(c->minmax.p, 0xFF, 8, c->stream));
+    AMS_CK(cudaMemsetAsync(static_cast<uint8_t*>(c->minmax.p) + 8, 0, 8, c->stream));
     mm = c->minmax.as<unsigned long long>();
   }
   uint64_t nel = 0;
@@ -941,7 +755,7 @@ int partition_rounds(ams_ctx* c, void* src, void* src_vals, void* tmp, void* tmp
       AMS_CK(launch_final_ranges(c->stream, bounds, nb_seg, nbs, c->dcls.as<DigitCls>()));
     }
     AMS_CK(upload_segments(st, c->stream, b_off.data(), b_len.data(), idx.data(), nb_seg, nullptr,
-                           0, &m, &nchunks));
+                           0, &m, &nchunks, nbs));
     uint64_t nel = 0;
     for (uint64_t v : b_len) nel += v;
     int rc = run_histogram(c, cur, AMS_KEY_U64, true, m, nchunks, nbs, c->dcls.as<DigitCls>(),
@@ -1071,7 +885,7 @@ int final_sort_bm(ams_ctx* c, void* src, void* tmp, void* out, int key_kind,
   SegMeta m;
   uint64_t nchunks;
   AMS_CK(upload_segments(c->st_final, c->stream, f_off.data(), f_len.data(), idx.data(), nseg, nullptr,
-                         0, &m, &nchunks));
+                         0, &m, &nchunks, 1));
   AMS_CK(c->dcls.ensure(sizeof(DigitCls) * (size_t)nseg));
   AMS_CK(c->fx_fill.ensure(4 * (size_t)ncells));
   AMS_CK(c->fx_ovf.ensure(4 * (size_t)nseg));
@@ -1184,6 +998,20 @@ int final_sort_lohi(ams_ctx* c, void* src, void* src_vals, void* tmp, void* tmp_
 }
 
 }  // namespace
+
+}  // extern "C"
+
+namespace ams {
+int sort_segments_lohi(ams_ctx* c, void* src, void* src_vals, void* tmp, void* tmp_vals, void* out,
+                       void* out_vals, int key_kind, int nseg, const uint64_t* h_seg_off,
+                       const uint64_t* h_seg_len, const std::vector<uint64_t>& lo,
+                       const std::vector<uint64_t>& hi) {
+  return final_sort_lohi(c, src, src_vals, tmp, tmp_vals, out, out_vals, key_kind, nseg, h_seg_off,
+                         h_seg_len, lo, hi);
+}
+}  // namespace ams
+
+extern "C" {
 
 int ams_final_sort(ams_ctx_t* c, void* src, void* src_vals, void* tmp, void* tmp_vals, void* out,
                    void* out_vals, int key_kind, int nseg, const uint64_t* h_seg_off,
@@ -1472,7 +1300,14 @@ int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* p
     rec.group_first = gf; rec.group_npe = gn; rec.nb = nb;
     rec.sizes_before = sizes; rec.drawn = drawn;
     rec.holders = std::move(holders);
-    rec.hist.assign((size_t)p * nb_stride, 0);
+    // Fully overwritten by the classify step; a buffer recycled from the
+    // oldest kept run avoids 4 MB of page faults and zeroing per level at
+    // 256 PEs x 4096 buckets.
+    if (!c->hist_pool.empty()) {
+      rec.hist = std::move(c->hist_pool.back());
+      c->hist_pool.pop_back();
+    }
+    rec.hist.resize((size_t)p * nb_stride);
     c->level_tags = tie_tags;
     tr.mark("sample");
     rc = ams_level_classify(c, src, src_kind, p, offs.data(), sizes.data(), seg_group.data(), G,
@@ -1608,16 +1443,21 @@ int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* p
     std::vector<uint64_t> bo, bl;
     std::vector<int32_t> bg, bb;
     uint64_t at = 0;
+    std::vector<uint64_t> tot;
     for (int g = 0; g < L.G; ++g) {
+      // Bucket totals of the group: member rows outermost (each row is
+      // contiguous; 256 PEs x 4096 buckets is 4 MB of histogram).
+      tot.assign((size_t)L.nb[g], 0);
+      for (int j = 0; j < L.group_npe[g]; ++j) {
+        const uint32_t* row = L.hist.data() + (size_t)(L.group_first[g] + j) * L.nb_stride;
+        for (int b = 0; b < L.nb[g]; ++b) tot[b] += row[b];
+      }
       for (int b = 0; b < L.nb[g]; ++b) {
-        uint64_t h = 0;
-        for (int j = 0; j < L.group_npe[g]; ++j)
-          h += L.hist[(size_t)(L.group_first[g] + j) * L.nb_stride + b];
         bo.push_back(at);
-        bl.push_back(h);
+        bl.push_back(tot[b]);
         bg.push_back(g);
         bb.push_back(b);
-        at += h;
+        at += tot[b];
       }
     }
     if ((rc = final_sort_bm(c, const_cast<void*>(src), tmp, dst_out, prm->key_kind, bo, bl, bg, bb,
@@ -1652,7 +1492,11 @@ int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* p
   c->run_id += 1;
   c->run_history.emplace_back(c->run_id, std::move(c->run_levels));
   c->run_levels.clear();
-  if (c->run_history.size() > ams_ctx::kRunHistory) c->run_history.erase(c->run_history.begin());
+  if (c->run_history.size() > ams_ctx::kRunHistory) {
+    for (auto& lr : c->run_history.front().second)
+      if (c->hist_pool.size() < 2 * AMS_MAX_LEVELS) c->hist_pool.push_back(std::move(lr.hist));
+    c->run_history.erase(c->run_history.begin());
+  }
   c->run_final_sizes = sizes;
   if (out_pe_sizes) std::memcpy(out_pe_sizes, sizes.data(), sizeof(uint64_t) * p);
   return AMS_OK;

@@ -338,6 +338,29 @@ int ams_plan_level(int ngroups, const int32_t* group_npe, const int32_t* group_n
   return AMS_OK;
 }
 
+// deliver_simple (delivery.py:151-180) for one group from its piece sizes
+// [P][r]: the member arrays are consecutive slices of the group's simple
+// layout (no relayout), so only the new member sizes (quota slots,
+// delivery.py:78-80) and the exchange stats are produced.
+int ams_deliver_simple(int P, int r, const uint64_t* pieces, uint64_t* out_new_sizes,
+                       uint64_t* out_stats) {
+  if (r < 1 || P < 1 || P % r != 0)
+    return set_error(AMS_EINVAL, std::to_string(P) + " PEs cannot form " + std::to_string(r) + " groups");
+  if (!pieces || !out_new_sizes) return set_error(AMS_EINVAL, "null argument");
+  const int sub = P / r;
+  for (int g = 0; g < r; ++g) {
+    uint64_t m = 0;
+    for (int j = 0; j < P; ++j) m += pieces[(size_t)j * r + g];
+    for (int t = 0; t < sub; ++t) {
+      const uint64_t a = (uint64_t)(((unsigned __int128)m * t) / sub);
+      const uint64_t b = (uint64_t)(((unsigned __int128)m * (t + 1)) / sub);
+      out_new_sizes[(size_t)g * sub + t] = b - a;
+    }
+  }
+  if (out_stats) exchange_stats(std::vector<uint64_t>(pieces, pieces + (size_t)P * r), P, r, out_stats);
+  return AMS_OK;
+}
+
 // deliver_deterministic (delivery.py:188-306) for one group of P members
 // and r subgroups (members [g*P/r, (g+1)*P/r) form subgroup g), from the
 // piece sizes [P][r] (member j's buckets of group g).  Small pieces

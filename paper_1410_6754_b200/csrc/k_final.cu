@@ -52,8 +52,8 @@ __global__ void __launch_bounds__(kThreadsU, 2)
   int32_t* lim = reinterpret_cast<int32_t*>(cnt + nbp);         // writable keys of the run
   uint16_t* bkt = reinterpret_cast<uint16_t*>(lim + nbp);
   const uint64_t seg_off = m.off[s];
-  const uint64_t first = (c - m.chunk_prefix[s]) * (uint64_t)kChunk;
-  const uint64_t last = min(first + (uint64_t)kChunk, m.len[s]);
+  const uint64_t first = (c - m.chunk_prefix[s]) * (uint64_t)m.chunk;
+  const uint64_t last = min(first + (uint64_t)m.chunk, m.len[s]);
   const int ntiles = (int)((last - first + kTile - 1) / kTile);
   const uint64_t cbase = cell0[s];
   // Tile t = keys [base, base + tc); the copy starts at the 16-byte boundary

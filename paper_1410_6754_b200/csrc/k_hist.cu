@@ -7,6 +7,10 @@
 #include "ams_device.cuh"
 #include "launch.h"
 
+#ifndef AMS_HIST_PLAIN
+#define AMS_HIST_PLAIN 1
+#endif
+
 namespace ams {
 
 namespace {
@@ -42,8 +46,8 @@ __global__ void __launch_bounds__(kThreads) k_hist(const uint64_t* __restrict__ 
   __syncthreads();
   const int s = s_seg;
   const uint64_t seg_off = m.off[s], seg_len = m.len[s];
-  const uint64_t first = (c - m.chunk_prefix[s]) * (uint64_t)kChunk;
-  const uint64_t last = min(first + (uint64_t)kChunk, seg_len);
+  const uint64_t first = (c - m.chunk_prefix[s]) * (uint64_t)m.chunk;
+  const uint64_t last = min(first + (uint64_t)m.chunk, seg_len);
   const int cls = m.cls[s];
   TreeView tv;
   DigitView dv;
@@ -63,6 +67,36 @@ __global__ void __launch_bounds__(kThreads) k_hist(const uint64_t* __restrict__ 
   // first in the many-splitter LUT cells; fixed for the tile, so the items'
   // classifications stay independent.
   uint32_t hint = kInvalid;
+  // Chunks whose first and last key share a bucket (sorted / duplicate-heavy
+  // input: most of the chunk is one bucket, and one atomic per key would
+  // serialise 32-way on that counter) aggregate runs; the others (keys
+  // spread over the buckets) take one atomic per key — no run bookkeeping.
+  bool runs = true;
+#if AMS_HIST_PLAIN
+  if constexpr (!DIGIT && !TAGS && DUP == 1) {
+    if (last > first) {
+      const uint32_t pb = (uint32_t)((int64_t)seg_off + posbase);
+      const uint32_t b0 = tv.classify(to_ordered<KIND>(src[seg_off + first]), pb + (uint32_t)first);
+      const uint32_t b1 = tv.classify(to_ordered<KIND>(src[seg_off + last - 1]), pb + (uint32_t)(last - 1));
+      runs = b0 == b1;
+    }
+  }
+#endif
+  auto tile_plain = [&](const uint64_t t0) {  // full tiles only
+    const uint64_t base = seg_off + t0;
+    uint64_t keys[kItems];
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) keys[i] = to_ordered<KIND>(ldg_stream(src + base + i * kThreads + threadIdx.x));
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+      const uint32_t e = i * kThreads + threadIdx.x;
+      const uint32_t b = tv.classify(keys[i], (uint32_t)((int64_t)base + posbase) + e, hint);
+      if constexpr (IDS == 1) ids[base + e] = (uint8_t)b;
+      if constexpr (IDS == 2) reinterpret_cast<uint16_t*>(ids)[base + e] = (uint16_t)b;
+      if constexpr (MINMAX) { mn = min(mn, (unsigned long long)keys[i]); mx = max(mx, (unsigned long long)keys[i]); }
+      atomicAdd(&hist[b], 1u);
+    }
+  };
   auto tile = [&](const uint64_t t0, const uint32_t tcount, auto full_tag) {
     constexpr bool FULL = decltype(full_tag)::value;
     const uint64_t base = seg_off + t0;
@@ -99,8 +133,14 @@ __global__ void __launch_bounds__(kThreads) k_hist(const uint64_t* __restrict__ 
   };
   for (uint64_t t0 = first; t0 < last; t0 += kTile) {
     const uint32_t tcount = (uint32_t)min((uint64_t)kTile, last - t0);
-    if (tcount == (uint32_t)kTile) tile(t0, tcount, std::true_type{});
-    else tile(t0, tcount, std::false_type{});
+    if (tcount == (uint32_t)kTile) {
+      if constexpr (!DIGIT && !TAGS && DUP == 1) {
+        if (!runs) { tile_plain(t0); continue; }
+      }
+      tile(t0, tcount, std::true_type{});
+    } else {
+      tile(t0, tcount, std::false_type{});
+    }
   }
   __syncthreads();
   for (int b = threadIdx.x; b < nb_stride; b += kThreads) {

@@ -53,8 +53,8 @@ __global__ void __launch_bounds__(kThreads, VALS ? 2 : 4)
   __syncthreads();
   const int s = s_seg;
   const uint64_t seg_off = m.off[s];
-  const uint64_t first = (c - m.chunk_prefix[s]) * (uint64_t)kChunk;
-  const uint64_t last = min(first + (uint64_t)kChunk, m.len[s]);
+  const uint64_t first = (c - m.chunk_prefix[s]) * (uint64_t)m.chunk;
+  const uint64_t last = min(first + (uint64_t)m.chunk, m.len[s]);
   const int cls = m.cls[s];
   {
     const uint32_t* ct = chunk_tot + c * nb_stride;
@@ -266,8 +266,8 @@ __global__ void __launch_bounds__(kThreadsU, 2)
   __syncthreads();
   const int s = s_seg;
   const uint64_t seg_off = m.off[s];
-  const uint64_t first = (c - m.chunk_prefix[s]) * (uint64_t)kChunk;
-  const uint64_t last = min(first + (uint64_t)kChunk, m.len[s]);
+  const uint64_t first = (c - m.chunk_prefix[s]) * (uint64_t)m.chunk;
+  const uint64_t last = min(first + (uint64_t)m.chunk, m.len[s]);
   const int ntiles = (int)((last - first + kTile - 1) / kTile);
   // Tile t = keys [base, base + tc); the copy covers whole 16-byte units
   // from the boundary base - h, so key e of the tile sits at buf[e + h]; when

@@ -113,6 +113,76 @@ __global__ void __launch_bounds__(256) k_sample_rank(const uint64_t* __restrict_
   }
 }
 
+// Large samples (config 5 with one level: 256 PEs x 4096 buckets draw ~53 K
+// sample elements, and counting over all pairs is S^2 = 2.8 G compares):
+// the same rank-by-counting, with the counting done by binary search.
+//   k_sample_block_sort  each CTA sorts kSortBlock elements by (key, pos)
+//                        (bitonic network in shared memory) into tmp;
+//   k_sample_merge_rank  rank of an element = its index in its own block +
+//                        its lower bound in every other sorted block.
+// (key, pos) pairs are unique inside a group, so ranks are a permutation.
+constexpr int kSortBlock = 1024;
+__global__ void __launch_bounds__(kSortBlock / 2)
+    k_sample_block_sort(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ pos,
+                        const uint64_t* __restrict__ soff, uint64_t* __restrict__ tk,
+                        uint32_t* __restrict__ tp) {
+  __shared__ uint64_t sk[kSortBlock];
+  __shared__ uint32_t sp[kSortBlock];
+  const int g = blockIdx.y;
+  const uint64_t s0 = soff[g], S = soff[g + 1] - s0;
+  const uint64_t first = (uint64_t)blockIdx.x * kSortBlock;
+  if (first >= S) return;
+  for (int i = threadIdx.x; i < kSortBlock; i += blockDim.x) {
+    const bool ok = first + i < S;
+    sk[i] = ok ? keys[s0 + first + i] : ~0ULL;
+    sp[i] = ok ? pos[s0 + first + i] : 0xFFFFFFFFu;
+  }
+  __syncthreads();
+  for (int k = 2; k <= kSortBlock; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const int t = threadIdx.x;
+      const int a = ((t & ~(j - 1)) << 1) | (t & (j - 1));  // lower index of the pair
+      const int b = a | j;
+      const bool up = (a & k) == 0;
+      const uint64_t ka = sk[a], kb = sk[b];
+      const uint32_t pa = sp[a], pb = sp[b];
+      const bool a_after = ka > kb || (ka == kb && pa > pb);
+      if (a_after == up) { sk[a] = kb; sk[b] = ka; sp[a] = pb; sp[b] = pa; }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < kSortBlock; i += blockDim.x) {
+    if (first + i < S) { tk[s0 + first + i] = sk[i]; tp[s0 + first + i] = sp[i]; }
+  }
+}
+
+__global__ void __launch_bounds__(256)
+    k_sample_merge_rank(const uint64_t* __restrict__ tk, const uint32_t* __restrict__ tp,
+                        const uint64_t* __restrict__ soff, uint64_t* __restrict__ sorted_keys,
+                        uint32_t* __restrict__ sorted_pos) {
+  const int g = blockIdx.y;
+  const uint64_t s0 = soff[g], S = soff[g + 1] - s0;
+  const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= S) return;
+  const uint64_t k = tk[s0 + e];
+  const uint32_t p = tp[s0 + e];
+  const uint64_t mine = e / kSortBlock, nblk = (S + kSortBlock - 1) / kSortBlock;
+  uint64_t rank = e % kSortBlock;
+  for (uint64_t bj = 0; bj < nblk; ++bj) {
+    if (bj == mine) continue;
+    const uint64_t b0 = s0 + bj * kSortBlock;
+    uint32_t lo = 0, hi = (uint32_t)min((uint64_t)kSortBlock, S - bj * kSortBlock);
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      const uint64_t km = tk[b0 + mid];
+      if (km < k || (km == k && tp[b0 + mid] < p)) lo = mid + 1; else hi = mid;
+    }
+    rank += lo;
+  }
+  sorted_keys[s0 + rank] = k;
+  sorted_pos[s0 + rank] = p;
+}
+
 __device__ __forceinline__ uint32_t lower_bound_smem(const uint64_t* a, uint32_t n, uint64_t x) {
   uint32_t lo = 0, hi = n;
   while (lo < hi) {
@@ -535,8 +605,15 @@ cudaError_t launch_gather_vals(cudaStream_t st, const void* vals, const void* id
 
 cudaError_t launch_sample_rank(cudaStream_t st, int ngroups, uint64_t max_s, const uint64_t* keys,
                                const uint32_t* pos, const uint64_t* soff, uint64_t* sorted_keys,
-                               uint32_t* sorted_pos) {
+                               uint32_t* sorted_pos, uint64_t* tmp_keys, uint32_t* tmp_pos) {
   if (ngroups == 0 || max_s == 0) return cudaSuccess;
+  if (max_s > kSampleRankPairsMax && tmp_keys && tmp_pos) {
+    const dim3 ga((unsigned)((max_s + kSortBlock - 1) / kSortBlock), (unsigned)ngroups);
+    k_sample_block_sort<<<ga, kSortBlock / 2, 0, st>>>(keys, pos, soff, tmp_keys, tmp_pos);
+    const dim3 gb((unsigned)((max_s + 255) / 256), (unsigned)ngroups);
+    k_sample_merge_rank<<<gb, 256, 0, st>>>(tmp_keys, tmp_pos, soff, sorted_keys, sorted_pos);
+    return cudaGetLastError();
+  }
   dim3 grid((unsigned)((max_s + kRankElems - 1) / kRankElems), (unsigned)ngroups);
   k_sample_rank<<<grid, 256, 0, st>>>(keys, pos, soff, sorted_keys, sorted_pos);
   return cudaGetLastError();

@@ -17,6 +17,7 @@ struct SegMeta {
   const int64_t* posbase;        // [ncls] tie-break position = index + posbase
   int nseg;
   const uint64_t* tags;          // origin tags (deterministic delivery, levels >= 2): tie-break by tag
+  uint32_t chunk;                // keys per chunk (a multiple of kTile, <= kChunk): one CTA's share
 };
 
 // Groups of one level (contiguous runs of segments).
@@ -62,9 +63,13 @@ cudaError_t launch_iota(cudaStream_t st, void* dst, uint64_t n);
 cudaError_t launch_copy_bytes(cudaStream_t st, void* dst, const void* src, size_t bytes);
 // out[i] = vals[idx[i]]
 cudaError_t launch_gather_vals(cudaStream_t st, const void* vals, const void* idx, void* out, uint64_t n);
+// Samples above kSampleRankPairsMax elements per group take the block-sort +
+// merge-rank kernels (tmp_keys / tmp_pos: scratch of the sample's size).
+constexpr uint64_t kSampleRankPairsMax = 4096;
 cudaError_t launch_sample_rank(cudaStream_t st, int ngroups, uint64_t max_s, const uint64_t* keys,
                                const uint32_t* pos, const uint64_t* soff, uint64_t* sorted_keys,
-                               uint32_t* sorted_pos);
+                               uint32_t* sorted_pos, uint64_t* tmp_keys = nullptr,
+                               uint32_t* tmp_pos = nullptr);
 cudaError_t launch_build_cls(cudaStream_t st, int ngroups, const uint64_t* sorted_keys,
                              const uint32_t* sorted_pos, const uint64_t* soff, const int32_t* nbs,
                              uint8_t* blobs);
@@ -133,5 +138,17 @@ cudaError_t launch_bucket_ranges(cudaStream_t st, const uint8_t* blobs, const ui
                                  const int32_t* seg_gb, int nseg, DigitCls* out);
 cudaError_t launch_map_keys(cudaStream_t st, const void* src, void* dst, uint64_t n, int from,
                             int to);
+
+// RLM-sort selection (k_rlm.cu): one query = the element of rank `target`
+// (1-based) among the members [first, first + npe) of a group; the members'
+// cut positions go to cuts[out .. out + npe).
+struct RlmQuery {
+  int32_t first, npe;
+  uint64_t target;
+  uint64_t out;
+};
+cudaError_t launch_rlm_select(cudaStream_t st, const uint64_t* keys, const uint64_t* tags,
+                              const uint64_t* pe_off, const RlmQuery* qs, int nq, uint64_t max_tag,
+                              uint64_t* cuts, uint64_t* split_key);
 
 }  // namespace ams
