@@ -294,6 +294,20 @@ typedef struct {
   int record_holders;                  /* keep, per level and PE, how many splitters were drawn from
                                           the PE (the ledger's extract_by_ranks charge,
                                           fastsort.py:111-130; one small D2H per level) */
+  /* Continuation of a sort whose first levels ran elsewhere (multi-GPU:
+   * level 1 is the exchange between the GPUs); all zero for a
+   * whole sort.  The p PEs of the call are the global PEs [pe_base, pe_base
+   * + p) and start as init_groups equal groups at level level_base (0-based
+   * index into group_counts, which still lists every level of the sort);
+   * the context holds the groups' key bounds (ams_level_scatter_peers /
+   * ams_level_scatter leave them).  oversampling must be given (> 0: `a`
+   * comes from the global n).  With a non-simple scheme `vals` holds the
+   * origin tags of the input (index in the whole sort's input), which break
+   * key ties (delivery.py:188-455 can reorder sources); user payloads are
+   * not carried in that case and out_vals is unused. */
+  int level_base;
+  int init_groups;                     /* 0 or 1: one group */
+  int pe_base;
 } ams_params_t;
 
 /* One level's report (ams.py:294-308; exchange maxima simnet.py:109-124). */
@@ -336,6 +350,14 @@ int ams_run_level_at(ams_ctx_t* ctx, uint64_t run, int level, int32_t* group_fir
  * (replaces the holder bookkeeping of extract_by_ranks, fastsort.py:111-130,
  * for CostLedger parity); needs params.record_holders. */
 int ams_run_level_holders_at(ams_ctx_t* ctx, uint64_t run, int level, uint32_t* holders);
+
+/* Relayout helpers of the non-simple deliveries for callers that run a
+ * level themselves (the multi-GPU drivers): dst[d + i] = src[s + i] for
+ * every range {s, d, len} (host array of 3 * nranges u64; values too when
+ * given), and dst[i] = start + i. */
+int ams_copy_ranges(ams_ctx_t* ctx, const uint64_t* h_ranges, int nranges, const void* src, void* dst,
+                    const void* src_vals, void* dst_vals);
+int ams_fill_iota(ams_ctx_t* ctx, void* dst, uint64_t n, uint64_t start);
 
 /* ------------------------------------------------------------------ */
 /* RLM-sort (recurse-last multiway mergesort, rlm.py:86-132): SURVEY     */

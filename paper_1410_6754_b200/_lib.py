@@ -78,6 +78,8 @@ _SIGNATURES = {
     "ams_run_level_dims": (_I, [_P, _I, _P, _P, _P, _P, _P]),
     "ams_run_level": (_I, [_P, _I] + [_P] * 11),
     "ams_deliver_simple": (_I, [_I, _I, _P, _P, _P]),
+    "ams_copy_ranges": (_I, [_P, _P, _I, _P, _P, _P, _P]),
+    "ams_fill_iota": (_I, [_P, _P, _U64, _U64]),
     "ams_rlm_sort_run": (_I, [_P, _I, _P, _I, _I64, C.c_char_p, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P]),
     "ams_rlm_level_dims": (_I, [_P, _I, _P, _P, _P]),
     "ams_rlm_level": (_I, [_P, _I] + [_P] * 6),
@@ -93,7 +95,8 @@ class ParamsT(C.Structure):
                 ("oversampling", C.c_double), ("overpartition", C.c_int),
                 ("imbalance", C.c_double), ("master_seed", C.c_int64),
                 ("stream_id", C.c_char_p), ("key_kind", C.c_int), ("with_stats", C.c_int),
-                ("scheme", C.c_int), ("record_holders", C.c_int)]
+                ("scheme", C.c_int), ("record_holders", C.c_int), ("level_base", C.c_int),
+                ("init_groups", C.c_int), ("pe_base", C.c_int)]
 
 
 class LevelReportT(C.Structure):
@@ -455,6 +458,15 @@ class Context:
         check(lib.ams_sort_run(self.h, C.byref(params), len(sz), sz.ctypes.data, ptr(keys),
                                ptr(vals), ptr(out), ptr(out_vals), out_sizes.ctypes.data, reps))
         return out_sizes[: len(sz)], list(reps)
+
+    def copy_ranges(self, ranges, src, dst, src_vals=None, dst_vals=None):
+        """dst[d + i] = src[s + i] for every (s, d, len) row of ``ranges``."""
+        rg = np.ascontiguousarray(ranges, dtype=np.uint64).reshape(-1, 3)
+        check(lib.ams_copy_ranges(self.h, rg.ctypes.data, len(rg), ptr(src), ptr(dst), ptr(src_vals),
+                                  ptr(dst_vals)))
+
+    def fill_iota(self, dst, n: int, start: int = 0):
+        check(lib.ams_fill_iota(self.h, ptr(dst), int(n), int(start)))
 
     def rlm_sort_run(self, group_counts, scheme: int, master_seed: int, stream_id: str, key_kind: int,
                      pe_sizes, keys, vals, out, out_origin, out_vals):

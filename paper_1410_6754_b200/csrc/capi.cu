@@ -643,6 +643,45 @@ int ams_level_scatter_peers(ams_ctx_t* c, const void* src, const void* src_vals,
   return AMS_OK;
 }
 
+int ams_copy_ranges(ams_ctx_t* c, const uint64_t* h_ranges, int nranges, const void* src, void* dst,
+                    const void* src_vals, void* dst_vals) {
+  if (!c || nranges < 0 || (nranges && (!h_ranges || !src || !dst))) return set_error(AMS_EINVAL, "null argument");
+  if ((src_vals == nullptr) != (dst_vals == nullptr))
+    return set_error(AMS_EINVAL, "values must be given for both source and destination");
+  if (nranges == 0) return AMS_OK;
+  AMS_ON_DEVICE(c->device);
+  // One work item (CTA) per kCopyItemKeys keys of a range.
+  std::vector<uint64_t> items;
+  uint64_t total = 0;
+  for (int q = 0; q < nranges; ++q) {
+    const uint64_t s0 = h_ranges[3 * q], d0 = h_ranges[3 * q + 1], len = h_ranges[3 * q + 2];
+    total += len;
+    for (uint64_t o = 0; o < len; o += kCopyItemKeys) {
+      items.push_back(s0 + o);
+      items.push_back(d0 + o);
+      items.push_back(std::min<uint64_t>(kCopyItemKeys, len - o));
+    }
+  }
+  if (items.empty()) return AMS_OK;
+  Stage& sc = c->st_copy;
+  sc.reset();
+  const size_t oi = sc.put(items);
+  AMS_CK(sc.upload(c->stream));
+  KTimer kt(c, AMS_KCAT_SCATTER, (src_vals ? 32.0 : 16.0) * (double)total);
+  AMS_CK(launch_copy_ranges(c->stream, sc.dev<uint64_t>(oi), (int)(items.size() / 3), src, dst, src_vals,
+                            dst_vals, total));
+  c->launches += 1;
+  return AMS_OK;
+}
+
+int ams_fill_iota(ams_ctx_t* c, void* dst, uint64_t n, uint64_t start) {
+  if (!c || (n && !dst)) return set_error(AMS_EINVAL, "null argument");
+  AMS_ON_DEVICE(c->device);
+  AMS_CK(launch_iota(c->stream, dst, n, start));
+  c->launches += n ? 1 : 0;
+  return AMS_OK;
+}
+
 int ams_get_minmax(ams_ctx_t* c, uint64_t out[2]) {
   if (!c || !out) return set_error(AMS_EINVAL, "null argument");
   if (!c->minmax.p) return set_error(AMS_EINVAL, "no min/max recorded");
@@ -1178,10 +1217,20 @@ int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* p
   if (!c || !prm) return set_error(AMS_EINVAL, "null argument");
   const int k = prm->levels;
   if (k < 1 || k > AMS_MAX_LEVELS) return set_error(AMS_EINVAL, "levels outside 1..AMS_MAX_LEVELS");
-  uint64_t prod = 1;
+  // Continuation (multi-GPU: the levels below level_base ran as the
+  // exchange between the GPUs): this call's PEs start as g0 equal groups.
+  const int lv0 = prm->level_base;
+  const int g0 = prm->init_groups > 0 ? prm->init_groups : 1;
+  const int pe_base = prm->pe_base;
+  if (lv0 < 0 || lv0 > k || pe_base < 0) return set_error(AMS_EINVAL, "bad continuation parameters");
+  if (lv0 == 0 && (g0 != 1 || pe_base != 0))
+    return set_error(AMS_EINVAL, "init_groups / pe_base need level_base > 0");
+  if (lv0 > 0 && !(prm->oversampling > 0))
+    return set_error(AMS_EINVAL, "a continuation needs the sort's oversampling factor");
+  uint64_t prod = (uint64_t)g0;
   for (int lv = 0; lv < k; ++lv) {  // AmsParams validation (ams.py:45-52, 61-65)
     if (prm->group_counts[lv] < 1) return set_error(AMS_EINVAL, "group counts must be positive");
-    prod *= (uint64_t)prm->group_counts[lv];
+    if (lv >= lv0) prod *= (uint64_t)prm->group_counts[lv];
   }
   if (prm->overpartition < 1) return set_error(AMS_EINVAL, "overpartitioning factor must be at least 1");
   if (!(prm->imbalance > 0)) return set_error(AMS_EINVAL, "imbalance budget must be positive");
@@ -1193,10 +1242,14 @@ int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* p
   uint64_t n = 0;
   for (int i = 0; i < p; ++i) n += pe_sizes[i];
   if (n && (!keys || !out)) return set_error(AMS_EINVAL, "null key buffer");
-  const bool user_vals = vals != nullptr;
-  if (user_vals && !out_vals) return set_error(AMS_EINVAL, "values need an output buffer");
   if (prm->scheme < AMS_SCHEME_SIMPLE || prm->scheme > AMS_SCHEME_RANDOMIZED)
     return set_error(AMS_EINVAL, "unknown delivery scheme");
+  // A continuation under a non-simple scheme takes the input's origin tags
+  // as `vals` (not user payloads).
+  const bool tags_in = lv0 > 0 && prm->scheme != AMS_SCHEME_SIMPLE && n > 0;
+  if (tags_in && !vals) return set_error(AMS_EINVAL, "the continuation needs the origin tags as vals");
+  const bool user_vals = vals != nullptr && !tags_in;
+  if (user_vals && !out_vals) return set_error(AMS_EINVAL, "values need an output buffer");
   // Deterministic delivery (delivery.py:188-306) can put a later source's
   // piece into an earlier member, so group-buffer order stops being origin
   // order: origin tags travel as the values and break key ties
@@ -1221,23 +1274,27 @@ int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* p
     if (with_vals) AMS_CK(c->work_v[i].ensure(wb));
   }
   if (det) {
-    AMS_CK(c->tags0.ensure(wb));
-    AMS_CK(launch_iota(c->stream, c->tags0.p, n));
-    c->launches += 1;
+    AMS_CK(c->tags0.ensure(wb));  // origin tags, later relayout scratch
+    if (!tags_in) {
+      AMS_CK(launch_iota(c->stream, c->tags0.p, n));
+      c->launches += 1;
+    }
   }
   const void* src = n ? keys : c->work[1].p;
-  const void* src_v = det ? c->tags0.p : (with_vals ? (n ? vals : c->work_v[1].p) : nullptr);
+  const void* src_v = tags_in ? vals : det ? c->tags0.p : (with_vals ? (n ? vals : c->work_v[1].p) : nullptr);
   void* dst_out = n ? out : c->work[1].p;
   void* dst_out_v = with_vals ? (n && !det ? out_vals : c->work_v[1].p) : nullptr;
-  int src_kind = prm->key_kind;
+  // A continuation's input went through a level scatter: order-mapped u64.
+  int src_kind = lv0 > 0 ? AMS_KEY_U64 : prm->key_kind;
   std::vector<uint64_t> sizes(pe_sizes, pe_sizes + p);
-  std::vector<int32_t> gf{0}, gn{p};
+  std::vector<int32_t> gf, gn;
+  for (int g = 0; g < g0; ++g) { gf.push_back(g * (p / g0)); gn.push_back(p / g0); }
   c->run_levels.assign(k, ams_ctx::LevelRec{});
   HostTrace tr(c->host_trace);
   tr.mark("setup");
   int rc;
   bool used_bm = false;
-  for (int lv = 0; lv < k; ++lv) {
+  for (int lv = lv0; lv < k; ++lv) {
     const int r = prm->group_counts[lv];
     const int G = (int)gf.size();
     std::vector<uint64_t> offs(p + 1, 0);
@@ -1254,9 +1311,21 @@ int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* p
     uint64_t cap = 0;
     for (uint64_t t : targets) cap += t;
     std::vector<uint64_t> idx(std::max<uint64_t>(cap, 1)), gpos(std::max<uint64_t>(cap, 1)), drawn(G);
-    rc = ams_draw_sample_positions(prm->master_seed, prm->stream_id, lv, G, gf.data(), gn.data(),
-                                   targets.data(), sizes.data(), offs.data(), cap, idx.data(),
-                                   gpos.data(), drawn.data());
+    if (pe_base == 0) {
+      rc = ams_draw_sample_positions(prm->master_seed, prm->stream_id, lv, G, gf.data(), gn.data(),
+                                     targets.data(), sizes.data(), offs.data(), cap, idx.data(),
+                                     gpos.data(), drawn.data());
+    } else {
+      // The streams are named by global PE ids (ams.py:168-174): shifted tables.
+      std::vector<uint64_t> gsz((size_t)pe_base + p, 0), gof((size_t)pe_base + p, 0);
+      std::copy(sizes.begin(), sizes.end(), gsz.begin() + pe_base);
+      std::copy(offs.begin(), offs.begin() + p, gof.begin() + pe_base);
+      std::vector<int32_t> gfn(gf);
+      for (int32_t& f : gfn) f += pe_base;
+      rc = ams_draw_sample_positions(prm->master_seed, prm->stream_id, lv, G, gfn.data(), gn.data(),
+                                     targets.data(), gsz.data(), gof.data(), cap, idx.data(),
+                                     gpos.data(), drawn.data());
+    }
     if (rc) return rc;
     tr.mark("draw");
     std::vector<int32_t> nb(G);
@@ -1274,6 +1343,8 @@ int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* p
     AMS_CK(c->s_keys.ensure(8 * (size_t)std::max<uint64_t>(S, 1)));
     AMS_CK(c->s_pos.ensure(4 * (size_t)std::max<uint64_t>(S, 1)));
     const uint64_t* tie_tags = det && lv > 0 ? static_cast<const uint64_t*>(src_v) : nullptr;
+    // (lv counts from the whole sort's first level: a continuation's input
+    // already went through a non-simple delivery.)
     if ((rc = level_sample_impl(c, src, src_kind, S, idx.data(), gpos.data(), c->s_keys.as<uint64_t>(),
                                 c->s_pos.as<uint32_t>(), tie_tags)))
       return rc;
@@ -1353,7 +1424,7 @@ int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* p
         int ns = 0;
         uint64_t* st4 = rec.has_stats ? rec.stats.data() + 4 * (size_t)g : nullptr;
         const std::string ls = std::string(prm->stream_id) + "/L" + std::to_string(lv) + "-g" +
-                               std::to_string(gf[g]);
+                               std::to_string(gf[g] + pe_base);
         if (prm->scheme == AMS_SCHEME_PERMUTED)
           rc = ams_deliver_permuted(P, r, prm->master_seed, ls.c_str(), pieces.data(),
                                     rec.new_sizes.data() + gf[g], slices.data(), cap, &ns, st4);
@@ -1361,7 +1432,7 @@ int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* p
           rc = ams_deliver_randomized(P, r, prm->master_seed, ls.c_str(), pieces.data(),
                                       rec.new_sizes.data() + gf[g], slices.data(), cap, &ns, st4);
         else
-          rc = ams_deliver_deterministic(P, r, gf[g], pieces.data(), rec.new_sizes.data() + gf[g],
+          rc = ams_deliver_deterministic(P, r, gf[g] + pe_base, pieces.data(), rec.new_sizes.data() + gf[g],
                                          slices.data(), cap, &ns, st4);
         if (rc) return rc;
         for (int q = 0; relayout && q < ns; ++q) {
@@ -1378,7 +1449,7 @@ int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* p
     void* sdst_v = dst_v;
     if (relayout) {  // scratch for the simple layout: the free work buffer / the output
       sdst = lv == 0 ? c->work[1].p : dst_out;
-      sdst_v = lv == 0 ? c->work_v[1].p : c->tags0.p;
+      sdst_v = lv == 0 ? c->work_v[1].p : c->tags0.p;  // tags0: free once level 1 is done
     }
     tr.mark("plan");
     if ((rc = level_scatter_impl(c, src, src_v, src_kind, sdst, sdst_v, r, rec.boundaries.data(),

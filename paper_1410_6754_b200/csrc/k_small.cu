@@ -49,10 +49,10 @@ __global__ void k_copy_bytes(uint8_t* __restrict__ dst, const uint8_t* __restric
   for (size_t i = head + tid; i < bytes; i += nt) dst[i] = src[i];
 }
 
-__global__ void k_iota(uint64_t* __restrict__ dst, uint64_t n) {
+__global__ void k_iota(uint64_t* __restrict__ dst, uint64_t n, uint64_t start) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x)
-    dst[i] = i;
+    dst[i] = start + i;
 }
 
 __global__ void k_gather_vals(const uint64_t* __restrict__ vals, const uint64_t* __restrict__ idx,
@@ -588,10 +588,10 @@ cudaError_t launch_copy_bytes(cudaStream_t st, void* dst, const void* src, size_
   return cudaGetLastError();
 }
 
-cudaError_t launch_iota(cudaStream_t st, void* dst, uint64_t n) {
+cudaError_t launch_iota(cudaStream_t st, void* dst, uint64_t n, uint64_t start) {
   if (n == 0) return cudaSuccess;
   const unsigned blocks = (unsigned)std::min<uint64_t>((n + 255) / 256, 148 * 16);
-  k_iota<<<blocks, 256, 0, st>>>(static_cast<uint64_t*>(dst), n);
+  k_iota<<<blocks, 256, 0, st>>>(static_cast<uint64_t*>(dst), n, start);
   return cudaGetLastError();
 }
 

@@ -58,7 +58,7 @@ cudaError_t launch_gather_sample(cudaStream_t st, const void* src, int kind, con
 // delivery's relayout.
 cudaError_t launch_copy_ranges(cudaStream_t st, const uint64_t* ranges, int nranges, const void* src,
                                void* dst, const void* src_vals, void* dst_vals, uint64_t total);
-cudaError_t launch_iota(cudaStream_t st, void* dst, uint64_t n);
+cudaError_t launch_iota(cudaStream_t st, void* dst, uint64_t n, uint64_t start = 0);
 // Byte copy by a kernel (mapped host memory <-> device without the copy engines).
 cudaError_t launch_copy_bytes(cudaStream_t st, void* dst, const void* src, size_t bytes);
 // out[i] = vals[idx[i]]

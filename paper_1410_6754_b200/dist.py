@@ -39,7 +39,8 @@ import torch
 import torch.distributed as dist
 
 from . import _lib as L
-from .engine import LevelRecord, bucket_table, check_out, load_budget, level_targets, key_kind_of
+from .engine import (SCHEMES, LevelRecord, check_out, key_kind_of, level_targets, load_budget,
+                     native_params, run_records)
 from .params import as_params, as_seed
 
 
@@ -145,6 +146,27 @@ class CudaOps:
     def final_sort(self, src, src_v, tmp, tmp_v, out, out_v, kind, offs, sizes):
         self.ctx.final_sort(src, src_v, tmp, tmp_v, out, out_v, kind, offs, sizes)
 
+    def iota(self, dst, n, start):
+        self.ctx.fill_iota(dst, n, start)
+
+    def copy_ranges(self, ranges, src, dst, src_v, dst_v):
+        self.ctx.copy_ranges(ranges, src, dst, src_v, dst_v)
+
+    def run_from(self, src, src_v, params, a, master, stream_id, kind, scheme, level_base,
+                 init_groups, pe_base, local_sizes, out, out_vals):
+        """The levels from `level_base` on and the final sort of this rank's
+        PEs: ams_sort_run continuing on the context that ran level 1 (it
+        holds the groups' key bounds).  Returns (final PE sizes, records)."""
+        prm = native_params(params, master, stream_id, kind, True, SCHEMES[scheme], False,
+                            oversampling=a, level_base=level_base, init_groups=init_groups,
+                            pe_base=pe_base)
+        n = int(np.asarray(local_sizes, dtype=np.uint64).sum())
+        final_sizes, _ = self.ctx.sort_run(prm, local_sizes, src if n else None,
+                                           src_v if n else None, out if n else None,
+                                           out_vals if (n and out_vals is not None) else None)
+        return final_sizes, run_records(self.ctx, self.ctx.run_id(), tuple(params.group_counts),
+                                        params.per_level_imbalance(), first_level=level_base)
+
     def final_sort_buckets(self, src, tmp, out, kind, bk_off, bk_len, bk_group, bk_bucket):
         self.ctx.final_sort_buckets(src, tmp, out, kind, bk_off, bk_len, bk_group, bk_bucket)
 
@@ -199,18 +221,27 @@ def level1_cell_base(hist: np.ndarray, bnd: np.ndarray, rank: int, world: int, p
 
 def sort_distributed(keys: torch.Tensor, pe_sizes_local, params, seed, ops, vals=None, out=None,
                      out_vals=None, key_kind=None, group=None, scheme: str = "simple"):
-    """Sort this rank's PEs as part of one global ams_sort(scheme="simple").
-    The multi-GPU driver implements the simple delivery scheme only; any
-    other ``scheme`` raises ValueError (single-GPU ``ams_sort_tensors``
-    implements all four).
+    """Sort this rank's PEs as part of one global ams_sort(scheme).
+
+    Level 1 (the group of all PEs) runs here across the ranks; under a
+    non-simple scheme (delivery.py:188-455) its delivery is the simple
+    exchange followed by a rank-local relayout (the members of a subgroup
+    live on one rank), with origin tags travelling as the values to break
+    key ties from level 2 on.  The later levels and the final sort are
+    rank-local: one ``ops.run_from`` call (``ams_sort_run`` continuing at
+    level 2 on the GPU).  User payloads are carried under the simple scheme
+    only.
 
     ``keys`` holds this rank's PEs (PE-major), ``pe_sizes_local`` their
     sizes; PE ids are rank-major (rank k owns PEs [k*p/G, (k+1)*p/G)).
     Returns (sorted local keys, vals, local per-PE sizes, level records); the
     rank-ordered concatenation of the outputs is the global sort."""
-    if scheme != "simple":
-        raise ValueError(f"the multi-GPU driver implements the simple delivery scheme only, "
-                         f"not {scheme!r}")
+    if scheme not in SCHEMES:
+        raise ValueError(f"unknown delivery scheme {scheme!r}; supported: {tuple(SCHEMES)}")
+    det = scheme != "simple"
+    if det and vals is not None:
+        raise ValueError("the multi-GPU driver carries payloads under the simple delivery scheme only "
+                         f"(origin tags travel as the values under {scheme!r})")
     params = as_params(params)
     master, stream_id = as_seed(seed)
     world = dist.get_world_size(group)
@@ -290,78 +321,51 @@ def sort_distributed(keys: torch.Tensor, pe_sizes_local, params, seed, ops, vals
         ops.set_minmax(min(los), max(his))
     bnd, loads, mx, new_sizes, stats = L.plan_level(gn, nb, r, hist)
     # Keys-only single level: buckets contiguous for the final sort (F7).
-    bucket_major = k_levels == 1 and vals is None
+    bucket_major = k_levels == 1 and vals is None and not det
     cell_base, bucket_dst, need = level1_cell_base(hist, bnd[0].astype(np.int64), rank, world,
                                                     pl, bucket_major)
     gpr = r // world                                               # groups per rank
-    recv, recv_v = ops.exchange(keys, vals, kind, need, cell_base, bucket_dst, r, bnd[0],
+    # Non-simple schemes: origin tags (index in the global input) travel as the values.
+    src_v = vals
+    if det:
+        src_v = ops.empty(n_local, torch.int64)
+        ops.iota(src_v, n_local, rank_off)
+    recv, recv_v = ops.exchange(keys, src_v, kind, need, cell_base, bucket_dst, r, bnd[0],
                                 rank * gpr, gpr, group=group)
+    n_recv = int(need[rank])
+    step = p // r                                                  # members of a subgroup
+    if det:
+        # Member assignment of the scheme from the replicated piece matrix;
+        # subgroup g's members all live on g's owner rank, so the relayout
+        # of the simple layout into the member arrays is rank-local.
+        bd = bnd[0].astype(np.int64)
+        pieces = np.stack([hist[:, bd[g]:bd[g + 1]].sum(axis=1, dtype=np.uint64) for g in range(r)],
+                          axis=1)
+        ls_name = f"{stream_id}/L0-g0"
+        if scheme == "deterministic":
+            new_sizes, slices, st4 = L.deliver_deterministic(pieces, 0)
+        elif scheme == "permuted":
+            new_sizes, slices, st4 = L.deliver_permuted(pieces, master, ls_name)
+        else:
+            new_sizes, slices, st4 = L.deliver_randomized(pieces, master, ls_name)
+        stats = st4.reshape(1, 4)
+        if step > 1:
+            m_g = pieces.sum(axis=0)
+            e0 = int(m_g[:rank * gpr].sum())                        # this rank's part of the simple layout
+            d0 = int(new_sizes[:pe_lo].sum())                       # ... and of the member arrays
+            sel = (slices[:, 0] >= e0) & (slices[:, 0] < e0 + n_recv) & (slices[:, 2] > 0)
+            loc = slices[sel].copy()
+            loc[:, 0] -= np.uint64(e0)
+            loc[:, 1] -= np.uint64(d0)
+            relaid, relaid_v = ops.empty(n_recv, torch.int64), ops.empty(n_recv, torch.int64)
+            ops.copy_ranges(loc, recv, relaid, recv_v, relaid_v)
+            recv, recv_v = relaid, relaid_v
     rec = LevelRecord(lv, r, gf, gn, sizes.copy(), drawn, nb, hist, bnd, loads, mx,
                       load_budget(n_g, r, eps_l), new_sizes, stats)
     levels.append(rec)
     my_groups = np.arange(rank * gpr, (rank + 1) * gpr)
-    final_buckets = None
-    if bucket_major:  # this rank's buckets in output order (level1_cell_base's layout)
-        tot = hist.astype(np.int64).sum(axis=0)
-        bk = np.arange(int(bnd[0][my_groups[0]]), int(bnd[0][my_groups[-1] + 1]), dtype=np.int32)
-        ln = tot[bk].astype(np.uint64)
-        off = np.concatenate([[0], np.cumsum(ln)[:-1]]).astype(np.uint64)
-        final_buckets = (off, ln, np.zeros(len(bk), np.int32), bk)
-
-    # ---------------- later levels: rank-local ------------------------------
-    sizes = new_sizes.astype(np.uint64)           # global-length; local entries used
-    src, src_v, src_kind = recv, recv_v, L.KEY_U64
-    step = p // r
-    gf = (pe_lo + np.arange(gpr, dtype=np.int64) * step).astype(np.int32)
-    gn = np.full(gpr, step, np.int32)
-    n_recv = int(need[rank])
-    work, work_v = ops.workspace(max(n_recv, 1), vals is not None)
-    buf = 0
-    for lv in range(1, k_levels):
-        r = params.group_counts[lv]
-        offs = np.zeros(p + 1, np.uint64)          # positions in the local buffer
-        np.cumsum(np.where((np.arange(p) >= pe_lo) & (np.arange(p) < pe_lo + pl), sizes, 0),
-                  out=offs[1:])
-        G = len(gf)
-        n_g = np.array([int(sizes[f:f + c].sum()) for f, c in zip(gf, gn)], np.uint64)
-        br, target = level_targets(n_g, r, b, a)
-        idx, gpos, drawn = L.draw_sample_positions(master, stream_id, lv, gf, gn, target, sizes,
-                                                   offs[:-1])
-        nb = np.minimum(br, drawn.astype(np.int64) + 1)
-        soff = np.zeros(G + 1, np.uint64)
-        np.cumsum(drawn, out=soff[1:])
-        S = int(soff[-1])
-        s_keys, s_pos = ops.empty(S, torch.int64), ops.empty(S, torch.int32)
-        ops.sample(src, src_kind, idx, gpos, s_keys, s_pos)
-        ops.splitters(s_keys, s_pos, soff, nb)
-        loc = slice(pe_lo, pe_lo + pl)
-        seg_group = np.repeat(np.arange(G, dtype=np.int32), gn)
-        posbase = -offs[gf].astype(np.int64)
-        nb_stride = int(nb.max())
-        last_level = lv == k_levels - 1
-        hist = ops.classify(src, src_kind, offs[loc], sizes[loc], seg_group, posbase, nb_stride,
-                            False, not (last_level and vals is None))
-        bnd, loads, mx, new_local, stats = L.plan_level(gn, nb, r, hist)
-        dst, dst_v = work[buf], work_v[buf]
-        # Keys-only last level: bucket-major groups for the fixed-capacity final sort.
-        bucket_major = last_level and vals is None
-        ops.scatter(src, src_v, src_kind, dst, dst_v, r, bnd, offs[gf], 0, G * r,
-                    bucket_major=bucket_major)
-        if bucket_major:
-            final_buckets = bucket_table(hist, gf - pe_lo, gn, nb, offs[gf])
-        rec = LevelRecord(lv, r, gf.copy(), gn.copy(), sizes[loc].copy(), drawn, nb, hist, bnd,
-                          loads, mx, load_budget(n_g, r, eps_l), new_local, stats)
-        levels.append(rec)
-        sizes = sizes.copy()
-        sizes[loc] = new_local
-        src, src_v = dst, dst_v
-        buf = 1 - buf
-        step = gn // r
-        gf = (gf[:, None] + np.arange(r, dtype=np.int32)[None, :] * step[:, None]).reshape(-1)
-        gf = gf.astype(np.int32)
-        gn = np.repeat(step, r).astype(np.int32)
-    local_final = sizes[pe_lo:pe_lo + pl].astype(np.uint64)
-    n_out = int(local_final.sum())
+    local_next = np.asarray(new_sizes, dtype=np.uint64)[pe_lo:pe_lo + pl]
+    n_out = int(local_next.sum())
     if isinstance(out, torch.Tensor) and out.is_cuda:
         check_out(out, n_out, dev, "out")
         check_out(out_vals, n_out, dev, "out_vals")
@@ -369,11 +373,54 @@ def sort_distributed(keys: torch.Tensor, pe_sizes_local, params, seed, ops, vals
         out = torch.empty(max(n_out, 1), dtype=keys.dtype, device=dev)
     if vals is not None and out_vals is None:
         out_vals = torch.empty(max(n_out, 1), dtype=vals.dtype, device=dev)
-    offs = np.zeros(pl + 1, np.uint64)
-    np.cumsum(local_final, out=offs[1:])
-    tmp, tmp_v = work[buf], work_v[buf]
-    if final_buckets is not None:
-        ops.final_sort_buckets(src, tmp, out, kind, *final_buckets)
-    else:
-        ops.final_sort(src, src_v, tmp, tmp_v, out, out_vals, kind, offs[:-1], local_final)
-    return out[:n_out], (out_vals[:n_out] if out_vals is not None else None), local_final, levels
+
+    if k_levels == 1:
+        # Single level: the received groups are the final PEs.
+        offs = np.zeros(pl + 1, np.uint64)
+        np.cumsum(local_next, out=offs[1:])
+        work, work_v = ops.workspace(max(n_recv, 1), recv_v is not None)
+        if bucket_major:  # this rank's buckets in output order (level1_cell_base's layout)
+            tot = hist.astype(np.int64).sum(axis=0)
+            bk = np.arange(int(bnd[0][my_groups[0]]), int(bnd[0][my_groups[-1] + 1]), dtype=np.int32)
+            ln = tot[bk].astype(np.uint64)
+            off = np.concatenate([[0], np.cumsum(ln)[:-1]]).astype(np.uint64)
+            ops.final_sort_buckets(recv, work[0], out, kind, off, ln, np.zeros(len(bk), np.int32), bk)
+        elif det:
+            # keys only (equal keys are indistinguishable): a key sort of every PE
+            ops.final_sort(recv, None, work[0], None, out, None, kind, offs[:-1], local_next)
+        else:
+            ops.final_sort(recv, recv_v, work[0], work_v[0], out, out_vals, kind, offs[:-1], local_next)
+        return out[:n_out], (out_vals[:n_out] if out_vals is not None else None), local_next, levels
+
+    # ---------------- later levels and the final sort: rank-local -----------
+    final_sizes, later = ops.run_from(recv, recv_v, params, a, master, stream_id, kind, scheme,
+                                      level_base=1, init_groups=gpr, pe_base=pe_lo,
+                                      local_sizes=local_next, out=out, out_vals=out_vals)
+    return (out[:n_out], (out_vals[:n_out] if out_vals is not None else None),
+            np.asarray(final_sizes, dtype=np.uint64), _Levels(levels, later))
+
+
+class _Levels(list):
+    """Level 1's record followed by the continuation's records, which are
+    read from the context on first use."""
+
+    def __init__(self, first, later):
+        super().__init__(first)
+        self._later = later
+
+    def _fill(self):
+        if self._later is not None:
+            later, self._later = self._later, None
+            self.extend(later() if callable(later) else later)
+
+    def __iter__(self):
+        self._fill()
+        return super().__iter__()
+
+    def __len__(self):
+        self._fill()
+        return super().__len__()
+
+    def __getitem__(self, i):
+        self._fill()
+        return super().__getitem__(i)

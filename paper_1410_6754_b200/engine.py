@@ -145,6 +145,54 @@ def load_budget(n_g: np.ndarray, r: int, eps_level: float) -> np.ndarray:
     return np.array([math.ceil((1.0 + eps_level) * int(n) / r) for n in n_g], dtype=np.int64)
 
 
+def run_records(ctx, run: int, group_counts, eps_l: float, first_level: int = 0,
+                record_holders: bool = False):
+    """Callable that reads the level records of ams_sort_run `run` from the
+    context on first use (levels first_level..; the context keeps 8 runs)."""
+
+    def levels():
+        recs = []
+        for lv in range(first_level, len(group_counts)):
+            r = group_counts[lv]
+            d = ctx.run_level(lv, run)
+            n_g = np.add.reduceat(d["sizes_before"], d["group_first"]) if len(d["sizes_before"]) \
+                else np.zeros(len(d["group_first"]), np.uint64)
+            recs.append(LevelRecord(lv, r, d["group_first"], d["group_npe"], d["sizes_before"],
+                                    d["drawn"], d["nb"].astype(np.int64), d["seg_hist"],
+                                    d["boundaries"], d["loads"], d["max_load"],
+                                    load_budget(n_g, r, eps_l), d["new_sizes"], d["stats"]))
+            if record_holders:
+                recs[-1].holders = ctx.run_level_holders(lv, len(d["sizes_before"]), run)
+        return recs
+    return levels
+
+
+def native_params(params, master, stream_id, kind, with_stats=True, scheme=0, record_holders=False,
+                  oversampling=None, level_base=0, init_groups=0, pe_base=0):
+    """ams_params_t for ams_sort_run (include/ams_b200.h)."""
+    prm = L.ParamsT()
+    gc = tuple(params.group_counts)
+    if len(gc) > L.MAX_LEVELS:
+        raise ValueError(f"at most {L.MAX_LEVELS} levels are supported")
+    prm.levels = len(gc)
+    for i, r in enumerate(gc):
+        prm.group_counts[i] = int(r)
+    a = oversampling if oversampling is not None else params.oversampling
+    prm.oversampling = float(a) if a is not None else 0.0
+    prm.overpartition = int(params.overpartition)
+    prm.imbalance = float(params.imbalance)
+    prm.master_seed = int(master)
+    prm.stream_id = stream_id.encode()
+    prm.key_kind = int(kind)
+    prm.with_stats = int(bool(with_stats))
+    prm.scheme = int(scheme)
+    prm.record_holders = int(bool(record_holders))
+    prm.level_base = int(level_base)
+    prm.init_groups = int(init_groups)
+    prm.pe_base = int(pe_base)
+    return prm
+
+
 class AmsSorter:
     """Device-resident AMS-sort on one GPU (one process per GPU)."""
 
@@ -297,39 +345,11 @@ class AmsSorter:
 
     def _sort_native(self, keys, vals, ret_out, ret_vals, out, out_vals, sizes, params, master,
                      stream_id, kind, with_stats, launches0, n, scheme=0, record_holders=False):
-        prm = L.ParamsT()
         gc = tuple(params.group_counts)
-        if len(gc) > L.MAX_LEVELS:
-            raise ValueError(f"at most {L.MAX_LEVELS} levels are supported")
-        prm.levels = len(gc)
-        for i, r in enumerate(gc):
-            prm.group_counts[i] = int(r)
-        prm.oversampling = float(params.oversampling) if params.oversampling is not None else 0.0
-        prm.overpartition = int(params.overpartition)
-        prm.imbalance = float(params.imbalance)
-        prm.master_seed = int(master)
-        prm.stream_id = stream_id.encode()
-        prm.key_kind = int(kind)
-        prm.with_stats = int(bool(with_stats))
-        prm.scheme = int(scheme)
-        prm.record_holders = int(bool(record_holders))
+        prm = native_params(params, master, stream_id, kind, with_stats, scheme, record_holders)
         final_sizes, _ = self.ctx.sort_run(prm, sizes, keys if n else None,
                                            vals if n else None, out if n else None,
                                            out_vals if n else None)
-        eps_l = params.per_level_imbalance()
-        ctx, run = self.ctx, self.ctx.run_id()
-
-        def levels():
-            recs = []
-            for lv, r in enumerate(gc):
-                d = ctx.run_level(lv, run)
-                n_g = np.add.reduceat(d["sizes_before"], d["group_first"]) if len(d["sizes_before"]) \
-                    else np.zeros(len(d["group_first"]), np.uint64)
-                recs.append(LevelRecord(lv, r, d["group_first"], d["group_npe"], d["sizes_before"],
-                                        d["drawn"], d["nb"].astype(np.int64), d["seg_hist"],
-                                        d["boundaries"], d["loads"], d["max_load"],
-                                        load_budget(n_g, r, eps_l), d["new_sizes"], d["stats"]))
-                if record_holders:
-                    recs[-1].holders = ctx.run_level_holders(lv, len(d["sizes_before"]), run)
-            return recs
+        levels = run_records(self.ctx, self.ctx.run_id(), gc, params.per_level_imbalance(),
+                             record_holders=record_holders)
         return SortOutput(ret_out, ret_vals, final_sizes, levels, self.ctx.launches - launches0)

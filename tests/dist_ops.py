@@ -158,3 +158,58 @@ class NumpyOps:
             o_[o:o + n] = _from_ordered(x[o:o + n][order], kind)
             if src_v is not None:
                 out_v.numpy()[o:o + n] = src_v.numpy()[o:o + n][order]
+
+    def iota(self, dst, n, start):
+        dst.numpy()[:n] = np.arange(start, start + n, dtype=np.int64)
+
+    def copy_ranges(self, ranges, src, dst, src_v, dst_v):
+        for s0, d0, ln in np.asarray(ranges, np.int64).reshape(-1, 3):
+            dst.numpy()[d0:d0 + ln] = src.numpy()[s0:s0 + ln]
+            if src_v is not None:
+                dst_v.numpy()[d0:d0 + ln] = src_v.numpy()[s0:s0 + ln]
+
+    def run_from(self, src, src_v, params, a, master, stream_id, kind, scheme, level_base,
+                 init_groups, pe_base, local_sizes, out, out_vals):
+        """The oracle's level loop (ams_oracle.ams_sort) from `level_base` on
+        for this rank's PEs [pe_base, pe_base + len(local_sizes))."""
+        from types import SimpleNamespace
+        sizes = [int(x) for x in local_sizes]
+        pl = len(sizes)
+        n = sum(sizes)
+        buf = _u(src)[:n].copy()
+        det = scheme != "simple"
+        org = src_v.numpy()[:n].astype(np.int64).copy() if det else np.arange(n, dtype=np.int64)
+        vbuf = src_v.numpy()[:n].copy() if (src_v is not None and not det) else None
+        groups = [(i * (pl // init_groups), pl // init_groups) for i in range(init_groups)]
+        recs = []
+        for lv in range(level_base, len(params.group_counts)):
+            r = params.group_counts[lv]
+            offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+            nbuf, norg = np.empty_like(buf), np.empty_like(org)
+            nv = None if vbuf is None else np.empty_like(vbuf)
+            nsz = list(sizes)
+            nxt, bnds = [], []
+            for lo, cnt in groups:
+                gs, ge = int(offs[lo]), int(offs[lo + cnt])
+                o, ov, ns, info, oo = O.ams_level(
+                    buf[gs:ge], sizes[lo:lo + cnt], r, params.overpartition, a, master, stream_id, lv,
+                    pe_base + lo, None if vbuf is None else vbuf[gs:ge], False, scheme,
+                    org[gs:ge] if det else None)
+                nbuf[gs:ge], norg[gs:ge] = o, (oo if det else org[gs:ge])
+                if nv is not None:
+                    nv[gs:ge] = ov
+                nsz[lo:lo + cnt] = ns
+                bnds.append(list(info.plan.boundaries))
+                stp = cnt // r
+                nxt.extend((lo + i * stp, stp) for i in range(r))
+            buf, org, vbuf, sizes, groups = nbuf, norg, nv, nsz, nxt
+            recs.append(SimpleNamespace(level=lv, boundaries=np.asarray(bnds, np.uint64)))
+        offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+        o_ = _u(out)
+        for pe in range(pl):
+            s_, e_ = int(offs[pe]), int(offs[pe + 1])
+            order = np.lexsort((org[s_:e_], buf[s_:e_])) if det else np.argsort(buf[s_:e_], kind="stable")
+            o_[s_:e_] = _from_ordered(buf[s_:e_][order], kind)
+            if vbuf is not None:
+                out_vals.numpy()[s_:e_] = vbuf[s_:e_][order]
+        return np.asarray(sizes, np.uint64), recs

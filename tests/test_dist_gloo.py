@@ -23,7 +23,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, keys, pe_sizes, groups, vals, q):
+def _worker(rank, world, port, keys, pe_sizes, groups, vals, q, scheme="simple"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -39,7 +39,7 @@ def _worker(rank, world, port, keys, pe_sizes, groups, vals, q):
         v = torch.from_numpy(vals[a:b].copy()) if vals is not None else None
         out, ov, sizes, levels = sort_distributed(
             k, pe_sizes[rank * pl:(rank + 1) * pl], AmsParams(tuple(groups), None, 16, 0.1),
-            SeedSpec(5, "algo/rep0"), NumpyOps(), vals=v, key_kind="u64")
+            SeedSpec(5, "algo/rep0"), NumpyOps(), vals=v, key_kind="u64", scheme=scheme)
         q.put((rank, out.numpy().view(np.uint64).copy(),
                None if ov is None else ov.numpy().copy(), [int(x) for x in sizes],
                [lv.boundaries.tolist() for lv in levels]))
@@ -49,11 +49,11 @@ def _worker(rank, world, port, keys, pe_sizes, groups, vals, q):
         dist.destroy_process_group()
 
 
-def run_world(world, keys, pe_sizes, groups, vals=None):
+def run_world(world, keys, pe_sizes, groups, vals=None, scheme="simple"):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, keys, pe_sizes, groups, vals, q))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, keys, pe_sizes, groups, vals, q, scheme))
              for r in range(world)]
     for pr in procs:
         pr.start()
@@ -104,13 +104,38 @@ def test_rejects_groups_straddling_ranks():
 
 
 @pytest.mark.parametrize("scheme", ["deterministic", "permuted", "randomized"])
-def test_rejects_other_schemes(scheme):
-    """The multi-GPU driver implements scheme="simple" only and says so
-    before touching the process group."""
+@pytest.mark.parametrize("world,groups,npe,dist_kind", [
+    (2, (4, 4), 250, "sorted"),
+    (2, (2, 2, 4), 250, "equal"),
+    (4, (8, 2), 300, "zipf"),
+    (2, (8,), 400, "uniform"),
+])
+def test_distributed_other_schemes_match_oracle(scheme, world, groups, npe, dist_kind):
+    """Non-simple deliveries (delivery.py:188-455) across ranks: level 1's
+    relayout is rank-local, origin tags break ties from level 2 on; keys
+    only.  Sorted / equal inputs place members differently from "simple"."""
+    p = int(np.prod(groups))
+    n = p * npe
+    rng = np.random.default_rng(world * 7 + npe)
+    keys = {"uniform": lambda: rng.integers(0, 2**64, n, dtype=np.uint64),
+            "zipf": lambda: O.zipf_keys(n, 3), "equal": lambda: np.full(n, 7, dtype=np.uint64),
+            "sorted": lambda: np.arange(n, dtype=np.uint64)}[dist_kind]()
+    pe_sizes = [npe] * p
+    ref = O.ams_sort(keys, pe_sizes, groups, None, 16, 0.1, 5, "algo/rep0", scheme=scheme)
+    res = run_world(world, keys, pe_sizes, groups, None, scheme)
+    assert np.array_equal(np.concatenate([r[1] for r in res]), ref.keys)
+    assert sum((r[3] for r in res), []) == list(ref.pe_sizes)
+    for r in res:
+        assert [int(x) for x in r[4][0][0]] == list(ref.levels[0][0].plan.boundaries)
+
+
+def test_other_schemes_reject_payloads():
     from paper_1410_6754_b200 import dist as D
     with pytest.raises(ValueError, match="simple delivery scheme only"):
         D.sort_distributed(torch.zeros(8, dtype=torch.int64), [4, 4], (2,), 1, ops=None,
-                           scheme=scheme)
+                           vals=torch.zeros(8, dtype=torch.int64), scheme="deterministic")
+    with pytest.raises(ValueError, match="unknown delivery scheme"):
+        D.sort_distributed(torch.zeros(8, dtype=torch.int64), [4, 4], (2,), 1, ops=None, scheme="x")
 
 
 @pytest.mark.parametrize("world,groups,npe,dist_kind", [
