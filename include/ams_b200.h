@@ -360,6 +360,39 @@ int ams_copy_ranges(ams_ctx_t* ctx, const uint64_t* h_ranges, int nranges, const
 int ams_fill_iota(ams_ctx_t* ctx, void* dst, uint64_t n, uint64_t start);
 
 /* ------------------------------------------------------------------ */
+/* Single-process multi-device driver: one context   */
+/* per entry of devices[] (entries may repeat: several contexts on one   */
+/* GPU), each with its own stream; peer access is enabled between        */
+/* distinct devices.  PE i lives on context i * G / p, and               */
+/* group_counts[0] must be a multiple of G, so only level 1 crosses      */
+/* devices: its pieces are stored straight into the owners' receive      */
+/* buffers over peer pointers (ams_level_scatter_peers); the later       */
+/* levels and the final sort run as ams_sort_run continuations.          */
+
+typedef struct ams_mg ams_mg_t;
+int ams_mg_create(const int* devices, int ngpu, ams_mg_t** out);
+int ams_mg_destroy(ams_mg_t* mg);
+int ams_mg_size(const ams_mg_t* mg);
+/* The i-th context (its ams_run_level* records hold the later levels of the
+ * PEs that live there; timing; launch counts). */
+int ams_mg_ctx(ams_mg_t* mg, int i, ams_ctx_t** out);
+/* ams_sort (ams.py:271-313) over G devices: keys[i] / out[i] (and vals /
+ * out_vals, simple scheme only; NULL otherwise) are device i's buffers for
+ * PEs [i*p/G, (i+1)*p/G), PE-major; out[i] must hold the device's final
+ * keys (sum of its out_pe_sizes; at most (1 + eps) n / G, ams.py:258).  The
+ * caller's inputs must be ready (no stream is shared with the caller); the
+ * call returns when every device has finished.  Results are bit-identical
+ * for every G (same logical PEs and seeded streams). */
+int ams_mg_sort_run(ams_mg_t* mg, const ams_params_t* params, int p, const uint64_t* pe_sizes,
+                    const void* const* keys, const void* const* vals, void* const* out,
+                    void* const* out_vals, uint64_t* out_pe_sizes, ams_level_report_t* reports);
+/* Level-1 records of the last ams_mg_sort_run (as ams_run_level; one group). */
+int ams_mg_level1_dims(const ams_mg_t* mg, int* r, int* p, int* nb_stride);
+int ams_mg_level1(const ams_mg_t* mg, uint64_t* sizes_before, uint64_t* drawn, int32_t* nb,
+                  uint32_t* seg_hist, uint64_t* boundaries, uint64_t* loads, uint64_t* max_load,
+                  uint64_t* new_sizes, uint64_t* stats);
+
+/* ------------------------------------------------------------------ */
 /* RLM-sort (recurse-last multiway mergesort, rlm.py:86-132): SURVEY     */
 /* section 8(f) row 4.                                                   */
 

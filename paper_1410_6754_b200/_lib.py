@@ -78,6 +78,13 @@ _SIGNATURES = {
     "ams_run_level_dims": (_I, [_P, _I, _P, _P, _P, _P, _P]),
     "ams_run_level": (_I, [_P, _I] + [_P] * 11),
     "ams_deliver_simple": (_I, [_I, _I, _P, _P, _P]),
+    "ams_mg_create": (_I, [_P, _I, C.POINTER(_P)]),
+    "ams_mg_destroy": (_I, [_P]),
+    "ams_mg_size": (_I, [_P]),
+    "ams_mg_ctx": (_I, [_P, _I, C.POINTER(_P)]),
+    "ams_mg_sort_run": (_I, [_P, _P, _I, _P, _P, _P, _P, _P, _P, _P]),
+    "ams_mg_level1_dims": (_I, [_P, _P, _P, _P]),
+    "ams_mg_level1": (_I, [_P] * 10),
     "ams_copy_ranges": (_I, [_P, _P, _I, _P, _P, _P, _P]),
     "ams_fill_iota": (_I, [_P, _P, _U64, _U64]),
     "ams_rlm_sort_run": (_I, [_P, _I, _P, _I, _I64, C.c_char_p, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P]),
