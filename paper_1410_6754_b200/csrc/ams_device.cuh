@@ -21,9 +21,7 @@ static_assert(kItems * kThreads == kTile, "tile geometry");
 // Tree classifier blob (one per group) in global memory: header, sorted
 // splitter keys and positions, and a key-range LUT whose cells hold
 // (first splitter index | splitter count << 16).
-#ifndef AMS_LUT_EXTRA_BITS
-#define AMS_LUT_EXTRA_BITS 6
-#endif
+constexpr int kLutExtraBits = 6;  // LUT cells per splitter = 2^6
 constexpr int kMaxSpl = AMS_MAX_BUCKETS;  // room for nb-1 <= 4095 splitters
 constexpr int kMaxLutBits = 13;
 constexpr int kMaxCells = 1 << kMaxLutBits;
@@ -82,7 +80,7 @@ __host__ __device__ inline int bit_length64(uint64_t x) {
 // one, so classification is one LUT load plus at most one compare.
 __host__ __device__ inline int lut_bits_for(int nspl) {
   int lg = bit_length64((uint64_t)nspl);  // ~ceil(log2(nspl+1))
-  int b = lg + AMS_LUT_EXTRA_BITS;
+  int b = lg + kLutExtraBits;
   return b < 4 ? 4 : (b > kMaxLutBits ? kMaxLutBits : b);
 }
 

@@ -184,9 +184,7 @@ int ams_ctx_create(int device, void* stream, ams_ctx_t** out) {
   ams_ctx* c = new ams_ctx();
   c->device = device;
   c->stream = static_cast<cudaStream_t>(stream);
-  if (const char* e = std::getenv("AMS_FINAL_BM")) c->bm_final = std::atoi(e) != 0;
   if (const char* e = std::getenv("AMS_HOST_TRACE")) c->host_trace = std::atoi(e) != 0;
-  if (const char* e = std::getenv("AMS_FIXED_FILL")) c->fixed_fill_pct = std::min(99, std::max(10, std::atoi(e)));
   *out = c;
   return AMS_OK;
 }
@@ -436,14 +434,12 @@ int ams_level_classify(ams_ctx_t* c, const void* src, int key_kind, int nseg,
   // classifying again.
   uint8_t* ids = nullptr;
   int id_bytes = nb_stride <= 256 ? 1 : 2;  // u16 ids up to AMS_MAX_BUCKETS buckets
-#ifndef AMS_NO_IDS
   {
     uint64_t span = 0;
     for (int s = 0; s < nseg; ++s) span = std::max(span, h_seg_off[s] + h_seg_len[s]);
     AMS_CK(c->ids.ensure((size_t)id_bytes * std::max<uint64_t>(span, 1)));
     ids = c->ids.as<uint8_t>();
   }
-#endif
   c->level_ids = ids != nullptr;
   c->level_id_bytes = id_bytes;
   int rc = run_histogram(c, src, key_kind, false, c->meta, c->nchunks, nb_stride, nullptr, mm,

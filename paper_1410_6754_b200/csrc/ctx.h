@@ -187,9 +187,9 @@ struct ams_ctx {
   DevBuf fx_scratch, fx_fill, fx_ovf, fx_base, fx_cnt, fx_seg;
   Stage st_fixed;
   uint64_t fixed_segments = 0, fixed_overflow_segments = 0;
-  bool bm_final = true;  // AMS_FINAL_BM=0 keeps the (g(b), j, b) last level + PE digit partition
+  bool bm_final = true;  // keys-only runs: bucket-major last level + fixed-capacity final sort
   bool host_trace = false;  // AMS_HOST_TRACE=1: host-side step times of ams_sort_run on stderr
-  int fixed_fill_pct = 88;  // AMS_FIXED_FILL: mean fill of the fixed-capacity cells (percent)
+  int fixed_fill_pct = 88;  // mean fill of the fixed-capacity cells (percent)
   // multi-GPU: buffers peers map (CUDA IPC) and the peers' buffers mapped here
   DevBuf peer_buf[8];
   std::vector<std::pair<std::string, void*>> peer_open;  // (handle bytes, mapped address)

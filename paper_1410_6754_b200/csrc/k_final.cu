@@ -175,10 +175,7 @@ __global__ void __launch_bounds__(kThreadsU, 2)
 }
 
 // -------------------------------------------------------------------- K9
-#ifndef AMS_SORT_THREADS
-#define AMS_SORT_THREADS 256
-#endif
-constexpr int kSortThreads = AMS_SORT_THREADS;
+constexpr int kSortThreads = 256;
 constexpr int kSortWarps = kSortThreads / 32;
 constexpr int kSortCap = AMS_SMEM_SORT_CAP;
 constexpr int kSortItems = kSortCap / kSortThreads;  // per-warp iterations
@@ -357,14 +354,7 @@ __global__ void __launch_bounds__(kSortThreads, 1)
 // keys alone skip step 4.  Cells whose keys cluster (a sub-bucket above
 // kRankMax that still needs ordering) go to the LSD fallback list.
 constexpr int kRankMax = 64;
-#ifndef AMS_SORT_CTAS
-#define AMS_SORT_CTAS 3
-#endif
-constexpr int kSortCtas = AMS_SORT_CTAS;  // resident CTAs per SM (register budget)
-#ifndef AMS_NIT_BREAK
-#define AMS_NIT_BREAK 0
-#endif
-constexpr bool kNitBreak = AMS_NIT_BREAK;
+constexpr int kSortCtas = 3;  // resident CTAs per SM (register budget)
 constexpr int kSubK = kCellSubBuckets;                   // sub-buckets of the refined digit
 constexpr int kScanWords = kSubK / 2 / kSortThreads;  // counter words per thread (2 sub-buckets each)
 static_assert(kScanWords % 4 == 0, "scan loads 4 words at a time");
@@ -489,11 +479,9 @@ __global__ void __launch_bounds__(kSortThreads, kSortCtas)
       sub0 = (blockIdx.x - cs.cell0[seg]) * (uint32_t)kSubK;
     }
   }
-  const int nit = (int)((n + kSortThreads - 1) / kSortThreads);  // items in use per thread
   uint64_t kr[kSortItems];
 #pragma unroll
   for (int it = 0; it < kSortItems; ++it) {
-    if (kNitBreak && it >= nit) break;
     const uint32_t i = it * kSortThreads + tid;
     kr[it] = i < n ? ldg_stream(src + off + i) : ~0ULL;
   }
@@ -512,7 +500,6 @@ __global__ void __launch_bounds__(kSortThreads, kSortCtas)
       uint64_t mn = ~0ULL, mx = 0;
 #pragma unroll
       for (int it = 0; it < kSortItems; ++it) {
-        if (kNitBreak && it >= nit) break;
         mn = min(mn, kr[it]);
         if (it * kSortThreads + tid < n) mx = max(mx, kr[it]);
       }
@@ -543,7 +530,6 @@ __global__ void __launch_bounds__(kSortThreads, kSortCtas)
     uint32_t nq = 0;  // sub-buckets this thread will queue (its keys of rank 1)
 #pragma unroll
     for (int it = 0; it < kSortItems; ++it) {
-      if (kNitBreak && it >= nit) break;
       pk[it] = 0xFFFFFFFFu;
       if (it * kSortThreads + tid < n) {
         const uint64_t x = kr[it] - lo;
@@ -609,7 +595,6 @@ __global__ void __launch_bounds__(kSortThreads, kSortCtas)
   // 3. place: slot = start(sub-bucket) + rank.
 #pragma unroll
   for (int it = 0; it < kSortItems; ++it) {
-    if (kNitBreak && it >= nit) break;
     if (pk[it] != 0xFFFFFFFFu) {
       const uint32_t s = pk[it] >> 16, rk = pk[it] & 0xFFFFu;
       const uint32_t slot = c16[sw16(s)] + rk;
@@ -696,15 +681,12 @@ __global__ void __launch_bounds__(kSortThreads, kSortCtas)
 //   5. 16-byte stores to the output.
 // Cells without a refined digit (m * K >= 2^32) go to the LSD list; cells
 // of counting-only buckets (m == 0) are one key value: filled directly.
-#ifndef AMS_FX_U16
-#define AMS_FX_U16 1
-#endif
 constexpr int kFxThreads = 256;
 constexpr int kFxItems = kSortCap / kFxThreads;   // 16
-constexpr int kFxCtas = AMS_FX_U16 ? 4 : 3;
-// Counters: 32-bit words, or (AMS_FX_U16) pairs of 16-bit halves.
-constexpr int kFxWords = kSubK / kFxThreads / (AMS_FX_U16 ? 2 : 1);  // counter words per scan thread
-static_assert(kFxWords == 32 || kFxWords == 16, "fixed-cell counter layout");
+constexpr int kFxCtas = 4;
+// Counters: pairs of 16-bit halves in 32-bit words.
+constexpr int kFxWords = kSubK / kFxThreads / 2;  // counter words per scan thread
+static_assert(kFxWords == 16, "fixed-cell counter layout");
 constexpr int kFxChunks = kFxWords / 4;
 __device__ __forceinline__ uint32_t fx_sw(uint32_t w) {
   // word w belongs to scan thread w / kFxWords, whose chunk c sits at c ^ rot(thread)
@@ -712,9 +694,8 @@ __device__ __forceinline__ uint32_t fx_sw(uint32_t w) {
 }
 
 // Start of sub-bucket s after the scan.
-__device__ __forceinline__ uint32_t fx_start(const uint32_t* cnt, const uint16_t* c16, uint32_t s) {
-  if constexpr (AMS_FX_U16) return c16[2 * fx_sw(s >> 1) + (s & 1)];
-  else return cnt[fx_sw(s)];
+__device__ __forceinline__ uint32_t fx_start(const uint16_t* c16, uint32_t s) {
+  return c16[2 * fx_sw(s >> 1) + (s & 1)];
 }
 
 template <int KIND_OUT>
@@ -762,7 +743,7 @@ __global__ void __launch_bounds__(kFxThreads, kFxCtas)
   }
   const uint32_t sh = d.sh, mk = (uint32_t)d.q, sub0 = digit * (uint32_t)kSubK;
   uint4* const cw4 = reinterpret_cast<uint4*>(cnt) + tid * (kFxWords / 4);
-  const uint32_t rot = (kFxChunks == 8 ? tid : tid >> 1) & (uint32_t)(kFxChunks - 1);
+  const uint32_t rot = (tid >> 1) & (uint32_t)(kFxChunks - 1);
 #pragma unroll
   for (int c = 0; c < kFxWords / 4; ++c) cw4[c ^ rot] = make_uint4(0, 0, 0, 0);
   const uint32_t nit = (n + kFxThreads - 1) / kFxThreads;  // uniform
@@ -781,13 +762,8 @@ __global__ void __launch_bounds__(kFxThreads, kFxCtas)
       pk[it] = 0xFFFFFFFFu;
       if (it * kFxThreads + tid < n) {
         const uint32_t sb = exact ? (uint32_t)(kr[it] - lo) : __umulhi((uint32_t)((kr[it] - lo) >> sh), mk) - sub0;
-        uint32_t rk;
-        if constexpr (AMS_FX_U16) {
-          const uint32_t hs = (sb & 1) * 16;
-          rk = (atomicAdd(&cnt[fx_sw(sb >> 1)], 1u << hs) >> hs) & 0xFFFFu;
-        } else {
-          rk = atomicAdd(&cnt[fx_sw(sb)], 1u);
-        }
+        const uint32_t hs = (sb & 1) * 16;
+        const uint32_t rk = (atomicAdd(&cnt[fx_sw(sb >> 1)], 1u << hs) >> hs) & 0xFFFFu;
         pk[it] = (sb << 12) | rk;
         nq += rk == 1;
       }
@@ -801,13 +777,10 @@ __global__ void __launch_bounds__(kFxThreads, kFxCtas)
     const uint4 v = cw4[c ^ rot];
     tw += v.x + v.y + v.z + v.w;
     big = max(big, max(max(v.x, v.y), max(v.z, v.w)));
-    if constexpr (AMS_FX_U16)
-      big = max(big, max(max(v.x << 16, v.y << 16), max(v.z << 16, v.w << 16)));
+    big = max(big, max(max(v.x << 16, v.y << 16), max(v.z << 16, v.w << 16)));
   }
-  if constexpr (AMS_FX_U16) {
-    big >>= 16;
-    tw = (tw & 0xFFFFu) + (tw >> 16);  // halves cannot carry: total <= n
-  }
+  big >>= 16;
+  tw = (tw & 0xFFFFu) + (tw >> 16);  // halves cannot carry: total <= n
   const uint32_t mine = tw | (nq << 16);  // both prefixes < 2^16
   const uint32_t inc = warp_incl_scan(mine);
 #pragma unroll
@@ -834,13 +807,8 @@ __global__ void __launch_bounds__(kFxThreads, kFxCtas)
 #pragma unroll
     for (int qq = 0; qq < 4; ++qq) {
       const uint32_t t = wv[qq];
-      if constexpr (AMS_FX_U16) {  // (start of low half, start of high half)
-        wv[qq] = run | ((run + (t & 0xFFFFu)) << 16);
-        run += (t & 0xFFFFu) + (t >> 16);
-      } else {
-        wv[qq] = run;
-        run += t;
-      }
+      wv[qq] = run | ((run + (t & 0xFFFFu)) << 16);  // (start of low half, start of high half)
+      run += (t & 0xFFFFu) + (t >> 16);
     }
     cw4[c ^ rot] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
   }
@@ -850,7 +818,7 @@ __global__ void __launch_bounds__(kFxThreads, kFxCtas)
   for (int it = 0; it < kFxItems; ++it) {
     if (it < (int)nit && pk[it] != 0xFFFFFFFFu) {
       const uint32_t sb = pk[it] >> 12, rk = pk[it] & 0xFFFu;
-      kB[fx_start(cnt, c16, sb) + rk] = kr[it];
+      kB[fx_start(c16, sb) + rk] = kr[it];
       if (rk == 1) q[qpos++] = (uint16_t)sb;
     }
   }
@@ -858,8 +826,8 @@ __global__ void __launch_bounds__(kFxThreads, kFxCtas)
   const uint32_t nqueue = exact ? 0 : s_scan[kFxThreads / 32] >> 16;  // exact: one value per sub-bucket
   for (uint32_t i = tid; i < nqueue; i += kFxThreads) {
     const uint32_t sb = q[i];
-    const uint32_t b0 = fx_start(cnt, c16, sb);
-    const uint32_t b1 = sb + 1 < (uint32_t)kSubK ? fx_start(cnt, c16, sb + 1) : n;
+    const uint32_t b0 = fx_start(c16, sb);
+    const uint32_t b1 = sb + 1 < (uint32_t)kSubK ? fx_start(c16, sb + 1) : n;
     if (b1 - b0 <= 3) {
       uint64_t k0 = kB[b0], k1 = kB[b0 + 1];
       if (b1 - b0 == 3) {
@@ -905,16 +873,12 @@ size_t smem_sort_lsd_bytes() {
   return (size_t)kSortCap * (8 + 8 + 2 + 2) + (size_t)4 * kSortWarps * kRadix + 4 * kRadix;
 }
 
-#ifndef AMS_FX_SORT
-#define AMS_FX_SORT 1
-#endif
-
 cudaError_t launch_smem_sort(cudaStream_t st, const void* src, const void* src_vals, void* out,
                              void* out_vals, int kind_out, const CellSource& cs, uint64_t ncells,
                              OverflowRec* ovf, unsigned int* ovf_count, OverflowRec* fb,
                              unsigned int* fb_count) {
   if (ncells == 0) return cudaSuccess;
-  if (AMS_FX_SORT && cs.mode == 3 && !src_vals && (out != nullptr) &&
+  if (cs.mode == 3 && !src_vals && (out != nullptr) &&
       ((reinterpret_cast<uintptr_t>(out) & 15) == 0)) {
     const size_t smem = (size_t)kSortCap * 8 + (size_t)kFxWords * kFxThreads * 4 + 2 * (size_t)kQueueCap;
     cudaError_t e = cudaSuccess;

@@ -7,10 +7,6 @@
 #include "ams_device.cuh"
 #include "launch.h"
 
-#ifndef AMS_HIST_PLAIN
-#define AMS_HIST_PLAIN 1
-#endif
-
 namespace ams {
 
 namespace {
@@ -72,7 +68,6 @@ __global__ void __launch_bounds__(kThreads) k_hist(const uint64_t* __restrict__ 
   // serialise 32-way on that counter) aggregate runs; the others (keys
   // spread over the buckets) take one atomic per key — no run bookkeeping.
   bool runs = true;
-#if AMS_HIST_PLAIN
   if constexpr (!DIGIT && !TAGS && DUP == 1) {
     if (last > first) {
       const uint32_t pb = (uint32_t)((int64_t)seg_off + posbase);
@@ -81,7 +76,6 @@ __global__ void __launch_bounds__(kThreads) k_hist(const uint64_t* __restrict__ 
       runs = b0 == b1;
     }
   }
-#endif
   auto tile_plain = [&](const uint64_t t0) {  // full tiles only
     const uint64_t base = seg_off + t0;
     uint64_t keys[kItems];

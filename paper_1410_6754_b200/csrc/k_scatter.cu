@@ -408,33 +408,18 @@ size_t scatter_u_smem_bytes(int nb, int nspl_cap, int cells_cap, bool digit) {
   return b;
 }
 
-#ifndef AMS_SCATTER_U_IDS
-#define AMS_SCATTER_U_IDS 0
-#endif
-constexpr bool kScatterUIds = AMS_SCATTER_U_IDS;
-
-cudaError_t launch_scatter_u(cudaStream_t st, const void* src, int kind, bool digit, void* dst,
-                             const SegMeta& m, uint64_t nchunks, const uint8_t* blobs,
-                             const DigitCls* dcls, int nspl_cap, int cells_cap, int nb_stride,
-                             const uint32_t* chunk_tot, const uint64_t* cell_base,
-                             const uint8_t* ids) {
+// The lean unstable kernel serves the exact digit rounds of the final sort
+// (keys only); the tree / stored-id classifiers keep the 4-CTA k_scatter.
+cudaError_t launch_scatter_u(cudaStream_t st, const void* src, void* dst, const SegMeta& m,
+                             uint64_t nchunks, const DigitCls* dcls, int nb_stride,
+                             const uint32_t* chunk_tot, const uint64_t* cell_base) {
   if (nchunks == 0) return cudaSuccess;
-  const size_t smem = scatter_u_smem_bytes(nb_stride, nspl_cap, cells_cap, digit || ids);
-  const uint64_t* s = static_cast<const uint64_t*>(src);
-  uint64_t* d = static_cast<uint64_t*>(dst);
-  cudaError_t e = cudaSuccess;
-#define AMS_SCATTER_U_GO(K, CL)                                                               \
-  {                                                                                           \
-    auto fn = k_scatter_u<K, CL>;                                                             \
-    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
-    if (e != cudaSuccess) return e;                                                           \
-    fn<<<(unsigned)nchunks, kThreadsU, smem, st>>>(s, d, m, blobs, dcls, nspl_cap, nb_stride, \
-                                                    chunk_tot, cell_base, ids);               \
-  }
-  if (digit) AMS_SCATTER_U_GO(AMS_KEY_U64, kClsDigit)
-  else if (ids) AMS_KIND_DISPATCH(kind, K, AMS_SCATTER_U_GO(K, kClsIds))
-  else AMS_KIND_DISPATCH(kind, K, AMS_SCATTER_U_GO(K, kClsTree))
-#undef AMS_SCATTER_U_GO
+  const size_t smem = scatter_u_smem_bytes(nb_stride, 0, 0, true);
+  auto fn = k_scatter_u<AMS_KEY_U64, kClsDigit>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  fn<<<(unsigned)nchunks, kThreadsU, smem, st>>>(static_cast<const uint64_t*>(src), static_cast<uint64_t*>(dst),
+                                                  m, nullptr, dcls, 0, nb_stride, chunk_tot, cell_base, nullptr);
   return cudaGetLastError();
 }
 
@@ -445,13 +430,8 @@ cudaError_t launch_scatter(cudaStream_t st, const void* src, const void* src_val
                            const uint64_t* cell_base, const uint8_t* ids, int id_bytes) {
   if (nchunks == 0) return cudaSuccess;
   const bool vals = src_vals != nullptr;
-#ifndef AMS_NO_SCATTER_U
-  // The lean unstable kernel pays off with the cheap digit classifier (the
-  // final partition); the tree classifier keeps the 4-CTA kernel below.
-  if (!stable && !vals && (digit || (ids && id_bytes == 1 && kScatterUIds)))
-    return launch_scatter_u(st, src, kind, digit, dst, m, nchunks, blobs, dcls, nspl_cap,
-                            cells_cap, nb_stride, chunk_tot, cell_base, digit ? nullptr : ids);
-#endif
+  if (!stable && !vals && digit)
+    return launch_scatter_u(st, src, dst, m, nchunks, dcls, nb_stride, chunk_tot, cell_base);
   const int mode = scatter_mode(nb_stride, stable);
   // Bucket bytes from the histogram pass replace the tree (and its shared memory).
   const size_t smem = scatter_smem_bytes(nb_stride, nspl_cap, cells_cap, digit || ids, vals, stable);
