@@ -162,6 +162,17 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU arms
+# What the reference arm is: the reference is pure Python and lives only in
+# the build container (/root/reference does not exist on the GPU box), so the
+# arm times its pinned numpy restatement (oracle/ams_oracle.py) at reduced n.
+# Measured in the build container (1 core, config 1 at full size, 2^20 keys):
+# the real mlpsort.ams.ams_sort 1.82 s = 0.58 M keys/s, the port 0.47 s =
+# 2.24 M keys/s - the port is the faster baseline.
+PORT_NOTE = ("oracle port of the Python reference at reduced n, not the reference itself and not the "
+             "same n as the GPU arm; in the build container the real mlpsort.ams.ams_sort sorts "
+             "config 1 (2^20 keys, 1 core) at 0.58 M keys/s and this port at 2.24 M keys/s")
+
+
 def cpu_port_rate(w: dict, budget_s: float = 20.0):
     """The oracle port (numpy restatement of the reference algorithm) on a
     bounded sample of the workload: same p, group counts, a-rule, b, eps;
@@ -251,7 +262,7 @@ def reference_arm(args, w):
         "config": {"workload": args.workload, "desc": w["desc"], "groups": list(w["groups"]),
                    "p": w["p"]},
         "cpu_baseline": {"value": rate, "unit": UNIT, "cores": workers, "kind": "port",
-                         "sample": sample, "host_cpus": os.cpu_count()},
+                         "sample": sample, "host_cpus": os.cpu_count(), "note": PORT_NOTE},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)

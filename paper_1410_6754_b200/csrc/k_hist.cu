@@ -7,9 +7,17 @@
 #include "ams_device.cuh"
 #include "launch.h"
 
+#ifndef AMS_PLAIN_BATCH
+#define AMS_PLAIN_BATCH 16
+#endif
+#ifndef AMS_HIST_CTAS
+#define AMS_HIST_CTAS 4
+#endif
+
 namespace ams {
 
 namespace {
+constexpr int kPlainBatch = AMS_PLAIN_BATCH;  // keys a thread loads before classifying them
 // -------------------------------------------------------------------- K3
 // One CTA per chunk (<= kChunkTiles tiles of one segment): classify every
 // key, count buckets in shared memory with run-aggregated atomics (a run of
@@ -24,7 +32,7 @@ namespace {
 // (duplicate-heavy keys), trying the thread's previous bucket first in
 // the binary search.  Each CTA of the other variant exits at once.
 template <int KIND, bool DIGIT, bool MINMAX, int IDS, bool TAGS = false, int DUP = 1>
-__global__ void __launch_bounds__(kThreads) k_hist(const uint64_t* __restrict__ src, SegMeta m,
+__global__ void __launch_bounds__(kThreads, AMS_HIST_CTAS) k_hist(const uint64_t* __restrict__ src, SegMeta m,
                                                    const uint8_t* __restrict__ blobs,
                                                    const DigitCls* __restrict__ dcls, int nspl_cap,
                                                    int nb_stride, uint32_t* __restrict__ chunk_tot,
@@ -78,17 +86,21 @@ __global__ void __launch_bounds__(kThreads) k_hist(const uint64_t* __restrict__ 
   }
   auto tile_plain = [&](const uint64_t t0) {  // full tiles only
     const uint64_t base = seg_off + t0;
-    uint64_t keys[kItems];
 #pragma unroll
-    for (int i = 0; i < kItems; ++i) keys[i] = to_ordered<KIND>(ldg_stream(src + base + i * kThreads + threadIdx.x));
+    for (int h = 0; h < kItems / kPlainBatch; ++h) {
+      uint64_t keys[kPlainBatch];
 #pragma unroll
-    for (int i = 0; i < kItems; ++i) {
-      const uint32_t e = i * kThreads + threadIdx.x;
-      const uint32_t b = tv.classify(keys[i], (uint32_t)((int64_t)base + posbase) + e, hint);
-      if constexpr (IDS == 1) ids[base + e] = (uint8_t)b;
-      if constexpr (IDS == 2) reinterpret_cast<uint16_t*>(ids)[base + e] = (uint16_t)b;
-      if constexpr (MINMAX) { mn = min(mn, (unsigned long long)keys[i]); mx = max(mx, (unsigned long long)keys[i]); }
-      atomicAdd(&hist[b], 1u);
+      for (int i = 0; i < kPlainBatch; ++i)
+        keys[i] = to_ordered<KIND>(ldg_stream(src + base + (h * kPlainBatch + i) * kThreads + threadIdx.x));
+#pragma unroll
+      for (int i = 0; i < kPlainBatch; ++i) {
+        const uint32_t e = (h * kPlainBatch + i) * kThreads + threadIdx.x;
+        const uint32_t b = tv.classify(keys[i], (uint32_t)((int64_t)base + posbase) + e, hint);
+        if constexpr (IDS == 1) ids[base + e] = (uint8_t)b;
+        if constexpr (IDS == 2) reinterpret_cast<uint16_t*>(ids)[base + e] = (uint16_t)b;
+        if constexpr (MINMAX) { mn = min(mn, (unsigned long long)keys[i]); mx = max(mx, (unsigned long long)keys[i]); }
+        atomicAdd(&hist[b], 1u);
+      }
     }
   };
   auto tile = [&](const uint64_t t0, const uint32_t tcount, auto full_tag) {

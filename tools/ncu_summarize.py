@@ -15,16 +15,16 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 # Kernel template -> bench category, in launch order of one cfg2 sort.
 CATS = [
     ("k_hist<0, 0, 1", "level_hist (level 1, minmax)"),
-    ("k_scatter<0, 2, 0, 0>", "level_scatter"),
-    ("k_scatter<0, 0, 0, 0>", "level_scatter"),
+    ("k_scatter<0, 2, 0, 0,", "level_scatter"),
+    ("k_scatter<0, 0, 0, 0,", "level_scatter"),
     ("k_hist<0, 0, 0", "level_hist (level 2)"),
-    ("k_scatter<0, 2, 0, 2>", "level_scatter_unstable"),
+    ("k_scatter<0, 2, 0, 2,", "level_scatter_unstable"),
     ("k_scatter_u<0, 2>", "level_scatter_unstable"),
     ("k_scatter_u<0, 0>", "level_scatter_unstable"),
     ("k_hist<0, 1", "final_hist"),
     ("k_scatter_fixed<0>", "final_scatter"),
     ("k_scatter_u<0, 1>", "final_scatter"),
-    ("k_scatter<0, 1, 0, 2>", "final_scatter"),
+    ("k_scatter<0, 1, 0, 2,", "final_scatter"),
     ("k_smem_sort<0, 0", "smem_sort"),
     ("k_cell_sort_fixed<0>", "smem_sort"),
     ("k_bucket_sort", "smem_sort"),
