@@ -198,7 +198,8 @@ __global__ void __launch_bounds__(kThreads, VALS ? 2 : 4)
       for (int i = 0; i < kItems; ++i) {
         if (pk[i] != kInvalid) {
           const uint32_t b = pk[i] >> 16;
-          const uint32_t slot = btot[b] + whw[b] + (pk[i] & 0xFFFFu);
+          // (one counter array: its scanned base is zero — no load)
+          const uint32_t slot = btot[b] + (kHists > 1 ? whw[b] : 0u) + (pk[i] & 0xFFFFu);
           keys_s[slot] = to_ordered<KIND>(kr[i]);
           bkt_s[slot] = (uint16_t)b;
           if constexpr (VALS) vals_s[slot] = vr[i];
