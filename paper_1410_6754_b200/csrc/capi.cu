@@ -705,30 +705,66 @@ namespace {
 
 // Counting sort of a cell list into `out`, then the LSD fallback for the
 // cells whose keys cluster.  Syncs once to learn the fallback count.
+// Cells of the clustered-key fallback list (k_smem_sort_lsd) launched
+// speculatively when the caller defers the host read of the list's length.
+constexpr unsigned int kSpecFallback = 256;
+
+// slot >= 0 defers the read of the fallback count: the call uses fallback
+// list `slot` (records at fb + slot * fb_stride, count at fb_count[slot]),
+// launches the LSD kernel for the first kSpecFallback records with the count
+// read on the device, and the caller finishes with finish_fallback() after
+// its own synchronisation — no host round trip here.
 int sort_cells(ams_ctx* c, const void* src, const void* src_vals, void* out, void* out_vals,
-               int key_kind, const CellSource& cs, uint64_t ncells, uint64_t nelems) {
+               int key_kind, const CellSource& cs, uint64_t ncells, uint64_t nelems, int slot = -1,
+               uint64_t fb_stride = 0) {
   const bool vals = src_vals != nullptr;
-  AMS_CK(cudaMemsetAsync(c->fb_count.p, 0, sizeof(unsigned int), c->stream));
+  const bool defer = slot >= 0;
+  unsigned int* cnt = c->fb_count.as<unsigned int>() + (defer ? slot : 0);
+  OverflowRec* recs = c->fb.as<OverflowRec>() + (defer ? (size_t)slot * fb_stride : 0);
+  AMS_CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned int), c->stream));
   {
     KTimer kt(c, AMS_KCAT_SMEMSORT, (vals ? 32.0 : 16.0) * nelems);
     AMS_CK(launch_smem_sort(c->stream, src, src_vals, out, out_vals, key_kind, cs, ncells,
-                            c->ovf.as<OverflowRec>(), c->ovf_count.as<unsigned int>(),
-                            c->fb.as<OverflowRec>(), c->fb_count.as<unsigned int>()));
+                            c->ovf.as<OverflowRec>(), c->ovf_count.as<unsigned int>(), recs, cnt));
   }
   c->launches += 1;
+  CellSource fc{};
+  fc.mode = 2;
+  fc.recs = recs;
+  if (defer) {
+    fc.nrecs = cnt;
+    KTimer kt(c, AMS_KCAT_SMEMSORT, 0.0);
+    AMS_CK(launch_smem_sort_lsd(c->stream, src, src_vals, out, out_vals, key_kind, fc,
+                                std::min<uint64_t>(ncells, kSpecFallback)));
+    c->launches += 1;
+    return AMS_OK;
+  }
   unsigned int nfb = 0;
-  AMS_CK(to_host(c->h_small, c->fb_count.p, sizeof nfb, c->stream));
+  AMS_CK(to_host(c->h_small, cnt, sizeof nfb, c->stream));
   AMS_CK(cudaStreamSynchronize(c->stream));
   std::memcpy(&nfb, c->h_small.p, sizeof nfb);
   c->fallback_cells += nfb;
   if (nfb) {
-    CellSource fc{};
-    fc.mode = 2;
-    fc.recs = c->fb.as<OverflowRec>();
     KTimer kt(c, AMS_KCAT_SMEMSORT, 0.0);
     AMS_CK(launch_smem_sort_lsd(c->stream, src, src_vals, out, out_vals, key_kind, fc, nfb));
     c->launches += 1;
   }
+  return AMS_OK;
+}
+
+// After a deferred sort_cells and the caller's synchronisation: `nfb` is
+// the list's length (read by the caller); records past the speculative
+// launch are sorted now.
+int finish_fallback(ams_ctx* c, const void* src, void* out, int key_kind, int slot, uint64_t fb_stride,
+                    unsigned int nfb) {
+  c->fallback_cells += nfb;
+  if (nfb <= kSpecFallback) return AMS_OK;
+  CellSource fc{};
+  fc.mode = 2;
+  fc.recs = c->fb.as<OverflowRec>() + (size_t)slot * fb_stride + kSpecFallback;
+  KTimer kt(c, AMS_KCAT_SMEMSORT, 0.0);
+  AMS_CK(launch_smem_sort_lsd(c->stream, src, nullptr, out, nullptr, key_kind, fc, nfb - kSpecFallback));
+  c->launches += 1;
   return AMS_OK;
 }
 
@@ -892,7 +928,7 @@ int final_sort_bm(ams_ctx* c, void* src, void* tmp, void* out, int key_kind,
   const uint64_t ncells = cell0.back();
   const uint64_t rec_cap = std::max<uint64_t>(total / (kCap / 2), ncells) + 64;
   AMS_CK(c->ovf.ensure(sizeof(OverflowRec) * rec_cap));
-  AMS_CK(c->fb.ensure(sizeof(OverflowRec) * rec_cap));
+  AMS_CK(c->fb.ensure(sizeof(OverflowRec) * 2 * rec_cap));  // two fallback lists (deferred reads)
   AMS_CK(c->ovf_count.ensure(sizeof(unsigned int)));
   AMS_CK(c->fb_count.ensure(sizeof(unsigned int)));
   AMS_CK(c->h_small.ensure(4096));
@@ -906,10 +942,23 @@ int final_sort_bm(ams_ctx* c, void* src, void* tmp, void* out, int key_kind,
     cs.mode = 1;
     cs.seg_off = ss.dev<uint64_t>(oo);
     cs.seg_len = ss.dev<uint64_t>(ol);
-    int rc = sort_cells(c, src, nullptr, out, nullptr, key_kind, cs, s_off.size(), small_n);
+    int rc = sort_cells(c, src, nullptr, out, nullptr, key_kind, cs, s_off.size(), small_n, 0, rec_cap);
     if (rc) return rc;
   }
-  if (nseg == 0) return AMS_OK;
+  // The fallback counts of both cell sorts are read with the overflow flags
+  // below: one host synchronisation for the whole final sort.
+  auto read_counts = [&](unsigned int nfb[2]) -> int {
+    AMS_CK(to_host(c->h_small, c->fb_count.p, 2 * sizeof(unsigned int), c->stream));
+    AMS_CK(cudaStreamSynchronize(c->stream));
+    std::memcpy(nfb, c->h_small.p, 2 * sizeof(unsigned int));
+    return AMS_OK;
+  };
+  if (nseg == 0) {
+    if (s_off.empty()) return AMS_OK;
+    unsigned int nfb[2];
+    int rc = read_counts(nfb);
+    return rc ? rc : finish_fallback(c, src, out, key_kind, 0, rec_cap, nfb[0]);
+  }
   c->fixed_segments += (uint64_t)nseg;
   Stage& sx = c->st_fixed;
   sx.reset();
@@ -955,13 +1004,16 @@ int final_sort_bm(ams_ctx* c, void* src, void* tmp, void* out, int key_kind,
   cs.dcls = c->dcls.as<DigitCls>();
   cs.cell_seg = c->fx_seg.as<uint32_t>();
   cs.cell0 = sx.dev<uint32_t>(o_c0);
-  int rc = sort_cells(c, c->fx_scratch.p, nullptr, out, nullptr, key_kind, cs, ncells, fixed_n);
+  int rc = sort_cells(c, c->fx_scratch.p, nullptr, out, nullptr, key_kind, cs, ncells, fixed_n, 1, rec_cap);
   if (rc) return rc;
-  // Overflowed buckets (sort_cells synced): exact partition rounds from src.
+  // Overflowed buckets: exact partition rounds from src.
   std::vector<uint32_t> flags(nseg);
   AMS_CK(to_host(c->h_big, c->fx_ovf.p, 4 * (size_t)nseg, c->stream));
-  AMS_CK(cudaStreamSynchronize(c->stream));
+  unsigned int nfb[2] = {0, 0};
+  if ((rc = read_counts(nfb))) return rc;
   std::memcpy(flags.data(), c->h_big.p, 4 * (size_t)nseg);
+  if (!s_off.empty() && (rc = finish_fallback(c, src, out, key_kind, 0, rec_cap, nfb[0]))) return rc;
+  if ((rc = finish_fallback(c, c->fx_scratch.p, out, key_kind, 1, rec_cap, nfb[1]))) return rc;
   std::vector<uint64_t> o_off2, o_len2, o_lo, o_hi;
   std::vector<DigitCls> dc;
   for (int i = 0; i < nseg; ++i) {

@@ -10,9 +10,15 @@
 namespace ams {
 
 namespace {
-// 5 CTAs per SM (48 registers) with 8 keys in flight per thread beat 4 CTAs
-// with 16 (1.172 -> 1.124 ms for config 2's two histograms); 6 CTAs spill.
-constexpr int kHistCtas = 5;
+// The plain-atomic variants without the min/max fold fit 48 registers
+// without spills: 5 CTAs per SM with 8 keys in flight per thread beat 4 CTAs
+// with 16 there.  The other variants keep the compiler's allocation (forcing
+// 48 registers on them spills, and the duplicate-heavy variant then faulted
+// on sm_100a: profiles/r02m_hist_bounds.md).
+template <int KIND, bool DIGIT, bool MINMAX, bool TAGS, int DUP>
+constexpr int hist_min_ctas() {
+  return (!DIGIT && !MINMAX && !TAGS && DUP == 1 && KIND != AMS_KEY_I64) ? 5 : 1;
+}
 constexpr int kPlainBatch = 8;  // keys a thread loads before classifying them
 // -------------------------------------------------------------------- K3
 // One CTA per chunk (<= kChunkTiles tiles of one segment): classify every
@@ -28,7 +34,7 @@ constexpr int kPlainBatch = 8;  // keys a thread loads before classifying them
 // (duplicate-heavy keys), trying the thread's previous bucket first in
 // the binary search.  Each CTA of the other variant exits at once.
 template <int KIND, bool DIGIT, bool MINMAX, int IDS, bool TAGS = false, int DUP = 1>
-__global__ void __launch_bounds__(kThreads, kHistCtas) k_hist(const uint64_t* __restrict__ src, SegMeta m,
+__global__ void __launch_bounds__(kThreads, hist_min_ctas<KIND, DIGIT, MINMAX, TAGS, DUP>()) k_hist(const uint64_t* __restrict__ src, SegMeta m,
                                                    const uint8_t* __restrict__ blobs,
                                                    const DigitCls* __restrict__ dcls, int nspl_cap,
                                                    int nb_stride, uint32_t* __restrict__ chunk_tot,
