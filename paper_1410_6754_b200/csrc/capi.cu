@@ -894,7 +894,7 @@ int final_sort_bm(ams_ctx* c, void* src, void* tmp, void* out, int key_kind,
                   const std::vector<uint64_t>& bk_off, const std::vector<uint64_t>& bk_len,
                   const std::vector<int32_t>& bk_g, const std::vector<int32_t>& bk_b,
                   const uint64_t* d_group_bounds) {
-  constexpr uint64_t kCap = AMS_SMEM_SORT_CAP;
+  constexpr uint64_t kCap = AMS_FX_CAP;
   // Cells average fixed_fill_pct of capacity: with keys uniform inside a
   // bucket a cell's count is ~ N(target, sqrt(target)), far below capacity.
   const uint64_t kTarget = kCap * (uint64_t)c->fixed_fill_pct / 100;

@@ -18,17 +18,30 @@ namespace {
 // order (only membership matters: F7).  A cell that would exceed its
 // capacity flags its segment; the host re-partitions such segments exactly
 // from `src`, which this kernel does not modify.
+// Geometry of the fixed-capacity partition: 2048-key tiles, 256 threads, 4
+// CTAs per SM (4096-key tiles on 512 threads at 2 CTAs per SM: 1.202 ->
+// 1.154 ms at config 2 — fewer warps per barrier, more CTAs to interleave).
+#ifndef AMS_FTILE
+#define AMS_FTILE 2048
+#endif
+constexpr int kFTile = AMS_FTILE;
+constexpr int kFItems = 8;
+constexpr int kFThreads = kFTile / kFItems;
+constexpr int kFWarps = kFThreads / 32;
+constexpr int kFCtas = 2 * 4096 / kFTile;
+static_assert(kTile % kFTile == 0, "chunks are whole tiles of both kinds");
+
 template <int KIND>
-__global__ void __launch_bounds__(kThreadsU, 2)
+__global__ void __launch_bounds__(kFThreads, kFCtas)
     k_scatter_fixed(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst, SegMeta m,
                     const DigitCls* __restrict__ dcls, const uint32_t* __restrict__ cell0,
                     uint32_t* __restrict__ fill, uint32_t* __restrict__ seg_ovf) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ int s_seg;
-  __shared__ uint32_t s_scan[kWarpsU + 1];
+  __shared__ uint32_t s_scan[kFWarps + 1];
   __shared__ uint32_t s_clip;
   __shared__ __align__(8) uint64_t s_bar[2];
-  constexpr int kBuf = kTile + 2;
+  constexpr int kBuf = kFTile + 2;
   uint64_t* buf0 = reinterpret_cast<uint64_t*>(smem);
   const int tid = threadIdx.x;
   const uint64_t c = blockIdx.x;
@@ -45,8 +58,8 @@ __global__ void __launch_bounds__(kThreadsU, 2)
   const int nb = (int)dc.nb;
   const uint64_t dlo = dc.lo;
   const uint32_t dsh = dc.sh, dm = dc.m32, dmax = dc.nb - 1;
-  const int per = (nb + kThreadsU - 1) / kThreadsU | 1;
-  const int nbp = per * kThreadsU;
+  const int per = (nb + kFThreads - 1) / kFThreads | 1;
+  const int nbp = per * kFThreads;
   int64_t* adj = reinterpret_cast<int64_t*>(buf0 + 2 * kBuf);  // this tile: dst index - slot
   uint32_t* cnt = reinterpret_cast<uint32_t*>(adj + nbp);       // counts, then tile starts
   int32_t* lim = reinterpret_cast<int32_t*>(cnt + nbp);         // writable keys of the run
@@ -54,26 +67,26 @@ __global__ void __launch_bounds__(kThreadsU, 2)
   const uint64_t seg_off = m.off[s];
   const uint64_t first = (c - m.chunk_prefix[s]) * (uint64_t)m.chunk;
   const uint64_t last = min(first + (uint64_t)m.chunk, m.len[s]);
-  const int ntiles = (int)((last - first + kTile - 1) / kTile);
+  const int ntiles = (int)((last - first + kFTile - 1) / kFTile);
   const uint64_t cbase = cell0[s];
   // Tile t = keys [base, base + tc); the copy starts at the 16-byte boundary
   // base - h and is rounded up to whole 16-byte units (the source is the
   // last level's work buffer, padded by two keys), so key e of the tile sits
   // at buf[e + h].
   auto issue = [&](int t) {
-    const uint64_t base = seg_off + first + (uint64_t)t * kTile;
-    const uint32_t tc = (uint32_t)min((uint64_t)kTile, last - first - (uint64_t)t * kTile);
+    const uint64_t base = seg_off + first + (uint64_t)t * kFTile;
+    const uint32_t tc = (uint32_t)min((uint64_t)kFTile, last - first - (uint64_t)t * kFTile);
     const uint32_t h = (uint32_t)(base & 1);
     bulk_load(buf0 + (t & 1) * kBuf, src + (base - h), ((tc + h + 1) & ~1u) * 8, &s_bar[t & 1]);
   };
   if (tid == 0) issue(0);
-  for (int b = tid; b < nbp; b += kThreadsU) cnt[b] = 0;
+  for (int b = tid; b < nbp; b += kFThreads) cnt[b] = 0;
   const int w = tid >> 5, lane = tid & 31;
   __syncthreads();
   for (int t = 0; t < ntiles; ++t) {
     uint64_t* buf = buf0 + (t & 1) * kBuf;
-    const uint64_t base = seg_off + first + (uint64_t)t * kTile;
-    const uint32_t tc = (uint32_t)min((uint64_t)kTile, last - first - (uint64_t)t * kTile);
+    const uint64_t base = seg_off + first + (uint64_t)t * kFTile;
+    const uint32_t tc = (uint32_t)min((uint64_t)kFTile, last - first - (uint64_t)t * kFTile);
     const uint32_t h = (uint32_t)(base & 1);
     if (tid == 0 && t + 1 < ntiles) {
       fence_proxy_async();
@@ -81,13 +94,13 @@ __global__ void __launch_bounds__(kThreadsU, 2)
     }
     mbar_wait(&s_bar[t & 1], (uint32_t)(t >> 1) & 1u);
     const uint64_t* tb = buf + h;
-    uint64_t kr[kItemsU];
-    uint32_t pk[kItemsU];
+    uint64_t kr[kFItems];
+    uint32_t pk[kFItems];
     auto classify_all = [&](auto full_tag) {
       constexpr bool FULL = decltype(full_tag)::value;
 #pragma unroll
-      for (int i = 0; i < kItemsU; ++i) {
-        const uint32_t e = w * (kItemsU * 32) + i * 32 + lane;
+      for (int i = 0; i < kFItems; ++i) {
+        const uint32_t e = w * (kFItems * 32) + i * 32 + lane;
         pk[i] = kInvalid;
         if (FULL || e < tc) {
           const uint64_t key = to_ordered<KIND>(tb[e]);
@@ -107,12 +120,12 @@ __global__ void __launch_bounds__(kThreadsU, 2)
         }
       }
     };
-    if (tc == (uint32_t)kTile) classify_all(std::true_type{});
+    if (tc == (uint32_t)kFTile) classify_all(std::true_type{});
     else classify_all(std::false_type{});
     __syncthreads();
     if (dm == 0) {
       // One key value per cell: only the counts matter (no capacity bound).
-      for (int b = tid; b < nbp; b += kThreadsU) {
+      for (int b = tid; b < nbp; b += kFThreads) {
         const uint32_t v = cnt[b];
         if (v) atomicAdd(&fill[cbase + b], v);
         cnt[b] = 0;
@@ -126,7 +139,7 @@ __global__ void __launch_bounds__(kThreadsU, 2)
       for (int j = 0; j < per; ++j) sum += cnt[b0 + j];
       const uint32_t inc = warp_incl_scan(sum);
       if (lane == 31) s_scan[w] = inc;
-      scan_warp_totals<kThreadsU>(s_scan);
+      scan_warp_totals<kFThreads>(s_scan);
       uint32_t start = s_scan[w] + inc - sum;
       for (int j = 0; j < per; ++j) {
         const int b = b0 + j;
@@ -135,8 +148,8 @@ __global__ void __launch_bounds__(kThreadsU, 2)
         if (v) {
           // Reserve this run's room in cell (s, b).
           const uint32_t at = atomicAdd(&fill[cbase + b], v);
-          adj[b] = (int64_t)((cbase + b) * (uint64_t)AMS_SMEM_SORT_CAP + at) - (int64_t)start;
-          const int32_t room = (int32_t)AMS_SMEM_SORT_CAP - (int32_t)at;
+          adj[b] = (int64_t)((cbase + b) * (uint64_t)AMS_FX_CAP + at) - (int64_t)start;
+          const int32_t room = (int32_t)AMS_FX_CAP - (int32_t)at;
           lim[b] = (int32_t)start + room;  // slots below lim are written
           if ((uint32_t)max(room, 0) < v) {
             s_clip = 1;
@@ -148,7 +161,7 @@ __global__ void __launch_bounds__(kThreadsU, 2)
     }
     __syncthreads();
 #pragma unroll
-    for (int i = 0; i < kItemsU; ++i) {
+    for (int i = 0; i < kFItems; ++i) {
       if (pk[i] != kInvalid) {
         const uint32_t b = pk[i] >> 16;
         const uint32_t slot = cnt[b] + (pk[i] & 0xFFFFu);
@@ -158,9 +171,9 @@ __global__ void __launch_bounds__(kThreadsU, 2)
     }
     __syncthreads();
     if (!s_clip) {
-      for (uint32_t j = tid; j < tc; j += kThreadsU) dst[adj[bkt[j]] + j] = buf[j];
+      for (uint32_t j = tid; j < tc; j += kFThreads) dst[adj[bkt[j]] + j] = buf[j];
     } else {
-      for (uint32_t j = tid; j < tc; j += kThreadsU) {
+      for (uint32_t j = tid; j < tc; j += kFThreads) {
         const uint32_t b = bkt[j];
         if ((int32_t)j < lim[b]) dst[adj[b] + j] = buf[j];
       }
@@ -212,7 +225,7 @@ __device__ __forceinline__ void cell_of(const CellSource& cs, uint64_t cid, uint
     count = cs.recs[cid].count;
     oo = cs.recs[cid].out;
   } else {  // fixed-capacity cells: source slot cid, output base from k_fixed_cells
-    off = cid * (uint64_t)AMS_SMEM_SORT_CAP;
+    off = cid * (uint64_t)AMS_FX_CAP;
     count = cs.cell_cnt[cid];
     oo = cs.cell_base[cid];
   }
@@ -476,7 +489,7 @@ __global__ void __launch_bounds__(kSortThreads, kSortCtas)
       lo = d.lo;
       m32 = (uint32_t)d.q;
       sh = d.sh;
-      sub0 = (blockIdx.x - cs.cell0[seg]) * (uint32_t)kSubK;
+      sub0 = (blockIdx.x - cs.cell0[seg]) * (uint32_t)kFxSubBuckets;
     }
   }
   uint64_t kr[kSortItems];
@@ -681,12 +694,18 @@ __global__ void __launch_bounds__(kSortThreads, kSortCtas)
 //   5. 16-byte stores to the output.
 // Cells without a refined digit (m * K >= 2^32) go to the LSD list; cells
 // of counting-only buckets (m == 0) are one key value: filled directly.
-constexpr int kFxThreads = 256;
-constexpr int kFxItems = kSortCap / kFxThreads;   // 16
-constexpr int kFxCtas = 4;
+#ifndef AMS_FX_ITEMS
+#define AMS_FX_ITEMS 16
+#endif
+constexpr int kFxItems = AMS_FX_ITEMS;
+constexpr int kFxCap = AMS_FX_CAP;
+constexpr int kFxSubK = kFxSubBuckets;
+constexpr int kFxQueueCap = kFxCap / 2;
+constexpr int kFxThreads = kFxCap / kFxItems;
+constexpr int kFxCtas = (kFxItems == 16 ? 4 : 6) * 256 / kFxThreads;
 // Counters: pairs of 16-bit halves in 32-bit words.
-constexpr int kFxWords = kSubK / kFxThreads / 2;  // counter words per scan thread
-static_assert(kFxWords == 16, "fixed-cell counter layout");
+constexpr int kFxWords = kFxSubK / kFxThreads / 2;  // counter words per scan thread
+static_assert(kFxWords == 16 || kFxWords == 8, "fixed-cell counter layout");
 constexpr int kFxChunks = kFxWords / 4;
 __device__ __forceinline__ uint32_t fx_sw(uint32_t w) {
   // word w belongs to scan thread w / kFxWords, whose chunk c sits at c ^ rot(thread)
@@ -706,13 +725,13 @@ __global__ void __launch_bounds__(kFxThreads, kFxCtas)
   __shared__ uint32_t s_scan[kFxThreads / 32 + 1];
   __shared__ uint32_t s_big[kFxThreads / 32];
   uint64_t* kB = reinterpret_cast<uint64_t*>(smem);
-  uint32_t* cnt = reinterpret_cast<uint32_t*>(kB + kSortCap);
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(kB + kFxCap);
   uint16_t* q = reinterpret_cast<uint16_t*>(cnt + kFxWords * kFxThreads);
   const uint16_t* c16 = reinterpret_cast<const uint16_t*>(cnt);
   const uint32_t cid = blockIdx.x;
   const uint32_t n = cs.cell_cnt[cid];
   if (n == 0) return;
-  const uint64_t off = (uint64_t)cid * kSortCap, oo = cs.cell_base[cid];
+  const uint64_t off = (uint64_t)cid * kFxCap, oo = cs.cell_base[cid];
   const uint32_t seg = cs.cell_seg[cid];
   const DigitCls& d = cs.dcls[seg];
   const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -731,7 +750,7 @@ __global__ void __launch_bounds__(kFxThreads, kFxCtas)
     const uint64_t m = d.m32;
     const uint64_t x0 = (((uint64_t)digit << 32) + m - 1) / m;
     const uint64_t x1 = (((uint64_t)(digit + 1) << 32) + m - 1) / m;
-    if (d.sh != 0 || x1 - x0 > (uint64_t)kSubK) {
+    if (d.sh != 0 || x1 - x0 > (uint64_t)kFxSubK) {
       if (tid == 0) {
         OverflowRec r; r.off = off; r.count = n; r.lo = 0; r.hi = 0; r.out = oo;
         fb[atomicAdd(fb_count, 1u)] = r;
@@ -741,9 +760,10 @@ __global__ void __launch_bounds__(kFxThreads, kFxCtas)
     exact = true;
     lo += x0;
   }
-  const uint32_t sh = d.sh, mk = (uint32_t)d.q, sub0 = digit * (uint32_t)kSubK;
+  const uint32_t sh = d.sh, mk = (uint32_t)d.q, sub0 = digit * (uint32_t)kFxSubK;
   uint4* const cw4 = reinterpret_cast<uint4*>(cnt) + tid * (kFxWords / 4);
-  const uint32_t rot = (tid >> 1) & (uint32_t)(kFxChunks - 1);
+  // chunk c of thread t sits at c ^ rot(t), rot(t) = ((first word of t) >> 5) & (chunks - 1)
+  const uint32_t rot = ((tid * (uint32_t)kFxWords) >> 5) & (uint32_t)(kFxChunks - 1);
 #pragma unroll
   for (int c = 0; c < kFxWords / 4; ++c) cw4[c ^ rot] = make_uint4(0, 0, 0, 0);
   const uint32_t nit = (n + kFxThreads - 1) / kFxThreads;  // uniform
@@ -827,7 +847,7 @@ __global__ void __launch_bounds__(kFxThreads, kFxCtas)
   for (uint32_t i = tid; i < nqueue; i += kFxThreads) {
     const uint32_t sb = q[i];
     const uint32_t b0 = fx_start(c16, sb);
-    const uint32_t b1 = sb + 1 < (uint32_t)kSubK ? fx_start(c16, sb + 1) : n;
+    const uint32_t b1 = sb + 1 < (uint32_t)kFxSubK ? fx_start(c16, sb + 1) : n;
     if (b1 - b0 <= 3) {
       uint64_t k0 = kB[b0], k1 = kB[b0 + 1];
       if (b1 - b0 == 3) {
@@ -880,7 +900,7 @@ cudaError_t launch_smem_sort(cudaStream_t st, const void* src, const void* src_v
   if (ncells == 0) return cudaSuccess;
   if (cs.mode == 3 && !src_vals && (out != nullptr) &&
       ((reinterpret_cast<uintptr_t>(out) & 15) == 0)) {
-    const size_t smem = (size_t)kSortCap * 8 + (size_t)kFxWords * kFxThreads * 4 + 2 * (size_t)kQueueCap;
+    const size_t smem = (size_t)kFxCap * 8 + (size_t)kFxWords * kFxThreads * 4 + 2 * (size_t)kFxQueueCap;
     cudaError_t e = cudaSuccess;
     AMS_KIND_DISPATCH(kind_out, K, {
       auto fn = k_cell_sort_fixed<K>;
@@ -941,9 +961,9 @@ cudaError_t launch_smem_sort_lsd(cudaStream_t st, const void* src, const void* s
 }
 
 size_t scatter_fixed_smem_bytes(int nb) {
-  const int per = (nb + kThreadsU - 1) / kThreadsU | 1;
-  const size_t nbp = (size_t)per * kThreadsU;
-  return 2 * 8 * (size_t)(kTile + 2) + 16 * nbp + 2 * (size_t)kTile;
+  const int per = (nb + kFThreads - 1) / kFThreads | 1;
+  const size_t nbp = (size_t)per * kFThreads;
+  return 2 * 8 * (size_t)(kFTile + 2) + 16 * nbp + 2 * (size_t)kFTile;
 }
 
 cudaError_t launch_scatter_fixed(cudaStream_t st, const void* src, int kind, void* dst,
@@ -959,7 +979,7 @@ cudaError_t launch_scatter_fixed(cudaStream_t st, const void* src, int kind, voi
   auto fn = k_scatter_fixed<AMS_KEY_U64>;
   e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  fn<<<(unsigned)nchunks, kThreadsU, smem, st>>>(s, d, m, dcls, cell0, fill, seg_ovf);
+  fn<<<(unsigned)nchunks, kFThreads, smem, st>>>(s, d, m, dcls, cell0, fill, seg_ovf);
   return cudaGetLastError();
 }
 

@@ -17,7 +17,7 @@ namespace {
 // on sm_100a: profiles/r02m_hist_bounds.md).
 template <int KIND, bool DIGIT, bool MINMAX, bool TAGS, int DUP>
 constexpr int hist_min_ctas() {
-  return (!DIGIT && !MINMAX && !TAGS && DUP == 1 && KIND != AMS_KEY_I64) ? 5 : 0;  // 0: no bound
+  return (!DIGIT && !MINMAX && !TAGS && DUP == 1 && KIND != AMS_KEY_I64) ? 5 * kCtaDiv : 0;  // 0: no bound
 }
 // -------------------------------------------------------------------- K3
 // One CTA per chunk (<= kChunkTiles tiles of one segment): classify every
@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(kThreads, hist_min_ctas<KIND, DIGIT, MINMAX, T
     }
   }
   // keys a thread loads before classifying them: 8 at 5 CTAs/SM, else all 16
-  constexpr int kPlainBatch = hist_min_ctas<KIND, DIGIT, MINMAX, TAGS, DUP>() == 5 ? 8 : kItems;
+  constexpr int kPlainBatch = hist_min_ctas<KIND, DIGIT, MINMAX, TAGS, DUP>() != 0 ? 8 : kItems;
   auto tile_plain = [&](const uint64_t t0) {  // full tiles only
     const uint64_t base = seg_off + t0;
 #pragma unroll

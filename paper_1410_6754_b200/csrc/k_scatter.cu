@@ -23,7 +23,7 @@ namespace {
 // bucket_dst[b] (values: bucket_vdst[b]) — this GPU's own or a peer GPU's,
 // mapped over NVLink — at the cell bases' indices; dst / dst_vals are unused.
 template <int KIND, int CLS, bool VALS, int MODE, bool PEERS = false>
-__global__ void __launch_bounds__(kThreads, VALS ? 2 : 4)
+__global__ void __launch_bounds__(kThreads, (VALS ? 2 : 4) * kCtaDiv)
     k_scatter(const uint64_t* __restrict__ src, const uint64_t* __restrict__ src_vals,
               uint64_t* __restrict__ dst, uint64_t* __restrict__ dst_vals, SegMeta m,
               const uint8_t* __restrict__ blobs, const DigitCls* __restrict__ dcls, int nspl_cap,
@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(kThreads, VALS ? 2 : 4)
 // tile is permuted bucket-major in place and written as coalesced runs.
 
 template <int KIND, int CLS>
-__global__ void __launch_bounds__(kThreadsU, 2)
+__global__ void __launch_bounds__(kThreadsU, 2 * kCtaDiv)
     k_scatter_u(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst, SegMeta m,
                 const uint8_t* __restrict__ blobs, const DigitCls* __restrict__ dcls, int nspl_cap,
                 int nb, const uint32_t* __restrict__ chunk_tot,

@@ -511,7 +511,7 @@ __global__ void k_bucket_ranges(const uint8_t* __restrict__ blobs, const uint64_
   d.sh = (uint32_t)max(0, bit_length64(range) - 26);
   const uint64_t R = range >> d.sh;
   d.m32 = R + 1 <= (uint64_t)d.nb ? 0u : (uint32_t)(((uint64_t)d.nb << 32) / (R + 1));
-  const uint64_t mk = (uint64_t)d.m32 * (uint64_t)(kCellSubBuckets);
+  const uint64_t mk = (uint64_t)d.m32 * (uint64_t)(kFxSubBuckets);
   d.q = mk < (1ull << 32) ? mk : 0;  // sub-bucket multiplier of the cell sort
   out[s] = d;
 }
