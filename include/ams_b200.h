@@ -42,14 +42,10 @@ extern "C" {
 
 /* Kernel tile (elements per CTA tile in the level kernels) and the
  * largest bucket the CTA-local final sort handles in shared memory. */
-#ifndef AMS_TILE
 #define AMS_TILE 4096
-#endif
 #define AMS_SMEM_SORT_CAP 4096
 /* capacity of the fixed-capacity digit cells of the keys-only final sort */
-#ifndef AMS_FX_CAP
 #define AMS_FX_CAP 2048
-#endif
 #define AMS_MAX_BUCKETS 4096
 
 const char* ams_last_error(void);

@@ -10,15 +10,11 @@ namespace ams {
 // Level kernel geometry: a tile is kThreads x kItems consecutive keys of one
 // segment (PE); a chunk is up to kChunkTiles consecutive tiles of one
 // segment, processed by one CTA of the histogram kernel.
-#ifndef AMS_CTA_DIV
-#define AMS_CTA_DIV 1
-#endif
-constexpr int kCtaDiv = AMS_CTA_DIV;
-constexpr int kThreads = 256 / kCtaDiv;
+constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kItems = AMS_TILE / kThreads;  // 16
 constexpr int kTile = AMS_TILE;              // 4096
-constexpr int kChunkTiles = 16 * kCtaDiv;
+constexpr int kChunkTiles = 16;
 constexpr int kChunk = kTile * kChunkTiles;  // keys per histogram / scatter CTA
 static_assert(kItems * kThreads == kTile, "tile geometry");
 
@@ -310,7 +306,7 @@ __device__ inline void block_excl_scan_u16(uint32_t* wv, int nwords, uint32_t* s
 
 // ---- helpers shared by the kernel translation units -------------------------
 // Unstable scatters (k_scatter_u, k_scatter_fixed): 16 warps x 8 keys per tile, 2 CTAs per SM.
-constexpr int kThreadsU = 512 / kCtaDiv;
+constexpr int kThreadsU = 512;
 constexpr int kItemsU = kTile / kThreadsU;
 constexpr int kWarpsU = kThreadsU / 32;
 // Sub-buckets of the cell sort: two per key of cell capacity.

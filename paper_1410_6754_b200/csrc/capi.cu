@@ -103,22 +103,22 @@ void chunk_layout(const uint64_t* len, int nseg, uint64_t chunk, std::vector<uin
 // many buckets a chunk stays >= 4 keys per bucket (its histogram row is
 // nb_stride words of scan work).
 constexpr uint64_t kFillCtas = 148 * 8;
-uint32_t pick_chunk(const uint64_t* len, int nseg, int nb_stride) {
+uint32_t pick_chunk(const uint64_t* len, int nseg, int nb_stride, uint64_t max_chunk) {
   uint64_t total = 0;
   for (int s = 0; s < nseg; ++s) total += len[s];
   uint64_t c = (total / kFillCtas + kTile - 1) / kTile * kTile;
   c = std::max<uint64_t>(c, (uint64_t)kTile);
-  c = std::max<uint64_t>(c, std::min<uint64_t>((uint64_t)kChunk, 4 * (uint64_t)std::max(nb_stride, 1) / kTile * kTile));
-  return (uint32_t)std::min<uint64_t>(c, (uint64_t)kChunk);
+  c = std::max<uint64_t>(c, std::min<uint64_t>(max_chunk, 4 * (uint64_t)std::max(nb_stride, 1) / kTile * kTile));
+  return (uint32_t)std::min<uint64_t>(c, max_chunk);
 }
 
 // Upload a segment table; returns the device-side SegMeta.
 cudaError_t upload_segments(Stage& st, cudaStream_t stream, const uint64_t* off,
                             const uint64_t* len, const int32_t* cls, int nseg,
                             const int64_t* posbase, int ncls, SegMeta* m, uint64_t* nchunks,
-                            int nb_stride) {
+                            int nb_stride, uint64_t max_chunk = kChunk) {
   std::vector<uint64_t> cp;
-  m->chunk = pick_chunk(len, nseg, nb_stride);
+  m->chunk = pick_chunk(len, nseg, nb_stride, max_chunk);
   chunk_layout(len, nseg, m->chunk, cp);
   st.reset();
   const size_t o_off = st.put(off, nseg), o_len = st.put(len, nseg), o_cls = st.put(cls, nseg);
@@ -968,8 +968,9 @@ int final_sort_bm(ams_ctx* c, void* src, void* tmp, void* out, int key_kind,
   for (int i = 0; i < nseg; ++i) idx[i] = i;
   SegMeta m;
   uint64_t nchunks;
+  // (the fixed partition likes half-size chunks: 1.153 -> 1.131 ms at config 2)
   AMS_CK(upload_segments(c->st_final, c->stream, f_off.data(), f_len.data(), idx.data(), nseg, nullptr,
-                         0, &m, &nchunks, 1));
+                         0, &m, &nchunks, 1, kChunk / 2));
   AMS_CK(c->dcls.ensure(sizeof(DigitCls) * (size_t)nseg));
   AMS_CK(c->fx_fill.ensure(4 * (size_t)ncells));
   AMS_CK(c->fx_ovf.ensure(4 * (size_t)nseg));

@@ -21,10 +21,7 @@ namespace {
 // Geometry of the fixed-capacity partition: 2048-key tiles, 256 threads, 4
 // CTAs per SM (4096-key tiles on 512 threads at 2 CTAs per SM: 1.202 ->
 // 1.154 ms at config 2 — fewer warps per barrier, more CTAs to interleave).
-#ifndef AMS_FTILE
-#define AMS_FTILE 2048
-#endif
-constexpr int kFTile = AMS_FTILE;
+constexpr int kFTile = 2048;
 constexpr int kFItems = 8;
 constexpr int kFThreads = kFTile / kFItems;
 constexpr int kFWarps = kFThreads / 32;
@@ -694,15 +691,12 @@ __global__ void __launch_bounds__(kSortThreads, kSortCtas)
 //   5. 16-byte stores to the output.
 // Cells without a refined digit (m * K >= 2^32) go to the LSD list; cells
 // of counting-only buckets (m == 0) are one key value: filled directly.
-#ifndef AMS_FX_ITEMS
-#define AMS_FX_ITEMS 16
-#endif
-constexpr int kFxItems = AMS_FX_ITEMS;
+constexpr int kFxItems = 16;  // 8 keys per thread on twice the threads measured no better
 constexpr int kFxCap = AMS_FX_CAP;
 constexpr int kFxSubK = kFxSubBuckets;
 constexpr int kFxQueueCap = kFxCap / 2;
 constexpr int kFxThreads = kFxCap / kFxItems;
-constexpr int kFxCtas = (kFxItems == 16 ? 4 : 6) * 256 / kFxThreads;
+constexpr int kFxCtas = 4 * 256 / kFxThreads;
 // Counters: pairs of 16-bit halves in 32-bit words.
 constexpr int kFxWords = kFxSubK / kFxThreads / 2;  // counter words per scan thread
 static_assert(kFxWords == 16 || kFxWords == 8, "fixed-cell counter layout");

@@ -17,7 +17,7 @@ namespace {
 // on sm_100a: profiles/r02m_hist_bounds.md).
 template <int KIND, bool DIGIT, bool MINMAX, bool TAGS, int DUP>
 constexpr int hist_min_ctas() {
-  return (!DIGIT && !MINMAX && !TAGS && DUP == 1 && KIND != AMS_KEY_I64) ? 5 * kCtaDiv : 0;  // 0: no bound
+  return (!DIGIT && !MINMAX && !TAGS && DUP == 1 && KIND != AMS_KEY_I64) ? 5 : 0;  // 0: no bound
 }
 // -------------------------------------------------------------------- K3
 // One CTA per chunk (<= kChunkTiles tiles of one segment): classify every

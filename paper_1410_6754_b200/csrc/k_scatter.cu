@@ -22,8 +22,14 @@ namespace {
 // PEERS (multi-GPU level 1): bucket b's runs go to the buffer at address
 // bucket_dst[b] (values: bucket_vdst[b]) — this GPU's own or a peer GPU's,
 // mapped over NVLink — at the cell bases' indices; dst / dst_vals are unused.
+// 256 threads x 16 keys per 4096-key tile, 4 CTAs per SM (512 threads x 8 keys
+// at 2 or 3 CTAs per SM: 1.47 -> 1.75-1.92 ms, profiles/r02v_ab_scatter_threads.txt).
+constexpr int kSThreads = 256;
+constexpr int kSWarps = kSThreads / 32;
+constexpr int kSItems = kTile / kSThreads;
+constexpr int kSCtas = 4;  // resident CTAs per SM without values
 template <int KIND, int CLS, bool VALS, int MODE, bool PEERS = false>
-__global__ void __launch_bounds__(kThreads, (VALS ? 2 : 4) * kCtaDiv)
+__global__ void __launch_bounds__(kSThreads, VALS ? kSCtas / 2 : kSCtas)
     k_scatter(const uint64_t* __restrict__ src, const uint64_t* __restrict__ src_vals,
               uint64_t* __restrict__ dst, uint64_t* __restrict__ dst_vals, SegMeta m,
               const uint8_t* __restrict__ blobs, const DigitCls* __restrict__ dcls, int nspl_cap,
@@ -33,8 +39,8 @@ __global__ void __launch_bounds__(kThreads, (VALS ? 2 : 4) * kCtaDiv)
               const uint64_t* __restrict__ bucket_vdst = nullptr) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ int s_seg;
-  __shared__ uint32_t s_scan[kWarps + 1];
-  constexpr int kHists = MODE == kRankWarp ? kWarps : 1;
+  __shared__ uint32_t s_scan[kSWarps + 1];
+  constexpr int kHists = MODE == kRankWarp ? kSWarps : 1;
   uint64_t* keys_s = reinterpret_cast<uint64_t*>(smem);
   uint64_t* vals_s = keys_s + kTile;
   // Per-bucket output bases of the tile (dst index - slot); the serial mode
@@ -59,7 +65,7 @@ __global__ void __launch_bounds__(kThreads, (VALS ? 2 : 4) * kCtaDiv)
   {
     const uint32_t* ct = chunk_tot + c * nb_stride;
     const uint64_t* cb = cell_base + (uint64_t)s * nb_stride;
-    for (int b = threadIdx.x; b < nb_stride; b += kThreads) run[b] = (int64_t)(cb[b] + ct[b]);
+    for (int b = threadIdx.x; b < nb_stride; b += kSThreads) run[b] = (int64_t)(cb[b] + ct[b]);
   }
   TreeView tv;
   DigitView dv;
@@ -88,21 +94,21 @@ __global__ void __launch_bounds__(kThreads, (VALS ? 2 : 4) * kCtaDiv)
   for (uint64_t t0 = first; t0 < last; t0 += kTile) {
     const uint32_t tcount = (uint32_t)min((uint64_t)kTile, last - t0);
     const uint64_t base = seg_off + t0;
-    for (uint32_t j = threadIdx.x; j < tcount; j += kThreads) {
+    for (uint32_t j = threadIdx.x; j < tcount; j += kSThreads) {
       cp_async8(keys_s + j, src + base + j);
       if constexpr (VALS) cp_async8(vals_s + j, src_vals + base + j);
     }
-    for (int i = threadIdx.x; i < kHists * nb_stride; i += kThreads) wh[i] = 0;
+    for (int i = threadIdx.x; i < kHists * nb_stride; i += kSThreads) wh[i] = 0;
     cp_async_wait_all();
     __syncthreads();  // tile staged, counters zeroed, tree loaded
-    uint32_t pk[kItems];
+    uint32_t pk[kSItems];
     auto classify_all = [&](auto full_tag, auto runs_tag) {
       constexpr bool FULL = decltype(full_tag)::value;
       constexpr bool RUNS = decltype(runs_tag)::value;
       [[maybe_unused]] const uint32_t pos0 = (uint32_t)((int64_t)base + posbase);
 #pragma unroll
-      for (int i = 0; i < kItems; ++i) {
-        const uint32_t e = w * (kItems * 32) + i * 32 + lane;
+      for (int i = 0; i < kSItems; ++i) {
+        const uint32_t e = w * (kSItems * 32) + i * 32 + lane;
         uint32_t b = kInvalid;
         if (FULL || e < tcount) {
           if constexpr (CLS == kClsIds) {
@@ -146,13 +152,13 @@ __global__ void __launch_bounds__(kThreads, (VALS ? 2 : 4) * kCtaDiv)
       auto rank_all = [&](auto nbits_tag) {
         constexpr int NB = decltype(nbits_tag)::value;
 #pragma unroll
-        for (int i = 0; i < kItems; ++i) {
+        for (int i = 0; i < kSItems; ++i) {
           const uint32_t b = pk[i];
           const uint32_t r = warp_stable_rank<NB>(b, lane, lt, whw, full);
           if (b != kInvalid) pk[i] = (b << 16) | r;
         }
       };
-      for (int turn = 0; turn < (MODE == kRankSerial ? kWarps : 1); ++turn) {
+      for (int turn = 0; turn < (MODE == kRankSerial ? kSWarps : 1); ++turn) {
         if (MODE == kRankWarp || w == turn) {
           if (nbits <= 7) rank_all(std::integral_constant<int, 7>{});
           else if (nbits <= 9) rank_all(std::integral_constant<int, 9>{});
@@ -162,7 +168,7 @@ __global__ void __launch_bounds__(kThreads, (VALS ? 2 : 4) * kCtaDiv)
       }
     }
     __syncthreads();
-    for (int b = threadIdx.x; b < nb_stride; b += kThreads) {
+    for (int b = threadIdx.x; b < nb_stride; b += kSThreads) {
       uint32_t acc = 0;
 #pragma unroll
       for (int ww = 0; ww < kHists; ++ww) {
@@ -173,20 +179,20 @@ __global__ void __launch_bounds__(kThreads, (VALS ? 2 : 4) * kCtaDiv)
       btot[b] = acc;
     }
     __syncthreads();
-    block_excl_scan<kThreads>(btot, nb_stride, s_scan);
+    block_excl_scan<kSThreads>(btot, nb_stride, s_scan);
     // Permute the staged tile bucket-major in place.
     {
-      uint64_t kr[kItems];
-      uint64_t vr[VALS ? kItems : 1];
+      uint64_t kr[kSItems];
+      uint64_t vr[VALS ? kSItems : 1];
 #pragma unroll
-      for (int i = 0; i < kItems; ++i) {
-        const uint32_t e = w * (kItems * 32) + i * 32 + lane;
+      for (int i = 0; i < kSItems; ++i) {
+        const uint32_t e = w * (kSItems * 32) + i * 32 + lane;
         kr[i] = keys_s[e];
         if constexpr (VALS) vr[i] = vals_s[e];
       }
       // Output base of every bucket run of this tile; advance the running offsets.
       if constexpr (kAdj) {
-        for (int b = threadIdx.x; b < nb_stride; b += kThreads) {
+        for (int b = threadIdx.x; b < nb_stride; b += kSThreads) {
           const uint32_t st = btot[b];
           const int64_t r = run[b];
           adj[b] = r - (int64_t)st;
@@ -195,7 +201,7 @@ __global__ void __launch_bounds__(kThreads, (VALS ? 2 : 4) * kCtaDiv)
       }
       __syncthreads();
 #pragma unroll
-      for (int i = 0; i < kItems; ++i) {
+      for (int i = 0; i < kSItems; ++i) {
         if (pk[i] != kInvalid) {
           const uint32_t b = pk[i] >> 16;
           // (one counter array: its scanned base is zero — no load)
@@ -207,7 +213,7 @@ __global__ void __launch_bounds__(kThreads, (VALS ? 2 : 4) * kCtaDiv)
       }
     }
     __syncthreads();
-    for (uint32_t j = threadIdx.x; j < tcount; j += kThreads) {
+    for (uint32_t j = threadIdx.x; j < tcount; j += kSThreads) {
       const uint32_t b = bkt_s[j];
       const int64_t d = (kAdj ? adj[b] : run[b] - (int64_t)btot[b]) + (int64_t)j;
       if constexpr (PEERS) {
@@ -220,7 +226,7 @@ __global__ void __launch_bounds__(kThreads, (VALS ? 2 : 4) * kCtaDiv)
     }
     __syncthreads();
     if constexpr (!kAdj) {
-      for (int b = threadIdx.x; b < nb_stride; b += kThreads)
+      for (int b = threadIdx.x; b < nb_stride; b += kSThreads)
         run[b] += (int64_t)((b + 1 < nb_stride ? btot[b + 1] : tcount) - btot[b]);
     }
   }
@@ -236,7 +242,7 @@ __global__ void __launch_bounds__(kThreads, (VALS ? 2 : 4) * kCtaDiv)
 // tile is permuted bucket-major in place and written as coalesced runs.
 
 template <int KIND, int CLS>
-__global__ void __launch_bounds__(kThreadsU, 2 * kCtaDiv)
+__global__ void __launch_bounds__(kThreadsU, 2)
     k_scatter_u(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst, SegMeta m,
                 const uint8_t* __restrict__ blobs, const DigitCls* __restrict__ dcls, int nspl_cap,
                 int nb, const uint32_t* __restrict__ chunk_tot,
@@ -391,7 +397,7 @@ size_t scatter_smem_bytes(int nb_stride, int nspl_cap, int cells_cap, bool digit
   const int mode = scatter_mode(nb_stride, stable);
   size_t b = (vals ? 16 : 8) * (size_t)kTile;                         // keys (+vals)
   b += 8 * (size_t)nb_stride;                                         // running offsets
-  b += 4 * (size_t)(mode == kRankWarp ? kWarps : 1) * nb_stride;      // bucket counters
+  b += 4 * (size_t)(mode == kRankWarp ? kSWarps : 1) * nb_stride;      // bucket counters
   b += 4 * (size_t)nb_stride;                                         // tile bucket starts
   if (mode != kRankSerial) b += 8 * (size_t)nb_stride;                // tile output bases
   b += 2 * (size_t)kTile;                                             // bucket ids
@@ -448,7 +454,7 @@ cudaError_t launch_scatter(cudaStream_t st, const void* src, const void* src_val
                                     : k_scatter<K, CL, V, kRankAtomic>;                       \
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
     if (e != cudaSuccess) return e;                                                           \
-    fn<<<(unsigned)nchunks, kThreads, smem, st>>>(s, sv, d, dv, m, blobs, dcls, nspl_cap,     \
+    fn<<<(unsigned)nchunks, kSThreads, smem, st>>>(s, sv, d, dv, m, blobs, dcls, nspl_cap,     \
                                                    nb_stride, chunk_tot, cell_base, ids,      \
                                                    nullptr, nullptr);                          \
   }
@@ -494,7 +500,7 @@ cudaError_t launch_scatter_peers(cudaStream_t st, const void* src, const void* s
     auto fn = k_scatter<K, CL, V, kRankWarp, true>;                                                 \
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);           \
     if (e != cudaSuccess) return e;                                                                 \
-    fn<<<(unsigned)nchunks, kThreads, smem, st>>>(s, sv, nullptr, nullptr, m, nullptr, nullptr, 0,  \
+    fn<<<(unsigned)nchunks, kSThreads, smem, st>>>(s, sv, nullptr, nullptr, m, nullptr, nullptr, 0,  \
                                                    nb_stride, chunk_tot, cell_base, ids, bucket_dst, \
                                                    bucket_vdst);                                    \
   }
