@@ -21,7 +21,7 @@ static_assert(kItems * kThreads == kTile, "tile geometry");
 // Tree classifier blob (one per group) in global memory: header, sorted
 // splitter keys and positions, and a key-range LUT whose cells hold
 // (first splitter index | splitter count << 16).
-constexpr int kLutExtraBits = 6;  // LUT cells per splitter = 2^6
+constexpr int kLutExtraBits = 6;  // LUT cells per splitter = 2^6 (2^5: 1.129 -> 1.161 ms for config 2's histograms)
 constexpr int kMaxSpl = AMS_MAX_BUCKETS;  // room for nb-1 <= 4095 splitters
 constexpr int kMaxLutBits = 13;
 constexpr int kMaxCells = 1 << kMaxLutBits;
@@ -312,7 +312,7 @@ constexpr int kWarpsU = kThreadsU / 32;
 // Sub-buckets of the cell sort: two per key of cell capacity.
 constexpr int kCellSubBuckets = 2 * AMS_SMEM_SORT_CAP;
 // ... and of the fixed-capacity cells (their refined digit, k_bucket_ranges).
-constexpr int kFxSubBuckets = 2 * AMS_FX_CAP;
+constexpr int kFxSubBuckets = 2 * AMS_FX_CAP;  // (one per key of capacity: 1.345 -> 1.467 ms)
 
 __device__ __forceinline__ int upper_bound_u64(const uint64_t* a, int n, uint64_t x) {
   int lo = 0, hi = n;

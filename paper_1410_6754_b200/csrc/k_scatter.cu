@@ -94,6 +94,7 @@ __global__ void __launch_bounds__(kSThreads, VALS ? kSCtas / 2 : kSCtas)
   for (uint64_t t0 = first; t0 < last; t0 += kTile) {
     const uint32_t tcount = (uint32_t)min((uint64_t)kTile, last - t0);
     const uint64_t base = seg_off + t0;
+    // (16-byte copies, two keys each, measured worse here: 1.475 -> 1.503 ms)
     for (uint32_t j = threadIdx.x; j < tcount; j += kSThreads) {
       cp_async8(keys_s + j, src + base + j);
       if constexpr (VALS) cp_async8(vals_s + j, src_vals + base + j);
