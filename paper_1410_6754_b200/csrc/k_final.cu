@@ -10,17 +10,10 @@
 namespace ams {
 
 namespace {
-// Fixed-capacity digit partition (keys only, the final sort of a bucket-major
-// last level): segments are the last level's buckets, each split into nb_s
-// digit cells of capacity kSortCap in `dst` (cell ci at dst[ci * kSortCap]).
-// No histogram pass: every (tile, digit) run reserves its room with one
-// global atomic on the cell's fill counter, so a cell's keys land in any
-// order (only membership matters: F7).  A cell that would exceed its
-// capacity flags its segment; the host re-partitions such segments exactly
-// from `src`, which this kernel does not modify.
 // Geometry of the fixed-capacity partition: 2048-key tiles, 256 threads, 4
 // CTAs per SM (4096-key tiles on 512 threads at 2 CTAs per SM: 1.202 ->
-// 1.154 ms at config 2 — fewer warps per barrier, more CTAs to interleave).
+// 1.154 ms at config 2 — fewer warps per barrier, more CTAs to interleave;
+// 1024-key tiles: 1.36 ms, profiles/r02t_ab_fixed_tile.txt).
 constexpr int kFTile = 2048;
 constexpr int kFItems = 8;
 constexpr int kFThreads = kFTile / kFItems;
@@ -28,6 +21,14 @@ constexpr int kFWarps = kFThreads / 32;
 constexpr int kFCtas = 2 * 4096 / kFTile;
 static_assert(kTile % kFTile == 0, "chunks are whole tiles of both kinds");
 
+// Fixed-capacity digit partition (keys only, the final sort of a bucket-major
+// last level): segments are the last level's buckets, each split into nb_s
+// digit cells of capacity AMS_FX_CAP in `dst` (cell ci at dst[ci * AMS_FX_CAP]).
+// No histogram pass: every (tile, digit) run reserves its room with one
+// global atomic on the cell's fill counter, so a cell's keys land in any
+// order (only membership matters: F7).  A cell that would exceed its
+// capacity flags its segment; the host re-partitions such segments exactly
+// from `src`, which this kernel does not modify.
 template <int KIND>
 __global__ void __launch_bounds__(kFThreads, kFCtas)
     k_scatter_fixed(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst, SegMeta m,

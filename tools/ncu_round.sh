@@ -10,7 +10,7 @@ timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
   --log-file $out/launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline \
   > $out/ncu_launches.log 2>&1 || echo "launch list failed"
 timeout 900 ncu --set full --clock-control none --import-source on \
-  -k regex:"${KREGEX:-k_hist|k_scatter|k_smem_sort|k_cell_sort}" --launch-skip ${KSKIP:-8} --launch-count ${KCOUNT:-8} \
+  -k regex:"${KREGEX:-k_hist|k_scatter|k_cell_sort}" --launch-skip ${KSKIP:-8} --launch-count ${KCOUNT:-8} \
   -o $out/full -f python tools/profile_case.py $log2n 2 > $out/ncu_full.log 2>&1 || echo "full failed"
 ncu -i $out/full.ncu-rep --page raw --csv > $out/full_raw.csv 2>/dev/null || true
 ls -la $out
