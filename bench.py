@@ -710,7 +710,7 @@ def ours_arm_multi(args, w, world, rank, local):
                    "groups": list(w["groups"]), "eps": w["eps"], "a": w["a"], "b": 16,
                    "scheme": "simple", "sample_mode": "parity (reference seeded streams)",
                    "l2": "inputs (8 B x n) larger than the 126 MB L2 between steps",
-                   "parallelism": f"{p} PEs on {world} GPUs, level 1 over NCCL P2P"},
+                   "parallelism": f"{p} PEs on {world} GPUs, level 1 stored into the owner GPUs over peer pointers (NVLink), later levels GPU-local"},
         "verified": {"sorted_and_checksum": ok_sorted, "pe_size_bound": ok_bound},
         "gpu_launches": launches, "roofline": roofline, "clocks": clk, "e2e": e2e,
         "cpu_baseline": cpu,
