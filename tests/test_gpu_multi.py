@@ -139,3 +139,47 @@ def test_mg_rejects_bad_shapes():
                     scheme="deterministic")
     finally:
         mg.close()
+
+
+@pytest.mark.parametrize("G", [2, 4])
+@pytest.mark.parametrize("scheme", ["simple", "deterministic"])
+def test_mg_ragged_and_empty_contexts(G, scheme):
+    """Ragged PE sizes, PEs without keys, and a whole context without input
+    (it still receives its groups' keys)."""
+    from paper_1410_6754_b200 import AmsParams, SeedSpec
+    from paper_1410_6754_b200.multi import MultiDeviceSorter
+    groups, p = (4, 4), 16
+    rng = np.random.default_rng(G * 3 + len(scheme))
+    sizes = [int(x) for x in rng.integers(0, 3000, p)]
+    sizes[1] = 0
+    for j in range(p // G):          # the first context holds nothing
+        sizes[j] = 0
+    n = sum(sizes)
+    keys = rng.integers(0, 1 << 40, n, dtype=np.uint64)
+    ref = O.ams_sort(keys, sizes, groups, None, 16, 0.3, 5, "algo/rep0", scheme=scheme)
+    pl = p // G
+    offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    ks = [torch.from_numpy(keys[offs[i * pl]:offs[(i + 1) * pl]].view(np.int64).copy()).cuda() for i in range(G)]
+    mg = MultiDeviceSorter([0] * G)
+    try:
+        ok, _, sz, reports, l1 = mg.sort(ks, sizes, AmsParams(groups, None, 16, 0.3), SeedSpec(5, "algo/rep0"),
+                                         scheme=scheme, key_kind="u64")
+    finally:
+        mg.close()
+    out = np.concatenate([t.cpu().numpy().view(np.uint64) for t in ok])
+    assert np.array_equal(out, ref.keys)
+    assert [int(x) for x in sz] == list(ref.pe_sizes)
+    assert [int(x) for x in l1["boundaries"]] == list(ref.levels[0][0].plan.boundaries)
+
+
+def test_mg_empty_input():
+    from paper_1410_6754_b200 import AmsParams, SeedSpec
+    from paper_1410_6754_b200.multi import MultiDeviceSorter
+    mg = MultiDeviceSorter([0, 0])
+    try:
+        ks = [torch.zeros(0, dtype=torch.int64, device="cuda") for _ in range(2)]
+        ok, _, sz, reports, _ = mg.sort(ks, [0] * 8, AmsParams((4, 2), None, 16, 0.1), SeedSpec(1, "x"),
+                                        key_kind="u64")
+    finally:
+        mg.close()
+    assert all(t.numel() == 0 for t in ok) and [int(x) for x in sz] == [0] * 8

@@ -120,3 +120,23 @@ def test_rlm_large_balanced():
     assert set(int(x) for x in res.pe_sizes) == {n // p}
     o = res.origin.cpu().numpy()
     assert np.array_equal(keys[o], np.sort(keys))
+
+
+def test_rlm_payloads_and_ragged_sizes():
+    """Payloads follow their keys; PEs of very different sizes (and empty
+    ones) still end perfectly balanced (rlm.py:1-9)."""
+    from oracle import rlm_oracle as R
+    rng = np.random.default_rng(9)
+    p = 16
+    sizes = [0, 5000, 1, 0, 12000, 300, 300, 0, 7000, 2, 2, 2, 9000, 0, 0, 4096]
+    n = sum(sizes)
+    keys = rng.integers(0, 50, n, dtype=np.uint64)          # heavy duplicates: ties by origin
+    vals = rng.integers(0, 2**62, n, dtype=np.int64)
+    for scheme in ("simple", "randomized"):
+        ref = R.rlm_sort(keys, sizes, (4, 4), scheme, 2, "r", vals=vals)
+        res = run_gpu(keys, sizes, (4, 4), scheme, 2, "r", vals=vals)
+        assert np.array_equal(res.keys.cpu().numpy().view(np.uint64), ref.keys)
+        assert np.array_equal(res.origin.cpu().numpy(), ref.origin)
+        assert np.array_equal(res.vals.cpu().numpy(), ref.vals)
+        assert [int(x) for x in res.pe_sizes] == list(ref.pe_sizes)
+        assert max(res.pe_sizes) - min(res.pe_sizes) <= 2
