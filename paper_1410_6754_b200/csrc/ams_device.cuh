@@ -248,6 +248,21 @@ __device__ __forceinline__ uint32_t scan_warp_totals(uint32_t* scratch) {
   return scratch[NW];
 }
 
+// The same with ONE barrier: every warp's last lane has stored its inclusive
+// total in scratch[w]; returns the sum of the totals of the warps below this
+// one (a few broadcast loads instead of a second barrier).  scratch must not
+// be rewritten before every thread has passed a later barrier.
+template <int NT>
+__device__ __forceinline__ uint32_t warp_base_direct(const uint32_t* scratch) {
+  constexpr int NW = NT / 32;
+  const int w = threadIdx.x >> 5;
+  __syncthreads();
+  uint32_t s = 0;
+#pragma unroll
+  for (int ww = 0; ww < NW; ++ww) s += ww < w ? scratch[ww] : 0u;
+  return s;
+}
+
 // VAL(i) = value of entry i (u32 array or packed u16 pairs).
 template <int NT>
 __device__ inline uint32_t block_excl_scan(uint32_t* a, int n, uint32_t* scratch) {
