@@ -390,3 +390,29 @@ def test_host_pipeline_batches(api):
         ref = O.ams_sort(b, [npe] * p, (8, 8), None, 16, 0.1, 1, "algo/rep0")
         assert [int(x) for x in sz] == list(ref.pe_sizes)
 
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("ndistinct", [1 << 14, 1 << 18])
+def test_many_fallback_cells_keys_only(api, ndistinct):
+    """Keys-only fast path with thousands of clustered cells (a few key
+    values per cell, each repeated well above the cell sort's fix-up bound):
+    the LSD fallback list is far longer than its speculative launch, so the
+    deferred remainder launch runs too.  Output == numpy.sort."""
+    from paper_1410_6754_b200 import AmsParams, SeedSpec
+    from paper_1410_6754_b200.api import get_sorter
+    n, p = 1 << 24, 64
+    rng = np.random.default_rng(ndistinct)
+    values = rng.integers(0, 2**64, ndistinct, dtype=np.uint64)
+    keys = values[rng.integers(0, ndistinct, n)]
+    d_keys = torch.from_numpy(keys.view(np.int64)).cuda()
+    sorter = get_sorter(0)
+    before = sorter.ctx.final_sort_stats()
+    res = api.ams_sort_tensors(d_keys, [n // p] * p, AmsParams((8, 8), None, 16, 0.1), SeedSpec(3, "f"),
+                               key_kind="u64")
+    torch.cuda.synchronize()
+    after = sorter.ctx.final_sort_stats()
+    assert np.array_equal(res.keys.cpu().numpy().view(np.uint64), np.sort(keys))
+    if ndistinct == 1 << 14:
+        assert after["fallback_cells"] - before["fallback_cells"] > 256, \
+            "expected more fallback cells than the speculative launch"
