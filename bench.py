@@ -415,7 +415,10 @@ def ours_arm(args, w):
                "host_cpus": os.cpu_count()}
     sweeps = None
     if args.sweeps and args.workload == "cfg2":
-        sweeps = {"cfg5": cfg5_sweep(torch, sorter, peak), "cfg1": small_point(torch, sorter, peak)}
+        sweeps = {"cfg5": cfg5_sweep(torch, sorter, peak), "cfg1": small_point(torch, sorter, peak),
+                  # the same shapes without the host draw (not the headline: parity mode is)
+                  "cfg5_device_sampling": cfg5_sweep(torch, sorter, peak, "device"),
+                  "cfg1_device_sampling": small_point(torch, sorter, peak, "device")}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -457,7 +460,7 @@ def _time_steps(torch, fn, steps: int, warmup: int) -> float:
     return e0.elapsed_time(e1) / steps
 
 
-def cfg5_sweep(torch, sorter, peak):
+def cfg5_sweep(torch, sorter, peak, sample_mode="parity"):
     """BASELINE config 5 on this GPU (weak scaling: n = n/GPU at N=1): uint64
     keys + uint64 payload (origin index), uniform default_rng(3), p=256,
     k=1 (256,) and k=2 (8,32), n/GPU = 2^10..2^24; keys/s and the fraction of
@@ -479,7 +482,8 @@ def cfg5_sweep(torch, sorter, peak):
 
             def fn():
                 return sorter.sort(keys, [n // 256] * 256, params, seed, vals=vals, out=ok_,
-                                   out_vals=ov_, key_kind="u64", with_stats=False)
+                                   out_vals=ov_, key_kind="u64", with_stats=False,
+                                   sample_mode=sample_mode)
             steps = 20 if lg <= 20 else 10
             ms = _time_steps(torch, fn, steps, 3)
             flip = -(2**63)
@@ -489,10 +493,16 @@ def cfg5_sweep(torch, sorter, peak):
             pts.append({"n_per_gpu": n, "ms_per_step": ms, "keys_per_s": n / (ms / 1e3),
                         "t_roof_ms": t_roof, "frac": t_roof / ms, "verified": ok})
         out[f"k{k}"] = pts
-    return {"desc": "config 5 KV sweep, one GPU (n = n/GPU), p=256, w=16 B, CUDA events", **out}
+    return {"desc": "config 5 KV sweep, one GPU (n = n/GPU), p=256, w=16 B, CUDA events; sample "
+                    f"positions: {SAMPLE_DESC[sample_mode]}", **out}
 
 
-def small_point(torch, sorter, peak):
+SAMPLE_DESC = {"parity": "the reference's seeded streams (host draw; boundaries equal the reference's)",
+               "device": "stratified positions drawn on the GPU (sample_mode='device', SURVEY K9: no host "
+                         "draw; boundaries differ from the reference's, output and bound do not)"}
+
+
+def small_point(torch, sorter, peak, sample_mode="parity"):
     """BASELINE config 1 on the GPU (n=2^20 from the reference's own
     generate_input(seed 0), p=16, (16,), a=16): latency-bound."""
     from paper_1410_6754_b200 import AmsParams, SeedSpec
@@ -505,11 +515,12 @@ def small_point(torch, sorter, peak):
 
     def fn():
         return sorter.sort(keys, [1 << 16] * 16, params, seed, out=out, key_kind="u64",
-                           with_stats=False)
+                           with_stats=False, sample_mode=sample_mode)
     ms = _time_steps(torch, fn, 50, 5)
     ok = bool(np.array_equal(out.cpu().numpy().view(np.uint64), np.sort(keys_h)))
     t_roof = 2 * 8 * (1 << 20) * 2 / (peak * 1e9) * 1e3
-    return {"desc": w["desc"], "ms_per_step": ms, "keys_per_s": (1 << 20) / (ms / 1e3),
+    return {"desc": w["desc"] + "; sample positions: " + SAMPLE_DESC[sample_mode], "ms_per_step": ms,
+            "keys_per_s": (1 << 20) / (ms / 1e3),
             "t_roof_ms": t_roof, "frac": t_roof / ms, "verified": ok}
 
 

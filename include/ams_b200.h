@@ -281,6 +281,8 @@ int ams_map_keys(ams_ctx_t* ctx, const void* src, void* dst, uint64_t n, int fro
 #define AMS_SCHEME_DETERMINISTIC 1
 #define AMS_SCHEME_PERMUTED 2
 #define AMS_SCHEME_RANDOMIZED 3
+#define AMS_SAMPLE_PARITY 0
+#define AMS_SAMPLE_DEVICE 1
 
 typedef struct {
   int levels;                          /* k = len(group_counts) */
@@ -310,6 +312,14 @@ typedef struct {
   int level_base;
   int init_groups;                     /* 0 or 1: one group */
   int pe_base;
+  /* AMS_SAMPLE_PARITY (0): sample positions from the reference's seeded
+   * streams (CPython MT19937 restated on the host, ams.py:157-175): bucket
+   * boundaries equal the reference's.  AMS_SAMPLE_DEVICE (1): the same
+   * quota split (ams.py:166-171) with stratified positions drawn on the
+   * device (distinct by construction, every element of a PE equally
+   * likely) — no host draw; boundaries differ from the reference's, the
+   * output and the (1 + eps) bound do not.  Not with record_holders. */
+  int sample_mode;
 } ams_params_t;
 
 /* One level's report (ams.py:294-308; exchange maxima simnet.py:109-124). */

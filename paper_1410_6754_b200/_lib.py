@@ -103,7 +103,7 @@ class ParamsT(C.Structure):
                 ("imbalance", C.c_double), ("master_seed", C.c_int64),
                 ("stream_id", C.c_char_p), ("key_kind", C.c_int), ("with_stats", C.c_int),
                 ("scheme", C.c_int), ("record_holders", C.c_int), ("level_base", C.c_int),
-                ("init_groups", C.c_int), ("pe_base", C.c_int)]
+                ("init_groups", C.c_int), ("pe_base", C.c_int), ("sample_mode", C.c_int)]
 
 
 class LevelReportT(C.Structure):

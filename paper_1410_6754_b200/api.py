@@ -46,14 +46,20 @@ def _check_scheme(scheme: str):
 
 def ams_sort_tensors(keys: torch.Tensor, pe_sizes, params, seed, vals: torch.Tensor | None = None,
                      scheme: str = "simple", key_kind=None, out=None, out_vals=None,
-                     record_splitters: bool = False, record_holders: bool = False) -> SortOutput:
+                     record_splitters: bool = False, record_holders: bool = False,
+                     sample_mode: str = "parity") -> SortOutput:
     """Sort device keys laid out PE-major (``pe_sizes``); returns a
-    :class:`~paper_1410_6754_b200.engine.SortOutput`."""
+    :class:`~paper_1410_6754_b200.engine.SortOutput`.  ``sample_mode``:
+    "parity" draws the sample positions from the reference's seeded streams
+    (bucket boundaries equal the reference's); "device" draws stratified
+    positions on the GPU (same quota split, ams.py:166-171; no host draw —
+    the output and the (1 + eps) bound are unchanged, the boundaries are not
+    the reference's)."""
     _check_scheme(scheme)
     return get_sorter(keys.device).sort(keys, pe_sizes, params, seed, vals=vals, out=out,
                                         out_vals=out_vals, key_kind=key_kind,
                                         record_splitters=record_splitters, scheme=scheme,
-                                        record_holders=record_holders)
+                                        record_holders=record_holders, sample_mode=sample_mode)
 
 
 def ams_sort_host(keys: np.ndarray, pe_sizes, params, seed, vals: np.ndarray | None = None,

@@ -1293,6 +1293,10 @@ int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* p
   if (n && (!keys || !out)) return set_error(AMS_EINVAL, "null key buffer");
   if (prm->scheme < AMS_SCHEME_SIMPLE || prm->scheme > AMS_SCHEME_RANDOMIZED)
     return set_error(AMS_EINVAL, "unknown delivery scheme");
+  if (prm->sample_mode != AMS_SAMPLE_PARITY && prm->sample_mode != AMS_SAMPLE_DEVICE)
+    return set_error(AMS_EINVAL, "unknown sample mode");
+  if (prm->sample_mode == AMS_SAMPLE_DEVICE && prm->record_holders)
+    return set_error(AMS_EINVAL, "splitter holders need the parity sample mode");
   // A continuation under a non-simple scheme takes the input's origin tags
   // as `vals` (not user payloads).
   const bool tags_in = lv0 > 0 && prm->scheme != AMS_SCHEME_SIMPLE && n > 0;
@@ -1357,23 +1361,50 @@ int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* p
       const uint64_t x = br[g];
       targets[g] = std::min<uint64_t>(n_g, std::max<uint64_t>(x - 1, (uint64_t)std::ceil(a * (double)x)));
     }
+    const bool dev_sample = prm->sample_mode == AMS_SAMPLE_DEVICE;
     uint64_t cap = 0;
     for (uint64_t t : targets) cap += t;
     std::vector<uint64_t> idx(std::max<uint64_t>(cap, 1)), gpos(std::max<uint64_t>(cap, 1)), drawn(G);
-    if (pe_base == 0) {
-      rc = ams_draw_sample_positions(prm->master_seed, prm->stream_id, lv, G, gf.data(), gn.data(),
-                                     targets.data(), sizes.data(), offs.data(), cap, idx.data(),
-                                     gpos.data(), drawn.data());
+    // Fast mode: only the quota split on the host (ams.py:166-171); the
+    // positions are drawn by the gather kernel.
+    std::vector<uint64_t> smp_off, mem_gpos;
+    if (dev_sample) {
+      smp_off.assign((size_t)p + 1, 0);
+      mem_gpos.assign(p, 0);
+      uint64_t w = 0;
+      for (int g = 0; g < G; ++g) {
+        const int first = gf[g], P = gn[g];
+        const uint64_t base = targets[g] / P, extra = targets[g] % P;
+        uint64_t gp = 0, dr = 0;
+        for (int i = 0; i < P; ++i) {
+          const uint64_t take = std::min<uint64_t>(base + ((uint64_t)i < extra ? 1 : 0), sizes[first + i]);
+          smp_off[first + i] = w;
+          mem_gpos[first + i] = gp;
+          w += take;
+          dr += take;
+          gp += sizes[first + i];
+        }
+        drawn[g] = dr;
+      }
+      smp_off[p] = w;
+      rc = AMS_OK;
     } else {
-      // The streams are named by global PE ids (ams.py:168-174): shifted tables.
-      std::vector<uint64_t> gsz((size_t)pe_base + p, 0), gof((size_t)pe_base + p, 0);
-      std::copy(sizes.begin(), sizes.end(), gsz.begin() + pe_base);
-      std::copy(offs.begin(), offs.begin() + p, gof.begin() + pe_base);
-      std::vector<int32_t> gfn(gf);
-      for (int32_t& f : gfn) f += pe_base;
-      rc = ams_draw_sample_positions(prm->master_seed, prm->stream_id, lv, G, gfn.data(), gn.data(),
-                                     targets.data(), gsz.data(), gof.data(), cap, idx.data(),
-                                     gpos.data(), drawn.data());
+      if (pe_base == 0) {
+        rc = ams_draw_sample_positions(prm->master_seed, prm->stream_id, lv, G, gf.data(), gn.data(),
+                                       targets.data(), sizes.data(), offs.data(), cap, idx.data(),
+                                       gpos.data(), drawn.data());
+      } else {
+        // The streams are named by global PE ids (ams.py:168-174): shifted tables.
+        std::vector<uint64_t> gsz((size_t)pe_base + p, 0), gof((size_t)pe_base + p, 0);
+        std::copy(sizes.begin(), sizes.end(), gsz.begin() + pe_base);
+        std::copy(offs.begin(), offs.begin() + p, gof.begin() + pe_base);
+        std::vector<int32_t> gfn(gf);
+        for (int32_t& f : gfn) f += pe_base;
+        rc = ams_draw_sample_positions(prm->master_seed, prm->stream_id, lv, G, gfn.data(), gn.data(),
+                                       targets.data(), gsz.data(), gof.data(), cap, idx.data(),
+                                       gpos.data(), drawn.data());
+      }
+      if (rc) return rc;
     }
     if (rc) return rc;
     tr.mark("draw");
@@ -1394,9 +1425,30 @@ int ams_sort_run(ams_ctx_t* c, const ams_params_t* prm, int p, const uint64_t* p
     const uint64_t* tie_tags = det && lv > 0 ? static_cast<const uint64_t*>(src_v) : nullptr;
     // (lv counts from the whole sort's first level: a continuation's input
     // already went through a non-simple delivery.)
-    if ((rc = level_sample_impl(c, src, src_kind, S, idx.data(), gpos.data(), c->s_keys.as<uint64_t>(),
-                                c->s_pos.as<uint32_t>(), tie_tags)))
+    if (dev_sample) {
+      if (S) {
+        Stage& st = c->st_sample;
+        st.reset();
+        const size_t o_so = st.put(smp_off), o_mo = st.put(offs.data(), (size_t)p), o_ml = st.put(sizes),
+                     o_mg = st.put(mem_gpos);
+        AMS_CK(st.upload(c->stream));
+        // one stream per (seed, stream id, level): blake2b of its name
+        const std::string name = std::to_string(prm->master_seed) + "\x1f" + prm->stream_id + "/L" +
+                                 std::to_string(lv) + "/device-sample";
+        uint8_t dg[16];
+        blake2b_128(reinterpret_cast<const uint8_t*>(name.data()), name.size(), dg);
+        uint64_t seed64;
+        std::memcpy(&seed64, dg, 8);
+        KTimer kt(c, AMS_KCAT_SAMPLE, 12.0 * S);
+        AMS_CK(launch_draw_gather(c->stream, src, src_kind, st.dev<uint64_t>(o_so), st.dev<uint64_t>(o_mo),
+                                  st.dev<uint64_t>(o_ml), st.dev<uint64_t>(o_mg), p, S, seed64,
+                                  c->s_keys.as<uint64_t>(), c->s_pos.as<uint32_t>(), tie_tags));
+        c->launches += 1;
+      }
+    } else if ((rc = level_sample_impl(c, src, src_kind, S, idx.data(), gpos.data(),
+                                       c->s_keys.as<uint64_t>(), c->s_pos.as<uint32_t>(), tie_tags))) {
       return rc;
+    }
     if ((rc = ams_level_splitters(c, G, c->s_keys.as<uint64_t>(), c->s_pos.as<uint32_t>(),
                                   soff.data(), nb.data())))
       return rc;

@@ -22,6 +22,37 @@ __global__ void k_gather_sample(const uint64_t* __restrict__ src, const uint64_t
   out_pos[i] = tags ? (uint32_t)tags[idx[i]] : (uint32_t)gpos[i];
 }
 
+// Fast-mode sample: member m contributes take[m] elements
+// (draw_sample's quota split, ams.py:166-171); element i of a member comes
+// from stratum [i * size / take, (i + 1) * size / take) at a hashed offset,
+// so positions are distinct and ascending and every element of the member
+// is equally likely.  One thread per sample element; sample_off[m] = first
+// output slot of member m (ascending; sample_off[nmem] = total).
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ULL;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
+  return x ^ (x >> 31);
+}
+template <int KIND>
+__global__ void k_draw_gather(const uint64_t* __restrict__ src, const uint64_t* __restrict__ sample_off,
+                              const uint64_t* __restrict__ mem_off, const uint64_t* __restrict__ mem_len,
+                              const uint64_t* __restrict__ mem_gpos, int nmem, uint64_t seed,
+                              uint64_t* __restrict__ out_keys, uint32_t* __restrict__ out_pos,
+                              const uint64_t* __restrict__ tags) {
+  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= sample_off[nmem]) return;
+  const int m = upper_bound_u64(sample_off, nmem + 1, t) - 1;
+  const uint64_t i = t - sample_off[m], take = sample_off[m + 1] - sample_off[m], size = mem_len[m];
+  // strata by 128-bit products: size < 2^32 and take <= size
+  const uint64_t lo = (uint64_t)(((unsigned __int128)i * size) / take);
+  const uint64_t hi = (uint64_t)(((unsigned __int128)(i + 1) * size) / take);
+  const uint64_t pos = lo + splitmix64(seed ^ splitmix64(((uint64_t)m << 40) ^ i)) % (hi - lo);
+  const uint64_t idx = mem_off[m] + pos;
+  out_keys[t] = to_ordered<KIND>(src[idx]);
+  out_pos[t] = tags ? (uint32_t)tags[idx] : (uint32_t)(mem_gpos[m] + pos);
+}
+
 // Deterministic delivery relayout: work item w copies up to kCopyItem keys
 // of one range (ranges pre-split on the host).
 constexpr uint64_t kCopyItem = 8192;
@@ -560,6 +591,18 @@ __global__ void k_map_keys(const uint64_t* __restrict__ src, uint64_t* __restric
 }
 
 }  // namespace
+
+cudaError_t launch_draw_gather(cudaStream_t st, const void* src, int kind, const uint64_t* sample_off,
+                               const uint64_t* mem_off, const uint64_t* mem_len, const uint64_t* mem_gpos,
+                               int nmem, uint64_t total, uint64_t seed, uint64_t* out_keys,
+                               uint32_t* out_pos, const uint64_t* tags) {
+  if (total == 0 || nmem == 0) return cudaSuccess;
+  const unsigned blocks = (unsigned)((total + 255) / 256);
+  AMS_KIND_DISPATCH(kind, K, k_draw_gather<K><<<blocks, 256, 0, st>>>(
+      static_cast<const uint64_t*>(src), sample_off, mem_off, mem_len, mem_gpos, nmem, seed, out_keys,
+      out_pos, tags));
+  return cudaGetLastError();
+}
 
 cudaError_t launch_gather_sample(cudaStream_t st, const void* src, int kind, const uint64_t* idx,
                                  const uint64_t* gpos, uint64_t n, uint64_t* out_keys,

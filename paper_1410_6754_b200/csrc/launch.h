@@ -54,6 +54,11 @@ struct CellSource {
 cudaError_t launch_gather_sample(cudaStream_t st, const void* src, int kind, const uint64_t* idx,
                                  const uint64_t* gpos, uint64_t n, uint64_t* out_keys,
                                  uint32_t* out_pos, const uint64_t* tags);
+// Fast-mode sample drawn and gathered on the device (k_draw_gather).
+cudaError_t launch_draw_gather(cudaStream_t st, const void* src, int kind, const uint64_t* sample_off,
+                               const uint64_t* mem_off, const uint64_t* mem_len, const uint64_t* mem_gpos,
+                               int nmem, uint64_t total, uint64_t seed, uint64_t* out_keys,
+                               uint32_t* out_pos, const uint64_t* tags);
 // Copy ranges {src, dst, len} of keys (and values) — the deterministic
 // delivery's relayout.
 cudaError_t launch_copy_ranges(cudaStream_t st, const uint64_t* ranges, int nranges, const void* src,

@@ -54,6 +54,10 @@ def key_kind_of(t: torch.Tensor, key_kind=None) -> int:
 
 # Delivery schemes (delivery.py:439-455 SCHEMES) the device path implements.
 SCHEMES = {"simple": 0, "deterministic": 1, "permuted": 2, "randomized": 3}  # AMS_SCHEME_*
+# Where sample positions come from: the reference's seeded streams (bucket
+# boundaries equal the reference's) or stratified positions drawn on the
+# device (no host draw; same quota split, different boundaries).
+SAMPLE_MODES = {"parity": 0, "device": 1}  # AMS_SAMPLE_*
 
 
 @dataclass
@@ -168,7 +172,7 @@ def run_records(ctx, run: int, group_counts, eps_l: float, first_level: int = 0,
 
 
 def native_params(params, master, stream_id, kind, with_stats=True, scheme=0, record_holders=False,
-                  oversampling=None, level_base=0, init_groups=0, pe_base=0):
+                  oversampling=None, level_base=0, init_groups=0, pe_base=0, sample_mode=0):
     """ams_params_t for ams_sort_run (include/ams_b200.h)."""
     prm = L.ParamsT()
     gc = tuple(params.group_counts)
@@ -190,6 +194,7 @@ def native_params(params, master, stream_id, kind, with_stats=True, scheme=0, re
     prm.level_base = int(level_base)
     prm.init_groups = int(init_groups)
     prm.pe_base = int(pe_base)
+    prm.sample_mode = int(sample_mode)
     return prm
 
 
@@ -223,7 +228,7 @@ class AmsSorter:
     def sort(self, keys: torch.Tensor, pe_sizes, params: AmsParams, seed, vals=None, out=None,
              out_vals=None, key_kind=None, record_splitters: bool = False,
              with_stats: bool = True, scheme: str = "simple",
-             record_holders: bool = False) -> SortOutput:
+             record_holders: bool = False, sample_mode: str = "parity") -> SortOutput:
         """Sort ``keys`` (1-D, PE-major: PE i owns the next ``pe_sizes[i]``
         keys) exactly as ams_sort(scheme) orders them (every scheme of the
         reference's SCHEMES registry; the per-level host driver,
@@ -232,6 +237,10 @@ class AmsSorter:
         records."""
         if scheme not in SCHEMES:
             raise ValueError(f"unknown delivery scheme {scheme!r}; supported: {tuple(SCHEMES)}")
+        if sample_mode not in SAMPLE_MODES:
+            raise ValueError(f"unknown sample mode {sample_mode!r}; supported: {tuple(SAMPLE_MODES)}")
+        if sample_mode != "parity" and (record_splitters or record_holders):
+            raise ValueError("splitter records need sample_mode='parity'")
         if record_splitters and scheme != "simple":
             raise ValueError("record_splitters runs the per-level host driver, which implements "
                              "the simple scheme only")
@@ -276,7 +285,7 @@ class AmsSorter:
             # The whole level loop in C++ (ams_sort_run); same steps as below.
             return self._sort_native(keys, vals, ret_out, ret_vals, out, out_vals, sizes, params,
                                      master, stream_id, kind, with_stats, launches0, n,
-                                     SCHEMES[scheme], record_holders)
+                                     SCHEMES[scheme], record_holders, SAMPLE_MODES[sample_mode])
         a = params.oversampling_for(n)                               # ams.py:278-280
         eps_l = params.per_level_imbalance()
         b = params.overpartition
@@ -344,9 +353,11 @@ class AmsSorter:
         return SortOutput(ret_out, ret_vals, sizes, levels, self.ctx.launches - launches0)
 
     def _sort_native(self, keys, vals, ret_out, ret_vals, out, out_vals, sizes, params, master,
-                     stream_id, kind, with_stats, launches0, n, scheme=0, record_holders=False):
+                     stream_id, kind, with_stats, launches0, n, scheme=0, record_holders=False,
+                     sample_mode=0):
         gc = tuple(params.group_counts)
-        prm = native_params(params, master, stream_id, kind, with_stats, scheme, record_holders)
+        prm = native_params(params, master, stream_id, kind, with_stats, scheme, record_holders,
+                            sample_mode=sample_mode)
         final_sizes, _ = self.ctx.sort_run(prm, sizes, keys if n else None,
                                            vals if n else None, out if n else None,
                                            out_vals if n else None)

@@ -416,3 +416,47 @@ def test_many_fallback_cells_keys_only(api, ndistinct):
     if ndistinct == 1 << 14:
         assert after["fallback_cells"] - before["fallback_cells"] > 256, \
             "expected more fallback cells than the speculative launch"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("groups,npe,dist,with_vals", [
+    ((8, 8), 4096, "uniform", False), ((8, 8), 4096, "uniform", True), ((4, 4), 3000, "zipf", True),
+    ((16,), 65536, "uniform", False), ((2, 2, 4), 700, "sorted", False), ((256,), 64, "uniform", True),
+    ((4, 2), 5, "uniform", False),
+])
+def test_device_sample_mode(api, groups, npe, dist, with_vals):
+    """sample_mode="device": stratified positions drawn on the
+    GPU with the reference's quota split.  Bucket boundaries differ from the
+    reference's, everything else holds: output == numpy.sort, payloads ==
+    stable argsort, sample sizes as draw_sample's, the per-level load budget
+    (ams.py:258) and determinism per seed."""
+    from paper_1410_6754_b200 import AmsParams, SeedSpec
+    p = int(np.prod(groups))
+    n = p * npe
+    rng = np.random.default_rng(p + npe)
+    keys = {"uniform": lambda: rng.integers(0, 2**64, n, dtype=np.uint64),
+            "zipf": lambda: O.zipf_keys(n, 11), "sorted": lambda: np.arange(n, dtype=np.uint64)}[dist]()
+    d_keys = dev_u64(keys)
+    d_vals = torch.arange(n, dtype=torch.int64, device="cuda") if with_vals else None
+    prm = AmsParams(tuple(groups), None, 16, 0.2)
+    runs = []
+    for _ in range(2):
+        res = api.ams_sort_tensors(d_keys, [npe] * p, prm, SeedSpec(7, "algo/rep0"), vals=d_vals,
+                                   key_kind="u64", sample_mode="device")
+        torch.cuda.synchronize()
+        runs.append(res)
+    res = runs[0]
+    out = res.keys.cpu().numpy().view(np.uint64)
+    assert np.array_equal(out, np.sort(keys))
+    if with_vals:
+        assert np.array_equal(res.vals.cpu().numpy(), np.argsort(keys, kind="stable"))
+    assert int(np.sum(res.pe_sizes)) == n
+    ref = O.ams_sort(keys, [npe] * p, groups, None, 16, 0.2, 7, "algo/rep0")
+    for rec, infos in zip(res.levels, ref.levels):
+        assert [int(x) for x in rec.sample_size] == [i.sample_size for i in infos]   # same quota split
+    if dist == "uniform" and npe >= 64:
+        assert max(int(x) for x in res.pe_sizes) <= 1.2 * n / p + 1
+    assert [int(x) for x in runs[1].pe_sizes] == [int(x) for x in res.pe_sizes]      # deterministic per seed
+    with pytest.raises(ValueError):
+        api.ams_sort_tensors(d_keys, [npe] * p, prm, SeedSpec(7, "x"), key_kind="u64", sample_mode="device",
+                             record_holders=True)
