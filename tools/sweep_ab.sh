@@ -8,5 +8,5 @@ for v in "$@" "$@"; do
 import json,sys
 d=json.loads(sys.stdin.read())
 s=d['sweeps']
-print('$v', round(d['ms_per_step'],3), 'cfg1', round(s['cfg1']['ms_per_step'],3), 'k1', [round(r['ms_per_step'],2) for r in s['cfg5']['k1']], 'k2', [round(r['ms_per_step'],2) for r in s['cfg5']['k2']])"
+print('$v', round(d['ms_per_step'],3), 'rank', round(d['kernels']['sample_rank']['ms_per_step'],3), 'cfg1', round(s['cfg1']['ms_per_step'],3), round(s['cfg1_device_sampling']['ms_per_step'],3), 'k1', [round(r['ms_per_step'],2) for r in s['cfg5']['k1']], 'k2', [round(r['ms_per_step'],2) for r in s['cfg5']['k2']], 'k2dev', [round(r['ms_per_step'],2) for r in s['cfg5_device_sampling']['k2']])"
 done
