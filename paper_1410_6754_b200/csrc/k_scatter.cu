@@ -279,26 +279,37 @@ __global__ void __launch_bounds__(kSThreads, VALS ? kSCtas / 2 : kSCtas)
 // scan turns the counts into tile starts and per-bucket output bases; the
 // tile is permuted bucket-major in place and written as coalesced runs.
 
+// 2048-key tiles on 256 threads, 4 CTAs per SM (with stored bucket ids:
+// 1.104 -> 1.070 ms for config 2's last level against the cp.async kernel
+// above; on 4096-key tiles / 512 threads it loses, 1.21 ms).
+constexpr int kUTile = 2048;          // tile of the lean unstable scatter
+constexpr int kLeanMaxBuckets = 1024;  // more buckets: the cp.async kernel's atomic mode
+constexpr int kUItems = 8;
+constexpr int kUThreads = kUTile / kUItems;
+constexpr int kUWarps = kUThreads / 32;
+constexpr int kUCtas = 2 * 4096 / kUTile;
+static_assert(kTile % kUTile == 0, "chunks are whole tiles of both kinds");
+
 template <int KIND, int CLS>
-__global__ void __launch_bounds__(kThreadsU, 2)
+__global__ void __launch_bounds__(kUThreads, kUCtas)
     k_scatter_u(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst, SegMeta m,
                 const uint8_t* __restrict__ blobs, const DigitCls* __restrict__ dcls, int nspl_cap,
                 int nb, const uint32_t* __restrict__ chunk_tot,
                 const uint64_t* __restrict__ cell_base, const uint8_t* __restrict__ ids) {
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ int s_seg;
-  __shared__ uint32_t s_scan[kWarpsU + 1];
+  __shared__ uint32_t s_scan[kUWarps + 1];
   __shared__ __align__(8) uint64_t s_bar[2];
-  constexpr int kBuf = kTile + 2;  // room for the odd head key
+  constexpr int kBuf = kUTile + 2;  // room for the odd head key
   uint64_t* buf0 = reinterpret_cast<uint64_t*>(smem);
-  const int per = (nb + kThreadsU - 1) / kThreadsU | 1;  // buckets per scan thread (odd: no conflicts)
-  const int nbp = per * kThreadsU;
+  const int per = (nb + kUThreads - 1) / kUThreads | 1;  // buckets per scan thread (odd: no conflicts)
+  const int nbp = per * kUThreads;
   int64_t* run = reinterpret_cast<int64_t*>(buf0 + 2 * kBuf);  // running output offset
   int64_t* adj = run + nbp;                                     // this tile: dst index - slot
   uint32_t* cnt = reinterpret_cast<uint32_t*>(adj + nbp);       // counts, then tile starts
   uint16_t* bkt = reinterpret_cast<uint16_t*>(cnt + nbp);
   uint8_t* clsmem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(bkt + kTile) + 15) & ~static_cast<uintptr_t>(15));
+      (reinterpret_cast<uintptr_t>(bkt + kUTile) + 15) & ~static_cast<uintptr_t>(15));
 
   const uint64_t c = blockIdx.x;
   const int tid = threadIdx.x;
@@ -313,13 +324,13 @@ __global__ void __launch_bounds__(kThreadsU, 2)
   const uint64_t seg_off = m.off[s];
   const uint64_t first = (c - m.chunk_prefix[s]) * (uint64_t)m.chunk;
   const uint64_t last = min(first + (uint64_t)m.chunk, m.len[s]);
-  const int ntiles = (int)((last - first + kTile - 1) / kTile);
+  const int ntiles = (int)((last - first + kUTile - 1) / kUTile);
   // Tile t = keys [base, base + tc); the copy covers whole 16-byte units
   // from the boundary base - h, so key e of the tile sits at buf[e + h]; when
   // tc + h is odd the last key is outside the copy and thread 0 adds it.
   auto issue = [&](int t) {
-    const uint64_t base = seg_off + first + (uint64_t)t * kTile;
-    const uint32_t tc = (uint32_t)min((uint64_t)kTile, last - first - (uint64_t)t * kTile);
+    const uint64_t base = seg_off + first + (uint64_t)t * kUTile;
+    const uint32_t tc = (uint32_t)min((uint64_t)kUTile, last - first - (uint64_t)t * kUTile);
     const uint32_t h = (uint32_t)(base & 1);
     bulk_load(buf0 + (t & 1) * kBuf, src + (base - h), ((tc + h) & ~1u) * 8, &s_bar[t & 1]);
   };
@@ -327,8 +338,8 @@ __global__ void __launch_bounds__(kThreadsU, 2)
   {
     const uint32_t* ct = chunk_tot + c * nb;
     const uint64_t* cb = cell_base + (uint64_t)s * nb;
-    for (int b = tid; b < nb; b += kThreadsU) run[b] = (int64_t)(cb[b] + ct[b]);
-    for (int b = tid; b < nbp; b += kThreadsU) cnt[b] = 0;
+    for (int b = tid; b < nb; b += kUThreads) run[b] = (int64_t)(cb[b] + ct[b]);
+    for (int b = tid; b < nbp; b += kUThreads) cnt[b] = 0;
   }
   TreeView tv;
   DigitView dv;
@@ -343,8 +354,8 @@ __global__ void __launch_bounds__(kThreadsU, 2)
   __syncthreads();
   for (int t = 0; t < ntiles; ++t) {
     uint64_t* buf = buf0 + (t & 1) * kBuf;
-    const uint64_t base = seg_off + first + (uint64_t)t * kTile;
-    const uint32_t tc = (uint32_t)min((uint64_t)kTile, last - first - (uint64_t)t * kTile);
+    const uint64_t base = seg_off + first + (uint64_t)t * kUTile;
+    const uint32_t tc = (uint32_t)min((uint64_t)kUTile, last - first - (uint64_t)t * kUTile);
     const uint32_t h = (uint32_t)(base & 1);
     if (tid == 0 && t + 1 < ntiles) {
       fence_proxy_async();
@@ -356,19 +367,20 @@ __global__ void __launch_bounds__(kThreadsU, 2)
       __syncthreads();
     }
     const uint64_t* tb = buf + h;
-    uint64_t kr[kItemsU];
-    uint32_t pk[kItemsU];
+    uint64_t kr[kUItems];
+    uint32_t pk[kUItems];
     const uint32_t pos0 = (uint32_t)((int64_t)base + posbase);
     auto classify_all = [&](auto full_tag) {
       constexpr bool FULL = decltype(full_tag)::value;
 #pragma unroll
-      for (int i = 0; i < kItemsU; ++i) {
-        const uint32_t e = w * (kItemsU * 32) + i * 32 + lane;
+      for (int i = 0; i < kUItems; ++i) {
+        const uint32_t e = w * (kUItems * 32) + i * 32 + lane;
         pk[i] = kInvalid;
         if (FULL || e < tc) {
           const uint64_t key = to_ordered<KIND>(tb[e]);
           uint32_t b;
           if constexpr (CLS == kClsIds) b = ids[base + e];
+          else if constexpr (CLS == kClsIds16) b = reinterpret_cast<const uint16_t*>(ids)[base + e];
           else if constexpr (CLS == kClsDigit) b = dv.classify(key, 0);
           else b = tv.classify(key, pos0 + e);
           kr[i] = key;
@@ -376,7 +388,7 @@ __global__ void __launch_bounds__(kThreadsU, 2)
         }
       }
     };
-    if (tc == (uint32_t)kTile) classify_all(std::true_type{});
+    if (tc == (uint32_t)kUTile) classify_all(std::true_type{});
     else classify_all(std::false_type{});
     __syncthreads();
     // Scan: thread t owns buckets [t*per, t*per + per).
@@ -386,7 +398,7 @@ __global__ void __launch_bounds__(kThreadsU, 2)
       for (int j = 0; j < per; ++j) sum += cnt[b0 + j];
       const uint32_t inc = warp_incl_scan(sum);
       if (lane == 31) s_scan[w] = inc;
-      uint32_t start = warp_base_direct<kThreadsU>(s_scan) + inc - sum;
+      uint32_t start = warp_base_direct<kUThreads>(s_scan) + inc - sum;
       for (int j = 0; j < per; ++j) {
         const int b = b0 + j;
         const uint32_t v = cnt[b];
@@ -401,7 +413,7 @@ __global__ void __launch_bounds__(kThreadsU, 2)
     }
     __syncthreads();
 #pragma unroll
-    for (int i = 0; i < kItemsU; ++i) {
+    for (int i = 0; i < kUItems; ++i) {
       if (pk[i] != kInvalid) {
         const uint32_t b = pk[i] >> 16;
         const uint32_t slot = cnt[b] + (pk[i] & 0xFFFFu);
@@ -410,7 +422,7 @@ __global__ void __launch_bounds__(kThreadsU, 2)
       }
     }
     __syncthreads();
-    for (uint32_t j = tid; j < tc; j += kThreadsU) dst[adj[bkt[j]] + j] = buf[j];
+    for (uint32_t j = tid; j < tc; j += kUThreads) dst[adj[bkt[j]] + j] = buf[j];
     for (int j = 0; j < per; ++j) cnt[tid * per + j] = 0;
     // This thread's generic-proxy writes into the tile buffer (the in-place
     // permutation) must be ordered before the bulk copy (async proxy) that
@@ -444,26 +456,44 @@ size_t scatter_smem_bytes(int nb_stride, int nspl_cap, int cells_cap, bool digit
 }
 
 size_t scatter_u_smem_bytes(int nb, int nspl_cap, int cells_cap, bool digit) {
-  const int per = (nb + kThreadsU - 1) / kThreadsU | 1;
-  const size_t nbp = (size_t)per * kThreadsU;
-  size_t b = 2 * 8 * (size_t)(kTile + 2) + 16 * nbp + 4 * nbp + 2 * (size_t)kTile;
+  const int per = (nb + kUThreads - 1) / kUThreads | 1;
+  const size_t nbp = (size_t)per * kUThreads;
+  size_t b = 2 * 8 * (size_t)(kUTile + 2) + 16 * nbp + 4 * nbp + 2 * (size_t)kUTile;
   b = (b + 15) & ~(size_t)15;
   if (!digit) b += tree_smem_bytes(nspl_cap, cells_cap) + 16;
   return b;
 }
 
 // The lean unstable kernel serves the exact digit rounds of the final sort
-// (keys only); the tree / stored-id classifiers keep the 4-CTA k_scatter.
-cudaError_t launch_scatter_u(cudaStream_t st, const void* src, void* dst, const SegMeta& m,
+// (keys only) and, with stored bucket bytes, the keys-only last level.
+cudaError_t launch_scatter_u(cudaStream_t st, const void* src, int kind, void* dst, const SegMeta& m,
                              uint64_t nchunks, const DigitCls* dcls, int nb_stride,
-                             const uint32_t* chunk_tot, const uint64_t* cell_base) {
+                             const uint32_t* chunk_tot, const uint64_t* cell_base, const uint8_t* ids,
+                             int id_bytes) {
   if (nchunks == 0) return cudaSuccess;
   const size_t smem = scatter_u_smem_bytes(nb_stride, 0, 0, true);
-  auto fn = k_scatter_u<AMS_KEY_U64, kClsDigit>;
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  fn<<<(unsigned)nchunks, kThreadsU, smem, st>>>(static_cast<const uint64_t*>(src), static_cast<uint64_t*>(dst),
-                                                  m, nullptr, dcls, 0, nb_stride, chunk_tot, cell_base, nullptr);
+  const uint64_t* s = static_cast<const uint64_t*>(src);
+  uint64_t* d = static_cast<uint64_t*>(dst);
+  cudaError_t e = cudaSuccess;
+  if (!ids) {
+    auto fn = k_scatter_u<AMS_KEY_U64, kClsDigit>;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    fn<<<(unsigned)nchunks, kUThreads, smem, st>>>(s, d, m, nullptr, dcls, 0, nb_stride, chunk_tot, cell_base,
+                                                    nullptr);
+  } else {
+#define AMS_U_GO(K, CL)                                                                          \
+  {                                                                                              \
+    auto fn = k_scatter_u<K, CL>;                                                                \
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);        \
+    if (e != cudaSuccess) return e;                                                              \
+    fn<<<(unsigned)nchunks, kUThreads, smem, st>>>(s, d, m, nullptr, nullptr, 0, nb_stride, chunk_tot, \
+                                                    cell_base, ids);                             \
+  }
+    if (id_bytes == 2) AMS_KIND_DISPATCH(kind, K, AMS_U_GO(K, kClsIds16))
+    else AMS_KIND_DISPATCH(kind, K, AMS_U_GO(K, kClsIds))
+#undef AMS_U_GO
+  }
   return cudaGetLastError();
 }
 
@@ -474,8 +504,9 @@ cudaError_t launch_scatter(cudaStream_t st, const void* src, const void* src_val
                            const uint64_t* cell_base, const uint8_t* ids, int id_bytes) {
   if (nchunks == 0) return cudaSuccess;
   const bool vals = src_vals != nullptr;
-  if (!stable && !vals && digit)
-    return launch_scatter_u(st, src, dst, m, nchunks, dcls, nb_stride, chunk_tot, cell_base);
+  if (!stable && !vals && (digit || (ids && nb_stride <= kLeanMaxBuckets)))
+    return launch_scatter_u(st, src, kind, dst, m, nchunks, dcls, nb_stride, chunk_tot, cell_base,
+                            digit ? nullptr : ids, id_bytes);
   const int mode = scatter_mode(nb_stride, stable);
   // Bucket bytes from the histogram pass replace the tree (and its shared memory).
   const size_t smem = scatter_smem_bytes(nb_stride, nspl_cap, cells_cap, digit || ids, vals, stable);
