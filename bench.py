@@ -113,12 +113,48 @@ _REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_
 
 
 class ClockSampler:
+    """SM clock and clock-event reasons sampled DURING the timed region: NVML
+    polled every 5 ms on a thread (nvidia_ml_py), else `nvidia-smi -lms 100`."""
+
     def __init__(self, index: int):
         self.index = index
         self.proc = None
         self.lines = []
+        self.samples = []     # (sm_mhz, reasons mask) from NVML
+        self.mx = None
+        self._stop = threading.Event()
+        self.t = None
+        self.nvml = None
+
+    def _poll(self):
+        n, h = self.nvml, self.handle
+        while not self._stop.is_set():
+            try:
+                sm = n.nvmlDeviceGetClockInfo(h, n.NVML_CLOCK_SM)
+                try:
+                    mask = n.nvmlDeviceGetCurrentClocksEventReasons(h)
+                except Exception:
+                    mask = n.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                self.samples.append((float(sm), int(mask)))
+            except Exception:
+                pass
+            self._stop.wait(0.005)
 
     def start(self):
+        try:
+            import pynvml as n
+            n.nvmlInit()
+            # torch's device index follows CUDA_VISIBLE_DEVICES; NVML's does not
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            phys = int(vis.split(",")[self.index]) if vis and vis.split(",")[self.index].isdigit() else self.index
+            self.handle = n.nvmlDeviceGetHandleByIndex(phys)
+            self.mx = float(n.nvmlDeviceGetMaxClockInfo(self.handle, n.NVML_CLOCK_SM))
+            self.nvml = n
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index),
@@ -135,6 +171,17 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def stop(self):
+        sm, mx, reasons = [], self.mx, set()
+        if self.nvml is not None:
+            self._stop.set()
+            self.t.join(timeout=2)
+            for clk, mask in self.samples:
+                sm.append(clk)
+                for bit, name in _REASONS.items():
+                    if mask & bit and name != "gpu_idle":
+                        reasons.add(name)
+            return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                    "reasons": sorted(reasons), "samples": len(sm), "source": "nvml, 5 ms period"}
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
@@ -143,7 +190,6 @@ class ClockSampler:
         except Exception:
             self.proc.kill()
         self.t.join(timeout=2)
-        sm, mx, reasons = [], None, set()
         for ln in self.lines:
             parts = [x.strip() for x in ln.split(",")]
             if len(parts) < 3:
@@ -158,7 +204,7 @@ class ClockSampler:
                 if mask & bit and name != "gpu_idle":
                     reasons.add(name)
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "source": "nvidia-smi -lms 100"}
 
 
 # ------------------------------------------------------------------ CPU arms
