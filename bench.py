@@ -735,30 +735,61 @@ def ours_arm_multi(args, w, world, rank, local):
                "host_cpus": os.cpu_count()}
     e2e = None
     if not args.no_e2e:
+        # Every rank streams its own share: pinned host -> device, the
+        # distributed sort, device -> pinned host, with the copies of
+        # consecutive steps overlapped on their own streams (as
+        # api.HostSortPipeline does on one GPU).  Every step's bytes make the
+        # whole trip inside the timed region.
+        import math
+        r1 = w["groups"][0]
+        eps_l = params.per_level_imbalance()
+        cap = int(math.ceil((1.0 + eps_l) * n / r1)) * max(r1 // world, 1) + 16   # ams.py:258
         h_in = kt_host.pin_memory()
-        d_in = torch.empty_like(keys_dev)
-        h_out = torch.empty_like(h_in).pin_memory()
+        d_ins = [torch.empty_like(keys_dev) for _ in range(2)]
+        d_outs = [torch.empty(cap, dtype=keys_dev.dtype, device="cuda") for _ in range(2)]
+        h_outs = [torch.empty(cap, dtype=keys_dev.dtype).pin_memory() for _ in range(2)]
+        s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+        ev_in = [torch.cuda.Event() for _ in range(2)]
+        ev_sorted = [torch.cuda.Event() for _ in range(2)]
+        ev_out = [torch.cuda.Event() for _ in range(2)]
+        comp = torch.cuda.current_stream()
 
-        def e2e_step():
-            d_in.view(torch.int64).copy_(h_in.view(torch.int64), non_blocking=True)
-            r_ = sort_distributed(d_in, sizes, params, seed, ops, key_kind=kind)
-            m = min(r_[0].numel(), h_out.numel())
-            h_out.view(torch.int64)[:m].copy_(r_[0].view(torch.int64)[:m], non_blocking=True)
-            return r_
+        def h2d(j):
+            with torch.cuda.stream(s_in):
+                d_ins[j].view(torch.int64).copy_(h_in.view(torch.int64), non_blocking=True)
+                ev_in[j].record(s_in)
 
-        e2e_step()
-        torch.cuda.synchronize()
-        ke = max(1, min(args.steps, 3))
+        def e2e_run(k):
+            h2d(0)
+            for i in range(k):
+                j = i % 2
+                if i + 1 < k:
+                    s_in.wait_event(ev_sorted[1 - j])      # d_ins[1 - j] was read by sort i - 1
+                    h2d(1 - j)
+                comp.wait_event(ev_in[j])
+                comp.wait_event(ev_out[j])                  # d_outs[j] was read by the D2H of step i - 2
+                r_ = sort_distributed(d_ins[j], sizes, params, seed, ops, key_kind=kind, out=d_outs[j])
+                ev_sorted[j].record(comp)
+                m = r_[0].numel()
+                with torch.cuda.stream(s_out):
+                    s_out.wait_event(ev_sorted[j])
+                    h_outs[j].view(torch.int64)[:m].copy_(r_[0].view(torch.int64), non_blocking=True)
+                    ev_out[j].record(s_out)
+            s_out.synchronize()
+            torch.cuda.synchronize()
+
+        e2e_run(2)
+        ke = max(2, min(args.steps, 6))
         dist.barrier()
         t0 = time.perf_counter()
-        for _ in range(ke):
-            e2e_step()
-        torch.cuda.synchronize()
+        e2e_run(ke)
         wall = torch.tensor([time.perf_counter() - t0], device="cuda", dtype=torch.float64)
         dist.all_reduce(wall, op=dist.ReduceOp.MAX)
         e2e = {"value": n * ke / float(wall.item()), "unit": UNIT,
                "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
-               "ms_per_step": float(wall.item()) * 1e3 / ke}
+               "ms_per_step": float(wall.item()) * 1e3 / ke, "steps": ke,
+               "api": "dist.sort_distributed per rank (pinned host buffers; H2D / sort / D2H of "
+                      "consecutive steps overlapped on separate streams)"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
